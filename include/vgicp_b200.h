@@ -1,0 +1,159 @@
+/*
+ * vgicp_b200 — C ABI of the B200-native (sm_100a) VGICP matching-cost path.
+ *
+ * This is the drop-in boundary for the reference's hot path (/root/reference/proj):
+ *   GaussianVoxelMap            include/vgicp/voxelmap.hpp:28-56, src/voxelmap.cpp:65-117
+ *   overlap_rate                include/vgicp/voxelmap.hpp:60-61, src/voxelmap.cpp:119-135
+ *   MatchingCostFactor          include/vgicp/factors.hpp:36-45, src/factors.cpp:50-67
+ *   linearize_matching_cost     include/vgicp/factors.hpp:76-77, src/factors.cpp:90-148
+ *   evaluate_matching_cost      include/vgicp/factors.hpp:80-81, src/factors.cpp:150-181
+ *   gicp_error                  include/vgicp/factors.hpp:70,    src/factors.cpp:75-88
+ * plus the batch entry points the paper's "issue all cost evaluations, sync, collect" needs
+ * (SURVEY.md §8b): one launch linearizes / evaluates every matching-cost factor of a graph, the
+ * integration point of linearize_all / total_error (src/optimizer.cpp:45-75).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no C++ or torch types cross this boundary, and no
+ *    exception either: every call returns a vgicp_status and vgicp_last_error() (thread-local)
+ *    holds the message. The reference's std::invalid_argument maps to
+ *    VGICP_E_INVALID_ARGUMENT and std::out_of_range to VGICP_E_OUT_OF_RANGE.
+ *  - A pose is 12 doubles: row-major rotation R (9) followed by the translation t (3), i.e.
+ *    Pose{rotation, translation} of include/vgicp/se3.hpp:33-56.
+ *  - Point means are float32 (KITTI .bin precision, src/io.cpp:50); covariances are the six
+ *    unique float32 entries (xx, xy, xz, yy, yz, zz) of a symmetric 3×3. The _f64 upload
+ *    variant accepts the reference's double layout and rounds to that contract.
+ *  - A linearized factor is VGICP_LINEARIZED_DOUBLES doubles, the fields of LinearizedFactor
+ *    (include/vgicp/factors.hpp:19-29) in order: H_ii(6×6) H_ij(6×6) H_jj(6×6) b_i(6) b_j(6)
+ *    error(1), matrices row-major; inlier counts are returned separately as int32.
+ *    Block i is the factor's target variable, j its source variable (src/factors.cpp:137-138).
+ *  - Every device-side result is deterministic: reductions run in a fixed order, so repeated
+ *    calls on identical inputs return bit-identical outputs.
+ *  - One host thread drives a context (the optimizer is not reentrant either).
+ *    Handles keep what they reference alive (reference counts), like the reference's
+ *    shared_ptr<const ...> members.
+ */
+#ifndef VGICP_B200_H
+#define VGICP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VGICP_LINEARIZED_DOUBLES 121
+#define VGICP_KEY_MISS UINT64_MAX
+
+typedef enum vgicp_status {
+  VGICP_OK = 0,
+  VGICP_E_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  VGICP_E_OUT_OF_RANGE = 2,     /* std::out_of_range (voxelmap.cpp:49-51) */
+  VGICP_E_CUDA = 3,             /* CUDA runtime / launch failure */
+  VGICP_E_NO_DEVICE = 4,        /* no usable sm_100 device */
+  VGICP_E_OUT_OF_MEMORY = 5
+} vgicp_status;
+
+typedef struct vgicp_ctx_s* vgicp_ctx;
+typedef struct vgicp_cloud_s* vgicp_cloud;
+typedef struct vgicp_map_s* vgicp_map;
+typedef struct vgicp_graph_s* vgicp_graph;
+
+/* MatchingCostFactor (include/vgicp/factors.hpp:36-45): the older frame owns the map
+ * (target), the newer frame supplies the points (source). */
+typedef struct vgicp_factor_desc {
+  int32_t target_index;
+  int32_t source_index;
+  vgicp_cloud source;
+  vgicp_map target;
+} vgicp_factor_desc;
+
+/* ---------------------------------------------------------------- library / context */
+const char* vgicp_last_error(void);
+const char* vgicp_version(void);
+int vgicp_device_count(int* count);
+
+/* One context per device; it owns a CUDA stream (or adopts `stream` when non-NULL). */
+int vgicp_ctx_create(int device, void* stream, vgicp_ctx* out);
+int vgicp_ctx_destroy(vgicp_ctx ctx);
+int vgicp_ctx_stream(vgicp_ctx ctx, void** stream);
+int vgicp_ctx_synchronize(vgicp_ctx ctx);
+/* Kernels this context has launched so far (bench evidence for gpu_launches). */
+int vgicp_ctx_launch_count(vgicp_ctx ctx, uint64_t* launches);
+
+/* ---------------------------------------------------------------- point clouds (PointCloud,
+ * include/vgicp/point_cloud.hpp:21-37). cov6 may be NULL for a raw cloud (overlap only). */
+int vgicp_cloud_upload(vgicp_ctx ctx, const float* xyz, const float* cov6, size_t n, vgicp_cloud* out);
+/* Reference layout: n×3 double means, n×9 double covariances (may be NULL); rounded to float32. */
+int vgicp_cloud_upload_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, vgicp_cloud* out);
+int vgicp_cloud_size(vgicp_cloud cloud, size_t* n);
+int vgicp_cloud_has_covariances(vgicp_cloud cloud, int* has);
+int vgicp_cloud_destroy(vgicp_cloud cloud);
+
+/* ---------------------------------------------------------------- Gaussian voxel maps */
+/* GaussianVoxelMap(cloud, resolution) — voxelmap.cpp:65-104. Errors: resolution <= 0 or a
+ * cloud without covariances -> INVALID_ARGUMENT; a coordinate beyond ±2^20 voxels ->
+ * OUT_OF_RANGE (and no map). */
+int vgicp_voxelmap_build(vgicp_ctx ctx, vgicp_cloud cloud, double resolution, vgicp_map* out);
+/* m maps in one batched build (all-or-nothing: on error no map is returned). */
+int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* resolutions, int m,
+                               vgicp_map* out);
+int vgicp_voxelmap_destroy(vgicp_map map);
+int vgicp_voxelmap_size(vgicp_map map, size_t* voxels);                 /* voxelmap.hpp:36 */
+int vgicp_voxelmap_resolution(vgicp_map map, double* resolution);       /* voxelmap.hpp:35 */
+int vgicp_voxelmap_total_points(vgicp_map map, size_t* total_points);   /* voxelmap.hpp:49 */
+/* voxels() (voxelmap.hpp:47) in ascending key order: keys[V], counts[V], means[V×3],
+ * covs[V×9] (row-major, float64 statistics). Any pointer may be NULL. */
+int vgicp_voxelmap_export(vgicp_map map, uint64_t* keys, int32_t* counts, double* means, double* covs);
+/* lookup() (voxelmap.cpp:106-117) for n points (n×3 double): the packed key of the
+ * populated voxel containing each point, VGICP_KEY_MISS when absent or out of range. */
+int vgicp_voxelmap_lookup(vgicp_map map, const double* points, size_t n, uint64_t* keys_out);
+/* voxel_coord + pack_key (voxelmap.cpp:45-63) on the host; OUT_OF_RANGE beyond ±2^20. */
+int vgicp_voxel_key(double resolution, const double point[3], uint64_t* key);
+
+/* ---------------------------------------------------------------- overlap (Eq. 7/8) */
+/* overlap_rate(cloud, pose_rel, map) — voxelmap.cpp:119-135. Exact hits / N. */
+int vgicp_overlap_rate(vgicp_ctx ctx, vgicp_cloud cloud, const double pose_rel[12], vgicp_map map, double* rate);
+/* m independent (cloud, pose, map) probes in one launch; hits[k] is the exact hit count. */
+int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* poses12, const vgicp_map* maps,
+                        int m, uint64_t* hits);
+
+/* ---------------------------------------------------------------- matching cost factors */
+/* linearize_matching_cost (factors.cpp:90-148) for one factor. */
+int vgicp_linearize_matching_cost(vgicp_ctx ctx, const vgicp_factor_desc* factor, const double T_target[12],
+                                  const double T_source[12], double out[VGICP_LINEARIZED_DOUBLES],
+                                  int32_t* inliers);
+/* evaluate_matching_cost (factors.cpp:150-181) for one factor. */
+int vgicp_evaluate_matching_cost(vgicp_ctx ctx, const vgicp_factor_desc* factor, const double T_target[12],
+                                 const double T_source[12], double* error, int32_t* inliers);
+/* gicp_error (factors.cpp:75-88): covariances as full row-major 3×3. */
+int vgicp_gicp_error(vgicp_ctx ctx, const double source_mean[3], const double source_cov[9],
+                     const double target_mean[3], const double target_cov[9], const double T[12], double* error,
+                     double residual[3], double information[9], int* valid);
+
+/* ---------------------------------------------------------------- batched factor graphs */
+/* A fixed set of matching-cost factors over num_poses pose variables. Validation mirrors the
+ * MatchingCostFactor constructor (factors.cpp:57-66): distinct variables, non-empty source with
+ * covariances, non-empty target map; indices must lie in [0, num_poses). `chunk` is the number
+ * of source points per CTA work item (0 = default 2048). */
+int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses, int chunk,
+                       vgicp_graph* out);
+int vgicp_graph_destroy(vgicp_graph graph);
+int vgicp_graph_num_factors(vgicp_graph graph, int* num_factors);
+/* Σ source points over the graph's factors (the per-pass point-evaluation count). */
+int vgicp_graph_num_points(vgicp_graph graph, uint64_t* points);
+/* linearize_all for matching factors (optimizer.cpp:45-62): host poses in, host blocks out
+ * (num_factors × VGICP_LINEARIZED_DOUBLES, factor order), synchronous. */
+int vgicp_graph_linearize(vgicp_graph graph, const double* poses12, double* out, int32_t* inliers);
+/* Per-factor errors / inliers for total_error (optimizer.cpp:66-75), synchronous. */
+int vgicp_graph_evaluate(vgicp_graph graph, const double* poses12, double* errors, int32_t* inliers);
+/* Device-resident variants: every pointer is device memory of the context's device; the work
+ * is enqueued on the context stream and the call returns without synchronising. */
+int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, double* d_out, int32_t* d_inliers);
+int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, double* d_errors, int32_t* d_inliers);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VGICP_B200_H */

@@ -1,0 +1,126 @@
+"""ctypes loader for the product library lib/libvgicp_b200.so (C ABI: include/vgicp_b200.h).
+
+There is no CPU fallback: if the CUDA library is missing, or no sm_100 device is visible when a
+context is created, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "lib" / "libvgicp_b200.so"
+HEADER = PKG.parent / "include" / "vgicp_b200.h"
+
+LINEARIZED_DOUBLES = 121
+KEY_MISS = (1 << 64) - 1
+
+OK = 0
+E_INVALID_ARGUMENT = 1
+E_OUT_OF_RANGE = 2
+E_CUDA = 3
+E_NO_DEVICE = 4
+E_OUT_OF_MEMORY = 5
+
+
+class VgicpError(RuntimeError):
+    """A CUDA / device failure inside the library."""
+
+
+class NoDeviceError(VgicpError):
+    pass
+
+
+class FactorDesc(C.Structure):
+    _fields_ = [
+        ("target_index", C.c_int32),
+        ("source_index", C.c_int32),
+        ("source", C.c_void_p),
+        ("target", C.c_void_p),
+    ]
+
+
+_vp = C.c_void_p
+_sz = C.c_size_t
+_d = C.c_double
+_i = C.c_int
+_PD = C.POINTER(C.c_double)
+
+# name -> (restype, argtypes); every entry point declared in include/vgicp_b200.h
+SIGNATURES = {
+    "vgicp_last_error": (C.c_char_p, []),
+    "vgicp_version": (C.c_char_p, []),
+    "vgicp_device_count": (_i, [C.POINTER(_i)]),
+    "vgicp_ctx_create": (_i, [_i, _vp, C.POINTER(_vp)]),
+    "vgicp_ctx_destroy": (_i, [_vp]),
+    "vgicp_ctx_stream": (_i, [_vp, C.POINTER(_vp)]),
+    "vgicp_ctx_synchronize": (_i, [_vp]),
+    "vgicp_ctx_launch_count": (_i, [_vp, C.POINTER(C.c_uint64)]),
+    "vgicp_cloud_upload": (_i, [_vp, _vp, _vp, _sz, C.POINTER(_vp)]),
+    "vgicp_cloud_upload_f64": (_i, [_vp, _vp, _vp, _sz, C.POINTER(_vp)]),
+    "vgicp_cloud_size": (_i, [_vp, C.POINTER(_sz)]),
+    "vgicp_cloud_has_covariances": (_i, [_vp, C.POINTER(_i)]),
+    "vgicp_cloud_destroy": (_i, [_vp]),
+    "vgicp_voxelmap_build": (_i, [_vp, _vp, _d, C.POINTER(_vp)]),
+    "vgicp_voxelmap_build_batch": (_i, [_vp, _vp, _vp, _i, _vp]),
+    "vgicp_voxelmap_destroy": (_i, [_vp]),
+    "vgicp_voxelmap_size": (_i, [_vp, C.POINTER(_sz)]),
+    "vgicp_voxelmap_resolution": (_i, [_vp, _PD]),
+    "vgicp_voxelmap_total_points": (_i, [_vp, C.POINTER(_sz)]),
+    "vgicp_voxelmap_export": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "vgicp_voxelmap_lookup": (_i, [_vp, _vp, _sz, _vp]),
+    "vgicp_voxel_key": (_i, [_d, _vp, C.POINTER(C.c_uint64)]),
+    "vgicp_overlap_rate": (_i, [_vp, _vp, _vp, _vp, _PD]),
+    "vgicp_overlap_batch": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
+    "vgicp_linearize_matching_cost": (_i, [_vp, C.POINTER(FactorDesc), _vp, _vp, _vp, C.POINTER(C.c_int32)]),
+    "vgicp_evaluate_matching_cost": (_i, [_vp, C.POINTER(FactorDesc), _vp, _vp, _PD, C.POINTER(C.c_int32)]),
+    "vgicp_gicp_error": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _PD, _vp, _vp, C.POINTER(_i)]),
+    "vgicp_graph_create": (_i, [_vp, _vp, _i, _i, _i, C.POINTER(_vp)]),
+    "vgicp_graph_destroy": (_i, [_vp]),
+    "vgicp_graph_num_factors": (_i, [_vp, C.POINTER(_i)]),
+    "vgicp_graph_num_points": (_i, [_vp, C.POINTER(C.c_uint64)]),
+    "vgicp_graph_linearize": (_i, [_vp, _vp, _vp, _vp]),
+    "vgicp_graph_evaluate": (_i, [_vp, _vp, _vp, _vp]),
+    "vgicp_graph_linearize_device": (_i, [_vp, _vp, _vp, _vp]),
+    "vgicp_graph_evaluate_device": (_i, [_vp, _vp, _vp, _vp]),
+}
+
+_LIB = None
+
+
+def load() -> C.CDLL:
+    """Load the in-tree CUDA library (built by __graft_entry__.build()); raise if absent."""
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(vgicp_b200 has no CPU fallback)"
+            )
+        lib = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def last_error() -> str:
+    return load().vgicp_last_error().decode()
+
+
+def check(rc: int) -> None:
+    """Map a vgicp_status onto the exception the reference would raise."""
+    if rc == OK:
+        return
+    msg = last_error()
+    if rc == E_INVALID_ARGUMENT:
+        raise ValueError(msg)  # std::invalid_argument
+    if rc == E_OUT_OF_RANGE:
+        raise IndexError(msg)  # std::out_of_range
+    if rc == E_NO_DEVICE:
+        raise NoDeviceError(msg)
+    if rc == E_OUT_OF_MEMORY:
+        raise MemoryError(msg)
+    raise VgicpError(msg)

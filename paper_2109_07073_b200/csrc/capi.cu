@@ -1,0 +1,776 @@
+// C ABI (include/vgicp_b200.h): contexts, handles, validation and launch orchestration.
+// Host code only; the kernels live in voxelmap.cu and factor.cu.
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <new>
+
+#include "internal.h"
+
+namespace vgicp {
+
+namespace {
+thread_local std::string g_error;
+}
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t err, const char* what) {
+  g_error = std::string(what) + ": " + cudaGetErrorString(err);
+  return err == cudaErrorMemoryAllocation ? VGICP_E_OUT_OF_MEMORY : VGICP_E_CUDA;
+}
+
+namespace {
+
+constexpr double kKeyBiasD = 1048576.0;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+unsigned next_pow2(unsigned long long x) {
+  unsigned p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int ensure_scratch(vgicp_ctx ctx, size_t bytes) {
+  if (ctx->scratch_bytes >= bytes) return VGICP_OK;
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  const size_t want = std::max(bytes, ctx->scratch_bytes * 2);
+  if (ctx->scratch) VG_CUDA(cudaFree(ctx->scratch));
+  ctx->scratch = nullptr;
+  ctx->scratch_bytes = 0;
+  VG_CUDA(cudaMalloc(&ctx->scratch, want));
+  ctx->scratch_bytes = want;
+  return VGICP_OK;
+}
+
+int ensure_pinned(vgicp_ctx ctx, size_t bytes) {
+  if (ctx->pinned_bytes >= bytes) return VGICP_OK;
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  const size_t want = std::max<size_t>(std::max(bytes, ctx->pinned_bytes * 2), 1 << 20);
+  if (ctx->pinned) VG_CUDA(cudaFreeHost(ctx->pinned));
+  ctx->pinned = nullptr;
+  ctx->pinned_bytes = 0;
+  VG_CUDA(cudaMallocHost(&ctx->pinned, want));
+  ctx->pinned_bytes = want;
+  return VGICP_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void release(vgicp_cloud c) {
+  if (c && c->refs.fetch_sub(1) == 1) {
+    DeviceGuard g(c->ctx->device);
+    cudaFree(c->block);
+    delete c;
+  }
+}
+
+void release(vgicp_map m) {
+  if (m && m->refs.fetch_sub(1) == 1) {
+    DeviceGuard g(m->ctx->device);
+    cudaFree(m->block);
+    delete m;
+  }
+}
+
+// voxel_coord + pack_key on the host (voxelmap.cpp:45-63); same division/floor semantics.
+int host_voxel_key(double resolution, const double p[3], uint64_t* key) {
+  uint64_t k = 0;
+  for (int a = 0; a < 3; ++a) {
+    const double c = std::floor(p[a] / resolution);
+    if (!(c >= -kKeyBiasD && c < kKeyBiasD))
+      return fail(VGICP_E_OUT_OF_RANGE, "point beyond the +-2^20 voxel-per-axis range limit");
+    k = (k << 21) | static_cast<uint64_t>(static_cast<int64_t>(c) + (1 << 20));
+  }
+  *key = k;
+  return VGICP_OK;
+}
+
+}  // namespace
+}  // namespace vgicp
+
+using namespace vgicp;
+
+extern "C" {
+
+const char* vgicp_last_error(void) { return g_error.c_str(); }
+
+const char* vgicp_version(void) { return "vgicp_b200 0.1 (sm_100a)"; }
+
+int vgicp_device_count(int* count) {
+  if (!count) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *count = n;
+  return VGICP_OK;
+}
+
+int vgicp_ctx_create(int device, void* stream, vgicp_ctx* out) {
+  if (!out) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(VGICP_E_NO_DEVICE, "no CUDA device visible (vgicp_b200 has no CPU fallback)");
+  if (device < 0 || device >= n) return fail(VGICP_E_INVALID_ARGUMENT, "device index out of range");
+  cudaDeviceProp prop;
+  VG_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(VGICP_E_NO_DEVICE, std::string("vgicp_b200 is built for sm_100a; device is ") + prop.name);
+  DeviceGuard g(device);
+  auto ctx = std::make_unique<vgicp_ctx_s>();
+  ctx->device = device;
+  if (stream) {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    VG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  *out = ctx.release();
+  return VGICP_OK;
+}
+
+int vgicp_ctx_destroy(vgicp_ctx ctx) {
+  if (!ctx) return VGICP_OK;
+  DeviceGuard g(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->scratch) cudaFree(ctx->scratch);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return VGICP_OK;
+}
+
+int vgicp_ctx_stream(vgicp_ctx ctx, void** stream) {
+  if (!ctx || !stream) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *stream = ctx->stream;
+  return VGICP_OK;
+}
+
+int vgicp_ctx_synchronize(vgicp_ctx ctx) {
+  if (!ctx) return fail(VGICP_E_INVALID_ARGUMENT, "null context");
+  DeviceGuard g(ctx->device);
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return VGICP_OK;
+}
+
+int vgicp_ctx_launch_count(vgicp_ctx ctx, uint64_t* launches) {
+  if (!ctx || !launches) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *launches = ctx->launches;
+  return VGICP_OK;
+}
+
+// ------------------------------------------------------------------------------------ clouds
+static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov6, size_t n, vgicp_cloud* out) {
+  if (!ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (n > 0 && !xyz) return fail(VGICP_E_INVALID_ARGUMENT, "null point array");
+  if (n >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "cloud too large (>= 2^31 points)");
+  DeviceGuard g(ctx->device);
+  auto c = std::make_unique<vgicp_cloud_s>();
+  c->ctx = ctx;
+  c->n = n;
+  c->has_cov = (cov6 != nullptr) && n > 0;
+  const size_t na = align_up(n * sizeof(float4), 256);
+  const size_t nc = align_up(n * sizeof(float), 256);
+  const size_t bytes = std::max<size_t>(na * 2 + nc, 256);
+  VG_CUDA(cudaMalloc(&c->block, bytes));
+  char* base = static_cast<char*>(c->block);
+  c->pa = reinterpret_cast<float4*>(base);
+  c->pb = reinterpret_cast<float4*>(base + na);
+  c->pc = reinterpret_cast<float*>(base + 2 * na);
+  if (n > 0) {
+    if (int rc = ensure_pinned(ctx, bytes)) return rc;
+    VG_CUDA(cudaStreamSynchronize(ctx->stream));
+    char* h = static_cast<char*>(ctx->pinned);
+    float4* ha = reinterpret_cast<float4*>(h);
+    float4* hb = reinterpret_cast<float4*>(h + na);
+    float* hc = reinterpret_cast<float*>(h + 2 * na);
+    for (size_t i = 0; i < n; ++i) {
+      const float* p = xyz + 3 * i;
+      if (cov6) {
+        const float* q = cov6 + 6 * i;
+        ha[i] = make_float4(p[0], p[1], p[2], q[0]);
+        hb[i] = make_float4(q[1], q[2], q[3], q[4]);
+        hc[i] = q[5];
+      } else {
+        ha[i] = make_float4(p[0], p[1], p[2], 0.f);
+        hb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        hc[i] = 0.f;
+      }
+    }
+    VG_CUDA(cudaMemcpyAsync(c->block, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  *out = c.release();
+  return VGICP_OK;
+}
+
+int vgicp_cloud_upload(vgicp_ctx ctx, const float* xyz, const float* cov6, size_t n, vgicp_cloud* out) {
+  return cloud_upload_packed(ctx, xyz, cov6, n, out);
+}
+
+int vgicp_cloud_upload_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, vgicp_cloud* out) {
+  if (n > 0 && !xyz) return fail(VGICP_E_INVALID_ARGUMENT, "null point array");
+  std::vector<float> p(3 * n), c(cov9 ? 6 * n : 0);
+  for (size_t i = 0; i < 3 * n; ++i) p[i] = static_cast<float>(xyz[i]);
+  if (cov9) {
+    for (size_t i = 0; i < n; ++i) {
+      const double* m = cov9 + 9 * i;
+      const int idx[6] = {0, 1, 2, 4, 5, 8};
+      for (int k = 0; k < 6; ++k) c[6 * i + k] = static_cast<float>(m[idx[k]]);
+    }
+  }
+  return cloud_upload_packed(ctx, p.data(), cov9 ? c.data() : nullptr, n, out);
+}
+
+int vgicp_cloud_size(vgicp_cloud cloud, size_t* n) {
+  if (!cloud || !n) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *n = cloud->n;
+  return VGICP_OK;
+}
+
+int vgicp_cloud_has_covariances(vgicp_cloud cloud, int* has) {
+  if (!cloud || !has) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *has = cloud->has_cov ? 1 : 0;
+  return VGICP_OK;
+}
+
+int vgicp_cloud_destroy(vgicp_cloud cloud) {
+  release(cloud);
+  return VGICP_OK;
+}
+
+// ------------------------------------------------------------------------------------ voxel maps
+int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* resolutions, int m,
+                               vgicp_map* out) {
+  if (!ctx || !out || (m > 0 && (!clouds || !resolutions))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (m <= 0) return VGICP_OK;
+  for (int k = 0; k < m; ++k) out[k] = nullptr;
+  // GaussianVoxelMap ctor validation order (voxelmap.cpp:67-72)
+  for (int k = 0; k < m; ++k) {
+    if (!(resolutions[k] > 0.0)) return fail(VGICP_E_INVALID_ARGUMENT, "voxel resolution must be positive");
+    if (!clouds[k] || clouds[k]->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "cloud of another context");
+    if (!clouds[k]->has_cov)
+      return fail(VGICP_E_INVALID_ARGUMENT, "voxel map construction requires per-point covariances");
+  }
+  DeviceGuard g(ctx->device);
+  std::vector<BuildSeg> segs(m);
+  unsigned long long total = 0;
+  unsigned max_n = 0;
+  for (int k = 0; k < m; ++k) {
+    const vgicp_cloud c = clouds[k];
+    segs[k] = BuildSeg{c->pa, c->pb, c->pc, total, static_cast<unsigned>(c->n), 0u, resolutions[k],
+                       1.0 / resolutions[k]};
+    total += c->n;
+    max_n = std::max<unsigned>(max_n, static_cast<unsigned>(c->n));
+  }
+  if (total >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "batched build exceeds 2^31 points");
+  const int ntot = static_cast<int>(total);
+
+  // scratch layout
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t o_segs = carve(sizeof(BuildSeg) * m);
+  const size_t o_outs = carve(sizeof(BuildOut) * m);
+  const size_t o_offs = carve(sizeof(int) * (m + 1));
+  const size_t o_err = carve(sizeof(int) * m);
+  const size_t o_vcnt = carve(sizeof(unsigned) * m);
+  const size_t o_vbase = carve(sizeof(unsigned) * m);
+  const size_t o_k0 = carve(sizeof(unsigned long long) * total);
+  const size_t o_k1 = carve(sizeof(unsigned long long) * total);
+  const size_t o_v0 = carve(sizeof(unsigned) * total);
+  const size_t o_v1 = carve(sizeof(unsigned) * total);
+  const size_t o_heads = carve(sizeof(unsigned) * total);
+  const size_t o_vidx = carve(sizeof(unsigned) * total);
+  std::vector<int> offsets(m + 1);
+  for (int k = 0; k < m; ++k) offsets[k] = static_cast<int>(segs[k].offset);
+  offsets[m] = ntot;
+  size_t sort_bytes = 0, scan_bytes = 0;
+  VG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, sort_bytes, (const unsigned long long*)nullptr,
+                                                   (unsigned long long*)nullptr, (const unsigned*)nullptr,
+                                                   (unsigned*)nullptr, ntot, m, (const int*)nullptr,
+                                                   (const int*)nullptr, 0, 63, ctx->stream));
+  VG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const unsigned*)nullptr, (unsigned*)nullptr, ntot,
+                                        ctx->stream));
+  const size_t o_temp = carve(std::max(sort_bytes, scan_bytes));
+  if (int rc = ensure_scratch(ctx, off)) return rc;
+  char* sb = static_cast<char*>(ctx->scratch);
+  auto* d_segs = reinterpret_cast<BuildSeg*>(sb + o_segs);
+  auto* d_outs = reinterpret_cast<BuildOut*>(sb + o_outs);
+  auto* d_offs = reinterpret_cast<int*>(sb + o_offs);
+  auto* d_err = reinterpret_cast<int*>(sb + o_err);
+  auto* d_vcnt = reinterpret_cast<unsigned*>(sb + o_vcnt);
+  auto* d_vbase = reinterpret_cast<unsigned*>(sb + o_vbase);
+  auto* d_k0 = reinterpret_cast<unsigned long long*>(sb + o_k0);
+  auto* d_k1 = reinterpret_cast<unsigned long long*>(sb + o_k1);
+  auto* d_v0 = reinterpret_cast<unsigned*>(sb + o_v0);
+  auto* d_v1 = reinterpret_cast<unsigned*>(sb + o_v1);
+  auto* d_heads = reinterpret_cast<unsigned*>(sb + o_heads);
+  auto* d_vidx = reinterpret_cast<unsigned*>(sb + o_vidx);
+  void* d_temp = sb + o_temp;
+  cudaStream_t s = ctx->stream;
+
+  VG_CUDA(cudaMemcpyAsync(d_segs, segs.data(), sizeof(BuildSeg) * m, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemcpyAsync(d_offs, offsets.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int) * m, s));
+  VG_CUDA(launch_build_keys(d_segs, m, max_n, d_k0, d_v0, d_err, s));
+  VG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(d_temp, sort_bytes, d_k0, d_k1, d_v0, d_v1, ntot, m, d_offs,
+                                                   d_offs + 1, 0, 63, s));
+  VG_CUDA(launch_build_heads(d_segs, m, max_n, d_k1, d_heads, s));
+  VG_CUDA(cub::DeviceScan::ExclusiveSum(d_temp, scan_bytes, d_heads, d_vidx, ntot, s));
+  VG_CUDA(launch_build_counts(d_segs, m, d_heads, d_vidx, d_vcnt, d_vbase, s));
+  ctx->launches += 5;  // keys, heads, counts + CUB sort/scan (counted as one each)
+  std::vector<int> herr(m);
+  std::vector<unsigned> hv(m), hbase(m);
+  VG_CUDA(cudaMemcpyAsync(herr.data(), d_err, sizeof(int) * m, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaMemcpyAsync(hv.data(), d_vcnt, sizeof(unsigned) * m, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaMemcpyAsync(hbase.data(), d_vbase, sizeof(unsigned) * m, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  for (int k = 0; k < m; ++k)
+    if (herr[k]) return fail(VGICP_E_OUT_OF_RANGE, "point beyond the +-2^20 voxel-per-axis range limit");
+
+  // allocate maps
+  std::vector<vgicp_map> maps(m, nullptr);
+  auto cleanup = [&]() {
+    for (auto* mp : maps) release(mp);
+  };
+  std::vector<BuildOut> outs(m);
+  for (int k = 0; k < m; ++k) {
+    auto* mp = new (std::nothrow) vgicp_map_s();
+    if (!mp) {
+      cleanup();
+      return fail(VGICP_E_OUT_OF_MEMORY, "host allocation failed");
+    }
+    maps[k] = mp;
+    mp->ctx = ctx;
+    mp->res = resolutions[k];
+    mp->inv_res = 1.0 / resolutions[k];
+    mp->voxels = hv[k];
+    mp->total_points = clouds[k]->n;
+    mp->capacity = std::max(64u, next_pow2(2ull * hv[k]));
+    unsigned lg = 0;
+    while ((1u << lg) < mp->capacity) ++lg;
+    mp->shift = 64 - lg;
+    const size_t V = hv[k];
+    const size_t b_table = align_up(sizeof(VoxelRec) * mp->capacity, 256);
+    const size_t b_keys = align_up(sizeof(unsigned long long) * V, 256);
+    const size_t b_counts = align_up(sizeof(int) * V, 256);
+    const size_t b_mean = align_up(sizeof(double) * 3 * V, 256);
+    const size_t b_cov = align_up(sizeof(double) * 9 * V, 256);
+    const cudaError_t e = cudaMalloc(&mp->block, b_table + b_keys + b_counts + b_mean + b_cov);
+    if (e != cudaSuccess) {
+      cleanup();
+      return cuda_fail(e, "cudaMalloc(voxel map)");
+    }
+    char* b = static_cast<char*>(mp->block);
+    mp->table = reinterpret_cast<VoxelRec*>(b);
+    mp->keys = reinterpret_cast<unsigned long long*>(b + b_table);
+    mp->counts = reinterpret_cast<int*>(b + b_table + b_keys);
+    mp->mean64 = reinterpret_cast<double*>(b + b_table + b_keys + b_counts);
+    mp->cov64 = reinterpret_cast<double*>(b + b_table + b_keys + b_counts + b_mean);
+    const cudaError_t e2 = cudaMemsetAsync(mp->table, 0xFF, sizeof(VoxelRec) * mp->capacity, s);
+    if (e2 != cudaSuccess) {
+      cleanup();
+      return cuda_fail(e2, "cudaMemsetAsync(table)");
+    }
+    outs[k] = BuildOut{mp->table, mp->keys, mp->counts, mp->mean64, mp->cov64, mp->shift, mp->capacity - 1,
+                       hbase[k], 0u};
+  }
+  cudaError_t e = cudaMemcpyAsync(d_outs, outs.data(), sizeof(BuildOut) * m, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = launch_build_accumulate(d_segs, d_outs, m, max_n, d_k1, d_v1, d_heads, d_vidx, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "voxel map accumulate");
+  }
+  ctx->launches += 1;
+  for (int k = 0; k < m; ++k) out[k] = maps[k];
+  return VGICP_OK;
+}
+
+int vgicp_voxelmap_build(vgicp_ctx ctx, vgicp_cloud cloud, double resolution, vgicp_map* out) {
+  if (!out) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
+  return vgicp_voxelmap_build_batch(ctx, &cloud, &resolution, 1, out);
+}
+
+int vgicp_voxelmap_destroy(vgicp_map map) {
+  release(map);
+  return VGICP_OK;
+}
+
+int vgicp_voxelmap_size(vgicp_map map, size_t* voxels) {
+  if (!map || !voxels) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *voxels = map->voxels;
+  return VGICP_OK;
+}
+
+int vgicp_voxelmap_resolution(vgicp_map map, double* resolution) {
+  if (!map || !resolution) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *resolution = map->res;
+  return VGICP_OK;
+}
+
+int vgicp_voxelmap_total_points(vgicp_map map, size_t* total) {
+  if (!map || !total) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *total = map->total_points;
+  return VGICP_OK;
+}
+
+int vgicp_voxelmap_export(vgicp_map map, uint64_t* keys, int32_t* counts, double* means, double* covs) {
+  if (!map) return fail(VGICP_E_INVALID_ARGUMENT, "null map");
+  DeviceGuard g(map->ctx->device);
+  cudaStream_t s = map->ctx->stream;
+  const size_t V = map->voxels;
+  if (V == 0) return VGICP_OK;
+  if (keys) VG_CUDA(cudaMemcpyAsync(keys, map->keys, sizeof(uint64_t) * V, cudaMemcpyDeviceToHost, s));
+  if (counts) VG_CUDA(cudaMemcpyAsync(counts, map->counts, sizeof(int32_t) * V, cudaMemcpyDeviceToHost, s));
+  if (means) VG_CUDA(cudaMemcpyAsync(means, map->mean64, sizeof(double) * 3 * V, cudaMemcpyDeviceToHost, s));
+  if (covs) VG_CUDA(cudaMemcpyAsync(covs, map->cov64, sizeof(double) * 9 * V, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  return VGICP_OK;
+}
+
+int vgicp_voxelmap_lookup(vgicp_map map, const double* points, size_t n, uint64_t* keys_out) {
+  if (!map || (n > 0 && (!points || !keys_out))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (n == 0) return VGICP_OK;
+  vgicp_ctx ctx = map->ctx;
+  DeviceGuard g(ctx->device);
+  const size_t bp = align_up(sizeof(double) * 3 * n, 256);
+  if (int rc = ensure_scratch(ctx, bp + sizeof(uint64_t) * n)) return rc;
+  char* sb = static_cast<char*>(ctx->scratch);
+  double* d_pts = reinterpret_cast<double*>(sb);
+  auto* d_keys = reinterpret_cast<unsigned long long*>(sb + bp);
+  VG_CUDA(cudaMemcpyAsync(d_pts, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+  VG_CUDA(launch_lookup(map->dev(), d_pts, n, d_keys, ctx->stream));
+  ctx->launches += 1;
+  VG_CUDA(cudaMemcpyAsync(keys_out, d_keys, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return VGICP_OK;
+}
+
+int vgicp_voxel_key(double resolution, const double point[3], uint64_t* key) {
+  if (!point || !key) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  return host_voxel_key(resolution, point, key);
+}
+
+// ------------------------------------------------------------------------------------ overlap
+int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* poses12, const vgicp_map* maps,
+                        int m, uint64_t* hits) {
+  if (!ctx || (m > 0 && (!clouds || !poses12 || !maps || !hits)))
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (m <= 0) return VGICP_OK;
+  std::vector<OverlapItem> items(m);
+  unsigned max_n = 0;
+  for (int k = 0; k < m; ++k) {
+    if (!clouds[k] || !maps[k]) return fail(VGICP_E_INVALID_ARGUMENT, "null cloud or map");
+    if (clouds[k]->ctx != ctx || maps[k]->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "handle of another context");
+    if (clouds[k]->n == 0) return fail(VGICP_E_INVALID_ARGUMENT, "overlap_rate requires a nonempty cloud");
+    OverlapItem& it = items[k];
+    it.pa = clouds[k]->pa;
+    it.map = maps[k]->dev();
+    std::memcpy(it.T, poses12 + 12 * k, sizeof(double) * 12);
+    it.n = static_cast<unsigned>(clouds[k]->n);
+    it.pad = 0;
+    max_n = std::max(max_n, it.n);
+  }
+  DeviceGuard g(ctx->device);
+  const size_t bi = align_up(sizeof(OverlapItem) * m, 256);
+  if (int rc = ensure_scratch(ctx, bi + sizeof(unsigned long long) * m)) return rc;
+  char* sb = static_cast<char*>(ctx->scratch);
+  auto* d_items = reinterpret_cast<OverlapItem*>(sb);
+  auto* d_hits = reinterpret_cast<unsigned long long*>(sb + bi);
+  cudaStream_t s = ctx->stream;
+  VG_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(OverlapItem) * m, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long) * m, s));
+  VG_CUDA(launch_overlap(d_items, m, max_n, d_hits, s));
+  ctx->launches += 1;
+  VG_CUDA(cudaMemcpyAsync(hits, d_hits, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  return VGICP_OK;
+}
+
+int vgicp_overlap_rate(vgicp_ctx ctx, vgicp_cloud cloud, const double pose_rel[12], vgicp_map map, double* rate) {
+  if (!rate || !cloud || !map || !pose_rel) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  uint64_t hits = 0;
+  if (int rc = vgicp_overlap_batch(ctx, &cloud, pose_rel, &map, 1, &hits)) return rc;
+  *rate = static_cast<double>(hits) / static_cast<double>(cloud->n);  // voxelmap.cpp:134
+  return VGICP_OK;
+}
+
+// ------------------------------------------------------------------------------------ graphs
+int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses, int chunk,
+                       vgicp_graph* out) {
+  if (!ctx || !out || (num_factors > 0 && !factors)) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (num_factors < 0 || num_poses < 0) return fail(VGICP_E_INVALID_ARGUMENT, "negative size");
+  if (chunk <= 0) chunk = 2048;
+  chunk = std::max(kFactorThreads, (chunk + kFactorThreads - 1) / kFactorThreads * kFactorThreads);
+  // MatchingCostFactor ctor validation (factors.cpp:57-66)
+  for (int f = 0; f < num_factors; ++f) {
+    const vgicp_factor_desc& d = factors[f];
+    if (d.target_index == d.source_index)
+      return fail(VGICP_E_INVALID_ARGUMENT, "matching cost factor requires distinct variables");
+    if (!d.source || d.source->n == 0)
+      return fail(VGICP_E_INVALID_ARGUMENT, "matching cost factor requires a nonempty source cloud");
+    if (!d.source->has_cov) return fail(VGICP_E_INVALID_ARGUMENT, "matching cost factor requires source covariances");
+    if (!d.target || d.target->voxels == 0)
+      return fail(VGICP_E_INVALID_ARGUMENT, "matching cost factor requires a nonempty target voxel map");
+    if (d.source->ctx != ctx || d.target->ctx != ctx)
+      return fail(VGICP_E_INVALID_ARGUMENT, "factor handles belong to another context");
+    if (d.target_index < 0 || d.target_index >= num_poses || d.source_index < 0 || d.source_index >= num_poses)
+      return fail(VGICP_E_INVALID_ARGUMENT, "factor variable index out of range");
+  }
+  DeviceGuard g(ctx->device);
+  std::vector<FactorDev> fd(num_factors);
+  std::vector<WorkItem> items;
+  uint64_t points = 0;
+  for (int f = 0; f < num_factors; ++f) {
+    const vgicp_factor_desc& d = factors[f];
+    FactorDev& x = fd[f];
+    x.pa = d.source->pa;
+    x.pb = d.source->pb;
+    x.pc = d.source->pc;
+    x.map = d.target->dev();
+    x.n = static_cast<int>(d.source->n);
+    x.tgt = d.target_index;
+    x.src = d.source_index;
+    x.item_begin = static_cast<int>(items.size());
+    for (int b = 0; b < x.n; b += chunk) items.push_back(WorkItem{f, b, std::min(x.n, b + chunk), 0});
+    x.item_count = static_cast<int>(items.size()) - x.item_begin;
+    x.pad = 0;
+    points += d.source->n;
+  }
+  auto gr = std::make_unique<vgicp_graph_s>();
+  gr->ctx = ctx;
+  gr->num_factors = num_factors;
+  gr->num_poses = num_poses;
+  gr->num_items = static_cast<int>(items.size());
+  gr->num_points = points;
+  const size_t nf = std::max(num_factors, 1), ni = std::max<size_t>(items.size(), 1);
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t o_f = carve(sizeof(FactorDev) * nf);
+  const size_t o_i = carve(sizeof(WorkItem) * ni);
+  const size_t o_p = carve(sizeof(double) * kPartialStride * ni);
+  const size_t o_pi = carve(sizeof(int) * ni);
+  const size_t o_c = carve(sizeof(unsigned) * nf);
+  const size_t o_pose = carve(sizeof(double) * 12 * std::max(num_poses, 1));
+  const size_t o_out = carve(sizeof(double) * VGICP_LINEARIZED_DOUBLES * nf);
+  const size_t o_oi = carve(sizeof(int) * nf);
+  const size_t o_err = carve(sizeof(double) * nf);
+  VG_CUDA(cudaMalloc(&gr->block, off));
+  char* b = static_cast<char*>(gr->block);
+  gr->d_factors = reinterpret_cast<FactorDev*>(b + o_f);
+  gr->d_items = reinterpret_cast<WorkItem*>(b + o_i);
+  gr->d_partials = reinterpret_cast<double*>(b + o_p);
+  gr->d_part_inl = reinterpret_cast<int*>(b + o_pi);
+  gr->d_counters = reinterpret_cast<unsigned*>(b + o_c);
+  gr->d_poses = reinterpret_cast<double*>(b + o_pose);
+  gr->d_out = reinterpret_cast<double*>(b + o_out);
+  gr->d_out_inl = reinterpret_cast<int*>(b + o_oi);
+  gr->d_err = reinterpret_cast<double*>(b + o_err);
+  cudaStream_t s = ctx->stream;
+  int rc = VGICP_OK;
+  auto step = [&](cudaError_t e, const char* what) {
+    if (rc == VGICP_OK && e != cudaSuccess) rc = cuda_fail(e, what);
+  };
+  if (num_factors > 0) {
+    step(cudaMemcpyAsync(gr->d_factors, fd.data(), sizeof(FactorDev) * num_factors, cudaMemcpyHostToDevice, s),
+         "upload factors");
+    step(cudaMemcpyAsync(gr->d_items, items.data(), sizeof(WorkItem) * items.size(), cudaMemcpyHostToDevice, s),
+         "upload items");
+  }
+  step(cudaMemsetAsync(gr->d_counters, 0, sizeof(unsigned) * nf, s), "zero counters");
+  step(cudaStreamSynchronize(s), "graph create");
+  if (rc != VGICP_OK) {
+    cudaFree(gr->block);
+    return rc;
+  }
+  for (int f = 0; f < num_factors; ++f) {
+    factors[f].source->refs.fetch_add(1);
+    factors[f].target->refs.fetch_add(1);
+    gr->clouds.push_back(factors[f].source);
+    gr->maps.push_back(factors[f].target);
+  }
+  *out = gr.release();
+  return VGICP_OK;
+}
+
+int vgicp_graph_destroy(vgicp_graph graph) {
+  if (!graph) return VGICP_OK;
+  {
+    DeviceGuard g(graph->ctx->device);
+    cudaStreamSynchronize(graph->ctx->stream);
+    cudaFree(graph->block);
+  }
+  for (auto c : graph->clouds) release(c);
+  for (auto m : graph->maps) release(m);
+  delete graph;
+  return VGICP_OK;
+}
+
+int vgicp_graph_num_factors(vgicp_graph graph, int* n) {
+  if (!graph || !n) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *n = graph->num_factors;
+  return VGICP_OK;
+}
+
+int vgicp_graph_num_points(vgicp_graph graph, uint64_t* points) {
+  if (!graph || !points) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *points = graph->num_points;
+  return VGICP_OK;
+}
+
+int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, double* d_out, int32_t* d_inliers) {
+  if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_out || !d_inliers)))
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  DeviceGuard g(graph->ctx->device);
+  VG_CUDA(launch_factor(true, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
+                        graph->d_part_inl, graph->d_counters, d_out, d_inliers, graph->ctx->stream));
+  graph->ctx->launches += graph->num_items > 0 ? 1 : 0;
+  return VGICP_OK;
+}
+
+int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, double* d_errors, int32_t* d_inliers) {
+  if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_errors || !d_inliers)))
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  DeviceGuard g(graph->ctx->device);
+  VG_CUDA(launch_factor(false, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
+                        graph->d_part_inl, graph->d_counters, d_errors, d_inliers, graph->ctx->stream));
+  graph->ctx->launches += graph->num_items > 0 ? 1 : 0;
+  return VGICP_OK;
+}
+
+static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses12, double* out, int32_t* inliers) {
+  if (!graph || !poses12 || (graph->num_factors > 0 && (!out || !inliers)))
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  vgicp_ctx ctx = graph->ctx;
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const int nf = graph->num_factors;
+  if (nf == 0) return VGICP_OK;
+  const size_t pose_bytes = sizeof(double) * 12 * graph->num_poses;
+  const size_t res_bytes = linearize ? sizeof(double) * VGICP_LINEARIZED_DOUBLES * nf : sizeof(double) * nf;
+  const size_t inl_bytes = sizeof(int32_t) * nf;
+  if (int rc = ensure_pinned(ctx, align_up(pose_bytes, 256) + align_up(res_bytes, 256) + inl_bytes)) return rc;
+  char* h = static_cast<char*>(ctx->pinned);
+  double* h_poses = reinterpret_cast<double*>(h);
+  double* h_res = reinterpret_cast<double*>(h + align_up(pose_bytes, 256));
+  auto* h_inl = reinterpret_cast<int32_t*>(h + align_up(pose_bytes, 256) + align_up(res_bytes, 256));
+  std::memcpy(h_poses, poses12, pose_bytes);
+  VG_CUDA(cudaMemcpyAsync(graph->d_poses, h_poses, pose_bytes, cudaMemcpyHostToDevice, s));
+  double* d_res = linearize ? graph->d_out : graph->d_err;
+  VG_CUDA(launch_factor(linearize, graph->d_factors, graph->d_items, graph->num_items, graph->d_poses,
+                        graph->d_partials, graph->d_part_inl, graph->d_counters, d_res, graph->d_out_inl, s));
+  ctx->launches += 1;
+  VG_CUDA(cudaMemcpyAsync(h_res, d_res, res_bytes, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaMemcpyAsync(h_inl, graph->d_out_inl, inl_bytes, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(out, h_res, res_bytes);
+  std::memcpy(inliers, h_inl, inl_bytes);
+  return VGICP_OK;
+}
+
+int vgicp_graph_linearize(vgicp_graph graph, const double* poses12, double* out, int32_t* inliers) {
+  return graph_run_host(graph, true, poses12, out, inliers);
+}
+
+int vgicp_graph_evaluate(vgicp_graph graph, const double* poses12, double* errors, int32_t* inliers) {
+  return graph_run_host(graph, false, poses12, errors, inliers);
+}
+
+// Single-factor entry points: a one-factor graph over poses {target, source}.
+static int single_factor(vgicp_ctx ctx, const vgicp_factor_desc* factor, const double* T_target,
+                         const double* T_source, bool linearize, double* out, int32_t* inliers) {
+  if (!ctx || !factor || !T_target || !T_source || !out || !inliers)
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (factor->target_index == factor->source_index)
+    return fail(VGICP_E_INVALID_ARGUMENT, "matching cost factor requires distinct variables");
+  vgicp_factor_desc d = *factor;
+  d.target_index = 0;
+  d.source_index = 1;
+  vgicp_graph gr = nullptr;
+  if (int rc = vgicp_graph_create(ctx, &d, 1, 2, 0, &gr)) return rc;
+  double poses[24];
+  std::memcpy(poses, T_target, sizeof(double) * 12);
+  std::memcpy(poses + 12, T_source, sizeof(double) * 12);
+  const int rc = graph_run_host(gr, linearize, poses, out, inliers);
+  vgicp_graph_destroy(gr);
+  return rc;
+}
+
+int vgicp_linearize_matching_cost(vgicp_ctx ctx, const vgicp_factor_desc* factor, const double T_target[12],
+                                  const double T_source[12], double out[VGICP_LINEARIZED_DOUBLES],
+                                  int32_t* inliers) {
+  return single_factor(ctx, factor, T_target, T_source, true, out, inliers);
+}
+
+int vgicp_evaluate_matching_cost(vgicp_ctx ctx, const vgicp_factor_desc* factor, const double T_target[12],
+                                 const double T_source[12], double* error, int32_t* inliers) {
+  return single_factor(ctx, factor, T_target, T_source, false, error, inliers);
+}
+
+int vgicp_gicp_error(vgicp_ctx ctx, const double source_mean[3], const double source_cov[9],
+                     const double target_mean[3], const double target_cov[9], const double T[12], double* error,
+                     double residual[3], double information[9], int* valid) {
+  if (!ctx || !source_mean || !source_cov || !target_mean || !target_cov || !T || !error || !residual ||
+      !information || !valid)
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  DeviceGuard g(ctx->device);
+  if (int rc = ensure_scratch(ctx, 64 * sizeof(double))) return rc;
+  if (int rc = ensure_pinned(ctx, 64 * sizeof(double))) return rc;
+  double* h = static_cast<double*>(ctx->pinned);
+  std::memcpy(h, source_mean, 3 * sizeof(double));
+  std::memcpy(h + 3, source_cov, 9 * sizeof(double));
+  std::memcpy(h + 12, target_mean, 3 * sizeof(double));
+  std::memcpy(h + 15, target_cov, 9 * sizeof(double));
+  std::memcpy(h + 24, T, 12 * sizeof(double));
+  double* d = static_cast<double*>(ctx->scratch);
+  cudaStream_t s = ctx->stream;
+  VG_CUDA(cudaMemcpyAsync(d, h, 36 * sizeof(double), cudaMemcpyHostToDevice, s));
+  VG_CUDA(launch_gicp_error(d, d + 40, s));
+  ctx->launches += 1;
+  VG_CUDA(cudaMemcpyAsync(h + 40, d + 40, 14 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  *error = h[40];
+  std::memcpy(residual, h + 41, 3 * sizeof(double));
+  std::memcpy(information, h + 44, 9 * sizeof(double));
+  *valid = h[53] != 0.0 ? 1 : 0;
+  return VGICP_OK;
+}
+
+}  // extern "C"

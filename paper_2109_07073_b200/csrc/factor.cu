@@ -1,0 +1,362 @@
+// Batched VGICP matching-cost factor kernels (sm_100a): linearize (factors.cpp:90-148) and
+// evaluate (factors.cpp:150-181) for every factor of a graph in ONE launch.
+//
+// Grid: one CTA per work item (factor, chunk of source points). Per source point:
+//   fp64  q = T_ts·mu (reference op order), exact voxel key, hash probe of the target map
+//   fp32  e = voxel-local mean - (q - corner), M = C_t + R C_s Rᵀ, Omega = M⁻¹ (cofactor),
+//         H_tt = AᵀΩA with A = [-[q]x | I] as Q = -[q]xΩ[q]x (6), P = [q]xΩ (9), Ω (6),
+//         b_t = [-q×Ωe; -Ωe] (6), error eᵀΩe  -> 28 fp32 accumulators + int inliers
+//   near-singular M (fp32 Sylvester test without margin) -> the oracle-identical fp64 LDLT path
+// Reduction without float atomics: per-thread fp32 -> warp shuffle in fp64 ->
+// shared-memory CTA sum in fp64 -> one partial per CTA; the last CTA of a factor (integer
+// arrival counter) sums the factor's partials in item order and expands, in fp64,
+//   H_ts = -H_tt·Ad,  H_ss = AdᵀH_tt·Ad,  b_s = -Adᵀb_t,  Ad = Ad(T_ts) (se3.cpp:107-113),
+// which is exact algebra because B = -A·Ad(T_ts). Fixed orders everywhere => deterministic.
+#include "exact_math.cuh"
+#include "internal.h"
+
+namespace vgicp {
+
+namespace {
+
+constexpr int kWarps = kFactorThreads / 32;
+
+// T_ts = T_target⁻¹ · T_source (factors.cpp:94), entry k of the 12-double pose, computed with
+// the oracle's op order: inverse (se3.hpp:45) then compose (se3.cpp:42-44).
+__device__ __forceinline__ double relative_pose_entry(const double* Tt, const double* Ts, int k) {
+  if (k < 9) {
+    const int i = k / 3, j = k % 3;
+    return dot3_rn(Tt[i], Tt[3 + i], Tt[6 + i], Ts[j], Ts[3 + j], Ts[6 + j]);
+  }
+  const int i = k - 9;
+  const double inv_t = -dot3_rn(Tt[i], Tt[3 + i], Tt[6 + i], Tt[9], Tt[10], Tt[11]);
+  return __dadd_rn(dot3_rn(Tt[i], Tt[3 + i], Tt[6 + i], Ts[9], Ts[10], Ts[11]), inv_t);
+}
+
+// Rare path: M near singular in fp32 -> recompute M and the LDLT decision in fp64 exactly as
+// the oracle (factors.cpp:38-46, :107) and return Omega as fp32.
+__device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, float sxz, float syy, float syz,
+                                        float szz, const double* Ct, float* om) {
+  const double Cs[9] = {sxx, sxy, sxz, sxy, syy, syz, sxz, syz, szz};
+  double M[9], O[9];
+  combined_cov_rn(T, Cs, Ct, M);
+  if (!invert_covariance_rn(M, O)) return false;
+  om[0] = (float)O[0];
+  om[1] = (float)O[1];
+  om[2] = (float)O[2];
+  om[3] = (float)O[4];
+  om[4] = (float)O[5];
+  om[5] = (float)O[8];
+  return true;
+}
+
+template <bool kLinearize>
+__global__ void __launch_bounds__(kFactorThreads) factor_kernel(
+    const FactorDev* __restrict__ factors, const WorkItem* __restrict__ items, const double* __restrict__ poses,
+    double* __restrict__ partials, int* __restrict__ part_inl, unsigned* __restrict__ counters,
+    double* __restrict__ out, int* __restrict__ out_inl) {
+  constexpr int kAcc = kLinearize ? kLinAcc : 1;
+  __shared__ double sT[12];
+  __shared__ double sRed[kWarps][kAcc];
+  __shared__ int sInl[kWarps];
+  __shared__ int sLast;
+  __shared__ double sTot[kLinAcc];
+  __shared__ int sTotInl;
+  __shared__ double sH[36], sAd[36], sHA[36], sHss[36];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const WorkItem w = items[blockIdx.x];
+  const FactorDev* __restrict__ fp = factors + w.factor;
+
+  if (tid < 12) sT[tid] = relative_pose_entry(poses + 12 * fp->tgt, poses + 12 * fp->src, tid);
+  __syncthreads();
+
+  const float4* __restrict__ pa = fp->pa;
+  const float4* __restrict__ pb = fp->pb;
+  const float* __restrict__ pc = fp->pc;
+  const MapDev map = fp->map;
+
+  double T[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) T[k] = sT[k];
+  const float r00 = (float)T[0], r01 = (float)T[1], r02 = (float)T[2];
+  const float r10 = (float)T[3], r11 = (float)T[4], r12 = (float)T[5];
+  const float r20 = (float)T[6], r21 = (float)T[7], r22 = (float)T[8];
+
+  float acc[kAcc];
+#pragma unroll
+  for (int k = 0; k < kAcc; ++k) acc[k] = 0.f;
+  int inl = 0;
+
+  for (int i = w.begin + tid; i < w.end; i += kFactorThreads) {
+    const float4 A = __ldg(pa + i);
+    double q0, q1, q2;
+    apply_pose_rn(T, A.x, A.y, A.z, q0, q1, q2);
+    unsigned long long key;
+    double c0, c1, c2;
+    if (!voxel_key(q0, q1, q2, map.res, map.inv_res, key, c0, c1, c2)) continue;
+    float mx, my;
+    const int slot = probe(map.table, map.shift, map.mask, key, mx, my);
+    if (slot < 0) continue;
+    const float4* rec = reinterpret_cast<const float4*>(map.table + slot);
+    const float4 v1 = __ldg(rec + 1);  // mz cxx cxy cxz
+    const float4 v2 = __ldg(rec + 2);  // cyy cyz czz vid
+    const float4 B = __ldg(pb + i);    // sxy sxz syy syz
+    const float szz = __ldg(pc + i);
+    const float sxx = A.w, sxy = B.x, sxz = B.y, syy = B.z, syz = B.w;
+
+    // residual e = mu' - q in voxel-local coordinates (mu' and q differ by < 2 voxels)
+    const float e0 = mx - (float)__dsub_rn(q0, __dmul_rn(c0, map.res));
+    const float e1 = my - (float)__dsub_rn(q1, __dmul_rn(c1, map.res));
+    const float e2 = v1.x - (float)__dsub_rn(q2, __dmul_rn(c2, map.res));
+
+    // M = C_t + R C_s Rᵀ (fp32)
+    const float t00 = r00 * sxx + r01 * sxy + r02 * sxz;
+    const float t01 = r00 * sxy + r01 * syy + r02 * syz;
+    const float t02 = r00 * sxz + r01 * syz + r02 * szz;
+    const float t10 = r10 * sxx + r11 * sxy + r12 * sxz;
+    const float t11 = r10 * sxy + r11 * syy + r12 * syz;
+    const float t12 = r10 * sxz + r11 * syz + r12 * szz;
+    const float t20 = r20 * sxx + r21 * sxy + r22 * sxz;
+    const float t21 = r20 * sxy + r21 * syy + r22 * syz;
+    const float t22 = r20 * sxz + r21 * syz + r22 * szz;
+    const float m00 = v1.y + (t00 * r00 + t01 * r01 + t02 * r02);
+    const float m01 = v1.z + (t00 * r10 + t01 * r11 + t02 * r12);
+    const float m02 = v1.w + (t00 * r20 + t01 * r21 + t02 * r22);
+    const float m11 = v2.x + (t10 * r10 + t11 * r11 + t12 * r12);
+    const float m12 = v2.y + (t10 * r20 + t11 * r21 + t12 * r22);
+    const float m22 = v2.z + (t20 * r20 + t21 * r21 + t22 * r22);
+
+    // Omega = M⁻¹ by cofactors; Sylvester test with margins decides the fast path
+    const float a00 = m11 * m22 - m12 * m12;
+    const float a01 = m02 * m12 - m01 * m22;
+    const float a02 = m01 * m12 - m02 * m11;
+    const float a11 = m00 * m22 - m02 * m02;
+    const float a12 = m01 * m02 - m00 * m12;
+    const float a22 = m00 * m11 - m01 * m01;
+    const float det = m00 * a00 + m01 * a01 + m02 * a02;
+    const float tr = m00 + m11 + m22;
+    float om[6];
+    if (tr > 0.f && m00 > 1e-6f * tr && a22 > 1e-6f * tr * tr && det > 1e-5f * tr * tr * tr) {
+      const float inv = __frcp_rn(det);
+      om[0] = a00 * inv;
+      om[1] = a01 * inv;
+      om[2] = a02 * inv;
+      om[3] = a11 * inv;
+      om[4] = a12 * inv;
+      om[5] = a22 * inv;
+    } else {
+      if (!omega_fp64(sT, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.w), om)) continue;
+    }
+    const float o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
+    const float w0 = o00 * e0 + o01 * e1 + o02 * e2;
+    const float w1 = o01 * e0 + o11 * e1 + o12 * e2;
+    const float w2 = o02 * e0 + o12 * e1 + o22 * e2;
+    ++inl;
+    if constexpr (!kLinearize) {
+      acc[0] += e0 * w0 + e1 * w1 + e2 * w2;
+    } else {
+      const float qf0 = (float)q0, qf1 = (float)q1, qf2 = (float)q2;
+      // P = [q]x Ω
+      const float p00 = qf1 * o02 - qf2 * o01, p01 = qf1 * o12 - qf2 * o11, p02 = qf1 * o22 - qf2 * o12;
+      const float p10 = qf2 * o00 - qf0 * o02, p11 = qf2 * o01 - qf0 * o12, p12 = qf2 * o02 - qf0 * o22;
+      const float p20 = qf0 * o01 - qf1 * o00, p21 = qf0 * o11 - qf1 * o01, p22 = qf0 * o12 - qf1 * o02;
+      // Q = -P [q]x  (symmetric)
+      acc[0] += p02 * qf1 - p01 * qf2;   // Q00
+      acc[1] += p00 * qf2 - p02 * qf0;   // Q01
+      acc[2] += p01 * qf0 - p00 * qf1;   // Q02
+      acc[3] += p10 * qf2 - p12 * qf0;   // Q11
+      acc[4] += p11 * qf0 - p10 * qf1;   // Q12
+      acc[5] += p21 * qf0 - p20 * qf1;   // Q22
+      acc[6] += p00;
+      acc[7] += p01;
+      acc[8] += p02;
+      acc[9] += p10;
+      acc[10] += p11;
+      acc[11] += p12;
+      acc[12] += p20;
+      acc[13] += p21;
+      acc[14] += p22;
+      acc[15] += o00;
+      acc[16] += o01;
+      acc[17] += o02;
+      acc[18] += o11;
+      acc[19] += o12;
+      acc[20] += o22;
+      // b_t = -AᵀΩe = [-(q × w); -w]
+      acc[21] -= qf1 * w2 - qf2 * w1;
+      acc[22] -= qf2 * w0 - qf0 * w2;
+      acc[23] -= qf0 * w1 - qf1 * w0;
+      acc[24] -= w0;
+      acc[25] -= w1;
+      acc[26] -= w2;
+      acc[27] += e0 * w0 + e1 * w1 + e2 * w2;
+    }
+  }
+
+  // ---- CTA reduction: warp shuffle in fp64, then fixed-order sum over warps ----
+#pragma unroll
+  for (int k = 0; k < kAcc; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if (lane == 0) sRed[warp][k] = v;
+  }
+  inl = __reduce_add_sync(0xffffffffu, inl);
+  if (lane == 0) sInl[warp] = inl;
+  __syncthreads();
+  if (tid < kAcc) {
+    double s = sRed[0][tid];
+#pragma unroll
+    for (int q = 1; q < kWarps; ++q) s += sRed[q][tid];
+    partials[(size_t)blockIdx.x * kPartialStride + tid] = s;
+  }
+  if (tid == kAcc) {
+    int s = 0;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) s += sInl[q];
+    part_inl[blockIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) sLast = (atomicAdd(&counters[w.factor], 1u) + 1u == (unsigned)fp->item_count);
+  __syncthreads();
+  if (!sLast) return;
+  __threadfence();
+
+  // ---- last CTA of this factor: item-ordered sum of partials, then the fp64 epilogue ----
+  const int ib = fp->item_begin, ic = fp->item_count;
+  if (tid < kAcc) {
+    double s = 0.0;
+    for (int it = 0; it < ic; ++it) s += __ldcg(&partials[(size_t)(ib + it) * kPartialStride + tid]);
+    sTot[tid] = s;
+  }
+  if (tid == 32) {
+    int s = 0;
+    for (int it = 0; it < ic; ++it) s += __ldcg(&part_inl[ib + it]);
+    sTotInl = s;
+  }
+  if (tid == 0) counters[w.factor] = 0u;  // ready for the next launch
+  __syncthreads();
+
+  if constexpr (!kLinearize) {
+    if (tid == 0) {
+      out[w.factor] = sTot[0];
+      out_inl[w.factor] = sTotInl;
+    }
+    return;
+  } else {
+    const int f = w.factor;
+    double* o = out + (size_t)f * VGICP_LINEARIZED_DOUBLES;
+    if (tid < 36) {
+      const int i = tid / 6, j = tid % 6;
+      // H_tt = [[Q, P], [Pᵀ, Ω]]
+      const int qi[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+      double h;
+      if (i < 3 && j < 3) h = sTot[qi[i][j]];
+      else if (i < 3) h = sTot[6 + 3 * i + (j - 3)];
+      else if (j < 3) h = sTot[6 + 3 * j + (i - 3)];
+      else h = sTot[15 + qi[i - 3][j - 3]];
+      sH[tid] = h;
+      // Ad(T_ts) = [[R, 0], [[t]x R, R]]
+      double ad = 0.0;
+      if (i < 3 && j < 3) ad = sT[3 * i + j];
+      else if (i >= 3 && j >= 3) ad = sT[3 * (i - 3) + (j - 3)];
+      else if (i >= 3 && j < 3) {
+        const int r = i - 3;
+        const double tx = sT[9], ty = sT[10], tz = sT[11];
+        const double sk[3][3] = {{0.0, -tz, ty}, {tz, 0.0, -tx}, {-ty, tx, 0.0}};
+        ad = dot3_rn(sk[r][0], sk[r][1], sk[r][2], sT[j], sT[3 + j], sT[6 + j]);
+      }
+      sAd[tid] = ad;
+    }
+    __syncthreads();
+    if (tid < 36) {
+      const int i = tid / 6, j = tid % 6;
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < 6; ++m) s += sH[6 * i + m] * sAd[6 * m + j];
+      sHA[tid] = s;  // H_tt · Ad
+    }
+    __syncthreads();
+    if (tid < 36) {
+      const int i = tid / 6, j = tid % 6;
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < 6; ++m) s += sAd[6 * m + i] * sHA[6 * m + j];
+      sHss[tid] = s;  // Adᵀ · H_tt · Ad
+    }
+    __syncthreads();
+    if (tid < 36) {
+      const int i = tid / 6, j = tid % 6;
+      o[tid] = sH[tid];                                       // H_ii (exactly symmetric)
+      o[36 + tid] = -sHA[tid];                                // H_ij
+      o[72 + tid] = 0.5 * (sHss[6 * i + j] + sHss[6 * j + i]);  // H_jj, symmetrised (factors.cpp:141)
+    } else if (tid < 42) {
+      const int i = tid - 36;
+      o[108 + i] = sTot[21 + i];  // b_i = b_t
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < 6; ++m) s += sAd[6 * m + i] * sTot[21 + m];
+      o[114 + i] = -s;  // b_j = -Adᵀ b_t
+    } else if (tid == 42) {
+      o[120] = sTot[27];
+      out_inl[f] = sTotInl;
+    }
+  }
+}
+
+// gicp_error (factors.cpp:75-88) in fp64, bit-identical to the oracle.
+// in: src_mean(3) src_cov(9) tgt_mean(3) tgt_cov(9) T(12); out: error, residual(3), info(9), valid
+__global__ void gicp_error_kernel(const double* __restrict__ in, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double* sm = in;
+  const double* sc = in + 3;
+  const double* tm = in + 12;
+  const double* tc = in + 15;
+  const double* T = in + 24;
+  double q0, q1, q2;
+  apply_pose_rn(T, sm[0], sm[1], sm[2], q0, q1, q2);
+  const double d0 = __dsub_rn(tm[0], q0), d1 = __dsub_rn(tm[1], q1), d2 = __dsub_rn(tm[2], q2);
+  out[1] = d0;
+  out[2] = d1;
+  out[3] = d2;
+  double M[9], O[9];
+  combined_cov_rn(T, sc, tc, M);
+  if (!invert_covariance_rn(M, O)) {
+    out[0] = 0.0;
+    for (int k = 0; k < 9; ++k) out[4 + k] = 0.0;
+    out[13] = 0.0;
+    return;
+  }
+  for (int k = 0; k < 9; ++k) out[4 + k] = O[k];
+  const double w0 = dot3_rn(O[0], O[1], O[2], d0, d1, d2);
+  const double w1 = dot3_rn(O[3], O[4], O[5], d0, d1, d2);
+  const double w2 = dot3_rn(O[6], O[7], O[8], d0, d1, d2);
+  out[0] = dot3_rn(d0, d1, d2, w0, w1, w2);
+  out[13] = 1.0;
+}
+
+}  // namespace
+
+cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkItem* items, int num_items,
+                          const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
+                          int* out_inl, cudaStream_t s) {
+  if (num_items <= 0) return cudaSuccess;
+  if (linearize)
+    factor_kernel<true><<<num_items, kFactorThreads, 0, s>>>(factors, items, poses, partials, part_inl, counters,
+                                                            out, out_inl);
+  else
+    factor_kernel<false><<<num_items, kFactorThreads, 0, s>>>(factors, items, poses, partials, part_inl, counters,
+                                                             out, out_inl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s) {
+  gicp_error_kernel<<<1, 32, 0, s>>>(in, out);
+  return cudaGetLastError();
+}
+
+}  // namespace vgicp

@@ -1,0 +1,162 @@
+// Host-side handle structures and launch entry points shared by the translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/vgicp_b200.h"
+#include "vgicp_device.cuh"
+
+namespace vgicp {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t err, const char* what);
+
+#define VG_CUDA(call)                                  \
+  do {                                                 \
+    const cudaError_t _e = (call);                     \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+// Work decomposition of a batched factor launch: one CTA per (factor, point chunk).
+struct WorkItem {
+  int factor;
+  int begin;
+  int end;
+  int pad;
+};
+
+struct FactorDev {
+  const float4* pa;
+  const float4* pb;
+  const float* pc;
+  MapDev map;
+  int n;
+  int tgt;
+  int src;
+  int item_begin;
+  int item_count;
+  int pad;
+};
+
+struct OverlapItem {
+  const float4* pa;
+  MapDev map;
+  double T[12];
+  unsigned n;
+  unsigned pad;
+};
+
+struct BuildSeg {
+  const float4* pa;
+  const float4* pb;
+  const float* pc;
+  unsigned long long offset;  // start of this map's points in the concatenated arrays
+  unsigned n;
+  unsigned pad;
+  double res;
+  double inv_res;
+};
+
+struct BuildOut {
+  VoxelRec* table;
+  unsigned long long* keys;
+  int* counts;
+  double* mean64;
+  double* cov64;
+  unsigned shift;
+  unsigned mask;
+  unsigned vbase;
+  unsigned pad;
+};
+
+constexpr int kFactorThreads = 256;
+constexpr int kLinAcc = 28;     // Q(6) P(9) Omega(6) b(6) error(1)
+constexpr int kPartialStride = 32;
+
+// ---- kernel launchers (return cudaError_t of the launch) ----
+cudaError_t launch_build_keys(const BuildSeg* segs, int m, unsigned max_n, unsigned long long* keys, unsigned* vals,
+                              int* range_err, cudaStream_t s);
+cudaError_t launch_build_heads(const BuildSeg* segs, int m, unsigned max_n, const unsigned long long* keys,
+                               unsigned* heads, cudaStream_t s);
+cudaError_t launch_build_counts(const BuildSeg* segs, int m, const unsigned* heads, const unsigned* vidx,
+                                unsigned* vcount, unsigned* vbase, cudaStream_t s);
+cudaError_t launch_build_accumulate(const BuildSeg* segs, const BuildOut* outs, int m, unsigned max_n,
+                                    const unsigned long long* keys, const unsigned* vals, const unsigned* heads,
+                                    const unsigned* vidx, cudaStream_t s);
+cudaError_t launch_lookup(MapDev map, const double* pts, size_t n, unsigned long long* keys_out, cudaStream_t s);
+cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsigned long long* hits, cudaStream_t s);
+cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkItem* items, int num_items,
+                          const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
+                          int* out_inl, cudaStream_t s);
+cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s);
+
+}  // namespace vgicp
+
+struct vgicp_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint64_t launches = 0;
+  // growable device scratch and pinned host staging
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+};
+
+struct vgicp_cloud_s {
+  vgicp_ctx ctx = nullptr;
+  size_t n = 0;
+  bool has_cov = false;
+  void* block = nullptr;  // single allocation holding pa | pb | pc
+  float4* pa = nullptr;
+  float4* pb = nullptr;
+  float* pc = nullptr;
+  std::atomic<int> refs{1};
+};
+
+struct vgicp_map_s {
+  vgicp_ctx ctx = nullptr;
+  double res = 1.0;
+  double inv_res = 1.0;
+  size_t voxels = 0;
+  size_t total_points = 0;
+  unsigned capacity = 0;
+  unsigned shift = 0;
+  void* block = nullptr;  // table | keys | counts | mean64 | cov64
+  vgicp::VoxelRec* table = nullptr;
+  unsigned long long* keys = nullptr;
+  int* counts = nullptr;
+  double* mean64 = nullptr;
+  double* cov64 = nullptr;
+  std::atomic<int> refs{1};
+  vgicp::MapDev dev() const {
+    return vgicp::MapDev{table, cov64, res, inv_res, shift, capacity - 1};
+  }
+};
+
+struct vgicp_graph_s {
+  vgicp_ctx ctx = nullptr;
+  int num_factors = 0;
+  int num_poses = 0;
+  int num_items = 0;
+  uint64_t num_points = 0;
+  void* block = nullptr;  // factors | items | partials | part_inl | counters | poses | out | out_inl | err
+  vgicp::FactorDev* d_factors = nullptr;
+  vgicp::WorkItem* d_items = nullptr;
+  double* d_partials = nullptr;
+  int* d_part_inl = nullptr;
+  unsigned* d_counters = nullptr;
+  double* d_poses = nullptr;
+  double* d_out = nullptr;
+  int* d_out_inl = nullptr;
+  double* d_err = nullptr;
+  std::vector<vgicp_cloud> clouds;
+  std::vector<vgicp_map> maps;
+};

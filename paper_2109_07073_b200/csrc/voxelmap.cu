@@ -1,0 +1,226 @@
+// Gaussian voxel map build, lookup and overlap kernels (sm_100a).
+//
+// Build (GaussianVoxelMap ctor, voxelmap.cpp:65-104), batched over m maps per call:
+//   K1 build_keys       fp64 transform-free key per point (exact floor(p/r), ±2^20 check)
+//   (CUB)               stable segmented radix sort of (key, point index) per map
+//   K2 build_heads      run heads of equal keys
+//   (CUB)               exclusive scan of heads -> compact voxel ids (ascending key order)
+//   K3 build_counts     voxels per map
+//   K4 build_accumulate one thread per voxel: Kahan fp64 sums over the voxel's points in input
+//                       order (exactly the reference's per-shard order, voxelmap.cpp:87-94),
+//                       finalize (voxelmap.cpp:34-40), atomicCAS insert into the open-addressing
+//                       table and write the fp32 voxel-local hot record + fp64 cold statistics.
+// Sorting instead of float atomics makes the statistics deterministic and bit-identical to the
+// reference's Kahan merge; the hash table itself is built with 64-bit atomicCAS.
+#include "internal.h"
+
+namespace vgicp {
+
+__global__ void build_keys_kernel(const BuildSeg* __restrict__ segs, unsigned long long* __restrict__ keys,
+                                  unsigned* __restrict__ vals, int* __restrict__ range_err) {
+  const BuildSeg s = segs[blockIdx.y];
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += gridDim.x * blockDim.x) {
+    const float4 a = __ldg(s.pa + i);
+    unsigned long long key;
+    double c0, c1, c2;
+    if (!voxel_key(a.x, a.y, a.z, s.res, s.inv_res, key, c0, c1, c2)) {
+      atomicOr(&range_err[blockIdx.y], 1);
+      key = 0;
+    }
+    keys[s.offset + i] = key;
+    vals[s.offset + i] = i;
+  }
+}
+
+__global__ void build_heads_kernel(const BuildSeg* __restrict__ segs, const unsigned long long* __restrict__ keys,
+                                   unsigned* __restrict__ heads) {
+  const BuildSeg s = segs[blockIdx.y];
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += gridDim.x * blockDim.x) {
+    const unsigned long long o = s.offset + i;
+    heads[o] = (i == 0 || keys[o] != keys[o - 1]) ? 1u : 0u;
+  }
+}
+
+__global__ void build_counts_kernel(const BuildSeg* __restrict__ segs, int m, const unsigned* __restrict__ heads,
+                                    const unsigned* __restrict__ vidx, unsigned* __restrict__ vcount,
+                                    unsigned* __restrict__ vbase) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const BuildSeg s = segs[k];
+  if (s.n == 0) {
+    vcount[k] = 0;
+    vbase[k] = 0;
+    return;
+  }
+  const unsigned long long last = s.offset + s.n - 1;
+  vbase[k] = vidx[s.offset];
+  vcount[k] = vidx[last] + heads[last] - vidx[s.offset];
+}
+
+__device__ __forceinline__ void kahan_add(double& sum, double& comp, double value) {  // parallel.hpp:106-111
+  const double y = __dsub_rn(value, comp);
+  const double t = __dadd_rn(sum, y);
+  comp = __dsub_rn(__dsub_rn(t, sum), y);
+  sum = t;
+}
+
+__global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const BuildOut* __restrict__ outs,
+                                        const unsigned long long* __restrict__ keys,
+                                        const unsigned* __restrict__ vals, const unsigned* __restrict__ heads,
+                                        const unsigned* __restrict__ vidx) {
+  const BuildSeg s = segs[blockIdx.y];
+  const BuildOut o = outs[blockIdx.y];
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += gridDim.x * blockDim.x) {
+    const unsigned long long g = s.offset + i;
+    if (!heads[g]) continue;
+    const unsigned long long key = keys[g];
+    const unsigned v = vidx[g] - o.vbase;
+    // VoxelAccumulator::add (voxelmap.cpp:28-32) with KahanSum, component-wise.
+    double ms[3] = {0, 0, 0}, mc[3] = {0, 0, 0};
+    double ss[6] = {0, 0, 0, 0, 0, 0}, sc[6] = {0, 0, 0, 0, 0, 0};  // xx xy xz yy yz zz
+    int count = 0;
+    for (unsigned j = i; j < s.n && (j == i || !heads[s.offset + j]); ++j) {
+      const unsigned p = vals[s.offset + j];
+      const float4 a = __ldg(s.pa + p);
+      const float4 b = __ldg(s.pb + p);
+      const float czz = __ldg(s.pc + p);
+      const double m0 = a.x, m1 = a.y, m2 = a.z;
+      kahan_add(ms[0], mc[0], m0);
+      kahan_add(ms[1], mc[1], m1);
+      kahan_add(ms[2], mc[2], m2);
+      kahan_add(ss[0], sc[0], __dadd_rn((double)a.w, __dmul_rn(m0, m0)));
+      kahan_add(ss[1], sc[1], __dadd_rn((double)b.x, __dmul_rn(m0, m1)));
+      kahan_add(ss[2], sc[2], __dadd_rn((double)b.y, __dmul_rn(m0, m2)));
+      kahan_add(ss[3], sc[3], __dadd_rn((double)b.z, __dmul_rn(m1, m1)));
+      kahan_add(ss[4], sc[4], __dadd_rn((double)b.w, __dmul_rn(m1, m2)));
+      kahan_add(ss[5], sc[5], __dadd_rn((double)czz, __dmul_rn(m2, m2)));
+      ++count;
+    }
+    // finalize (voxelmap.cpp:34-40)
+    const double cnt = static_cast<double>(count);
+    const double mean[3] = {__ddiv_rn(ms[0], cnt), __ddiv_rn(ms[1], cnt), __ddiv_rn(ms[2], cnt)};
+    double cov[6];
+    cov[0] = __dsub_rn(__ddiv_rn(ss[0], cnt), __dmul_rn(mean[0], mean[0]));
+    cov[1] = __dsub_rn(__ddiv_rn(ss[1], cnt), __dmul_rn(mean[0], mean[1]));
+    cov[2] = __dsub_rn(__ddiv_rn(ss[2], cnt), __dmul_rn(mean[0], mean[2]));
+    cov[3] = __dsub_rn(__ddiv_rn(ss[3], cnt), __dmul_rn(mean[1], mean[1]));
+    cov[4] = __dsub_rn(__ddiv_rn(ss[4], cnt), __dmul_rn(mean[1], mean[2]));
+    cov[5] = __dsub_rn(__ddiv_rn(ss[5], cnt), __dmul_rn(mean[2], mean[2]));
+    // cold fp64 statistics (ascending key order)
+    o.keys[v] = key;
+    o.counts[v] = count;
+    o.mean64[3 * v + 0] = mean[0];
+    o.mean64[3 * v + 1] = mean[1];
+    o.mean64[3 * v + 2] = mean[2];
+    double* c9 = o.cov64 + 9 * v;
+    c9[0] = cov[0], c9[1] = cov[1], c9[2] = cov[2];
+    c9[3] = cov[1], c9[4] = cov[3], c9[5] = cov[4];
+    c9[6] = cov[2], c9[7] = cov[4], c9[8] = cov[5];
+    // hot record: statistics relative to the voxel's lower corner, fp32
+    const double corner0 = __dmul_rn(key_coord(key, 0), s.res);
+    const double corner1 = __dmul_rn(key_coord(key, 1), s.res);
+    const double corner2 = __dmul_rn(key_coord(key, 2), s.res);
+    unsigned slot = hash_slot(key, o.shift);
+    while (atomicCAS(&o.table[slot].key, kEmptyKey, key) != kEmptyKey) slot = (slot + 1) & o.mask;
+    VoxelRec* r = o.table + slot;
+    r->mx = static_cast<float>(__dsub_rn(mean[0], corner0));
+    r->my = static_cast<float>(__dsub_rn(mean[1], corner1));
+    r->mz = static_cast<float>(__dsub_rn(mean[2], corner2));
+    r->cxx = static_cast<float>(cov[0]);
+    r->cxy = static_cast<float>(cov[1]);
+    r->cxz = static_cast<float>(cov[2]);
+    r->cyy = static_cast<float>(cov[3]);
+    r->cyz = static_cast<float>(cov[4]);
+    r->czz = static_cast<float>(cov[5]);
+    r->vid = static_cast<int>(v);
+  }
+}
+
+__global__ void lookup_kernel(MapDev map, const double* __restrict__ pts, size_t n,
+                              unsigned long long* __restrict__ keys_out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned long long key;
+    double c0, c1, c2;
+    unsigned long long out = kEmptyKey;
+    if (voxel_key(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], map.res, map.inv_res, key, c0, c1, c2)) {
+      if (probe_hit(map.table, map.shift, map.mask, key)) out = key;
+    }
+    keys_out[i] = out;
+  }
+}
+
+// overlap_rate (voxelmap.cpp:119-135), batched: blockIdx.y walks (cloud, pose, map) items,
+// hits are integer-exact (warp-aggregated 64-bit atomics), so the result is exactly hits / N.
+__global__ void __launch_bounds__(256) overlap_kernel(const OverlapItem* __restrict__ items, int m,
+                                                      unsigned long long* __restrict__ hits) {
+  for (int k = blockIdx.y; k < m; k += gridDim.y) {
+    const OverlapItem& it = items[k];
+    const unsigned n = it.n;
+    if (blockIdx.x * blockDim.x >= n) continue;
+    double T[12];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) T[q] = it.T[q];
+    const MapDev map = it.map;
+    const float4* __restrict__ pa = it.pa;
+    unsigned count = 0;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      const float4 a = __ldg(pa + i);
+      double q0, q1, q2;
+      apply_pose_rn(T, a.x, a.y, a.z, q0, q1, q2);
+      unsigned long long key;
+      double c0, c1, c2;
+      if (voxel_key(q0, q1, q2, map.res, map.inv_res, key, c0, c1, c2) &&
+          probe_hit(map.table, map.shift, map.mask, key))
+        ++count;
+    }
+    count = __reduce_add_sync(0xffffffffu, count);
+    if ((threadIdx.x & 31) == 0 && count) atomicAdd(&hits[k], static_cast<unsigned long long>(count));
+  }
+}
+
+namespace {
+unsigned grid_for(unsigned n, unsigned threads, unsigned cap) {
+  unsigned g = (n + threads - 1) / threads;
+  if (g == 0) g = 1;
+  return g < cap ? g : cap;
+}
+}  // namespace
+
+cudaError_t launch_build_keys(const BuildSeg* segs, int m, unsigned max_n, unsigned long long* keys, unsigned* vals,
+                              int* range_err, cudaStream_t s) {
+  build_keys_kernel<<<dim3(grid_for(max_n, 256, 4096), m), 256, 0, s>>>(segs, keys, vals, range_err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_heads(const BuildSeg* segs, int m, unsigned max_n, const unsigned long long* keys,
+                               unsigned* heads, cudaStream_t s) {
+  build_heads_kernel<<<dim3(grid_for(max_n, 256, 4096), m), 256, 0, s>>>(segs, keys, heads);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_counts(const BuildSeg* segs, int m, const unsigned* heads, const unsigned* vidx,
+                                unsigned* vcount, unsigned* vbase, cudaStream_t s) {
+  build_counts_kernel<<<(m + 127) / 128, 128, 0, s>>>(segs, m, heads, vidx, vcount, vbase);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_accumulate(const BuildSeg* segs, const BuildOut* outs, int m, unsigned max_n,
+                                    const unsigned long long* keys, const unsigned* vals, const unsigned* heads,
+                                    const unsigned* vidx, cudaStream_t s) {
+  build_accumulate_kernel<<<dim3(grid_for(max_n, 128, 4096), m), 128, 0, s>>>(segs, outs, keys, vals, heads, vidx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lookup(MapDev map, const double* pts, size_t n, unsigned long long* keys_out, cudaStream_t s) {
+  lookup_kernel<<<grid_for(static_cast<unsigned>(n < (1u << 30) ? n : (1u << 30)), 256, 4096), 256, 0, s>>>(
+      map, pts, n, keys_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsigned long long* hits, cudaStream_t s) {
+  const unsigned gy = m < 65535 ? m : 65535;
+  overlap_kernel<<<dim3(grid_for(max_n, 256 * 4, 1024), gy), 256, 0, s>>>(items, m, hits);
+  return cudaGetLastError();
+}
+
+}  // namespace vgicp

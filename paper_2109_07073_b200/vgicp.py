@@ -1,0 +1,451 @@
+"""Python mirror of the reference's VGICP operator API over the C ABI (include/vgicp_b200.h).
+
+Names, argument meaning and error behaviour follow /root/reference/proj:
+  GaussianVoxelMap            include/vgicp/voxelmap.hpp:28-56   (ValueError ~ std::invalid_argument,
+  overlap_rate                include/vgicp/voxelmap.hpp:60-61    IndexError ~ std::out_of_range)
+  MatchingCostFactor          include/vgicp/factors.hpp:36-45
+  LinearizedFactor            include/vgicp/factors.hpp:19-29
+  linearize_matching_cost     include/vgicp/factors.hpp:76-77
+  evaluate_matching_cost      include/vgicp/factors.hpp:80-81
+  gicp_error                  include/vgicp/factors.hpp:62-70
+Batch entry points (FactorGraph.linearize / .evaluate, overlap_rates) issue one launch for all
+factors / probes — the integration point of linearize_all / total_error (optimizer.cpp:45-75).
+
+All compute runs in the sm_100a kernels of lib/libvgicp_b200.so; this module only marshals.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import FactorDesc, check
+
+__all__ = [
+    "Context",
+    "default_context",
+    "PointCloud",
+    "GaussianVoxelMap",
+    "overlap_rate",
+    "overlap_rates",
+    "MatchingCostFactor",
+    "LinearizedFactor",
+    "GicpErrorResult",
+    "linearize_matching_cost",
+    "evaluate_matching_cost",
+    "gicp_error",
+    "FactorGraph",
+    "as_pose12",
+    "cov6_from",
+]
+
+
+# ------------------------------------------------------------------------------------ helpers
+def as_pose12(T) -> np.ndarray:
+    """Pose as 12 doubles (row-major R, then t). Accepts 12-vectors, 4×4 / 3×4 matrices, (R, t)."""
+    if isinstance(T, tuple) and len(T) == 2:
+        R, t = T
+        return np.ascontiguousarray(np.concatenate([np.asarray(R, np.float64).reshape(9), np.asarray(t, np.float64).reshape(3)]))
+    a = np.asarray(T, dtype=np.float64)
+    if a.shape == (12,):
+        return np.ascontiguousarray(a)
+    if a.shape in ((4, 4), (3, 4)):
+        return np.ascontiguousarray(np.concatenate([a[:3, :3].reshape(9), a[:3, 3]]))
+    raise ValueError(f"cannot interpret pose of shape {a.shape}")
+
+
+def poses_array(poses) -> np.ndarray:
+    a = np.asarray(poses, dtype=np.float64)
+    if a.ndim == 2 and a.shape[1] == 12:
+        return np.ascontiguousarray(a)
+    return np.ascontiguousarray(np.stack([as_pose12(p) for p in poses]))
+
+
+def cov6_from(covs) -> np.ndarray:
+    """Six unique entries (xx, xy, xz, yy, yz, zz) as float32 from n×3×3, n×9 or n×6."""
+    c = np.asarray(covs)
+    if c.ndim == 3:
+        c = c.reshape(len(c), 9)
+    if c.shape[-1] == 9:
+        c = c[:, [0, 1, 2, 4, 5, 8]]
+    elif c.shape[-1] != 6:
+        raise ValueError("covariances must be n×3×3, n×9 or n×6")
+    return np.ascontiguousarray(c, dtype=np.float32)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+# ------------------------------------------------------------------------------------ context
+class Context:
+    """One CUDA device + stream (vgicp_ctx). Not reentrant, like the reference optimizer."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        lib = _lib.load()
+        h = C.c_void_p()
+        check(lib.vgicp_ctx_create(int(device), C.c_void_p(stream) if stream else None, C.byref(h)))
+        self._h = h
+        self.device = int(device)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(_lib.load().vgicp_ctx_stream(self._h, C.byref(s)))
+        return int(s.value or 0)
+
+    def synchronize(self) -> None:
+        check(_lib.load().vgicp_ctx_synchronize(self._h))
+
+    def launch_count(self) -> int:
+        n = C.c_uint64()
+        check(_lib.load().vgicp_ctx_launch_count(self._h, C.byref(n)))
+        return int(n.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.load().vgicp_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_DEFAULT: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _DEFAULT:
+        _DEFAULT[device] = Context(device)
+    return _DEFAULT[device]
+
+
+class _Handle:
+    _destroy = ""
+
+    def __init__(self, ctx: Context, h: C.c_void_p):
+        self.ctx = ctx
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            getattr(_lib.load(), self._destroy)(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------------------------ clouds
+class PointCloud(_Handle):
+    """Device-resident PointCloud (point_cloud.hpp:21-37): float32 means + 6 unique cov floats."""
+
+    _destroy = "vgicp_cloud_destroy"
+
+    def __init__(self, means, covariances=None, ctx: Context | None = None):
+        ctx = ctx or default_context()
+        m = np.ascontiguousarray(np.asarray(means, dtype=np.float32).reshape(-1, 3))
+        c = None if covariances is None else cov6_from(covariances)
+        if c is not None and len(c) != len(m):
+            raise ValueError("covariance count does not match point count")
+        h = C.c_void_p()
+        check(_lib.load().vgicp_cloud_upload(ctx.handle, _ptr(m), _ptr(c) if c is not None else None, len(m), C.byref(h)))
+        super().__init__(ctx, h)
+        self.means = m
+        self.cov6 = c
+
+    def size(self) -> int:
+        return len(self.means)
+
+    def __len__(self) -> int:
+        return self.size()
+
+    def empty(self) -> bool:
+        return self.size() == 0
+
+    def has_covariances(self) -> bool:
+        return self.cov6 is not None and self.size() > 0
+
+
+# ------------------------------------------------------------------------------------ voxel maps
+class GaussianVoxelMap(_Handle):
+    """GaussianVoxelMap(cloud, resolution) — voxelmap.cpp:65-104, built on the GPU."""
+
+    _destroy = "vgicp_voxelmap_destroy"
+
+    def __init__(self, cloud: PointCloud, resolution: float, _handle=None):
+        if _handle is None:
+            h = C.c_void_p()
+            check(_lib.load().vgicp_voxelmap_build(cloud.ctx.handle, cloud.handle, float(resolution), C.byref(h)))
+        else:
+            h = _handle
+        super().__init__(cloud.ctx, h)
+        self.cloud = cloud  # keeps the source alive for callers that re-derive stats
+        self._resolution = float(resolution)
+
+    @staticmethod
+    def build_batch(clouds: Sequence[PointCloud], resolutions) -> list["GaussianVoxelMap"]:
+        """Build m maps in one batched pass (all-or-nothing)."""
+        m = len(clouds)
+        if m == 0:
+            return []
+        ctx = clouds[0].ctx
+        res = np.ascontiguousarray(np.broadcast_to(np.asarray(resolutions, np.float64), (m,)))
+        hs = (C.c_void_p * m)(*[c.handle for c in clouds])
+        outs = (C.c_void_p * m)()
+        check(_lib.load().vgicp_voxelmap_build_batch(ctx.handle, hs, _ptr(res), m, outs))
+        return [GaussianVoxelMap(clouds[k], res[k], _handle=C.c_void_p(outs[k])) for k in range(m)]
+
+    def resolution(self) -> float:
+        return self._resolution
+
+    def size(self) -> int:
+        n = C.c_size_t()
+        check(_lib.load().vgicp_voxelmap_size(self._h, C.byref(n)))
+        return int(n.value)
+
+    def __len__(self) -> int:
+        return self.size()
+
+    def total_points(self) -> int:
+        n = C.c_size_t()
+        check(_lib.load().vgicp_voxelmap_total_points(self._h, C.byref(n)))
+        return int(n.value)
+
+    def export(self):
+        """voxels() in ascending key order: (keys u64[V], counts i32[V], means f64[V,3], covs f64[V,3,3])."""
+        v = self.size()
+        keys = np.zeros(v, np.uint64)
+        counts = np.zeros(v, np.int32)
+        means = np.zeros((v, 3))
+        covs = np.zeros((v, 9))
+        check(_lib.load().vgicp_voxelmap_export(self._h, _ptr(keys), _ptr(counts), _ptr(means), _ptr(covs)))
+        return keys, counts, means, covs.reshape(v, 3, 3)
+
+    def voxels(self) -> dict:
+        keys, counts, means, covs = self.export()
+        return {int(k): (means[i], covs[i], int(counts[i])) for i, k in enumerate(keys)}
+
+    def lookup(self, points) -> np.ndarray:
+        """Packed key of the voxel containing each point, or KEY_MISS (voxelmap.cpp:106-117)."""
+        p = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3))
+        out = np.zeros(len(p), np.uint64)
+        check(_lib.load().vgicp_voxelmap_lookup(self._h, _ptr(p), len(p), _ptr(out)))
+        return out
+
+    @staticmethod
+    def pack_key(resolution: float, point) -> int:
+        """voxel_coord + pack_key (voxelmap.cpp:45-63); IndexError beyond ±2^20 voxels."""
+        p = np.ascontiguousarray(np.asarray(point, dtype=np.float64).reshape(3))
+        k = C.c_uint64()
+        check(_lib.load().vgicp_voxel_key(float(resolution), _ptr(p), C.byref(k)))
+        return int(k.value)
+
+
+def overlap_rate(cloud: PointCloud, pose_rel, voxelmap: GaussianVoxelMap) -> float:
+    """Exact hits / N (voxelmap.cpp:119-135); ValueError on an empty cloud."""
+    T = as_pose12(pose_rel)
+    r = C.c_double()
+    check(_lib.load().vgicp_overlap_rate(cloud.ctx.handle, cloud.handle, _ptr(T), voxelmap.handle, C.byref(r)))
+    return r.value
+
+
+def overlap_hits(clouds, poses, maps) -> np.ndarray:
+    """Exact hit counts of m (cloud, pose, map) probes in one launch."""
+    maps = list(maps)
+    m = len(maps)
+    if isinstance(clouds, PointCloud):
+        clouds = [clouds] * m
+    clouds = list(clouds)
+    if len(clouds) != m:
+        raise ValueError("clouds and maps differ in length")
+    P = poses_array(poses)
+    if len(P) != m:
+        raise ValueError("poses and maps differ in length")
+    hits = np.zeros(m, np.uint64)
+    if m == 0:
+        return hits
+    ctx = maps[0].ctx
+    ch = (C.c_void_p * m)(*[c.handle for c in clouds])
+    mh = (C.c_void_p * m)(*[x.handle for x in maps])
+    check(_lib.load().vgicp_overlap_batch(ctx.handle, ch, _ptr(P), mh, m, _ptr(hits)))
+    return hits
+
+
+def overlap_rates(clouds, poses, maps) -> np.ndarray:
+    maps = list(maps)
+    hits = overlap_hits(clouds, poses, maps)
+    sizes = np.array([c.size() for c in ([clouds] * len(maps) if isinstance(clouds, PointCloud) else clouds)], np.float64)
+    return hits.astype(np.float64) / sizes
+
+
+# ------------------------------------------------------------------------------------ factors
+@dataclass
+class LinearizedFactor:
+    """LinearizedFactor (factors.hpp:19-29); b = -ΣJᵀΩe, gradient = -2[b_i; b_j]."""
+
+    i: int = -1
+    j: int = -1
+    H_ii: np.ndarray = field(default_factory=lambda: np.zeros((6, 6)))
+    H_ij: np.ndarray = field(default_factory=lambda: np.zeros((6, 6)))
+    H_jj: np.ndarray = field(default_factory=lambda: np.zeros((6, 6)))
+    b_i: np.ndarray = field(default_factory=lambda: np.zeros(6))
+    b_j: np.ndarray = field(default_factory=lambda: np.zeros(6))
+    error: float = 0.0
+    inliers: int = 0
+
+    @staticmethod
+    def from_raw(raw: np.ndarray, i: int, j: int, inliers: int) -> "LinearizedFactor":
+        return LinearizedFactor(
+            i=i, j=j, H_ii=raw[0:36].reshape(6, 6), H_ij=raw[36:72].reshape(6, 6), H_jj=raw[72:108].reshape(6, 6),
+            b_i=raw[108:114], b_j=raw[114:120], error=float(raw[120]), inliers=int(inliers),
+        )
+
+
+class MatchingCostFactor:
+    """MatchingCostFactor (factors.cpp:50-67): target owns the map, source supplies the points."""
+
+    def __init__(self, target_index: int, source_index: int, source_points: PointCloud, target_voxels: GaussianVoxelMap):
+        if target_index == source_index:
+            raise ValueError("matching cost factor requires distinct variables")
+        if source_points is None or source_points.empty():
+            raise ValueError("matching cost factor requires a nonempty source cloud")
+        if not source_points.has_covariances():
+            raise ValueError("matching cost factor requires source covariances")
+        if target_voxels is None or target_voxels.size() == 0:
+            raise ValueError("matching cost factor requires a nonempty target voxel map")
+        self.target_index = int(target_index)
+        self.source_index = int(source_index)
+        self.source_points = source_points
+        self.target_voxels = target_voxels
+
+    def desc(self) -> FactorDesc:
+        return FactorDesc(self.target_index, self.source_index, self.source_points.handle, self.target_voxels.handle)
+
+
+def linearize_matching_cost(factor: MatchingCostFactor, T_target, T_source) -> LinearizedFactor:
+    out = np.zeros(_lib.LINEARIZED_DOUBLES)
+    inl = C.c_int32()
+    d = factor.desc()
+    check(
+        _lib.load().vgicp_linearize_matching_cost(
+            factor.source_points.ctx.handle, C.byref(d), _ptr(as_pose12(T_target)), _ptr(as_pose12(T_source)), _ptr(out), C.byref(inl)
+        )
+    )
+    return LinearizedFactor.from_raw(out, factor.target_index, factor.source_index, inl.value)
+
+
+def evaluate_matching_cost(factor: MatchingCostFactor, T_target, T_source) -> tuple[float, int]:
+    err = C.c_double()
+    inl = C.c_int32()
+    d = factor.desc()
+    check(
+        _lib.load().vgicp_evaluate_matching_cost(
+            factor.source_points.ctx.handle, C.byref(d), _ptr(as_pose12(T_target)), _ptr(as_pose12(T_source)), C.byref(err), C.byref(inl)
+        )
+    )
+    return err.value, int(inl.value)
+
+
+@dataclass
+class GicpErrorResult:
+    """GicpErrorResult (factors.hpp:62-67)."""
+
+    error: float
+    residual: np.ndarray
+    information: np.ndarray
+    valid: bool
+
+
+def gicp_error(source_mean, source_cov, target_mean, target_cov, T, ctx: Context | None = None) -> GicpErrorResult:
+    ctx = ctx or default_context()
+    f = lambda a, n: np.ascontiguousarray(np.asarray(a, np.float64).reshape(n))  # noqa: E731
+    sm, sc, tm, tc = f(source_mean, 3), f(source_cov, 9), f(target_mean, 3), f(target_cov, 9)
+    err = C.c_double()
+    res = np.zeros(3)
+    info = np.zeros(9)
+    valid = C.c_int()
+    check(
+        _lib.load().vgicp_gicp_error(
+            ctx.handle, _ptr(sm), _ptr(sc), _ptr(tm), _ptr(tc), _ptr(as_pose12(T)), C.byref(err), _ptr(res), _ptr(info), C.byref(valid)
+        )
+    )
+    return GicpErrorResult(err.value, res, info.reshape(3, 3), bool(valid.value))
+
+
+class FactorGraph(_Handle):
+    """A fixed set of matching-cost factors linearized / evaluated in one launch per pass."""
+
+    _destroy = "vgicp_graph_destroy"
+
+    def __init__(self, factors: Iterable[MatchingCostFactor], num_poses: int, chunk: int = 0, ctx: Context | None = None):
+        self.factors = list(factors)
+        ctx = ctx or (self.factors[0].source_points.ctx if self.factors else default_context())
+        n = len(self.factors)
+        descs = (FactorDesc * max(n, 1))(*[f.desc() for f in self.factors])
+        h = C.c_void_p()
+        check(_lib.load().vgicp_graph_create(ctx.handle, descs, n, int(num_poses), int(chunk), C.byref(h)))
+        super().__init__(ctx, h)
+        self.num_poses = int(num_poses)
+        self._ij = np.array([[f.target_index, f.source_index] for f in self.factors], np.int64).reshape(-1, 2)
+
+    def num_factors(self) -> int:
+        return len(self.factors)
+
+    def num_points(self) -> int:
+        n = C.c_uint64()
+        check(_lib.load().vgicp_graph_num_points(self._h, C.byref(n)))
+        return int(n.value)
+
+    def linearize_raw(self, poses) -> tuple[np.ndarray, np.ndarray]:
+        P = poses_array(poses)
+        if len(P) != self.num_poses:
+            raise ValueError("pose count does not match the graph")
+        out = np.zeros((self.num_factors(), _lib.LINEARIZED_DOUBLES))
+        inl = np.zeros(self.num_factors(), np.int32)
+        check(_lib.load().vgicp_graph_linearize(self._h, _ptr(P), _ptr(out), _ptr(inl)))
+        return out, inl
+
+    def linearize(self, poses) -> list[LinearizedFactor]:
+        out, inl = self.linearize_raw(poses)
+        return [LinearizedFactor.from_raw(out[k], int(self._ij[k, 0]), int(self._ij[k, 1]), inl[k]) for k in range(len(out))]
+
+    def evaluate(self, poses) -> tuple[np.ndarray, np.ndarray]:
+        P = poses_array(poses)
+        if len(P) != self.num_poses:
+            raise ValueError("pose count does not match the graph")
+        err = np.zeros(self.num_factors())
+        inl = np.zeros(self.num_factors(), np.int32)
+        check(_lib.load().vgicp_graph_evaluate(self._h, _ptr(P), _ptr(err), _ptr(inl)))
+        return err, inl
+
+    def total_error(self, poses) -> float:
+        """Σ factor errors in factor order (total_error, optimizer.cpp:66-75, matching part)."""
+        err, _ = self.evaluate(poses)
+        s = 0.0
+        for e in err:
+            s += float(e)
+        return s
+
+    # device-resident variants (pointers are device addresses, e.g. torch tensor data_ptr())
+    def linearize_device(self, d_poses: int, d_out: int, d_inliers: int) -> None:
+        check(_lib.load().vgicp_graph_linearize_device(self._h, C.c_void_p(d_poses), C.c_void_p(d_out), C.c_void_p(d_inliers)))
+
+    def evaluate_device(self, d_poses: int, d_errors: int, d_inliers: int) -> None:
+        check(_lib.load().vgicp_graph_evaluate_device(self._h, C.c_void_p(d_poses), C.c_void_p(d_errors), C.c_void_p(d_inliers)))

@@ -1,0 +1,385 @@
+"""GPU (sm_100a) parity against the CPU oracle, through the C ABI (paper_2109_07073_b200.vgicp).
+
+Bar:
+  - voxel keys, per-voxel counts, lookups, overlap hit counts, per-factor inlier counts: bit-exact;
+  - voxel statistics (fp64 Kahan build): bit-exact;
+  - H_ii, H_ij, H_jj, b_i, b_j: ‖Δ‖_F / max(1, ‖H_ii,ref‖_F) <= H_TOL (float32 per-point math vs
+    the reference's double; normalisation of test_reference.cpp:85-91);
+  - error: relative <= ERR_TOL (plane-regularised covariances, point_cloud.cpp:78); DEGENERATE_TOL
+    for near-singular combined covariances, where fp32 Omega loses ~cond(M)·eps.
+Inputs follow the GPU contract (float32 means and covariances); the oracle receives the same values.
+"""
+import numpy as np
+import pytest
+
+import oracle_ctypes as O
+from helpers import contract_inputs, lin_dict, rel_block_error
+
+V = pytest.importorskip("paper_2109_07073_b200")
+
+pytestmark = pytest.mark.gpu
+
+H_TOL = 1e-5
+ERR_TOL = 1e-5
+# near-singular combined covariances (zero or rank-deficient inputs): fp32 Omega loses ~cond(M)·eps
+DEGENERATE_TOL = 1e-4
+MISS = np.iinfo(np.uint64).max
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return V.default_context(0)
+
+
+def gpu_cloud(ctx, means, covs=None):
+    m, c9, c6 = contract_inputs(means, covs)
+    return V.PointCloud(m, c6, ctx), m, c9
+
+
+def assert_map_parity(gmap: "V.GaussianVoxelMap", omap: O.OracleMap):
+    gk, gc, gm, gv = gmap.export()
+    ok, oc, om, ov = omap.export()
+    assert gmap.size() == omap.size()
+    assert np.array_equal(gk, ok)
+    assert np.array_equal(gc, oc)
+    assert np.array_equal(gm, om), np.max(np.abs(gm - om))
+    assert np.array_equal(gv, ov), np.max(np.abs(gv - ov))
+
+
+# ------------------------------------------------------------------------------ voxel map
+def test_single_point_voxel(ctx):  # test_voxelmap.cpp:23-34
+    cloud, m, c9 = gpu_cloud(ctx, [[0.2, 0.3, 0.4]], np.diag([1.0, 1.0, 1e-3])[None])
+    g = V.GaussianVoxelMap(cloud, 1.0)
+    assert g.size() == 1 and g.total_points() == 1
+    keys, counts, means, covs = g.export()
+    assert counts[0] == 1 and np.array_equal(means[0], m[0])
+    assert np.linalg.norm(covs[0] - c9[0].reshape(3, 3)) < 1e-15
+    assert g.lookup(m)[0] == keys[0]
+
+
+def test_two_point_voxel(ctx):  # test_voxelmap.cpp:36-48
+    cloud, m, c9 = gpu_cloud(ctx, [[0.1, 0.1, 0.1], [0.3, 0.1, 0.1]], O.unit_covariances(2))
+    g = V.GaussianVoxelMap(cloud, 1.0)
+    assert_map_parity(g, O.OracleMap(m, c9, 1.0))
+    _, counts, means, covs = g.export()
+    assert counts[0] == 2
+    assert np.linalg.norm(means[0] - m.mean(axis=0)) < 1e-9
+
+
+@pytest.mark.parametrize("seed,n,scale,res", [(10, 1000, 10.0, 1.0), (11, 5000, 20.0, 0.7), (13, 2000, 10.0, 0.5), (81, 5000, 20.0, 0.8)])
+def test_voxelmap_bit_exact(ctx, seed, n, scale, res):  # test_voxelmap.cpp:50-136, test_reference.cpp:43-57
+    rng = O.Rng(seed)
+    means, covs = rng.gaussian_cloud(n, scale)
+    cloud, m, c9 = gpu_cloud(ctx, means, covs)
+    g = V.GaussianVoxelMap(cloud, res)
+    omap = O.OracleMap(m, c9, res, threads=4, deterministic=True)
+    assert_map_parity(g, omap)
+    assert g.total_points() == n
+    _, counts, _, _ = g.export()
+    assert counts.sum() == n
+    # brute-force bucketing (oracles.hpp:45-61)
+    assert g.size() == len(O.brute_force_buckets(m, res))
+
+
+def test_voxelmap_order_independence(ctx):  # test_voxelmap.cpp:95-120
+    rng = O.Rng(12)
+    pts = np.array([rng.vector(15.0) for _ in range(3000)])
+    perm = rng.shuffle(3000).astype(np.int64)
+    a, _, _ = gpu_cloud(ctx, pts, O.unit_covariances(3000))
+    b, _, _ = gpu_cloud(ctx, pts[perm], O.unit_covariances(3000))
+    ka, ca, ma, va = V.GaussianVoxelMap(a, 1.0).export()
+    kb, cb, mb, vb = V.GaussianVoxelMap(b, 1.0).export()
+    assert np.array_equal(ka, kb) and np.array_equal(ca, cb)
+    assert np.max(np.abs(ma - mb)) < 1e-9 and np.max(np.abs(va - vb)) < 1e-9
+
+
+def test_voxelmap_batch_equals_single(ctx):
+    rng = O.Rng(90)
+    clouds, singles = [], []
+    for k in range(5):
+        means, covs = rng.gaussian_cloud(500 + 300 * k, 10.0)
+        c, m, c9 = gpu_cloud(ctx, means, covs)
+        clouds.append(c)
+    res = [0.5, 1.0, 2.0, 0.7, 1.3]
+    batch = V.GaussianVoxelMap.build_batch(clouds, res)
+    for c, r, b in zip(clouds, res, batch):
+        s = V.GaussianVoxelMap(c, r)
+        for x, y in zip(s.export(), b.export()):
+            assert np.array_equal(x, y)
+
+
+def test_floor_boundary_lookup(ctx):  # test_voxelmap.cpp:71-82
+    cloud, _, _ = gpu_cloud(ctx, [[0.5, 0.5, 0.5]], O.unit_covariances(1))
+    g = V.GaussianVoxelMap(cloud, 1.0)
+    got = g.lookup([[0.9, 0.9, 0.9], [5.0, 5.0, 5.0], [1.0, 0.5, 0.5], [0.0, 0.0, 0.0], [1.0 - 1e-12, 0.5, 0.5], [np.nan, 0, 0], [3e6, 0, 0]])
+    assert got[0] != MISS and got[1] == MISS and got[2] == MISS and got[3] != MISS and got[4] != MISS
+    assert got[5] == MISS and got[6] == MISS
+
+
+@pytest.mark.parametrize("res", [0.3, 0.25, 1.0])
+def test_lookup_matches_oracle_near_faces(ctx, res):
+    """Points and probes within a few ulps of voxel faces (and exactly on them): the exact-floor
+    fast path and its IEEE-division fallback must agree with floor(p / r) bit for bit."""
+    rng = np.random.default_rng(5)
+    base = rng.integers(-50, 50, size=(2000, 3)).astype(np.float64) * res
+    b32 = base.astype(np.float32)
+    ulp32 = np.spacing(np.abs(b32) + np.float32(res)).astype(np.float32)
+    pts = (b32 + rng.integers(-3, 4, size=(2000, 3)).astype(np.float32) * ulp32).astype(np.float64)
+    pts = np.concatenate([pts, b32.astype(np.float64)])
+    cloud, m, c9 = gpu_cloud(ctx, pts, O.unit_covariances(len(pts)))
+    g = V.GaussianVoxelMap(cloud, res)
+    omap = O.OracleMap(m, c9, res)
+    assert_map_parity(g, omap)
+    eps = rng.integers(-4, 5, size=base.shape) * np.spacing(np.abs(base) + res)
+    probes = np.concatenate([pts, base, base + eps, base + res * 0.5, -base + eps])
+    assert np.array_equal(g.lookup(probes), omap.lookup(probes))
+
+
+def test_range_and_invalid(ctx):  # test_voxelmap.cpp:185-188, voxelmap.cpp:67-72
+    cloud, _, _ = gpu_cloud(ctx, [[2.0e6, 0, 0]], O.unit_covariances(1))
+    with pytest.raises(IndexError):
+        V.GaussianVoxelMap(cloud, 1.0)
+    ok, _, _ = gpu_cloud(ctx, [[0.0, 0, 0]], O.unit_covariances(1))
+    with pytest.raises(ValueError):
+        V.GaussianVoxelMap(ok, 0.0)
+    raw = V.PointCloud(np.zeros((3, 3), np.float32), None, ctx)
+    with pytest.raises(ValueError):
+        V.GaussianVoxelMap(raw, 1.0)
+    empty = V.PointCloud(np.zeros((0, 3), np.float32), None, ctx)
+    g = V.GaussianVoxelMap(ok, 1.0)
+    with pytest.raises(ValueError):
+        V.overlap_rate(empty, O.IDENTITY, g)
+
+
+# ------------------------------------------------------------------------------ overlap
+def test_overlap_self_and_far(ctx):  # test_voxelmap.cpp:138-149
+    rng = O.Rng(14)
+    pts = np.array([rng.vector(10.0) for _ in range(2000)])
+    cloud, _, _ = gpu_cloud(ctx, pts, O.unit_covariances(2000))
+    g = V.GaussianVoxelMap(cloud, 0.5)
+    assert V.overlap_rate(cloud, O.IDENTITY, g) == 1.0
+    assert V.overlap_rate(cloud, O.pose(t=(500, 0, 0)), g) == 0.0
+
+
+def test_overlap_20_scenes_exact(ctx):  # test_voxelmap.cpp:151-169
+    from test_oracle_kats import reference_overlap_scenes
+
+    for map_pts, cloud_pts, res, rel in reference_overlap_scenes():
+        mc, mm, mc9 = gpu_cloud(ctx, map_pts, O.unit_covariances(len(map_pts)))
+        qc, qm, _ = gpu_cloud(ctx, cloud_pts)
+        g = V.GaussianVoxelMap(mc, res)
+        got = V.overlap_rate(qc, rel, g)
+        expected = O.brute_force_overlap_count(qm, rel, mm, res)
+        assert got == expected / len(qm)
+        assert got == O.overlap_rate(qm, rel, O.OracleMap(mm, mc9, res))
+
+
+def test_overlap_37_of_100(ctx):  # test_voxelmap.cpp:171-183
+    map_pts = [[x + 0.5, y + 0.5, 0.5] for x in range(5) for y in range(5)]
+    cloud = [[0.5 + 0.1 * (i % 5), 0.5 + (i // 5 % 5), 0.5] for i in range(37)] + [[100.0 + i, 0.0, 0.0] for i in range(63)]
+    mc, _, _ = gpu_cloud(ctx, map_pts, O.unit_covariances(25))
+    qc, _, _ = gpu_cloud(ctx, cloud)
+    assert V.overlap_hits(qc, [O.IDENTITY], [V.GaussianVoxelMap(mc, 1.0)])[0] == 37
+
+
+def test_overlap_batch_matches_serial(ctx):  # test_reference.cpp:59-69
+    rng = O.Rng(82)
+    mcl, mcov = rng.gaussian_cloud(3000, 15.0)
+    qcl, _ = rng.gaussian_cloud(3000, 15.0)
+    mc, mm, mc9 = gpu_cloud(ctx, mcl, mcov)
+    qc, qm, _ = gpu_cloud(ctx, qcl)
+    g = V.GaussianVoxelMap(mc, 0.5)
+    omap = O.OracleMap(mm, mc9, 0.5)
+    rels = [rng.random_pose(0.3, 3.0) for _ in range(10)]
+    rates = V.overlap_rates(qc, rels, [g] * 10)
+    for rel, r in zip(rels, rates):
+        assert r == O.overlap_rate(qm, rel, omap, serial=True)
+
+
+# ------------------------------------------------------------------------------ factors
+def factor_case(ctx, sm, sc, tm, tc, res):
+    src, smm, sc9 = gpu_cloud(ctx, sm, sc)
+    tgt, tmm, tc9 = gpu_cloud(ctx, tm, tc)
+    g = V.GaussianVoxelMap(tgt, res)
+    omap = O.OracleMap(tmm, tc9, res)
+    return V.MatchingCostFactor(0, 1, src, g), smm, sc9, omap
+
+
+def check_factor(fac, smm, sc9, omap, Tt, Ts, h_tol=H_TOL, e_tol=ERR_TOL):
+    lin = V.linearize_matching_cost(fac, Tt, Ts)
+    ref = O.linearize(smm, sc9, omap, Tt, Ts)
+    assert lin.inliers == ref["inliers"]
+    errs = rel_block_error(lin_dict(lin), ref)
+    for k, v in errs.items():
+        assert v <= (e_tol if k == "error" else h_tol), (k, v, errs)
+    err, inl = V.evaluate_matching_cost(fac, Tt, Ts)
+    ref_err, ref_inl = O.evaluate(smm, sc9, omap, Tt, Ts)
+    assert inl == ref_inl
+    assert abs(err - ref_err) <= e_tol * max(1.0, abs(ref_err))
+    assert np.array_equal(lin.H_ii, lin.H_ii.T) and np.array_equal(lin.H_jj, lin.H_jj.T)
+    return lin, ref, errs
+
+
+def test_linearize_reference_scene_83(ctx):  # test_reference.cpp:71-93
+    rng = O.Rng(83)
+    tm, tc = rng.gaussian_cloud(4000, 12.0)
+    sm, sc = rng.gaussian_cloud(4000, 12.0)
+    fac, smm, sc9, omap = factor_case(ctx, sm, sc, tm, tc, 1.0)
+    Ti = rng.random_pose(0.1, 1.0)
+    Tj = rng.random_pose(0.1, 1.0)
+    check_factor(fac, smm, sc9, omap, Ti, Tj)
+
+
+@pytest.mark.parametrize("seed,points", [(33, 200), (34, 300), (37, 400), (38, 3000)])
+def test_linearize_make_scene(ctx, seed, points):  # test_factors.cpp:33-68 scenes
+    rng = O.Rng(seed)
+    s = rng.make_scene(points, 1.0)
+    fac, smm, sc9, omap = factor_case(ctx, s["source_means"], s["source_covs"], s["target_means"], s["target_covs"], 1.0)
+    lin, ref, _ = check_factor(fac, smm, sc9, omap, s["T_target"], s["T_source"])
+    assert lin.inliers > 0.75 * points
+
+
+def test_gauge_invariance(ctx):  # test_factors.cpp:243-253
+    rng = O.Rng(37)
+    s = rng.make_scene(400, 1.0)
+    fac, smm, sc9, omap = factor_case(ctx, s["source_means"], s["source_covs"], s["target_means"], s["target_covs"], 1.0)
+    base, _ = V.evaluate_matching_cost(fac, s["T_target"], s["T_source"])
+    for _ in range(10):
+        G = rng.random_pose(1.0, 50.0)
+        e, _ = V.evaluate_matching_cost(fac, O.compose(G, s["T_target"]), O.compose(G, s["T_source"]))
+        assert abs(e - base) < 1e-5 * max(1.0, base)
+
+
+def test_disjoint_zero_factor(ctx):  # test_factors.cpp:224-241
+    rng = O.Rng(36)
+    sm, sc, tm, tc = [], [], [], []
+    for _ in range(50):
+        sm.append(rng.vector(2.0))
+        sc.append(rng.plane_covariance())
+        tm.append(rng.vector(2.0) + [1000, 0, 0])
+        tc.append(rng.plane_covariance())
+    fac, _, _, _ = factor_case(ctx, sm, sc, tm, tc, 1.0)
+    lin = V.linearize_matching_cost(fac, O.IDENTITY, O.IDENTITY)
+    assert lin.inliers == 0 and lin.error == 0.0
+    assert not np.any(lin.H_ii) and not np.any(lin.H_ij) and not np.any(lin.H_jj)
+    assert not np.any(lin.b_i) and not np.any(lin.b_j)
+
+
+def test_perfect_alignment(ctx):  # test_factors.cpp:122-162
+    rng = O.Rng(32)
+    means = np.array([[20.0 * (i % 10) + 5.0, 20.0 * (i // 10) + 5.0, 5.0] for i in range(100)])
+    covs = np.array([rng.plane_covariance() for _ in range(100)])
+    fac, smm, sc9, omap = factor_case(ctx, means, covs, means, covs, 10.0)
+    T = rng.random_pose(0.5, 3.0)
+    lin = V.linearize_matching_cost(fac, T, T)
+    assert lin.inliers == 100
+    assert lin.error < 1e-6
+    H = np.block([[lin.H_ii, lin.H_ij], [lin.H_ij.T, lin.H_jj]])
+    assert np.linalg.eigvalsh(H).min() > -1e-6 * max(1.0, np.abs(H).max())
+
+
+def test_singular_combined_covariance_skipped(ctx):  # factors.cpp:108-110, :39-41
+    """Zero covariances make M singular: the fp64 LDLT path must skip exactly like the oracle."""
+    rng = O.Rng(44)
+    n = 300
+    sm = np.array([rng.vector(3.0) for _ in range(n)])
+    tm = sm + 0.01 * np.array([rng.vector(1.0) for _ in range(n)])
+    sc = np.zeros((n, 3, 3))
+    tc = np.zeros((n, 3, 3))
+    sc[: n // 2] = [rng.plane_covariance() for _ in range(n // 2)]  # half the points regular
+    tc[::3] = [rng.plane_covariance() for _ in range(len(tc[::3]))]
+    fac, smm, sc9, omap = factor_case(ctx, sm, sc, tm, tc, 0.5)
+    T = O.IDENTITY
+    lin, ref, _ = check_factor(fac, smm, sc9, omap, T, T, h_tol=1e-5, e_tol=DEGENERATE_TOL)
+    assert 0 < ref["inliers"] < n
+
+
+def test_gicp_error_kat(ctx):  # test_factors.cpp:92-120 (fp64 kernel: bit-exact vs oracle)
+    mean = np.array([1.0, 2.0, 3.0])
+    half = 0.5 * np.eye(3)
+    r = V.gicp_error(mean, half, mean, half, O.IDENTITY)
+    assert r.error == 0.0 and r.valid
+    r = V.gicp_error(mean, half, mean + [1, 0, 0], half, O.IDENTITY)
+    assert r.error == pytest.approx(1.0, rel=1e-12)
+    assert np.linalg.norm(r.information - np.eye(3)) < 1e-12
+    rng = O.Rng(31)
+    for _ in range(20):
+        sm, tm = rng.vector(5.0), rng.vector(5.0)
+        sc, tc = rng.plane_covariance(), rng.plane_covariance()
+        T = rng.random_pose(0.5, 2.0)
+        g = V.gicp_error(sm, sc, tm, tc, T)
+        e, res, info, valid = O.gicp_error(sm, sc, tm, tc, T)
+        assert g.valid == valid and g.error == e
+        assert np.array_equal(g.residual, res) and np.array_equal(g.information, info)
+    bad = V.gicp_error(mean, np.zeros((3, 3)), mean + 1, np.zeros((3, 3)), O.IDENTITY)
+    assert not bad.valid and bad.error == 0.0
+
+
+def test_factor_validation(ctx):  # factors.cpp:57-66
+    rng = O.Rng(50)
+    means, covs = rng.gaussian_cloud(100, 5.0)
+    c, _, _ = gpu_cloud(ctx, means, covs)
+    g = V.GaussianVoxelMap(c, 1.0)
+    with pytest.raises(ValueError):
+        V.MatchingCostFactor(1, 1, c, g)
+    raw = V.PointCloud(np.zeros((5, 3), np.float32), None, ctx)
+    with pytest.raises(ValueError):
+        V.MatchingCostFactor(0, 1, raw, g)
+
+
+# ------------------------------------------------------------------------------ batched graph
+def build_graph_case(ctx, nframes=6, n=3000, seed=60, res=1.0):
+    rng = O.Rng(seed)
+    clouds, frames = [], []
+    for _ in range(nframes):
+        means, covs = rng.gaussian_cloud(n, 10.0)
+        c, m, c9 = gpu_cloud(ctx, means, covs)
+        clouds.append(c)
+        frames.append((m, c9))
+    maps = V.GaussianVoxelMap.build_batch(clouds, res)
+    omaps = [O.OracleMap(m, c9, res) for m, c9 in frames]
+    poses = [rng.random_pose(0.05, 0.5) for _ in range(nframes)]
+    factors = []
+    for j in range(nframes):
+        for d in (1, 2):
+            i = j - d
+            if i >= 0:
+                factors.append(V.MatchingCostFactor(i, j, clouds[j], maps[i]))
+    return factors, frames, omaps, poses
+
+
+def test_graph_batch_matches_oracle(ctx):
+    factors, frames, omaps, poses = build_graph_case(ctx)
+    graph = V.FactorGraph(factors, len(poses), chunk=1024)
+    lins = graph.linearize(poses)
+    errs, inls = graph.evaluate(poses)
+    for f, lin, e, inl in zip(factors, lins, errs, inls):
+        m, c9 = frames[f.source_index]
+        ref = O.linearize(m, c9, omaps[f.target_index], poses[f.target_index], poses[f.source_index])
+        assert lin.inliers == ref["inliers"] == inl
+        assert lin.i == f.target_index and lin.j == f.source_index
+        d = rel_block_error(lin_dict(lin), ref)
+        assert max(d.values()) <= H_TOL, d
+        assert abs(e - ref["error"]) <= ERR_TOL * max(1.0, ref["error"])
+
+
+def test_graph_deterministic_and_chunk_invariant_counts(ctx):
+    factors, _, _, poses = build_graph_case(ctx, nframes=4, n=5000, seed=61)
+    g1 = V.FactorGraph(factors, len(poses), chunk=512)
+    a, ia = g1.linearize_raw(poses)
+    b, ib = g1.linearize_raw(poses)
+    assert np.array_equal(a, b) and np.array_equal(ia, ib)  # bitwise run-to-run
+    g2 = V.FactorGraph(factors, len(poses), chunk=4096)
+    c, ic = g2.linearize_raw(poses)
+    assert np.array_equal(ia, ic)
+    scale = np.maximum(1.0, np.linalg.norm(a[:, :36], axis=1))
+    assert np.max(np.linalg.norm(a - c, axis=1) / scale) < 1e-6  # fp32 per-thread order changes with chunking
+
+
+def test_graph_validation(ctx):
+    factors, _, _, poses = build_graph_case(ctx, nframes=3, n=500, seed=62)
+    with pytest.raises(ValueError):
+        V.FactorGraph(factors, 2)  # index out of range
+    g = V.FactorGraph(factors, 3)
+    with pytest.raises(ValueError):
+        g.linearize(poses[:2])
