@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark: VGICP factor linearizations/s on the KITTI-00-shaped dense graph (BASELINE C3).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one linearize pass over every matching-cost factor of the graph (~4,500 factors x
+~20k points; ONE kernel launch), inputs resident in HBM (clouds + voxel maps ~1 GB > 126 MB L2,
+so no L2 flush is needed between steps). Under torchrun each rank owns its own C3-sized graph
+(weak scaling; seed = 1 + rank) and the per-factor blocks are gathered to rank 0 over NCCL in the
+same step (the host solver's input, north star). Rank 0 prints one JSON line.
+
+--impl reference times the reference's CPU implementation of the path — the oracle port
+(oracle/, a restatement of proj/src/factors.cpp + voxelmap.cpp; the reference itself needs Eigen
+and cannot be built here) — with every host thread, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "VGICP factor linearizations/sec (C3 dense graph)"
+UNIT = "factors/s"
+BYTES_PER_POINT = 36  # fp32 mean (12 B) + 6 unique fp32 covariance entries (24 B), SURVEY §8(d)
+BYTES_PER_HIT = 44  # 8 B key + 12 B voxel mean + 24 B voxel covariance
+BYTES_PER_FACTOR_OUT = 116  # 29-value reduced block (fp32 equivalent), SURVEY §8(d)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--frames", type=int, default=450)
+    p.add_argument("--points", type=int, default=20000)
+    p.add_argument("--chunk", type=int, default=0)
+    p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU work for cpu_baseline")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu / e2e legs)")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.file, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.file.flush()
+        rows = []
+        for line in Path(self.file.name).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.file.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------ CPU reference
+def cpu_reference_run(scans, links, threads: int, budget_s: float, resolution: float = 1.0, max_factors=None):
+    """Time the oracle port (parallel ExecPolicy{threads, false}) over `links` until the budget
+    is spent. Returns (factors_done, seconds, points_done)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_ctypes as O
+
+    cache_m, cache_c, maps = {}, {}, {}
+
+    def frame(k):
+        if k not in cache_m:
+            cache_m[k] = scans.means[k].astype(np.float64)
+            cache_c[k] = O.cov9(scans.cov6[k].astype(np.float64))
+        return cache_m[k], cache_c[k]
+
+    done = 0
+    pts = 0
+    elapsed = 0.0
+    for (i, j) in links:
+        if max_factors is not None and done >= max_factors:
+            break
+        if i not in maps:
+            m, c = frame(i)
+            maps[i] = O.OracleMap(m, c, resolution, threads=threads)
+        sm, sc = frame(j)
+        t0 = time.perf_counter()
+        O.linearize(sm, sc, maps[i], scans.odom[i], scans.odom[j], threads=threads)
+        elapsed += time.perf_counter() - t0
+        done += 1
+        pts += len(sm)
+        if elapsed >= budget_s:
+            break
+    return done, elapsed, pts
+
+
+def reference_links(scans, frames, max_links=10, min_overlap=0.025, resolution=1.0, threads=0):
+    """Factor-creation rule on the oracle (pipeline.cpp:135-141) for frames in `frames`."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_ctypes as O
+    from paper_2109_07073_b200.workloads import pose_inv, pose_mul, select_links
+
+    maps = {}
+    overlaps = {}
+    for j in frames:
+        mj = scans.means[j].astype(np.float64)
+        for i in range(j):
+            if i not in maps:
+                maps[i] = O.OracleMap(scans.means[i].astype(np.float64), O.cov9(scans.cov6[i].astype(np.float64)), resolution, threads=threads)
+            rel = pose_mul(pose_inv(scans.gt[i]), scans.gt[j])
+            overlaps[(i, j)] = O.overlap_rate(mj, rel, maps[i], threads=threads)
+    links = select_links(overlaps, max(frames) + 1, max_links, min_overlap)
+    return [l for l in links if l[1] in set(frames)]
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2109_07073_b200 import workloads as W
+
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    spec = W.c3_spec(args.frames, args.points, seed=1)
+    sample_frames = list(range(11, 11 + 20))  # frames with a full set of 10 predecessors
+    scans = W.make_scans(spec, frames_needed=range(0, max(sample_frames) + 1), threads=threads)
+    links = reference_links(scans, sample_frames, threads=threads)
+    # one step = the whole bounded sample (≈200 factors)
+    for _ in range(args.warmup):
+        cpu_reference_run(scans, links, threads, 1e9)
+    times = []
+    pts = 0
+    for _ in range(args.steps):
+        n, dt, pts = cpu_reference_run(scans, links, threads, 1e9)
+        times.append(dt)
+    t = sum(times)
+    value = len(links) * args.steps / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C3 KITTI-00-shaped dense graph (figure-eight, 450 frames x 20k pts, 1.0 m voxels, <=10 links/frame)",
+                   "sample": f"{len(links)} factors of frames {sample_frames[0]}-{sample_frames[-1]} per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{len(links)} factors x {args.steps} steps (oracle/ restatement, ExecPolicy{{{threads}, false}})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "points_per_s": pts * args.steps / t,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+
+    import paper_2109_07073_b200 as V
+    from paper_2109_07073_b200 import workloads as W
+
+    ctx = V.Context(local, stream=stream.cuda_stream)
+    threads = max(1, (os.cpu_count() or 1) // max(world, 1))
+    t_build0 = time.perf_counter()
+    wl = W.build_graph_workload(ctx, W.c3_spec(args.frames, args.points, seed=1 + rank), chunk=args.chunk, threads=threads)
+    t_build = time.perf_counter() - t_build0
+    graph = wl.graph
+    F = wl.num_factors
+    P = wl.num_points()
+
+    d_poses = torch.tensor(wl.poses, dtype=torch.float64, device=dev)
+    d_out = torch.zeros((F, V.LINEARIZED_DOUBLES), dtype=torch.float64, device=dev)
+    d_inl = torch.zeros(F, dtype=torch.int32, device=dev)
+    d_err = torch.zeros(F, dtype=torch.float64, device=dev)
+    d_inl2 = torch.zeros(F, dtype=torch.int32, device=dev)
+    gather_list = None
+    if world > 1:
+        counts = torch.tensor([F], device=dev)
+        all_counts = [torch.zeros_like(counts) for _ in range(world)]
+        dist.all_gather(all_counts, counts)
+        fmax = int(max(c.item() for c in all_counts))
+        d_send = torch.zeros((fmax, V.LINEARIZED_DOUBLES), dtype=torch.float64, device=dev)
+        gather_list = [torch.zeros_like(d_send) for _ in range(world)] if rank == 0 else None
+
+    def step():
+        graph.linearize_device(d_poses.data_ptr(), d_out.data_ptr(), d_inl.data_ptr())
+        if world > 1:
+            d_send[:F].copy_(d_out)
+            dist.gather(d_send, gather_list, dst=0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    if not args.profile:
+        clocks.start()
+    launches0 = ctx.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - launches0
+    clk = clocks.stop() if not args.profile else {}
+
+    # kernel-only timing of the dominant kernel (linearize), per launch, on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in ev:
+        a.record(stream)
+        graph.linearize_device(d_poses.data_ptr(), d_out.data_ptr(), d_inl.data_ptr())
+        b.record(stream)
+    torch.cuda.synchronize()
+    k_ms = [a.elapsed_time(b) for a, b in ev]
+    k_avg = sum(k_ms) / len(k_ms)
+    # error-only pass (total_error) timing
+    ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in ee:
+        a.record(stream)
+        graph.evaluate_device(d_poses.data_ptr(), d_err.data_ptr(), d_inl2.data_ptr())
+        b.record(stream)
+    torch.cuda.synchronize()
+    eval_avg = sum(a.elapsed_time(b) for a, b in ee) / len(ee)
+    inliers = int(d_inl.sum().item())
+
+    # end-to-end through the C ABI with host buffers: poses H2D, launch, blocks D2H, every step
+    e2e_ms = None
+    if not args.profile:
+        poses_host = np.ascontiguousarray(wl.poses)
+        graph.linearize_raw(poses_host)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            graph.linearize_raw(poses_host)
+        e2e_ms = 1e3 * (time.perf_counter() - t0) / args.steps
+
+    vals = torch.tensor([ms, k_avg, eval_avg, e2e_ms or 0.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        tot = torch.tensor([F, P, inliers], dtype=torch.float64, device=dev)
+        dist.all_reduce(tot)
+        F_all, P_all, inl_all = (float(x) for x in tot.tolist())
+    else:
+        F_all, P_all, inl_all = float(F), float(P), float(inliers)
+    ms_max, k_avg, eval_avg, e2e_ms = (float(x) for x in vals.tolist())
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    ms_step = ms_max / args.steps
+    value = F_all / (ms_step * 1e-3)
+    bytes_alg = BYTES_PER_POINT * P + BYTES_PER_HIT * inliers + BYTES_PER_FACTOR_OUT * F  # rank 0's launch
+    achieved = bytes_alg / (k_avg * 1e-3) / 1e9
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    traffic = None
+    tf = ROOT / "profiles" / "linearize_dram_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+    data_bytes = sum(36 * len(m) for m in wl.scans.means) + sum(48 * int(m.size()) * 2 for m in wl.maps)
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and not args.profile:
+        threads_all = os.cpu_count() or 1
+        n, dt, pts = cpu_reference_run(wl.scans, wl.links, threads_all, args.cpu_budget)
+        cpu = {"value": n / dt, "unit": UNIT, "cores": threads_all, "kind": "port",
+               "sample": f"first {n} of {F} C3 factors in graph order ({pts} source points, {dt:.1f} s), oracle/ restatement, ExecPolicy{{{threads_all}, false}}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {
+            "workload": "C3 KITTI-00-shaped dense graph (figure-eight, 450 frames x 20k pts, 1.0 m voxels, <=10 links/frame)",
+            "factors_per_gpu": F, "points_per_gpu": P, "frames": args.frames, "points_per_scan": args.points,
+            "parallelism": f"factor-sharded x{world} (one graph per rank) + NCCL gather to rank 0" if world > 1 else "single GPU",
+            "l2": f"no flush: resident inputs {data_bytes / 1e6:.0f} MB > 126 MB L2",
+            "dtype_detail": "fp64 transform/keys, fp32 per-point algebra, fp64 reduction above warp level",
+        },
+        "points_per_s": P_all / (ms_step * 1e-3),
+        "ms_linearize_kernel": k_avg,
+        "ms_evaluate_kernel": eval_avg,
+        "ms_lm_iteration_factor_part": k_avg + eval_avg,
+        "gpu_launches": int(launches),
+        "e2e": {"value": F_all / (e2e_ms * 1e-3) if e2e_ms else None, "unit": UNIT,
+                "h2d_bytes_per_step": int(wl.poses.nbytes), "d2h_bytes_per_step": int(F * (V.LINEARIZED_DOUBLES * 8 + 4)),
+                "ms_per_step": e2e_ms, "path": "vgicp_graph_linearize (C ABI, pinned staging, synchronous)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "bytes_alg_per_launch": bytes_alg,
+                     "bytes_alg_formula": "36*sum(N_f) + 44*sum(inliers_f) + 116*F (SURVEY 8d)"},
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "inlier_fraction": inliers / P,
+        "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()} | {"total": round(t_build, 3)},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

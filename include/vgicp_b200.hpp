@@ -1,0 +1,345 @@
+// vgicp_b200.hpp — header-only C++ façade over the C ABI (vgicp_b200.h) with the reference's
+// operator API: same class / function names, argument meaning and exceptions as
+//   proj/include/vgicp/voxelmap.hpp:28-61  (GaussianVoxelMap, overlap_rate)
+//   proj/include/vgicp/factors.hpp:19-81   (LinearizedFactor, MatchingCostFactor,
+//                                           gicp_error, linearize_/evaluate_matching_cost)
+// plus the batch entry points (linearize_matching_costs / evaluate_matching_costs /
+// overlap_rates) that optimizer.cpp:45-75 and pipeline.cpp:135-150 switch to.
+//
+// Eigen-free on purpose (the boundary carries plain arrays); INTEGRATION.md shows the few lines
+// that adapt the reference's Eigen types to it. Errors: std::invalid_argument,
+// std::out_of_range (as the reference) and vgicp::cuda_error for device failures.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "vgicp_b200.h"
+
+namespace vgicp {
+
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == VGICP_OK) return;
+  const std::string msg = vgicp_last_error();
+  if (rc == VGICP_E_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (rc == VGICP_E_OUT_OF_RANGE) throw std::out_of_range(msg);
+  if (rc == VGICP_E_OUT_OF_MEMORY) throw std::bad_alloc();
+  throw cuda_error(msg);
+}
+
+using Mat3 = std::array<double, 9>;   // row-major
+using Vec3 = std::array<double, 3>;
+using Mat6 = std::array<double, 36>;  // row-major
+using Vec6 = std::array<double, 6>;
+
+// Pose{rotation, translation} (se3.hpp:33-56) as 12 doubles: row-major R, then t.
+struct Pose {
+  std::array<double, 12> m{1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+  static Pose Identity() { return Pose{}; }
+  static Pose from(const Mat3& R, const Vec3& t) {
+    Pose p;
+    for (int k = 0; k < 9; ++k) p.m[k] = R[k];
+    for (int k = 0; k < 3; ++k) p.m[9 + k] = t[k];
+    return p;
+  }
+  const double* data() const { return m.data(); }
+};
+
+class Context {
+ public:
+  explicit Context(int device = 0, void* stream = nullptr) {
+    vgicp_ctx c = nullptr;
+    check(vgicp_ctx_create(device, stream, &c));
+    h_.reset(c, [](vgicp_ctx x) { vgicp_ctx_destroy(x); });
+  }
+  vgicp_ctx get() const { return h_.get(); }
+  void synchronize() const { check(vgicp_ctx_synchronize(get())); }
+  std::uint64_t launch_count() const {
+    std::uint64_t n = 0;
+    check(vgicp_ctx_launch_count(get(), &n));
+    return n;
+  }
+
+ private:
+  std::shared_ptr<vgicp_ctx_s> h_;
+};
+
+// Device-resident PointCloud (point_cloud.hpp:21-37). means: n×3, cov6: n×(xx xy xz yy yz zz).
+class PointCloud {
+ public:
+  PointCloud(const Context& ctx, const std::vector<float>& xyz, const std::vector<float>& cov6 = {}) : ctx_(ctx) {
+    if (xyz.size() % 3) throw std::invalid_argument("xyz must hold n*3 floats");
+    const std::size_t n = xyz.size() / 3;
+    if (!cov6.empty() && cov6.size() != 6 * n) throw std::invalid_argument("covariance count does not match point count");
+    vgicp_cloud c = nullptr;
+    check(vgicp_cloud_upload(ctx.get(), xyz.data(), cov6.empty() ? nullptr : cov6.data(), n, &c));
+    h_.reset(c, [](vgicp_cloud x) { vgicp_cloud_destroy(x); });
+  }
+  std::size_t size() const {
+    std::size_t n = 0;
+    check(vgicp_cloud_size(get(), &n));
+    return n;
+  }
+  bool empty() const { return size() == 0; }
+  bool has_covariances() const {
+    int has = 0;
+    check(vgicp_cloud_has_covariances(get(), &has));
+    return has != 0;
+  }
+  vgicp_cloud get() const { return h_.get(); }
+  const Context& context() const { return ctx_; }
+
+ private:
+  Context ctx_;
+  std::shared_ptr<vgicp_cloud_s> h_;
+};
+
+struct GaussianVoxel {  // voxelmap.hpp:18-22
+  Vec3 mean{};
+  Mat3 covariance{};
+  int count = 0;
+};
+
+// GaussianVoxelMap (voxelmap.hpp:28-56): immutable after construction.
+class GaussianVoxelMap {
+ public:
+  GaussianVoxelMap(const PointCloud& cloud, double resolution) : ctx_(cloud.context()) {
+    vgicp_map m = nullptr;
+    check(vgicp_voxelmap_build(ctx_.get(), cloud.get(), resolution, &m));
+    h_.reset(m, [](vgicp_map x) { vgicp_voxelmap_destroy(x); });
+  }
+  double resolution() const {
+    double r = 0;
+    check(vgicp_voxelmap_resolution(get(), &r));
+    return r;
+  }
+  std::size_t size() const {
+    std::size_t v = 0;
+    check(vgicp_voxelmap_size(get(), &v));
+    return v;
+  }
+  std::size_t total_points() const {
+    std::size_t n = 0;
+    check(vgicp_voxelmap_total_points(get(), &n));
+    return n;
+  }
+  // voxels() in ascending key order
+  std::vector<std::pair<std::uint64_t, GaussianVoxel>> voxels() const {
+    const std::size_t v = size();
+    std::vector<std::uint64_t> keys(v);
+    std::vector<std::int32_t> counts(v);
+    std::vector<double> means(3 * v), covs(9 * v);
+    check(vgicp_voxelmap_export(get(), keys.data(), counts.data(), means.data(), covs.data()));
+    std::vector<std::pair<std::uint64_t, GaussianVoxel>> out(v);
+    for (std::size_t i = 0; i < v; ++i) {
+      out[i].first = keys[i];
+      for (int a = 0; a < 3; ++a) out[i].second.mean[a] = means[3 * i + a];
+      for (int a = 0; a < 9; ++a) out[i].second.covariance[a] = covs[9 * i + a];
+      out[i].second.count = counts[i];
+    }
+    return out;
+  }
+  // lookup (voxelmap.cpp:106-117): key of the populated voxel or VGICP_KEY_MISS
+  std::vector<std::uint64_t> lookup(const std::vector<double>& points) const {
+    std::vector<std::uint64_t> out(points.size() / 3);
+    check(vgicp_voxelmap_lookup(get(), points.data(), out.size(), out.data()));
+    return out;
+  }
+  static std::uint64_t pack_key(double resolution, const Vec3& point) {
+    std::uint64_t k = 0;
+    check(vgicp_voxel_key(resolution, point.data(), &k));
+    return k;
+  }
+  vgicp_map get() const { return h_.get(); }
+  const Context& context() const { return ctx_; }
+
+ private:
+  Context ctx_;
+  std::shared_ptr<vgicp_map_s> h_;
+};
+
+inline double overlap_rate(const PointCloud& cloud, const Pose& pose_rel, const GaussianVoxelMap& map) {
+  double r = 0.0;
+  check(vgicp_overlap_rate(cloud.context().get(), cloud.get(), pose_rel.data(), map.get(), &r));
+  return r;
+}
+
+// overlap_rates: one probe cloud against many maps in one launch (pipeline.cpp:135-150 loop).
+inline std::vector<double> overlap_rates(const PointCloud& cloud, const std::vector<Pose>& poses,
+                                         const std::vector<const GaussianVoxelMap*>& maps) {
+  if (poses.size() != maps.size()) throw std::invalid_argument("poses and maps differ in length");
+  const int m = static_cast<int>(maps.size());
+  std::vector<vgicp_cloud> cl(m, cloud.get());
+  std::vector<vgicp_map> mh(m);
+  std::vector<double> P(12 * m);
+  for (int k = 0; k < m; ++k) {
+    mh[k] = maps[k]->get();
+    for (int q = 0; q < 12; ++q) P[12 * k + q] = poses[k].m[q];
+  }
+  std::vector<std::uint64_t> hits(m);
+  check(vgicp_overlap_batch(cloud.context().get(), cl.data(), P.data(), mh.data(), m, hits.data()));
+  std::vector<double> out(m);
+  for (int k = 0; k < m; ++k) out[k] = static_cast<double>(hits[k]) / static_cast<double>(cloud.size());
+  return out;
+}
+
+struct LinearizedFactor {  // factors.hpp:19-29
+  int i = -1;
+  int j = -1;
+  Mat6 H_ii{};
+  Mat6 H_ij{};
+  Mat6 H_jj{};
+  Vec6 b_i{};
+  Vec6 b_j{};
+  double error = 0.0;
+  int inliers = 0;
+
+  static LinearizedFactor from(const double* raw, int i, int j, int inliers) {
+    LinearizedFactor f;
+    f.i = i;
+    f.j = j;
+    for (int k = 0; k < 36; ++k) {
+      f.H_ii[k] = raw[k];
+      f.H_ij[k] = raw[36 + k];
+      f.H_jj[k] = raw[72 + k];
+    }
+    for (int k = 0; k < 6; ++k) {
+      f.b_i[k] = raw[108 + k];
+      f.b_j[k] = raw[114 + k];
+    }
+    f.error = raw[120];
+    f.inliers = inliers;
+    return f;
+  }
+};
+
+struct MatchingCostFactor {  // factors.hpp:36-45, validation of factors.cpp:57-66
+  int target_index = -1;
+  int source_index = -1;
+  std::shared_ptr<const PointCloud> source_points;
+  std::shared_ptr<const GaussianVoxelMap> target_voxels;
+
+  MatchingCostFactor(int target, int source, std::shared_ptr<const PointCloud> points,
+                     std::shared_ptr<const GaussianVoxelMap> voxels)
+      : target_index(target), source_index(source), source_points(std::move(points)), target_voxels(std::move(voxels)) {
+    if (target_index == source_index) throw std::invalid_argument("matching cost factor requires distinct variables");
+    if (!source_points || source_points->empty())
+      throw std::invalid_argument("matching cost factor requires a nonempty source cloud");
+    if (!source_points->has_covariances()) throw std::invalid_argument("matching cost factor requires source covariances");
+    if (!target_voxels || target_voxels->size() == 0)
+      throw std::invalid_argument("matching cost factor requires a nonempty target voxel map");
+  }
+  vgicp_factor_desc desc() const { return {target_index, source_index, source_points->get(), target_voxels->get()}; }
+};
+
+inline LinearizedFactor linearize_matching_cost(const MatchingCostFactor& f, const Pose& T_target, const Pose& T_source) {
+  double raw[VGICP_LINEARIZED_DOUBLES];
+  std::int32_t inl = 0;
+  const vgicp_factor_desc d = f.desc();
+  check(vgicp_linearize_matching_cost(f.source_points->context().get(), &d, T_target.data(), T_source.data(), raw, &inl));
+  return LinearizedFactor::from(raw, f.target_index, f.source_index, inl);
+}
+
+inline std::pair<double, int> evaluate_matching_cost(const MatchingCostFactor& f, const Pose& T_target,
+                                                     const Pose& T_source) {
+  double err = 0.0;
+  std::int32_t inl = 0;
+  const vgicp_factor_desc d = f.desc();
+  check(vgicp_evaluate_matching_cost(f.source_points->context().get(), &d, T_target.data(), T_source.data(), &err, &inl));
+  return {err, inl};
+}
+
+struct GicpErrorResult {  // factors.hpp:62-67
+  double error = 0.0;
+  Vec3 residual{};
+  Mat3 information{};
+  bool valid = true;
+};
+
+inline GicpErrorResult gicp_error(const Context& ctx, const Vec3& source_mean, const Mat3& source_cov,
+                                  const GaussianVoxel& target, const Pose& T) {
+  GicpErrorResult r;
+  int valid = 0;
+  check(vgicp_gicp_error(ctx.get(), source_mean.data(), source_cov.data(), target.mean.data(), target.covariance.data(),
+                         T.data(), &r.error, r.residual.data(), r.information.data(), &valid));
+  r.valid = valid != 0;
+  return r;
+}
+
+// Batched factors over a fixed graph: one launch linearizes / evaluates every factor.
+class MatchingCostBatch {
+ public:
+  MatchingCostBatch(const Context& ctx, const std::vector<MatchingCostFactor>& factors, int num_poses, int chunk = 0)
+      : ctx_(ctx), factors_(factors), num_poses_(num_poses) {
+    std::vector<vgicp_factor_desc> d;
+    d.reserve(factors.size());
+    for (const auto& f : factors) d.push_back(f.desc());
+    vgicp_graph g = nullptr;
+    check(vgicp_graph_create(ctx.get(), d.data(), static_cast<int>(d.size()), num_poses, chunk, &g));
+    h_.reset(g, [](vgicp_graph x) { vgicp_graph_destroy(x); });
+  }
+  // linearize_all (optimizer.cpp:45-62), matching part, factor order
+  std::vector<LinearizedFactor> linearize(const std::vector<Pose>& poses) const {
+    const std::vector<double> P = flatten(poses);
+    std::vector<double> raw(factors_.size() * VGICP_LINEARIZED_DOUBLES);
+    std::vector<std::int32_t> inl(factors_.size());
+    check(vgicp_graph_linearize(h_.get(), P.data(), raw.data(), inl.data()));
+    std::vector<LinearizedFactor> out(factors_.size());
+    for (std::size_t k = 0; k < factors_.size(); ++k)
+      out[k] = LinearizedFactor::from(raw.data() + k * VGICP_LINEARIZED_DOUBLES, factors_[k].target_index,
+                                      factors_[k].source_index, inl[k]);
+    return out;
+  }
+  // per-factor (error, inliers) for total_error (optimizer.cpp:66-75)
+  std::vector<std::pair<double, int>> evaluate(const std::vector<Pose>& poses) const {
+    const std::vector<double> P = flatten(poses);
+    std::vector<double> err(factors_.size());
+    std::vector<std::int32_t> inl(factors_.size());
+    check(vgicp_graph_evaluate(h_.get(), P.data(), err.data(), inl.data()));
+    std::vector<std::pair<double, int>> out(factors_.size());
+    for (std::size_t k = 0; k < out.size(); ++k) out[k] = {err[k], inl[k]};
+    return out;
+  }
+  double total_error(const std::vector<Pose>& poses) const {
+    double s = 0.0;
+    for (const auto& e : evaluate(poses)) s += e.first;
+    return s;
+  }
+  std::size_t size() const { return factors_.size(); }
+
+ private:
+  std::vector<double> flatten(const std::vector<Pose>& poses) const {
+    if (static_cast<int>(poses.size()) != num_poses_) throw std::invalid_argument("pose count does not match the batch");
+    std::vector<double> P(12 * poses.size());
+    for (std::size_t k = 0; k < poses.size(); ++k)
+      for (int q = 0; q < 12; ++q) P[12 * k + q] = poses[k].m[q];
+    return P;
+  }
+  Context ctx_;
+  std::vector<MatchingCostFactor> factors_;
+  int num_poses_;
+  std::shared_ptr<vgicp_graph_s> h_;
+};
+
+inline std::vector<LinearizedFactor> linearize_matching_costs(const Context& ctx,
+                                                              const std::vector<MatchingCostFactor>& factors,
+                                                              const std::vector<Pose>& poses) {
+  return MatchingCostBatch(ctx, factors, static_cast<int>(poses.size())).linearize(poses);
+}
+
+inline std::vector<std::pair<double, int>> evaluate_matching_costs(const Context& ctx,
+                                                                   const std::vector<MatchingCostFactor>& factors,
+                                                                   const std::vector<Pose>& poses) {
+  return MatchingCostBatch(ctx, factors, static_cast<int>(poses.size())).evaluate(poses);
+}
+
+}  // namespace vgicp

@@ -1,0 +1,99 @@
+// C++ façade smoke test (include/vgicp_b200.hpp): the reference-facing C++ API end to end on a
+// GPU. Built by __graft_entry__.build(); run by tests/test_facade_cpp.py (-m gpu).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <stdexcept>
+
+#include "vgicp_b200.hpp"
+
+#define REQUIRE(c)                                                  \
+  do {                                                              \
+    if (!(c)) {                                                     \
+      std::fprintf(stderr, "FAILED %s:%d: %s\n", __FILE__, __LINE__, #c); \
+      std::exit(1);                                                 \
+    }                                                               \
+  } while (0)
+
+int main() {
+  using namespace vgicp;
+  Context ctx(0);
+  std::mt19937_64 rng(7);
+  std::uniform_real_distribution<float> U(-10.f, 10.f);
+  const int n = 5000;
+  std::vector<float> xyz(3 * n), cov(6 * n);
+  for (int i = 0; i < n; ++i) {
+    for (int a = 0; a < 3; ++a) xyz[3 * i + a] = U(rng);
+    // plane covariance with normal z: diag(1, 1, 1e-3)
+    cov[6 * i + 0] = 1.f, cov[6 * i + 1] = 0.f, cov[6 * i + 2] = 0.f;
+    cov[6 * i + 3] = 1.f, cov[6 * i + 4] = 0.f, cov[6 * i + 5] = 1e-3f;
+  }
+  auto cloud = std::make_shared<PointCloud>(ctx, xyz, cov);
+  auto map = std::make_shared<GaussianVoxelMap>(*cloud, 1.0);
+  REQUIRE(map->total_points() == static_cast<std::size_t>(n));
+  REQUIRE(map->size() > 0 && map->size() <= static_cast<std::size_t>(n));
+  std::size_t total = 0;
+  for (const auto& kv : map->voxels()) total += kv.second.count;
+  REQUIRE(total == static_cast<std::size_t>(n));
+
+  // overlap: self at identity = 1, far = 0 (test_voxelmap.cpp:138-149)
+  REQUIRE(overlap_rate(*cloud, Pose::Identity(), *map) == 1.0);
+  REQUIRE(overlap_rate(*cloud, Pose::from({1, 0, 0, 0, 1, 0, 0, 0, 1}, {500, 0, 0}), *map) == 0.0);
+  const auto rates = overlap_rates(*cloud, {Pose::Identity(), Pose::from({1, 0, 0, 0, 1, 0, 0, 0, 1}, {0.5, 0, 0})},
+                                   {map.get(), map.get()});
+  REQUIRE(rates[0] == 1.0 && rates[1] > 0.0 && rates[1] < 1.0);
+
+  // factor: identical clouds at equal poses -> every point hits its own voxel
+  MatchingCostFactor factor(0, 1, cloud, map);
+  const Pose T = Pose::from({1, 0, 0, 0, 1, 0, 0, 0, 1}, {0.3, -0.2, 0.1});
+  const LinearizedFactor lin = linearize_matching_cost(factor, T, T);
+  REQUIRE(lin.inliers == n);
+  const auto ev = evaluate_matching_cost(factor, T, T);
+  REQUIRE(ev.second == n);
+  REQUIRE(std::abs(ev.first - lin.error) <= 1e-6 * std::max(1.0, lin.error));
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) REQUIRE(lin.H_ii[6 * r + c] == lin.H_ii[6 * c + r]);
+
+  // batch == single
+  MatchingCostBatch batch(ctx, {factor}, 2);
+  const auto lins = batch.linearize({T, T});
+  REQUIRE(lins.size() == 1 && lins[0].inliers == lin.inliers);
+  for (int k = 0; k < 36; ++k) REQUIRE(lins[0].H_ij[k] == lin.H_ij[k]);
+  REQUIRE(batch.total_error({T, T}) == ev.first);
+
+  // exceptions mirror the reference
+  bool threw = false;
+  try {
+    MatchingCostFactor bad(1, 1, cloud, map);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  REQUIRE(threw);
+  threw = false;
+  try {
+    PointCloud far(ctx, {2.0e6f, 0.f, 0.f}, {1, 0, 0, 1, 0, 1});
+    GaussianVoxelMap m(far, 1.0);
+  } catch (const std::out_of_range&) {
+    threw = true;
+  }
+  REQUIRE(threw);
+  threw = false;
+  try {
+    GaussianVoxelMap m(*cloud, -1.0);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  REQUIRE(threw);
+
+  // gicp_error KAT (test_factors.cpp:107-111)
+  GaussianVoxel v;
+  v.mean = {2, 2, 3};
+  v.covariance = {0.5, 0, 0, 0, 0.5, 0, 0, 0, 0.5};
+  const auto g = gicp_error(ctx, {1, 2, 3}, {0.5, 0, 0, 0, 0.5, 0, 0, 0, 0.5}, v, Pose::Identity());
+  REQUIRE(g.valid && std::abs(g.error - 1.0) < 1e-12);
+
+  std::printf("facade ok: voxels=%zu inliers=%d error=%.6f launches=%llu\n", map->size(), lin.inliers, lin.error,
+              static_cast<unsigned long long>(ctx.launch_count()));
+  return 0;
+}
