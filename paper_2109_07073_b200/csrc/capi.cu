@@ -90,9 +90,29 @@ void release(vgicp_cloud c) {
 void release(vgicp_map m) {
   if (m && m->refs.fetch_sub(1) == 1) {
     DeviceGuard g(m->ctx->device);
-    cudaFree(m->block);
+    cudaFree(m->cold);
+    cudaFree(m->table);
     delete m;
   }
+}
+
+// (Re)allocate a map's hash table with `buckets` buckets (power of two), all slots empty.
+int alloc_table(vgicp_map mp, unsigned buckets, cudaStream_t s) {
+  if (mp->table) VG_CUDA(cudaFree(mp->table));
+  mp->table = nullptr;
+  mp->num_buckets = buckets;
+  unsigned lg = 0;
+  while ((1u << lg) < buckets) ++lg;
+  mp->shift = 32 - lg;
+  const size_t cap = static_cast<size_t>(kBucket) * buckets;
+  const size_t b_keys = align_up(sizeof(unsigned long long) * cap, 256);
+  const size_t b_sa = align_up(sizeof(SlotStatsA) * cap, 256);
+  VG_CUDA(cudaMalloc(&mp->table, b_keys + b_sa + sizeof(SlotStatsB) * cap));
+  mp->tkeys = static_cast<unsigned long long*>(mp->table);
+  mp->sa = reinterpret_cast<SlotStatsA*>(static_cast<char*>(mp->table) + b_keys);
+  mp->sb = reinterpret_cast<SlotStatsB*>(static_cast<char*>(mp->table) + b_keys + b_sa);
+  VG_CUDA(cudaMemsetAsync(mp->tkeys, 0xFF, sizeof(unsigned long long) * cap, s));
+  return VGICP_OK;
 }
 
 // voxel_coord + pack_key on the host (voxelmap.cpp:45-63); same division/floor semantics.
@@ -312,6 +332,9 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
   const size_t o_v1 = carve(sizeof(unsigned) * total);
   const size_t o_heads = carve(sizeof(unsigned) * total);
   const size_t o_vidx = carve(sizeof(unsigned) * total);
+  const size_t o_hot = carve(sizeof(VoxelStats) * total);  // compact hot records (V <= N)
+  const size_t o_jobs = carve(sizeof(InsertJob) * m);
+  const size_t o_ovf = carve(sizeof(int) * m);
   std::vector<int> offsets(m + 1);
   for (int k = 0; k < m; ++k) offsets[k] = static_cast<int>(segs[k].offset);
   offsets[m] = ntot;
@@ -337,6 +360,9 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
   auto* d_v1 = reinterpret_cast<unsigned*>(sb + o_v1);
   auto* d_heads = reinterpret_cast<unsigned*>(sb + o_heads);
   auto* d_vidx = reinterpret_cast<unsigned*>(sb + o_vidx);
+  auto* d_hot = reinterpret_cast<VoxelStats*>(sb + o_hot);
+  auto* d_jobs = reinterpret_cast<InsertJob*>(sb + o_jobs);
+  auto* d_ovf = reinterpret_cast<int*>(sb + o_ovf);
   void* d_temp = sb + o_temp;
   cudaStream_t s = ctx->stream;
 
@@ -359,12 +385,13 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
   for (int k = 0; k < m; ++k)
     if (herr[k]) return fail(VGICP_E_OUT_OF_RANGE, "point beyond the +-2^20 voxel-per-axis range limit");
 
-  // allocate maps
+  // allocate maps: cold fp64 arrays + a two-choice table with >= V/2 buckets (load <= 0.5)
   std::vector<vgicp_map> maps(m, nullptr);
   auto cleanup = [&]() {
     for (auto* mp : maps) release(mp);
   };
   std::vector<BuildOut> outs(m);
+  unsigned max_v = 1;
   for (int k = 0; k < m; ++k) {
     auto* mp = new (std::nothrow) vgicp_map_s();
     if (!mp) {
@@ -377,43 +404,73 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
     mp->inv_res = 1.0 / resolutions[k];
     mp->voxels = hv[k];
     mp->total_points = clouds[k]->n;
-    mp->capacity = std::max(64u, next_pow2(2ull * hv[k]));
-    unsigned lg = 0;
-    while ((1u << lg) < mp->capacity) ++lg;
-    mp->shift = 64 - lg;
+    max_v = std::max(max_v, hv[k]);
     const size_t V = hv[k];
-    const size_t b_table = align_up(sizeof(VoxelRec) * mp->capacity, 256);
     const size_t b_keys = align_up(sizeof(unsigned long long) * V, 256);
     const size_t b_counts = align_up(sizeof(int) * V, 256);
     const size_t b_mean = align_up(sizeof(double) * 3 * V, 256);
     const size_t b_cov = align_up(sizeof(double) * 9 * V, 256);
-    const cudaError_t e = cudaMalloc(&mp->block, b_table + b_keys + b_counts + b_mean + b_cov);
+    const cudaError_t e = cudaMalloc(&mp->cold, std::max<size_t>(b_keys + b_counts + b_mean + b_cov, 256));
     if (e != cudaSuccess) {
       cleanup();
       return cuda_fail(e, "cudaMalloc(voxel map)");
     }
-    char* b = static_cast<char*>(mp->block);
-    mp->table = reinterpret_cast<VoxelRec*>(b);
-    mp->keys = reinterpret_cast<unsigned long long*>(b + b_table);
-    mp->counts = reinterpret_cast<int*>(b + b_table + b_keys);
-    mp->mean64 = reinterpret_cast<double*>(b + b_table + b_keys + b_counts);
-    mp->cov64 = reinterpret_cast<double*>(b + b_table + b_keys + b_counts + b_mean);
-    const cudaError_t e2 = cudaMemsetAsync(mp->table, 0xFF, sizeof(VoxelRec) * mp->capacity, s);
-    if (e2 != cudaSuccess) {
+    char* b = static_cast<char*>(mp->cold);
+    mp->keys = reinterpret_cast<unsigned long long*>(b);
+    mp->counts = reinterpret_cast<int*>(b + b_keys);
+    mp->mean64 = reinterpret_cast<double*>(b + b_keys + b_counts);
+    mp->cov64 = reinterpret_cast<double*>(b + b_keys + b_counts + b_mean);
+    if (int rc = alloc_table(mp, std::max(16u, next_pow2((hv[k] + 1) / 2)), s)) {
       cleanup();
-      return cuda_fail(e2, "cudaMemsetAsync(table)");
+      return rc;
     }
-    outs[k] = BuildOut{mp->table, mp->keys, mp->counts, mp->mean64, mp->cov64, mp->shift, mp->capacity - 1,
-                       hbase[k], 0u};
+    outs[k] = BuildOut{mp->keys, mp->counts, mp->mean64, mp->cov64, hbase[k], 0u};
   }
   cudaError_t e = cudaMemcpyAsync(d_outs, outs.data(), sizeof(BuildOut) * m, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = launch_build_accumulate(d_segs, d_outs, m, max_n, d_k1, d_v1, d_heads, d_vidx, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess)
+    e = launch_build_accumulate(d_segs, d_outs, m, max_n, d_k1, d_v1, d_heads, d_vidx, d_hot, s);
   if (e != cudaSuccess) {
     cleanup();
     return cuda_fail(e, "voxel map accumulate");
   }
   ctx->launches += 1;
+  // insert; maps whose two-choice insertion overflowed are rebuilt with twice the buckets
+  std::vector<int> todo(m);
+  for (int k = 0; k < m; ++k) todo[k] = k;
+  for (int attempt = 0; !todo.empty(); ++attempt) {
+    if (attempt > 8) {
+      cleanup();
+      return fail(VGICP_E_CUDA, "voxel hash table insertion did not converge");
+    }
+    std::vector<InsertJob> jobs;
+    for (int k : todo) {
+      vgicp_map mp = maps[k];
+      jobs.push_back(InsertJob{mp->tkeys, mp->sa, mp->sb, mp->keys, hbase[k], static_cast<unsigned>(mp->voxels), mp->shift, 0u});
+    }
+    const int nj = static_cast<int>(jobs.size());
+    std::vector<int> hovf(nj, 0);
+    e = cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(InsertJob) * nj, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_ovf, 0, sizeof(int) * nj, s);
+    if (e == cudaSuccess) e = launch_build_insert(d_jobs, nj, max_v, d_hot, d_ovf, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hovf.data(), d_ovf, sizeof(int) * nj, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      cleanup();
+      return cuda_fail(e, "voxel map insert");
+    }
+    ctx->launches += 1;
+    std::vector<int> next;
+    for (int q = 0; q < nj; ++q) {
+      if (!hovf[q]) continue;
+      const int k = todo[q];
+      if (int rc = alloc_table(maps[k], maps[k]->num_buckets * 2, s)) {
+        cleanup();
+        return rc;
+      }
+      next.push_back(k);
+    }
+    todo.swap(next);
+  }
   for (int k = 0; k < m; ++k) out[k] = maps[k];
   return VGICP_OK;
 }
@@ -533,8 +590,8 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   if (!ctx || !out || (num_factors > 0 && !factors)) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   if (num_factors < 0 || num_poses < 0) return fail(VGICP_E_INVALID_ARGUMENT, "negative size");
-  if (chunk <= 0) chunk = 2048;
-  chunk = std::max(kFactorThreads, (chunk + kFactorThreads - 1) / kFactorThreads * kFactorThreads);
+  if (chunk <= 0) chunk = kDefaultChunk;
+  chunk = std::max(kFactorTile, (chunk + kFactorTile - 1) / kFactorTile * kFactorTile);
   // MatchingCostFactor ctor validation (factors.cpp:57-66)
   for (int f = 0; f < num_factors; ++f) {
     const vgicp_factor_desc& d = factors[f];

@@ -35,7 +35,7 @@ __device__ __forceinline__ void dswap(double& a, double& b) {
 // invert_covariance (factors.cpp:38-46): Eigen-style LDLT with diagonal pivoting on the lower
 // triangle; rejects on failure or any pivot <= 0; Omega = solve(I), symmetrised.
 // Same operation sequence as the CPU checker's LDLT restatement.
-__device__ __noinline__ bool invert_covariance_rn(const double* M, double* out) {
+static __device__ __noinline__ bool invert_covariance_rn(const double* M, double* out) {
   double a[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i)

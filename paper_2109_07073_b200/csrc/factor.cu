@@ -50,8 +50,23 @@ __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, f
   return true;
 }
 
+constexpr int kILP = 2;                    // points per thread per tile (independent probes in flight)
+constexpr int kWarpTile = 32 * kILP;       // points per warp per tile
+constexpr int kTile = kFactorThreads * kILP;  // points per CTA tile
+static_assert(kTile == kFactorTile, "tile size mismatch");
+
+// Per-warp staging between the probe phase and the math phase (uncompacted by lane position,
+// plus a compacted, position-ordered hit list => deterministic).
+struct WarpStage {
+  float lx[kWarpTile], ly[kWarpTile], lz[kWarpTile];  // q - voxel corner (fp64 -> fp32)
+  float qx[kWarpTile], qy[kWarpTile], qz[kWarpTile];  // q (Jacobian lever arm)
+  float sxx[kWarpTile];                               // source c_xx (lives in the mean float4)
+  int slot[kWarpTile];
+  unsigned char list[kWarpTile];
+};
+
 template <bool kLinearize>
-__global__ void __launch_bounds__(kFactorThreads) factor_kernel(
+__global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
     const FactorDev* __restrict__ factors, const WorkItem* __restrict__ items, const double* __restrict__ poses,
     double* __restrict__ partials, int* __restrict__ part_inl, unsigned* __restrict__ counters,
     double* __restrict__ out, int* __restrict__ out_inl) {
@@ -63,6 +78,7 @@ __global__ void __launch_bounds__(kFactorThreads) factor_kernel(
   __shared__ double sTot[kLinAcc];
   __shared__ int sTotInl;
   __shared__ double sH[36], sAd[36], sHA[36], sHss[36];
+  __shared__ WarpStage sStage[kWarps];
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -77,123 +93,169 @@ __global__ void __launch_bounds__(kFactorThreads) factor_kernel(
   const float4* __restrict__ pb = fp->pb;
   const float* __restrict__ pc = fp->pc;
   const MapDev map = fp->map;
+  WarpStage& st = sStage[warp];
 
-  double T[12];
-#pragma unroll
-  for (int k = 0; k < 12; ++k) T[k] = sT[k];
-  const float r00 = (float)T[0], r01 = (float)T[1], r02 = (float)T[2];
-  const float r10 = (float)T[3], r11 = (float)T[4], r12 = (float)T[5];
-  const float r20 = (float)T[6], r21 = (float)T[7], r22 = (float)T[8];
+  // T_ts stays in shared memory (broadcast reads) to keep registers for in-flight probes.
+  const double* T = sT;
+  __shared__ float sRf[9];
+  if (tid < 9) sRf[tid] = (float)sT[tid];
+  __syncthreads();
+  const unsigned lane_lt = (1u << lane) - 1u;
 
   float acc[kAcc];
 #pragma unroll
   for (int k = 0; k < kAcc; ++k) acc[k] = 0.f;
   int inl = 0;
 
-  for (int i = w.begin + tid; i < w.end; i += kFactorThreads) {
-    const float4 A = __ldg(pa + i);
-    double q0, q1, q2;
-    apply_pose_rn(T, A.x, A.y, A.z, q0, q1, q2);
-    unsigned long long key;
-    double c0, c1, c2;
-    if (!voxel_key(q0, q1, q2, map.res, map.inv_res, key, c0, c1, c2)) continue;
-    float mx, my;
-    const int slot = probe(map.table, map.shift, map.mask, key, mx, my);
-    if (slot < 0) continue;
-    const float4* rec = reinterpret_cast<const float4*>(map.table + slot);
-    const float4 v1 = __ldg(rec + 1);  // mz cxx cxy cxz
-    const float4 v2 = __ldg(rec + 2);  // cyy cyz czz vid
-    const float4 B = __ldg(pb + i);    // sxy sxz syy syz
-    const float szz = __ldg(pc + i);
-    const float sxx = A.w, sxy = B.x, sxz = B.y, syy = B.z, syz = B.w;
-
-    // residual e = mu' - q in voxel-local coordinates (mu' and q differ by < 2 voxels)
-    const float e0 = mx - (float)__dsub_rn(q0, __dmul_rn(c0, map.res));
-    const float e1 = my - (float)__dsub_rn(q1, __dmul_rn(c1, map.res));
-    const float e2 = v1.x - (float)__dsub_rn(q2, __dmul_rn(c2, map.res));
-
-    // M = C_t + R C_s Rᵀ (fp32)
-    const float t00 = r00 * sxx + r01 * sxy + r02 * sxz;
-    const float t01 = r00 * sxy + r01 * syy + r02 * syz;
-    const float t02 = r00 * sxz + r01 * syz + r02 * szz;
-    const float t10 = r10 * sxx + r11 * sxy + r12 * sxz;
-    const float t11 = r10 * sxy + r11 * syy + r12 * syz;
-    const float t12 = r10 * sxz + r11 * syz + r12 * szz;
-    const float t20 = r20 * sxx + r21 * sxy + r22 * sxz;
-    const float t21 = r20 * sxy + r21 * syy + r22 * syz;
-    const float t22 = r20 * sxz + r21 * syz + r22 * szz;
-    const float m00 = v1.y + (t00 * r00 + t01 * r01 + t02 * r02);
-    const float m01 = v1.z + (t00 * r10 + t01 * r11 + t02 * r12);
-    const float m02 = v1.w + (t00 * r20 + t01 * r21 + t02 * r22);
-    const float m11 = v2.x + (t10 * r10 + t11 * r11 + t12 * r12);
-    const float m12 = v2.y + (t10 * r20 + t11 * r21 + t12 * r22);
-    const float m22 = v2.z + (t20 * r20 + t21 * r21 + t22 * r22);
-
-    // Omega = M⁻¹ by cofactors; Sylvester test with margins decides the fast path
-    const float a00 = m11 * m22 - m12 * m12;
-    const float a01 = m02 * m12 - m01 * m22;
-    const float a02 = m01 * m12 - m02 * m11;
-    const float a11 = m00 * m22 - m02 * m02;
-    const float a12 = m01 * m02 - m00 * m12;
-    const float a22 = m00 * m11 - m01 * m01;
-    const float det = m00 * a00 + m01 * a01 + m02 * a02;
-    const float tr = m00 + m11 + m22;
-    float om[6];
-    if (tr > 0.f && m00 > 1e-6f * tr && a22 > 1e-6f * tr * tr && det > 1e-5f * tr * tr * tr) {
-      const float inv = __frcp_rn(det);
-      om[0] = a00 * inv;
-      om[1] = a01 * inv;
-      om[2] = a02 * inv;
-      om[3] = a11 * inv;
-      om[4] = a12 * inv;
-      om[5] = a22 * inv;
-    } else {
-      if (!omega_fp64(sT, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.w), om)) continue;
+  for (int tb = w.begin + warp * kWarpTile; tb < w.end; tb += kTile) {
+    // ---- phase 1: transform, exact key, both bucket loads for kILP points per lane ----
+    unsigned hi[kILP], lo[kILP], b1[kILP], b2[kILP];
+    bool ok[kILP];
+#pragma unroll
+    for (int u = 0; u < kILP; ++u) {
+      const int p = u * 32 + lane;
+      const int i = min(tb + p, w.end - 1);  // clamped: every lane computes, only in-range lanes count
+      const float4 A = __ldg(pa + i);
+      double q0, q1, q2, l0, l1, l2;
+      apply_pose_rn(T, A.x, A.y, A.z, q0, q1, q2);
+      unsigned k0 = 0, k1 = 0, k2 = 0;
+      ok[u] = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && (tb + p < w.end);
+      pack_key32(k0, k1, k2, hi[u], lo[u]);
+      b1[u] = bucket1(k0, k1, k2, map.shift);
+      b2[u] = bucket2(k0, k1, k2, map.shift);
+      st.lx[p] = (float)l0;
+      st.ly[p] = (float)l1;
+      st.lz[p] = (float)l2;
+      st.qx[p] = (float)q0;
+      st.qy[p] = (float)q1;
+      st.qz[p] = (float)q2;
+      st.sxx[p] = A.w;
     }
-    const float o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
-    const float w0 = o00 * e0 + o01 * e1 + o02 * e2;
-    const float w1 = o01 * e0 + o11 * e1 + o12 * e2;
-    const float w2 = o02 * e0 + o12 * e1 + o22 * e2;
-    ++inl;
-    if constexpr (!kLinearize) {
-      acc[0] += e0 * w0 + e1 * w1 + e2 * w2;
-    } else {
-      const float qf0 = (float)q0, qf1 = (float)q1, qf2 = (float)q2;
-      // P = [q]x Ω
-      const float p00 = qf1 * o02 - qf2 * o01, p01 = qf1 * o12 - qf2 * o11, p02 = qf1 * o22 - qf2 * o12;
-      const float p10 = qf2 * o00 - qf0 * o02, p11 = qf2 * o01 - qf0 * o12, p12 = qf2 * o02 - qf0 * o22;
-      const float p20 = qf0 * o01 - qf1 * o00, p21 = qf0 * o11 - qf1 * o01, p22 = qf0 * o12 - qf1 * o02;
-      // Q = -P [q]x  (symmetric)
-      acc[0] += p02 * qf1 - p01 * qf2;   // Q00
-      acc[1] += p00 * qf2 - p02 * qf0;   // Q01
-      acc[2] += p01 * qf0 - p00 * qf1;   // Q02
-      acc[3] += p10 * qf2 - p12 * qf0;   // Q11
-      acc[4] += p11 * qf0 - p10 * qf1;   // Q12
-      acc[5] += p21 * qf0 - p20 * qf1;   // Q22
-      acc[6] += p00;
-      acc[7] += p01;
-      acc[8] += p02;
-      acc[9] += p10;
-      acc[10] += p11;
-      acc[11] += p12;
-      acc[12] += p20;
-      acc[13] += p21;
-      acc[14] += p22;
-      acc[15] += o00;
-      acc[16] += o01;
-      acc[17] += o02;
-      acc[18] += o11;
-      acc[19] += o12;
-      acc[20] += o22;
-      // b_t = -AᵀΩe = [-(q × w); -w]
-      acc[21] -= qf1 * w2 - qf2 * w1;
-      acc[22] -= qf2 * w0 - qf0 * w2;
-      acc[23] -= qf0 * w1 - qf1 * w0;
-      acc[24] -= w0;
-      acc[25] -= w1;
-      acc[26] -= w2;
-      acc[27] += e0 * w0 + e1 * w1 + e2 * w2;
+    BucketPair bp[kILP];
+#pragma unroll
+    for (int u = 0; u < kILP; ++u) bp[u] = load_buckets(map.keys, b1[u], b2[u]);  // always in-bounds
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < kILP; ++u) {
+      const int s = ok[u] ? match_buckets(bp[u], b1[u], b2[u], hi[u], lo[u]) : -1;
+      const bool hit = s >= 0;
+      const unsigned ball = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        const int p = u * 32 + lane;
+        st.slot[p] = s;
+        st.list[cnt + __popc(ball & lane_lt)] = static_cast<unsigned char>(p);
+      }
+      cnt += __popc(ball);
     }
+    __syncwarp();
+
+    // ---- phase 2: per-hit fp32 algebra over the compacted list (all lanes busy) ----
+    for (int e = lane; e < cnt; e += 32) {
+      const int p = st.list[e];
+      const int i = tb + p;
+      const int sl = st.slot[p];
+      float4 v0, v1;  // (mx my mz cxx) (cxy cxz cyy cyz)
+      ldg256(map.sa + sl, reinterpret_cast<unsigned&>(v0.x), reinterpret_cast<unsigned&>(v0.y),
+             reinterpret_cast<unsigned&>(v0.z), reinterpret_cast<unsigned&>(v0.w), reinterpret_cast<unsigned&>(v1.x),
+             reinterpret_cast<unsigned&>(v1.y), reinterpret_cast<unsigned&>(v1.z), reinterpret_cast<unsigned&>(v1.w));
+      const float2 v2 = __ldg(reinterpret_cast<const float2*>(map.sb + sl));  // czz vid
+      const float4 B = __ldg(pb + i);    // sxy sxz syy syz
+      const float szz = __ldg(pc + i);
+      const float sxx = st.sxx[p], sxy = B.x, sxz = B.y, syy = B.z, syz = B.w;
+
+      // residual e = mu' - q in voxel-local coordinates
+      const float e0 = v0.x - st.lx[p];
+      const float e1 = v0.y - st.ly[p];
+      const float e2 = v0.z - st.lz[p];
+
+      // M = C_t + R C_s Rᵀ (fp32)
+      const float r00 = sRf[0], r01 = sRf[1], r02 = sRf[2];
+      const float r10 = sRf[3], r11 = sRf[4], r12 = sRf[5];
+      const float r20 = sRf[6], r21 = sRf[7], r22 = sRf[8];
+      const float t00 = r00 * sxx + r01 * sxy + r02 * sxz;
+      const float t01 = r00 * sxy + r01 * syy + r02 * syz;
+      const float t02 = r00 * sxz + r01 * syz + r02 * szz;
+      const float t10 = r10 * sxx + r11 * sxy + r12 * sxz;
+      const float t11 = r10 * sxy + r11 * syy + r12 * syz;
+      const float t12 = r10 * sxz + r11 * syz + r12 * szz;
+      const float t20 = r20 * sxx + r21 * sxy + r22 * sxz;
+      const float t21 = r20 * sxy + r21 * syy + r22 * syz;
+      const float t22 = r20 * sxz + r21 * syz + r22 * szz;
+      const float m00 = v0.w + (t00 * r00 + t01 * r01 + t02 * r02);
+      const float m01 = v1.x + (t00 * r10 + t01 * r11 + t02 * r12);
+      const float m02 = v1.y + (t00 * r20 + t01 * r21 + t02 * r22);
+      const float m11 = v1.z + (t10 * r10 + t11 * r11 + t12 * r12);
+      const float m12 = v1.w + (t10 * r20 + t11 * r21 + t12 * r22);
+      const float m22 = v2.x + (t20 * r20 + t21 * r21 + t22 * r22);
+
+      // Omega = M⁻¹ by cofactors; Sylvester test with margins decides the fast path
+      const float a00 = m11 * m22 - m12 * m12;
+      const float a01 = m02 * m12 - m01 * m22;
+      const float a02 = m01 * m12 - m02 * m11;
+      const float a11 = m00 * m22 - m02 * m02;
+      const float a12 = m01 * m02 - m00 * m12;
+      const float a22 = m00 * m11 - m01 * m01;
+      const float det = m00 * a00 + m01 * a01 + m02 * a02;
+      const float tr = m00 + m11 + m22;
+      float o00, o01, o02, o11, o12, o22;
+      if (tr > 0.f && m00 > 1e-6f * tr && a22 > 1e-6f * tr * tr && det > 1e-5f * tr * tr * tr) {
+        const float inv = __frcp_rn(det);
+        o00 = a00 * inv;
+        o01 = a01 * inv;
+        o02 = a02 * inv;
+        o11 = a11 * inv;
+        o12 = a12 * inv;
+        o22 = a22 * inv;
+      } else {
+        float om[6];
+        if (!omega_fp64(sT, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.y), om)) continue;
+        o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
+      }
+      const float w0 = o00 * e0 + o01 * e1 + o02 * e2;
+      const float w1 = o01 * e0 + o11 * e1 + o12 * e2;
+      const float w2 = o02 * e0 + o12 * e1 + o22 * e2;
+      ++inl;
+      if constexpr (!kLinearize) {
+        acc[0] += e0 * w0 + e1 * w1 + e2 * w2;
+      } else {
+        const float qf0 = st.qx[p], qf1 = st.qy[p], qf2 = st.qz[p];
+        // P = [q]x Ω
+        const float p00 = qf1 * o02 - qf2 * o01, p01 = qf1 * o12 - qf2 * o11, p02 = qf1 * o22 - qf2 * o12;
+        const float p10 = qf2 * o00 - qf0 * o02, p11 = qf2 * o01 - qf0 * o12, p12 = qf2 * o02 - qf0 * o22;
+        const float p20 = qf0 * o01 - qf1 * o00, p21 = qf0 * o11 - qf1 * o01, p22 = qf0 * o12 - qf1 * o02;
+        // Q = -P [q]x  (symmetric)
+        acc[0] += p02 * qf1 - p01 * qf2;   // Q00
+        acc[1] += p00 * qf2 - p02 * qf0;   // Q01
+        acc[2] += p01 * qf0 - p00 * qf1;   // Q02
+        acc[3] += p10 * qf2 - p12 * qf0;   // Q11
+        acc[4] += p11 * qf0 - p10 * qf1;   // Q12
+        acc[5] += p21 * qf0 - p20 * qf1;   // Q22
+        acc[6] += p00;
+        acc[7] += p01;
+        acc[8] += p02;
+        acc[9] += p10;
+        acc[10] += p11;
+        acc[11] += p12;
+        acc[12] += p20;
+        acc[13] += p21;
+        acc[14] += p22;
+        acc[15] += o00;
+        acc[16] += o01;
+        acc[17] += o02;
+        acc[18] += o11;
+        acc[19] += o12;
+        acc[20] += o22;
+        // b_t = -AᵀΩe = [-(q × w); -w]
+        acc[21] -= qf1 * w2 - qf2 * w1;
+        acc[22] -= qf2 * w0 - qf0 * w2;
+        acc[23] -= qf0 * w1 - qf1 * w0;
+        acc[24] -= w0;
+        acc[25] -= w1;
+        acc[26] -= w2;
+        acc[27] += e0 * w0 + e1 * w1 + e2 * w2;
+      }
+    }
+    __syncwarp();
   }
 
   // ---- CTA reduction: warp shuffle in fp64, then fixed-order sum over warps ----

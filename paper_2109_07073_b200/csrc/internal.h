@@ -63,19 +63,29 @@ struct BuildSeg {
   double inv_res;
 };
 
-struct BuildOut {
-  VoxelRec* table;
+struct BuildOut {       // cold fp64 statistics of one map (ascending key order)
   unsigned long long* keys;
   int* counts;
   double* mean64;
   double* cov64;
-  unsigned shift;
-  unsigned mask;
+  unsigned vbase;          // global voxel id of this map's first voxel
+  unsigned pad;
+};
+
+struct InsertJob {       // hash-table insertion of one map's voxels
+  unsigned long long* tkeys;
+  SlotStatsA* sa;
+  SlotStatsB* sb;
+  const unsigned long long* keys;  // cold keys (ascending)
   unsigned vbase;
+  unsigned voxels;
+  unsigned shift;
   unsigned pad;
 };
 
 constexpr int kFactorThreads = 256;
+constexpr int kFactorTile = 512;    // points per CTA tile (kFactorThreads x kILP)
+constexpr int kDefaultChunk = 8192;  // points per CTA work item
 constexpr int kLinAcc = 28;     // Q(6) P(9) Omega(6) b(6) error(1)
 constexpr int kPartialStride = 32;
 
@@ -88,7 +98,9 @@ cudaError_t launch_build_counts(const BuildSeg* segs, int m, const unsigned* hea
                                 unsigned* vcount, unsigned* vbase, cudaStream_t s);
 cudaError_t launch_build_accumulate(const BuildSeg* segs, const BuildOut* outs, int m, unsigned max_n,
                                     const unsigned long long* keys, const unsigned* vals, const unsigned* heads,
-                                    const unsigned* vidx, cudaStream_t s);
+                                    const unsigned* vidx, VoxelStats* hot, cudaStream_t s);
+cudaError_t launch_build_insert(const InsertJob* jobs, int m, unsigned max_v, const VoxelStats* hot, int* overflow,
+                                cudaStream_t s);
 cudaError_t launch_lookup(MapDev map, const double* pts, size_t n, unsigned long long* keys_out, cudaStream_t s);
 cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsigned long long* hits, cudaStream_t s);
 cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkItem* items, int num_items,
@@ -127,18 +139,19 @@ struct vgicp_map_s {
   double inv_res = 1.0;
   size_t voxels = 0;
   size_t total_points = 0;
-  unsigned capacity = 0;
+  unsigned num_buckets = 0;
   unsigned shift = 0;
-  void* block = nullptr;  // table | keys | counts | mean64 | cov64
-  vgicp::VoxelRec* table = nullptr;
+  void* cold = nullptr;   // keys | counts | mean64 | cov64
+  void* table = nullptr;  // tkeys | stats
   unsigned long long* keys = nullptr;
   int* counts = nullptr;
   double* mean64 = nullptr;
   double* cov64 = nullptr;
+  unsigned long long* tkeys = nullptr;
+  vgicp::SlotStatsA* sa = nullptr;
+  vgicp::SlotStatsB* sb = nullptr;
   std::atomic<int> refs{1};
-  vgicp::MapDev dev() const {
-    return vgicp::MapDev{table, cov64, res, inv_res, shift, capacity - 1};
-  }
+  vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov64, res, inv_res, shift, 0u}; }
 };
 
 struct vgicp_graph_s {

@@ -4,9 +4,10 @@
 //  - source cloud, SoA, 36 B/point: pa[i] = (x, y, z, c_xx) float4, pb[i] = (c_xy, c_xz, c_yy, c_yz)
 //    float4, pc[i] = c_zz float. Means are float32 (KITTI precision), so the fp64 transform below
 //    sees exactly the values the oracle sees.
-//  - voxel map: open-addressing hash table of 48-B records (key + voxel-local fp32 statistics),
-//    capacity a power of two >= 2V (load factor <= 0.5, linear probing), plus cold fp64 arrays in
-//    ascending key order (keys, counts, means, covariances) for export and the rare fp64 path.
+//  - voxel map: two-choice bucketed hash table (buckets of 4 keys = 32 B, load <= 0.5, every
+//    lookup = two independent sector loads), 48-B voxel-local fp32 statistics per slot, plus cold
+//    fp64 arrays in ascending key order (keys, counts, means, covariances) for export and the
+//    rare fp64 path.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -18,24 +19,48 @@ constexpr unsigned long long kEmptyKey = ~0ull;  // valid keys use 63 bits (voxe
 constexpr int kKeyBits = 21;                     // voxelmap.cpp:12
 constexpr double kKeyBias = 1048576.0;           // 2^20, voxelmap.cpp:13
 
-// 48-byte hash-table record. The first 16 B (key + 2 mean floats) is all a probe reads.
-struct __align__(16) VoxelRec {
-  unsigned long long key;
-  float mx, my;                 // voxel-local mean: mean - coord * resolution (fp32)
-  float mz, cxx, cxy, cxz;      // covariance (fp32), symmetric
-  float cyy, cyz, czz;
+// Two-choice bucketed hash table. Keys live in buckets of kBucket = 4 slots (32 B = one L2
+// sector); a key is stored in one of two buckets chosen by independent hashes, so every lookup
+// is exactly two independent sector loads (no probe chains). Per-slot statistics live in a
+// parallel array indexed by slot.
+constexpr int kBucket = 4;
+
+struct __align__(16) VoxelStats {  // compact build-time record (by voxel id)
+  float mx, my, mz, cxx;        // voxel-local mean (mean - coord * resolution) and covariance, fp32
+  float cxy, cxz, cyy, cyz;
+  float czz;
   int vid;                      // index into the cold fp64 arrays (ascending key order)
+  int pad0, pad1;
 };
-static_assert(sizeof(VoxelRec) == 48, "VoxelRec must be 48 bytes");
+static_assert(sizeof(VoxelStats) == 48, "VoxelStats must be 48 bytes");
+
+// Per-slot statistics in the table, split so a hit costs one 32-B and one 8-B gather.
+struct __align__(32) SlotStatsA {
+  float mx, my, mz, cxx, cxy, cxz, cyy, cyz;
+};
+struct __align__(8) SlotStatsB {
+  float czz;
+  int vid;
+};
 
 struct MapDev {
-  const VoxelRec* table;
-  const double* cov64;  // V×9 row-major fp64 covariances (cold)
+  const unsigned long long* keys;  // capacity = kBucket * num_buckets, kEmptyKey when free
+  const SlotStatsA* sa;            // per slot
+  const SlotStatsB* sb;            // per slot
+  const double* cov64;             // V×9 row-major fp64 covariances (cold)
   double res;
   double inv_res;
-  unsigned shift;       // 64 - log2(capacity)
-  unsigned mask;        // capacity - 1
+  unsigned shift;                  // 32 - log2(num_buckets)
+  unsigned pad;
 };
+
+// 256-bit read-only global load (sm_100: LDG.E.ENL2.256).
+__device__ __forceinline__ void ldg256(const void* p, unsigned& r0, unsigned& r1, unsigned& r2, unsigned& r3,
+                                       unsigned& r4, unsigned& r5, unsigned& r6, unsigned& r7) {
+  asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(r4), "=r"(r5), "=r"(r6), "=r"(r7)
+      : "l"(p));
+}
 
 // ------------------------------------------------------------------------------------------
 // Exact fp64 helpers: explicit round-to-nearest intrinsics are never contracted into FMAs,
@@ -53,27 +78,51 @@ __device__ __forceinline__ void apply_pose_rn(const double* T, double p0, double
   q2 = __dadd_rn(dot3_rn(T[6], T[7], T[8], p0, p1, p2), T[11]);
 }
 
-// floor(x / r) exactly as std::floor(point[a] / resolution_) (voxelmap.cpp:48, :109), i.e. the
-// floor of the correctly rounded IEEE quotient. Fast path: y = x * fl(1/r) is within 3.4e-16|y|
-// of fl(x/r); when no integer lies within 8e-16|y| of y both have the same floor. Otherwise
-// (points within ~1e-15 relative of a voxel face, zero, NaN) take the IEEE division.
-__device__ __forceinline__ double voxel_floor(double x, double r, double inv_r) {
+// One axis of voxel_coord (voxelmap.cpp:45-55): floor(x / r) exactly as
+// std::floor(point[a] / resolution_) — the floor of the correctly rounded IEEE quotient — and
+// the ±2^20 range check. Fast path: y = x·fl(1/r) differs from fl(x/r) by < 3.4e-16|y| (< 7.2e-10
+// for |y| < 2^21), so when frac(y) lies in (2e-9, 1 - 2e-9) both have the same floor. Points
+// within ~1e-9 voxel of a face, zeros, infinities and NaN take the IEEE division. On success
+// returns the biased 21-bit coordinate k = c + 2^20 and frac_r ≈ x - c·r (voxel-local offset).
+// Exact path (out of line, returns by value so the fast path keeps everything in registers):
+// (c, x - c·r) with c = floor(fl(x / r)); c is NaN for NaN input.
+static __device__ __noinline__ double2 voxel_axis_exact(double x, double r) {
+  const double c = floor(__ddiv_rn(x, r));
+  return make_double2(c, __dsub_rn(x, __dmul_rn(c, r)));
+}
+
+__device__ __forceinline__ bool voxel_axis(double x, double r, double inv_r, unsigned& k, double& local) {
   const double y = __dmul_rn(x, inv_r);
-  const double tol = fmax(fabs(y) * 8.0e-16, 1.0e-300);
-  const double lo = floor(__dsub_rn(y, tol));
-  const double hi = floor(__dadd_rn(y, tol));
-  if (lo == hi) return lo;
-  return floor(__ddiv_rn(x, r));
+  double c = floor(y);
+  const double f = __dsub_rn(y, c);
+  if (f > 2.0e-9 && f < 1.0 - 2.0e-9) {
+    local = __dmul_rn(f, r);
+  } else {
+    const double2 e = voxel_axis_exact(x, r);
+    c = e.x;
+    local = e.y;
+  }
+  const bool in = c >= -kKeyBias && c < kKeyBias;  // false for NaN
+  k = static_cast<unsigned>((in ? __double2int_rz(c) : 0) + (1 << 20));
+  return in;
 }
 
 __device__ __forceinline__ bool in_key_range(double c) { return c >= -kKeyBias && c < kKeyBias; }
 
-// pack_key (voxelmap.cpp:57-63) for in-range integral coordinates.
-__device__ __forceinline__ unsigned long long pack_key(double c0, double c1, double c2) {
-  const unsigned long long k0 = static_cast<unsigned long long>(static_cast<long long>(c0) + (1ll << 20));
-  const unsigned long long k1 = static_cast<unsigned long long>(static_cast<long long>(c1) + (1ll << 20));
-  const unsigned long long k2 = static_cast<unsigned long long>(static_cast<long long>(c2) + (1ll << 20));
-  return (((k0 << kKeyBits) | k1) << kKeyBits) | k2;
+// pack_key (voxelmap.cpp:57-63) as (hi, lo) 32-bit halves of ((k0 << 42) | (k1 << 21) | k2).
+__device__ __forceinline__ void pack_key32(unsigned k0, unsigned k1, unsigned k2, unsigned& hi, unsigned& lo) {
+  lo = k2 | (k1 << 21);
+  hi = (k1 >> 11) | (k0 << 10);
+}
+
+__device__ __forceinline__ unsigned long long key64(unsigned hi, unsigned lo) {
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
+__device__ __forceinline__ void unpack_key(unsigned long long key, unsigned& k0, unsigned& k1, unsigned& k2) {
+  k0 = static_cast<unsigned>(key >> 42) & 0x1FFFFFu;
+  k1 = static_cast<unsigned>(key >> 21) & 0x1FFFFFu;
+  k2 = static_cast<unsigned>(key) & 0x1FFFFFu;
 }
 
 __device__ __forceinline__ double key_coord(unsigned long long key, int axis) {
@@ -81,49 +130,51 @@ __device__ __forceinline__ double key_coord(unsigned long long key, int axis) {
   return static_cast<double>(static_cast<long long>((key >> sh) & 0x1FFFFFull) - (1ll << 20));
 }
 
-// Voxel key of point q under resolution r; false when any axis is outside ±2^20 (or NaN).
-__device__ __forceinline__ bool voxel_key(double q0, double q1, double q2, double r, double inv_r,
-                                          unsigned long long& key, double& c0, double& c1, double& c2) {
-  c0 = voxel_floor(q0, r, inv_r);
-  c1 = voxel_floor(q1, r, inv_r);
-  c2 = voxel_floor(q2, r, inv_r);
-  if (!(in_key_range(c0) && in_key_range(c1) && in_key_range(c2))) return false;
-  key = pack_key(c0, c1, c2);
-  return true;
+// Two independent spatial hashes of the biased voxel coordinates -> bucket index (32-bit ops).
+__device__ __forceinline__ unsigned bucket1(unsigned k0, unsigned k1, unsigned k2, unsigned shift) {
+  const unsigned h = (k0 * 73856093u) ^ (k1 * 19349663u) ^ (k2 * 83492791u);
+  return (h * 0x9E3779B1u) >> shift;
+}
+__device__ __forceinline__ unsigned bucket2(unsigned k0, unsigned k1, unsigned k2, unsigned shift) {
+  const unsigned h = (k0 * 2654435761u) ^ (k1 * 2246822519u) ^ (k2 * 3266489917u) ^ 0x5bd1e995u;
+  return ((h ^ (h >> 15)) * 0x85EBCA6Bu) >> shift;
 }
 
-// Fibonacci hashing into a power-of-two table.
-__device__ __forceinline__ unsigned hash_slot(unsigned long long key, unsigned shift) {
-  return static_cast<unsigned>((key * 0x9E3779B97F4A7C15ull) >> shift);
+// Voxel key of q under resolution r; false when any axis is outside ±2^20 (or NaN).
+__device__ __forceinline__ bool voxel_key(double q0, double q1, double q2, double r, double inv_r, unsigned& k0,
+                                          unsigned& k1, unsigned& k2, double& l0, double& l1, double& l2) {
+  return voxel_axis(q0, r, inv_r, k0, l0) & voxel_axis(q1, r, inv_r, k1, l1) & voxel_axis(q2, r, inv_r, k2, l2);
 }
 
-// Linear probe. Returns the slot of `key` or -1. Also returns the record's first 16 B
-// (mx, my) through the out-params to save one load on a hit.
-__device__ __forceinline__ int probe(const VoxelRec* __restrict__ table, unsigned shift, unsigned mask,
-                                     unsigned long long key, float& mx, float& my) {
-  unsigned slot = hash_slot(key, shift);
-  while (true) {
-    const uint4 h = __ldg(reinterpret_cast<const uint4*>(table + slot));
-    const unsigned long long k = (static_cast<unsigned long long>(h.y) << 32) | h.x;
-    if (k == key) {
-      mx = __uint_as_float(h.z);
-      my = __uint_as_float(h.w);
-      return static_cast<int>(slot);
-    }
-    if (k == kEmptyKey) return -1;
-    slot = (slot + 1) & mask;
+// Issue the two bucket loads (2 × 32 B, independent) for a key.
+struct BucketPair {
+  unsigned a[8];
+  unsigned b[8];
+};
+__device__ __forceinline__ BucketPair load_buckets(const unsigned long long* __restrict__ keys, unsigned b1,
+                                                   unsigned b2) {
+  BucketPair r;
+  ldg256(keys + kBucket * b1, r.a[0], r.a[1], r.a[2], r.a[3], r.a[4], r.a[5], r.a[6], r.a[7]);
+  ldg256(keys + kBucket * b2, r.b[0], r.b[1], r.b[2], r.b[3], r.b[4], r.b[5], r.b[6], r.b[7]);
+  return r;
+}
+
+// Slot of (hi, lo) among the 8 loaded candidates, or -1.
+__device__ __forceinline__ int match_buckets(const BucketPair& p, unsigned b1, unsigned b2, unsigned hi, unsigned lo) {
+  int s = -1;
+#pragma unroll
+  for (int q = 0; q < kBucket; ++q) {
+    s = (p.a[2 * q] == lo && p.a[2 * q + 1] == hi) ? static_cast<int>(kBucket * b1 + q) : s;
+    s = (p.b[2 * q] == lo && p.b[2 * q + 1] == hi) ? static_cast<int>(kBucket * b2 + q) : s;
   }
+  return s;
 }
 
-__device__ __forceinline__ bool probe_hit(const VoxelRec* __restrict__ table, unsigned shift, unsigned mask,
-                                          unsigned long long key) {
-  unsigned slot = hash_slot(key, shift);
-  while (true) {
-    const unsigned long long k = __ldg(&table[slot].key);
-    if (k == key) return true;
-    if (k == kEmptyKey) return false;
-    slot = (slot + 1) & mask;
-  }
+__device__ __forceinline__ int find_slot(const MapDev& map, unsigned k0, unsigned k1, unsigned k2) {
+  unsigned hi, lo;
+  pack_key32(k0, k1, k2, hi, lo);
+  const unsigned b1 = bucket1(k0, k1, k2, map.shift), b2 = bucket2(k0, k1, k2, map.shift);
+  return match_buckets(load_buckets(map.keys, b1, b2), b1, b2, hi, lo);
 }
 
 }  // namespace vgicp

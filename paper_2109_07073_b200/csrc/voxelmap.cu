@@ -21,11 +21,14 @@ __global__ void build_keys_kernel(const BuildSeg* __restrict__ segs, unsigned lo
   const BuildSeg s = segs[blockIdx.y];
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += gridDim.x * blockDim.x) {
     const float4 a = __ldg(s.pa + i);
-    unsigned long long key;
-    double c0, c1, c2;
-    if (!voxel_key(a.x, a.y, a.z, s.res, s.inv_res, key, c0, c1, c2)) {
+    unsigned k0, k1, k2, hi, lo;
+    double l0, l1, l2;
+    unsigned long long key = 0;
+    if (voxel_key(a.x, a.y, a.z, s.res, s.inv_res, k0, k1, k2, l0, l1, l2)) {
+      pack_key32(k0, k1, k2, hi, lo);
+      key = key64(hi, lo);
+    } else {
       atomicOr(&range_err[blockIdx.y], 1);
-      key = 0;
     }
     keys[s.offset + i] = key;
     vals[s.offset + i] = i;
@@ -67,7 +70,7 @@ __device__ __forceinline__ void kahan_add(double& sum, double& comp, double valu
 __global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const BuildOut* __restrict__ outs,
                                         const unsigned long long* __restrict__ keys,
                                         const unsigned* __restrict__ vals, const unsigned* __restrict__ heads,
-                                        const unsigned* __restrict__ vidx) {
+                                        const unsigned* __restrict__ vidx, VoxelStats* __restrict__ hot) {
   const BuildSeg s = segs[blockIdx.y];
   const BuildOut o = outs[blockIdx.y];
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += gridDim.x * blockDim.x) {
@@ -116,34 +119,72 @@ __global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const
     c9[0] = cov[0], c9[1] = cov[1], c9[2] = cov[2];
     c9[3] = cov[1], c9[4] = cov[3], c9[5] = cov[4];
     c9[6] = cov[2], c9[7] = cov[4], c9[8] = cov[5];
-    // hot record: statistics relative to the voxel's lower corner, fp32
+    // hot record (compact by global voxel id): statistics relative to the voxel's lower corner
     const double corner0 = __dmul_rn(key_coord(key, 0), s.res);
     const double corner1 = __dmul_rn(key_coord(key, 1), s.res);
     const double corner2 = __dmul_rn(key_coord(key, 2), s.res);
-    unsigned slot = hash_slot(key, o.shift);
-    while (atomicCAS(&o.table[slot].key, kEmptyKey, key) != kEmptyKey) slot = (slot + 1) & o.mask;
-    VoxelRec* r = o.table + slot;
-    r->mx = static_cast<float>(__dsub_rn(mean[0], corner0));
-    r->my = static_cast<float>(__dsub_rn(mean[1], corner1));
-    r->mz = static_cast<float>(__dsub_rn(mean[2], corner2));
-    r->cxx = static_cast<float>(cov[0]);
-    r->cxy = static_cast<float>(cov[1]);
-    r->cxz = static_cast<float>(cov[2]);
-    r->cyy = static_cast<float>(cov[3]);
-    r->cyz = static_cast<float>(cov[4]);
-    r->czz = static_cast<float>(cov[5]);
-    r->vid = static_cast<int>(v);
+    VoxelStats r;
+    r.mx = static_cast<float>(__dsub_rn(mean[0], corner0));
+    r.my = static_cast<float>(__dsub_rn(mean[1], corner1));
+    r.mz = static_cast<float>(__dsub_rn(mean[2], corner2));
+    r.cxx = static_cast<float>(cov[0]);
+    r.cxy = static_cast<float>(cov[1]);
+    r.cxz = static_cast<float>(cov[2]);
+    r.cyy = static_cast<float>(cov[3]);
+    r.cyz = static_cast<float>(cov[4]);
+    r.czz = static_cast<float>(cov[5]);
+    r.vid = static_cast<int>(v);
+    r.pad0 = r.pad1 = 0;
+    hot[vidx[g]] = r;
+  }
+}
+
+// Two-choice insertion (64-bit atomicCAS on key slots): try the emptier of the key's two
+// buckets first, then the other; a key that finds both full flags the map for a rebuild with
+// twice the buckets. Slot positions may differ between runs; lookups never do.
+__global__ void build_insert_kernel(const InsertJob* __restrict__ jobs, const VoxelStats* __restrict__ hot,
+                                    int* __restrict__ overflow) {
+  const InsertJob j = jobs[blockIdx.y];
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < j.voxels; v += gridDim.x * blockDim.x) {
+    const unsigned long long key = j.keys[v];
+    unsigned k0, k1, k2;
+    unpack_key(key, k0, k1, k2);
+    const unsigned b1 = bucket1(k0, k1, k2, j.shift), b2 = bucket2(k0, k1, k2, j.shift);
+    int free1 = 0, free2 = 0;
+#pragma unroll
+    for (int q = 0; q < kBucket; ++q) {
+      free1 += j.tkeys[kBucket * b1 + q] == kEmptyKey;
+      free2 += j.tkeys[kBucket * b2 + q] == kEmptyKey;
+    }
+    const unsigned order[2] = {free2 > free1 ? b2 : b1, free2 > free1 ? b1 : b2};
+    int slot = -1;
+    for (int c = 0; c < 2 && slot < 0; ++c)
+      for (int q = 0; q < kBucket && slot < 0; ++q) {
+        const unsigned sidx = kBucket * order[c] + q;
+        if (atomicCAS(&j.tkeys[sidx], kEmptyKey, key) == kEmptyKey) slot = static_cast<int>(sidx);
+      }
+    if (slot < 0) {
+      atomicOr(&overflow[blockIdx.y], 1);
+      continue;
+    }
+    const VoxelStats h = hot[j.vbase + v];
+    SlotStatsA a;
+    a.mx = h.mx, a.my = h.my, a.mz = h.mz, a.cxx = h.cxx, a.cxy = h.cxy, a.cxz = h.cxz, a.cyy = h.cyy, a.cyz = h.cyz;
+    j.sa[slot] = a;
+    j.sb[slot] = SlotStatsB{h.czz, h.vid};
   }
 }
 
 __global__ void lookup_kernel(MapDev map, const double* __restrict__ pts, size_t n,
                               unsigned long long* __restrict__ keys_out) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    unsigned long long key;
-    double c0, c1, c2;
+    unsigned k0, k1, k2, hi, lo;
+    double l0, l1, l2;
     unsigned long long out = kEmptyKey;
-    if (voxel_key(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], map.res, map.inv_res, key, c0, c1, c2)) {
-      if (probe_hit(map.table, map.shift, map.mask, key)) out = key;
+    if (voxel_key(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], map.res, map.inv_res, k0, k1, k2, l0, l1, l2) &&
+        find_slot(map, k0, k1, k2) >= 0) {
+      pack_key32(k0, k1, k2, hi, lo);
+      out = key64(hi, lo);
     }
     keys_out[i] = out;
   }
@@ -151,11 +192,16 @@ __global__ void lookup_kernel(MapDev map, const double* __restrict__ pts, size_t
 
 // overlap_rate (voxelmap.cpp:119-135), batched: blockIdx.y walks (cloud, pose, map) items,
 // hits are integer-exact (warp-aggregated 64-bit atomics), so the result is exactly hits / N.
+// Each thread keeps kOverlapILP points' bucket pairs in flight (keys first, then all loads).
+constexpr int kOverlapILP = 4;
+
 __global__ void __launch_bounds__(256) overlap_kernel(const OverlapItem* __restrict__ items, int m,
                                                       unsigned long long* __restrict__ hits) {
   for (int k = blockIdx.y; k < m; k += gridDim.y) {
     const OverlapItem& it = items[k];
     const unsigned n = it.n;
+    const unsigned stride = gridDim.x * blockDim.x;
+    const unsigned first = blockIdx.x * blockDim.x + threadIdx.x;
     if (blockIdx.x * blockDim.x >= n) continue;
     double T[12];
 #pragma unroll
@@ -163,15 +209,27 @@ __global__ void __launch_bounds__(256) overlap_kernel(const OverlapItem* __restr
     const MapDev map = it.map;
     const float4* __restrict__ pa = it.pa;
     unsigned count = 0;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-      const float4 a = __ldg(pa + i);
-      double q0, q1, q2;
-      apply_pose_rn(T, a.x, a.y, a.z, q0, q1, q2);
-      unsigned long long key;
-      double c0, c1, c2;
-      if (voxel_key(q0, q1, q2, map.res, map.inv_res, key, c0, c1, c2) &&
-          probe_hit(map.table, map.shift, map.mask, key))
-        ++count;
+    for (unsigned base = first; base < n; base += kOverlapILP * stride) {
+      unsigned hi[kOverlapILP], lo[kOverlapILP], b1[kOverlapILP], b2[kOverlapILP];
+      bool ok[kOverlapILP];
+#pragma unroll
+      for (int u = 0; u < kOverlapILP; ++u) {
+        const unsigned i = base + u * stride;
+        const float4 a = __ldg(pa + min(i, n - 1));
+        double q0, q1, q2, l0, l1, l2;
+        apply_pose_rn(T, a.x, a.y, a.z, q0, q1, q2);
+        unsigned k0 = 0, k1 = 0, k2 = 0;
+        ok[u] = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && i < n;
+        pack_key32(k0, k1, k2, hi[u], lo[u]);
+        b1[u] = bucket1(k0, k1, k2, map.shift);
+        b2[u] = bucket2(k0, k1, k2, map.shift);
+      }
+      BucketPair bp[kOverlapILP];
+#pragma unroll
+      for (int u = 0; u < kOverlapILP; ++u) bp[u] = load_buckets(map.keys, b1[u], b2[u]);
+#pragma unroll
+      for (int u = 0; u < kOverlapILP; ++u)
+        if (ok[u] && match_buckets(bp[u], b1[u], b2[u], hi[u], lo[u]) >= 0) ++count;
     }
     count = __reduce_add_sync(0xffffffffu, count);
     if ((threadIdx.x & 31) == 0 && count) atomicAdd(&hits[k], static_cast<unsigned long long>(count));
@@ -206,8 +264,15 @@ cudaError_t launch_build_counts(const BuildSeg* segs, int m, const unsigned* hea
 
 cudaError_t launch_build_accumulate(const BuildSeg* segs, const BuildOut* outs, int m, unsigned max_n,
                                     const unsigned long long* keys, const unsigned* vals, const unsigned* heads,
-                                    const unsigned* vidx, cudaStream_t s) {
-  build_accumulate_kernel<<<dim3(grid_for(max_n, 128, 4096), m), 128, 0, s>>>(segs, outs, keys, vals, heads, vidx);
+                                    const unsigned* vidx, VoxelStats* hot, cudaStream_t s) {
+  build_accumulate_kernel<<<dim3(grid_for(max_n, 128, 4096), m), 128, 0, s>>>(segs, outs, keys, vals, heads, vidx,
+                                                                              hot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_insert(const InsertJob* jobs, int m, unsigned max_v, const VoxelStats* hot, int* overflow,
+                                cudaStream_t s) {
+  build_insert_kernel<<<dim3(grid_for(max_v, 128, 4096), m), 128, 0, s>>>(jobs, hot, overflow);
   return cudaGetLastError();
 }
 
@@ -219,7 +284,7 @@ cudaError_t launch_lookup(MapDev map, const double* pts, size_t n, unsigned long
 
 cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsigned long long* hits, cudaStream_t s) {
   const unsigned gy = m < 65535 ? m : 65535;
-  overlap_kernel<<<dim3(grid_for(max_n, 256 * 4, 1024), gy), 256, 0, s>>>(items, m, hits);
+  overlap_kernel<<<dim3(grid_for(max_n, 256 * kOverlapILP, 1024), gy), 256, 0, s>>>(items, m, hits);
   return cudaGetLastError();
 }
 
