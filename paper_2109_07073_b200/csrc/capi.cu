@@ -5,6 +5,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -434,7 +436,7 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
     return cuda_fail(e, "voxel map accumulate");
   }
   ctx->launches += 1;
-  // insert; maps whose two-choice insertion overflowed are rebuilt with twice the buckets
+  // cuckoo-insert the keys; maps whose insertion overflowed are rebuilt with twice the buckets
   std::vector<int> todo(m);
   for (int k = 0; k < m; ++k) todo[k] = k;
   for (int attempt = 0; !todo.empty(); ++attempt) {
@@ -445,13 +447,14 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
     std::vector<InsertJob> jobs;
     for (int k : todo) {
       vgicp_map mp = maps[k];
-      jobs.push_back(InsertJob{mp->tkeys, mp->sa, mp->sb, mp->keys, hbase[k], static_cast<unsigned>(mp->voxels), mp->shift, 0u});
+      jobs.push_back(InsertJob{mp->tkeys, mp->sa, mp->sb, mp->keys, hbase[k], static_cast<unsigned>(mp->voxels),
+                               mp->shift, 0u});
     }
     const int nj = static_cast<int>(jobs.size());
     std::vector<int> hovf(nj, 0);
     e = cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(InsertJob) * nj, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_ovf, 0, sizeof(int) * nj, s);
-    if (e == cudaSuccess) e = launch_build_insert(d_jobs, nj, max_v, d_hot, d_ovf, s);
+    if (e == cudaSuccess) e = launch_build_insert(d_jobs, nj, max_v, d_ovf, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(hovf.data(), d_ovf, sizeof(int) * nj, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
@@ -469,7 +472,25 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
       }
       next.push_back(k);
     }
+    if (std::getenv("VGICP_VERBOSE"))
+      std::fprintf(stderr, "[vgicp] build insert pass %d: %d maps, %zu overflowed\n", attempt, nj, next.size());
     todo.swap(next);
+  }
+  {
+    std::vector<InsertJob> jobs;
+    for (int k = 0; k < m; ++k) {
+      vgicp_map mp = maps[k];
+      jobs.push_back(InsertJob{mp->tkeys, mp->sa, mp->sb, mp->keys, hbase[k], static_cast<unsigned>(mp->voxels),
+                               mp->shift, 0u});
+    }
+    e = cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(InsertJob) * m, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = launch_build_place(d_jobs, m, max_v, d_hot, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      cleanup();
+      return cuda_fail(e, "voxel map place");
+    }
+    ctx->launches += 1;
   }
   for (int k = 0; k < m; ++k) out[k] = maps[k];
   return VGICP_OK;

@@ -50,20 +50,71 @@ __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, f
   return true;
 }
 
-constexpr int kILP = 2;                    // points per thread per tile (independent probes in flight)
-constexpr int kWarpTile = 32 * kILP;       // points per warp per tile
-constexpr int kTile = kFactorThreads * kILP;  // points per CTA tile
+constexpr int kILP = 2;                        // points per lane per tile (independent probes in flight)
+constexpr int kWarpTile = 32 * kILP;           // points per warp per tile
+constexpr int kTile = kFactorThreads * kILP;   // points per CTA tile
 static_assert(kTile == kFactorTile, "tile size mismatch");
+constexpr int kRedStride = kFactorThreads + 1;  // padded column stride of the reduction transpose
 
-// Per-warp staging between the probe phase and the math phase (uncompacted by lane position,
-// plus a compacted, position-ordered hit list => deterministic).
+// ---- TMA (cp.async.bulk) + mbarrier helpers --------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Shared memory of one CTA. Every warp owns a private kStages-deep ring of source tiles that it
+// fills itself with TMA bulk copies (cp.async.bulk, mbarrier completion), so warps never wait on
+// each other inside the point loop; after the loop the rings are reused for the reduction.
+constexpr int kStages = 3;
+struct WarpTile {
+  float4 pa[kWarpTile];  // x y z c_xx
+  float4 pb[kWarpTile];  // c_xy c_xz c_yy c_yz
+  float pc[kWarpTile];   // c_zz
+};
 struct WarpStage {
   float lx[kWarpTile], ly[kWarpTile], lz[kWarpTile];  // q - voxel corner (fp64 -> fp32)
   float qx[kWarpTile], qy[kWarpTile], qz[kWarpTile];  // q (Jacobian lever arm)
-  float sxx[kWarpTile];                               // source c_xx (lives in the mean float4)
   int slot[kWarpTile];
   unsigned char list[kWarpTile];
 };
+struct __align__(128) FactorSmem {
+  union {
+    WarpTile ring[kWarps][kStages];
+    float red[kLinAcc * kRedStride];
+  } u;
+  WarpStage stage[kWarps];
+  unsigned long long bar[kWarps][kStages];
+  double T[12];
+  float Rf[9];
+  double part[kLinAcc][8];
+  double tot[kLinAcc];
+  double H[36], Ad[36], HA[36], Hss[36];
+  int inl[kWarps];
+  int tot_inl;
+  int last;
+};
+static_assert(sizeof(float) * kLinAcc * kRedStride <= sizeof(WarpTile) * kWarps * kStages,
+              "reduction transpose must fit in the tile rings");
 
 template <bool kLinearize>
 __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
@@ -71,35 +122,48 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
     double* __restrict__ partials, int* __restrict__ part_inl, unsigned* __restrict__ counters,
     double* __restrict__ out, int* __restrict__ out_inl) {
   constexpr int kAcc = kLinearize ? kLinAcc : 1;
-  __shared__ double sT[12];
-  __shared__ double sRed[kWarps][kAcc];
-  __shared__ int sInl[kWarps];
-  __shared__ int sLast;
-  __shared__ double sTot[kLinAcc];
-  __shared__ int sTotInl;
-  __shared__ double sH[36], sAd[36], sHA[36], sHss[36];
-  __shared__ WarpStage sStage[kWarps];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  FactorSmem& sm = *reinterpret_cast<FactorSmem*>(smem_raw);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const WorkItem w = items[blockIdx.x];
   const FactorDev* __restrict__ fp = factors + w.factor;
-
-  if (tid < 12) sT[tid] = relative_pose_entry(poses + 12 * fp->tgt, poses + 12 * fp->src, tid);
+  const float4* __restrict__ gpa = fp->pa;
+  const float4* __restrict__ gpb = fp->pb;
+  const float* __restrict__ gpc = fp->pc;
+  // Warp `warp` processes the item's 64-point tiles warp, warp + kWarps, ... (balanced, no CTA
+  // barrier in the loop); lane 0 streams them into the warp's ring with TMA bulk copies.
+  const int ntiles_all = (w.end - w.begin + kWarpTile - 1) / kWarpTile;
+  const int my_tiles = ntiles_all > warp ? (ntiles_all - warp + kWarps - 1) / kWarps : 0;
+  unsigned long long* bars = sm.bar[warp];
+  auto issue_tile = [&](int k) {  // k-th tile of this warp -> ring slot k % kStages
+    const int stage = k % kStages;
+    const int base = w.begin + (warp + k * kWarps) * kWarpTile;
+    const int cnt = min(kWarpTile, w.end - base);
+    const unsigned ba = static_cast<unsigned>(cnt) * 16u;
+    const unsigned bc = static_cast<unsigned>((cnt + 3) & ~3) * 4u;  // clouds are padded to 256 B
+    WarpTile& dst = sm.u.ring[warp][stage];
+    mbar_expect_tx(&bars[stage], 2u * ba + bc);
+    bulk_g2s(dst.pa, gpa + base, ba, &bars[stage]);
+    bulk_g2s(dst.pb, gpb + base, ba, &bars[stage]);
+    bulk_g2s(dst.pc, gpc + base, bc, &bars[stage]);
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < kStages; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = 0; k < kStages && k < my_tiles; ++k) issue_tile(k);
+  }
+  if (tid < 12) sm.T[tid] = relative_pose_entry(poses + 12 * fp->tgt, poses + 12 * fp->src, tid);
+  __syncthreads();
+  if (tid < 9) sm.Rf[tid] = (float)sm.T[tid];
   __syncthreads();
 
-  const float4* __restrict__ pa = fp->pa;
-  const float4* __restrict__ pb = fp->pb;
-  const float* __restrict__ pc = fp->pc;
   const MapDev map = fp->map;
-  WarpStage& st = sStage[warp];
-
-  // T_ts stays in shared memory (broadcast reads) to keep registers for in-flight probes.
-  const double* T = sT;
-  __shared__ float sRf[9];
-  if (tid < 9) sRf[tid] = (float)sT[tid];
-  __syncthreads();
+  const double* T = sm.T;  // T_ts stays in shared memory (broadcast reads)
+  WarpStage& st = sm.stage[warp];
   const unsigned lane_lt = (1u << lane) - 1u;
 
   float acc[kAcc];
@@ -107,19 +171,26 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
   for (int k = 0; k < kAcc; ++k) acc[k] = 0.f;
   int inl = 0;
 
-  for (int tb = w.begin + warp * kWarpTile; tb < w.end; tb += kTile) {
+  for (int k = 0; k < my_tiles; ++k) {
+    const int stage = k % kStages;
+    while (!mbar_try_wait(&bars[stage], (k / kStages) & 1)) {
+    }
+    const WarpTile& tb = sm.u.ring[warp][stage];
+    const int tile_n = min(kWarpTile, w.end - (w.begin + (warp + k * kWarps) * kWarpTile));
+    const int wbase = 0;
+
     // ---- phase 1: transform, exact key, both bucket loads for kILP points per lane ----
     unsigned hi[kILP], lo[kILP], b1[kILP], b2[kILP];
     bool ok[kILP];
 #pragma unroll
     for (int u = 0; u < kILP; ++u) {
       const int p = u * 32 + lane;
-      const int i = min(tb + p, w.end - 1);  // clamped: every lane computes, only in-range lanes count
-      const float4 A = __ldg(pa + i);
+      const int lp = min(wbase + p, tile_n - 1);  // clamped: every lane computes, in-range lanes count
+      const float4 A = tb.pa[lp];
       double q0, q1, q2, l0, l1, l2;
       apply_pose_rn(T, A.x, A.y, A.z, q0, q1, q2);
       unsigned k0 = 0, k1 = 0, k2 = 0;
-      ok[u] = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && (tb + p < w.end);
+      ok[u] = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && (wbase + p < tile_n);
       pack_key32(k0, k1, k2, hi[u], lo[u]);
       b1[u] = bucket1(k0, k1, k2, map.shift);
       b2[u] = bucket2(k0, k1, k2, map.shift);
@@ -129,7 +200,6 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
       st.qx[p] = (float)q0;
       st.qy[p] = (float)q1;
       st.qz[p] = (float)q2;
-      st.sxx[p] = A.w;
     }
     BucketPair bp[kILP];
 #pragma unroll
@@ -152,16 +222,16 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
     // ---- phase 2: per-hit fp32 algebra over the compacted list (all lanes busy) ----
     for (int e = lane; e < cnt; e += 32) {
       const int p = st.list[e];
-      const int i = tb + p;
+      const int lp = wbase + p;
       const int sl = st.slot[p];
       float4 v0, v1;  // (mx my mz cxx) (cxy cxz cyy cyz)
       ldg256(map.sa + sl, reinterpret_cast<unsigned&>(v0.x), reinterpret_cast<unsigned&>(v0.y),
              reinterpret_cast<unsigned&>(v0.z), reinterpret_cast<unsigned&>(v0.w), reinterpret_cast<unsigned&>(v1.x),
              reinterpret_cast<unsigned&>(v1.y), reinterpret_cast<unsigned&>(v1.z), reinterpret_cast<unsigned&>(v1.w));
       const float2 v2 = __ldg(reinterpret_cast<const float2*>(map.sb + sl));  // czz vid
-      const float4 B = __ldg(pb + i);    // sxy sxz syy syz
-      const float szz = __ldg(pc + i);
-      const float sxx = st.sxx[p], sxy = B.x, sxz = B.y, syy = B.z, syz = B.w;
+      const float4 B = tb.pb[lp];  // sxy sxz syy syz
+      const float szz = tb.pc[lp];
+      const float sxx = tb.pa[lp].w, sxy = B.x, sxz = B.y, syy = B.z, syz = B.w;
 
       // residual e = mu' - q in voxel-local coordinates
       const float e0 = v0.x - st.lx[p];
@@ -169,9 +239,9 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
       const float e2 = v0.z - st.lz[p];
 
       // M = C_t + R C_s Rᵀ (fp32)
-      const float r00 = sRf[0], r01 = sRf[1], r02 = sRf[2];
-      const float r10 = sRf[3], r11 = sRf[4], r12 = sRf[5];
-      const float r20 = sRf[6], r21 = sRf[7], r22 = sRf[8];
+      const float r00 = sm.Rf[0], r01 = sm.Rf[1], r02 = sm.Rf[2];
+      const float r10 = sm.Rf[3], r11 = sm.Rf[4], r12 = sm.Rf[5];
+      const float r20 = sm.Rf[6], r21 = sm.Rf[7], r22 = sm.Rf[8];
       const float t00 = r00 * sxx + r01 * sxy + r02 * sxz;
       const float t01 = r00 * sxy + r01 * syy + r02 * syz;
       const float t02 = r00 * sxz + r01 * syz + r02 * szz;
@@ -208,7 +278,7 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
         o22 = a22 * inv;
       } else {
         float om[6];
-        if (!omega_fp64(sT, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.y), om)) continue;
+        if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.y), om)) continue;
         o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
       }
       const float w0 = o00 * e0 + o01 * e1 + o02 * e2;
@@ -255,37 +325,47 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
         acc[27] += e0 * w0 + e1 * w1 + e2 * w2;
       }
     }
-    __syncwarp();
+    __syncwarp();  // the warp is done with this ring slot
+    if (lane == 0 && k + kStages < my_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async refill
+      issue_tile(k + kStages);
+    }
   }
+  __syncthreads();  // all warps done with their rings before the reduction reuses them
 
-  // ---- CTA reduction: warp shuffle in fp64, then fixed-order sum over warps ----
+
+  // ---- CTA reduction: transpose through shared memory, fp64 column sums in fixed order ----
 #pragma unroll
-  for (int k = 0; k < kAcc; ++k) {
-    double v = acc[k];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-    if (lane == 0) sRed[warp][k] = v;
-  }
+  for (int k = 0; k < kAcc; ++k) sm.u.red[k * kRedStride + tid] = acc[k];  // after the barrier above
   inl = __reduce_add_sync(0xffffffffu, inl);
-  if (lane == 0) sInl[warp] = inl;
+  if (lane == 0) sm.inl[warp] = inl;
+  __syncthreads();
+  if (tid < kAcc * 8) {
+    const int c = tid >> 3, part = tid & 7;
+    const float* col = sm.u.red + c * kRedStride + part * (kFactorThreads / 8);
+    double s = 0.0;
+#pragma unroll 8
+    for (int r = 0; r < kFactorThreads / 8; ++r) s += col[r];
+    sm.part[c][part] = s;
+  }
   __syncthreads();
   if (tid < kAcc) {
-    double s = sRed[0][tid];
+    double s = sm.part[tid][0];
 #pragma unroll
-    for (int q = 1; q < kWarps; ++q) s += sRed[q][tid];
+    for (int q = 1; q < 8; ++q) s += sm.part[tid][q];
     partials[(size_t)blockIdx.x * kPartialStride + tid] = s;
   }
   if (tid == kAcc) {
     int s = 0;
 #pragma unroll
-    for (int q = 0; q < kWarps; ++q) s += sInl[q];
+    for (int q = 0; q < kWarps; ++q) s += sm.inl[q];
     part_inl[blockIdx.x] = s;
   }
   __threadfence();
   __syncthreads();
-  if (tid == 0) sLast = (atomicAdd(&counters[w.factor], 1u) + 1u == (unsigned)fp->item_count);
+  if (tid == 0) sm.last = (atomicAdd(&counters[w.factor], 1u) + 1u == (unsigned)fp->item_count);
   __syncthreads();
-  if (!sLast) return;
+  if (!sm.last) return;
   __threadfence();
 
   // ---- last CTA of this factor: item-ordered sum of partials, then the fp64 epilogue ----
@@ -293,20 +373,20 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
   if (tid < kAcc) {
     double s = 0.0;
     for (int it = 0; it < ic; ++it) s += __ldcg(&partials[(size_t)(ib + it) * kPartialStride + tid]);
-    sTot[tid] = s;
+    sm.tot[tid] = s;
   }
   if (tid == 32) {
     int s = 0;
     for (int it = 0; it < ic; ++it) s += __ldcg(&part_inl[ib + it]);
-    sTotInl = s;
+    sm.tot_inl = s;
   }
   if (tid == 0) counters[w.factor] = 0u;  // ready for the next launch
   __syncthreads();
 
   if constexpr (!kLinearize) {
     if (tid == 0) {
-      out[w.factor] = sTot[0];
-      out_inl[w.factor] = sTotInl;
+      out[w.factor] = sm.tot[0];
+      out_inl[w.factor] = sm.tot_inl;
     }
     return;
   } else {
@@ -317,55 +397,55 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
       // H_tt = [[Q, P], [Pᵀ, Ω]]
       const int qi[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
       double h;
-      if (i < 3 && j < 3) h = sTot[qi[i][j]];
-      else if (i < 3) h = sTot[6 + 3 * i + (j - 3)];
-      else if (j < 3) h = sTot[6 + 3 * j + (i - 3)];
-      else h = sTot[15 + qi[i - 3][j - 3]];
-      sH[tid] = h;
+      if (i < 3 && j < 3) h = sm.tot[qi[i][j]];
+      else if (i < 3) h = sm.tot[6 + 3 * i + (j - 3)];
+      else if (j < 3) h = sm.tot[6 + 3 * j + (i - 3)];
+      else h = sm.tot[15 + qi[i - 3][j - 3]];
+      sm.H[tid] = h;
       // Ad(T_ts) = [[R, 0], [[t]x R, R]]
       double ad = 0.0;
-      if (i < 3 && j < 3) ad = sT[3 * i + j];
-      else if (i >= 3 && j >= 3) ad = sT[3 * (i - 3) + (j - 3)];
+      if (i < 3 && j < 3) ad = sm.T[3 * i + j];
+      else if (i >= 3 && j >= 3) ad = sm.T[3 * (i - 3) + (j - 3)];
       else if (i >= 3 && j < 3) {
         const int r = i - 3;
-        const double tx = sT[9], ty = sT[10], tz = sT[11];
+        const double tx = sm.T[9], ty = sm.T[10], tz = sm.T[11];
         const double sk[3][3] = {{0.0, -tz, ty}, {tz, 0.0, -tx}, {-ty, tx, 0.0}};
-        ad = dot3_rn(sk[r][0], sk[r][1], sk[r][2], sT[j], sT[3 + j], sT[6 + j]);
+        ad = dot3_rn(sk[r][0], sk[r][1], sk[r][2], sm.T[j], sm.T[3 + j], sm.T[6 + j]);
       }
-      sAd[tid] = ad;
+      sm.Ad[tid] = ad;
     }
     __syncthreads();
     if (tid < 36) {
       const int i = tid / 6, j = tid % 6;
       double s = 0.0;
 #pragma unroll
-      for (int m = 0; m < 6; ++m) s += sH[6 * i + m] * sAd[6 * m + j];
-      sHA[tid] = s;  // H_tt · Ad
+      for (int m = 0; m < 6; ++m) s += sm.H[6 * i + m] * sm.Ad[6 * m + j];
+      sm.HA[tid] = s;  // H_tt · Ad
     }
     __syncthreads();
     if (tid < 36) {
       const int i = tid / 6, j = tid % 6;
       double s = 0.0;
 #pragma unroll
-      for (int m = 0; m < 6; ++m) s += sAd[6 * m + i] * sHA[6 * m + j];
-      sHss[tid] = s;  // Adᵀ · H_tt · Ad
+      for (int m = 0; m < 6; ++m) s += sm.Ad[6 * m + i] * sm.HA[6 * m + j];
+      sm.Hss[tid] = s;  // Adᵀ · H_tt · Ad
     }
     __syncthreads();
     if (tid < 36) {
       const int i = tid / 6, j = tid % 6;
-      o[tid] = sH[tid];                                       // H_ii (exactly symmetric)
-      o[36 + tid] = -sHA[tid];                                // H_ij
-      o[72 + tid] = 0.5 * (sHss[6 * i + j] + sHss[6 * j + i]);  // H_jj, symmetrised (factors.cpp:141)
+      o[tid] = sm.H[tid];                                             // H_ii (exactly symmetric)
+      o[36 + tid] = -sm.HA[tid];                                      // H_ij
+      o[72 + tid] = 0.5 * (sm.Hss[6 * i + j] + sm.Hss[6 * j + i]);    // H_jj, symmetrised (factors.cpp:141)
     } else if (tid < 42) {
       const int i = tid - 36;
-      o[108 + i] = sTot[21 + i];  // b_i = b_t
+      o[108 + i] = sm.tot[21 + i];  // b_i = b_t
       double s = 0.0;
 #pragma unroll
-      for (int m = 0; m < 6; ++m) s += sAd[6 * m + i] * sTot[21 + m];
+      for (int m = 0; m < 6; ++m) s += sm.Ad[6 * m + i] * sm.tot[21 + m];
       o[114 + i] = -s;  // b_j = -Adᵀ b_t
     } else if (tid == 42) {
-      o[120] = sTot[27];
-      out_inl[f] = sTotInl;
+      o[120] = sm.tot[27];
+      out_inl[f] = sm.tot_inl;
     }
   }
 }
@@ -407,12 +487,21 @@ cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkIt
                           const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
                           int* out_inl, cudaStream_t s) {
   if (num_items <= 0) return cudaSuccess;
+  constexpr size_t kSmem = sizeof(FactorSmem);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(factor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
   if (linearize)
-    factor_kernel<true><<<num_items, kFactorThreads, 0, s>>>(factors, items, poses, partials, part_inl, counters,
-                                                            out, out_inl);
+    factor_kernel<true><<<num_items, kFactorThreads, kSmem, s>>>(factors, items, poses, partials, part_inl, counters,
+                                                                out, out_inl);
   else
-    factor_kernel<false><<<num_items, kFactorThreads, 0, s>>>(factors, items, poses, partials, part_inl, counters,
-                                                             out, out_inl);
+    factor_kernel<false><<<num_items, kFactorThreads, kSmem, s>>>(factors, items, poses, partials, part_inl,
+                                                                 counters, out, out_inl);
   return cudaGetLastError();
 }
 

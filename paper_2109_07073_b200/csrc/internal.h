@@ -99,8 +99,8 @@ cudaError_t launch_build_counts(const BuildSeg* segs, int m, const unsigned* hea
 cudaError_t launch_build_accumulate(const BuildSeg* segs, const BuildOut* outs, int m, unsigned max_n,
                                     const unsigned long long* keys, const unsigned* vals, const unsigned* heads,
                                     const unsigned* vidx, VoxelStats* hot, cudaStream_t s);
-cudaError_t launch_build_insert(const InsertJob* jobs, int m, unsigned max_v, const VoxelStats* hot, int* overflow,
-                                cudaStream_t s);
+cudaError_t launch_build_insert(const InsertJob* jobs, int m, unsigned max_v, int* overflow, cudaStream_t s);
+cudaError_t launch_build_place(const InsertJob* jobs, int m, unsigned max_v, const VoxelStats* hot, cudaStream_t s);
 cudaError_t launch_lookup(MapDev map, const double* pts, size_t n, unsigned long long* keys_out, cudaStream_t s);
 cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsigned long long* hits, cudaStream_t s);
 cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkItem* items, int num_items,

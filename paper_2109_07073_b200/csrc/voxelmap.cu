@@ -139,34 +139,54 @@ __global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const
   }
 }
 
-// Two-choice insertion (64-bit atomicCAS on key slots): try the emptier of the key's two
-// buckets first, then the other; a key that finds both full flags the map for a rebuild with
-// twice the buckets. Slot positions may differ between runs; lookups never do.
-__global__ void build_insert_kernel(const InsertJob* __restrict__ jobs, const VoxelStats* __restrict__ hot,
-                                    int* __restrict__ overflow) {
+// Bucketized cuckoo insertion of the keys (2 choices × 4 slots): a thread claims an empty slot in
+// either of its key's buckets with atomicCAS; when both are full it evicts a resident key with
+// atomicExch and carries the victim to the victim's other bucket. Every key is always either in
+// the table or carried by exactly one thread, so the table is complete when all threads finish;
+// a walk longer than kMaxKicks flags the map for a rebuild with twice the buckets. Slot positions
+// depend on scheduling; lookup results never do.
+constexpr int kMaxKicks = 256;
+
+__global__ void build_insert_kernel(const InsertJob* __restrict__ jobs, int* __restrict__ overflow) {
+  const InsertJob j = jobs[blockIdx.y];
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < j.voxels; v += gridDim.x * blockDim.x) {
+    unsigned long long cur = j.keys[v];
+    unsigned from = 0xFFFFFFFFu;  // bucket the carried key was evicted from
+    bool placed = false;
+    for (int kick = 0; kick < kMaxKicks && !placed; ++kick) {
+      unsigned k0, k1, k2;
+      unpack_key(cur, k0, k1, k2);
+      const unsigned bb[2] = {bucket1(k0, k1, k2, j.shift), bucket2(k0, k1, k2, j.shift)};
+      for (int c = 0; c < 2 && !placed; ++c) {
+        if (bb[c] == from) continue;
+        for (int q = 0; q < kBucket && !placed; ++q)
+          placed = atomicCAS(&j.tkeys[kBucket * bb[c] + q], kEmptyKey, cur) == kEmptyKey;
+      }
+      if (placed) break;
+      // both candidate buckets full: evict from the bucket we did not just come from
+      const unsigned b = (from == bb[0]) ? bb[1] : (from == bb[1]) ? bb[0] : bb[kick & 1];
+      const unsigned victim_slot = kBucket * b + ((v + kick) & (kBucket - 1));
+      cur = atomicExch(&j.tkeys[victim_slot], cur);
+      from = b;
+      if (cur == kEmptyKey) placed = true;  // the slot emptied meanwhile: nothing to carry
+    }
+    if (!placed) atomicOr(&overflow[blockIdx.y], 1);
+  }
+}
+
+// After insertion: every voxel finds its slot and writes its fp32 statistics there.
+__global__ void build_place_kernel(const InsertJob* __restrict__ jobs, const VoxelStats* __restrict__ hot) {
   const InsertJob j = jobs[blockIdx.y];
   for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < j.voxels; v += gridDim.x * blockDim.x) {
     const unsigned long long key = j.keys[v];
     unsigned k0, k1, k2;
     unpack_key(key, k0, k1, k2);
-    const unsigned b1 = bucket1(k0, k1, k2, j.shift), b2 = bucket2(k0, k1, k2, j.shift);
-    int free1 = 0, free2 = 0;
-#pragma unroll
-    for (int q = 0; q < kBucket; ++q) {
-      free1 += j.tkeys[kBucket * b1 + q] == kEmptyKey;
-      free2 += j.tkeys[kBucket * b2 + q] == kEmptyKey;
-    }
-    const unsigned order[2] = {free2 > free1 ? b2 : b1, free2 > free1 ? b1 : b2};
+    const unsigned bb[2] = {bucket1(k0, k1, k2, j.shift), bucket2(k0, k1, k2, j.shift)};
     int slot = -1;
-    for (int c = 0; c < 2 && slot < 0; ++c)
-      for (int q = 0; q < kBucket && slot < 0; ++q) {
-        const unsigned sidx = kBucket * order[c] + q;
-        if (atomicCAS(&j.tkeys[sidx], kEmptyKey, key) == kEmptyKey) slot = static_cast<int>(sidx);
-      }
-    if (slot < 0) {
-      atomicOr(&overflow[blockIdx.y], 1);
-      continue;
-    }
+    for (int c = 0; c < 2; ++c)
+      for (int q = 0; q < kBucket; ++q)
+        if (j.tkeys[kBucket * bb[c] + q] == key) slot = kBucket * bb[c] + q;
+    if (slot < 0) continue;  // cannot happen after a successful insert pass
     const VoxelStats h = hot[j.vbase + v];
     SlotStatsA a;
     a.mx = h.mx, a.my = h.my, a.mz = h.mz, a.cxx = h.cxx, a.cxy = h.cxy, a.cxz = h.cxz, a.cyy = h.cyy, a.cyz = h.cyz;
@@ -270,9 +290,13 @@ cudaError_t launch_build_accumulate(const BuildSeg* segs, const BuildOut* outs, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_build_insert(const InsertJob* jobs, int m, unsigned max_v, const VoxelStats* hot, int* overflow,
-                                cudaStream_t s) {
-  build_insert_kernel<<<dim3(grid_for(max_v, 128, 4096), m), 128, 0, s>>>(jobs, hot, overflow);
+cudaError_t launch_build_insert(const InsertJob* jobs, int m, unsigned max_v, int* overflow, cudaStream_t s) {
+  build_insert_kernel<<<dim3(grid_for(max_v, 128, 4096), m), 128, 0, s>>>(jobs, overflow);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_place(const InsertJob* jobs, int m, unsigned max_v, const VoxelStats* hot, cudaStream_t s) {
+  build_place_kernel<<<dim3(grid_for(max_v, 128, 4096), m), 128, 0, s>>>(jobs, hot);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,232 @@
+"""Levenberg–Marquardt over matching-cost factors with batched GPU linearization.
+
+Host-side caller of the hot path, mirroring proj/src/optimizer.cpp:88-194 for graphs whose
+factors are all VGICP matching-cost factors: every accepted estimate is re-linearized with ONE
+launch for all factors (FactorGraph.linearize, the linearize_all of optimizer.cpp:45-62), every
+candidate is scored with ONE error-only launch (total_error, optimizer.cpp:66-75, summed in factor
+order on the host), Marquardt damping diag += λ·max(diag, 1e-10) (optimizer.cpp:119-123), step
+acceptance iff the error decreases, λ ×0.1 / ×10, termination on relative decrease < 1e-6, step
+norm < 1e-8, λ > 1e10 or max iterations. Gauge: the first pose of every connected component
+without a fixed variable is anchored (optimizer.cpp:24-43). The reduced normal equations are
+solved with a dense Cholesky (the reference's block Cholesky, block_solver.cpp:64-123, is ~3% of
+the time per PAPER.md:410; a failed factorization escalates λ like the reference's failed pivot).
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .vgicp import FactorGraph, poses_array
+
+SMALL_ANGLE = 1e-8  # se3.cpp:10
+ORTHONORMALIZE_EVERY = 50  # se3.cpp:11
+
+
+def skew(v):
+    return np.array([[0.0, -v[2], v[1]], [v[2], 0.0, -v[0]], [-v[1], v[0], 0.0]])
+
+
+def so3_exp(w):  # se3.cpp:46-55
+    th = float(np.linalg.norm(w))
+    W = skew(w)
+    if th < SMALL_ANGLE:
+        return np.eye(3) + W + 0.5 * (W @ W)
+    return np.eye(3) + (np.sin(th) / th) * W + ((1.0 - np.cos(th)) / (th * th)) * (W @ W)
+
+
+def so3_left_jacobian(w):  # se3.cpp:14-24
+    th = float(np.linalg.norm(w))
+    W = skew(w)
+    if th < SMALL_ANGLE:
+        return np.eye(3) + 0.5 * W + (W @ W) / 6.0
+    t2 = th * th
+    return np.eye(3) + ((1.0 - np.cos(th)) / t2) * W + ((th - np.sin(th)) / (t2 * th)) * (W @ W)
+
+
+def se3_exp(xi) -> np.ndarray:  # se3.cpp:74-78, rotation part first
+    xi = np.asarray(xi, np.float64)
+    R = so3_exp(xi[:3])
+    t = so3_left_jacobian(xi[:3]) @ xi[3:]
+    return np.concatenate([R.reshape(9), t])
+
+
+def compose(a, b) -> np.ndarray:  # se3.cpp:42-44
+    Ra, Rb = a[:9].reshape(3, 3), b[:9].reshape(3, 3)
+    return np.concatenate([(Ra @ Rb).reshape(9), Ra @ b[9:] + a[9:]])
+
+
+def orthonormalized(T) -> np.ndarray:  # se3.cpp:80-91 (polar projection)
+    U, _, Vt = np.linalg.svd(T[:9].reshape(3, 3))
+    if np.linalg.det(U @ Vt) < 0:
+        U[:, 2] = -U[:, 2]
+    return np.concatenate([(U @ Vt).reshape(9), T[9:]])
+
+
+@dataclass
+class LmSettings:  # optimizer.hpp:12-21
+    max_iterations: int = 50
+    lambda_init: float = 1e-5
+    lambda_increase: float = 10.0
+    lambda_decrease: float = 0.1
+    lambda_max: float = 1e10
+    relative_error_decrease: float = 1e-6
+    step_norm_tolerance: float = 1e-8
+
+
+@dataclass
+class IterationRecord:  # optimizer.hpp:33-39
+    iteration: int
+    error: float
+    lam: float
+    step_norm: float
+    accepted: bool
+
+
+@dataclass
+class OptimizerReport:  # optimizer.hpp:41-50
+    iterations: int = 0
+    initial_error: float = 0.0
+    final_error: float = 0.0
+    trace: list = field(default_factory=list)
+    reason: str = "max_iterations"
+    wall_time_seconds: float = 0.0
+    aborted: bool = False
+    diagnostic: str = ""
+    iteration_seconds: list = field(default_factory=list)  # wall time of each outer iteration
+
+
+def effective_fixed_mask(num_poses: int, ij, fixed) -> np.ndarray:  # optimizer.cpp:24-43
+    parent = list(range(num_poses))
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    for i, j in ij:
+        parent[find(i)] = find(j)
+    out = np.array(fixed, dtype=bool).copy()
+    has = {}
+    for v in range(num_poses):
+        if out[v]:
+            has[find(v)] = True
+    for v in range(num_poses):
+        r = find(v)
+        if not has.get(r, False):
+            out[v] = True
+            has[r] = True
+    return out
+
+
+def assemble(raw: np.ndarray, ij: np.ndarray, num_poses: int):
+    """Dense normal equations from 121-double factor blocks (block_solver.cpp:14-62 semantics)."""
+    n6 = 6 * num_poses
+    H = np.zeros((n6, n6))
+    b = np.zeros(n6)
+    for f in range(len(raw)):
+        i, j = int(ij[f, 0]), int(ij[f, 1])
+        r = raw[f]
+        si, sj = slice(6 * i, 6 * i + 6), slice(6 * j, 6 * j + 6)
+        Hij = r[36:72].reshape(6, 6)
+        H[si, si] += r[0:36].reshape(6, 6)
+        H[sj, sj] += r[72:108].reshape(6, 6)
+        H[si, sj] += Hij
+        H[sj, si] += Hij.T
+        b[si] += r[108:114]
+        b[sj] += r[114:120]
+    return H, b
+
+
+def solve_damped(H, b, active, lam):
+    """Cholesky solve of the damped reduced system; None when not positive definite."""
+    idx = np.concatenate([np.arange(6 * v, 6 * v + 6) for v in np.flatnonzero(active)]) if active.any() else np.zeros(0, int)
+    Hr = H[np.ix_(idx, idx)].copy()
+    d = np.diag(Hr).copy()
+    Hr[np.diag_indices_from(Hr)] = d + lam * np.maximum(d, 1e-10)
+    try:
+        L = np.linalg.cholesky(Hr)
+    except np.linalg.LinAlgError:
+        return None
+    y = np.linalg.solve(L, b[idx]) if len(idx) else np.zeros(0)
+    x = np.linalg.solve(L.T, y) if len(idx) else np.zeros(0)
+    delta = np.zeros_like(b)
+    delta[idx] = x
+    return delta
+
+
+def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None = None):
+    """Run LM on `graph` from `poses` (num_poses × 12). Returns (poses, OptimizerReport)."""
+    settings = settings or LmSettings()
+    t_start = time.perf_counter()
+    report = OptimizerReport()
+    poses = poses_array(poses).copy()
+    n = len(poses)
+    ij = graph._ij
+    fixed_mask = effective_fixed_mask(n, ij, np.zeros(n, bool) if fixed is None else fixed)
+    active = ~fixed_mask
+    updates = np.zeros(n, dtype=np.int64)
+
+    raw, _ = graph.linearize_raw(poses)
+    current = graph.total_error(poses)
+    report.initial_error = report.final_error = current
+    lam = settings.lambda_init
+    any_accepted = False
+    for it in range(settings.max_iterations):
+        t_it = time.perf_counter()
+        H, b = assemble(raw, ij, n)
+        accepted = False
+        while True:
+            delta = solve_damped(H, b, active, lam)
+            if delta is None:
+                lam *= settings.lambda_increase
+                if lam > settings.lambda_max:
+                    if not any_accepted:
+                        report.aborted = True
+                        report.reason = "solver_abort"
+                        report.diagnostic = "linear solve failed at maximum damping; poses unchanged"
+                    else:
+                        report.reason = "lambda_limit"
+                    break
+                continue
+            step_norm = float(np.linalg.norm(delta))
+            if step_norm < settings.step_norm_tolerance:
+                report.trace.append(IterationRecord(it, current, lam, step_norm, False))
+                report.reason = "converged_step_norm"
+                break
+            cand = poses.copy()
+            cand_updates = updates.copy()
+            for v in np.flatnonzero(active):
+                cand[v] = compose(poses[v], se3_exp(delta[6 * v:6 * v + 6]))  # Pose::retract (se3.cpp:93-101)
+                cand_updates[v] += 1
+                if cand_updates[v] >= ORTHONORMALIZE_EVERY:
+                    cand[v] = orthonormalized(cand[v])
+                    cand_updates[v] = 0
+            cand_error = graph.total_error(cand)
+            if cand_error < current:
+                decrease = (current - cand_error) / max(current, 1e-300)
+                poses, updates = cand, cand_updates
+                any_accepted = accepted = True
+                report.trace.append(IterationRecord(it, cand_error, lam, step_norm, True))
+                current = cand_error
+                lam = max(lam * settings.lambda_decrease, 1e-12)
+                report.iterations += 1
+                report.reason = "converged_relative_error" if decrease < settings.relative_error_decrease else report.reason
+                break
+            report.trace.append(IterationRecord(it, current, lam, step_norm, False))
+            lam *= settings.lambda_increase
+            if lam > settings.lambda_max:
+                report.reason = "lambda_limit"
+                break
+        if not accepted or report.reason == "converged_relative_error":
+            report.iteration_seconds.append(time.perf_counter() - t_it)
+            break
+        raw, _ = graph.linearize_raw(poses)
+        report.reason = "max_iterations"
+        report.iteration_seconds.append(time.perf_counter() - t_it)
+    if not report.aborted:
+        report.final_error = current
+    report.wall_time_seconds = time.perf_counter() - t_start
+    return poses, report
