@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--chunk", type=int, default=0)
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU work for cpu_baseline")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-lm", action="store_true", help="skip the C2 full-LM leg")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu / e2e legs)")
     return p.parse_args()
 
@@ -189,6 +190,28 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------------ C2 LM
+def run_lm_c2(ctx, threads):
+    """BASELINE config C2: 100-frame circle, factors (k-d -> k), d = 1..3 (294 factors), full LM to
+    convergence with default LmSettings (optimizer.hpp:12-21). Each iteration = assemble + damped
+    solve (+ retries) + candidate error launch(es) + re-linearization launch, wall clock."""
+    from paper_2109_07073_b200 import optimizer as LM
+    from paper_2109_07073_b200 import workloads as W
+
+    wl = W.build_graph_workload(ctx, W.c2_spec(), links=W.c2_links(100), threads=threads)
+    LM.optimize(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=2))  # warm-up
+    poses, rep = LM.optimize(wl.graph, wl.poses)
+    its = sorted(rep.iteration_seconds)
+    return {
+        "factors": wl.num_factors, "poses": len(wl.poses), "iterations": rep.iterations,
+        "ms_per_lm_iteration_median": 1e3 * its[len(its) // 2] if its else None,
+        "ms_total": 1e3 * rep.wall_time_seconds, "initial_error": rep.initial_error, "final_error": rep.final_error,
+        "reason": rep.reason,
+        "note": "host LM (paper_2109_07073_b200/optimizer.py, dense Cholesky) around one linearize launch per "
+                "accepted step and one error launch per candidate; wall clock incl. H2D/D2H",
+    }
+
+
 # ------------------------------------------------------------------------------ ours
 def run_ours(args):
     import torch
@@ -323,6 +346,10 @@ def run_ours(args):
         traffic = json.loads(tf.read_text()).get("bytes_per_launch")
     data_bytes = sum(36 * len(m) for m in wl.scans.means) + sum(48 * int(m.size()) * 2 for m in wl.maps)
 
+    lm = None
+    if world == 1 and not args.profile and not args.no_lm:
+        lm = run_lm_c2(ctx, threads)
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
         threads_all = os.cpu_count() or 1
@@ -354,6 +381,7 @@ def run_ours(args):
                      "bytes_alg_per_launch": bytes_alg,
                      "bytes_alg_formula": "36*sum(N_f) + 44*sum(inliers_f) + 116*F (SURVEY 8d)"},
         "cpu_baseline": cpu,
+        "lm_c2": lm,
         "clocks": clk,
         "inlier_fraction": inliers / P,
         "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()} | {"total": round(t_build, 3)},

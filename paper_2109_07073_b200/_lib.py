@@ -9,7 +9,9 @@ import ctypes as C
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "lib" / "libvgicp_b200.so"
+import os as _os
+
+LIB_PATH = Path(_os.environ["VGICP_LIB"]) if _os.environ.get("VGICP_LIB") else PKG / "lib" / "libvgicp_b200.so"
 HEADER = PKG.parent / "include" / "vgicp_b200.h"
 
 LINEARIZED_DOUBLES = 121

@@ -663,8 +663,8 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   };
   const size_t o_f = carve(sizeof(FactorDev) * nf);
   const size_t o_i = carve(sizeof(WorkItem) * ni);
-  const size_t o_p = carve(sizeof(double) * kPartialStride * ni);
-  const size_t o_pi = carve(sizeof(int) * ni);
+  const size_t o_p = carve(sizeof(double) * kPartialStride * kFactorWarps * ni);  // one partial per warp
+  const size_t o_pi = carve(sizeof(int) * kFactorWarps * ni);
   const size_t o_c = carve(sizeof(unsigned) * nf);
   const size_t o_pose = carve(sizeof(double) * 12 * std::max(num_poses, 1));
   const size_t o_out = carve(sizeof(double) * VGICP_LINEARIZED_DOUBLES * nf);

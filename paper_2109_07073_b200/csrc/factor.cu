@@ -50,10 +50,16 @@ __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, f
   return true;
 }
 
-constexpr int kILP = 2;                        // points per lane per tile (independent probes in flight)
+#ifndef VG_ILP
+#define VG_ILP 2
+#endif
+#ifndef VG_STAGES
+#define VG_STAGES 3
+#endif
+constexpr int kILP = VG_ILP;                        // points per lane per tile (independent probes in flight)
 constexpr int kWarpTile = 32 * kILP;           // points per warp per tile
 constexpr int kTile = kFactorThreads * kILP;   // points per CTA tile
-static_assert(kTile == kFactorTile, "tile size mismatch");
+static_assert(kFactorTile % 4 == 0, "work-item starts must keep c_zz TMA copies 16-B aligned");
 constexpr int kRedStride = kFactorThreads + 1;  // padded column stride of the reduction transpose
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers --------------------------------------------------
@@ -85,7 +91,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // Shared memory of one CTA. Every warp owns a private kStages-deep ring of source tiles that it
 // fills itself with TMA bulk copies (cp.async.bulk, mbarrier completion), so warps never wait on
 // each other inside the point loop; after the loop the rings are reused for the reduction.
-constexpr int kStages = 3;
+constexpr int kStages = VG_STAGES;
 struct WarpTile {
   float4 pa[kWarpTile];  // x y z c_xx
   float4 pb[kWarpTile];  // c_xy c_xz c_yy c_yz
@@ -100,21 +106,14 @@ struct WarpStage {
 struct __align__(128) FactorSmem {
   union {
     WarpTile ring[kWarps][kStages];
-    float red[kLinAcc * kRedStride];
   } u;
   WarpStage stage[kWarps];
   unsigned long long bar[kWarps][kStages];
   double T[12];
   float Rf[9];
-  double part[kLinAcc][8];
-  double tot[kLinAcc];
-  double H[36], Ad[36], HA[36], Hss[36];
-  int inl[kWarps];
-  int tot_inl;
-  int last;
 };
-static_assert(sizeof(float) * kLinAcc * kRedStride <= sizeof(WarpTile) * kWarps * kStages,
-              "reduction transpose must fit in the tile rings");
+static_assert(sizeof(WarpTile) * kStages >= sizeof(float) * kLinAcc * 33 + 64 * 4 + sizeof(double) * 180,
+              "per-warp reduction scratch must fit in the warp's ring");
 
 template <bool kLinearize>
 __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
@@ -331,77 +330,71 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
       issue_tile(k + kStages);
     }
   }
-  __syncthreads();  // all warps done with their rings before the reduction reuses them
+  __syncwarp();  // this warp is done with its ring (no CTA-wide barrier after the prologue)
 
-
-  // ---- CTA reduction: transpose through shared memory, fp64 column sums in fixed order ----
+  // ---- warp reduction: transpose the warp's 32 x kAcc fp32 sums through its idle ring slot,
+  //      fp64 column sums in fixed order, one partial per warp (no float atomics) ----
+  float* red = reinterpret_cast<float*>(&sm.u.ring[warp][0]);
 #pragma unroll
-  for (int k = 0; k < kAcc; ++k) sm.u.red[k * kRedStride + tid] = acc[k];  // after the barrier above
+  for (int k = 0; k < kAcc; ++k) red[k * 33 + lane] = acc[k];
   inl = __reduce_add_sync(0xffffffffu, inl);
-  if (lane == 0) sm.inl[warp] = inl;
-  __syncthreads();
-  if (tid < kAcc * 8) {
-    const int c = tid >> 3, part = tid & 7;
-    const float* col = sm.u.red + c * kRedStride + part * (kFactorThreads / 8);
-    double s = 0.0;
+  __syncwarp();
+  const size_t gw = (size_t)blockIdx.x * kWarps + warp;  // this warp's partial slot
+  if (lane < kAcc) {
+    double sum = 0.0;
 #pragma unroll 8
-    for (int r = 0; r < kFactorThreads / 8; ++r) s += col[r];
-    sm.part[c][part] = s;
+    for (int r = 0; r < 32; ++r) sum += red[lane * 33 + r];
+    partials[gw * kPartialStride + lane] = sum;
   }
-  __syncthreads();
-  if (tid < kAcc) {
-    double s = sm.part[tid][0];
-#pragma unroll
-    for (int q = 1; q < 8; ++q) s += sm.part[tid][q];
-    partials[(size_t)blockIdx.x * kPartialStride + tid] = s;
-  }
-  if (tid == kAcc) {
-    int s = 0;
-#pragma unroll
-    for (int q = 0; q < kWarps; ++q) s += sm.inl[q];
-    part_inl[blockIdx.x] = s;
-  }
+  if (lane == 0) part_inl[gw] = inl;
   __threadfence();
-  __syncthreads();
-  if (tid == 0) sm.last = (atomicAdd(&counters[w.factor], 1u) + 1u == (unsigned)fp->item_count);
-  __syncthreads();
-  if (!sm.last) return;
+  __syncwarp();
+  unsigned last = 0;
+  if (lane == 0) last = (atomicAdd(&counters[w.factor], 1u) + 1u == (unsigned)(fp->item_count * kWarps)) ? 1u : 0u;
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
   __threadfence();
 
-  // ---- last CTA of this factor: item-ordered sum of partials, then the fp64 epilogue ----
-  const int ib = fp->item_begin, ic = fp->item_count;
-  if (tid < kAcc) {
-    double s = 0.0;
-    for (int it = 0; it < ic; ++it) s += __ldcg(&partials[(size_t)(ib + it) * kPartialStride + tid]);
-    sm.tot[tid] = s;
+  // ---- last warp of this factor: (item, warp)-ordered sum of the partials, fp64 epilogue ----
+  double* ws = reinterpret_cast<double*>(&sm.u.ring[warp][0]) + 64;  // per-warp scratch (after `red`)
+  double* tot = ws;           // 28
+  double* H = ws + 32;        // 36
+  double* Ad = ws + 72;       // 36
+  double* HA = ws + 108;      // 36
+  double* Hss = ws + 144;     // 36
+  const size_t gb = (size_t)fp->item_begin * kWarps;
+  const int gc = fp->item_count * kWarps;
+  if (lane < kAcc) {
+    double sum = 0.0;
+    for (int g = 0; g < gc; ++g) sum += __ldcg(&partials[(gb + g) * kPartialStride + lane]);
+    tot[lane] = sum;
   }
-  if (tid == 32) {
-    int s = 0;
-    for (int it = 0; it < ic; ++it) s += __ldcg(&part_inl[ib + it]);
-    sm.tot_inl = s;
+  int tinl = 0;
+  if (lane == 0) {
+    for (int g = 0; g < gc; ++g) tinl += __ldcg(&part_inl[gb + g]);
+    counters[w.factor] = 0u;  // ready for the next launch
   }
-  if (tid == 0) counters[w.factor] = 0u;  // ready for the next launch
-  __syncthreads();
+  __syncwarp();
 
   if constexpr (!kLinearize) {
-    if (tid == 0) {
-      out[w.factor] = sm.tot[0];
-      out_inl[w.factor] = sm.tot_inl;
+    if (lane == 0) {
+      out[w.factor] = tot[0];
+      out_inl[w.factor] = tinl;
     }
     return;
   } else {
     const int f = w.factor;
     double* o = out + (size_t)f * VGICP_LINEARIZED_DOUBLES;
-    if (tid < 36) {
-      const int i = tid / 6, j = tid % 6;
+    for (int t = lane; t < 36; t += 32) {
+      const int i = t / 6, j = t % 6;
       // H_tt = [[Q, P], [Pᵀ, Ω]]
       const int qi[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
       double h;
-      if (i < 3 && j < 3) h = sm.tot[qi[i][j]];
-      else if (i < 3) h = sm.tot[6 + 3 * i + (j - 3)];
-      else if (j < 3) h = sm.tot[6 + 3 * j + (i - 3)];
-      else h = sm.tot[15 + qi[i - 3][j - 3]];
-      sm.H[tid] = h;
+      if (i < 3 && j < 3) h = tot[qi[i][j]];
+      else if (i < 3) h = tot[6 + 3 * i + (j - 3)];
+      else if (j < 3) h = tot[6 + 3 * j + (i - 3)];
+      else h = tot[15 + qi[i - 3][j - 3]];
+      H[t] = h;
       // Ad(T_ts) = [[R, 0], [[t]x R, R]]
       double ad = 0.0;
       if (i < 3 && j < 3) ad = sm.T[3 * i + j];
@@ -412,40 +405,41 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
         const double sk[3][3] = {{0.0, -tz, ty}, {tz, 0.0, -tx}, {-ty, tx, 0.0}};
         ad = dot3_rn(sk[r][0], sk[r][1], sk[r][2], sm.T[j], sm.T[3 + j], sm.T[6 + j]);
       }
-      sm.Ad[tid] = ad;
+      Ad[t] = ad;
     }
-    __syncthreads();
-    if (tid < 36) {
-      const int i = tid / 6, j = tid % 6;
-      double s = 0.0;
+    __syncwarp();
+    for (int t = lane; t < 36; t += 32) {
+      const int i = t / 6, j = t % 6;
+      double sum = 0.0;
 #pragma unroll
-      for (int m = 0; m < 6; ++m) s += sm.H[6 * i + m] * sm.Ad[6 * m + j];
-      sm.HA[tid] = s;  // H_tt · Ad
+      for (int m = 0; m < 6; ++m) sum += H[6 * i + m] * Ad[6 * m + j];
+      HA[t] = sum;  // H_tt · Ad
     }
-    __syncthreads();
-    if (tid < 36) {
-      const int i = tid / 6, j = tid % 6;
-      double s = 0.0;
+    __syncwarp();
+    for (int t = lane; t < 36; t += 32) {
+      const int i = t / 6, j = t % 6;
+      double sum = 0.0;
 #pragma unroll
-      for (int m = 0; m < 6; ++m) s += sm.Ad[6 * m + i] * sm.HA[6 * m + j];
-      sm.Hss[tid] = s;  // Adᵀ · H_tt · Ad
+      for (int m = 0; m < 6; ++m) sum += Ad[6 * m + i] * HA[6 * m + j];
+      Hss[t] = sum;  // Adᵀ · H_tt · Ad
     }
-    __syncthreads();
-    if (tid < 36) {
-      const int i = tid / 6, j = tid % 6;
-      o[tid] = sm.H[tid];                                             // H_ii (exactly symmetric)
-      o[36 + tid] = -sm.HA[tid];                                      // H_ij
-      o[72 + tid] = 0.5 * (sm.Hss[6 * i + j] + sm.Hss[6 * j + i]);    // H_jj, symmetrised (factors.cpp:141)
-    } else if (tid < 42) {
-      const int i = tid - 36;
-      o[108 + i] = sm.tot[21 + i];  // b_i = b_t
-      double s = 0.0;
+    __syncwarp();
+    for (int t = lane; t < 36; t += 32) {
+      const int i = t / 6, j = t % 6;
+      o[t] = H[t];                                       // H_ii (exactly symmetric)
+      o[36 + t] = -HA[t];                                // H_ij
+      o[72 + t] = 0.5 * (Hss[6 * i + j] + Hss[6 * j + i]);  // H_jj, symmetrised (factors.cpp:141)
+    }
+    if (lane < 6) {
+      o[108 + lane] = tot[21 + lane];  // b_i = b_t
+      double sum = 0.0;
 #pragma unroll
-      for (int m = 0; m < 6; ++m) s += sm.Ad[6 * m + i] * sm.tot[21 + m];
-      o[114 + i] = -s;  // b_j = -Adᵀ b_t
-    } else if (tid == 42) {
-      o[120] = sm.tot[27];
-      out_inl[f] = sm.tot_inl;
+      for (int m = 0; m < 6; ++m) sum += Ad[6 * m + lane] * tot[21 + m];
+      o[114 + lane] = -sum;  // b_j = -Adᵀ b_t
+    }
+    if (lane == 0) {
+      o[120] = tot[27];
+      out_inl[f] = tinl;
     }
   }
 }

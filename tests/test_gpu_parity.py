@@ -215,6 +215,7 @@ def check_factor(fac, smm, sc9, omap, Tt, Ts, h_tol=H_TOL, e_tol=ERR_TOL):
     err, inl = V.evaluate_matching_cost(fac, Tt, Ts)
     ref_err, ref_inl = O.evaluate(smm, sc9, omap, Tt, Ts)
     assert inl == ref_inl
+    assert err == lin.error  # same per-point arithmetic and reduction order in both kernels
     assert abs(err - ref_err) <= e_tol * max(1.0, abs(ref_err))
     assert np.array_equal(lin.H_ii, lin.H_ii.T) and np.array_equal(lin.H_jj, lin.H_jj.T)
     return lin, ref, errs
