@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU work for cpu_baseline")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-lm", action="store_true", help="skip the C2 full-LM leg")
+    p.add_argument("--no-extra", action="store_true", help="skip the C1 / C4 legs")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu / e2e legs)")
     return p.parse_args()
 
@@ -212,6 +213,67 @@ def run_lm_c2(ctx, threads):
     }
 
 
+# ------------------------------------------------------------------------------ C1 / C4
+def run_c1(ctx, threads, reps=50):
+    """BASELINE config C1: one factor between two ~20k-point line scans (1 m apart), source pose
+    perturbed by (0.01 rad, 0.1 m), 1.0 m voxels: one linearize + one evaluate + one overlap,
+    each through the host C ABI (pinned H2D of the poses, D2H of the block), wall clock."""
+    import paper_2109_07073_b200 as V
+    from paper_2109_07073_b200 import optimizer as LM
+    from paper_2109_07073_b200 import workloads as W
+
+    sc = W.make_scans(W.c1_spec(), threads=threads)
+    tgt = V.PointCloud(sc.means[0], sc.cov6[0], ctx)
+    src = V.PointCloud(sc.means[1], sc.cov6[1], ctx)
+    vmap = V.GaussianVoxelMap(tgt, 1.0)
+    graph = V.FactorGraph([V.MatchingCostFactor(0, 1, src, vmap)], 2)
+    poses = np.stack([sc.gt[0], LM.compose(sc.gt[1], LM.se3_exp([0.0, 0.0, 0.01, 0.1, 0.0, 0.0]))])
+    rel = LM.compose(W.pose_inv(poses[0]), poses[1])
+
+    def timed(fn):
+        fn()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        return 1e3 * (time.perf_counter() - t0) / reps
+
+    out = {"points": [len(sc.means[0]), len(sc.means[1])], "voxels": vmap.size(),
+           "ms_linearize": timed(lambda: graph.linearize_raw(poses)),
+           "ms_evaluate": timed(lambda: graph.evaluate(poses)),
+           "ms_overlap": timed(lambda: V.overlap_rate(src, rel, vmap))}
+    raw, inl = graph.linearize_raw(poses)
+    out["inliers"] = int(inl[0])
+    out["note"] = "latency of single calls through the C ABI (host in/out), mean of %d" % reps
+    return out
+
+
+def run_c4(ctx, n_maps=4000, points=20000, reps=5):
+    """BASELINE config C4: one new frame against n_maps keyframe voxel maps (1.0 m), the overlap
+    query of keyframe / factor creation (pipeline.cpp:135-150) as ONE batched launch."""
+    import paper_2109_07073_b200 as V
+    from paper_2109_07073_b200 import synthetic as S
+    from paper_2109_07073_b200 import workloads as W
+
+    t0 = time.perf_counter()
+    seq = S.generate(S.SceneSpec(shape="figure_eight", frames=n_maps + 1, radius=50.0, points_per_scan=points, seed=4))
+    unit = np.tile(np.array([1, 0, 0, 1, 0, 1], np.float32), (points, 1))  # overlap reads keys only
+    clouds = [V.PointCloud(m, unit[: len(m)], ctx) for m in seq.scans]
+    maps = V.GaussianVoxelMap.build_batch(clouds[:n_maps], 1.0)
+    ctx.synchronize()
+    t_build = time.perf_counter() - t0
+    new = clouds[n_maps]
+    rels = np.stack([W.pose_mul(W.pose_inv(seq.ground_truth[i]), seq.ground_truth[n_maps]) for i in range(n_maps)])
+    hits = V.overlap_hits(new, rels, maps)
+    t1 = time.perf_counter()
+    for _ in range(reps):
+        hits = V.overlap_hits(new, rels, maps)
+    ms = 1e3 * (time.perf_counter() - t1) / reps
+    probes = n_maps * len(seq.scans[n_maps])
+    return {"maps": n_maps, "points": len(seq.scans[n_maps]), "ms_per_sweep": ms, "probes_per_s": probes / (ms * 1e-3),
+            "maps_over_0.025": int(np.sum(hits / len(seq.scans[n_maps]) > 0.025)), "build_seconds": round(t_build, 2),
+            "note": "host C ABI call incl. H2D of the per-map (pose, map) items and D2H of the hit counts"}
+
+
 # ------------------------------------------------------------------------------ ours
 def run_ours(args):
     import torch
@@ -346,9 +408,12 @@ def run_ours(args):
         traffic = json.loads(tf.read_text()).get("bytes_per_launch")
     data_bytes = sum(36 * len(m) for m in wl.scans.means) + sum(48 * int(m.size()) * 2 for m in wl.maps)
 
-    lm = None
+    lm = c1 = c4 = None
     if world == 1 and not args.profile and not args.no_lm:
         lm = run_lm_c2(ctx, threads)
+    if world == 1 and not args.profile and not args.no_extra:
+        c1 = run_c1(ctx, threads)
+        c4 = run_c4(ctx)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -382,6 +447,8 @@ def run_ours(args):
                      "bytes_alg_formula": "36*sum(N_f) + 44*sum(inliers_f) + 116*F (SURVEY 8d)"},
         "cpu_baseline": cpu,
         "lm_c2": lm,
+        "c1_single_factor": c1,
+        "c4_overlap_sweep": c4,
         "clocks": clk,
         "inlier_fraction": inliers / P,
         "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()} | {"total": round(t_build, 3)},

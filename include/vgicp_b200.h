@@ -135,7 +135,7 @@ int vgicp_gicp_error(vgicp_ctx ctx, const double source_mean[3], const double so
 /* A fixed set of matching-cost factors over num_poses pose variables. Validation mirrors the
  * MatchingCostFactor constructor (factors.cpp:57-66): distinct variables, non-empty source with
  * covariances, non-empty target map; indices must lie in [0, num_poses). `chunk` is the number
- * of source points per CTA work item (0 = default 8192; rounded up to a multiple of 1024). */
+ * of source points per CTA work item (0 = default 20480; rounded up to a multiple of 512). */
 int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses, int chunk,
                        vgicp_graph* out);
 int vgicp_graph_destroy(vgicp_graph graph);

@@ -422,7 +422,7 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
     mp->counts = reinterpret_cast<int*>(b + b_keys);
     mp->mean64 = reinterpret_cast<double*>(b + b_keys + b_counts);
     mp->cov64 = reinterpret_cast<double*>(b + b_keys + b_counts + b_mean);
-    if (int rc = alloc_table(mp, std::max(16u, next_pow2((hv[k] + 1) / 2)), s)) {
+    if (int rc = alloc_table(mp, std::max(16u, next_pow2((2ull * hv[k] + kBucket - 1) / kBucket)), s)) {  // load <= 0.5
       cleanup();
       return rc;
     }

@@ -86,7 +86,7 @@ struct InsertJob {       // hash-table insertion of one map's voxels
 constexpr int kFactorThreads = 256;
 constexpr int kFactorWarps = kFactorThreads / 32;
 constexpr int kFactorTile = 512;    // points per CTA tile (kFactorThreads x kILP)
-constexpr int kDefaultChunk = 8192;  // points per CTA work item
+constexpr int kDefaultChunk = 20480;  // points per CTA work item (one item per typical 20k-point factor)
 constexpr int kLinAcc = 28;     // Q(6) P(9) Omega(6) b(6) error(1)
 constexpr int kPartialStride = 32;
 

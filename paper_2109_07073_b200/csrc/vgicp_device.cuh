@@ -19,11 +19,11 @@ constexpr unsigned long long kEmptyKey = ~0ull;  // valid keys use 63 bits (voxe
 constexpr int kKeyBits = 21;                     // voxelmap.cpp:12
 constexpr double kKeyBias = 1048576.0;           // 2^20, voxelmap.cpp:13
 
-// Two-choice bucketed hash table. Keys live in buckets of kBucket = 4 slots (32 B = one L2
-// sector); a key is stored in one of two buckets chosen by independent hashes, so every lookup
-// is exactly two independent sector loads (no probe chains). Per-slot statistics live in a
-// parallel array indexed by slot.
-constexpr int kBucket = 4;
+// Two-choice bucketed (cuckoo) hash table. Keys live in buckets of kBucket = 2 slots (16 B); a key
+// is stored in one of two buckets chosen by independent hashes, so every lookup is exactly two
+// independent 16-B loads (no probe chains) and 4 key compares. Per-slot statistics live in
+// parallel arrays indexed by slot.
+constexpr int kBucket = 2;  // slots per bucket (16 B of keys: one LDG.128)
 
 struct __align__(16) VoxelStats {  // compact build-time record (by voxel id)
   float mx, my, mz, cxx;        // voxel-local mean (mean - coord * resolution) and covariance, fp32
@@ -91,20 +91,27 @@ static __device__ __noinline__ double2 voxel_axis_exact(double x, double r) {
   return make_double2(c, __dsub_rn(x, __dmul_rn(c, r)));
 }
 
-__device__ __forceinline__ bool voxel_axis(double x, double r, double inv_r, unsigned& k, double& local) {
+// Fast path of one axis: y = x·fl(1/r), c = floor(y), f = y - c. Returns whether the fast path
+// is certain (f within (2e-9, 1 - 2e-9), i.e. |f - 0.5| < 0.5 - 2e-9; false for inf / NaN).
+__device__ __forceinline__ bool voxel_axis_fast(double x, double r, double inv_r, int& c_int, double& local) {
   const double y = __dmul_rn(x, inv_r);
-  double c = floor(y);
+  const double c = floor(y);
   const double f = __dsub_rn(y, c);
-  if (f > 2.0e-9 && f < 1.0 - 2.0e-9) {
-    local = __dmul_rn(f, r);
-  } else {
+  c_int = __double2int_rz(c);  // saturates: out-of-range values fail the range test below
+  local = __dmul_rn(f, r);
+  return fabs(__dsub_rn(f, 0.5)) < 0.5 - 2.0e-9;
+}
+
+__device__ __forceinline__ bool voxel_axis(double x, double r, double inv_r, unsigned& k, double& local) {
+  int c;
+  if (!voxel_axis_fast(x, r, inv_r, c, local)) {
     const double2 e = voxel_axis_exact(x, r);
-    c = e.x;
+    if (!(e.x >= -kKeyBias && e.x < kKeyBias)) return false;  // also rejects NaN
+    c = __double2int_rz(e.x);
     local = e.y;
   }
-  const bool in = c >= -kKeyBias && c < kKeyBias;  // false for NaN
-  k = static_cast<unsigned>((in ? __double2int_rz(c) : 0) + (1 << 20));
-  return in;
+  k = static_cast<unsigned>(c + (1 << 20));
+  return k < (1u << 21);
 }
 
 __device__ __forceinline__ bool in_key_range(double c) { return c >= -kKeyBias && c < kKeyBias; }
@@ -140,33 +147,47 @@ __device__ __forceinline__ unsigned bucket2(unsigned k0, unsigned k1, unsigned k
   return ((h ^ (h >> 15)) * 0x85EBCA6Bu) >> shift;
 }
 
-// Voxel key of q under resolution r; false when any axis is outside ±2^20 (or NaN).
+// Voxel key of q under resolution r; false when any axis is outside ±2^20 (or NaN). The three
+// axes share one branch to the exact path.
 __device__ __forceinline__ bool voxel_key(double q0, double q1, double q2, double r, double inv_r, unsigned& k0,
                                           unsigned& k1, unsigned& k2, double& l0, double& l1, double& l2) {
-  return voxel_axis(q0, r, inv_r, k0, l0) & voxel_axis(q1, r, inv_r, k1, l1) & voxel_axis(q2, r, inv_r, k2, l2);
+  int c0, c1, c2;
+  const bool f0 = voxel_axis_fast(q0, r, inv_r, c0, l0);
+  const bool f1 = voxel_axis_fast(q1, r, inv_r, c1, l1);
+  const bool f2 = voxel_axis_fast(q2, r, inv_r, c2, l2);
+  if (!(f0 && f1 && f2)) {
+    bool ok = true;
+    if (!f0) ok &= voxel_axis(q0, r, inv_r, k0, l0), c0 = static_cast<int>(k0) - (1 << 20);
+    if (!f1) ok &= voxel_axis(q1, r, inv_r, k1, l1), c1 = static_cast<int>(k1) - (1 << 20);
+    if (!f2) ok &= voxel_axis(q2, r, inv_r, k2, l2), c2 = static_cast<int>(k2) - (1 << 20);
+    if (!ok) return false;
+  }
+  k0 = static_cast<unsigned>(c0 + (1 << 20));
+  k1 = static_cast<unsigned>(c1 + (1 << 20));
+  k2 = static_cast<unsigned>(c2 + (1 << 20));
+  return (k0 < (1u << 21)) & (k1 < (1u << 21)) & (k2 < (1u << 21));
 }
 
-// Issue the two bucket loads (2 × 32 B, independent) for a key.
+// Issue the two bucket loads (2 × 16 B, independent) for a key.
 struct BucketPair {
-  unsigned a[8];
-  unsigned b[8];
+  uint4 a;
+  uint4 b;
 };
 __device__ __forceinline__ BucketPair load_buckets(const unsigned long long* __restrict__ keys, unsigned b1,
                                                    unsigned b2) {
   BucketPair r;
-  ldg256(keys + kBucket * b1, r.a[0], r.a[1], r.a[2], r.a[3], r.a[4], r.a[5], r.a[6], r.a[7]);
-  ldg256(keys + kBucket * b2, r.b[0], r.b[1], r.b[2], r.b[3], r.b[4], r.b[5], r.b[6], r.b[7]);
+  r.a = __ldg(reinterpret_cast<const uint4*>(keys + kBucket * b1));
+  r.b = __ldg(reinterpret_cast<const uint4*>(keys + kBucket * b2));
   return r;
 }
 
-// Slot of (hi, lo) among the 8 loaded candidates, or -1.
+// Slot of (hi, lo) among the 4 loaded candidates, or -1.
 __device__ __forceinline__ int match_buckets(const BucketPair& p, unsigned b1, unsigned b2, unsigned hi, unsigned lo) {
   int s = -1;
-#pragma unroll
-  for (int q = 0; q < kBucket; ++q) {
-    s = (p.a[2 * q] == lo && p.a[2 * q + 1] == hi) ? static_cast<int>(kBucket * b1 + q) : s;
-    s = (p.b[2 * q] == lo && p.b[2 * q + 1] == hi) ? static_cast<int>(kBucket * b2 + q) : s;
-  }
+  s = (p.a.x == lo && p.a.y == hi) ? static_cast<int>(kBucket * b1) : s;
+  s = (p.a.z == lo && p.a.w == hi) ? static_cast<int>(kBucket * b1 + 1) : s;
+  s = (p.b.x == lo && p.b.y == hi) ? static_cast<int>(kBucket * b2) : s;
+  s = (p.b.z == lo && p.b.w == hi) ? static_cast<int>(kBucket * b2 + 1) : s;
   return s;
 }
 

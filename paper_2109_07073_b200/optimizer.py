@@ -52,6 +52,32 @@ def se3_exp(xi) -> np.ndarray:  # se3.cpp:74-78, rotation part first
     return np.concatenate([R.reshape(9), t])
 
 
+def se3_exp_batch(xi) -> np.ndarray:
+    """se3_exp for n twists at once (n × 6 -> n × 12), same formulas and small-angle branch."""
+    xi = np.asarray(xi, np.float64).reshape(-1, 6)
+    w, v = xi[:, :3], xi[:, 3:]
+    th = np.linalg.norm(w, axis=1)
+    W = np.zeros((len(xi), 3, 3))
+    W[:, 0, 1], W[:, 0, 2], W[:, 1, 0] = -w[:, 2], w[:, 1], w[:, 2]
+    W[:, 1, 2], W[:, 2, 0], W[:, 2, 1] = -w[:, 0], -w[:, 1], w[:, 0]
+    WW = W @ W
+    small = th < SMALL_ANGLE
+    ths = np.where(small, 1.0, th)
+    a = np.where(small, 1.0, np.sin(ths) / ths)
+    b = np.where(small, 0.5, (1.0 - np.cos(ths)) / (ths * ths))
+    c = np.where(small, 1.0 / 6.0, (ths - np.sin(ths)) / (ths * ths * ths))
+    I = np.eye(3)[None]
+    R = I + a[:, None, None] * W + b[:, None, None] * WW
+    J = I + b[:, None, None] * W + c[:, None, None] * WW
+    t = np.einsum("nij,nj->ni", J, v)
+    return np.concatenate([R.reshape(-1, 9), t], axis=1)
+
+
+def compose_batch(A, B) -> np.ndarray:
+    Ra, Rb = A[:, :9].reshape(-1, 3, 3), B[:, :9].reshape(-1, 3, 3)
+    return np.concatenate([(Ra @ Rb).reshape(-1, 9), np.einsum("nij,nj->ni", Ra, B[:, 9:]) + A[:, 9:]], axis=1)
+
+
 def compose(a, b) -> np.ndarray:  # se3.cpp:42-44
     Ra, Rb = a[:9].reshape(3, 3), b[:9].reshape(3, 3)
     return np.concatenate([(Ra @ Rb).reshape(9), Ra @ b[9:] + a[9:]])
@@ -121,37 +147,59 @@ def effective_fixed_mask(num_poses: int, ij, fixed) -> np.ndarray:  # optimizer.
     return out
 
 
-def assemble(raw: np.ndarray, ij: np.ndarray, num_poses: int):
-    """Dense normal equations from 121-double factor blocks (block_solver.cpp:14-62 semantics)."""
+_ASM_CACHE: dict = {}
+
+
+def _assembly_indices(ij: np.ndarray, num_poses: int):
+    """Flat scatter indices of the 4 H blocks and 2 b segments of every factor (cached per graph)."""
+    key = (ij.tobytes(), num_poses)
+    hit = _ASM_CACHE.get(key)
+    if hit is not None:
+        return hit
     n6 = 6 * num_poses
-    H = np.zeros((n6, n6))
-    b = np.zeros(n6)
-    for f in range(len(raw)):
-        i, j = int(ij[f, 0]), int(ij[f, 1])
-        r = raw[f]
-        si, sj = slice(6 * i, 6 * i + 6), slice(6 * j, 6 * j + 6)
-        Hij = r[36:72].reshape(6, 6)
-        H[si, si] += r[0:36].reshape(6, 6)
-        H[sj, sj] += r[72:108].reshape(6, 6)
-        H[si, sj] += Hij
-        H[sj, si] += Hij.T
-        b[si] += r[108:114]
-        b[sj] += r[114:120]
+    r6 = np.arange(6)
+    rows = lambda v: 6 * v[:, None, None] + r6[None, :, None]  # noqa: E731
+    cols = lambda v: 6 * v[:, None, None] + r6[None, None, :]  # noqa: E731
+    i, j = ij[:, 0].astype(np.int64), ij[:, 1].astype(np.int64)
+    idx_ii = (rows(i) * n6 + cols(i)).reshape(len(ij), 36)
+    idx_ij = (rows(i) * n6 + cols(j)).reshape(len(ij), 36)
+    idx_ji = (rows(j) * n6 + cols(i)).reshape(len(ij), 36)
+    idx_jj = (rows(j) * n6 + cols(j)).reshape(len(ij), 36)
+    hidx = np.concatenate([idx_ii, idx_ij, idx_ji, idx_jj], axis=1).ravel()
+    bidx = np.concatenate([6 * i[:, None] + r6, 6 * j[:, None] + r6], axis=1).ravel()
+    _ASM_CACHE.clear()
+    _ASM_CACHE[key] = (hidx, bidx)
+    return hidx, bidx
+
+
+def assemble(raw: np.ndarray, ij: np.ndarray, num_poses: int):
+    """Dense normal equations from 121-double factor blocks (block_solver.cpp:14-62 semantics):
+    H[i,i] += H_ii, H[i,j] += H_ij, H[j,i] += H_ijᵀ, H[j,j] += H_jj, b[i] += b_i, b[j] += b_j."""
+    n6 = 6 * num_poses
+    hidx, bidx = _assembly_indices(np.asarray(ij), num_poses)
+    F = len(raw)
+    Hij = raw[:, 36:72].reshape(F, 6, 6)
+    vals = np.concatenate([raw[:, 0:36], raw[:, 36:72], Hij.transpose(0, 2, 1).reshape(F, 36), raw[:, 72:108]], axis=1)
+    H = np.bincount(hidx, weights=vals.ravel(), minlength=n6 * n6).reshape(n6, n6)
+    b = np.bincount(bidx, weights=raw[:, 108:120].ravel(), minlength=n6)
     return H, b
 
 
 def solve_damped(H, b, active, lam):
     """Cholesky solve of the damped reduced system; None when not positive definite."""
-    idx = np.concatenate([np.arange(6 * v, 6 * v + 6) for v in np.flatnonzero(active)]) if active.any() else np.zeros(0, int)
-    Hr = H[np.ix_(idx, idx)].copy()
-    d = np.diag(Hr).copy()
+    import scipy.linalg as sla
+
+    idx = np.flatnonzero(np.repeat(active, 6))
+    if len(idx) == 0:
+        return np.zeros_like(b)
+    Hr = H[np.ix_(idx, idx)]
+    d = Hr.diagonal().copy()
     Hr[np.diag_indices_from(Hr)] = d + lam * np.maximum(d, 1e-10)
     try:
-        L = np.linalg.cholesky(Hr)
+        c = sla.cho_factor(Hr, lower=True, overwrite_a=True, check_finite=False)
     except np.linalg.LinAlgError:
         return None
-    y = np.linalg.solve(L, b[idx]) if len(idx) else np.zeros(0)
-    x = np.linalg.solve(L.T, y) if len(idx) else np.zeros(0)
+    x = sla.cho_solve(c, b[idx], check_finite=False)
     delta = np.zeros_like(b)
     delta[idx] = x
     return delta
@@ -198,12 +246,13 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
                 break
             cand = poses.copy()
             cand_updates = updates.copy()
-            for v in np.flatnonzero(active):
-                cand[v] = compose(poses[v], se3_exp(delta[6 * v:6 * v + 6]))  # Pose::retract (se3.cpp:93-101)
-                cand_updates[v] += 1
-                if cand_updates[v] >= ORTHONORMALIZE_EVERY:
-                    cand[v] = orthonormalized(cand[v])
-                    cand_updates[v] = 0
+            act = np.flatnonzero(active)
+            # Pose::retract (se3.cpp:93-101): T · exp(δ), re-orthonormalised every 50 updates
+            cand[act] = compose_batch(poses[act], se3_exp_batch(delta.reshape(-1, 6)[act]))
+            cand_updates[act] += 1
+            for v in act[cand_updates[act] >= ORTHONORMALIZE_EVERY]:
+                cand[v] = orthonormalized(cand[v])
+                cand_updates[v] = 0
             cand_error = graph.total_error(cand)
             if cand_error < current:
                 decrease = (current - cand_error) / max(current, 1e-300)

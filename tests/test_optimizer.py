@@ -183,3 +183,13 @@ def test_chain_lm_reduces_error_and_drift():
         return max(np.linalg.norm(a[9:] - b[9:]) for a, b in zip(rel, rel_gt))
 
     assert drift(poses) < drift(wl.poses)
+
+
+def test_batched_se3_matches_scalar():
+    rng = np.random.default_rng(3)
+    xi = rng.uniform(-1, 1, (20, 6))
+    xi[3] = 1e-10
+    ref = np.stack([LM.se3_exp(x) for x in xi])
+    assert np.allclose(LM.se3_exp_batch(xi), ref, atol=1e-14)
+    A = LM.se3_exp_batch(rng.uniform(-1, 1, (20, 6)))
+    assert np.allclose(LM.compose_batch(A, ref), np.stack([LM.compose(a, r) for a, r in zip(A, ref)]), atol=1e-14)

@@ -1,11 +1,8 @@
 # Kernel-variant sweep on the C3 workload: prints linearize / evaluate kernel ms per variant.
 run() {  # $1 = label, rest = env/args
   local label=$1; shift
-  env "$@" python bench.py --profile --steps 20 --warmup 5 --no-cpu-baseline --no-lm $BENCH_ARGS 2>/dev/null | \
+  env "$@" python bench.py --profile --steps 20 --warmup 5 --no-cpu-baseline --no-lm --no-extra $BENCH_ARGS 2>/dev/null | \
     python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$label', 'lin %.3f ms' % d['ms_linearize_kernel'], 'eval %.3f ms' % d['ms_evaluate_kernel'], 'value %.0f' % d['value'])"
 }
 run default VGICP_LIB=$PWD/paper_2109_07073_b200/lib/libvgicp_b200.so
-for v in paper_2109_07073_b200/lib_variants/*; do run $(basename $v) VGICP_LIB=$PWD/$v/libvgicp_b200.so; done
-BENCH_ARGS="--chunk 4096" run chunk4096 VGICP_LIB=$PWD/paper_2109_07073_b200/lib/libvgicp_b200.so
-BENCH_ARGS="--chunk 16384" run chunk16384 VGICP_LIB=$PWD/paper_2109_07073_b200/lib/libvgicp_b200.so
-BENCH_ARGS="--chunk 20480" run chunk20480 VGICP_LIB=$PWD/paper_2109_07073_b200/lib/libvgicp_b200.so
+for v in paper_2109_07073_b200/lib_variants/*; do run "$(basename $v)" VGICP_LIB=$PWD/$v/libvgicp_b200.so; done
