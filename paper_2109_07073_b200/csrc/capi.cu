@@ -208,6 +208,43 @@ int vgicp_ctx_launch_count(vgicp_ctx ctx, uint64_t* launches) {
 }
 
 // ------------------------------------------------------------------------------------ clouds
+// Z-order permutation of the points (10 bits per axis over the bounding box). Deterministic:
+// ties keep input order.
+static std::vector<uint32_t> morton_order(const float* xyz, size_t n) {
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (size_t i = 0; i < n; ++i)
+    for (int a = 0; a < 3; ++a) {
+      const float v = xyz[3 * i + a];
+      if (std::isfinite(v)) {
+        lo[a] = std::min(lo[a], v);
+        hi[a] = std::max(hi[a], v);
+      }
+    }
+  auto spread = [](uint32_t x) {  // 10 bits -> every third bit
+    x &= 0x3FFu;
+    x = (x | (x << 16)) & 0x030000FFu;
+    x = (x | (x << 8)) & 0x0300F00Fu;
+    x = (x | (x << 4)) & 0x030C30C3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+  };
+  std::vector<std::pair<uint32_t, uint32_t>> code(n);
+  for (size_t i = 0; i < n; ++i) {
+    uint32_t c[3];
+    for (int a = 0; a < 3; ++a) {
+      const float ext = hi[a] - lo[a];
+      const float v = xyz[3 * i + a];
+      const float u = (std::isfinite(v) && ext > 0.f) ? (v - lo[a]) / ext : 0.f;
+      c[a] = static_cast<uint32_t>(std::min(1023.f, std::max(0.f, u * 1024.f)));
+    }
+    code[i] = {spread(c[0]) | (spread(c[1]) << 1) | (spread(c[2]) << 2), static_cast<uint32_t>(i)};
+  }
+  std::sort(code.begin(), code.end());
+  std::vector<uint32_t> perm(n);
+  for (size_t i = 0; i < n; ++i) perm[i] = code[i].second;
+  return perm;
+}
+
 static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov6, size_t n, vgicp_cloud* out) {
   if (!ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
@@ -220,30 +257,38 @@ static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov
   c->has_cov = (cov6 != nullptr) && n > 0;
   const size_t na = align_up(n * sizeof(float4), 256);
   const size_t nc = align_up(n * sizeof(float), 256);
-  const size_t bytes = std::max<size_t>(na * 2 + nc, 256);
+  const size_t half = na * 2 + nc;
+  const size_t bytes = std::max<size_t>(2 * half, 256);
   VG_CUDA(cudaMalloc(&c->block, bytes));
   char* base = static_cast<char*>(c->block);
   c->pa = reinterpret_cast<float4*>(base);
   c->pb = reinterpret_cast<float4*>(base + na);
   c->pc = reinterpret_cast<float*>(base + 2 * na);
+  c->spa = reinterpret_cast<float4*>(base + half);
+  c->spb = reinterpret_cast<float4*>(base + half + na);
+  c->spc = reinterpret_cast<float*>(base + half + 2 * na);
   if (n > 0) {
     if (int rc = ensure_pinned(ctx, bytes)) return rc;
     VG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const std::vector<uint32_t> perm = morton_order(xyz, n);
     char* h = static_cast<char*>(ctx->pinned);
-    float4* ha = reinterpret_cast<float4*>(h);
-    float4* hb = reinterpret_cast<float4*>(h + na);
-    float* hc = reinterpret_cast<float*>(h + 2 * na);
-    for (size_t i = 0; i < n; ++i) {
-      const float* p = xyz + 3 * i;
-      if (cov6) {
-        const float* q = cov6 + 6 * i;
-        ha[i] = make_float4(p[0], p[1], p[2], q[0]);
-        hb[i] = make_float4(q[1], q[2], q[3], q[4]);
-        hc[i] = q[5];
-      } else {
-        ha[i] = make_float4(p[0], p[1], p[2], 0.f);
-        hb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        hc[i] = 0.f;
+    for (int copy = 0; copy < 2; ++copy) {
+      float4* ha = reinterpret_cast<float4*>(h + copy * half);
+      float4* hb = reinterpret_cast<float4*>(h + copy * half + na);
+      float* hc = reinterpret_cast<float*>(h + copy * half + 2 * na);
+      for (size_t d = 0; d < n; ++d) {
+        const size_t i = copy == 0 ? d : perm[d];
+        const float* p = xyz + 3 * i;
+        if (cov6) {
+          const float* q = cov6 + 6 * i;
+          ha[d] = make_float4(p[0], p[1], p[2], q[0]);
+          hb[d] = make_float4(q[1], q[2], q[3], q[4]);
+          hc[d] = q[5];
+        } else {
+          ha[d] = make_float4(p[0], p[1], p[2], 0.f);
+          hb[d] = make_float4(0.f, 0.f, 0.f, 0.f);
+          hc[d] = 0.f;
+        }
       }
     }
     VG_CUDA(cudaMemcpyAsync(c->block, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -574,7 +619,7 @@ int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* 
     if (clouds[k]->ctx != ctx || maps[k]->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "handle of another context");
     if (clouds[k]->n == 0) return fail(VGICP_E_INVALID_ARGUMENT, "overlap_rate requires a nonempty cloud");
     OverlapItem& it = items[k];
-    it.pa = clouds[k]->pa;
+    it.pa = clouds[k]->spa;  // Morton order (hit counts are order-independent)
     it.map = maps[k]->dev();
     std::memcpy(it.T, poses12 + 12 * k, sizeof(double) * 12);
     it.n = static_cast<unsigned>(clouds[k]->n);
@@ -635,9 +680,9 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   for (int f = 0; f < num_factors; ++f) {
     const vgicp_factor_desc& d = factors[f];
     FactorDev& x = fd[f];
-    x.pa = d.source->pa;
-    x.pb = d.source->pb;
-    x.pc = d.source->pc;
+    x.pa = d.source->spa;  // Morton order: neighbouring lanes probe neighbouring voxels
+    x.pb = d.source->spb;
+    x.pc = d.source->spc;
     x.map = d.target->dev();
     x.n = static_cast<int>(d.source->n);
     x.tgt = d.target_index;

@@ -127,10 +127,13 @@ struct vgicp_cloud_s {
   vgicp_ctx ctx = nullptr;
   size_t n = 0;
   bool has_cov = false;
-  void* block = nullptr;  // single allocation holding pa | pb | pc
-  float4* pa = nullptr;
+  void* block = nullptr;  // single allocation: pa | pb | pc (input order) | sa | sb | sc (Morton order)
+  float4* pa = nullptr;   // input order: voxel-map builds accumulate in this order (voxelmap.cpp:87-94)
   float4* pb = nullptr;
   float* pc = nullptr;
+  float4* spa = nullptr;  // Morton (Z-order) copy: streamed by the factor / overlap kernels so that
+  float4* spb = nullptr;  // consecutive points probe neighbouring voxels (bucket1 locality, L1 hits)
+  float* spc = nullptr;
   std::atomic<int> refs{1};
 };
 

@@ -138,9 +138,13 @@ __device__ __forceinline__ double key_coord(unsigned long long key, int axis) {
 }
 
 // Two independent spatial hashes of the biased voxel coordinates -> bucket index (32-bit ops).
+// bucket1 is locality-preserving: the 8 voxels of an aligned 2×2×2 block share one hashed group of
+// 8 consecutive buckets (8 × 16 B = one 128-B line), so spatially ordered probes (source clouds are
+// streamed in Morton order) hit few lines and mostly L1. bucket2 is a plain spatial hash.
 __device__ __forceinline__ unsigned bucket1(unsigned k0, unsigned k1, unsigned k2, unsigned shift) {
-  const unsigned h = (k0 * 73856093u) ^ (k1 * 19349663u) ^ (k2 * 83492791u);
-  return (h * 0x9E3779B1u) >> shift;
+  const unsigned h = ((k0 >> 1) * 73856093u) ^ ((k1 >> 1) * 19349663u) ^ ((k2 >> 1) * 83492791u);
+  const unsigned group = (h * 0x9E3779B1u) >> (shift + 3);
+  return (group << 3) | (k0 & 1u) | ((k1 & 1u) << 1) | ((k2 & 1u) << 2);
 }
 __device__ __forceinline__ unsigned bucket2(unsigned k0, unsigned k1, unsigned k2, unsigned shift) {
   const unsigned h = (k0 * 2654435761u) ^ (k1 * 2246822519u) ^ (k2 * 3266489917u) ^ 0x5bd1e995u;

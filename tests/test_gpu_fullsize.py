@@ -1,0 +1,94 @@
+"""Parity and size-independent properties at BASELINE.json's full size (config C3: 450 frames ×
+20k points, 4,445 factors), through the C ABI.
+
+The oracle finishes a sample of factors in seconds, so exact / tolerance parity is checked on a
+spread sample; properties that need no oracle are checked on every factor: bitwise determinism,
+linearize/evaluate consistency, exact symmetry, gauge invariance of the total error, exact overlap
+counts against the oracle on sampled pairs.
+"""
+import numpy as np
+import pytest
+
+import oracle_ctypes as O
+from helpers import rel_block_error
+
+V = pytest.importorskip("paper_2109_07073_b200")
+from paper_2109_07073_b200 import workloads as W  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+H_TOL = 1e-5
+ERR_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def c3():
+    ctx = V.default_context(0)
+    return W.build_graph_workload(ctx, W.c3_spec())
+
+
+def oracle_frame(wl, k):
+    return wl.scans.means[k].astype(np.float64), O.cov9(wl.scans.cov6[k].astype(np.float64))
+
+
+def test_c3_shape(c3):
+    assert 4000 <= c3.num_factors <= 4500
+    assert c3.num_points() == sum(len(c3.scans.means[j]) for _, j in c3.links)
+    for i, j in c3.links:
+        assert i < j  # target = older frame (pipeline.cpp:46-48)
+
+
+def test_c3_deterministic_and_consistent(c3):
+    a, ia = c3.graph.linearize_raw(c3.poses)
+    b, ib = c3.graph.linearize_raw(c3.poses)
+    assert np.array_equal(a, b) and np.array_equal(ia, ib)
+    err, inl = c3.graph.evaluate(c3.poses)
+    assert np.array_equal(inl, ia)
+    assert np.array_equal(err, a[:, 120])
+    Hii = a[:, 0:36].reshape(-1, 6, 6)
+    Hjj = a[:, 72:108].reshape(-1, 6, 6)
+    assert np.array_equal(Hii, Hii.transpose(0, 2, 1)) and np.array_equal(Hjj, Hjj.transpose(0, 2, 1))
+    assert np.all(ia > 0)
+
+
+def test_c3_sampled_factors_match_oracle(c3):
+    raw, inl = c3.graph.linearize_raw(c3.poses)
+    sample = np.linspace(0, c3.num_factors - 1, 12).astype(int)
+    omaps = {}
+    for f in sample:
+        i, j = c3.links[f]
+        if i not in omaps:
+            m, c = oracle_frame(c3, i)
+            omaps[i] = O.OracleMap(m, c, 1.0)
+        sm, sc = oracle_frame(c3, j)
+        ref = O.linearize(sm, sc, omaps[i], c3.poses[i], c3.poses[j])
+        assert inl[f] == ref["inliers"], (f, inl[f], ref["inliers"])
+        got = O.unpack121(raw[f])
+        d = rel_block_error(got, ref)
+        assert max(v for k, v in d.items() if k != "error") <= H_TOL, (f, d)
+        assert d["error"] <= ERR_TOL, (f, d)
+
+
+def test_c3_gauge_invariance(c3):
+    base = c3.graph.total_error(c3.poses)
+    G = O.Rng(99).random_pose(1.0, 30.0)
+    moved = np.stack([O.compose(G, p) for p in c3.poses])
+    assert abs(c3.graph.total_error(moved) - base) <= 1e-5 * base
+
+
+def test_c3_overlap_counts_exact(c3):
+    rng = np.random.default_rng(7)
+    pairs = [c3.links[k] for k in rng.choice(len(c3.links), 8, replace=False)]
+    rels = [W.pose_mul(W.pose_inv(c3.scans.gt[i]), c3.scans.gt[j]) for i, j in pairs]
+    hits = V.overlap_hits([c3.clouds[j] for _, j in pairs], rels, [c3.maps[i] for i, _ in pairs])
+    for (i, j), rel, h in zip(pairs, rels, hits):
+        m, c = oracle_frame(c3, i)
+        assert int(h) == O.overlap_hits(c3.scans.means[j].astype(np.float64), rel, O.OracleMap(m, c, 1.0))
+
+
+def test_c3_maps_bit_exact_sample(c3):
+    for k in (0, 225, 449):
+        m, c = oracle_frame(c3, k)
+        om = O.OracleMap(m, c, 1.0, threads=4, deterministic=True)
+        for x, y in zip(c3.maps[k].export(), om.export()):
+            assert np.array_equal(x, y)
