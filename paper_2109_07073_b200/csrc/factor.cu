@@ -116,7 +116,10 @@ static_assert(sizeof(WarpTile) * kStages >= sizeof(float) * kLinAcc * 33 + 64 * 
               "per-warp reduction scratch must fit in the warp's ring");
 
 template <bool kLinearize>
-__global__ void __launch_bounds__(kFactorThreads, 2) factor_kernel(
+#ifndef VG_MINB
+#define VG_MINB 2
+#endif
+__global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
     const FactorDev* __restrict__ factors, const WorkItem* __restrict__ items, const double* __restrict__ poses,
     double* __restrict__ partials, int* __restrict__ part_inl, unsigned* __restrict__ counters,
     double* __restrict__ out, int* __restrict__ out_inl) {
