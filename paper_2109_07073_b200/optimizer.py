@@ -185,24 +185,53 @@ def assemble(raw: np.ndarray, ij: np.ndarray, num_poses: int):
     return H, b
 
 
-def solve_damped(H, b, active, lam):
-    """Cholesky solve of the damped reduced system; None when not positive definite."""
+def solve_damped(H, b, active, lam, bandwidth=None):
+    """Cholesky solve of the damped reduced system; None when not positive definite.
+
+    With `bandwidth` (in scalar rows, from the graph structure) small relative to the system, a
+    banded Cholesky (LAPACK pbtrf/pbtrs via scipy.linalg.solveh_banded) is used — odometry chains;
+    otherwise a dense Cholesky. Both fail exactly when the damped system is not positive definite,
+    which escalates λ like the reference's failed block pivot (block_solver.cpp:80-85)."""
     import scipy.linalg as sla
 
-    idx = np.flatnonzero(np.repeat(active, 6))
-    if len(idx) == 0:
+    act = np.flatnonzero(active)
+    if len(act) == 0:
         return np.zeros_like(b)
-    Hr = H[np.ix_(idx, idx)]
-    d = Hr.diagonal().copy()
-    Hr[np.diag_indices_from(Hr)] = d + lam * np.maximum(d, 1e-10)
+    if act[-1] - act[0] + 1 == len(act):  # contiguous active range: a view, no gather
+        s0, s1 = 6 * act[0], 6 * (act[-1] + 1)
+        Hr, br, idx = H[s0:s1, s0:s1], b[s0:s1], slice(s0, s1)
+    else:
+        idx = np.flatnonzero(np.repeat(active, 6))
+        Hr, br = H[np.ix_(idx, idx)], b[idx]
+    m = Hr.shape[0]
+    damp = lambda dg: dg + lam * np.maximum(dg, 1e-10)  # noqa: E731  (optimizer.cpp:119-123)
     try:
-        c = sla.cho_factor(Hr, lower=True, overwrite_a=True, check_finite=False)
+        if bandwidth is not None and bandwidth < m // 4:
+            ab = np.empty((bandwidth + 1, m))  # lower banded storage
+            ab[0] = damp(np.diagonal(Hr))
+            for k in range(1, bandwidth + 1):
+                ab[k, : m - k] = np.diagonal(Hr, -k)
+                ab[k, m - k:] = 0.0
+            x = sla.solveh_banded(ab, br, lower=True, check_finite=False)
+        else:
+            Hd = np.array(Hr, copy=True)
+            Hd[np.diag_indices_from(Hd)] = damp(np.diagonal(Hr))
+            c = sla.cho_factor(Hd, lower=True, overwrite_a=True, check_finite=False)
+            x = sla.cho_solve(c, br, check_finite=False)
     except np.linalg.LinAlgError:
         return None
-    x = sla.cho_solve(c, b[idx], check_finite=False)
     delta = np.zeros_like(b)
     delta[idx] = x
     return delta
+
+
+def graph_bandwidth(ij, active) -> int:
+    """Scalar half-bandwidth of the reduced normal equations (6·max |rank(i) − rank(j)| + 5)."""
+    rank = np.cumsum(active) - 1
+    both = active[ij[:, 0]] & active[ij[:, 1]]
+    if not both.any():
+        return 5
+    return int(6 * np.max(np.abs(rank[ij[both, 0]] - rank[ij[both, 1]])) + 5)
 
 
 def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None = None):
@@ -215,6 +244,7 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
     ij = graph._ij
     fixed_mask = effective_fixed_mask(n, ij, np.zeros(n, bool) if fixed is None else fixed)
     active = ~fixed_mask
+    bandwidth = graph_bandwidth(np.asarray(ij), active)
     updates = np.zeros(n, dtype=np.int64)
 
     raw, _ = graph.linearize_raw(poses)
@@ -227,7 +257,7 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
         H, b = assemble(raw, ij, n)
         accepted = False
         while True:
-            delta = solve_damped(H, b, active, lam)
+            delta = solve_damped(H, b, active, lam, bandwidth)
             if delta is None:
                 lam *= settings.lambda_increase
                 if lam > settings.lambda_max:

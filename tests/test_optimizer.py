@@ -193,3 +193,26 @@ def test_batched_se3_matches_scalar():
     assert np.allclose(LM.se3_exp_batch(xi), ref, atol=1e-14)
     A = LM.se3_exp_batch(rng.uniform(-1, 1, (20, 6)))
     assert np.allclose(LM.compose_batch(A, ref), np.stack([LM.compose(a, r) for a, r in zip(A, ref)]), atol=1e-14)
+
+
+def test_banded_solve_matches_dense():
+    rng = np.random.default_rng(5)
+    from paper_2109_07073_b200 import workloads as W
+
+    ij = np.array(W.c2_links(30))
+    raw = np.zeros((len(ij), 121))
+    for f in range(len(ij)):
+        S = rng.uniform(-1, 1, (12, 12))
+        Hf = S @ S.T + np.eye(12)
+        raw[f, 0:36], raw[f, 36:72], raw[f, 72:108] = Hf[:6, :6].ravel(), Hf[:6, 6:].ravel(), Hf[6:, 6:].ravel()
+        raw[f, 108:120] = rng.uniform(-1, 1, 12)
+    H, b = LM.assemble(raw, ij, 30)
+    active = np.ones(30, bool)
+    active[0] = False
+    bw = LM.graph_bandwidth(ij, active)
+    assert bw == 6 * 3 + 5
+    dense = LM.solve_damped(H, b, active, 1e-3, None)
+    banded = LM.solve_damped(H, b, active, 1e-3, bw)
+    assert np.allclose(dense, banded, rtol=1e-10, atol=1e-12)
+    active[5] = False  # non-contiguous active set -> gather path
+    assert np.allclose(LM.solve_damped(H, b, active, 1e-3, None), LM.solve_damped(H, b, active, 1e-3, LM.graph_bandwidth(ij, active)), rtol=1e-10, atol=1e-12)
