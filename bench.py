@@ -208,7 +208,7 @@ def run_lm_c2(ctx, threads):
         "ms_per_lm_iteration_median": 1e3 * its[len(its) // 2] if its else None,
         "ms_total": 1e3 * rep.wall_time_seconds, "initial_error": rep.initial_error, "final_error": rep.final_error,
         "reason": rep.reason,
-        "note": "host LM (paper_2109_07073_b200/optimizer.py, dense Cholesky) around one linearize launch per "
+        "note": "host LM (paper_2109_07073_b200/optimizer.py, banded Cholesky) around one linearize launch per "
                 "accepted step and one error launch per candidate; wall clock incl. H2D/D2H",
     }
 
@@ -222,7 +222,7 @@ def run_c1(ctx, threads, reps=50):
     from paper_2109_07073_b200 import optimizer as LM
     from paper_2109_07073_b200 import workloads as W
 
-    sc = W.make_scans(W.c1_spec(), threads=threads)
+    sc = W.make_scans(W.c1_spec(), threads=threads, ctx=ctx)
     tgt = V.PointCloud(sc.means[0], sc.cov6[0], ctx)
     src = V.PointCloud(sc.means[1], sc.cov6[1], ctx)
     vmap = V.GaussianVoxelMap(tgt, 1.0)
@@ -272,6 +272,21 @@ def run_c4(ctx, n_maps=4000, points=20000, reps=5):
     return {"maps": n_maps, "points": len(seq.scans[n_maps]), "ms_per_sweep": ms, "probes_per_s": probes / (ms * 1e-3),
             "maps_over_0.025": int(np.sum(hits / len(seq.scans[n_maps]) > 0.025)), "build_seconds": round(t_build, 2),
             "note": "host C ABI call incl. H2D of the per-map (pose, map) items and D2H of the hit counts"}
+
+
+def run_covariances(ctx, scans, reps=3):
+    """Per-point covariance preprocessing (point_cloud.cpp:44-83, k=10, eps=1e-3) of every C3 scan
+    in one batched call through the C ABI (H2D of the points, D2H of the n×6 covariances)."""
+    import paper_2109_07073_b200 as V
+
+    V.estimate_covariances_batch(scans[:2], 10, 1e-3, ctx)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        V.estimate_covariances_batch(scans, 10, 1e-3, ctx)
+    ms = 1e3 * (time.perf_counter() - t0) / reps
+    pts = sum(len(m) for m in scans)
+    return {"scans": len(scans), "points": pts, "k": 10, "ms_per_batch": ms, "points_per_s": pts / (ms * 1e-3),
+            "note": "exact kNN on a uniform grid + Jacobi eigenvectors, one batched C ABI call, wall clock incl. H2D/D2H"}
 
 
 # ------------------------------------------------------------------------------ ours
@@ -408,12 +423,13 @@ def run_ours(args):
         traffic = json.loads(tf.read_text()).get("bytes_per_launch")
     data_bytes = sum(36 * len(m) for m in wl.scans.means) + sum(48 * int(m.size()) * 2 for m in wl.maps)
 
-    lm = c1 = c4 = None
+    lm = c1 = c4 = cov = None
     if world == 1 and not args.profile and not args.no_lm:
         lm = run_lm_c2(ctx, threads)
     if world == 1 and not args.profile and not args.no_extra:
         c1 = run_c1(ctx, threads)
         c4 = run_c4(ctx)
+        cov = run_covariances(ctx, wl.scans.means)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -449,6 +465,7 @@ def run_ours(args):
         "lm_c2": lm,
         "c1_single_factor": c1,
         "c4_overlap_sweep": c4,
+        "covariances_c3": cov,
         "clocks": clk,
         "inlier_fraction": inliers / P,
         "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()} | {"total": round(t_build, 3)},

@@ -152,6 +152,15 @@ int vgicp_graph_evaluate(vgicp_graph graph, const double* poses12, double* error
 int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, double* d_out, int32_t* d_inliers);
 int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, double* d_errors, int32_t* d_inliers);
 
+/* ---------------------------------------------------------------- preprocessing */
+/* estimate_covariances (point_cloud.cpp:44-83) on the GPU: exact k nearest neighbours (the point
+ * itself included, ties by lower index), neighbourhood covariance, eigenvectors kept and the
+ * spectrum clamped to (plane_epsilon, 1, 1). xyz: n×3 float32; cov6: n×6 float32 output
+ * (xx xy xz yy yz zz). Errors: k < 4, n <= k, NaN/Inf -> INVALID_ARGUMENT; k > 32 unsupported. */
+int vgicp_estimate_covariances(vgicp_ctx ctx, const float* xyz, size_t n, int k, double plane_epsilon, float* cov6);
+int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, const size_t* n, int m, int k,
+                                     double plane_epsilon, float* const* cov6);
+
 #ifdef __cplusplus
 }
 #endif

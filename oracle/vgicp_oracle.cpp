@@ -1114,4 +1114,73 @@ void or_make_scene(or_rng* rng, int points, double resolution, double boundary_m
 
 void or_rng_shuffle(or_rng* rng, uint64_t* perm, size_t n) { std::shuffle(perm, perm + n, rng->engine); }
 
+// reference::estimate_covariances (reference.cpp:11-37) with the brute-force kNN of
+// oracles.hpp:24-35 (full sort by (squared distance, index)) and a Jacobi eigen-solver in place of
+// Eigen::SelfAdjointEigenSolver: V·diag(eps,1,1)·Vᵀ = I - (1-eps)·v0·v0ᵀ for the unit eigenvector
+// v0 of the smallest eigenvalue. Means are n×3 doubles, output n×9 doubles.
+int or_estimate_covariances(const double* means, size_t n, int k, double plane_epsilon, double* covs) {
+  return guarded([&] {
+    if (k < 4 || n <= static_cast<size_t>(k))
+      throw std::invalid_argument("covariance estimation requires k >= 4 and more than k points");
+    std::vector<std::pair<double, int>> all(n);
+    for (size_t q = 0; q < n; ++q) {
+      for (size_t i = 0; i < n; ++i) {
+        double d2 = 0.0;
+        for (int a = 0; a < 3; ++a) {
+          const double d = means[3 * i + a] - means[3 * q + a];
+          d2 += d * d;
+        }
+        all[i] = {d2, static_cast<int>(i)};
+      }
+      std::partial_sort(all.begin(), all.begin() + k, all.end());
+      double mean[3] = {0, 0, 0};
+      for (int j = 0; j < k; ++j)
+        for (int a = 0; a < 3; ++a) mean[a] += means[3 * all[j].second + a];
+      for (int a = 0; a < 3; ++a) mean[a] /= static_cast<double>(k);
+      double A[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+      for (int j = 0; j < k; ++j) {
+        double d[3];
+        for (int a = 0; a < 3; ++a) d[a] = means[3 * all[j].second + a] - mean[a];
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) A[r][c] += d[r] * d[c];
+      }
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) A[r][c] /= static_cast<double>(k);
+      double V[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+      for (int sweep = 0; sweep < 100; ++sweep) {
+        const double off = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
+        if (off < 1e-32 * (A[0][0] * A[0][0] + A[1][1] * A[1][1] + A[2][2] * A[2][2]) + 1e-300) break;
+        for (int p = 0; p < 2; ++p)
+          for (int r = p + 1; r < 3; ++r) {
+            if (A[p][r] == 0.0) continue;
+            const double theta = (A[r][r] - A[p][p]) / (2.0 * A[p][r]);
+            const double t = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1.0));
+            const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+            for (int m = 0; m < 3; ++m) {
+              const double amp = A[m][p], amr = A[m][r];
+              A[m][p] = c * amp - sn * amr;
+              A[m][r] = sn * amp + c * amr;
+            }
+            for (int m = 0; m < 3; ++m) {
+              const double apm = A[p][m], arm = A[r][m];
+              A[p][m] = c * apm - sn * arm;
+              A[r][m] = sn * apm + c * arm;
+            }
+            for (int m = 0; m < 3; ++m) {
+              const double vmp = V[m][p], vmr = V[m][r];
+              V[m][p] = c * vmp - sn * vmr;
+              V[m][r] = sn * vmp + c * vmr;
+            }
+          }
+      }
+      int mi = 0;
+      if (A[1][1] < A[mi][mi]) mi = 1;
+      if (A[2][2] < A[mi][mi]) mi = 2;
+      const double v[3] = {V[0][mi], V[1][mi], V[2][mi]};
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) covs[9 * q + 3 * r + c] = (r == c ? 1.0 : 0.0) - (1.0 - plane_epsilon) * v[r] * v[c];
+    }
+  });
+}
+
 }  // extern "C"

@@ -92,6 +92,8 @@ void or_random_gaussian_cloud(or_rng* rng, int n, double scale, double* means, d
 void or_make_scene(or_rng* rng, int points, double resolution, double boundary_margin, double* T_target,
                    double* T_source, double* source_means, double* source_covs, double* target_means,
                    double* target_covs);
+/* reference::estimate_covariances (reference.cpp:11-37): brute-force kNN, eigen-regularised. */
+int or_estimate_covariances(const double* means, size_t n, int k, double plane_epsilon, double* covs);
 /* std::shuffle(perm, rng.engine) as in test_voxelmap.cpp:104 */
 void or_rng_shuffle(or_rng* rng, uint64_t* perm, size_t n);
 

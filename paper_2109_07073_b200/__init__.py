@@ -17,6 +17,8 @@ from .vgicp import (
     as_pose12,
     cov6_from,
     default_context,
+    estimate_covariances,
+    estimate_covariances_batch,
     evaluate_matching_cost,
     gicp_error,
     linearize_matching_cost,
@@ -40,6 +42,8 @@ __all__ = [
     "as_pose12",
     "cov6_from",
     "default_context",
+    "estimate_covariances",
+    "estimate_covariances_batch",
     "evaluate_matching_cost",
     "gicp_error",
     "linearize_matching_cost",

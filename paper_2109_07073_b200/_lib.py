@@ -85,6 +85,8 @@ SIGNATURES = {
     "vgicp_graph_evaluate": (_i, [_vp, _vp, _vp, _vp]),
     "vgicp_graph_linearize_device": (_i, [_vp, _vp, _vp, _vp]),
     "vgicp_graph_evaluate_device": (_i, [_vp, _vp, _vp, _vp]),
+    "vgicp_estimate_covariances": (_i, [_vp, _vp, _sz, _i, _d, _vp]),
+    "vgicp_estimate_covariances_batch": (_i, [_vp, _vp, _vp, _i, _i, _d, _vp]),
 }
 
 _LIB = None

@@ -896,4 +896,107 @@ int vgicp_gicp_error(vgicp_ctx ctx, const double source_mean[3], const double so
   return VGICP_OK;
 }
 
+// ------------------------------------------------------------------------------------ preprocessing
+int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, const size_t* n, int m, int k,
+                                     double plane_epsilon, float* const* cov6) {
+  if (!ctx || (m > 0 && (!xyz || !n || !cov6))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (m <= 0) return VGICP_OK;
+  // estimate_covariances validation (point_cloud.cpp:47-53)
+  if (k < 4) return fail(VGICP_E_INVALID_ARGUMENT, "covariance estimation requires k >= 4 neighbors");
+  if (k > 32) return fail(VGICP_E_INVALID_ARGUMENT, "covariance estimation supports k <= 32 on the GPU");
+  std::vector<CovSeg> segs(m);
+  size_t total = 0;
+  unsigned long long cells = 0;
+  unsigned max_n = 0;
+  for (int c = 0; c < m; ++c) {
+    if (n[c] <= static_cast<size_t>(k))
+      return fail(VGICP_E_INVALID_ARGUMENT, "covariance estimation requires more than k points");
+    if (!xyz[c] || !cov6[c]) return fail(VGICP_E_INVALID_ARGUMENT, "null point or output array");
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (size_t i = 0; i < n[c]; ++i)
+      for (int a = 0; a < 3; ++a) {
+        const double v = xyz[c][3 * i + a];
+        if (!std::isfinite(v)) return fail(VGICP_E_INVALID_ARGUMENT, "point cloud contains NaN/Inf coordinates");
+        lo[a] = std::min(lo[a], v);
+        hi[a] = std::max(hi[a], v);
+      }
+    const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], 1e-3});
+    double cell = std::max(std::sqrt(ext * ext * k / static_cast<double>(n[c])), 1e-3);
+    int g[3];
+    for (;;) {
+      unsigned long long gc = 1;
+      for (int a = 0; a < 3; ++a) {
+        g[a] = static_cast<int>(std::floor((hi[a] - lo[a]) / cell)) + 1;
+        gc *= static_cast<unsigned long long>(g[a]);
+      }
+      if (gc <= (1ull << 22)) break;
+      cell *= 1.5;
+    }
+    CovSeg& sg = segs[c];
+    sg.offset = static_cast<unsigned>(total);
+    sg.n = static_cast<unsigned>(n[c]);
+    sg.cell_base = static_cast<unsigned>(cells);
+    sg.gx = g[0], sg.gy = g[1], sg.gz = g[2];
+    for (int a = 0; a < 3; ++a) sg.lo[a] = lo[a];
+    sg.cell = cell;
+    sg.eps = plane_epsilon;
+    total += n[c];
+    cells += static_cast<unsigned long long>(g[0]) * g[1] * g[2];
+    max_n = std::max(max_n, sg.n);
+  }
+  if (total >= (1ull << 31) || cells >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "batch too large");
+  DeviceGuard gd(ctx->device);
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t o_segs = carve(sizeof(CovSeg) * m);
+  const size_t o_xyz = carve(sizeof(float) * 3 * total);
+  const size_t o_cov = carve(sizeof(float) * 6 * total);
+  const size_t o_cell = carve(sizeof(unsigned) * total);
+  const size_t o_sorted = carve(sizeof(unsigned) * total);
+  const size_t o_cnt = carve(sizeof(unsigned) * (cells + 1));
+  const size_t o_start = carve(sizeof(unsigned) * (cells + 1));
+  const size_t o_cursor = carve(sizeof(unsigned) * cells);
+  size_t scan_bytes = 0;
+  VG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                        static_cast<int>(cells + 1), ctx->stream));
+  const size_t o_temp = carve(scan_bytes);
+  if (int rc = ensure_scratch(ctx, off)) return rc;
+  if (int rc = ensure_pinned(ctx, sizeof(float) * 6 * total)) return rc;
+  char* sb = static_cast<char*>(ctx->scratch);
+  auto* d_segs = reinterpret_cast<CovSeg*>(sb + o_segs);
+  auto* d_xyz = reinterpret_cast<float*>(sb + o_xyz);
+  auto* d_cov = reinterpret_cast<float*>(sb + o_cov);
+  auto* d_cell = reinterpret_cast<unsigned*>(sb + o_cell);
+  auto* d_sorted = reinterpret_cast<unsigned*>(sb + o_sorted);
+  auto* d_cnt = reinterpret_cast<unsigned*>(sb + o_cnt);
+  auto* d_start = reinterpret_cast<unsigned*>(sb + o_start);
+  auto* d_cursor = reinterpret_cast<unsigned*>(sb + o_cursor);
+  cudaStream_t s = ctx->stream;
+  VG_CUDA(cudaStreamSynchronize(s));
+  float* h = static_cast<float*>(ctx->pinned);
+  for (int c = 0; c < m; ++c) std::memcpy(h + 3 * segs[c].offset, xyz[c], sizeof(float) * 3 * n[c]);
+  VG_CUDA(cudaMemcpyAsync(d_xyz, h, sizeof(float) * 3 * total, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemcpyAsync(d_segs, segs.data(), sizeof(CovSeg) * m, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned) * (cells + 1), s));
+  VG_CUDA(cudaMemsetAsync(d_cursor, 0, sizeof(unsigned) * cells, s));
+  VG_CUDA(launch_cov_count(d_segs, m, max_n, d_xyz, d_cell, d_cnt, s));
+  VG_CUDA(cub::DeviceScan::ExclusiveSum(sb + o_temp, scan_bytes, d_cnt, d_start, static_cast<int>(cells + 1), s));
+  VG_CUDA(launch_cov_scatter(d_segs, m, max_n, d_cell, d_start, d_cursor, d_sorted, s));
+  VG_CUDA(launch_cov_knn(d_segs, m, max_n, d_xyz, d_start, d_sorted, k, d_cov, s));
+  ctx->launches += 4;
+  VG_CUDA(cudaMemcpyAsync(h, d_cov, sizeof(float) * 6 * total, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  for (int c = 0; c < m; ++c) std::memcpy(cov6[c], h + 6 * segs[c].offset, sizeof(float) * 6 * n[c]);
+  return VGICP_OK;
+}
+
+int vgicp_estimate_covariances(vgicp_ctx ctx, const float* xyz, size_t n, int k, double plane_epsilon,
+                               float* cov6) {
+  return vgicp_estimate_covariances_batch(ctx, &xyz, &n, 1, k, plane_epsilon, &cov6);
+}
+
 }  // extern "C"

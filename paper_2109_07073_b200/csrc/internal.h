@@ -83,6 +83,16 @@ struct InsertJob {       // hash-table insertion of one map's voxels
   unsigned pad;
 };
 
+struct CovSeg {          // covariance preprocessing of one cloud
+  unsigned offset;       // first point in the concatenated arrays
+  unsigned n;
+  unsigned cell_base;    // first cell of this cloud in the global cell arrays
+  int gx, gy, gz;
+  double lo[3];
+  double cell;
+  double eps;
+};
+
 constexpr int kFactorThreads = 256;
 constexpr int kFactorWarps = kFactorThreads / 32;
 constexpr int kFactorTile = 512;    // points per CTA tile (kFactorThreads x kILP)
@@ -108,6 +118,12 @@ cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkIt
                           const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
                           int* out_inl, cudaStream_t s);
 cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s);
+cudaError_t launch_cov_count(const CovSeg* segs, int m, unsigned max_n, const float* xyz, unsigned* cell_of,
+                             unsigned* cnt, cudaStream_t s);
+cudaError_t launch_cov_scatter(const CovSeg* segs, int m, unsigned max_n, const unsigned* cell_of,
+                               const unsigned* start, unsigned* cursor, unsigned* sorted, cudaStream_t s);
+cudaError_t launch_cov_knn(const CovSeg* segs, int m, unsigned max_n, const float* xyz, const unsigned* start,
+                           const unsigned* sorted, int k, float* cov6, cudaStream_t s);
 
 }  // namespace vgicp
 

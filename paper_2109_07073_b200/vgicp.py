@@ -40,6 +40,8 @@ __all__ = [
     "FactorGraph",
     "as_pose12",
     "cov6_from",
+    "estimate_covariances",
+    "estimate_covariances_batch",
 ]
 
 
@@ -181,6 +183,26 @@ class PointCloud(_Handle):
 
     def has_covariances(self) -> bool:
         return self.cov6 is not None and self.size() > 0
+
+
+def estimate_covariances(points, k: int = 10, plane_epsilon: float = 1e-3, ctx: Context | None = None) -> np.ndarray:
+    """estimate_covariances (point_cloud.cpp:44-83) on the GPU -> n×6 float32 (xx xy xz yy yz zz)."""
+    return estimate_covariances_batch([points], k, plane_epsilon, ctx)[0]
+
+
+def estimate_covariances_batch(clouds, k: int = 10, plane_epsilon: float = 1e-3, ctx: Context | None = None) -> list:
+    """Covariances of many clouds in one batched GPU pass."""
+    ctx = ctx or default_context()
+    pts = [np.ascontiguousarray(np.asarray(p, dtype=np.float32).reshape(-1, 3)) for p in clouds]
+    outs = [np.zeros((len(p), 6), np.float32) for p in pts]
+    m = len(pts)
+    if m == 0:
+        return []
+    xp = (C.c_void_p * m)(*[p.ctypes.data for p in pts])
+    ns = (C.c_size_t * m)(*[len(p) for p in pts])
+    op = (C.c_void_p * m)(*[o.ctypes.data for o in outs])
+    check(_lib.load().vgicp_estimate_covariances_batch(ctx.handle, xp, ns, m, int(k), float(plane_epsilon), op))
+    return outs
 
 
 # ------------------------------------------------------------------------------------ voxel maps

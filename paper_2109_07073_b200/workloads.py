@@ -18,7 +18,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import synthetic as S
-from .vgicp import Context, FactorGraph, GaussianVoxelMap, MatchingCostFactor, PointCloud, overlap_hits
+from .vgicp import (Context, FactorGraph, GaussianVoxelMap, MatchingCostFactor, PointCloud, estimate_covariances_batch,
+                    overlap_hits)
 
 
 def pose_inv(T):
@@ -43,12 +44,19 @@ class Scans:
     odom: np.ndarray
 
 
-def make_scans(spec: S.SceneSpec, frames_needed=None, threads: int = 0) -> Scans:
+def make_scans(spec: S.SceneSpec, frames_needed=None, threads: int = 0, ctx: Context | None = None) -> Scans:
+    """Generate the scans and their plane-regularised covariances (k=10, eps=1e-3, as
+    run_pipeline.cpp:131). With a context the covariances come from the batched GPU kernel
+    (estimate_covariances_batch), otherwise from the host preprocessing (synthetic.cpp)."""
     seq = S.generate(spec)
-    idx = range(len(seq.scans)) if frames_needed is None else frames_needed
+    idx = list(range(len(seq.scans)) if frames_needed is None else frames_needed)
     covs = [None] * len(seq.scans)
-    for k in idx:
-        covs[k] = S.estimate_covariances(seq.scans[k], 10, 1e-3, threads)
+    if ctx is not None:
+        for k, c in zip(idx, estimate_covariances_batch([seq.scans[k] for k in idx], 10, 1e-3, ctx)):
+            covs[k] = c
+    else:
+        for k in idx:
+            covs[k] = S.estimate_covariances(seq.scans[k], 10, 1e-3, threads)
     return Scans(seq.scans, covs, seq.ground_truth, seq.odometry)
 
 
@@ -103,9 +111,10 @@ class GraphWorkload:
 
 
 def build_graph_workload(ctx: Context, spec: S.SceneSpec, resolution: float = 1.0, max_links: int = 10,
-                         min_overlap: float = 0.025, links=None, chunk: int = 0, threads: int = 0) -> GraphWorkload:
+                         min_overlap: float = 0.025, links=None, chunk: int = 0, threads: int = 0,
+                         gpu_covariances: bool = True) -> GraphWorkload:
     t0 = time.perf_counter()
-    scans = make_scans(spec, threads=threads)
+    scans = make_scans(spec, threads=threads, ctx=ctx if gpu_covariances else None)
     t1 = time.perf_counter()
     clouds = [PointCloud(m, c, ctx) for m, c in zip(scans.means, scans.cov6)]
     maps = GaussianVoxelMap.build_batch(clouds, resolution)

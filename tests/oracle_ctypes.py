@@ -67,6 +67,7 @@ def _load():
         "or_random_gaussian_cloud": (None, [vp, i, d, _dp, _dp]),
         "or_make_scene": (None, [vp, i, d, d, _dp, _dp, _dp, _dp, _dp, _dp]),
         "or_rng_shuffle": (None, [vp, _u64p, sz]),
+        "or_estimate_covariances": (i, [_dp, sz, i, d, _dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -401,6 +402,14 @@ def brute_force_overlap_count(cloud, rel, map_points, resolution) -> int:
     idx = np.searchsorted(cells_v, q_v)
     idx = np.clip(idx, 0, len(cells_v) - 1)
     return int(np.sum(cells_v[idx] == q_v))
+
+
+def estimate_covariances(means, k=10, plane_epsilon=1e-3) -> np.ndarray:
+    """reference::estimate_covariances restatement (brute-force kNN); n×3×3."""
+    m = _f64(means, (-1, 3))
+    out = np.zeros((len(m), 9))
+    _check(lib().or_estimate_covariances(m, len(m), int(k), float(plane_epsilon), out))
+    return out.reshape(-1, 3, 3)
 
 
 def unit_covariances(n) -> np.ndarray:
