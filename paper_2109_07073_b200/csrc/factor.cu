@@ -97,17 +97,23 @@ struct WarpTile {
   float4 pb[kWarpTile];  // c_xy c_xz c_yy c_yz
   float pc[kWarpTile];   // c_zz
 };
-struct WarpStage {
-  float lx[kWarpTile], ly[kWarpTile], lz[kWarpTile];  // q - voxel corner (fp64 -> fp32)
-  float qx[kWarpTile], qy[kWarpTile], qz[kWarpTile];  // q (Jacobian lever arm)
-  int slot[kWarpTile];
-  unsigned char list[kWarpTile];
+// Per-warp FIFO of probe hits waiting for the math phase. The probe phase appends the hits of a
+// tile; the math phase consumes them only in full batches of 32 (every lane busy), carrying the
+// remainder over to the next tile. Entries are self-contained (the ring slot of their tile may be
+// refilled before they are consumed). SoA float4 columns: conflict-free 128-bit stores / loads.
+constexpr int kQueue = 128;  // > 31 carried + kWarpTile new
+static_assert((kQueue & (kQueue - 1)) == 0 && kQueue >= 31 + kWarpTile, "hit queue too small");
+struct HitQueue {
+  float4 a[kQueue];  // l.x l.y l.z q.x   (l = q - voxel corner, q = T_ts·mu)
+  float4 b[kQueue];  // q.y q.z slot c_xx
+  float4 c[kQueue];  // c_xy c_xz c_yy c_yz
+  float d[kQueue];   // c_zz
 };
 struct __align__(128) FactorSmem {
   union {
     WarpTile ring[kWarps][kStages];
   } u;
-  WarpStage stage[kWarps];
+  HitQueue hq[kWarps];
   unsigned long long bar[kWarps][kStages];
   double T[12];
   float Rf[9];
@@ -164,13 +170,123 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
 
   const MapDev map = fp->map;
   const double* T = sm.T;  // T_ts stays in shared memory (broadcast reads)
-  WarpStage& st = sm.stage[warp];
+  HitQueue& hq = sm.hq[warp];
   const unsigned lane_lt = (1u << lane) - 1u;
 
   float acc[kAcc];
 #pragma unroll
   for (int k = 0; k < kAcc; ++k) acc[k] = 0.f;
   int inl = 0;
+  unsigned head = 0, tail = 0;  // hit queue cursors (warp-uniform)
+
+  // ---- math phase for one queued hit ----
+  auto consume = [&](unsigned idx) {
+    const float4 qa = hq.a[idx];
+    const float4 qb = hq.b[idx];
+    const float4 qc = hq.c[idx];
+    const float szz = hq.d[idx];
+    const int sl = __float_as_int(qb.z);
+    float4 v0, v1;  // (mx my mz cxx) (cxy cxz cyy cyz)
+    ldg256(map.sa + sl, reinterpret_cast<unsigned&>(v0.x), reinterpret_cast<unsigned&>(v0.y),
+           reinterpret_cast<unsigned&>(v0.z), reinterpret_cast<unsigned&>(v0.w), reinterpret_cast<unsigned&>(v1.x),
+           reinterpret_cast<unsigned&>(v1.y), reinterpret_cast<unsigned&>(v1.z), reinterpret_cast<unsigned&>(v1.w));
+    const float2 v2 = __ldg(reinterpret_cast<const float2*>(map.sb + sl));  // czz vid
+    const float sxx = qb.w, sxy = qc.x, sxz = qc.y, syy = qc.z, syz = qc.w;
+
+    // residual e = mu' - q in voxel-local coordinates
+    const float e0 = v0.x - qa.x;
+    const float e1 = v0.y - qa.y;
+    const float e2 = v0.z - qa.z;
+
+    // M = C_t + R C_s Rᵀ (fp32)
+    const float r00 = sm.Rf[0], r01 = sm.Rf[1], r02 = sm.Rf[2];
+    const float r10 = sm.Rf[3], r11 = sm.Rf[4], r12 = sm.Rf[5];
+    const float r20 = sm.Rf[6], r21 = sm.Rf[7], r22 = sm.Rf[8];
+    const float t00 = r00 * sxx + r01 * sxy + r02 * sxz;
+    const float t01 = r00 * sxy + r01 * syy + r02 * syz;
+    const float t02 = r00 * sxz + r01 * syz + r02 * szz;
+    const float t10 = r10 * sxx + r11 * sxy + r12 * sxz;
+    const float t11 = r10 * sxy + r11 * syy + r12 * syz;
+    const float t12 = r10 * sxz + r11 * syz + r12 * szz;
+    const float t20 = r20 * sxx + r21 * sxy + r22 * sxz;
+    const float t21 = r20 * sxy + r21 * syy + r22 * syz;
+    const float t22 = r20 * sxz + r21 * syz + r22 * szz;
+    const float m00 = v0.w + (t00 * r00 + t01 * r01 + t02 * r02);
+    const float m01 = v1.x + (t00 * r10 + t01 * r11 + t02 * r12);
+    const float m02 = v1.y + (t00 * r20 + t01 * r21 + t02 * r22);
+    const float m11 = v1.z + (t10 * r10 + t11 * r11 + t12 * r12);
+    const float m12 = v1.w + (t10 * r20 + t11 * r21 + t12 * r22);
+    const float m22 = v2.x + (t20 * r20 + t21 * r21 + t22 * r22);
+
+    // Omega = M⁻¹ by cofactors; Sylvester test with margins decides the fast path
+    const float a00 = m11 * m22 - m12 * m12;
+    const float a01 = m02 * m12 - m01 * m22;
+    const float a02 = m01 * m12 - m02 * m11;
+    const float a11 = m00 * m22 - m02 * m02;
+    const float a12 = m01 * m02 - m00 * m12;
+    const float a22 = m00 * m11 - m01 * m01;
+    const float det = m00 * a00 + m01 * a01 + m02 * a02;
+    const float tr = m00 + m11 + m22;
+    float o00, o01, o02, o11, o12, o22;
+    if (tr > 0.f && m00 > 1e-6f * tr && a22 > 1e-6f * tr * tr && det > 1e-5f * tr * tr * tr) {
+      float inv;  // MUFU reciprocal + one Newton step (~1 ulp; the fp32 algebra sets the tolerance)
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(det));
+      inv = inv * (2.0f - det * inv);
+      o00 = a00 * inv;
+      o01 = a01 * inv;
+      o02 = a02 * inv;
+      o11 = a11 * inv;
+      o12 = a12 * inv;
+      o22 = a22 * inv;
+    } else {
+      float om[6];
+      if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.y), om)) return;
+      o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
+    }
+    const float w0 = o00 * e0 + o01 * e1 + o02 * e2;
+    const float w1 = o01 * e0 + o11 * e1 + o12 * e2;
+    const float w2 = o02 * e0 + o12 * e1 + o22 * e2;
+    ++inl;
+    if constexpr (!kLinearize) {
+      acc[0] += e0 * w0 + e1 * w1 + e2 * w2;
+    } else {
+      const float qf0 = qa.w, qf1 = qb.x, qf2 = qb.y;
+      // P = [q]x Ω
+      const float p00 = qf1 * o02 - qf2 * o01, p01 = qf1 * o12 - qf2 * o11, p02 = qf1 * o22 - qf2 * o12;
+      const float p10 = qf2 * o00 - qf0 * o02, p11 = qf2 * o01 - qf0 * o12, p12 = qf2 * o02 - qf0 * o22;
+      const float p20 = qf0 * o01 - qf1 * o00, p21 = qf0 * o11 - qf1 * o01, p22 = qf0 * o12 - qf1 * o02;
+      // Q = -P [q]x  (symmetric)
+      acc[0] += p02 * qf1 - p01 * qf2;   // Q00
+      acc[1] += p00 * qf2 - p02 * qf0;   // Q01
+      acc[2] += p01 * qf0 - p00 * qf1;   // Q02
+      acc[3] += p10 * qf2 - p12 * qf0;   // Q11
+      acc[4] += p11 * qf0 - p10 * qf1;   // Q12
+      acc[5] += p21 * qf0 - p20 * qf1;   // Q22
+      acc[6] += p00;
+      acc[7] += p01;
+      acc[8] += p02;
+      acc[9] += p10;
+      acc[10] += p11;
+      acc[11] += p12;
+      acc[12] += p20;
+      acc[13] += p21;
+      acc[14] += p22;
+      acc[15] += o00;
+      acc[16] += o01;
+      acc[17] += o02;
+      acc[18] += o11;
+      acc[19] += o12;
+      acc[20] += o22;
+      // b_t = -AᵀΩe = [-(q × w); -w]
+      acc[21] -= qf1 * w2 - qf2 * w1;
+      acc[22] -= qf2 * w0 - qf0 * w2;
+      acc[23] -= qf0 * w1 - qf1 * w0;
+      acc[24] -= w0;
+      acc[25] -= w1;
+      acc[26] -= w2;
+      acc[27] += e0 * w0 + e1 * w1 + e2 * w2;
+    }
+  };
 
   for (int k = 0; k < my_tiles; ++k) {
     const int stage = k % kStages;
@@ -178,165 +294,64 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
     }
     const WarpTile& tb = sm.u.ring[warp][stage];
     const int tile_n = min(kWarpTile, w.end - (w.begin + (warp + k * kWarps) * kWarpTile));
-    const int wbase = 0;
 
-    // ---- phase 1: transform, exact key, both bucket loads for kILP points per lane ----
-    double Tr[12];  // T_ts in registers for this tile's transforms only (dead again in phase 2)
+    // ---- probe phase: kILP points per lane — fp64 transform (reference op order, T_ts in
+    //      registers for this tile only), exact key, both bucket loads of all points issued before
+    //      any compare ----
+    double Tr[12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) Tr[q] = T[q];
     unsigned hi[kILP], lo[kILP], b1[kILP], b2[kILP];
+    float l0[kILP], l1[kILP], l2[kILP], q0[kILP], q1[kILP], q2[kILP];
     bool ok[kILP];
 #pragma unroll
     for (int u = 0; u < kILP; ++u) {
       const int p = u * 32 + lane;
-      const int lp = min(wbase + p, tile_n - 1);  // clamped: every lane computes, in-range lanes count
+      const int lp = min(p, tile_n - 1);  // clamped: every lane computes, in-range lanes count
       const float4 A = tb.pa[lp];
-      double q0, q1, q2, l0, l1, l2;
-      apply_pose_rn(Tr, A.x, A.y, A.z, q0, q1, q2);
+      double qd0, qd1, qd2, ld0, ld1, ld2;
+      apply_pose_rn(Tr, A.x, A.y, A.z, qd0, qd1, qd2);
       unsigned k0 = 0, k1 = 0, k2 = 0;
-      ok[u] = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && (wbase + p < tile_n);
+      ok[u] = voxel_key(qd0, qd1, qd2, map.res, map.inv_res, k0, k1, k2, ld0, ld1, ld2) && (p < tile_n);
       pack_key32(k0, k1, k2, hi[u], lo[u]);
       b1[u] = bucket1(k0, k1, k2, map.shift);
       b2[u] = bucket2(k0, k1, k2, map.shift);
-      st.lx[p] = (float)l0;
-      st.ly[p] = (float)l1;
-      st.lz[p] = (float)l2;
-      st.qx[p] = (float)q0;
-      st.qy[p] = (float)q1;
-      st.qz[p] = (float)q2;
+      l0[u] = (float)ld0, l1[u] = (float)ld1, l2[u] = (float)ld2;
+      q0[u] = (float)qd0, q1[u] = (float)qd1, q2[u] = (float)qd2;
     }
     BucketPair bp[kILP];
 #pragma unroll
     for (int u = 0; u < kILP; ++u) bp[u] = load_buckets(map.keys, b1[u], b2[u]);  // always in-bounds
-    int cnt = 0;
 #pragma unroll
     for (int u = 0; u < kILP; ++u) {
-      const int s = ok[u] ? match_buckets(bp[u], b1[u], b2[u], hi[u], lo[u]) : -1;
-      const bool hit = s >= 0;
+      const int s = match_buckets(bp[u], b1[u], b2[u], hi[u], lo[u]);
+      const bool hit = ok[u] && s >= 0;
       const unsigned ball = __ballot_sync(0xffffffffu, hit);
       if (hit) {
         const int p = u * 32 + lane;
-        st.slot[p] = s;
-        st.list[cnt + __popc(ball & lane_lt)] = static_cast<unsigned char>(p);
+        const unsigned idx = (tail + __popc(ball & lane_lt)) & (kQueue - 1);
+        const float4 B = tb.pb[p];
+        hq.a[idx] = make_float4(l0[u], l1[u], l2[u], q0[u]);
+        hq.b[idx] = make_float4(q1[u], q2[u], __int_as_float(s), tb.pa[p].w);
+        hq.c[idx] = B;
+        hq.d[idx] = tb.pc[p];
       }
-      cnt += __popc(ball);
+      tail += __popc(ball);
     }
-    __syncwarp();
-
-    // ---- phase 2: per-hit fp32 algebra over the compacted list (all lanes busy) ----
-    for (int e = lane; e < cnt; e += 32) {
-      const int p = st.list[e];
-      const int lp = wbase + p;
-      const int sl = st.slot[p];
-      float4 v0, v1;  // (mx my mz cxx) (cxy cxz cyy cyz)
-      ldg256(map.sa + sl, reinterpret_cast<unsigned&>(v0.x), reinterpret_cast<unsigned&>(v0.y),
-             reinterpret_cast<unsigned&>(v0.z), reinterpret_cast<unsigned&>(v0.w), reinterpret_cast<unsigned&>(v1.x),
-             reinterpret_cast<unsigned&>(v1.y), reinterpret_cast<unsigned&>(v1.z), reinterpret_cast<unsigned&>(v1.w));
-      const float2 v2 = __ldg(reinterpret_cast<const float2*>(map.sb + sl));  // czz vid
-      const float4 B = tb.pb[lp];  // sxy sxz syy syz
-      const float szz = tb.pc[lp];
-      const float sxx = tb.pa[lp].w, sxy = B.x, sxz = B.y, syy = B.z, syz = B.w;
-
-      // residual e = mu' - q in voxel-local coordinates
-      const float e0 = v0.x - st.lx[p];
-      const float e1 = v0.y - st.ly[p];
-      const float e2 = v0.z - st.lz[p];
-
-      // M = C_t + R C_s Rᵀ (fp32)
-      const float r00 = sm.Rf[0], r01 = sm.Rf[1], r02 = sm.Rf[2];
-      const float r10 = sm.Rf[3], r11 = sm.Rf[4], r12 = sm.Rf[5];
-      const float r20 = sm.Rf[6], r21 = sm.Rf[7], r22 = sm.Rf[8];
-      const float t00 = r00 * sxx + r01 * sxy + r02 * sxz;
-      const float t01 = r00 * sxy + r01 * syy + r02 * syz;
-      const float t02 = r00 * sxz + r01 * syz + r02 * szz;
-      const float t10 = r10 * sxx + r11 * sxy + r12 * sxz;
-      const float t11 = r10 * sxy + r11 * syy + r12 * syz;
-      const float t12 = r10 * sxz + r11 * syz + r12 * szz;
-      const float t20 = r20 * sxx + r21 * sxy + r22 * sxz;
-      const float t21 = r20 * sxy + r21 * syy + r22 * syz;
-      const float t22 = r20 * sxz + r21 * syz + r22 * szz;
-      const float m00 = v0.w + (t00 * r00 + t01 * r01 + t02 * r02);
-      const float m01 = v1.x + (t00 * r10 + t01 * r11 + t02 * r12);
-      const float m02 = v1.y + (t00 * r20 + t01 * r21 + t02 * r22);
-      const float m11 = v1.z + (t10 * r10 + t11 * r11 + t12 * r12);
-      const float m12 = v1.w + (t10 * r20 + t11 * r21 + t12 * r22);
-      const float m22 = v2.x + (t20 * r20 + t21 * r21 + t22 * r22);
-
-      // Omega = M⁻¹ by cofactors; Sylvester test with margins decides the fast path
-      const float a00 = m11 * m22 - m12 * m12;
-      const float a01 = m02 * m12 - m01 * m22;
-      const float a02 = m01 * m12 - m02 * m11;
-      const float a11 = m00 * m22 - m02 * m02;
-      const float a12 = m01 * m02 - m00 * m12;
-      const float a22 = m00 * m11 - m01 * m01;
-      const float det = m00 * a00 + m01 * a01 + m02 * a02;
-      const float tr = m00 + m11 + m22;
-      float o00, o01, o02, o11, o12, o22;
-      if (tr > 0.f && m00 > 1e-6f * tr && a22 > 1e-6f * tr * tr && det > 1e-5f * tr * tr * tr) {
-        float inv;  // MUFU reciprocal + one Newton step (~1 ulp; the fp32 algebra sets the tolerance)
-        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(det));
-        inv = inv * (2.0f - det * inv);
-        o00 = a00 * inv;
-        o01 = a01 * inv;
-        o02 = a02 * inv;
-        o11 = a11 * inv;
-        o12 = a12 * inv;
-        o22 = a22 * inv;
-      } else {
-        float om[6];
-        if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.y), om)) continue;
-        o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
-      }
-      const float w0 = o00 * e0 + o01 * e1 + o02 * e2;
-      const float w1 = o01 * e0 + o11 * e1 + o12 * e2;
-      const float w2 = o02 * e0 + o12 * e1 + o22 * e2;
-      ++inl;
-      if constexpr (!kLinearize) {
-        acc[0] += e0 * w0 + e1 * w1 + e2 * w2;
-      } else {
-        const float qf0 = st.qx[p], qf1 = st.qy[p], qf2 = st.qz[p];
-        // P = [q]x Ω
-        const float p00 = qf1 * o02 - qf2 * o01, p01 = qf1 * o12 - qf2 * o11, p02 = qf1 * o22 - qf2 * o12;
-        const float p10 = qf2 * o00 - qf0 * o02, p11 = qf2 * o01 - qf0 * o12, p12 = qf2 * o02 - qf0 * o22;
-        const float p20 = qf0 * o01 - qf1 * o00, p21 = qf0 * o11 - qf1 * o01, p22 = qf0 * o12 - qf1 * o02;
-        // Q = -P [q]x  (symmetric)
-        acc[0] += p02 * qf1 - p01 * qf2;   // Q00
-        acc[1] += p00 * qf2 - p02 * qf0;   // Q01
-        acc[2] += p01 * qf0 - p00 * qf1;   // Q02
-        acc[3] += p10 * qf2 - p12 * qf0;   // Q11
-        acc[4] += p11 * qf0 - p10 * qf1;   // Q12
-        acc[5] += p21 * qf0 - p20 * qf1;   // Q22
-        acc[6] += p00;
-        acc[7] += p01;
-        acc[8] += p02;
-        acc[9] += p10;
-        acc[10] += p11;
-        acc[11] += p12;
-        acc[12] += p20;
-        acc[13] += p21;
-        acc[14] += p22;
-        acc[15] += o00;
-        acc[16] += o01;
-        acc[17] += o02;
-        acc[18] += o11;
-        acc[19] += o12;
-        acc[20] += o22;
-        // b_t = -AᵀΩe = [-(q × w); -w]
-        acc[21] -= qf1 * w2 - qf2 * w1;
-        acc[22] -= qf2 * w0 - qf0 * w2;
-        acc[23] -= qf0 * w1 - qf1 * w0;
-        acc[24] -= w0;
-        acc[25] -= w1;
-        acc[26] -= w2;
-        acc[27] += e0 * w0 + e1 * w1 + e2 * w2;
-      }
-    }
-    __syncwarp();  // the warp is done with this ring slot
+    __syncwarp();  // queue entries visible; the warp is done with this ring slot
     if (lane == 0 && k + kStages < my_tiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async refill
       issue_tile(k + kStages);
     }
+
+    // ---- math phase: full batches of 32 queued hits (all lanes busy) ----
+    while (tail - head >= 32u) {
+      consume((head + lane) & (kQueue - 1));
+      head += 32u;
+      __syncwarp();
+    }
   }
+  if (head + lane < tail) consume((head + lane) & (kQueue - 1));  // the last partial batch
   __syncwarp();  // this warp is done with its ring (no CTA-wide barrier after the prologue)
 
   // ---- warp reduction: fp64 butterfly over the 32 lanes, fixed order; one partial per warp
