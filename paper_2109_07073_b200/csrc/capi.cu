@@ -258,38 +258,45 @@ static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov
   const size_t na = align_up(n * sizeof(float4), 256);
   const size_t nc = align_up(n * sizeof(float), 256);
   const size_t half = na * 2 + nc;
-  const size_t bytes = std::max<size_t>(2 * half, 256);
+  const size_t nblk = (n + kPointBlock - 1) / kPointBlock;
+  const size_t bytes = std::max<size_t>(half + nblk * sizeof(PointBlock), 256);
   VG_CUDA(cudaMalloc(&c->block, bytes));
   char* base = static_cast<char*>(c->block);
   c->pa = reinterpret_cast<float4*>(base);
   c->pb = reinterpret_cast<float4*>(base + na);
   c->pc = reinterpret_cast<float*>(base + 2 * na);
-  c->spa = reinterpret_cast<float4*>(base + half);
-  c->spb = reinterpret_cast<float4*>(base + half + na);
-  c->spc = reinterpret_cast<float*>(base + half + 2 * na);
+  c->sblk = reinterpret_cast<PointBlock*>(base + half);
   if (n > 0) {
     if (int rc = ensure_pinned(ctx, bytes)) return rc;
     VG_CUDA(cudaStreamSynchronize(ctx->stream));
     const std::vector<uint32_t> perm = morton_order(xyz, n);
     char* h = static_cast<char*>(ctx->pinned);
-    for (int copy = 0; copy < 2; ++copy) {
-      float4* ha = reinterpret_cast<float4*>(h + copy * half);
-      float4* hb = reinterpret_cast<float4*>(h + copy * half + na);
-      float* hc = reinterpret_cast<float*>(h + copy * half + 2 * na);
-      for (size_t d = 0; d < n; ++d) {
-        const size_t i = copy == 0 ? d : perm[d];
-        const float* p = xyz + 3 * i;
-        if (cov6) {
-          const float* q = cov6 + 6 * i;
-          ha[d] = make_float4(p[0], p[1], p[2], q[0]);
-          hb[d] = make_float4(q[1], q[2], q[3], q[4]);
-          hc[d] = q[5];
-        } else {
-          ha[d] = make_float4(p[0], p[1], p[2], 0.f);
-          hb[d] = make_float4(0.f, 0.f, 0.f, 0.f);
-          hc[d] = 0.f;
-        }
+    float4* ha = reinterpret_cast<float4*>(h);
+    float4* hb = reinterpret_cast<float4*>(h + na);
+    float* hc = reinterpret_cast<float*>(h + 2 * na);
+    PointBlock* hblk = reinterpret_cast<PointBlock*>(h + half);
+    for (size_t d = 0; d < nblk * kPointBlock; ++d) {
+      const size_t i = d < n ? d : n - 1;  // input order (builds); padded tail repeats the last point
+      const size_t m = d < n ? perm[d] : perm[n - 1];  // Morton order (factor / overlap kernels)
+      float4 a[2], b[2];
+      float cz[2];
+      for (int copy = 0; copy < 2; ++copy) {
+        const size_t j = copy == 0 ? i : m;
+        const float* p = xyz + 3 * j;
+        const float* q = cov6 ? cov6 + 6 * j : nullptr;
+        a[copy] = make_float4(p[0], p[1], p[2], q ? q[0] : 0.f);
+        b[copy] = q ? make_float4(q[1], q[2], q[3], q[4]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        cz[copy] = q ? q[5] : 0.f;
       }
+      if (d < n) {
+        ha[d] = a[0];
+        hb[d] = b[0];
+        hc[d] = cz[0];
+      }
+      PointBlock& blk = hblk[d / kPointBlock];
+      blk.pa[d % kPointBlock] = a[1];
+      blk.pb[d % kPointBlock] = b[1];
+      blk.pc[d % kPointBlock] = cz[1];
     }
     VG_CUDA(cudaMemcpyAsync(c->block, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
     VG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -619,7 +626,7 @@ int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* 
     if (clouds[k]->ctx != ctx || maps[k]->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "handle of another context");
     if (clouds[k]->n == 0) return fail(VGICP_E_INVALID_ARGUMENT, "overlap_rate requires a nonempty cloud");
     OverlapItem& it = items[k];
-    it.pa = clouds[k]->spa;  // Morton order (hit counts are order-independent)
+    it.blk = clouds[k]->sblk;  // Morton order (hit counts are order-independent)
     it.map = maps[k]->dev();
     std::memcpy(it.T, poses12 + 12 * k, sizeof(double) * 12);
     it.n = static_cast<unsigned>(clouds[k]->n);
@@ -680,9 +687,7 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   for (int f = 0; f < num_factors; ++f) {
     const vgicp_factor_desc& d = factors[f];
     FactorDev& x = fd[f];
-    x.pa = d.source->spa;  // Morton order: neighbouring lanes probe neighbouring voxels
-    x.pb = d.source->spb;
-    x.pc = d.source->spc;
+    x.blk = d.source->sblk;  // Morton order: neighbouring lanes probe neighbouring voxels
     x.map = d.target->dev();
     x.n = static_cast<int>(d.source->n);
     x.tgt = d.target_index;

@@ -59,7 +59,7 @@ __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, f
 constexpr int kILP = VG_ILP;                        // points per lane per tile (independent probes in flight)
 constexpr int kWarpTile = 32 * kILP;           // points per warp per tile
 constexpr int kTile = kFactorThreads * kILP;   // points per CTA tile
-static_assert(kFactorTile % 4 == 0, "work-item starts must keep c_zz TMA copies 16-B aligned");
+static_assert(kFactorTile % kPointBlock == 0, "work items must start on a point block");
 constexpr int kRedStride = kFactorThreads + 1;  // padded column stride of the reduction transpose
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers --------------------------------------------------
@@ -88,15 +88,235 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
+// Per-hit math of the linearization (factors.cpp:99-134) in fp32, accumulated into the 28 sums
+// (or the error only): l = (q - voxel corner, q.x), qy/qz the rest of q, C_s = (cxx, cs = (xy xz yy
+// yz), szz), v0/v1/v2 the voxel's slot statistics. Near-singular M -> the fp64 LDLT decision.
+template <bool kLinearize>
+__device__ __forceinline__ void hit_math(const float* Rf, const double* T, const MapDev& map, float4 l, float qy,
+                                         float qz, float cxx, float4 cs, float szz, float4 v0, float4 v1, float2 v2,
+                                         float* acc, int& inl) {
+  const float sxx = cxx, sxy = cs.x, sxz = cs.y, syy = cs.z, syz = cs.w;
+
+  // residual e = mu' - q in voxel-local coordinates
+  const float e0 = v0.x - l.x;
+  const float e1 = v0.y - l.y;
+  const float e2 = v0.z - l.z;
+
+  // M = C_t + R C_s Rᵀ (fp32)
+  const float r00 = Rf[0], r01 = Rf[1], r02 = Rf[2];
+  const float r10 = Rf[3], r11 = Rf[4], r12 = Rf[5];
+  const float r20 = Rf[6], r21 = Rf[7], r22 = Rf[8];
+  const float t00 = r00 * sxx + r01 * sxy + r02 * sxz;
+  const float t01 = r00 * sxy + r01 * syy + r02 * syz;
+  const float t02 = r00 * sxz + r01 * syz + r02 * szz;
+  const float t10 = r10 * sxx + r11 * sxy + r12 * sxz;
+  const float t11 = r10 * sxy + r11 * syy + r12 * syz;
+  const float t12 = r10 * sxz + r11 * syz + r12 * szz;
+  const float t20 = r20 * sxx + r21 * sxy + r22 * sxz;
+  const float t21 = r20 * sxy + r21 * syy + r22 * syz;
+  const float t22 = r20 * sxz + r21 * syz + r22 * szz;
+  const float m00 = v0.w + (t00 * r00 + t01 * r01 + t02 * r02);
+  const float m01 = v1.x + (t00 * r10 + t01 * r11 + t02 * r12);
+  const float m02 = v1.y + (t00 * r20 + t01 * r21 + t02 * r22);
+  const float m11 = v1.z + (t10 * r10 + t11 * r11 + t12 * r12);
+  const float m12 = v1.w + (t10 * r20 + t11 * r21 + t12 * r22);
+  const float m22 = v2.x + (t20 * r20 + t21 * r21 + t22 * r22);
+
+  // Omega = M⁻¹ by cofactors; Sylvester test with margins decides the fast path
+  const float a00 = m11 * m22 - m12 * m12;
+  const float a01 = m02 * m12 - m01 * m22;
+  const float a02 = m01 * m12 - m02 * m11;
+  const float a11 = m00 * m22 - m02 * m02;
+  const float a12 = m01 * m02 - m00 * m12;
+  const float a22 = m00 * m11 - m01 * m01;
+  const float det = m00 * a00 + m01 * a01 + m02 * a02;
+  const float tr = m00 + m11 + m22;
+  float o00, o01, o02, o11, o12, o22;
+  if (tr > 0.f && m00 > 1e-6f * tr && a22 > 1e-6f * tr * tr && det > 1e-5f * tr * tr * tr) {
+    float inv;  // MUFU reciprocal + one Newton step (~1 ulp; the fp32 algebra sets the tolerance)
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(det));
+    inv = inv * (2.0f - det * inv);
+    o00 = a00 * inv;
+    o01 = a01 * inv;
+    o02 = a02 * inv;
+    o11 = a11 * inv;
+    o12 = a12 * inv;
+    o22 = a22 * inv;
+  } else {
+    float om[6];
+    if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.y), om)) return;
+    o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
+  }
+  const float w0 = o00 * e0 + o01 * e1 + o02 * e2;
+  const float w1 = o01 * e0 + o11 * e1 + o12 * e2;
+  const float w2 = o02 * e0 + o12 * e1 + o22 * e2;
+  ++inl;
+  if constexpr (!kLinearize) {
+    acc[0] += e0 * w0 + e1 * w1 + e2 * w2;
+  } else {
+    const float qf0 = l.w, qf1 = qy, qf2 = qz;
+    // P = [q]x Ω
+    const float p00 = qf1 * o02 - qf2 * o01, p01 = qf1 * o12 - qf2 * o11, p02 = qf1 * o22 - qf2 * o12;
+    const float p10 = qf2 * o00 - qf0 * o02, p11 = qf2 * o01 - qf0 * o12, p12 = qf2 * o02 - qf0 * o22;
+    const float p20 = qf0 * o01 - qf1 * o00, p21 = qf0 * o11 - qf1 * o01, p22 = qf0 * o12 - qf1 * o02;
+    // Q = -P [q]x  (symmetric)
+    acc[0] += p02 * qf1 - p01 * qf2;   // Q00
+    acc[1] += p00 * qf2 - p02 * qf0;   // Q01
+    acc[2] += p01 * qf0 - p00 * qf1;   // Q02
+    acc[3] += p10 * qf2 - p12 * qf0;   // Q11
+    acc[4] += p11 * qf0 - p10 * qf1;   // Q12
+    acc[5] += p21 * qf0 - p20 * qf1;   // Q22
+    acc[6] += p00;
+    acc[7] += p01;
+    acc[8] += p02;
+    acc[9] += p10;
+    acc[10] += p11;
+    acc[11] += p12;
+    acc[12] += p20;
+    acc[13] += p21;
+    acc[14] += p22;
+    acc[15] += o00;
+    acc[16] += o01;
+    acc[17] += o02;
+    acc[18] += o11;
+    acc[19] += o12;
+    acc[20] += o22;
+    // b_t = -AᵀΩe = [-(q × w); -w]
+    acc[21] -= qf1 * w2 - qf2 * w1;
+    acc[22] -= qf2 * w0 - qf0 * w2;
+    acc[23] -= qf0 * w1 - qf1 * w0;
+    acc[24] -= w0;
+    acc[25] -= w1;
+    acc[26] -= w2;
+    acc[27] += e0 * w0 + e1 * w1 + e2 * w2;
+  }
+}
+
+// End of a warp's share of a work item: fp64 butterfly over the 32 lanes in a fixed order, one
+// partial per warp (no float atomics; once per ~2,500 points per warp). An integer arrival counter
+// elects the last warp of the factor, which sums the factor's partials in (item, warp) order and
+// expands in fp64. `gw` = this warp's partial slot, `parts` = partial slots per work item, `ws` =
+// 180 doubles of per-warp shared scratch.
+template <bool kLinearize>
+__device__ __forceinline__ void finish_factor(const float* acc, int inl, int lane, size_t gw, int parts,
+                                              const WorkItem& w, const FactorDev* __restrict__ fp, const double* T,
+                                              double* ws, double* __restrict__ partials, int* __restrict__ part_inl,
+                                              unsigned* __restrict__ counters, double* __restrict__ out,
+                                              int* __restrict__ out_inl) {
+  constexpr int kAcc = kLinearize ? kLinAcc : 1;
+  // ---- warp reduction: fp64 butterfly over the 32 lanes, fixed order; one partial per warp
+  //      (no float atomics). Once per ~2,500 points per warp, so its cost is negligible. ----
+#pragma unroll
+  for (int k = 0; k < kAcc; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) partials[gw * kPartialStride + k] = v;
+  }
+  inl = __reduce_add_sync(0xffffffffu, inl);
+  if (lane == 0) part_inl[gw] = inl;
+  __threadfence();
+  __syncwarp();
+  unsigned last = 0;
+  if (lane == 0) last = (atomicAdd(&counters[w.factor], 1u) + 1u == (unsigned)(fp->item_count * parts)) ? 1u : 0u;
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+
+  // ---- last warp of this factor: (item, warp)-ordered sum of the partials, fp64 epilogue ----
+  double* tot = ws;           // 28
+  double* H = ws + 32;        // 36
+  double* Ad = ws + 72;       // 36
+  double* HA = ws + 108;      // 36
+  double* Hss = ws + 144;     // 36
+  const size_t gb = (size_t)fp->item_begin * parts;
+  const int gc = fp->item_count * parts;
+  if (lane < kAcc) {
+    double sum = 0.0;
+    for (int g = 0; g < gc; ++g) sum += __ldcg(&partials[(gb + g) * kPartialStride + lane]);
+    tot[lane] = sum;
+  }
+  int tinl = 0;
+  if (lane == 0) {
+    for (int g = 0; g < gc; ++g) tinl += __ldcg(&part_inl[gb + g]);
+    counters[w.factor] = 0u;  // ready for the next launch
+  }
+  __syncwarp();
+
+  if constexpr (!kLinearize) {
+    if (lane == 0) {
+      out[w.factor] = tot[0];
+      out_inl[w.factor] = tinl;
+    }
+    return;
+  } else {
+    const int f = w.factor;
+    double* o = out + (size_t)f * VGICP_LINEARIZED_DOUBLES;
+    for (int t = lane; t < 36; t += 32) {
+      const int i = t / 6, j = t % 6;
+      // H_tt = [[Q, P], [Pᵀ, Ω]]
+      const int qi[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+      double h;
+      if (i < 3 && j < 3) h = tot[qi[i][j]];
+      else if (i < 3) h = tot[6 + 3 * i + (j - 3)];
+      else if (j < 3) h = tot[6 + 3 * j + (i - 3)];
+      else h = tot[15 + qi[i - 3][j - 3]];
+      H[t] = h;
+      // Ad(T_ts) = [[R, 0], [[t]x R, R]]
+      double ad = 0.0;
+      if (i < 3 && j < 3) ad = T[3 * i + j];
+      else if (i >= 3 && j >= 3) ad = T[3 * (i - 3) + (j - 3)];
+      else if (i >= 3 && j < 3) {
+        const int r = i - 3;
+        const double tx = T[9], ty = T[10], tz = T[11];
+        const double sk[3][3] = {{0.0, -tz, ty}, {tz, 0.0, -tx}, {-ty, tx, 0.0}};
+        ad = dot3_rn(sk[r][0], sk[r][1], sk[r][2], T[j], T[3 + j], T[6 + j]);
+      }
+      Ad[t] = ad;
+    }
+    __syncwarp();
+    for (int t = lane; t < 36; t += 32) {
+      const int i = t / 6, j = t % 6;
+      double sum = 0.0;
+#pragma unroll
+      for (int m = 0; m < 6; ++m) sum += H[6 * i + m] * Ad[6 * m + j];
+      HA[t] = sum;  // H_tt · Ad
+    }
+    __syncwarp();
+    for (int t = lane; t < 36; t += 32) {
+      const int i = t / 6, j = t % 6;
+      double sum = 0.0;
+#pragma unroll
+      for (int m = 0; m < 6; ++m) sum += Ad[6 * m + i] * HA[6 * m + j];
+      Hss[t] = sum;  // Adᵀ · H_tt · Ad
+    }
+    __syncwarp();
+    for (int t = lane; t < 36; t += 32) {
+      const int i = t / 6, j = t % 6;
+      o[t] = H[t];                                       // H_ii (exactly symmetric)
+      o[36 + t] = -HA[t];                                // H_ij
+      o[72 + t] = 0.5 * (Hss[6 * i + j] + Hss[6 * j + i]);  // H_jj, symmetrised (factors.cpp:141)
+    }
+    if (lane < 6) {
+      o[108 + lane] = tot[21 + lane];  // b_i = b_t
+      double sum = 0.0;
+#pragma unroll
+      for (int m = 0; m < 6; ++m) sum += Ad[6 * m + lane] * tot[21 + m];
+      o[114 + lane] = -sum;  // b_j = -Adᵀ b_t
+    }
+    if (lane == 0) {
+      o[120] = tot[27];
+      out_inl[f] = tinl;
+    }
+  }
+}
+
 // Shared memory of one CTA. Every warp owns a private kStages-deep ring of source tiles that it
 // fills itself with TMA bulk copies (cp.async.bulk, mbarrier completion), so warps never wait on
 // each other inside the point loop; after the loop the rings are reused for the reduction.
 constexpr int kStages = VG_STAGES;
-struct WarpTile {
-  float4 pa[kWarpTile];  // x y z c_xx
-  float4 pb[kWarpTile];  // c_xy c_xz c_yy c_yz
-  float pc[kWarpTile];   // c_zz
-};
+using WarpTile = PointBlock;  // one Morton-ordered 64-point block of the source cloud
+static_assert(kWarpTile == kPointBlock, "a warp tile is one point block");
 // Per-warp FIFO of probe hits waiting for the math phase. The probe phase appends the hits of a
 // tile; the math phase consumes them only in full batches of 32 (every lane busy), carrying the
 // remainder over to the next tile. Entries are self-contained (the ring slot of their tile may be
@@ -137,25 +357,17 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
   const int warp = tid >> 5;
   const WorkItem w = items[blockIdx.x];
   const FactorDev* __restrict__ fp = factors + w.factor;
-  const float4* __restrict__ gpa = fp->pa;
-  const float4* __restrict__ gpb = fp->pb;
-  const float* __restrict__ gpc = fp->pc;
+  const PointBlock* __restrict__ gblk = fp->blk + w.begin / kPointBlock;
   // Warp `warp` processes the item's 64-point tiles warp, warp + kWarps, ... (balanced, no CTA
   // barrier in the loop); lane 0 streams them into the warp's ring with TMA bulk copies.
   const int ntiles_all = (w.end - w.begin + kWarpTile - 1) / kWarpTile;
   const int my_tiles = ntiles_all > warp ? (ntiles_all - warp + kWarps - 1) / kWarps : 0;
   unsigned long long* bars = sm.bar[warp];
-  auto issue_tile = [&](int k) {  // k-th tile of this warp -> ring slot k % kStages
+  auto issue_tile = [&](int k) {  // k-th tile of this warp (one 64-point block) -> ring slot k % kStages
     const int stage = k % kStages;
-    const int base = w.begin + (warp + k * kWarps) * kWarpTile;
-    const int cnt = min(kWarpTile, w.end - base);
-    const unsigned ba = static_cast<unsigned>(cnt) * 16u;
-    const unsigned bc = static_cast<unsigned>((cnt + 3) & ~3) * 4u;  // clouds are padded to 256 B
-    WarpTile& dst = sm.u.ring[warp][stage];
-    mbar_expect_tx(&bars[stage], 2u * ba + bc);
-    bulk_g2s(dst.pa, gpa + base, ba, &bars[stage]);
-    bulk_g2s(dst.pb, gpb + base, ba, &bars[stage]);
-    bulk_g2s(dst.pc, gpc + base, bc, &bars[stage]);
+    mbar_expect_tx(&bars[stage], static_cast<unsigned>(sizeof(PointBlock)));
+    bulk_g2s(&sm.u.ring[warp][stage], gblk + warp + k * kWarps, static_cast<unsigned>(sizeof(PointBlock)),
+             &bars[stage]);
   };
   if (lane == 0) {
 #pragma unroll
@@ -184,108 +396,13 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
     const float4 qa = hq.a[idx];
     const float4 qb = hq.b[idx];
     const float4 qc = hq.c[idx];
-    const float szz = hq.d[idx];
     const int sl = __float_as_int(qb.z);
     float4 v0, v1;  // (mx my mz cxx) (cxy cxz cyy cyz)
     ldg256(map.sa + sl, reinterpret_cast<unsigned&>(v0.x), reinterpret_cast<unsigned&>(v0.y),
            reinterpret_cast<unsigned&>(v0.z), reinterpret_cast<unsigned&>(v0.w), reinterpret_cast<unsigned&>(v1.x),
            reinterpret_cast<unsigned&>(v1.y), reinterpret_cast<unsigned&>(v1.z), reinterpret_cast<unsigned&>(v1.w));
     const float2 v2 = __ldg(reinterpret_cast<const float2*>(map.sb + sl));  // czz vid
-    const float sxx = qb.w, sxy = qc.x, sxz = qc.y, syy = qc.z, syz = qc.w;
-
-    // residual e = mu' - q in voxel-local coordinates
-    const float e0 = v0.x - qa.x;
-    const float e1 = v0.y - qa.y;
-    const float e2 = v0.z - qa.z;
-
-    // M = C_t + R C_s Rᵀ (fp32)
-    const float r00 = sm.Rf[0], r01 = sm.Rf[1], r02 = sm.Rf[2];
-    const float r10 = sm.Rf[3], r11 = sm.Rf[4], r12 = sm.Rf[5];
-    const float r20 = sm.Rf[6], r21 = sm.Rf[7], r22 = sm.Rf[8];
-    const float t00 = r00 * sxx + r01 * sxy + r02 * sxz;
-    const float t01 = r00 * sxy + r01 * syy + r02 * syz;
-    const float t02 = r00 * sxz + r01 * syz + r02 * szz;
-    const float t10 = r10 * sxx + r11 * sxy + r12 * sxz;
-    const float t11 = r10 * sxy + r11 * syy + r12 * syz;
-    const float t12 = r10 * sxz + r11 * syz + r12 * szz;
-    const float t20 = r20 * sxx + r21 * sxy + r22 * sxz;
-    const float t21 = r20 * sxy + r21 * syy + r22 * syz;
-    const float t22 = r20 * sxz + r21 * syz + r22 * szz;
-    const float m00 = v0.w + (t00 * r00 + t01 * r01 + t02 * r02);
-    const float m01 = v1.x + (t00 * r10 + t01 * r11 + t02 * r12);
-    const float m02 = v1.y + (t00 * r20 + t01 * r21 + t02 * r22);
-    const float m11 = v1.z + (t10 * r10 + t11 * r11 + t12 * r12);
-    const float m12 = v1.w + (t10 * r20 + t11 * r21 + t12 * r22);
-    const float m22 = v2.x + (t20 * r20 + t21 * r21 + t22 * r22);
-
-    // Omega = M⁻¹ by cofactors; Sylvester test with margins decides the fast path
-    const float a00 = m11 * m22 - m12 * m12;
-    const float a01 = m02 * m12 - m01 * m22;
-    const float a02 = m01 * m12 - m02 * m11;
-    const float a11 = m00 * m22 - m02 * m02;
-    const float a12 = m01 * m02 - m00 * m12;
-    const float a22 = m00 * m11 - m01 * m01;
-    const float det = m00 * a00 + m01 * a01 + m02 * a02;
-    const float tr = m00 + m11 + m22;
-    float o00, o01, o02, o11, o12, o22;
-    if (tr > 0.f && m00 > 1e-6f * tr && a22 > 1e-6f * tr * tr && det > 1e-5f * tr * tr * tr) {
-      float inv;  // MUFU reciprocal + one Newton step (~1 ulp; the fp32 algebra sets the tolerance)
-      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(det));
-      inv = inv * (2.0f - det * inv);
-      o00 = a00 * inv;
-      o01 = a01 * inv;
-      o02 = a02 * inv;
-      o11 = a11 * inv;
-      o12 = a12 * inv;
-      o22 = a22 * inv;
-    } else {
-      float om[6];
-      if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.y), om)) return;
-      o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
-    }
-    const float w0 = o00 * e0 + o01 * e1 + o02 * e2;
-    const float w1 = o01 * e0 + o11 * e1 + o12 * e2;
-    const float w2 = o02 * e0 + o12 * e1 + o22 * e2;
-    ++inl;
-    if constexpr (!kLinearize) {
-      acc[0] += e0 * w0 + e1 * w1 + e2 * w2;
-    } else {
-      const float qf0 = qa.w, qf1 = qb.x, qf2 = qb.y;
-      // P = [q]x Ω
-      const float p00 = qf1 * o02 - qf2 * o01, p01 = qf1 * o12 - qf2 * o11, p02 = qf1 * o22 - qf2 * o12;
-      const float p10 = qf2 * o00 - qf0 * o02, p11 = qf2 * o01 - qf0 * o12, p12 = qf2 * o02 - qf0 * o22;
-      const float p20 = qf0 * o01 - qf1 * o00, p21 = qf0 * o11 - qf1 * o01, p22 = qf0 * o12 - qf1 * o02;
-      // Q = -P [q]x  (symmetric)
-      acc[0] += p02 * qf1 - p01 * qf2;   // Q00
-      acc[1] += p00 * qf2 - p02 * qf0;   // Q01
-      acc[2] += p01 * qf0 - p00 * qf1;   // Q02
-      acc[3] += p10 * qf2 - p12 * qf0;   // Q11
-      acc[4] += p11 * qf0 - p10 * qf1;   // Q12
-      acc[5] += p21 * qf0 - p20 * qf1;   // Q22
-      acc[6] += p00;
-      acc[7] += p01;
-      acc[8] += p02;
-      acc[9] += p10;
-      acc[10] += p11;
-      acc[11] += p12;
-      acc[12] += p20;
-      acc[13] += p21;
-      acc[14] += p22;
-      acc[15] += o00;
-      acc[16] += o01;
-      acc[17] += o02;
-      acc[18] += o11;
-      acc[19] += o12;
-      acc[20] += o22;
-      // b_t = -AᵀΩe = [-(q × w); -w]
-      acc[21] -= qf1 * w2 - qf2 * w1;
-      acc[22] -= qf2 * w0 - qf0 * w2;
-      acc[23] -= qf0 * w1 - qf1 * w0;
-      acc[24] -= w0;
-      acc[25] -= w1;
-      acc[26] -= w2;
-      acc[27] += e0 * w0 + e1 * w1 + e2 * w2;
-    }
+    hit_math<kLinearize>(sm.Rf, T, map, qa, qb.x, qb.y, qb.w, qc, hq.d[idx], v0, v1, v2, acc, inl);
   };
 
   for (int k = 0; k < my_tiles; ++k) {
@@ -354,113 +471,8 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
   if (head + lane < tail) consume((head + lane) & (kQueue - 1));  // the last partial batch
   __syncwarp();  // this warp is done with its ring (no CTA-wide barrier after the prologue)
 
-  // ---- warp reduction: fp64 butterfly over the 32 lanes, fixed order; one partial per warp
-  //      (no float atomics). Once per ~2,500 points per warp, so its cost is negligible. ----
-  const size_t gw = (size_t)blockIdx.x * kWarps + warp;  // this warp's partial slot
-#pragma unroll
-  for (int k = 0; k < kAcc; ++k) {
-    double v = acc[k];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0) partials[gw * kPartialStride + k] = v;
-  }
-  inl = __reduce_add_sync(0xffffffffu, inl);
-  if (lane == 0) part_inl[gw] = inl;
-  __threadfence();
-  __syncwarp();
-  unsigned last = 0;
-  if (lane == 0) last = (atomicAdd(&counters[w.factor], 1u) + 1u == (unsigned)(fp->item_count * kWarps)) ? 1u : 0u;
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  __threadfence();
-
-  // ---- last warp of this factor: (item, warp)-ordered sum of the partials, fp64 epilogue ----
-  double* ws = reinterpret_cast<double*>(&sm.u.ring[warp][0]);  // per-warp scratch (ring is idle now)
-  double* tot = ws;           // 28
-  double* H = ws + 32;        // 36
-  double* Ad = ws + 72;       // 36
-  double* HA = ws + 108;      // 36
-  double* Hss = ws + 144;     // 36
-  const size_t gb = (size_t)fp->item_begin * kWarps;
-  const int gc = fp->item_count * kWarps;
-  if (lane < kAcc) {
-    double sum = 0.0;
-    for (int g = 0; g < gc; ++g) sum += __ldcg(&partials[(gb + g) * kPartialStride + lane]);
-    tot[lane] = sum;
-  }
-  int tinl = 0;
-  if (lane == 0) {
-    for (int g = 0; g < gc; ++g) tinl += __ldcg(&part_inl[gb + g]);
-    counters[w.factor] = 0u;  // ready for the next launch
-  }
-  __syncwarp();
-
-  if constexpr (!kLinearize) {
-    if (lane == 0) {
-      out[w.factor] = tot[0];
-      out_inl[w.factor] = tinl;
-    }
-    return;
-  } else {
-    const int f = w.factor;
-    double* o = out + (size_t)f * VGICP_LINEARIZED_DOUBLES;
-    for (int t = lane; t < 36; t += 32) {
-      const int i = t / 6, j = t % 6;
-      // H_tt = [[Q, P], [Pᵀ, Ω]]
-      const int qi[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
-      double h;
-      if (i < 3 && j < 3) h = tot[qi[i][j]];
-      else if (i < 3) h = tot[6 + 3 * i + (j - 3)];
-      else if (j < 3) h = tot[6 + 3 * j + (i - 3)];
-      else h = tot[15 + qi[i - 3][j - 3]];
-      H[t] = h;
-      // Ad(T_ts) = [[R, 0], [[t]x R, R]]
-      double ad = 0.0;
-      if (i < 3 && j < 3) ad = sm.T[3 * i + j];
-      else if (i >= 3 && j >= 3) ad = sm.T[3 * (i - 3) + (j - 3)];
-      else if (i >= 3 && j < 3) {
-        const int r = i - 3;
-        const double tx = sm.T[9], ty = sm.T[10], tz = sm.T[11];
-        const double sk[3][3] = {{0.0, -tz, ty}, {tz, 0.0, -tx}, {-ty, tx, 0.0}};
-        ad = dot3_rn(sk[r][0], sk[r][1], sk[r][2], sm.T[j], sm.T[3 + j], sm.T[6 + j]);
-      }
-      Ad[t] = ad;
-    }
-    __syncwarp();
-    for (int t = lane; t < 36; t += 32) {
-      const int i = t / 6, j = t % 6;
-      double sum = 0.0;
-#pragma unroll
-      for (int m = 0; m < 6; ++m) sum += H[6 * i + m] * Ad[6 * m + j];
-      HA[t] = sum;  // H_tt · Ad
-    }
-    __syncwarp();
-    for (int t = lane; t < 36; t += 32) {
-      const int i = t / 6, j = t % 6;
-      double sum = 0.0;
-#pragma unroll
-      for (int m = 0; m < 6; ++m) sum += Ad[6 * m + i] * HA[6 * m + j];
-      Hss[t] = sum;  // Adᵀ · H_tt · Ad
-    }
-    __syncwarp();
-    for (int t = lane; t < 36; t += 32) {
-      const int i = t / 6, j = t % 6;
-      o[t] = H[t];                                       // H_ii (exactly symmetric)
-      o[36 + t] = -HA[t];                                // H_ij
-      o[72 + t] = 0.5 * (Hss[6 * i + j] + Hss[6 * j + i]);  // H_jj, symmetrised (factors.cpp:141)
-    }
-    if (lane < 6) {
-      o[108 + lane] = tot[21 + lane];  // b_i = b_t
-      double sum = 0.0;
-#pragma unroll
-      for (int m = 0; m < 6; ++m) sum += Ad[6 * m + lane] * tot[21 + m];
-      o[114 + lane] = -sum;  // b_j = -Adᵀ b_t
-    }
-    if (lane == 0) {
-      o[120] = tot[27];
-      out_inl[f] = tinl;
-    }
-  }
+  finish_factor<kLinearize>(acc, inl, lane, (size_t)blockIdx.x * kWarps + warp, kWarps, w, fp, sm.T,
+                            reinterpret_cast<double*>(&sm.u.ring[warp][0]), partials, part_inl, counters, out, out_inl);
 }
 
 // gicp_error (factors.cpp:75-88) in fp64, bit-identical to the oracle.
@@ -506,12 +518,6 @@ cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkIt
     cudaError_t e = cudaFuncSetAttribute(factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(factor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-#ifdef VG_CARVEOUT
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(factor_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, VG_CARVEOUT);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(factor_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, VG_CARVEOUT);
-#endif
     if (e != cudaSuccess) return e;
     configured = true;
   }

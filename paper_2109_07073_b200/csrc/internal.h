@@ -31,10 +31,18 @@ struct WorkItem {
   int pad;
 };
 
+// Source clouds are also stored Morton-ordered in blocks of 64 points (one TMA bulk copy per
+// 64-point tile of the factor kernel): SoA inside the block.
+constexpr int kPointBlock = 64;
+struct PointBlock {
+  float4 pa[kPointBlock];  // x y z c_xx
+  float4 pb[kPointBlock];  // c_xy c_xz c_yy c_yz
+  float pc[kPointBlock];   // c_zz
+};
+static_assert(sizeof(PointBlock) % 128 == 0, "blocks must stay 128-B aligned");
+
 struct FactorDev {
-  const float4* pa;
-  const float4* pb;
-  const float* pc;
+  const PointBlock* blk;
   MapDev map;
   int n;
   int tgt;
@@ -45,7 +53,7 @@ struct FactorDev {
 };
 
 struct OverlapItem {
-  const float4* pa;
+  const PointBlock* blk;
   MapDev map;
   double T[12];
   unsigned n;
@@ -143,13 +151,12 @@ struct vgicp_cloud_s {
   vgicp_ctx ctx = nullptr;
   size_t n = 0;
   bool has_cov = false;
-  void* block = nullptr;  // single allocation: pa | pb | pc (input order) | sa | sb | sc (Morton order)
+  void* block = nullptr;  // single allocation: pa | pb | pc (input order) | Morton-ordered PointBlocks
   float4* pa = nullptr;   // input order: voxel-map builds accumulate in this order (voxelmap.cpp:87-94)
   float4* pb = nullptr;
   float* pc = nullptr;
-  float4* spa = nullptr;  // Morton (Z-order) copy: streamed by the factor / overlap kernels so that
-  float4* spb = nullptr;  // consecutive points probe neighbouring voxels (bucket1 locality, L1 hits)
-  float* spc = nullptr;
+  vgicp::PointBlock* sblk = nullptr;  // Morton (Z-order) copy in 64-point blocks: streamed by the factor /
+                               // overlap kernels so that consecutive points probe neighbouring voxels
   std::atomic<int> refs{1};
 };
 

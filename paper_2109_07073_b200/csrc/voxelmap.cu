@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(256) overlap_kernel(const OverlapItem* __restr
 #pragma unroll
     for (int q = 0; q < 12; ++q) T[q] = it.T[q];
     const MapDev map = it.map;
-    const float4* __restrict__ pa = it.pa;
+    const PointBlock* __restrict__ blk = it.blk;
     unsigned count = 0;
     for (unsigned base = first; base < n; base += kOverlapILP * stride) {
       unsigned hi[kOverlapILP], lo[kOverlapILP], b1[kOverlapILP], b2[kOverlapILP];
@@ -235,7 +235,8 @@ __global__ void __launch_bounds__(256) overlap_kernel(const OverlapItem* __restr
 #pragma unroll
       for (int u = 0; u < kOverlapILP; ++u) {
         const unsigned i = base + u * stride;
-        const float4 a = __ldg(pa + min(i, n - 1));
+        const unsigned ic = min(i, n - 1);
+        const float4 a = __ldg(&blk[ic / kPointBlock].pa[ic % kPointBlock]);
         double q0, q1, q2, l0, l1, l2;
         apply_pose_rn(T, a.x, a.y, a.z, q0, q1, q2);
         unsigned k0 = 0, k1 = 0, k2 = 0;
