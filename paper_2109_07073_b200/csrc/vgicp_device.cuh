@@ -177,11 +177,29 @@ struct BucketPair {
   uint4 a;
   uint4 b;
 };
+#ifndef VG_B2_HINT
+#define VG_B2_HINT 2
+#endif
+// bucket2 is a random probe: optionally keep it out of L1 so that the spatially coherent bucket1
+// lines and slot statistics stay resident there.
+__device__ __forceinline__ uint4 ldg_bucket2(const void* p) {
+#if VG_B2_HINT == 1
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+#elif VG_B2_HINT == 2
+  return __ldcg(reinterpret_cast<const uint4*>(p));
+#else
+  return __ldg(reinterpret_cast<const uint4*>(p));
+#endif
+}
 __device__ __forceinline__ BucketPair load_buckets(const unsigned long long* __restrict__ keys, unsigned b1,
                                                    unsigned b2) {
   BucketPair r;
   r.a = __ldg(reinterpret_cast<const uint4*>(keys + kBucket * b1));
-  r.b = __ldg(reinterpret_cast<const uint4*>(keys + kBucket * b2));
+  r.b = ldg_bucket2(keys + kBucket * b2);
   return r;
 }
 
