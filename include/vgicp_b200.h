@@ -110,6 +110,26 @@ int vgicp_voxelmap_export(vgicp_map map, uint64_t* keys, int32_t* counts, double
 int vgicp_voxelmap_lookup(vgicp_map map, const double* points, size_t n, uint64_t* keys_out);
 /* voxel_coord + pack_key (voxelmap.cpp:45-63) on the host; OUT_OF_RANGE beyond ±2^20. */
 int vgicp_voxel_key(double resolution, const double point[3], uint64_t* key);
+/* GaussianVoxelMap over a float64 cloud (the reference's PointCloud layout: n×3 means, n×9
+ * covariances, all 9 entries accumulated) — voxelmap.cpp:65-104. With vgicp_voxelmap_export this
+ * is voxel_downsample (voxelmap.cpp:137-169): one point per voxel, ascending packed-key order. */
+int vgicp_voxelmap_build_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, double resolution,
+                             vgicp_map* out);
+
+/* ---------------------------------------------------------------- submap creation (§8f #2) */
+/* transform_cloud (point_cloud.cpp:26-42) in float64 on the device: out = T.apply(mean),
+ * out_cov = R·C·Rᵀ (full 9 entries). cov9 / out_cov9 may be NULL (means only). */
+int vgicp_transform_cloud(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, const double pose[12],
+                          double* out_xyz, double* out_cov9);
+/* The submap creation path of MappingPipeline::emit_submap (pipeline.cpp:92-114), on the device:
+ * every frame k transformed by poses12[k] (frame -> submap) in float64 and merged in frame order,
+ * voxel_downsample'd at downsample_resolution (skipped when <= 0), and the submap's voxel map built
+ * at map_resolution from the float64 downsampled cloud. Optional outputs: out_downsampled (the
+ * downsample map: export() = the submap cloud in float64, ascending key order) and out_cloud (that
+ * cloud as a float32 device cloud, the source of submap-level factors). */
+int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* poses12, int m,
+                       double downsample_resolution, double map_resolution, vgicp_map* out_downsampled,
+                       vgicp_cloud* out_cloud, vgicp_map* out_map);
 
 /* ---------------------------------------------------------------- overlap (Eq. 7/8) */
 /* overlap_rate(cloud, pose_rel, map) — voxelmap.cpp:119-135. Exact hits / N. */

@@ -1183,4 +1183,20 @@ int or_estimate_covariances(const double* means, size_t n, int k, double plane_e
   });
 }
 
+// transform_cloud (point_cloud.cpp:26-42): means -> T.apply(mean), covariances -> R·C·Rᵀ with
+// Eigen's evaluation order ((R·C) first, then ·Rᵀ). covs / out_covs may be NULL.
+void or_transform_cloud(const double* means, const double* covs, size_t n, const double pose[12], double* out_means,
+                        double* out_covs) {
+  const Pose T = pose_from(pose);
+  for (size_t i = 0; i < n; ++i) {
+    const V3 q = T.apply(v3_at(means, i));
+    for (int a = 0; a < 3; ++a) out_means[3 * i + a] = q[a];
+    if (covs && out_covs) {
+      const M3 C = rotate_cov(T.R, m3_at(covs, i));
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) out_covs[9 * i + 3 * r + c] = C.m[r][c];
+    }
+  }
+}
+
 }  // extern "C"

@@ -94,6 +94,9 @@ void or_make_scene(or_rng* rng, int points, double resolution, double boundary_m
                    double* target_covs);
 /* reference::estimate_covariances (reference.cpp:11-37): brute-force kNN, eigen-regularised. */
 int or_estimate_covariances(const double* means, size_t n, int k, double plane_epsilon, double* covs);
+/* transform_cloud (point_cloud.cpp:26-42); covs / out_covs may be NULL. */
+void or_transform_cloud(const double* means, const double* covs, size_t n, const double pose[12], double* out_means,
+                        double* out_covs);
 /* std::shuffle(perm, rng.engine) as in test_voxelmap.cpp:104 */
 void or_rng_shuffle(or_rng* rng, uint64_t* perm, size_t n);
 

@@ -14,7 +14,9 @@ from .vgicp import (
     LinearizedFactor,
     MatchingCostFactor,
     PointCloud,
+    Submap,
     as_pose12,
+    build_submap,
     cov6_from,
     default_context,
     estimate_covariances,
@@ -25,6 +27,8 @@ from .vgicp import (
     overlap_hits,
     overlap_rate,
     overlap_rates,
+    transform_cloud,
+    voxel_downsample,
 )
 
 __all__ = [
@@ -39,7 +43,9 @@ __all__ = [
     "LinearizedFactor",
     "MatchingCostFactor",
     "PointCloud",
+    "Submap",
     "as_pose12",
+    "build_submap",
     "cov6_from",
     "default_context",
     "estimate_covariances",
@@ -50,4 +56,6 @@ __all__ = [
     "overlap_hits",
     "overlap_rate",
     "overlap_rates",
+    "transform_cloud",
+    "voxel_downsample",
 ]

@@ -341,6 +341,8 @@ int vgicp_cloud_destroy(vgicp_cloud cloud) {
 }
 
 // ------------------------------------------------------------------------------------ voxel maps
+static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map* out);
+
 int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* resolutions, int m,
                                vgicp_map* out) {
   if (!ctx || !out || (m > 0 && (!clouds || !resolutions))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
@@ -355,14 +357,23 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
   }
   DeviceGuard g(ctx->device);
   std::vector<BuildSeg> segs(m);
+  for (int k = 0; k < m; ++k) {
+    const vgicp_cloud c = clouds[k];
+    segs[k] = BuildSeg{c->pa, c->pb, c->pc, nullptr, nullptr, 0ull, static_cast<unsigned>(c->n), 0u, resolutions[k],
+                       1.0 / resolutions[k]};
+  }
+  return build_segments(ctx, segs, out);
+}
+
+// Batched build core: segments are float32 device clouds or fp64 device arrays (BuildSeg).
+static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map* out) {
+  const int m = static_cast<int>(segs.size());
   unsigned long long total = 0;
   unsigned max_n = 0;
   for (int k = 0; k < m; ++k) {
-    const vgicp_cloud c = clouds[k];
-    segs[k] = BuildSeg{c->pa, c->pb, c->pc, total, static_cast<unsigned>(c->n), 0u, resolutions[k],
-                       1.0 / resolutions[k]};
-    total += c->n;
-    max_n = std::max<unsigned>(max_n, static_cast<unsigned>(c->n));
+    segs[k].offset = total;
+    total += segs[k].n;
+    max_n = std::max<unsigned>(max_n, segs[k].n);
   }
   if (total >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "batched build exceeds 2^31 points");
   const int ntot = static_cast<int>(total);
@@ -454,10 +465,10 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
     }
     maps[k] = mp;
     mp->ctx = ctx;
-    mp->res = resolutions[k];
-    mp->inv_res = 1.0 / resolutions[k];
+    mp->res = segs[k].res;
+    mp->inv_res = segs[k].inv_res;
     mp->voxels = hv[k];
-    mp->total_points = clouds[k]->n;
+    mp->total_points = segs[k].n;
     max_v = std::max(max_v, hv[k]);
     const size_t V = hv[k];
     const size_t b_keys = align_up(sizeof(unsigned long long) * V, 256);
@@ -551,6 +562,155 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
 int vgicp_voxelmap_build(vgicp_ctx ctx, vgicp_cloud cloud, double resolution, vgicp_map* out) {
   if (!out) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
   return vgicp_voxelmap_build_batch(ctx, &cloud, &resolution, 1, out);
+}
+
+// RAII device buffer for temporaries of the fp64 / submap paths.
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+}  // namespace
+
+int vgicp_voxelmap_build_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, double resolution,
+                             vgicp_map* out) {
+  if (!ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  // GaussianVoxelMap ctor validation order (voxelmap.cpp:67-72)
+  if (!(resolution > 0.0)) return fail(VGICP_E_INVALID_ARGUMENT, "voxel resolution must be positive");
+  if (!cov9 || n == 0) return fail(VGICP_E_INVALID_ARGUMENT, "voxel map construction requires per-point covariances");
+  if (!xyz) return fail(VGICP_E_INVALID_ARGUMENT, "null point array");
+  if (n >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "cloud too large (>= 2^31 points)");
+  DeviceGuard g(ctx->device);
+  DevBuf buf;
+  VG_CUDA(cudaMalloc(&buf.p, n * 12 * sizeof(double)));
+  double* d_xyz = static_cast<double*>(buf.p);
+  double* d_cov = d_xyz + 3 * n;
+  VG_CUDA(cudaMemcpyAsync(d_xyz, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  VG_CUDA(cudaMemcpyAsync(d_cov, cov9, n * 9 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  std::vector<BuildSeg> segs{BuildSeg{nullptr, nullptr, nullptr, d_xyz, d_cov, 0ull, static_cast<unsigned>(n), 0u,
+                                      resolution, 1.0 / resolution}};
+  const int rc = build_segments(ctx, segs, out);
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return rc;
+}
+
+int vgicp_transform_cloud(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, const double pose[12],
+                          double* out_xyz, double* out_cov9) {
+  if (!ctx || !pose || (n > 0 && (!xyz || !out_xyz))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (n == 0) return VGICP_OK;
+  const bool cov = cov9 && out_cov9;
+  DeviceGuard g(ctx->device);
+  DevBuf buf;
+  const size_t per = cov ? 24 : 6;  // doubles per point: in + out
+  VG_CUDA(cudaMalloc(&buf.p, (n * per + 12) * sizeof(double)));
+  double* d_in = static_cast<double*>(buf.p);
+  double* d_cin = d_in + 3 * n;
+  double* d_out = cov ? d_cin + 9 * n : d_in + 3 * n;
+  double* d_cout = cov ? d_out + 3 * n : nullptr;
+  double* d_T = d_out + (cov ? 12 * n : 3 * n);
+  cudaStream_t s = ctx->stream;
+  VG_CUDA(cudaMemcpyAsync(d_in, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (cov) VG_CUDA(cudaMemcpyAsync(d_cin, cov9, n * 9 * sizeof(double), cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemcpyAsync(d_T, pose, 12 * sizeof(double), cudaMemcpyHostToDevice, s));
+  VG_CUDA(launch_transform64(d_in, cov ? d_cin : nullptr, n, d_T, d_out, d_cout, s));
+  ctx->launches += 1;
+  VG_CUDA(cudaMemcpyAsync(out_xyz, d_out, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (cov) VG_CUDA(cudaMemcpyAsync(out_cov9, d_cout, n * 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  return VGICP_OK;
+}
+
+int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* poses12, int m,
+                       double downsample_resolution, double map_resolution, vgicp_map* out_downsampled,
+                       vgicp_cloud* out_cloud, vgicp_map* out_map) {
+  if (!ctx || !out_map || (m > 0 && (!frames || !poses12))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *out_map = nullptr;
+  if (out_downsampled) *out_downsampled = nullptr;
+  if (out_cloud) *out_cloud = nullptr;
+  if (m <= 0) return fail(VGICP_E_INVALID_ARGUMENT, "submap requires at least one frame");
+  if (!(map_resolution > 0.0)) return fail(VGICP_E_INVALID_ARGUMENT, "voxel resolution must be positive");
+  size_t total = 0;
+  unsigned max_n = 0;
+  for (int k = 0; k < m; ++k) {
+    if (!frames[k] || frames[k]->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "cloud of another context");
+    if (!frames[k]->has_cov)
+      return fail(VGICP_E_INVALID_ARGUMENT, "voxel map construction requires per-point covariances");
+    total += frames[k]->n;
+    max_n = std::max<unsigned>(max_n, static_cast<unsigned>(frames[k]->n));
+  }
+  if (total == 0) return fail(VGICP_E_INVALID_ARGUMENT, "voxel map construction requires per-point covariances");
+  if (total >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "submap too large (>= 2^31 points)");
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->stream;
+  // 1. transform_cloud of every frame into the submap frame, merged in frame order (pipeline.cpp:97-107)
+  DevBuf merged, items;
+  VG_CUDA(cudaMalloc(&merged.p, total * 12 * sizeof(double)));
+  VG_CUDA(cudaMalloc(&items.p, m * sizeof(TransformItem)));
+  double* d_xyz = static_cast<double*>(merged.p);
+  double* d_cov = d_xyz + 3 * total;
+  std::vector<TransformItem> hi(m);
+  size_t off = 0;
+  for (int k = 0; k < m; ++k) {
+    TransformItem& it = hi[k];
+    it.pa = frames[k]->pa;
+    it.pb = frames[k]->pb;
+    it.pc = frames[k]->pc;
+    it.offset = off;
+    it.n = static_cast<unsigned>(frames[k]->n);
+    it.pad = 0;
+    std::memcpy(it.T, poses12 + 12 * k, sizeof(it.T));
+    off += frames[k]->n;
+  }
+  VG_CUDA(cudaMemcpyAsync(items.p, hi.data(), m * sizeof(TransformItem), cudaMemcpyHostToDevice, s));
+  VG_CUDA(launch_transform(static_cast<const TransformItem*>(items.p), m, max_n, d_xyz, d_cov, s));
+  ctx->launches += 1;
+  // 2. voxel_downsample (voxelmap.cpp:137-169): the voxel means / covariances in ascending key
+  //    order are exactly the cold arrays of the map built at the downsample resolution
+  const double* src_xyz = d_xyz;
+  const double* src_cov = d_cov;
+  size_t src_n = total;
+  vgicp_map ds = nullptr;
+  if (downsample_resolution > 0.0) {
+    std::vector<BuildSeg> segs{BuildSeg{nullptr, nullptr, nullptr, d_xyz, d_cov, 0ull, static_cast<unsigned>(total),
+                                        0u, downsample_resolution, 1.0 / downsample_resolution}};
+    if (int rc = build_segments(ctx, segs, &ds)) return rc;
+    src_xyz = ds->mean64;
+    src_cov = ds->cov64;
+    src_n = ds->voxels;
+  }
+  // 3. the submap's voxel map at the global resolution (pipeline.cpp:114)
+  std::vector<BuildSeg> segs{BuildSeg{nullptr, nullptr, nullptr, src_xyz, src_cov, 0ull, static_cast<unsigned>(src_n),
+                                      0u, map_resolution, 1.0 / map_resolution}};
+  vgicp_map mp = nullptr;
+  if (int rc = build_segments(ctx, segs, &mp)) {
+    release(ds);
+    return rc;
+  }
+  // 4. the submap cloud as a float32 device cloud (source of submap-level factors)
+  if (out_cloud) {
+    std::vector<double> hx(3 * src_n), hc(9 * src_n);
+    cudaError_t e = cudaMemcpyAsync(hx.data(), src_xyz, hx.size() * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), src_cov, hc.size() * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      release(ds);
+      release(mp);
+      return cuda_fail(e, "submap cloud download");
+    }
+    if (int rc = vgicp_cloud_upload_f64(ctx, hx.data(), hc.data(), src_n, out_cloud)) {
+      release(ds);
+      release(mp);
+      return rc;
+    }
+  }
+  VG_CUDA(cudaStreamSynchronize(s));
+  if (out_downsampled) *out_downsampled = ds;
+  else release(ds);
+  *out_map = mp;
+  return VGICP_OK;
 }
 
 int vgicp_voxelmap_destroy(vgicp_map map) {

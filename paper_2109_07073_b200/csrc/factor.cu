@@ -311,15 +311,6 @@ __device__ __forceinline__ void finish_factor(const float* acc, int inl, int lan
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(__cvta_generic_to_global(src))
-               : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(__cvta_generic_to_global(src))
-               : "memory");
-}
-
 // Shared memory of one CTA. Every warp owns a private kStages-deep ring of source tiles that it
 // fills itself with TMA bulk copies (cp.async.bulk, mbarrier completion), so warps never wait on
 // each other inside the point loop; after the loop the rings are reused for the reduction.
@@ -330,23 +321,6 @@ static_assert(kWarpTile == kPointBlock, "a warp tile is one point block");
 // tile; the math phase consumes them only in full batches of 32 (every lane busy), carrying the
 // remainder over to the next tile. Entries are self-contained (the ring slot of their tile may be
 // refilled before they are consumed). SoA float4 columns: conflict-free 128-bit stores / loads.
-#ifndef VG_PIPE
-#define VG_PIPE 0
-#endif
-#if VG_PIPE
-// Pipelined variant: entries also carry the voxel's slot statistics, copied in with cp.async when
-// the hit is appended; a tile's hits are consumed one tile later (after cp.async.wait_all), while
-// the next tile's bucket loads are in flight.
-constexpr int kQueue = 96;  // < 32 carried + kWarpTile appended
-struct HitQueue {
-  float4 a[kQueue];   // l.x l.y l.z q.x
-  float4 b[kQueue];   // q.y q.z c_xx c_zz
-  float4 c[kQueue];   // c_xy c_xz c_yy c_yz
-  float4 s0[kQueue];  // slot stats A[0:4]  (cp.async)
-  float4 s1[kQueue];  // slot stats A[4:8]  (cp.async)
-  float2 s2[kQueue];  // slot stats B        (cp.async)
-};
-#else
 #ifndef VG_QUEUE
 #define VG_QUEUE 128
 #endif
@@ -358,7 +332,6 @@ struct HitQueue {
   float4 c[kQueue];  // c_xy c_xz c_yy c_yz
   float d[kQueue];   // c_zz
 };
-#endif
 struct __align__(128) FactorSmem {
   union {
     WarpTile ring[kWarps][kStages];
@@ -421,90 +394,6 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
   int inl = 0;
   unsigned head = 0, tail = 0;  // hit queue cursors (warp-uniform)
 
-#if VG_PIPE
-  auto qslot = [](unsigned x) { return x % static_cast<unsigned>(kQueue); };
-  auto consume = [&](unsigned idx) {
-    const float4 qa = hq.a[idx];
-    const float4 qb = hq.b[idx];
-    const float4 qc = hq.c[idx];
-    const float4 v0 = hq.s0[idx];
-    const float4 v1 = hq.s1[idx];
-    const float2 v2 = hq.s2[idx];
-    hit_math<kLinearize>(sm.Rf, T, map, qa, qb.x, qb.y, qb.z, qc, qb.w, v0, v1, v2, acc, inl);
-  };
-  for (int k = 0; k < my_tiles; ++k) {
-    const int stage = k % kStages;
-    while (!mbar_try_wait(&bars[stage], (k / kStages) & 1)) {
-    }
-    WarpTile& tb = sm.u.ring[warp][stage];
-    const int tile_n = min(kWarpTile, w.end - (w.begin + (warp + k * kWarps) * kWarpTile));
-    // ---- probe tile k; l is parked in the ring over the (no longer needed) source xyz ----
-    double Tr[12];
-#pragma unroll
-    for (int q = 0; q < 12; ++q) Tr[q] = T[q];
-    unsigned hi[kILP], lo[kILP], b1[kILP], b2[kILP];
-    float q0[kILP], q1[kILP], q2[kILP];
-    bool ok[kILP];
-#pragma unroll
-    for (int u = 0; u < kILP; ++u) {
-      const int p = u * 32 + lane;
-      const int lp = min(p, tile_n - 1);
-      const float4 A = tb.pa[lp];
-      double qd0, qd1, qd2;
-      apply_pose_rn(Tr, A.x, A.y, A.z, qd0, qd1, qd2);
-      unsigned k0 = 0, k1 = 0, k2 = 0;
-      double ld0, ld1, ld2;
-      ok[u] = voxel_key(qd0, qd1, qd2, map.res, map.inv_res, k0, k1, k2, ld0, ld1, ld2) && (p < tile_n);
-      pack_key32(k0, k1, k2, hi[u], lo[u]);
-      b1[u] = bucket1(k0, k1, k2, map.shift);
-      b2[u] = bucket2(k0, k1, k2, map.shift);
-      q0[u] = (float)qd0, q1[u] = (float)qd1, q2[u] = (float)qd2;
-      __syncwarp();  // every lane has read its A before any lane overwrites one (clamped reads)
-      if (p < tile_n) tb.pa[p] = make_float4((float)ld0, (float)ld1, (float)ld2, A.w);
-    }
-    BucketPair bp[kILP];
-#pragma unroll
-    for (int u = 0; u < kILP; ++u) bp[u] = load_buckets(map.keys, b1[u], b2[u]);
-    // ---- consume the hits of earlier tiles (their statistics copies were issued a tile ago) ----
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
-    while (tail - head >= 32u) {
-      consume(qslot(head + lane));
-      head += 32u;
-    }
-    __syncwarp();  // consumed entries are free before any lane appends over them
-    // ---- match tile k, append its hits and start their statistics copies ----
-#pragma unroll
-    for (int u = 0; u < kILP; ++u) {
-      const int s = match_buckets(bp[u], b1[u], b2[u], hi[u], lo[u]);
-      const bool hit = ok[u] && s >= 0;
-      const unsigned ball = __ballot_sync(0xffffffffu, hit);
-      if (hit) {
-        const int p = u * 32 + lane;
-        const unsigned idx = qslot(tail + __popc(ball & lane_lt));
-        const SlotStatsA* sa = map.sa + s;
-        cp_async16(&hq.s0[idx], sa);
-        cp_async16(&hq.s1[idx], reinterpret_cast<const float4*>(sa) + 1);
-        cp_async8(&hq.s2[idx], map.sb + s);
-        const float4 L = tb.pa[p];
-        hq.a[idx] = make_float4(L.x, L.y, L.z, q0[u]);
-        hq.b[idx] = make_float4(q1[u], q2[u], L.w, tb.pc[p]);
-        hq.c[idx] = tb.pb[p];
-      }
-      tail += __popc(ball);
-    }
-    __syncwarp();  // the warp is done with this ring slot
-    if (lane == 0 && k + kStages < my_tiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_tile(k + kStages);
-    }
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
-  for (; tail - head >= 32u; head += 32u) consume(qslot(head + lane));
-  if (head + lane < tail) consume(qslot(head + lane));  // the last partial batch
-  __syncwarp();
-#else
   // ---- math phase for one queued hit ----
   auto consume = [&](unsigned idx) {
     const float4 qa = hq.a[idx];
@@ -586,7 +475,6 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
   if (head + lane < tail) consume((head + lane) % static_cast<unsigned>(kQueue));  // the last partial batch
   __syncwarp();  // this warp is done with its ring (no CTA-wide barrier after the prologue)
 
-#endif
   finish_factor<kLinearize>(acc, inl, lane, (size_t)blockIdx.x * kWarps + warp, kWarps, w, fp, sm.T,
                             reinterpret_cast<double*>(&sm.u.ring[warp][0]), partials, part_inl, counters, out, out_inl);
 }

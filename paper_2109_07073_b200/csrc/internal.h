@@ -61,9 +61,11 @@ struct OverlapItem {
 };
 
 struct BuildSeg {
-  const float4* pa;
+  const float4* pa;           // float32 device cloud (input order) ...
   const float4* pb;
   const float* pc;
+  const double* xyz64;        // ... or fp64 points (n×3) + full fp64 covariances (n×9) when non-null
+  const double* cov9;         //     (transformed / downsampled submap clouds, point_cloud.cpp:26-42)
   unsigned long long offset;  // start of this map's points in the concatenated arrays
   unsigned n;
   unsigned pad;
@@ -126,6 +128,22 @@ cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkIt
                           const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
                           int* out_inl, cudaStream_t s);
 cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s);
+// transform_cloud (point_cloud.cpp:26-42) of float32 device clouds into fp64 arrays, batched:
+// item k maps cloud k's points (input order) through poses12[k] into out_xyz / out_cov9 at `offset`.
+struct TransformItem {
+  const float4* pa;
+  const float4* pb;
+  const float* pc;
+  unsigned long long offset;
+  unsigned n;
+  unsigned pad;
+  double T[12];
+};
+cudaError_t launch_transform(const TransformItem* items, int m, unsigned max_n, double* out_xyz, double* out_cov9,
+                             cudaStream_t s);
+// the same for fp64 host-provided input arrays (already on device)
+cudaError_t launch_transform64(const double* xyz, const double* cov9, size_t n, const double* T, double* out_xyz,
+                               double* out_cov9, cudaStream_t s);
 cudaError_t launch_cov_count(const CovSeg* segs, int m, unsigned max_n, const float* xyz, unsigned* cell_of,
                              unsigned* cnt, cudaStream_t s);
 cudaError_t launch_cov_scatter(const CovSeg* segs, int m, unsigned max_n, const unsigned* cell_of,

@@ -12,6 +12,8 @@
 //                       table and write the fp32 voxel-local hot record + fp64 cold statistics.
 // Sorting instead of float atomics makes the statistics deterministic and bit-identical to the
 // reference's Kahan merge; the hash table itself is built with 64-bit atomicCAS.
+#include <algorithm>
+
 #include "internal.h"
 
 namespace vgicp {
@@ -20,11 +22,17 @@ __global__ void build_keys_kernel(const BuildSeg* __restrict__ segs, unsigned lo
                                   unsigned* __restrict__ vals, int* __restrict__ range_err) {
   const BuildSeg s = segs[blockIdx.y];
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += gridDim.x * blockDim.x) {
-    const float4 a = __ldg(s.pa + i);
+    double x, y, z;
+    if (s.xyz64) {
+      x = s.xyz64[3 * (size_t)i], y = s.xyz64[3 * (size_t)i + 1], z = s.xyz64[3 * (size_t)i + 2];
+    } else {
+      const float4 a = __ldg(s.pa + i);
+      x = a.x, y = a.y, z = a.z;
+    }
     unsigned k0, k1, k2, hi, lo;
     double l0, l1, l2;
     unsigned long long key = 0;
-    if (voxel_key(a.x, a.y, a.z, s.res, s.inv_res, k0, k1, k2, l0, l1, l2)) {
+    if (voxel_key(x, y, z, s.res, s.inv_res, k0, k1, k2, l0, l1, l2)) {
       pack_key32(k0, k1, k2, hi, lo);
       key = key64(hi, lo);
     } else {
@@ -80,35 +88,63 @@ __global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const
     const unsigned v = vidx[g] - o.vbase;
     // VoxelAccumulator::add (voxelmap.cpp:28-32) with KahanSum, component-wise.
     double ms[3] = {0, 0, 0}, mc[3] = {0, 0, 0};
-    double ss[6] = {0, 0, 0, 0, 0, 0}, sc[6] = {0, 0, 0, 0, 0, 0};  // xx xy xz yy yz zz
+    double cov[9];  // finalized covariance, row-major
     int count = 0;
-    for (unsigned j = i; j < s.n && (j == i || !heads[s.offset + j]); ++j) {
-      const unsigned p = vals[s.offset + j];
-      const float4 a = __ldg(s.pa + p);
-      const float4 b = __ldg(s.pb + p);
-      const float czz = __ldg(s.pc + p);
-      const double m0 = a.x, m1 = a.y, m2 = a.z;
-      kahan_add(ms[0], mc[0], m0);
-      kahan_add(ms[1], mc[1], m1);
-      kahan_add(ms[2], mc[2], m2);
-      kahan_add(ss[0], sc[0], __dadd_rn((double)a.w, __dmul_rn(m0, m0)));
-      kahan_add(ss[1], sc[1], __dadd_rn((double)b.x, __dmul_rn(m0, m1)));
-      kahan_add(ss[2], sc[2], __dadd_rn((double)b.y, __dmul_rn(m0, m2)));
-      kahan_add(ss[3], sc[3], __dadd_rn((double)b.z, __dmul_rn(m1, m1)));
-      kahan_add(ss[4], sc[4], __dadd_rn((double)b.w, __dmul_rn(m1, m2)));
-      kahan_add(ss[5], sc[5], __dadd_rn((double)czz, __dmul_rn(m2, m2)));
-      ++count;
+    if (!s.xyz64) {
+      // float32 cloud: symmetric inputs, so the 6 unique second-moment sums equal the 9 of the
+      // reference bit for bit ((0,1) and (1,0) receive identical addends)
+      double ss[6] = {0, 0, 0, 0, 0, 0}, sc[6] = {0, 0, 0, 0, 0, 0};  // xx xy xz yy yz zz
+      for (unsigned j = i; j < s.n && (j == i || !heads[s.offset + j]); ++j) {
+        const unsigned p = vals[s.offset + j];
+        const float4 a = __ldg(s.pa + p);
+        const float4 b = __ldg(s.pb + p);
+        const float czz = __ldg(s.pc + p);
+        const double m0 = a.x, m1 = a.y, m2 = a.z;
+        kahan_add(ms[0], mc[0], m0);
+        kahan_add(ms[1], mc[1], m1);
+        kahan_add(ms[2], mc[2], m2);
+        kahan_add(ss[0], sc[0], __dadd_rn((double)a.w, __dmul_rn(m0, m0)));
+        kahan_add(ss[1], sc[1], __dadd_rn((double)b.x, __dmul_rn(m0, m1)));
+        kahan_add(ss[2], sc[2], __dadd_rn((double)b.y, __dmul_rn(m0, m2)));
+        kahan_add(ss[3], sc[3], __dadd_rn((double)b.z, __dmul_rn(m1, m1)));
+        kahan_add(ss[4], sc[4], __dadd_rn((double)b.w, __dmul_rn(m1, m2)));
+        kahan_add(ss[5], sc[5], __dadd_rn((double)czz, __dmul_rn(m2, m2)));
+        ++count;
+      }
+      const double cnt = static_cast<double>(count);
+      const double mean[3] = {__ddiv_rn(ms[0], cnt), __ddiv_rn(ms[1], cnt), __ddiv_rn(ms[2], cnt)};
+      const int r6[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+      for (int e = 0; e < 6; ++e) {
+        const int r = r6[e][0], c = r6[e][1];
+        cov[3 * r + c] = cov[3 * c + r] = __dsub_rn(__ddiv_rn(ss[e], cnt), __dmul_rn(mean[r], mean[c]));
+      }
+      ms[0] = mean[0], ms[1] = mean[1], ms[2] = mean[2];
+    } else {
+      // fp64 cloud with full (possibly 1-ulp asymmetric) covariances: all 9 sums, as the reference
+      double ss[9], sc[9];
+      for (int e = 0; e < 9; ++e) ss[e] = sc[e] = 0.0;
+      for (unsigned j = i; j < s.n && (j == i || !heads[s.offset + j]); ++j) {
+        const size_t p = vals[s.offset + j];
+        const double m[3] = {s.xyz64[3 * p], s.xyz64[3 * p + 1], s.xyz64[3 * p + 2]};
+        const double* C = s.cov9 + 9 * p;
+        kahan_add(ms[0], mc[0], m[0]);
+        kahan_add(ms[1], mc[1], m[1]);
+        kahan_add(ms[2], mc[2], m[2]);
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) kahan_add(ss[3 * r + c], sc[3 * r + c], __dadd_rn(C[3 * r + c], __dmul_rn(m[r], m[c])));
+        ++count;
+      }
+      const double cnt = static_cast<double>(count);
+      const double mean[3] = {__ddiv_rn(ms[0], cnt), __ddiv_rn(ms[1], cnt), __ddiv_rn(ms[2], cnt)};
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cov[3 * r + c] = __dsub_rn(__ddiv_rn(ss[3 * r + c], cnt), __dmul_rn(mean[r], mean[c]));
+      ms[0] = mean[0], ms[1] = mean[1], ms[2] = mean[2];
     }
-    // finalize (voxelmap.cpp:34-40)
-    const double cnt = static_cast<double>(count);
-    const double mean[3] = {__ddiv_rn(ms[0], cnt), __ddiv_rn(ms[1], cnt), __ddiv_rn(ms[2], cnt)};
-    double cov[6];
-    cov[0] = __dsub_rn(__ddiv_rn(ss[0], cnt), __dmul_rn(mean[0], mean[0]));
-    cov[1] = __dsub_rn(__ddiv_rn(ss[1], cnt), __dmul_rn(mean[0], mean[1]));
-    cov[2] = __dsub_rn(__ddiv_rn(ss[2], cnt), __dmul_rn(mean[0], mean[2]));
-    cov[3] = __dsub_rn(__ddiv_rn(ss[3], cnt), __dmul_rn(mean[1], mean[1]));
-    cov[4] = __dsub_rn(__ddiv_rn(ss[4], cnt), __dmul_rn(mean[1], mean[2]));
-    cov[5] = __dsub_rn(__ddiv_rn(ss[5], cnt), __dmul_rn(mean[2], mean[2]));
+    const double mean[3] = {ms[0], ms[1], ms[2]};
     // cold fp64 statistics (ascending key order)
     o.keys[v] = key;
     o.counts[v] = count;
@@ -116,9 +152,8 @@ __global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const
     o.mean64[3 * v + 1] = mean[1];
     o.mean64[3 * v + 2] = mean[2];
     double* c9 = o.cov64 + 9 * v;
-    c9[0] = cov[0], c9[1] = cov[1], c9[2] = cov[2];
-    c9[3] = cov[1], c9[4] = cov[3], c9[5] = cov[4];
-    c9[6] = cov[2], c9[7] = cov[4], c9[8] = cov[5];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) c9[e] = cov[e];
     // hot record (compact by global voxel id): statistics relative to the voxel's lower corner
     const double corner0 = __dmul_rn(key_coord(key, 0), s.res);
     const double corner1 = __dmul_rn(key_coord(key, 1), s.res);
@@ -130,9 +165,9 @@ __global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const
     r.cxx = static_cast<float>(cov[0]);
     r.cxy = static_cast<float>(cov[1]);
     r.cxz = static_cast<float>(cov[2]);
-    r.cyy = static_cast<float>(cov[3]);
-    r.cyz = static_cast<float>(cov[4]);
-    r.czz = static_cast<float>(cov[5]);
+    r.cyy = static_cast<float>(cov[4]);
+    r.cyz = static_cast<float>(cov[5]);
+    r.czz = static_cast<float>(cov[8]);
     r.vid = static_cast<int>(v);
     r.pad0 = r.pad1 = 0;
     hot[vidx[g]] = r;
@@ -310,6 +345,75 @@ cudaError_t launch_lookup(MapDev map, const double* pts, size_t n, unsigned long
 cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsigned long long* hits, cudaStream_t s) {
   const unsigned gy = m < 65535 ? m : 65535;
   overlap_kernel<<<dim3(grid_for(max_n, 256 * kOverlapILP, 1024), gy), 256, 0, s>>>(items, m, hits);
+  return cudaGetLastError();
+}
+
+
+// transform_cloud (point_cloud.cpp:26-42): q = T.apply(mu) and C' = (R·C)·Rᵀ in fp64 with the
+// reference's per-entry op order ((a0·b0 + a1·b1) + a2·b2), all 9 entries (R·C·Rᵀ is not exactly
+// symmetric in floating point, and the reference keeps the full matrix).
+__device__ __forceinline__ void transform_point(const double* T, double x, double y, double z, const double C[9],
+                                                double* q, double* Co) {
+  apply_pose_rn(T, x, y, z, q[0], q[1], q[2]);
+  double RC[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) RC[3 * r + c] = dot3_rn(T[3 * r], T[3 * r + 1], T[3 * r + 2], C[c], C[3 + c], C[6 + c]);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      Co[3 * r + c] = dot3_rn(RC[3 * r], RC[3 * r + 1], RC[3 * r + 2], T[3 * c], T[3 * c + 1], T[3 * c + 2]);
+}
+
+__global__ void transform_kernel(const TransformItem* __restrict__ items, double* __restrict__ out_xyz,
+                                 double* __restrict__ out_cov9) {
+  const TransformItem& it = items[blockIdx.y];
+  double T[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) T[q] = it.T[q];
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
+    const float4 a = __ldg(it.pa + i);
+    const float4 b = __ldg(it.pb + i);
+    const double czz = __ldg(it.pc + i);
+    const double C[9] = {a.w, b.x, b.y, b.x, b.z, b.w, b.y, b.w, czz};
+    const size_t o = it.offset + i;
+    transform_point(T, a.x, a.y, a.z, C, out_xyz + 3 * o, out_cov9 + 9 * o);
+  }
+}
+
+__global__ void transform64_kernel(const double* __restrict__ xyz, const double* __restrict__ cov9, size_t n,
+                                   const double* __restrict__ Tg, double* __restrict__ out_xyz,
+                                   double* __restrict__ out_cov9) {
+  double T[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) T[q] = Tg[q];
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    double C[9];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) C[e] = cov9 ? cov9[9 * i + e] : 0.0;
+    double q[3], Co[9];
+    transform_point(T, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], C, q, Co);
+    out_xyz[3 * i] = q[0], out_xyz[3 * i + 1] = q[1], out_xyz[3 * i + 2] = q[2];
+    if (out_cov9)
+#pragma unroll
+      for (int e = 0; e < 9; ++e) out_cov9[9 * i + e] = Co[e];
+  }
+}
+
+cudaError_t launch_transform(const TransformItem* items, int m, unsigned max_n, double* out_xyz, double* out_cov9,
+                             cudaStream_t s) {
+  if (m <= 0 || max_n == 0) return cudaSuccess;
+  transform_kernel<<<dim3(grid_for(max_n, 256, 1024), m), 256, 0, s>>>(items, out_xyz, out_cov9);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transform64(const double* xyz, const double* cov9, size_t n, const double* T, double* out_xyz,
+                               double* out_cov9, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  transform64_kernel<<<grid_for(static_cast<unsigned>(std::min<size_t>(n, 1u << 30)), 256, 4096), 256, 0, s>>>(
+      xyz, cov9, n, T, out_xyz, out_cov9);
   return cudaGetLastError();
 }
 

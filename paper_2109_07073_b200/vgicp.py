@@ -42,6 +42,10 @@ __all__ = [
     "cov6_from",
     "estimate_covariances",
     "estimate_covariances_batch",
+    "transform_cloud",
+    "voxel_downsample",
+    "build_submap",
+    "Submap",
 ]
 
 
@@ -173,7 +177,11 @@ class PointCloud(_Handle):
         self.cov6 = c
 
     def size(self) -> int:
-        return len(self.means)
+        if self.means is not None:
+            return len(self.means)
+        n = C.c_size_t()
+        check(_lib.load().vgicp_cloud_size(self._h, C.byref(n)))
+        return int(n.value)
 
     def __len__(self) -> int:
         return self.size()
@@ -182,7 +190,9 @@ class PointCloud(_Handle):
         return self.size() == 0
 
     def has_covariances(self) -> bool:
-        return self.cov6 is not None and self.size() > 0
+        h = C.c_int()
+        check(_lib.load().vgicp_cloud_has_covariances(self._h, C.byref(h)))
+        return bool(h.value) and self.size() > 0
 
 
 def estimate_covariances(points, k: int = 10, plane_epsilon: float = 1e-3, ctx: Context | None = None) -> np.ndarray:
@@ -205,21 +215,90 @@ def estimate_covariances_batch(clouds, k: int = 10, plane_epsilon: float = 1e-3,
     return outs
 
 
+# ------------------------------------------------------------------------------------ submap path
+def transform_cloud(means, covariances, pose, ctx: Context | None = None):
+    """transform_cloud (point_cloud.cpp:26-42) in float64 on the GPU: (T·means, R·C·Rᵀ)."""
+    ctx = ctx or default_context()
+    m = np.ascontiguousarray(np.asarray(means, np.float64).reshape(-1, 3))
+    c = None if covariances is None else np.ascontiguousarray(np.asarray(covariances, np.float64).reshape(-1, 9))
+    om = np.zeros_like(m)
+    oc = None if c is None else np.zeros_like(c)
+    T = as_pose12(pose)
+    check(_lib.load().vgicp_transform_cloud(ctx.handle, _ptr(m), _ptr(c) if c is not None else None, len(m), _ptr(T),
+                                            _ptr(om), _ptr(oc) if oc is not None else None))
+    return om, (None if oc is None else oc.reshape(-1, 3, 3))
+
+
+def voxel_downsample(means, covariances, resolution: float, ctx: Context | None = None):
+    """voxel_downsample (voxelmap.cpp:137-169): one (mean, covariance) per voxel in ascending packed
+    key order — the float64 voxel statistics of the map built at `resolution`."""
+    _, _, vm, vc = GaussianVoxelMap.from_arrays(means, covariances, resolution, ctx).export()
+    return vm, vc
+
+
+@dataclass
+class Submap:
+    cloud: "PointCloud | None"         # float32 device cloud of the (downsampled) merged points
+    voxels: "GaussianVoxelMap"         # the submap's voxel map (global resolution)
+    downsampled: "GaussianVoxelMap | None"  # export() = the float64 submap cloud
+
+
+def build_submap(frames: Sequence[PointCloud], poses, downsample_resolution: float, map_resolution: float,
+                 want_cloud: bool = True) -> Submap:
+    """MappingPipeline::emit_submap's data path (pipeline.cpp:92-114) on the GPU: frames transformed
+    into the submap frame by `poses` (frame -> submap), merged, voxel-downsampled and mapped."""
+    if not frames:
+        raise ValueError("submap requires at least one frame")
+    ctx = frames[0].ctx
+    m = len(frames)
+    P = poses_array(poses)
+    if len(P) != m:
+        raise ValueError("one pose per frame")
+    hs = (C.c_void_p * m)(*[f.handle for f in frames])
+    ds, cl, mp = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    check(_lib.load().vgicp_submap_build(ctx.handle, hs, _ptr(P), m, float(downsample_resolution), float(map_resolution),
+                                         C.byref(ds), C.byref(cl) if want_cloud else None, C.byref(mp)))
+    cloud = None
+    if want_cloud and cl.value:
+        cloud = PointCloud.__new__(PointCloud)
+        _Handle.__init__(cloud, ctx, cl)
+        n = C.c_size_t()
+        check(_lib.load().vgicp_cloud_size(cl, C.byref(n)))
+        cloud.means = None  # device-only (float32 copy of the float64 submap cloud)
+        cloud.cov6 = None
+    downs = GaussianVoxelMap(None, downsample_resolution, _handle=ds, _ctx=ctx) if ds.value else None
+    return Submap(cloud, GaussianVoxelMap(None, map_resolution, _handle=mp, _ctx=ctx), downs)
+
+
 # ------------------------------------------------------------------------------------ voxel maps
 class GaussianVoxelMap(_Handle):
     """GaussianVoxelMap(cloud, resolution) — voxelmap.cpp:65-104, built on the GPU."""
 
     _destroy = "vgicp_voxelmap_destroy"
 
-    def __init__(self, cloud: PointCloud, resolution: float, _handle=None):
+    def __init__(self, cloud: PointCloud | None, resolution: float, _handle=None, _ctx: Context | None = None):
         if _handle is None:
             h = C.c_void_p()
             check(_lib.load().vgicp_voxelmap_build(cloud.ctx.handle, cloud.handle, float(resolution), C.byref(h)))
         else:
             h = _handle
-        super().__init__(cloud.ctx, h)
+        super().__init__(cloud.ctx if cloud is not None else _ctx, h)
         self.cloud = cloud  # keeps the source alive for callers that re-derive stats
         self._resolution = float(resolution)
+
+    @staticmethod
+    def from_arrays(means, covariances, resolution: float, ctx: Context | None = None) -> "GaussianVoxelMap":
+        """GaussianVoxelMap over a float64 cloud in the reference layout (n×3 means, n×3×3 / n×9
+        covariances, all 9 entries accumulated) — voxelmap.cpp:65-104."""
+        ctx = ctx or default_context()
+        m = np.ascontiguousarray(np.asarray(means, np.float64).reshape(-1, 3))
+        c = None if covariances is None else np.ascontiguousarray(np.asarray(covariances, np.float64).reshape(-1, 9))
+        if c is not None and len(c) != len(m):
+            raise ValueError("covariance count does not match point count")
+        h = C.c_void_p()
+        check(_lib.load().vgicp_voxelmap_build_f64(ctx.handle, _ptr(m), _ptr(c) if c is not None else None, len(m),
+                                                   float(resolution), C.byref(h)))
+        return GaussianVoxelMap(None, resolution, _handle=h, _ctx=ctx)
 
     @staticmethod
     def build_batch(clouds: Sequence[PointCloud], resolutions) -> list["GaussianVoxelMap"]:

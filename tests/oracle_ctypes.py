@@ -68,6 +68,7 @@ def _load():
         "or_make_scene": (None, [vp, i, d, d, _dp, _dp, _dp, _dp, _dp, _dp]),
         "or_rng_shuffle": (None, [vp, _u64p, sz]),
         "or_estimate_covariances": (i, [_dp, sz, i, d, _dp]),
+        "or_transform_cloud": (None, [_dp, vp, sz, _dp, _dp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -410,6 +411,39 @@ def estimate_covariances(means, k=10, plane_epsilon=1e-3) -> np.ndarray:
     out = np.zeros((len(m), 9))
     _check(lib().or_estimate_covariances(m, len(m), int(k), float(plane_epsilon), out))
     return out.reshape(-1, 3, 3)
+
+
+def transform_cloud(means, covs, pose12):
+    """transform_cloud (point_cloud.cpp:26-42) restatement; returns (n×3, n×3×3 or None)."""
+    m = _f64(means, (-1, 3))
+    c = None if covs is None else cov9(covs)
+    om = np.zeros_like(m)
+    oc = None if c is None else np.zeros_like(c)
+    lib().or_transform_cloud(m, None if c is None else c.ctypes.data, len(m), _f64(pose12, (12,)), om,
+                             None if oc is None else oc.ctypes.data)
+    return om, (None if oc is None else oc.reshape(-1, 3, 3))
+
+
+def voxel_downsample(means, covs, resolution):
+    """voxel_downsample (voxelmap.cpp:137-169) restatement: the voxel statistics of the (Kahan)
+    GaussianVoxelMap in ascending packed-key order (intensities are not on this path)."""
+    _, _, vm, vc = OracleMap(means, covs, resolution).export()
+    return vm, vc
+
+
+def submap(frames, poses12, downsample_resolution, map_resolution):
+    """emit_submap's data path (pipeline.cpp:92-114): transform each frame into the submap frame,
+    merge in frame order, voxel_downsample, build the submap's voxel map. frames: [(means, covs)]."""
+    ms, cs = [], []
+    for (m, c), T in zip(frames, poses12):
+        tm, tc = transform_cloud(m, c, T)
+        ms.append(tm)
+        cs.append(tc)
+    m = np.concatenate(ms)
+    c = np.concatenate(cs)
+    if downsample_resolution > 0:
+        m, c = voxel_downsample(m, c, downsample_resolution)
+    return m, c, OracleMap(m, c, map_resolution)
 
 
 def unit_covariances(n) -> np.ndarray:
