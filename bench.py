@@ -289,6 +289,37 @@ def run_covariances(ctx, scans, reps=3):
             "note": "exact kNN on a uniform grid + Jacobi eigenvectors, one batched C ABI call, wall clock incl. H2D/D2H"}
 
 
+def run_submap(ctx, wl, threads, frames=20, reps=5):
+    """Submap creation (pipeline.cpp:92-114, config.hpp defaults: 20-frame window, 0.25 m
+    downsample, 1.0 m map) from C3 frames 0..19: GPU through the C ABI vs the oracle port."""
+    import paper_2109_07073_b200 as V
+    from paper_2109_07073_b200 import workloads as W
+
+    clouds = wl.clouds[:frames]
+    poses = np.stack([W.pose_mul(W.pose_inv(wl.scans.gt[0]), wl.scans.gt[k]) for k in range(frames)])
+    V.build_submap(clouds, poses, 0.25, 1.0)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        sub = V.build_submap(clouds, poses, 0.25, 1.0)
+    ms = 1e3 * (time.perf_counter() - t0) / reps
+    out = {"frames": frames, "points": int(sum(len(m) for m in wl.scans.means[:frames])),
+           "submap_points": sub.cloud.size(), "voxels": sub.voxels.size(), "ms_gpu": ms,
+           "note": "vgicp_submap_build: fp64 transform + merge, voxel_downsample 0.25 m, 1.0 m map, float32 cloud "
+                   "handle; wall clock through the C ABI"}
+    try:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_ctypes as O
+
+        f64 = [(wl.scans.means[k].astype(np.float64), O.cov9(wl.scans.cov6[k].astype(np.float64))) for k in range(frames)]
+        t0 = time.perf_counter()
+        O.submap(f64, poses, 0.25, 1.0)
+        out["ms_cpu_port"] = 1e3 * (time.perf_counter() - t0)
+        out["cpu_cores"] = threads
+    except Exception as e:  # the CPU port is a reported comparison only
+        out["cpu_port_error"] = str(e)
+    return out
+
+
 # ------------------------------------------------------------------------------ ours
 def run_ours(args):
     import torch
@@ -423,13 +454,14 @@ def run_ours(args):
         traffic = json.loads(tf.read_text()).get("bytes_per_launch")
     data_bytes = sum(36 * len(m) for m in wl.scans.means) + sum(48 * int(m.size()) * 2 for m in wl.maps)
 
-    lm = c1 = c4 = cov = None
+    lm = c1 = c4 = cov = sub = None
     if world == 1 and not args.profile and not args.no_lm:
         lm = run_lm_c2(ctx, threads)
     if world == 1 and not args.profile and not args.no_extra:
         c1 = run_c1(ctx, threads)
         c4 = run_c4(ctx)
         cov = run_covariances(ctx, wl.scans.means)
+        sub = run_submap(ctx, wl, threads)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -466,6 +498,7 @@ def run_ours(args):
         "c1_single_factor": c1,
         "c4_overlap_sweep": c4,
         "covariances_c3": cov,
+        "submap_c3": sub,
         "clocks": clk,
         "inlier_fraction": inliers / P,
         "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()} | {"total": round(t_build, 3)},

@@ -97,10 +97,21 @@ class PointCloud {
   }
   vgicp_cloud get() const { return h_.get(); }
   const Context& context() const { return ctx_; }
+  // takes ownership of a handle returned by the C ABI (e.g. vgicp_submap_build)
+  static PointCloud adopt(const Context& ctx, vgicp_cloud c) { return PointCloud(ctx, c); }
 
  private:
+  PointCloud(const Context& ctx, vgicp_cloud c) : ctx_(ctx) { h_.reset(c, [](vgicp_cloud x) { vgicp_cloud_destroy(x); }); }
   Context ctx_;
   std::shared_ptr<vgicp_cloud_s> h_;
+};
+
+// The reference's host PointCloud layout (point_cloud.hpp:21-37) for the float64 submap path.
+struct HostCloud {
+  std::vector<Vec3> means;
+  std::vector<Mat3> covariances;  // empty or one per point (row-major)
+  std::size_t size() const { return means.size(); }
+  bool has_covariances() const { return !covariances.empty() && covariances.size() == means.size(); }
 };
 
 struct GaussianVoxel {  // voxelmap.hpp:18-22
@@ -117,6 +128,15 @@ class GaussianVoxelMap {
     check(vgicp_voxelmap_build(ctx_.get(), cloud.get(), resolution, &m));
     h_.reset(m, [](vgicp_map x) { vgicp_voxelmap_destroy(x); });
   }
+  // over a float64 host cloud (all 9 covariance entries accumulated, voxelmap.cpp:65-104)
+  GaussianVoxelMap(const Context& ctx, const HostCloud& cloud, double resolution) : ctx_(ctx) {
+    vgicp_map m = nullptr;
+    check(vgicp_voxelmap_build_f64(ctx.get(), cloud.means.empty() ? nullptr : cloud.means[0].data(),
+                                   cloud.has_covariances() ? cloud.covariances[0].data() : nullptr, cloud.size(),
+                                   resolution, &m));
+    h_.reset(m, [](vgicp_map x) { vgicp_voxelmap_destroy(x); });
+  }
+  static GaussianVoxelMap adopt(const Context& ctx, vgicp_map m) { return GaussianVoxelMap(ctx, m); }
   double resolution() const {
     double r = 0;
     check(vgicp_voxelmap_resolution(get(), &r));
@@ -163,9 +183,57 @@ class GaussianVoxelMap {
   const Context& context() const { return ctx_; }
 
  private:
+  GaussianVoxelMap(const Context& ctx, vgicp_map m) : ctx_(ctx) { h_.reset(m, [](vgicp_map x) { vgicp_voxelmap_destroy(x); }); }
   Context ctx_;
   std::shared_ptr<vgicp_map_s> h_;
 };
+
+// transform_cloud (point_cloud.cpp:26-42), float64 on the device.
+inline HostCloud transform_cloud(const Context& ctx, const HostCloud& cloud, const Pose& T) {
+  HostCloud out;
+  out.means.resize(cloud.size());
+  if (cloud.has_covariances()) out.covariances.resize(cloud.size());
+  if (cloud.size() == 0) return out;
+  check(vgicp_transform_cloud(ctx.get(), cloud.means[0].data(), cloud.has_covariances() ? cloud.covariances[0].data() : nullptr,
+                              cloud.size(), T.data(), out.means[0].data(),
+                              cloud.has_covariances() ? out.covariances[0].data() : nullptr));
+  return out;
+}
+
+// voxel_downsample (voxelmap.cpp:137-169): one point per voxel, ascending packed-key order.
+inline HostCloud voxel_downsample(const Context& ctx, const HostCloud& cloud, double resolution) {
+  const GaussianVoxelMap map(ctx, cloud, resolution);
+  HostCloud out;
+  for (const auto& [key, v] : map.voxels()) {
+    out.means.push_back(v.mean);
+    out.covariances.push_back(v.covariance);
+  }
+  return out;
+}
+
+// MappingPipeline::emit_submap's data path (pipeline.cpp:92-114) on the device: frames transformed
+// by frame_poses (frame -> submap), merged, voxel_downsample'd and mapped at map_resolution.
+struct Submap {
+  PointCloud cloud;         // float32 copy of the (downsampled) float64 submap cloud
+  GaussianVoxelMap voxels;  // the submap's voxel map
+};
+inline Submap build_submap(const std::vector<const PointCloud*>& frames, const std::vector<Pose>& frame_poses,
+                           double downsample_resolution, double map_resolution) {
+  if (frames.empty()) throw std::invalid_argument("submap requires at least one frame");
+  if (frames.size() != frame_poses.size()) throw std::invalid_argument("one pose per frame");
+  const Context& ctx = frames[0]->context();
+  std::vector<vgicp_cloud> fh(frames.size());
+  std::vector<double> P(12 * frames.size());
+  for (std::size_t k = 0; k < frames.size(); ++k) {
+    fh[k] = frames[k]->get();
+    for (int q = 0; q < 12; ++q) P[12 * k + q] = frame_poses[k].m[q];
+  }
+  vgicp_cloud c = nullptr;
+  vgicp_map m = nullptr;
+  check(vgicp_submap_build(ctx.get(), fh.data(), P.data(), static_cast<int>(frames.size()), downsample_resolution,
+                           map_resolution, nullptr, &c, &m));
+  return Submap{PointCloud::adopt(ctx, c), GaussianVoxelMap::adopt(ctx, m)};
+}
 
 inline double overlap_rate(const PointCloud& cloud, const Pose& pose_rel, const GaussianVoxelMap& map) {
   double r = 0.0;

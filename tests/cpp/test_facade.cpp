@@ -93,6 +93,21 @@ int main() {
   const auto g = gicp_error(ctx, {1, 2, 3}, {0.5, 0, 0, 0, 0.5, 0, 0, 0, 0.5}, v, Pose::Identity());
   REQUIRE(g.valid && std::abs(g.error - 1.0) < 1e-12);
 
+  // submap path (§8f #2): transform_cloud, voxel_downsample, build_submap
+  {
+    HostCloud hc;
+    for (int i = 0; i < 200; ++i) {
+      hc.means.push_back({0.05 * i, 0.1 * (i % 7), 0.02 * (i % 13)});
+      hc.covariances.push_back({1, 0, 0, 0, 1, 0, 0, 0, 1e-3});
+    }
+    const HostCloud moved = transform_cloud(ctx, hc, Pose::from({1, 0, 0, 0, 1, 0, 0, 0, 1}, {1, 2, 3}));
+    REQUIRE(moved.size() == 200 && std::abs(moved.means[10][0] - (hc.means[10][0] + 1)) < 1e-12);
+    const HostCloud down = voxel_downsample(ctx, hc, 1.0);
+    REQUIRE(down.size() == GaussianVoxelMap(ctx, hc, 1.0).size());
+    const Submap sub = build_submap({cloud.get(), cloud.get()}, {Pose::Identity(), Pose::Identity()}, 0.5, 1.0);
+    REQUIRE(sub.cloud.has_covariances() && sub.voxels.size() > 0 && sub.voxels.total_points() == sub.cloud.size());
+  }
+
   std::printf("facade ok: voxels=%zu inliers=%d error=%.6f launches=%llu\n", map->size(), lin.inliers, lin.error,
               static_cast<unsigned long long>(ctx.launch_count()));
   return 0;
