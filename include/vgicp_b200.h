@@ -167,6 +167,20 @@ int vgicp_graph_num_points(vgicp_graph graph, uint64_t* points);
 int vgicp_graph_linearize(vgicp_graph graph, const double* poses12, double* out, int32_t* inliers);
 /* Per-factor errors / inliers for total_error (optimizer.cpp:66-75), synchronous. */
 int vgicp_graph_evaluate(vgicp_graph graph, const double* poses12, double* errors, int32_t* inliers);
+/* Device-side normal-equation assembly (§8f #3; assemble_normal_equations, block_solver.cpp:14-62).
+ * vgicp_graph_assembly_plan fixes the variable mask (fixed[num_poses], non-zero = fixed): active
+ * variables get slots in reverse insertion order (slot 0 = last active variable, :26-34); the
+ * distinct off-diagonal blocks are the slot pairs (a > b) in ascending (b, a) order — written to
+ * pairs[2·P] as (a, b) when pairs != NULL (call once with NULL to size it).
+ * vgicp_graph_linearize_assembled runs one linearization pass and assembles on the device:
+ * diag[S×36] = Σ H_ii / H_jj per slot, offdiag[P×36] = Σ H_ij (or H_ijᵀ) per pair, stored as the
+ * (row a, col b) block, rhs[S×6] = Σ b_i / b_j — each summed in factor order from zero, i.e.
+ * bit-identical to the reference's assembly of the same factor blocks. Only S·42 + P·36 doubles
+ * cross PCIe instead of F·121. */
+int vgicp_graph_assembly_plan(vgicp_graph graph, const uint8_t* fixed, int* num_slots, int* num_pairs, int32_t* pairs);
+int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, double* diag, double* offdiag,
+                                    double* rhs);
+
 /* Device-resident variants: every pointer is device memory of the context's device; the work
  * is enqueued on the context stream and the call returns without synchronising. */
 int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, double* d_out, int32_t* d_inliers);

@@ -1,5 +1,6 @@
 // C ABI (include/vgicp_b200.h): contexts, handles, validation and launch orchestration.
 // Host code only; the kernels live in voxelmap.cu and factor.cu.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>
 
@@ -9,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <memory>
 #include <new>
 
@@ -623,6 +625,53 @@ int vgicp_transform_cloud(vgicp_ctx ctx, const double* xyz, const double* cov9, 
   return VGICP_OK;
 }
 
+// float32 device cloud (same layout as cloud_upload_packed) from float64 device arrays.
+static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const double* d_cov9, size_t n, vgicp_cloud* out) {
+  *out = nullptr;
+  if (n >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "cloud too large (>= 2^31 points)");
+  cudaStream_t s = ctx->stream;
+  auto c = std::make_unique<vgicp_cloud_s>();
+  c->ctx = ctx;
+  c->n = n;
+  c->has_cov = n > 0;
+  const size_t na = align_up(n * sizeof(float4), 256);
+  const size_t nc = align_up(n * sizeof(float), 256);
+  const size_t half = na * 2 + nc;
+  const size_t nblk = (n + kPointBlock - 1) / kPointBlock;
+  VG_CUDA(cudaMalloc(&c->block, std::max<size_t>(half + nblk * sizeof(PointBlock), 256)));
+  char* base = static_cast<char*>(c->block);
+  c->pa = reinterpret_cast<float4*>(base);
+  c->pb = reinterpret_cast<float4*>(base + na);
+  c->pc = reinterpret_cast<float*>(base + 2 * na);
+  c->sblk = reinterpret_cast<PointBlock*>(base + half);
+  if (n > 0) {
+    size_t sort_bytes = 0;
+    VG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                            (const unsigned*)nullptr, (unsigned*)nullptr, static_cast<int>(n), 0, 30,
+                                            s));
+    DevBuf tmp;
+    const size_t b_vec = align_up(sizeof(unsigned) * n, 256);
+    VG_CUDA(cudaMalloc(&tmp.p, 256 + 4 * b_vec + sort_bytes));
+    char* t = static_cast<char*>(tmp.p);
+    auto* box = reinterpret_cast<unsigned*>(t);
+    auto* codes = reinterpret_cast<unsigned*>(t + 256);
+    auto* idx = reinterpret_cast<unsigned*>(t + 256 + b_vec);
+    auto* codes2 = reinterpret_cast<unsigned*>(t + 256 + 2 * b_vec);
+    auto* perm = reinterpret_cast<unsigned*>(t + 256 + 3 * b_vec);
+    void* temp = t + 256 + 4 * b_vec;
+    VG_CUDA(cudaMemsetAsync(box, 0xFF, 3 * sizeof(unsigned), s));
+    VG_CUDA(cudaMemsetAsync(box + 3, 0, 3 * sizeof(unsigned), s));
+    VG_CUDA(launch_cloud_bbox(d_xyz, n, box, s));
+    VG_CUDA(launch_cloud_morton(d_xyz, n, box, codes, idx, s));
+    VG_CUDA(cub::DeviceRadixSort::SortPairs(temp, sort_bytes, codes, codes2, idx, perm, static_cast<int>(n), 0, 30, s));
+    VG_CUDA(launch_cloud_fill(d_xyz, d_cov9, n, perm, c->pa, c->pb, c->pc, c->sblk, s));
+    ctx->launches += 4;
+    VG_CUDA(cudaStreamSynchronize(s));
+  }
+  *out = c.release();
+  return VGICP_OK;
+}
+
 int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* poses12, int m,
                        double downsample_resolution, double map_resolution, vgicp_map* out_downsampled,
                        vgicp_cloud* out_cloud, vgicp_map* out_map) {
@@ -689,18 +738,10 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
     release(ds);
     return rc;
   }
-  // 4. the submap cloud as a float32 device cloud (source of submap-level factors)
+  // 4. the submap cloud as a float32 device cloud (source of submap-level factors), built on the
+  //    device from the float64 arrays (no host round trip)
   if (out_cloud) {
-    std::vector<double> hx(3 * src_n), hc(9 * src_n);
-    cudaError_t e = cudaMemcpyAsync(hx.data(), src_xyz, hx.size() * sizeof(double), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), src_cov, hc.size() * sizeof(double), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) {
-      release(ds);
-      release(mp);
-      return cuda_fail(e, "submap cloud download");
-    }
-    if (int rc = vgicp_cloud_upload_f64(ctx, hx.data(), hc.data(), src_n, out_cloud)) {
+    if (int rc = cloud_from_device_f64(ctx, src_xyz, src_cov, src_n, out_cloud)) {
       release(ds);
       release(mp);
       return rc;
@@ -913,6 +954,8 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
     factors[f].target->refs.fetch_add(1);
     gr->clouds.push_back(factors[f].source);
     gr->maps.push_back(factors[f].target);
+    gr->tgt_idx.push_back(factors[f].target_index);
+    gr->src_idx.push_back(factors[f].source_index);
   }
   *out = gr.release();
   return VGICP_OK;
@@ -924,6 +967,7 @@ int vgicp_graph_destroy(vgicp_graph graph) {
     DeviceGuard g(graph->ctx->device);
     cudaStreamSynchronize(graph->ctx->stream);
     cudaFree(graph->block);
+    if (graph->plan) cudaFree(graph->plan);
   }
   for (auto c : graph->clouds) release(c);
   for (auto m : graph->maps) release(m);
@@ -999,6 +1043,107 @@ int vgicp_graph_linearize(vgicp_graph graph, const double* poses12, double* out,
 
 int vgicp_graph_evaluate(vgicp_graph graph, const double* poses12, double* errors, int32_t* inliers) {
   return graph_run_host(graph, false, poses12, errors, inliers);
+}
+
+// ------------------------------------------------------------------------------------ assembly
+int vgicp_graph_assembly_plan(vgicp_graph graph, const uint8_t* fixed, int* num_slots, int* num_pairs,
+                              int32_t* pairs) {
+  if (!graph || !num_slots || !num_pairs || (graph->num_poses > 0 && !fixed))
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  const int n = graph->num_poses;
+  const int nf = graph->num_factors;
+  // slot numbering: active variables in reverse insertion order (block_solver.cpp:26-34)
+  std::vector<int> slot_of(n, -1);
+  int active = 0;
+  for (int v = 0; v < n; ++v) active += fixed[v] ? 0 : 1;
+  for (int v = 0, rank = 0; v < n; ++v)
+    if (!fixed[v]) slot_of[v] = active - 1 - rank++;
+  // per-output contribution lists in factor order; pairs keyed by (col b, row a), a > b
+  std::vector<std::vector<int>> diag(active);
+  std::map<std::pair<int, int>, std::vector<int>> off;
+  for (int f = 0; f < nf; ++f) {
+    const int si = slot_of[graph->tgt_idx[f]], sj = slot_of[graph->src_idx[f]];
+    if (si >= 0) diag[si].push_back(4 * f + 0);
+    if (sj >= 0) diag[sj].push_back(4 * f + 1);
+    if (si >= 0 && sj >= 0) {
+      if (si >= sj) off[{sj, si}].push_back(4 * f + 2);
+      else off[{si, sj}].push_back(4 * f + 3);
+    }
+  }
+  const int P = static_cast<int>(off.size());
+  const int O = active + P;
+  std::vector<int> out_ptr(O + 1, 0), contrib;
+  for (int o = 0; o < active; ++o) {
+    contrib.insert(contrib.end(), diag[o].begin(), diag[o].end());
+    out_ptr[o + 1] = static_cast<int>(contrib.size());
+  }
+  int o = active;
+  for (const auto& [key, list] : off) {
+    contrib.insert(contrib.end(), list.begin(), list.end());
+    out_ptr[++o] = static_cast<int>(contrib.size());
+    if (pairs) {
+      pairs[2 * (o - 1 - active)] = key.second;  // row slot a
+      pairs[2 * (o - 1 - active) + 1] = key.first;  // column slot b
+    }
+  }
+  DeviceGuard g(graph->ctx->device);
+  if (graph->plan) {
+    VG_CUDA(cudaStreamSynchronize(graph->ctx->stream));
+    cudaFree(graph->plan);
+    graph->plan = nullptr;
+  }
+  const size_t b_ptr = align_up(sizeof(int) * (O + 1), 256);
+  const size_t b_con = align_up(sizeof(int) * std::max<size_t>(contrib.size(), 1), 256);
+  const size_t b_asm = sizeof(double) * (static_cast<size_t>(O) * 36 + static_cast<size_t>(active) * 6 + 1);
+  VG_CUDA(cudaMalloc(&graph->plan, b_ptr + b_con + b_asm));
+  char* b = static_cast<char*>(graph->plan);
+  graph->d_out_ptr = reinterpret_cast<int*>(b);
+  graph->d_contrib = reinterpret_cast<int*>(b + b_ptr);
+  graph->d_asm = reinterpret_cast<double*>(b + b_ptr + b_con);
+  VG_CUDA(cudaMemcpyAsync(graph->d_out_ptr, out_ptr.data(), sizeof(int) * (O + 1), cudaMemcpyHostToDevice,
+                          graph->ctx->stream));
+  if (!contrib.empty())
+    VG_CUDA(cudaMemcpyAsync(graph->d_contrib, contrib.data(), sizeof(int) * contrib.size(), cudaMemcpyHostToDevice,
+                            graph->ctx->stream));
+  VG_CUDA(cudaStreamSynchronize(graph->ctx->stream));
+  graph->num_slots = active;
+  graph->num_pairs = P;
+  *num_slots = active;
+  *num_pairs = P;
+  return VGICP_OK;
+}
+
+int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, double* diag, double* offdiag,
+                                    double* rhs) {
+  if (!graph || !poses12) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (!graph->plan) return fail(VGICP_E_INVALID_ARGUMENT, "no assembly plan (call vgicp_graph_assembly_plan)");
+  const int S = graph->num_slots, P = graph->num_pairs, O = S + P;
+  if ((S > 0 && (!diag || !rhs)) || (P > 0 && !offdiag)) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
+  vgicp_ctx ctx = graph->ctx;
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const size_t pose_bytes = sizeof(double) * 12 * graph->num_poses;
+  const size_t asm_bytes = sizeof(double) * (static_cast<size_t>(O) * 36 + static_cast<size_t>(S) * 6);
+  if (int rc = ensure_pinned(ctx, align_up(pose_bytes, 256) + asm_bytes + 8)) return rc;
+  char* h = static_cast<char*>(ctx->pinned);
+  double* h_asm = reinterpret_cast<double*>(h + align_up(pose_bytes, 256));
+  std::memcpy(h, poses12, pose_bytes);
+  VG_CUDA(cudaMemcpyAsync(graph->d_poses, h, pose_bytes, cudaMemcpyHostToDevice, s));
+  if (graph->num_items > 0) {
+    VG_CUDA(launch_factor(true, graph->d_factors, graph->d_items, graph->num_items, graph->d_poses, graph->d_partials,
+                          graph->d_part_inl, graph->d_counters, graph->d_out, graph->d_out_inl, s));
+    ctx->launches += 1;
+  } else if (graph->num_factors > 0) {
+    VG_CUDA(cudaMemsetAsync(graph->d_out, 0, sizeof(double) * VGICP_LINEARIZED_DOUBLES * graph->num_factors, s));
+  }
+  VG_CUDA(launch_assemble(graph->d_out_ptr, graph->d_contrib, S, O, graph->d_out, graph->d_asm, s));
+  ctx->launches += O > 0 ? 1 : 0;
+  VG_CUDA(cudaMemcpyAsync(h_asm, graph->d_asm, asm_bytes, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  if (S > 0) std::memcpy(diag, h_asm, sizeof(double) * 36 * S);
+  if (P > 0) std::memcpy(offdiag, h_asm + 36 * static_cast<size_t>(S), sizeof(double) * 36 * P);
+  if (S > 0) std::memcpy(rhs, h_asm + 36 * static_cast<size_t>(O), sizeof(double) * 6 * S);
+  return VGICP_OK;
 }
 
 // Single-factor entry points: a one-factor graph over poses {target, source}.

@@ -1,0 +1,118 @@
+// Device-side construction of a float32 cloud from float64 device arrays (the submap cloud of
+// vgicp_submap_build): float32 rounding, input-order SoA for builds, and the Morton-ordered
+// 64-point blocks for the probe kernels — the same layout vgicp_cloud_upload builds on the host
+// (Z-order code of 10 bits per axis over the finite bounding box, ties in input order).
+#include "internal.h"
+
+namespace vgicp {
+
+namespace {
+
+__device__ __forceinline__ unsigned ordered(float f) {  // monotone float -> uint map
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unordered(unsigned u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+__global__ void bbox_kernel(const double* __restrict__ xyz, size_t n, unsigned* __restrict__ box) {
+  unsigned lo[3] = {~0u, ~0u, ~0u}, hi[3] = {0u, 0u, 0u};
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = static_cast<float>(xyz[3 * i + a]);
+      if (isfinite(v)) {
+        lo[a] = min(lo[a], ordered(v));
+        hi[a] = max(hi[a], ordered(v));
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    atomicMin(&box[a], lo[a]);
+    atomicMax(&box[3 + a], hi[a]);
+  }
+}
+
+__device__ __forceinline__ unsigned spread10(unsigned x) {  // 10 bits -> every third bit
+  x &= 0x3FFu;
+  x = (x | (x << 16)) & 0x030000FFu;
+  x = (x | (x << 8)) & 0x0300F00Fu;
+  x = (x | (x << 4)) & 0x030C30C3u;
+  x = (x | (x << 2)) & 0x09249249u;
+  return x;
+}
+
+__global__ void morton_kernel(const double* __restrict__ xyz, size_t n, const unsigned* __restrict__ box,
+                              unsigned* __restrict__ codes, unsigned* __restrict__ idx) {
+  float lo[3], ext[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = unordered(box[a]);
+    ext[a] = unordered(box[3 + a]) - lo[a];
+  }
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = static_cast<float>(xyz[3 * i + a]);
+      const float u = (isfinite(v) && ext[a] > 0.f) ? (v - lo[a]) / ext[a] : 0.f;
+      c[a] = static_cast<unsigned>(fminf(1023.f, fmaxf(0.f, u * 1024.f)));
+    }
+    codes[i] = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
+    idx[i] = static_cast<unsigned>(i);
+  }
+}
+
+__global__ void fill_cloud_kernel(const double* __restrict__ xyz, const double* __restrict__ cov9, size_t n,
+                                  const unsigned* __restrict__ perm, float4* __restrict__ pa, float4* __restrict__ pb,
+                                  float* __restrict__ pc, PointBlock* __restrict__ blk, size_t padded) {
+  for (size_t d = blockIdx.x * (size_t)blockDim.x + threadIdx.x; d < padded; d += (size_t)gridDim.x * blockDim.x) {
+    const size_t dn = d < n ? d : n - 1;
+#pragma unroll
+    for (int copy = 0; copy < 2; ++copy) {
+      const size_t j = copy == 0 ? dn : perm[dn];
+      const double* p = xyz + 3 * j;
+      const double* q = cov9 + 9 * j;
+      const float4 a = make_float4((float)p[0], (float)p[1], (float)p[2], (float)q[0]);
+      const float4 b = make_float4((float)q[1], (float)q[2], (float)q[4], (float)q[5]);
+      const float z = (float)q[8];
+      if (copy == 0) {
+        if (d < n) pa[d] = a, pb[d] = b, pc[d] = z;
+      } else {
+        PointBlock& B = blk[d / kPointBlock];
+        B.pa[d % kPointBlock] = a;
+        B.pb[d % kPointBlock] = b;
+        B.pc[d % kPointBlock] = z;
+      }
+    }
+  }
+}
+
+unsigned grid_cloud(size_t n) {
+  const size_t g = (n + 255) / 256;
+  return static_cast<unsigned>(g == 0 ? 1 : (g < 4096 ? g : 4096));
+}
+
+}  // namespace
+
+cudaError_t launch_cloud_bbox(const double* xyz, size_t n, unsigned* box, cudaStream_t s) {
+  bbox_kernel<<<grid_cloud(n), 256, 0, s>>>(xyz, n, box);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cloud_morton(const double* xyz, size_t n, const unsigned* box, unsigned* codes, unsigned* idx,
+                                cudaStream_t s) {
+  morton_kernel<<<grid_cloud(n), 256, 0, s>>>(xyz, n, box, codes, idx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cloud_fill(const double* xyz, const double* cov9, size_t n, const unsigned* perm, float4* pa,
+                              float4* pb, float* pc, PointBlock* blk, cudaStream_t s) {
+  const size_t padded = (n + kPointBlock - 1) / kPointBlock * kPointBlock;
+  fill_cloud_kernel<<<grid_cloud(padded), 256, 0, s>>>(xyz, cov9, n, perm, pa, pb, pc, blk, padded);
+  return cudaGetLastError();
+}
+
+}  // namespace vgicp

@@ -510,7 +510,40 @@ __global__ void gicp_error_kernel(const double* __restrict__ in, double* __restr
   out[13] = 1.0;
 }
 
+
+// Device-side assemble_normal_equations (block_solver.cpp:14-62): one CTA per output block, one
+// thread per entry (36 H entries + 6 rhs entries for diagonal outputs), contributions summed in
+// factor order starting from zero — the reference's `block += H` sequence, so the assembled system
+// is bit-identical to a host assembly of the same factor blocks.
+__global__ void assemble_kernel(const int* __restrict__ out_ptr, const int* __restrict__ contrib, int num_slots,
+                                int num_outputs, const double* __restrict__ blocks, double* __restrict__ assembled) {
+  const int o = blockIdx.x;
+  const int t = threadIdx.x;
+  if (t >= 42 || (t >= 36 && o >= num_slots)) return;
+  double sum = 0.0;
+  for (int c = out_ptr[o]; c < out_ptr[o + 1]; ++c) {
+    const int code = contrib[c];
+    const double* B = blocks + (size_t)(code >> 2) * VGICP_LINEARIZED_DOUBLES;
+    const int kind = code & 3;
+    double v;
+    if (t < 36) {
+      v = kind == 0 ? B[t] : kind == 1 ? B[72 + t] : kind == 2 ? B[36 + t] : B[36 + (t % 6) * 6 + t / 6];
+    } else {
+      v = B[(kind == 0 ? 108 : 114) + (t - 36)];
+    }
+    sum = __dadd_rn(sum, v);
+  }
+  if (t < 36) assembled[(size_t)o * 36 + t] = sum;
+  else assembled[(size_t)num_outputs * 36 + (size_t)o * 6 + (t - 36)] = sum;
+}
 }  // namespace
+
+cudaError_t launch_assemble(const int* out_ptr, const int* contrib, int num_slots, int num_outputs,
+                            const double* blocks, double* assembled, cudaStream_t s) {
+  if (num_outputs <= 0) return cudaSuccess;
+  assemble_kernel<<<num_outputs, 64, 0, s>>>(out_ptr, contrib, num_slots, num_outputs, blocks, assembled);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkItem* items, int num_items,
                           const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,

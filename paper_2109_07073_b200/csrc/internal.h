@@ -128,6 +128,11 @@ cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkIt
                           const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
                           int* out_inl, cudaStream_t s);
 cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s);
+// assemble_normal_equations (block_solver.cpp:14-62) from F×121 factor blocks: output o < S is
+// slot o's diagonal block (+ rhs), o >= S the off-diagonal pair o - S; contrib codes f·4 + kind
+// (0 H_ii/b_i, 1 H_jj/b_j, 2 H_ij, 3 H_ijᵀ) listed per output in factor order.
+cudaError_t launch_assemble(const int* out_ptr, const int* contrib, int num_slots, int num_outputs,
+                            const double* blocks, double* assembled, cudaStream_t s);
 // transform_cloud (point_cloud.cpp:26-42) of float32 device clouds into fp64 arrays, batched:
 // item k maps cloud k's points (input order) through poses12[k] into out_xyz / out_cov9 at `offset`.
 struct TransformItem {
@@ -141,6 +146,12 @@ struct TransformItem {
 };
 cudaError_t launch_transform(const TransformItem* items, int m, unsigned max_n, double* out_xyz, double* out_cov9,
                              cudaStream_t s);
+// float32 cloud from float64 device arrays (cloud.cu)
+cudaError_t launch_cloud_bbox(const double* xyz, size_t n, unsigned* box, cudaStream_t s);
+cudaError_t launch_cloud_morton(const double* xyz, size_t n, const unsigned* box, unsigned* codes, unsigned* idx,
+                                cudaStream_t s);
+cudaError_t launch_cloud_fill(const double* xyz, const double* cov9, size_t n, const unsigned* perm, float4* pa,
+                              float4* pb, float* pc, PointBlock* blk, cudaStream_t s);
 // the same for fp64 host-provided input arrays (already on device)
 cudaError_t launch_transform64(const double* xyz, const double* cov9, size_t n, const double* T, double* out_xyz,
                                double* out_cov9, cudaStream_t s);
@@ -217,4 +228,11 @@ struct vgicp_graph_s {
   double* d_err = nullptr;
   std::vector<vgicp_cloud> clouds;
   std::vector<vgicp_map> maps;
+  std::vector<int32_t> tgt_idx, src_idx;  // factor variables (target i, source j)
+  // device-side normal-equation assembly plan (vgicp_graph_assembly_plan)
+  void* plan = nullptr;  // out_ptr[O+1] | contrib[C] | assembled[(S+P)·36 + S·6]
+  int num_slots = 0, num_pairs = 0;
+  int* d_out_ptr = nullptr;
+  int* d_contrib = nullptr;
+  double* d_asm = nullptr;
 };

@@ -75,6 +75,9 @@ __device__ __forceinline__ void kahan_add(double& sum, double& comp, double valu
   sum = t;
 }
 
+constexpr int kGroup = 8;    // points per batch of independent loads (float32 path)
+constexpr int kGroup64 = 4;  // (float64 path)
+
 __global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const BuildOut* __restrict__ outs,
                                         const unsigned long long* __restrict__ keys,
                                         const unsigned* __restrict__ vals, const unsigned* __restrict__ heads,
@@ -94,22 +97,41 @@ __global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const
       // float32 cloud: symmetric inputs, so the 6 unique second-moment sums equal the 9 of the
       // reference bit for bit ((0,1) and (1,0) receive identical addends)
       double ss[6] = {0, 0, 0, 0, 0, 0}, sc[6] = {0, 0, 0, 0, 0, 0};  // xx xy xz yy yz zz
-      for (unsigned j = i; j < s.n && (j == i || !heads[s.offset + j]); ++j) {
-        const unsigned p = vals[s.offset + j];
-        const float4 a = __ldg(s.pa + p);
-        const float4 b = __ldg(s.pb + p);
-        const float czz = __ldg(s.pc + p);
-        const double m0 = a.x, m1 = a.y, m2 = a.z;
-        kahan_add(ms[0], mc[0], m0);
-        kahan_add(ms[1], mc[1], m1);
-        kahan_add(ms[2], mc[2], m2);
-        kahan_add(ss[0], sc[0], __dadd_rn((double)a.w, __dmul_rn(m0, m0)));
-        kahan_add(ss[1], sc[1], __dadd_rn((double)b.x, __dmul_rn(m0, m1)));
-        kahan_add(ss[2], sc[2], __dadd_rn((double)b.y, __dmul_rn(m0, m2)));
-        kahan_add(ss[3], sc[3], __dadd_rn((double)b.z, __dmul_rn(m1, m1)));
-        kahan_add(ss[4], sc[4], __dadd_rn((double)b.w, __dmul_rn(m1, m2)));
-        kahan_add(ss[5], sc[5], __dadd_rn((double)czz, __dmul_rn(m2, m2)));
-        ++count;
+      // the run's points in groups of kGroup: independent loads first, then the in-order Kahan adds
+      for (unsigned j = i, more = 1; more; j += kGroup) {
+        bool val[kGroup];
+        float4 A[kGroup], B[kGroup];
+        float Z[kGroup];
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) {
+          const unsigned jj = j + q;
+          val[q] = jj < s.n && (jj == i || !heads[s.offset + jj]);
+        }
+#pragma unroll
+        for (int q = 1; q < kGroup; ++q) val[q] = val[q] && val[q - 1];
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) {
+          const unsigned p = val[q] ? vals[s.offset + j + q] : vals[s.offset + i];
+          A[q] = __ldg(s.pa + p);
+          B[q] = __ldg(s.pb + p);
+          Z[q] = __ldg(s.pc + p);
+        }
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) {
+          if (!val[q]) break;
+          const double m0 = A[q].x, m1 = A[q].y, m2 = A[q].z;
+          kahan_add(ms[0], mc[0], m0);
+          kahan_add(ms[1], mc[1], m1);
+          kahan_add(ms[2], mc[2], m2);
+          kahan_add(ss[0], sc[0], __dadd_rn((double)A[q].w, __dmul_rn(m0, m0)));
+          kahan_add(ss[1], sc[1], __dadd_rn((double)B[q].x, __dmul_rn(m0, m1)));
+          kahan_add(ss[2], sc[2], __dadd_rn((double)B[q].y, __dmul_rn(m0, m2)));
+          kahan_add(ss[3], sc[3], __dadd_rn((double)B[q].z, __dmul_rn(m1, m1)));
+          kahan_add(ss[4], sc[4], __dadd_rn((double)B[q].w, __dmul_rn(m1, m2)));
+          kahan_add(ss[5], sc[5], __dadd_rn((double)Z[q], __dmul_rn(m2, m2)));
+          ++count;
+        }
+        more = val[kGroup - 1];
       }
       const double cnt = static_cast<double>(count);
       const double mean[3] = {__ddiv_rn(ms[0], cnt), __ddiv_rn(ms[1], cnt), __ddiv_rn(ms[2], cnt)};
@@ -123,18 +145,42 @@ __global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const
       // fp64 cloud with full (possibly 1-ulp asymmetric) covariances: all 9 sums, as the reference
       double ss[9], sc[9];
       for (int e = 0; e < 9; ++e) ss[e] = sc[e] = 0.0;
-      for (unsigned j = i; j < s.n && (j == i || !heads[s.offset + j]); ++j) {
-        const size_t p = vals[s.offset + j];
-        const double m[3] = {s.xyz64[3 * p], s.xyz64[3 * p + 1], s.xyz64[3 * p + 2]};
-        const double* C = s.cov9 + 9 * p;
-        kahan_add(ms[0], mc[0], m[0]);
-        kahan_add(ms[1], mc[1], m[1]);
-        kahan_add(ms[2], mc[2], m[2]);
+      for (unsigned j = i, more = 1; more; j += kGroup64) {
+        bool val[kGroup64];
+        size_t pp[kGroup64];
 #pragma unroll
-        for (int r = 0; r < 3; ++r)
+        for (int q = 0; q < kGroup64; ++q) {
+          const unsigned jj = j + q;
+          val[q] = jj < s.n && (jj == i || !heads[s.offset + jj]);
+        }
 #pragma unroll
-          for (int c = 0; c < 3; ++c) kahan_add(ss[3 * r + c], sc[3 * r + c], __dadd_rn(C[3 * r + c], __dmul_rn(m[r], m[c])));
-        ++count;
+        for (int q = 1; q < kGroup64; ++q) val[q] = val[q] && val[q - 1];
+#pragma unroll
+        for (int q = 0; q < kGroup64; ++q) pp[q] = val[q] ? vals[s.offset + j + q] : vals[s.offset + i];
+        double M[kGroup64][3], Cq[kGroup64][9];
+#pragma unroll
+        for (int q = 0; q < kGroup64; ++q) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) M[q][a] = s.xyz64[3 * pp[q] + a];
+#pragma unroll
+          for (int e = 0; e < 9; ++e) Cq[q][e] = s.cov9[9 * pp[q] + e];
+        }
+#pragma unroll
+        for (int q = 0; q < kGroup64; ++q) {
+          if (!val[q]) break;
+          const double* m = M[q];
+          const double* C = Cq[q];
+          kahan_add(ms[0], mc[0], m[0]);
+          kahan_add(ms[1], mc[1], m[1]);
+          kahan_add(ms[2], mc[2], m[2]);
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              kahan_add(ss[3 * r + c], sc[3 * r + c], __dadd_rn(C[3 * r + c], __dmul_rn(m[r], m[c])));
+          ++count;
+        }
+        more = val[kGroup64 - 1];
       }
       const double cnt = static_cast<double>(count);
       const double mean[3] = {__ddiv_rn(ms[0], cnt), __ddiv_rn(ms[1], cnt), __ddiv_rn(ms[2], cnt)};

@@ -185,15 +185,33 @@ def assemble(raw: np.ndarray, ij: np.ndarray, num_poses: int):
     return H, b
 
 
-def solve_damped(H, b, active, lam, bandwidth=None):
-    """Cholesky solve of the damped reduced system; None when not positive definite.
-
-    With `bandwidth` (in scalar rows, from the graph structure) small relative to the system, a
-    banded Cholesky (LAPACK pbtrf/pbtrs via scipy.linalg.solveh_banded) is used — odometry chains;
-    otherwise a dense Cholesky. Both fail exactly when the damped system is not positive definite,
-    which escalates λ like the reference's failed block pivot (block_solver.cpp:80-85)."""
+def _cholesky_solve(Hr, br, lam, bandwidth=None):
+    """Marquardt-damped Cholesky solve of a reduced system (optimizer.cpp:119-123); None when the
+    damped system is not positive definite (escalates λ like a failed block pivot,
+    block_solver.cpp:80-85). Banded LAPACK (pbtrf/pbtrs) when the bandwidth is small, else dense."""
     import scipy.linalg as sla
 
+    m = Hr.shape[0]
+    damp = lambda dg: dg + lam * np.maximum(dg, 1e-10)  # noqa: E731
+    try:
+        if bandwidth is not None and bandwidth < m // 4:
+            ab = np.empty((bandwidth + 1, m))  # lower banded storage
+            ab[0] = damp(np.diagonal(Hr))
+            for k in range(1, bandwidth + 1):
+                ab[k, : m - k] = np.diagonal(Hr, -k)
+                ab[k, m - k:] = 0.0
+            return sla.solveh_banded(ab, br, lower=True, check_finite=False)
+        Hd = np.array(Hr, copy=True)
+        Hd[np.diag_indices_from(Hd)] = damp(np.diagonal(Hr))
+        c = sla.cho_factor(Hd, lower=True, overwrite_a=True, check_finite=False)
+        return sla.cho_solve(c, br, check_finite=False)
+    except np.linalg.LinAlgError:
+        return None
+
+
+def solve_damped(H, b, active, lam, bandwidth=None):
+    """Cholesky solve of the damped reduced system of a dense (all-variable) H; None when not
+    positive definite."""
     act = np.flatnonzero(active)
     if len(act) == 0:
         return np.zeros_like(b)
@@ -203,25 +221,37 @@ def solve_damped(H, b, active, lam, bandwidth=None):
     else:
         idx = np.flatnonzero(np.repeat(active, 6))
         Hr, br = H[np.ix_(idx, idx)], b[idx]
-    m = Hr.shape[0]
-    damp = lambda dg: dg + lam * np.maximum(dg, 1e-10)  # noqa: E731  (optimizer.cpp:119-123)
-    try:
-        if bandwidth is not None and bandwidth < m // 4:
-            ab = np.empty((bandwidth + 1, m))  # lower banded storage
-            ab[0] = damp(np.diagonal(Hr))
-            for k in range(1, bandwidth + 1):
-                ab[k, : m - k] = np.diagonal(Hr, -k)
-                ab[k, m - k:] = 0.0
-            x = sla.solveh_banded(ab, br, lower=True, check_finite=False)
-        else:
-            Hd = np.array(Hr, copy=True)
-            Hd[np.diag_indices_from(Hd)] = damp(np.diagonal(Hr))
-            c = sla.cho_factor(Hd, lower=True, overwrite_a=True, check_finite=False)
-            x = sla.cho_solve(c, br, check_finite=False)
-    except np.linalg.LinAlgError:
+    x = _cholesky_solve(Hr, br, lam, bandwidth)
+    if x is None:
         return None
     delta = np.zeros_like(b)
     delta[idx] = x
+    return delta
+
+
+def slot_system(diag, off, pairs, rhs):
+    """Dense reduced system in slot order from the device-assembled blocks (BlockSystem layout:
+    off[k] is the (row a, col b) block of pair k, a > b)."""
+    S = len(diag)
+    Hs = np.zeros((S, 6, S, 6))
+    s = np.arange(S)
+    Hs[s, :, s, :] = diag
+    if len(pairs):
+        a, b = pairs[:, 0], pairs[:, 1]
+        Hs[a, :, b, :] = off
+        Hs[b, :, a, :] = off.transpose(0, 2, 1)
+    return Hs.reshape(6 * S, 6 * S), rhs.reshape(-1)
+
+
+def solve_damped_slots(Hs, bs, var_of_slot, num_poses, lam, bandwidth=None):
+    """Solve in slot space and scatter the step back to variables (delta_by_var)."""
+    delta = np.zeros(6 * num_poses)
+    if len(var_of_slot) == 0:
+        return delta
+    x = _cholesky_solve(Hs, bs, lam, bandwidth)
+    if x is None:
+        return None
+    delta.reshape(-1, 6)[var_of_slot] = x.reshape(-1, 6)
     return delta
 
 
@@ -234,8 +264,12 @@ def graph_bandwidth(ij, active) -> int:
     return int(6 * np.max(np.abs(rank[ij[both, 0]] - rank[ij[both, 1]])) + 5)
 
 
-def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None = None):
-    """Run LM on `graph` from `poses` (num_poses × 12). Returns (poses, OptimizerReport)."""
+def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None = None, device_assembly: bool = True):
+    """Run LM on `graph` from `poses` (num_poses × 12). Returns (poses, OptimizerReport).
+
+    With device_assembly the normal equations are assembled on the GPU right after the
+    linearization (vgicp_graph_linearize_assembled, block_solver.cpp:14-62) and only the S + P
+    distinct blocks cross PCIe; otherwise the F factor blocks are downloaded and assembled here."""
     settings = settings or LmSettings()
     t_start = time.perf_counter()
     report = OptimizerReport()
@@ -247,17 +281,29 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
     bandwidth = graph_bandwidth(np.asarray(ij), active)
     updates = np.zeros(n, dtype=np.int64)
 
-    raw, _ = graph.linearize_raw(poses)
+    if device_assembly:
+        plan = graph.assembly_plan(fixed_mask.astype(np.uint8))
+
+    def linearize_system():
+        if device_assembly:
+            diag, off, rhs = graph.linearize_assembled(poses)
+            return slot_system(diag, off, plan.pairs, rhs)
+        return assemble(graph.linearize_raw(poses)[0], ij, n)
+
+    system = linearize_system()
     current = graph.total_error(poses)
     report.initial_error = report.final_error = current
     lam = settings.lambda_init
     any_accepted = False
     for it in range(settings.max_iterations):
         t_it = time.perf_counter()
-        H, b = assemble(raw, ij, n)
+        H, b = system
         accepted = False
         while True:
-            delta = solve_damped(H, b, active, lam, bandwidth)
+            if device_assembly:
+                delta = solve_damped_slots(H, b, plan.var_of_slot, n, lam, bandwidth)
+            else:
+                delta = solve_damped(H, b, active, lam, bandwidth)
             if delta is None:
                 lam *= settings.lambda_increase
                 if lam > settings.lambda_max:
@@ -302,7 +348,7 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
         if not accepted or report.reason == "converged_relative_error":
             report.iteration_seconds.append(time.perf_counter() - t_it)
             break
-        raw, _ = graph.linearize_raw(poses)
+        system = linearize_system()
         report.reason = "max_iterations"
         report.iteration_seconds.append(time.perf_counter() - t_it)
     if not report.aborted:

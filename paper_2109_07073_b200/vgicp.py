@@ -38,6 +38,7 @@ __all__ = [
     "evaluate_matching_cost",
     "gicp_error",
     "FactorGraph",
+    "AssemblyPlan",
     "as_pose12",
     "cov6_from",
     "estimate_covariances",
@@ -490,6 +491,13 @@ def gicp_error(source_mean, source_cov, target_mean, target_cov, T, ctx: Context
     return GicpErrorResult(err.value, res, info.reshape(3, 3), bool(valid.value))
 
 
+@dataclass
+class AssemblyPlan:
+    num_slots: int
+    pairs: np.ndarray        # P×2 (row slot a, column slot b), a > b, ascending (b, a)
+    var_of_slot: np.ndarray  # S variable indices
+
+
 class FactorGraph(_Handle):
     """A fixed set of matching-cost factors linearized / evaluated in one launch per pass."""
 
@@ -543,6 +551,36 @@ class FactorGraph(_Handle):
         for e in err:
             s += float(e)
         return s
+
+    # ---- device-side normal-equation assembly (block_solver.cpp:14-62) ----
+    def assembly_plan(self, fixed) -> "AssemblyPlan":
+        """Fix the variable mask; returns the slot numbering and the off-diagonal block pairs."""
+        fx = np.ascontiguousarray(np.asarray(fixed, dtype=np.uint8).reshape(-1))
+        if len(fx) != self.num_poses:
+            raise ValueError("fixed mask length does not match the graph")
+        S, P = C.c_int(), C.c_int()
+        check(_lib.load().vgicp_graph_assembly_plan(self._h, _ptr(fx), C.byref(S), C.byref(P), None))
+        pairs = np.zeros((P.value, 2), np.int32)
+        check(_lib.load().vgicp_graph_assembly_plan(self._h, _ptr(fx), C.byref(S), C.byref(P), _ptr(pairs)))
+        active = np.flatnonzero(fx == 0)
+        var_of_slot = active[::-1].copy()  # slot 0 = last active variable (block_solver.cpp:26-34)
+        self._plan = AssemblyPlan(int(S.value), pairs, var_of_slot)
+        return self._plan
+
+    def linearize_assembled(self, poses):
+        """One linearization pass assembled on the device: (diag S×6×6, offdiag P×6×6, rhs S×6)."""
+        plan = getattr(self, "_plan", None)
+        if plan is None:
+            raise ValueError("no assembly plan (call assembly_plan first)")
+        P = poses_array(poses)
+        if len(P) != self.num_poses:
+            raise ValueError("pose count does not match the graph")
+        S, Np = plan.num_slots, len(plan.pairs)
+        diag = np.zeros((S, 36))
+        off = np.zeros((Np, 36))
+        rhs = np.zeros((S, 6))
+        check(_lib.load().vgicp_graph_linearize_assembled(self._h, _ptr(P), _ptr(diag), _ptr(off), _ptr(rhs)))
+        return diag.reshape(S, 6, 6), off.reshape(Np, 6, 6), rhs
 
     # device-resident variants (pointers are device addresses, e.g. torch tensor data_ptr())
     def linearize_device(self, d_poses: int, d_out: int, d_inliers: int) -> None:

@@ -446,6 +446,40 @@ def submap(frames, poses12, downsample_resolution, map_resolution):
     return m, c, OracleMap(m, c, map_resolution)
 
 
+def assemble_normal_equations(blocks121, ij, fixed, num_variables):
+    """assemble_normal_equations (block_solver.cpp:14-62), restated with the reference's loop order:
+    slots in reverse insertion order of the active variables; for each factor in order
+    block(si,si) += H_ii, rhs[si] += b_i, block(sj,sj) += H_jj, rhs[sj] += b_j, and the off-diagonal
+    H_ij (or H_ijᵀ) into the lower-triangle block. Returns (slot_of_var, diag, {(a, b): block}, rhs)."""
+    fixed = np.asarray(fixed, bool)
+    active = int((~fixed).sum())
+    slot_of = -np.ones(num_variables, int)
+    rank = 0
+    for v in range(num_variables):
+        if not fixed[v]:
+            slot_of[v] = active - 1 - rank
+            rank += 1
+    diag = np.zeros((active, 6, 6))
+    rhs = np.zeros((active, 6))
+    off = {}
+    for f, (i, j) in enumerate(np.asarray(ij)):
+        B = np.asarray(blocks121[f], np.float64)
+        Hii, Hij, Hjj = B[0:36].reshape(6, 6), B[36:72].reshape(6, 6), B[72:108].reshape(6, 6)
+        si, sj = slot_of[i], slot_of[j]
+        if si >= 0:
+            diag[si] += Hii
+            rhs[si] += B[108:114]
+        if sj >= 0:
+            diag[sj] += Hjj
+            rhs[sj] += B[114:120]
+        if si >= 0 and sj >= 0:
+            if si >= sj:
+                off[(si, sj)] = off.get((si, sj), np.zeros((6, 6))) + Hij
+            else:
+                off[(sj, si)] = off.get((sj, si), np.zeros((6, 6))) + Hij.T
+    return slot_of, diag, off, rhs
+
+
 def unit_covariances(n) -> np.ndarray:
     return np.broadcast_to(np.eye(3), (n, 3, 3)).copy()
 

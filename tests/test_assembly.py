@@ -1,0 +1,138 @@
+"""Device-side normal-equation assembly: assemble_normal_equations
+(block_solver.cpp:14-62) after the batched linearization, on the GPU.
+
+CPU tests pin the restatement (tests/oracle_ctypes.assemble_normal_equations) to the reference's
+assembly tests (test_optimizer.cpp:80-140). GPU tests require the device assembly to be
+bit-identical to the restated assembly of the same (GPU-linearized) factor blocks — both sum each
+block in factor order from zero — and the LM on the device-assembled system to match the host one.
+"""
+import numpy as np
+import pytest
+
+import oracle_ctypes as O
+
+
+def random_se3_blocks(rng, n_vars, n_factors):  # test_optimizer.cpp:46-77 construction
+    ij, blocks = [], []
+    for f in range(n_factors):
+        if f < n_vars - 1:
+            i, j = f, f + 1
+        else:
+            i = int(rng.uniform(0, n_vars - 1))
+            j = int(rng.uniform(0, n_vars))
+            if j == i:
+                j = (i + 1) % n_vars
+        S = np.array([[rng.uniform(-1, 1) for _ in range(12)] for _ in range(12)])
+        H = S @ S.T + np.eye(12)
+        B = np.zeros(121)
+        B[0:36] = H[:6, :6].ravel()
+        B[36:72] = H[:6, 6:].ravel()
+        B[72:108] = H[6:, 6:].ravel()
+        B[108:120] = [rng.uniform(-1, 1) for _ in range(12)]
+        ij.append((i, j))
+        blocks.append(B)
+    return np.array(ij), np.array(blocks)
+
+
+def dense_assemble(blocks, ij, n):  # oracles.hpp dense_assemble
+    H = np.zeros((6 * n, 6 * n))
+    b = np.zeros(6 * n)
+    for B, (i, j) in zip(blocks, ij):
+        Hij = B[36:72].reshape(6, 6)
+        H[6 * i:6 * i + 6, 6 * i:6 * i + 6] += B[0:36].reshape(6, 6)
+        H[6 * i:6 * i + 6, 6 * j:6 * j + 6] += Hij
+        H[6 * j:6 * j + 6, 6 * i:6 * i + 6] += Hij.T
+        H[6 * j:6 * j + 6, 6 * j:6 * j + 6] += B[72:108].reshape(6, 6)
+        b[6 * i:6 * i + 6] += B[108:114]
+        b[6 * j:6 * j + 6] += B[114:120]
+    return H, b
+
+
+# ------------------------------------------------------------------------------ oracle (CPU)
+def test_oracle_assembly_single_factor_against_fixed():  # test_optimizer.cpp:80-94
+    ij, blocks = random_se3_blocks(O.Rng(60), 2, 1)
+    slot_of, diag, off, rhs = O.assemble_normal_equations(blocks, [(0, 1)], [1, 0], 2)
+    assert len(diag) == 1 and not off
+    assert np.array_equal(diag[0], blocks[0, 72:108].reshape(6, 6))
+    assert np.array_equal(rhs[0], blocks[0, 114:120])
+
+
+def test_oracle_assembly_matches_dense():  # test_optimizer.cpp:118-140
+    rng = O.Rng(61)
+    for _ in range(10):
+        n = 3 + int(rng.uniform(0, 17))
+        ij, blocks = random_se3_blocks(rng, n, 2 * n)
+        fixed = np.zeros(n, np.uint8)
+        fixed[0] = 1
+        Hd, bd = dense_assemble(blocks, ij, n)
+        slot_of, diag, off, rhs = O.assemble_normal_equations(blocks, ij, fixed, n)
+        var_of = {s: v for v, s in enumerate(slot_of) if s >= 0}
+        for s, v in var_of.items():
+            assert np.abs(rhs[s] - bd[6 * v:6 * v + 6]).max() < 1e-12
+            assert np.abs(diag[s] - Hd[6 * v:6 * v + 6, 6 * v:6 * v + 6]).max() < 1e-12
+        for (a, b), blk in off.items():
+            va, vb = var_of[a], var_of[b]
+            assert np.abs(blk - Hd[6 * va:6 * va + 6, 6 * vb:6 * vb + 6]).max() < 1e-12
+
+
+# ------------------------------------------------------------------------------ GPU
+gpu = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def V():
+    return pytest.importorskip("paper_2109_07073_b200")
+
+
+def graph_case(V, nframes=8, n=3000, seed=70):
+    rng = O.Rng(seed)
+    clouds = []
+    for _ in range(nframes):
+        m, c = rng.gaussian_cloud(n, 10.0)
+        clouds.append(V.PointCloud(m.astype(np.float32), V.cov6_from(c)))
+    maps = V.GaussianVoxelMap.build_batch(clouds, 1.0)
+    poses = np.stack([rng.random_pose(0.05, 0.5) for _ in range(nframes)])
+    factors = [V.MatchingCostFactor(j - d, j, clouds[j], maps[j - d]) for j in range(nframes) for d in (1, 2, 5)
+               if j - d >= 0]
+    factors.append(V.MatchingCostFactor(nframes - 1, 0, clouds[0], maps[nframes - 1]))  # i > j orientation
+    return V.FactorGraph(factors, nframes, chunk=2048), poses
+
+
+@gpu
+@pytest.mark.parametrize("fixed_vars", [(0,), (3,), (0, 4), ()])
+def test_gpu_assembly_bit_exact(V, fixed_vars):
+    graph, poses = graph_case(V)
+    n = len(poses)
+    fixed = np.zeros(n, np.uint8)
+    fixed[list(fixed_vars)] = 1
+    plan = graph.assembly_plan(fixed)
+    diag, off, rhs = graph.linearize_assembled(poses)
+    raw, _ = graph.linearize_raw(poses)
+    slot_of, rdiag, roff, rrhs = O.assemble_normal_equations(raw, graph._ij, fixed, n)
+    assert plan.num_slots == len(rdiag)
+    assert [tuple(p) for p in plan.pairs] == sorted(roff, key=lambda ab: (ab[1], ab[0]))
+    assert np.array_equal(diag, rdiag) and np.array_equal(rhs, rrhs)
+    for k, (a, b) in enumerate(plan.pairs):
+        assert np.array_equal(off[k], roff[(a, b)])
+    assert [int(v) for v in plan.var_of_slot] == [int(np.flatnonzero(slot_of == s)[0]) for s in range(plan.num_slots)]
+
+
+@gpu
+def test_gpu_assembly_validation(V):
+    graph, poses = graph_case(V, nframes=3, n=500)
+    with pytest.raises(ValueError):
+        graph.linearize_assembled(poses)  # no plan yet
+    with pytest.raises(ValueError):
+        graph.assembly_plan(np.zeros(2, np.uint8))
+
+
+@gpu
+def test_gpu_lm_device_assembly_matches_host(V):
+    from paper_2109_07073_b200 import optimizer as LM
+
+    graph, poses = graph_case(V, nframes=6, n=4000, seed=71)
+    p_host, r_host = LM.optimize(graph, poses, device_assembly=False)
+    p_dev, r_dev = LM.optimize(graph, poses, device_assembly=True)
+    assert r_dev.iterations == r_host.iterations and r_dev.reason == r_host.reason
+    assert abs(r_dev.final_error - r_host.final_error) <= 1e-9 * max(1.0, r_host.final_error)
+    assert np.abs(p_dev - p_host).max() < 1e-9
