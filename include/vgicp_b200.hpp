@@ -11,8 +11,10 @@
 // std::out_of_range (as the reference) and vgicp::cuda_error for device failures.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -344,6 +346,16 @@ inline GicpErrorResult gicp_error(const Context& ctx, const Vec3& source_mean, c
 }
 
 // Batched factors over a fixed graph: one launch linearizes / evaluates every factor.
+// BlockSystem (block_solver.hpp): lower-triangle blocks per column slot, rhs per slot; slots are
+// the active variables in reverse insertion order (block_solver.cpp:26-34).
+struct BlockSystem {
+  int num_slots = 0;
+  std::vector<int> slot_of_var;  // -1 for fixed variables
+  std::vector<int> var_of_slot;
+  std::vector<std::map<int, Mat6>> columns;  // columns[b][a] = block (row a, col b), a >= b
+  std::vector<Vec6> rhs;
+};
+
 class MatchingCostBatch {
  public:
   MatchingCostBatch(const Context& ctx, const std::vector<MatchingCostFactor>& factors, int num_poses, int chunk = 0)
@@ -383,6 +395,36 @@ class MatchingCostBatch {
     return s;
   }
   std::size_t size() const { return factors_.size(); }
+  // linearize_all + assemble_normal_equations (block_solver.cpp:14-62) with the assembly on the
+  // device (matching factors only); bit-identical to assembling linearize()'s blocks on the host.
+  BlockSystem linearize_assembled(const std::vector<Pose>& poses, const std::vector<std::uint8_t>& fixed) const {
+    if (static_cast<int>(fixed.size()) != num_poses_) throw std::invalid_argument("fixed mask size does not match");
+    int S = 0, P = 0;
+    check(vgicp_graph_assembly_plan(h_.get(), fixed.data(), &S, &P, nullptr));
+    std::vector<std::int32_t> pairs(2 * static_cast<std::size_t>(P));
+    check(vgicp_graph_assembly_plan(h_.get(), fixed.data(), &S, &P, pairs.data()));
+    const std::vector<double> Pz = flatten(poses);
+    std::vector<double> diag(36 * static_cast<std::size_t>(S)), off(36 * static_cast<std::size_t>(P)),
+        rhs(6 * static_cast<std::size_t>(S));
+    check(vgicp_graph_linearize_assembled(h_.get(), Pz.data(), diag.data(), off.data(), rhs.data()));
+    BlockSystem sys;
+    sys.num_slots = S;
+    sys.slot_of_var.assign(num_poses_, -1);
+    sys.var_of_slot.assign(S, -1);
+    for (int v = 0, rank = 0; v < num_poses_; ++v)
+      if (!fixed[v]) {
+        sys.slot_of_var[v] = S - 1 - rank++;
+        sys.var_of_slot[sys.slot_of_var[v]] = v;
+      }
+    sys.columns.resize(S);
+    sys.rhs.resize(S);
+    for (int k = 0; k < S; ++k) {
+      std::copy_n(diag.data() + 36 * k, 36, sys.columns[k][k].begin());
+      std::copy_n(rhs.data() + 6 * k, 6, sys.rhs[k].begin());
+    }
+    for (int k = 0; k < P; ++k) std::copy_n(off.data() + 36 * k, 36, sys.columns[pairs[2 * k + 1]][pairs[2 * k]].begin());
+    return sys;
+  }
 
  private:
   std::vector<double> flatten(const std::vector<Pose>& poses) const {

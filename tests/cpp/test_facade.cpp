@@ -93,6 +93,28 @@ int main() {
   const auto g = gicp_error(ctx, {1, 2, 3}, {0.5, 0, 0, 0, 0.5, 0, 0, 0, 0.5}, v, Pose::Identity());
   REQUIRE(g.valid && std::abs(g.error - 1.0) < 1e-12);
 
+  // device-side assembly (§8f #3) equals the host assembly of the same factor blocks
+  {
+    MatchingCostBatch b3(ctx, {MatchingCostFactor(0, 1, cloud, map), MatchingCostFactor(1, 2, cloud, map),
+                               MatchingCostFactor(2, 0, cloud, map)}, 3);
+    const std::vector<Pose> poses = {T, Pose::Identity(), Pose::from({1, 0, 0, 0, 1, 0, 0, 0, 1}, {0.1, 0.1, 0})};
+    const BlockSystem sys = b3.linearize_assembled(poses, {1, 0, 0});
+    REQUIRE(sys.num_slots == 2 && sys.var_of_slot[0] == 2 && sys.var_of_slot[1] == 1);
+    const auto lins = b3.linearize(poses);
+    for (int v = 1; v < 3; ++v) {
+      Mat6 d{};
+      Vec6 r{};
+      for (const auto& lf : lins) {
+        if (lf.i == v) for (int e = 0; e < 36; ++e) d[e] += lf.H_ii[e];
+        if (lf.i == v) for (int e = 0; e < 6; ++e) r[e] += lf.b_i[e];
+        if (lf.j == v) for (int e = 0; e < 36; ++e) d[e] += lf.H_jj[e];
+        if (lf.j == v) for (int e = 0; e < 6; ++e) r[e] += lf.b_j[e];
+      }
+      const int sl = sys.slot_of_var[v];
+      REQUIRE(sys.columns[sl].at(sl) == d && sys.rhs[sl] == r);
+    }
+  }
+
   // submap path (§8f #2): transform_cloud, voxel_downsample, build_submap
   {
     HostCloud hc;
