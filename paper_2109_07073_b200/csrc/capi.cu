@@ -1007,6 +1007,17 @@ int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, doub
   return VGICP_OK;
 }
 
+// True when `p` is page-locked host memory (cudaHostAlloc / cudaHostRegister / torch pin_memory):
+// copies can then target it directly instead of going through the context's pinned staging.
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses12, double* out, int32_t* inliers) {
   if (!graph || !poses12 || (graph->num_factors > 0 && (!out || !inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
@@ -1018,11 +1029,13 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
   const size_t pose_bytes = sizeof(double) * 12 * graph->num_poses;
   const size_t res_bytes = linearize ? sizeof(double) * VGICP_LINEARIZED_DOUBLES * nf : sizeof(double) * nf;
   const size_t inl_bytes = sizeof(int32_t) * nf;
-  if (int rc = ensure_pinned(ctx, align_up(pose_bytes, 256) + align_up(res_bytes, 256) + inl_bytes)) return rc;
+  const bool direct = is_pinned(out) && is_pinned(inliers);
+  if (int rc = ensure_pinned(ctx, align_up(pose_bytes, 256) + (direct ? 0 : align_up(res_bytes, 256) + inl_bytes)))
+    return rc;
   char* h = static_cast<char*>(ctx->pinned);
   double* h_poses = reinterpret_cast<double*>(h);
-  double* h_res = reinterpret_cast<double*>(h + align_up(pose_bytes, 256));
-  auto* h_inl = reinterpret_cast<int32_t*>(h + align_up(pose_bytes, 256) + align_up(res_bytes, 256));
+  double* h_res = direct ? out : reinterpret_cast<double*>(h + align_up(pose_bytes, 256));
+  auto* h_inl = direct ? inliers : reinterpret_cast<int32_t*>(h + align_up(pose_bytes, 256) + align_up(res_bytes, 256));
   std::memcpy(h_poses, poses12, pose_bytes);
   VG_CUDA(cudaMemcpyAsync(graph->d_poses, h_poses, pose_bytes, cudaMemcpyHostToDevice, s));
   double* d_res = linearize ? graph->d_out : graph->d_err;
@@ -1032,8 +1045,10 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
   VG_CUDA(cudaMemcpyAsync(h_res, d_res, res_bytes, cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaMemcpyAsync(h_inl, graph->d_out_inl, inl_bytes, cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaStreamSynchronize(s));
-  std::memcpy(out, h_res, res_bytes);
-  std::memcpy(inliers, h_inl, inl_bytes);
+  if (!direct) {
+    std::memcpy(out, h_res, res_bytes);
+    std::memcpy(inliers, h_inl, inl_bytes);
+  }
   return VGICP_OK;
 }
 

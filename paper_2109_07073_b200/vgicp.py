@@ -522,12 +522,22 @@ class FactorGraph(_Handle):
         check(_lib.load().vgicp_graph_num_points(self._h, C.byref(n)))
         return int(n.value)
 
-    def linearize_raw(self, poses) -> tuple[np.ndarray, np.ndarray]:
+    def linearize_raw(self, poses, out: np.ndarray | None = None, inliers: np.ndarray | None = None):
+        """F×121 blocks + F inliers. `out` / `inliers` may be preallocated (page-locked buffers,
+        e.g. from torch pin_memory, receive the device copy directly)."""
         P = poses_array(poses)
         if len(P) != self.num_poses:
             raise ValueError("pose count does not match the graph")
-        out = np.zeros((self.num_factors(), _lib.LINEARIZED_DOUBLES))
-        inl = np.zeros(self.num_factors(), np.int32)
+        F = self.num_factors()
+        if out is None:
+            out = np.empty((F, _lib.LINEARIZED_DOUBLES))
+        if inliers is None:
+            inliers = np.empty(F, np.int32)
+        if out.shape != (F, _lib.LINEARIZED_DOUBLES) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float64 F×121 array")
+        if inliers.shape != (F,) or inliers.dtype != np.int32 or not inliers.flags.c_contiguous:
+            raise ValueError("inliers must be a C-contiguous int32 array of length F")
+        inl = inliers
         check(_lib.load().vgicp_graph_linearize(self._h, _ptr(P), _ptr(out), _ptr(inl)))
         return out, inl
 

@@ -377,6 +377,24 @@ def test_graph_deterministic_and_chunk_invariant_counts(ctx):
     assert np.max(np.linalg.norm(a - c, axis=1) / scale) < 1e-6  # fp32 per-thread order changes with chunking
 
 
+def test_graph_preallocated_and_pinned_outputs(ctx):
+    """linearize_raw into caller buffers: pageable (staged) and page-locked (direct D2H)."""
+    import torch
+
+    factors, _, _, poses = build_graph_case(ctx, nframes=4, n=2000, seed=62)
+    g = V.FactorGraph(factors, len(poses))
+    a, ia = g.linearize_raw(poses)
+    F = len(factors)
+    b, ib = np.empty((F, 121)), np.empty(F, np.int32)
+    g.linearize_raw(poses, b, ib)
+    pc = torch.empty((F, 121), dtype=torch.float64).pin_memory().numpy()
+    pi = torch.empty(F, dtype=torch.int32).pin_memory().numpy()
+    g.linearize_raw(poses, pc, pi)
+    assert np.array_equal(a, b) and np.array_equal(a, pc) and np.array_equal(ia, ib) and np.array_equal(ia, pi)
+    with pytest.raises(ValueError):
+        g.linearize_raw(poses, np.empty((F, 120)), ib)
+
+
 def test_graph_validation(ctx):
     factors, _, _, poses = build_graph_case(ctx, nframes=3, n=500, seed=62)
     with pytest.raises(ValueError):
