@@ -8,8 +8,10 @@ order on the host), Marquardt damping diag += λ·max(diag, 1e-10) (optimizer.cp
 acceptance iff the error decreases, λ ×0.1 / ×10, termination on relative decrease < 1e-6, step
 norm < 1e-8, λ > 1e10 or max iterations. Gauge: the first pose of every connected component
 without a fixed variable is anchored (optimizer.cpp:24-43). The reduced normal equations are
-solved with a dense Cholesky (the reference's block Cholesky, block_solver.cpp:64-123, is ~3% of
-the time per PAPER.md:410; a failed factorization escalates λ like the reference's failed pivot).
+assembled on the device (block_solver.cpp:14-62, §8f #3) and solved with a banded host Cholesky
+(chains) or a dense Cholesky on the GPU (loop-closing graphs); the reference's block Cholesky,
+block_solver.cpp:64-123, is ~3% of the time per PAPER.md:410, and a failed factorization
+escalates λ like the reference's failed pivot.
 """
 from __future__ import annotations
 
@@ -209,6 +211,77 @@ def _cholesky_solve(Hr, br, lam, bandwidth=None):
         return None
 
 
+class _ReducedSolver:
+    """Damped solves of one device-assembled reduced system (slot order) for successive λ
+    (optimizer.cpp:117-131): a banded LAPACK Cholesky on the host when the bandwidth is small
+    (odometry chains; the band is filled straight from the blocks), otherwise a dense Cholesky —
+    on the GPU (cuSOLVER potrf/potrs through torch; the S + P blocks are uploaded and scattered on
+    the device once per linearization) when `device` is given, else on the host."""
+
+    def __init__(self, diag, off, pairs, rhs, bandwidth=None, device=None):
+        S = len(diag)
+        m = 6 * S
+        self.m, self.rhs = m, rhs.reshape(-1)
+        self.banded = bandwidth is not None and bandwidth < m // 4
+        self.gpu = device is not None and not self.banded and m > 0
+        if self.banded:
+            bw = bandwidth
+            ab = np.zeros((bw + 1, m))
+            r = np.arange(6)
+            rows = np.broadcast_to((6 * np.arange(S))[:, None, None] + r[None, :, None], (S, 6, 6))
+            cols = np.broadcast_to((6 * np.arange(S))[:, None, None] + r[None, None, :], (S, 6, 6))
+            lower = rows >= cols
+            ab[(rows - cols)[lower], cols[lower]] = diag[lower]
+            if len(pairs):
+                a, b = pairs[:, 0].astype(np.int64), pairs[:, 1].astype(np.int64)
+                R = np.broadcast_to((6 * a)[:, None, None] + r[None, :, None], off.shape)
+                Cc = np.broadcast_to((6 * b)[:, None, None] + r[None, None, :], off.shape)
+                k = (R - Cc).ravel()
+                ok = k <= bw
+                ab[k[ok], Cc.ravel()[ok]] = off.ravel()[ok]
+            self.ab = ab
+        elif self.gpu:
+            import torch
+
+            self.torch = torch
+            Hs = torch.zeros((S, 6, S, 6), dtype=torch.float64, device=device)
+            s_idx = torch.arange(S, device=device)
+            Hs[s_idx, :, s_idx, :] = torch.from_numpy(np.ascontiguousarray(diag)).to(device)
+            if len(pairs):
+                a = torch.from_numpy(pairs[:, 0].astype(np.int64)).to(device)
+                b = torch.from_numpy(pairs[:, 1].astype(np.int64)).to(device)
+                O = torch.from_numpy(np.ascontiguousarray(off)).to(device)
+                Hs[a, :, b, :] = O
+                Hs[b, :, a, :] = O.transpose(1, 2)
+            self.Hd = Hs.reshape(m, m)
+            self.bd = torch.from_numpy(np.ascontiguousarray(self.rhs)).to(device).reshape(-1, 1)
+            self.dg = torch.diagonal(self.Hd).clone()
+        else:
+            self.Hr, _ = slot_system(diag, off, pairs, rhs)
+
+    def solve(self, lam):
+        if self.m == 0:
+            return np.zeros(0)
+        if self.banded:
+            import scipy.linalg as sla
+
+            ab = self.ab.copy()
+            ab[0] = ab[0] + lam * np.maximum(ab[0], 1e-10)  # optimizer.cpp:119-123
+            try:
+                return sla.solveh_banded(ab, self.rhs, lower=True, check_finite=False)
+            except np.linalg.LinAlgError:
+                return None
+        if not self.gpu:
+            return _cholesky_solve(self.Hr, self.rhs, lam, None)
+        torch = self.torch
+        A = self.Hd.clone()
+        A.diagonal().copy_(self.dg + lam * torch.clamp(self.dg, min=1e-10))
+        L, info = torch.linalg.cholesky_ex(A)
+        if int(info.item()) != 0:
+            return None
+        return torch.cholesky_solve(self.bd, L).reshape(-1).cpu().numpy()
+
+
 def solve_damped(H, b, active, lam, bandwidth=None):
     """Cholesky solve of the damped reduced system of a dense (all-variable) H; None when not
     positive definite."""
@@ -243,16 +316,21 @@ def slot_system(diag, off, pairs, rhs):
     return Hs.reshape(6 * S, 6 * S), rhs.reshape(-1)
 
 
-def solve_damped_slots(Hs, bs, var_of_slot, num_poses, lam, bandwidth=None):
-    """Solve in slot space and scatter the step back to variables (delta_by_var)."""
+def scatter_slots(x, var_of_slot, num_poses):
+    """Slot-space step -> delta_by_var (fixed variables stay zero)."""
     delta = np.zeros(6 * num_poses)
-    if len(var_of_slot) == 0:
-        return delta
-    x = _cholesky_solve(Hs, bs, lam, bandwidth)
-    if x is None:
-        return None
-    delta.reshape(-1, 6)[var_of_slot] = x.reshape(-1, 6)
+    if x is not None and len(var_of_slot):
+        delta.reshape(-1, 6)[var_of_slot] = x.reshape(-1, 6)
     return delta
+
+
+def _gpu_device(graph: FactorGraph):
+    try:
+        import torch
+
+        return torch.device("cuda", graph.ctx.device) if torch.cuda.is_available() else None
+    except Exception:
+        return None
 
 
 def graph_bandwidth(ij, active) -> int:
@@ -264,12 +342,14 @@ def graph_bandwidth(ij, active) -> int:
     return int(6 * np.max(np.abs(rank[ij[both, 0]] - rank[ij[both, 1]])) + 5)
 
 
-def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None = None, device_assembly: bool = True):
+def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None = None, device_assembly: bool = True,
+             gpu_solve: bool = True):
     """Run LM on `graph` from `poses` (num_poses × 12). Returns (poses, OptimizerReport).
 
     With device_assembly the normal equations are assembled on the GPU right after the
     linearization (vgicp_graph_linearize_assembled, block_solver.cpp:14-62) and only the S + P
-    distinct blocks cross PCIe; otherwise the F factor blocks are downloaded and assembled here."""
+    distinct blocks cross PCIe; otherwise the F factor blocks are downloaded and assembled here.
+    With gpu_solve, systems too wide for the banded host solver are factorized on the GPU."""
     settings = settings or LmSettings()
     t_start = time.perf_counter()
     report = OptimizerReport()
@@ -287,7 +367,7 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
     def linearize_system():
         if device_assembly:
             diag, off, rhs = graph.linearize_assembled(poses)
-            return slot_system(diag, off, plan.pairs, rhs)
+            return diag, off, rhs
         return assemble(graph.linearize_raw(poses)[0], ij, n)
 
     system = linearize_system()
@@ -297,11 +377,16 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
     any_accepted = False
     for it in range(settings.max_iterations):
         t_it = time.perf_counter()
-        H, b = system
+        if device_assembly:
+            solver = _ReducedSolver(*system[:2], plan.pairs, system[2], bandwidth,
+                                    _gpu_device(graph) if gpu_solve else None)
+        else:
+            H, b = system
         accepted = False
         while True:
             if device_assembly:
-                delta = solve_damped_slots(H, b, plan.var_of_slot, n, lam, bandwidth)
+                x = solver.solve(lam)
+                delta = None if x is None else scatter_slots(x, plan.var_of_slot, n)
             else:
                 delta = solve_damped(H, b, active, lam, bandwidth)
             if delta is None:

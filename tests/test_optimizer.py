@@ -216,3 +216,20 @@ def test_banded_solve_matches_dense():
     assert np.allclose(dense, banded, rtol=1e-10, atol=1e-12)
     active[5] = False  # non-contiguous active set -> gather path
     assert np.allclose(LM.solve_damped(H, b, active, 1e-3, None), LM.solve_damped(H, b, active, 1e-3, LM.graph_bandwidth(ij, active)), rtol=1e-10, atol=1e-12)
+
+
+def test_reduced_solver_banded_matches_dense():
+    """Band filled straight from the device-assembled blocks == dense slot system (host)."""
+    rng = np.random.default_rng(0)
+    S = 12
+    pairs = np.array([[a, b] for b in range(S) for a in range(b + 1, min(S, b + 3))], np.int32)
+    diag = np.stack([(lambda M: M @ M.T + 6 * np.eye(6))(rng.standard_normal((6, 6))) for _ in range(S)])
+    off = rng.standard_normal((len(pairs), 6, 6)) * 0.1
+    rhs = rng.standard_normal((S, 6))
+    banded = LM._ReducedSolver(diag, off, pairs, rhs, 6 * 2 + 5, None)
+    dense = LM._ReducedSolver(diag, off, pairs, rhs, None, None)
+    assert banded.banded and not dense.banded
+    for lam in (0.0, 1e-3, 10.0):
+        assert np.abs(banded.solve(lam) - dense.solve(lam)).max() < 1e-12
+    H, b = LM.slot_system(diag, off, pairs, rhs)
+    assert np.array_equal(H, H.T)
