@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--no-lm", action="store_true", help="skip the C2 full-LM leg")
     p.add_argument("--no-extra", action="store_true", help="skip the C1 / C4 legs")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu / e2e legs)")
+    p.add_argument("--no-c5", action="store_true", help="skip the C5 (1,000-frame multi-resolution) leg")
     return p.parse_args()
 
 
@@ -230,6 +231,47 @@ def run_lm_c3(wl, max_iterations=30):
         "note": "linearize + device assembly (S+P blocks D2H), dense cuSOLVER Cholesky per damping trial, "
                 "one evaluate launch per candidate; wall clock incl. H2D/D2H",
     }
+
+
+def run_c5(ctx, steps=10):
+    """BASELINE config C5 on one GPU: 1,000-frame loop-closing graph, ~10k factors over 0.5 / 1 /
+    2 m maps; device-timed linearize / evaluate launches with resident inputs."""
+    import torch
+    from paper_2109_07073_b200 import workloads as W
+
+    wl = W.build_c5_workload(ctx)
+    g = wl.graph
+    F = wl.num_factors
+    stream = torch.cuda.current_stream()
+    d_poses = torch.from_numpy(np.ascontiguousarray(wl.poses)).to("cuda")
+    d_out = torch.empty((F, 121), dtype=torch.float64, device="cuda")
+    d_inl = torch.empty(F, dtype=torch.int32, device="cuda")
+    d_err = torch.empty(F, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        g.linearize_device(d_poses.data_ptr(), d_out.data_ptr(), d_inl.data_ptr())
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        a.record(stream)
+        g.linearize_device(d_poses.data_ptr(), d_out.data_ptr(), d_inl.data_ptr())
+        b.record(stream)
+    torch.cuda.synchronize()
+    lin = sorted(a.elapsed_time(b) for a, b in ev)[steps // 2]
+    for a, b in ev:
+        a.record(stream)
+        g.evaluate_device(d_poses.data_ptr(), d_err.data_ptr(), d_inl.data_ptr())
+        b.record(stream)
+    torch.cuda.synchronize()
+    evm = sorted(a.elapsed_time(b) for a, b in ev)[steps // 2]
+    pts = g.num_points()
+    by_res = {str(r): sum(1 for k in range(F) if W.C5_RESOLUTIONS[k % 3] == r) for r in W.C5_RESOLUTIONS}
+    out = {"frames": len(wl.clouds), "factors": F, "factors_by_resolution": by_res, "points": int(pts),
+           "ms_linearize_kernel": lin, "ms_evaluate_kernel": evm, "factors_per_s": F / (lin * 1e-3),
+           "points_per_s": pts / (lin * 1e-3), "inliers": int(d_inl.sum().item()),
+           "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()},
+           "note": "single GPU (the BASELINE config names 8xB200); one launch per pass over all resolutions"}
+    del wl, g
+    return out
 
 
 # ------------------------------------------------------------------------------ C1 / C4
@@ -476,7 +518,7 @@ def run_ours(args):
         traffic = json.loads(tf.read_text()).get("bytes_per_launch")
     data_bytes = sum(36 * len(m) for m in wl.scans.means) + sum(48 * int(m.size()) * 2 for m in wl.maps)
 
-    lm = lm3 = c1 = c4 = cov = sub = None
+    lm = lm3 = c1 = c4 = cov = sub = c5 = None
     if world == 1 and not args.profile and not args.no_lm:
         lm = run_lm_c2(ctx, threads)
         lm3 = run_lm_c3(wl)
@@ -485,6 +527,8 @@ def run_ours(args):
         c4 = run_c4(ctx)
         cov = run_covariances(ctx, wl.scans.means)
         sub = run_submap(ctx, wl, threads)
+        if not args.no_c5:
+            c5 = run_c5(ctx)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -523,6 +567,7 @@ def run_ours(args):
         "c4_overlap_sweep": c4,
         "covariances_c3": cov,
         "submap_c3": sub,
+        "c5_multires": c5,
         "clocks": clk,
         "inlier_fraction": inliers / P,
         "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()} | {"total": round(t_build, 3)},

@@ -5,6 +5,7 @@
 #include <cub/device/device_segmented_radix_sort.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -46,14 +47,22 @@ unsigned next_pow2(unsigned long long x) {
   return p;
 }
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync on the context
+// stream, release threshold raised at context creation): no implicit device synchronisation and
+// no page-mapping cost on the repeated graph / map / submap builds.
+cudaError_t dmalloc(vgicp_ctx ctx, void** p, size_t bytes) { return cudaMallocAsync(p, bytes, ctx->stream); }
+void dfree(vgicp_ctx ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
 int ensure_scratch(vgicp_ctx ctx, size_t bytes) {
   if (ctx->scratch_bytes >= bytes) return VGICP_OK;
   VG_CUDA(cudaStreamSynchronize(ctx->stream));
   const size_t want = std::max(bytes, ctx->scratch_bytes * 2);
-  if (ctx->scratch) VG_CUDA(cudaFree(ctx->scratch));
+  if (ctx->scratch) dfree(ctx, ctx->scratch);
   ctx->scratch = nullptr;
   ctx->scratch_bytes = 0;
-  VG_CUDA(cudaMalloc(&ctx->scratch, want));
+  VG_CUDA(dmalloc(ctx, &ctx->scratch, want));
   ctx->scratch_bytes = want;
   return VGICP_OK;
 }
@@ -86,7 +95,7 @@ struct DeviceGuard {
 void release(vgicp_cloud c) {
   if (c && c->refs.fetch_sub(1) == 1) {
     DeviceGuard g(c->ctx->device);
-    cudaFree(c->block);
+    dfree(c->ctx, c->block);
     delete c;
   }
 }
@@ -94,15 +103,15 @@ void release(vgicp_cloud c) {
 void release(vgicp_map m) {
   if (m && m->refs.fetch_sub(1) == 1) {
     DeviceGuard g(m->ctx->device);
-    cudaFree(m->cold);
-    cudaFree(m->table);
+    dfree(m->ctx, m->cold);
+    dfree(m->ctx, m->table);
     delete m;
   }
 }
 
 // (Re)allocate a map's hash table with `buckets` buckets (power of two), all slots empty.
 int alloc_table(vgicp_map mp, unsigned buckets, cudaStream_t s) {
-  if (mp->table) VG_CUDA(cudaFree(mp->table));
+  if (mp->table) dfree(mp->ctx, mp->table);
   mp->table = nullptr;
   mp->num_buckets = buckets;
   unsigned lg = 0;
@@ -111,7 +120,7 @@ int alloc_table(vgicp_map mp, unsigned buckets, cudaStream_t s) {
   const size_t cap = static_cast<size_t>(kBucket) * buckets;
   const size_t b_keys = align_up(sizeof(unsigned long long) * cap, 256);
   const size_t b_sa = align_up(sizeof(SlotStatsA) * cap, 256);
-  VG_CUDA(cudaMalloc(&mp->table, b_keys + b_sa + sizeof(SlotStatsB) * cap));
+  VG_CUDA(dmalloc(mp->ctx, &mp->table, b_keys + b_sa + sizeof(SlotStatsB) * cap));
   mp->tkeys = static_cast<unsigned long long*>(mp->table);
   mp->sa = reinterpret_cast<SlotStatsA*>(static_cast<char*>(mp->table) + b_keys);
   mp->sb = reinterpret_cast<SlotStatsB*>(static_cast<char*>(mp->table) + b_keys + b_sa);
@@ -175,6 +184,12 @@ int vgicp_ctx_create(int device, void* stream, vgicp_ctx* out) {
     VG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     ctx->own_stream = true;
   }
+  // keep freed blocks in the device's default pool (no return to the OS between builds)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t threshold = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
   *out = ctx.release();
   return VGICP_OK;
 }
@@ -183,7 +198,8 @@ int vgicp_ctx_destroy(vgicp_ctx ctx) {
   if (!ctx) return VGICP_OK;
   DeviceGuard g(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  if (ctx->scratch) cudaFree(ctx->scratch);
+  if (ctx->scratch) dfree(ctx, ctx->scratch);
+  cudaStreamSynchronize(ctx->stream);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -262,7 +278,7 @@ static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov
   const size_t half = na * 2 + nc;
   const size_t nblk = (n + kPointBlock - 1) / kPointBlock;
   const size_t bytes = std::max<size_t>(half + nblk * sizeof(PointBlock), 256);
-  VG_CUDA(cudaMalloc(&c->block, bytes));
+  VG_CUDA(dmalloc(ctx, &c->block, bytes));
   char* base = static_cast<char*>(c->block);
   c->pa = reinterpret_cast<float4*>(base);
   c->pb = reinterpret_cast<float4*>(base + na);
@@ -477,10 +493,10 @@ static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map*
     const size_t b_counts = align_up(sizeof(int) * V, 256);
     const size_t b_mean = align_up(sizeof(double) * 3 * V, 256);
     const size_t b_cov = align_up(sizeof(double) * 9 * V, 256);
-    const cudaError_t e = cudaMalloc(&mp->cold, std::max<size_t>(b_keys + b_counts + b_mean + b_cov, 256));
+    const cudaError_t e = dmalloc(ctx, &mp->cold, std::max<size_t>(b_keys + b_counts + b_mean + b_cov, 256));
     if (e != cudaSuccess) {
       cleanup();
-      return cuda_fail(e, "cudaMalloc(voxel map)");
+      return cuda_fail(e, "cudaMallocAsync(voxel map)");
     }
     char* b = static_cast<char*>(mp->cold);
     mp->keys = reinterpret_cast<unsigned long long*>(b);
@@ -568,11 +584,12 @@ int vgicp_voxelmap_build(vgicp_ctx ctx, vgicp_cloud cloud, double resolution, vg
 
 // RAII device buffer for temporaries of the fp64 / submap paths.
 namespace {
-struct DevBuf {
+struct DevBuf {  // stream-ordered temporary: freed on the context stream after its last use
+  vgicp_ctx ctx;
   void* p = nullptr;
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
+  explicit DevBuf(vgicp_ctx c) : ctx(c) {}
+  cudaError_t alloc(size_t bytes) { return dmalloc(ctx, &p, bytes); }
+  ~DevBuf() { dfree(ctx, p); }
 };
 }  // namespace
 
@@ -586,8 +603,8 @@ int vgicp_voxelmap_build_f64(vgicp_ctx ctx, const double* xyz, const double* cov
   if (!xyz) return fail(VGICP_E_INVALID_ARGUMENT, "null point array");
   if (n >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "cloud too large (>= 2^31 points)");
   DeviceGuard g(ctx->device);
-  DevBuf buf;
-  VG_CUDA(cudaMalloc(&buf.p, n * 12 * sizeof(double)));
+  DevBuf buf(ctx);
+  VG_CUDA(buf.alloc(n * 12 * sizeof(double)));
   double* d_xyz = static_cast<double*>(buf.p);
   double* d_cov = d_xyz + 3 * n;
   VG_CUDA(cudaMemcpyAsync(d_xyz, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -605,9 +622,9 @@ int vgicp_transform_cloud(vgicp_ctx ctx, const double* xyz, const double* cov9, 
   if (n == 0) return VGICP_OK;
   const bool cov = cov9 && out_cov9;
   DeviceGuard g(ctx->device);
-  DevBuf buf;
+  DevBuf buf(ctx);
   const size_t per = cov ? 24 : 6;  // doubles per point: in + out
-  VG_CUDA(cudaMalloc(&buf.p, (n * per + 12) * sizeof(double)));
+  VG_CUDA(buf.alloc((n * per + 12) * sizeof(double)));
   double* d_in = static_cast<double*>(buf.p);
   double* d_cin = d_in + 3 * n;
   double* d_out = cov ? d_cin + 9 * n : d_in + 3 * n;
@@ -638,7 +655,7 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
   const size_t nc = align_up(n * sizeof(float), 256);
   const size_t half = na * 2 + nc;
   const size_t nblk = (n + kPointBlock - 1) / kPointBlock;
-  VG_CUDA(cudaMalloc(&c->block, std::max<size_t>(half + nblk * sizeof(PointBlock), 256)));
+  VG_CUDA(dmalloc(ctx, &c->block, std::max<size_t>(half + nblk * sizeof(PointBlock), 256)));
   char* base = static_cast<char*>(c->block);
   c->pa = reinterpret_cast<float4*>(base);
   c->pb = reinterpret_cast<float4*>(base + na);
@@ -649,9 +666,9 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
     VG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
                                             (const unsigned*)nullptr, (unsigned*)nullptr, static_cast<int>(n), 0, 30,
                                             s));
-    DevBuf tmp;
+    DevBuf tmp(ctx);
     const size_t b_vec = align_up(sizeof(unsigned) * n, 256);
-    VG_CUDA(cudaMalloc(&tmp.p, 256 + 4 * b_vec + sort_bytes));
+    VG_CUDA(tmp.alloc(256 + 4 * b_vec + sort_bytes));
     char* t = static_cast<char*>(tmp.p);
     auto* box = reinterpret_cast<unsigned*>(t);
     auto* codes = reinterpret_cast<unsigned*>(t + 256);
@@ -694,10 +711,20 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
   if (total >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "submap too large (>= 2^31 points)");
   DeviceGuard g(ctx->device);
   cudaStream_t s = ctx->stream;
+  const bool verbose = std::getenv("VGICP_VERBOSE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto stage = [&](const char* what) {
+    if (!verbose) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[vgicp] submap %-12s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   // 1. transform_cloud of every frame into the submap frame, merged in frame order (pipeline.cpp:97-107)
-  DevBuf merged, items;
-  VG_CUDA(cudaMalloc(&merged.p, total * 12 * sizeof(double)));
-  VG_CUDA(cudaMalloc(&items.p, m * sizeof(TransformItem)));
+  DevBuf merged(ctx), items(ctx);
+  VG_CUDA(merged.alloc(total * 12 * sizeof(double)));
+  VG_CUDA(items.alloc(m * sizeof(TransformItem)));
   double* d_xyz = static_cast<double*>(merged.p);
   double* d_cov = d_xyz + 3 * total;
   std::vector<TransformItem> hi(m);
@@ -716,6 +743,7 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
   VG_CUDA(cudaMemcpyAsync(items.p, hi.data(), m * sizeof(TransformItem), cudaMemcpyHostToDevice, s));
   VG_CUDA(launch_transform(static_cast<const TransformItem*>(items.p), m, max_n, d_xyz, d_cov, s));
   ctx->launches += 1;
+  stage("transform");
   // 2. voxel_downsample (voxelmap.cpp:137-169): the voxel means / covariances in ascending key
   //    order are exactly the cold arrays of the map built at the downsample resolution
   const double* src_xyz = d_xyz;
@@ -729,6 +757,7 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
     src_xyz = ds->mean64;
     src_cov = ds->cov64;
     src_n = ds->voxels;
+    stage("downsample");
   }
   // 3. the submap's voxel map at the global resolution (pipeline.cpp:114)
   std::vector<BuildSeg> segs{BuildSeg{nullptr, nullptr, nullptr, src_xyz, src_cov, 0ull, static_cast<unsigned>(src_n),
@@ -738,6 +767,7 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
     release(ds);
     return rc;
   }
+  stage("map");
   // 4. the submap cloud as a float32 device cloud (source of submap-level factors), built on the
   //    device from the float64 arrays (no host round trip)
   if (out_cloud) {
@@ -746,6 +776,7 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
       release(mp);
       return rc;
     }
+    stage("cloud");
   }
   VG_CUDA(cudaStreamSynchronize(s));
   if (out_downsampled) *out_downsampled = ds;
@@ -921,7 +952,7 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   const size_t o_out = carve(sizeof(double) * VGICP_LINEARIZED_DOUBLES * nf);
   const size_t o_oi = carve(sizeof(int) * nf);
   const size_t o_err = carve(sizeof(double) * nf);
-  VG_CUDA(cudaMalloc(&gr->block, off));
+  VG_CUDA(dmalloc(ctx, &gr->block, off));
   char* b = static_cast<char*>(gr->block);
   gr->d_factors = reinterpret_cast<FactorDev*>(b + o_f);
   gr->d_items = reinterpret_cast<WorkItem*>(b + o_i);
@@ -946,7 +977,7 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   step(cudaMemsetAsync(gr->d_counters, 0, sizeof(unsigned) * nf, s), "zero counters");
   step(cudaStreamSynchronize(s), "graph create");
   if (rc != VGICP_OK) {
-    cudaFree(gr->block);
+    dfree(ctx, gr->block);
     return rc;
   }
   for (int f = 0; f < num_factors; ++f) {
@@ -966,8 +997,8 @@ int vgicp_graph_destroy(vgicp_graph graph) {
   {
     DeviceGuard g(graph->ctx->device);
     cudaStreamSynchronize(graph->ctx->stream);
-    cudaFree(graph->block);
-    if (graph->plan) cudaFree(graph->plan);
+    dfree(graph->ctx, graph->block);
+    dfree(graph->ctx, graph->plan);
   }
   for (auto c : graph->clouds) release(c);
   for (auto m : graph->maps) release(m);
@@ -1104,13 +1135,13 @@ int vgicp_graph_assembly_plan(vgicp_graph graph, const uint8_t* fixed, int* num_
   DeviceGuard g(graph->ctx->device);
   if (graph->plan) {
     VG_CUDA(cudaStreamSynchronize(graph->ctx->stream));
-    cudaFree(graph->plan);
+    dfree(graph->ctx, graph->plan);
     graph->plan = nullptr;
   }
   const size_t b_ptr = align_up(sizeof(int) * (O + 1), 256);
   const size_t b_con = align_up(sizeof(int) * std::max<size_t>(contrib.size(), 1), 256);
   const size_t b_asm = sizeof(double) * (static_cast<size_t>(O) * 36 + static_cast<size_t>(active) * 6 + 1);
-  VG_CUDA(cudaMalloc(&graph->plan, b_ptr + b_con + b_asm));
+  VG_CUDA(dmalloc(graph->ctx, &graph->plan, b_ptr + b_con + b_asm));
   char* b = static_cast<char*>(graph->plan);
   graph->d_out_ptr = reinterpret_cast<int*>(b);
   graph->d_contrib = reinterpret_cast<int*>(b + b_ptr);

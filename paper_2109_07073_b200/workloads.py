@@ -5,6 +5,9 @@
   C3 KITTI-00-shaped dense graph: 450-frame figure-eight, every frame linked to its (up to) 10
      highest-overlap predecessors with overlap > 0.025 (pipeline.cpp:135-141 rule), ~4,500 factors
   C4 overlap sweep: one new frame against many keyframe maps
+  C5 multi-resolution loop-closing graph: 1,000-frame figure-eight, up to 10 links per frame by
+     the overlap rule, factors assigned round-robin to 0.5 / 1 / 2 m maps (3 maps per frame),
+     ~10,000 factors
 Factor direction follows the reference: target = older frame (owns the map), source = newer frame
 (pipeline.cpp:46-48, 141). Factor selection runs the GPU overlap query (the keyframe / factor
 creation path, voxelmap.cpp:119-135).
@@ -137,3 +140,45 @@ def build_graph_workload(ctx: Context, spec: S.SceneSpec, resolution: float = 1.
 
 def c2_links(frames: int = 100, depth: int = 3):
     return [(k - d, k) for k in range(1, frames) for d in range(1, depth + 1) if k - d >= 0]
+
+
+C5_RESOLUTIONS = (0.5, 1.0, 2.0)
+
+
+def c5_spec(frames=1000, points=20000, seed=5) -> S.SceneSpec:
+    return S.SceneSpec(shape="figure_eight", frames=frames, radius=50.0, points_per_scan=points, seed=seed,
+                       drift=(0.0, 0.0, np.deg2rad(0.1), 0.01, 0.0, 0.0))
+
+
+def build_c5_workload(ctx: Context, spec: S.SceneSpec | None = None, max_links: int = 10, min_overlap: float = 0.025,
+                      chunk: int = 0) -> GraphWorkload:
+    """C5: every frame gets 0.5 / 1 / 2 m maps; links by the overlap rule on the 1 m maps; link k
+    uses the map of resolution C5_RESOLUTIONS[k % 3]."""
+    spec = spec or c5_spec()
+    t0 = time.perf_counter()
+    scans = make_scans(spec, ctx=ctx)
+    t1 = time.perf_counter()
+    clouds = [PointCloud(m, c, ctx) for m, c in zip(scans.means, scans.cov6)]
+    maps = {r: GaussianVoxelMap.build_batch(clouds, r) for r in C5_RESOLUTIONS}
+    ctx.synchronize()
+    t2 = time.perf_counter()
+    n = len(clouds)
+    pairs = [(i, j) for j in range(1, n) for i in range(j)]
+    gt = np.asarray(scans.gt)
+    Rs = gt[:, :9].reshape(-1, 3, 3)
+    ts = gt[:, 9:]
+    I = np.array([p[0] for p in pairs])
+    J = np.array([p[1] for p in pairs])
+    R = np.einsum("kba,kbc->kac", Rs[I], Rs[J])  # R_iᵀ R_j
+    t = np.einsum("kba,kb->ka", Rs[I], ts[J] - ts[I])  # R_iᵀ (t_j - t_i)
+    rels = np.concatenate([R.reshape(-1, 9), t], axis=1)
+    hits = overlap_hits([clouds[j] for j in J], rels, [maps[1.0][i] for i in I])
+    overlaps = {p: float(h) / len(scans.means[p[1]]) for p, h in zip(pairs, hits)}
+    links = select_links(overlaps, n, max_links, min_overlap)
+    t3 = time.perf_counter()
+    factors = [MatchingCostFactor(i, j, clouds[j], maps[C5_RESOLUTIONS[k % 3]][i]) for k, (i, j) in enumerate(links)]
+    graph = FactorGraph(factors, n, chunk=chunk, ctx=ctx)
+    t4 = time.perf_counter()
+    return GraphWorkload(ctx, scans, clouds, [m for r in C5_RESOLUTIONS for m in maps[r]], list(links), factors, graph,
+                         np.ascontiguousarray(scans.odom), 1.0,
+                         dict(scans=t1 - t0, upload_and_maps=t2 - t1, overlap_selection=t3 - t2, graph=t4 - t3))

@@ -377,6 +377,30 @@ def test_graph_deterministic_and_chunk_invariant_counts(ctx):
     assert np.max(np.linalg.norm(a - c, axis=1) / scale) < 1e-6  # fp32 per-thread order changes with chunking
 
 
+def test_graph_multiresolution_matches_oracle(ctx):
+    """C5 shape: one graph whose factors use 0.5 / 1 / 2 m maps round-robin (one launch)."""
+    rng = O.Rng(63)
+    res = (0.5, 1.0, 2.0)
+    clouds, frames = [], []
+    for _ in range(5):
+        means, covs = rng.gaussian_cloud(3000, 8.0)
+        c, m, c9 = gpu_cloud(ctx, means, covs)
+        clouds.append(c)
+        frames.append((m, c9))
+    maps = {r: V.GaussianVoxelMap.build_batch(clouds, r) for r in res}
+    omaps = {r: [O.OracleMap(m, c9, r) for m, c9 in frames] for r in res}
+    poses = [rng.random_pose(0.05, 0.5) for _ in range(5)]
+    links = [(i, j) for j in range(5) for i in range(j)]
+    factors = [V.MatchingCostFactor(i, j, clouds[j], maps[res[k % 3]][i]) for k, (i, j) in enumerate(links)]
+    graph = V.FactorGraph(factors, 5)
+    for k, ((i, j), lin) in enumerate(zip(links, graph.linearize(poses))):
+        m, c9 = frames[j]
+        ref = O.linearize(m, c9, omaps[res[k % 3]][i], poses[i], poses[j])
+        assert lin.inliers == ref["inliers"]
+        d = rel_block_error(lin_dict(lin), ref)
+        assert max(d.values()) <= H_TOL, (res[k % 3], d)
+
+
 def test_graph_preallocated_and_pinned_outputs(ctx):
     """linearize_raw into caller buffers: pageable (staged) and page-locked (direct D2H)."""
     import torch
