@@ -408,65 +408,6 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
     hit_math<kLinearize>(sm.Rf, T, map, qa, qb.x, qb.y, qb.w, qc, hq.d[idx], v0, v1, v2, acc, inl);
   };
 
-    double Tr[12];
-#pragma unroll
-    for (int q = 0; q < 12; ++q) Tr[q] = T[q];
-    unsigned hi[kILP], lo[kILP], b1[kILP], b2[kILP];
-    float q0[kILP], q1[kILP], q2[kILP];
-    bool ok[kILP];
-#pragma unroll
-    for (int u = 0; u < kILP; ++u) {
-      const int p = u * 32 + lane;
-      const int lp = min(p, tile_n - 1);  // clamped: every lane computes, in-range lanes count
-      const float4 A = tb.pa[lp];
-      double qd0, qd1, qd2;
-      apply_pose_rn(Tr, A.x, A.y, A.z, qd0, qd1, qd2);
-      unsigned k0 = 0, k1 = 0, k2 = 0;
-      double ld0, ld1, ld2;
-      ok[u] = voxel_key(qd0, qd1, qd2, map.res, map.inv_res, k0, k1, k2, ld0, ld1, ld2) && (p < tile_n);
-      __syncwarp();  // every lane has read its (clamped) A before any lane parks l over it
-      if (p < tile_n) tb.pa[p] = make_float4((float)ld0, (float)ld1, (float)ld2, A.w);
-      pack_key32(k0, k1, k2, hi[u], lo[u]);
-      b1[u] = bucket1(k0, k1, k2, map.shift);
-      b2[u] = bucket2(k0, k1, k2, map.shift);
-      q0[u] = (float)qd0, q1[u] = (float)qd1, q2[u] = (float)qd2;
-    }
-    BucketPair bp[kILP];
-#pragma unroll
-    for (int u = 0; u < kILP; ++u) bp[u] = load_buckets(map.keys, b1[u], b2[u]);  // always in-bounds
-    // ---- math phase on earlier tiles' hits while this tile's bucket loads are in flight ----
-    while (tail - head >= 32u) {
-      consume((head + lane) % static_cast<unsigned>(kQueue));
-      head += 32u;
-    }
-    __syncwarp();  // consumed entries are free before any lane appends over them
-#pragma unroll
-    for (int u = 0; u < kILP; ++u) {
-      const int s = match_buckets(bp[u], b1[u], b2[u], hi[u], lo[u]);
-      const bool hit = ok[u] && s >= 0;
-      const unsigned ball = __ballot_sync(0xffffffffu, hit);
-      if (hit) {
-        const int p = u * 32 + lane;
-        const unsigned idx = (tail + __popc(ball & lane_lt)) % static_cast<unsigned>(kQueue);
-        const float4 B = tb.pb[p];
-        const float4 L = tb.pa[p];
-        hq.a[idx] = make_float4(L.x, L.y, L.z, q0[u]);
-        hq.b[idx] = make_float4(q1[u], q2[u], __int_as_float(s), L.w);
-        hq.c[idx] = B;
-        hq.d[idx] = tb.pc[p];
-      }
-      tail += __popc(ball);
-    }
-    __syncwarp();  // queue entries visible; the warp is done with this ring slot
-    if (lane == 0 && k + kStages < my_tiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async refill
-      issue_tile(k + kStages);
-    }
-
-  }
-  for (; tail - head >= 32u; head += 32u) consume((head + lane) % static_cast<unsigned>(kQueue));
-  __syncwarp();
-#else
   for (int k = 0; k < my_tiles; ++k) {
     const int stage = k % kStages;
     while (!mbar_try_wait(&bars[stage], (k / kStages) & 1)) {
@@ -531,7 +472,6 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
       __syncwarp();
     }
   }
-#endif
   if (head + lane < tail) consume((head + lane) % static_cast<unsigned>(kQueue));  // the last partial batch
   __syncwarp();  // this warp is done with its ring (no CTA-wide barrier after the prologue)
 
