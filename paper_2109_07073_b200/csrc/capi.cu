@@ -5,6 +5,7 @@
 #include <cub/device/device_segmented_radix_sort.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -14,6 +15,8 @@
 #include <map>
 #include <memory>
 #include <new>
+#include <thread>
+#include <tuple>
 
 #include "internal.h"
 
@@ -1253,6 +1256,49 @@ int vgicp_gicp_error(vgicp_ctx ctx, const double source_mean[3], const double so
 }
 
 // ------------------------------------------------------------------------------------ preprocessing
+// memcpy split over host threads (staging of large point / covariance batches)
+static void parallel_copy(void* dst, const void* src, size_t bytes) {
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (bytes < (8u << 20) || hw == 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t chunk = (bytes + hw - 1) / hw;
+  for (unsigned t = 0; t < hw; ++t) {
+    const size_t o = t * chunk;
+    if (o >= bytes) break;
+    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(chunk, bytes - o)); });
+  }
+  for (auto& x : th) x.join();
+}
+
+// copies[k] = (dst, src, bytes), spread over host threads (fresh destination pages fault in parallel)
+static void parallel_copies(const std::vector<std::tuple<void*, const void*, size_t>>& copies) {
+  size_t total = 0;
+  for (const auto& c : copies) total += std::get<2>(c);
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (total < (4u << 20) || hw == 1 || copies.size() == 1) {
+    for (const auto& c : copies) parallel_copy(std::get<0>(c), std::get<1>(c), std::get<2>(c));
+    return;
+  }
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < hw; ++t)
+    th.emplace_back([&] {
+      for (size_t k; (k = next.fetch_add(1)) < copies.size();)
+        std::memcpy(std::get<0>(copies[k]), std::get<1>(copies[k]), std::get<2>(copies[k]));
+    });
+  for (auto& x : th) x.join();
+}
+
+static float unordered_host(unsigned u) {
+  const unsigned v = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+  float f;
+  std::memcpy(&f, &v, sizeof(f));
+  return f;
+}
+
 int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, const size_t* n, int m, int k,
                                      double plane_epsilon, float* const* cov6) {
   if (!ctx || (m > 0 && (!xyz || !n || !cov6))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
@@ -1262,20 +1308,73 @@ int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, con
   if (k > 32) return fail(VGICP_E_INVALID_ARGUMENT, "covariance estimation supports k <= 32 on the GPU");
   std::vector<CovSeg> segs(m);
   size_t total = 0;
-  unsigned long long cells = 0;
   unsigned max_n = 0;
   for (int c = 0; c < m; ++c) {
     if (n[c] <= static_cast<size_t>(k))
       return fail(VGICP_E_INVALID_ARGUMENT, "covariance estimation requires more than k points");
     if (!xyz[c] || !cov6[c]) return fail(VGICP_E_INVALID_ARGUMENT, "null point or output array");
-    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (size_t i = 0; i < n[c]; ++i)
-      for (int a = 0; a < 3; ++a) {
-        const double v = xyz[c][3 * i + a];
-        if (!std::isfinite(v)) return fail(VGICP_E_INVALID_ARGUMENT, "point cloud contains NaN/Inf coordinates");
-        lo[a] = std::min(lo[a], v);
-        hi[a] = std::max(hi[a], v);
-      }
+    segs[c] = CovSeg{};
+    segs[c].offset = static_cast<unsigned>(total);
+    segs[c].n = static_cast<unsigned>(n[c]);
+    segs[c].eps = plane_epsilon;
+    total += n[c];
+    max_n = std::max(max_n, segs[c].n);
+  }
+  if (total >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "batch too large");
+  DeviceGuard gd(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const bool verbose = std::getenv("VGICP_VERBOSE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto stage = [&](const char* what) {
+    if (!verbose) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[vgicp] covariances %-10s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
+  // 1. points to the device (pinned staging), per-cloud bounding boxes on the device
+  if (int rc = ensure_pinned(ctx, sizeof(float) * 6 * total)) return rc;
+  DevBuf pts(ctx), meta(ctx);
+  VG_CUDA(pts.alloc(align_up(sizeof(float) * 3 * total, 256) + sizeof(float) * 6 * total));
+  VG_CUDA(meta.alloc(align_up(sizeof(CovSeg) * m, 256) + sizeof(unsigned) * 6 * m + sizeof(int) * m));
+  auto* d_xyz = static_cast<float*>(pts.p);
+  auto* d_cov = reinterpret_cast<float*>(static_cast<char*>(pts.p) + align_up(sizeof(float) * 3 * total, 256));
+  auto* d_segs = static_cast<CovSeg*>(meta.p);
+  auto* d_box = reinterpret_cast<unsigned*>(static_cast<char*>(meta.p) + align_up(sizeof(CovSeg) * m, 256));
+  auto* d_bad = reinterpret_cast<int*>(d_box + 6 * m);
+  VG_CUDA(cudaStreamSynchronize(s));
+  float* h = static_cast<float*>(ctx->pinned);
+  {
+    std::vector<std::tuple<void*, const void*, size_t>> cp;
+    for (int c = 0; c < m; ++c) cp.emplace_back(h + 3 * segs[c].offset, xyz[c], sizeof(float) * 3 * n[c]);
+    parallel_copies(cp);
+  }
+  stage("stage-in");
+  VG_CUDA(cudaMemcpyAsync(d_xyz, h, sizeof(float) * 3 * total, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemcpyAsync(d_segs, segs.data(), sizeof(CovSeg) * m, cudaMemcpyHostToDevice, s));
+  stage("h2d");
+  for (int c = 0; c < m; ++c) {
+    VG_CUDA(cudaMemsetAsync(d_box + 6 * c, 0xFF, 3 * sizeof(unsigned), s));
+    VG_CUDA(cudaMemsetAsync(d_box + 6 * c + 3, 0, 3 * sizeof(unsigned), s));
+  }
+  VG_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int) * m, s));
+  VG_CUDA(launch_cov_bbox(d_segs, m, max_n, d_xyz, d_box, d_bad, s));
+  std::vector<unsigned> hbox(6 * m);
+  std::vector<int> hbad(m);
+  VG_CUDA(cudaMemcpyAsync(hbox.data(), d_box, sizeof(unsigned) * 6 * m, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaMemcpyAsync(hbad.data(), d_bad, sizeof(int) * m, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  stage("bbox");
+  // 2. grid parameters per cloud (cell ~ (extent^2 k / n)^(1/2) in the dominant plane, <= 2^22 cells)
+  unsigned long long cells = 0;
+  for (int c = 0; c < m; ++c) {
+    if (hbad[c]) return fail(VGICP_E_INVALID_ARGUMENT, "point cloud contains NaN/Inf coordinates");
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = unordered_host(hbox[6 * c + a]);
+      hi[a] = unordered_host(hbox[6 * c + 3 + a]);
+    }
     const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], 1e-3});
     double cell = std::max(std::sqrt(ext * ext * k / static_cast<double>(n[c])), 1e-3);
     int g[3];
@@ -1289,28 +1388,20 @@ int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, con
       cell *= 1.5;
     }
     CovSeg& sg = segs[c];
-    sg.offset = static_cast<unsigned>(total);
-    sg.n = static_cast<unsigned>(n[c]);
     sg.cell_base = static_cast<unsigned>(cells);
     sg.gx = g[0], sg.gy = g[1], sg.gz = g[2];
     for (int a = 0; a < 3; ++a) sg.lo[a] = lo[a];
     sg.cell = cell;
-    sg.eps = plane_epsilon;
-    total += n[c];
     cells += static_cast<unsigned long long>(g[0]) * g[1] * g[2];
-    max_n = std::max(max_n, sg.n);
   }
-  if (total >= (1ull << 31) || cells >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "batch too large");
-  DeviceGuard gd(ctx->device);
+  if (cells >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "batch too large");
+  // 3. counting sort into the cells, exact kNN, eigen regularisation
   size_t off = 0;
   auto carve = [&](size_t bytes) {
     const size_t o = off;
     off = align_up(off + bytes, 256);
     return o;
   };
-  const size_t o_segs = carve(sizeof(CovSeg) * m);
-  const size_t o_xyz = carve(sizeof(float) * 3 * total);
-  const size_t o_cov = carve(sizeof(float) * 6 * total);
   const size_t o_cell = carve(sizeof(unsigned) * total);
   const size_t o_sorted = carve(sizeof(unsigned) * total);
   const size_t o_cnt = carve(sizeof(unsigned) * (cells + 1));
@@ -1318,35 +1409,34 @@ int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, con
   const size_t o_cursor = carve(sizeof(unsigned) * cells);
   size_t scan_bytes = 0;
   VG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
-                                        static_cast<int>(cells + 1), ctx->stream));
+                                        static_cast<int>(cells + 1), s));
   const size_t o_temp = carve(scan_bytes);
   if (int rc = ensure_scratch(ctx, off)) return rc;
-  if (int rc = ensure_pinned(ctx, sizeof(float) * 6 * total)) return rc;
   char* sb = static_cast<char*>(ctx->scratch);
-  auto* d_segs = reinterpret_cast<CovSeg*>(sb + o_segs);
-  auto* d_xyz = reinterpret_cast<float*>(sb + o_xyz);
-  auto* d_cov = reinterpret_cast<float*>(sb + o_cov);
   auto* d_cell = reinterpret_cast<unsigned*>(sb + o_cell);
   auto* d_sorted = reinterpret_cast<unsigned*>(sb + o_sorted);
   auto* d_cnt = reinterpret_cast<unsigned*>(sb + o_cnt);
   auto* d_start = reinterpret_cast<unsigned*>(sb + o_start);
   auto* d_cursor = reinterpret_cast<unsigned*>(sb + o_cursor);
-  cudaStream_t s = ctx->stream;
-  VG_CUDA(cudaStreamSynchronize(s));
-  float* h = static_cast<float*>(ctx->pinned);
-  for (int c = 0; c < m; ++c) std::memcpy(h + 3 * segs[c].offset, xyz[c], sizeof(float) * 3 * n[c]);
-  VG_CUDA(cudaMemcpyAsync(d_xyz, h, sizeof(float) * 3 * total, cudaMemcpyHostToDevice, s));
   VG_CUDA(cudaMemcpyAsync(d_segs, segs.data(), sizeof(CovSeg) * m, cudaMemcpyHostToDevice, s));
   VG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned) * (cells + 1), s));
   VG_CUDA(cudaMemsetAsync(d_cursor, 0, sizeof(unsigned) * cells, s));
   VG_CUDA(launch_cov_count(d_segs, m, max_n, d_xyz, d_cell, d_cnt, s));
   VG_CUDA(cub::DeviceScan::ExclusiveSum(sb + o_temp, scan_bytes, d_cnt, d_start, static_cast<int>(cells + 1), s));
   VG_CUDA(launch_cov_scatter(d_segs, m, max_n, d_cell, d_start, d_cursor, d_sorted, s));
+  stage("grid");
   VG_CUDA(launch_cov_knn(d_segs, m, max_n, d_xyz, d_start, d_sorted, k, d_cov, s));
-  ctx->launches += 4;
+  ctx->launches += 5;
+  stage("knn");
   VG_CUDA(cudaMemcpyAsync(h, d_cov, sizeof(float) * 6 * total, cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaStreamSynchronize(s));
-  for (int c = 0; c < m; ++c) std::memcpy(cov6[c], h + 6 * segs[c].offset, sizeof(float) * 6 * n[c]);
+  stage("d2h");
+  {
+    std::vector<std::tuple<void*, const void*, size_t>> cp;
+    for (int c = 0; c < m; ++c) cp.emplace_back(cov6[c], h + 6 * segs[c].offset, sizeof(float) * 6 * n[c]);
+    parallel_copies(cp);
+  }
+  stage("stage-out");
   return VGICP_OK;
 }
 

@@ -7,6 +7,8 @@
 // Batched over clouds. Exact kNN on a uniform grid: points are counting-sorted into cells, each
 // thread scans Chebyshev rings of cells around its point with a sorted top-k list in registers and
 // stops once the k-th distance is below the distance to any unvisited cell.
+#include <algorithm>
+
 #include "internal.h"
 
 namespace vgicp {
@@ -170,6 +172,45 @@ __global__ void __launch_bounds__(128) cov_knn_kernel(const CovSeg* __restrict__
   }
 }
 
+__device__ __forceinline__ unsigned ord_f(float f) {  // monotone float -> uint
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// Per-cloud bounding box (ordered-uint atomics) and a non-finite flag, for the grid parameters.
+__global__ void cov_bbox_kernel(const CovSeg* __restrict__ segs, const float* __restrict__ xyz,
+                                unsigned* __restrict__ box, int* __restrict__ bad) {
+  const CovSeg s = segs[blockIdx.y];
+  unsigned lo[3] = {~0u, ~0u, ~0u}, hi[3] = {0u, 0u, 0u};
+  int nonfinite = 0;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += gridDim.x * blockDim.x) {
+    const float* p = xyz + 3 * (size_t)(s.offset + i);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = p[a];
+      if (!isfinite(v)) nonfinite = 1;
+      lo[a] = min(lo[a], ord_f(v));
+      hi[a] = max(hi[a], ord_f(v));
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+  }
+  nonfinite = __any_sync(0xffffffffu, nonfinite);
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&box[6 * blockIdx.y + a], lo[a]);
+      atomicMax(&box[6 * blockIdx.y + 3 + a], hi[a]);
+    }
+    if (nonfinite) atomicOr(&bad[blockIdx.y], 1);
+  }
+}
+
 unsigned grid_for_cov(unsigned n, unsigned threads) {
   unsigned g = (n + threads - 1) / threads;
   if (g == 0) g = 1;
@@ -177,6 +218,12 @@ unsigned grid_for_cov(unsigned n, unsigned threads) {
 }
 
 }  // namespace
+
+cudaError_t launch_cov_bbox(const CovSeg* segs, int m, unsigned max_n, const float* xyz, unsigned* box, int* bad,
+                            cudaStream_t s) {
+  cov_bbox_kernel<<<dim3(std::min(grid_for_cov(max_n, 256), 64u), m), 256, 0, s>>>(segs, xyz, box, bad);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_cov_count(const CovSeg* segs, int m, unsigned max_n, const float* xyz, unsigned* cell_of,
                              unsigned* cnt, cudaStream_t s) {

@@ -155,6 +155,8 @@ cudaError_t launch_cloud_fill(const double* xyz, const double* cov9, size_t n, c
 // the same for fp64 host-provided input arrays (already on device)
 cudaError_t launch_transform64(const double* xyz, const double* cov9, size_t n, const double* T, double* out_xyz,
                                double* out_cov9, cudaStream_t s);
+cudaError_t launch_cov_bbox(const CovSeg* segs, int m, unsigned max_n, const float* xyz, unsigned* box, int* bad,
+                            cudaStream_t s);
 cudaError_t launch_cov_count(const CovSeg* segs, int m, unsigned max_n, const float* xyz, unsigned* cell_of,
                              unsigned* cnt, cudaStream_t s);
 cudaError_t launch_cov_scatter(const CovSeg* segs, int m, unsigned max_n, const unsigned* cell_of,

@@ -205,7 +205,7 @@ def estimate_covariances_batch(clouds, k: int = 10, plane_epsilon: float = 1e-3,
     """Covariances of many clouds in one batched GPU pass."""
     ctx = ctx or default_context()
     pts = [np.ascontiguousarray(np.asarray(p, dtype=np.float32).reshape(-1, 3)) for p in clouds]
-    outs = [np.zeros((len(p), 6), np.float32) for p in pts]
+    outs = [np.empty((len(p), 6), np.float32) for p in pts]
     m = len(pts)
     if m == 0:
         return []
