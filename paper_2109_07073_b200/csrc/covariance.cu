@@ -15,7 +15,6 @@ namespace vgicp {
 
 namespace {
 
-constexpr int kMaxK = 32;  // largest supported k (the reference's configs use 10)
 
 __device__ __forceinline__ int cell_axis(double v, double lo, double cell, int g) {
   const int c = static_cast<int>(floor((v - lo) / cell));
@@ -52,48 +51,58 @@ __global__ void cov_scatter_kernel(const CovSeg* __restrict__ segs, const unsign
 }
 
 // Smallest-eigenvalue eigenvector of a symmetric 3×3 (cyclic Jacobi, double), same iteration as
-// the host preprocessing (csrc/host/synthetic.cpp).
-__device__ void smallest_eigenvector(double A[3][3], double v[3]) {
+// the host preprocessing (csrc/host/synthetic.cpp); rotations fully unrolled (register arrays).
+__device__ __forceinline__ void jacobi_rotate(double (&A)[3][3], double (&V)[3][3], int p, int q) {
+  if (A[p][q] == 0.0) return;
+  const double theta = (A[q][q] - A[p][p]) / (2.0 * A[p][q]);
+  const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+  const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double akp = A[k][p], akq = A[k][q];
+    A[k][p] = c * akp - s * akq;
+    A[k][q] = s * akp + c * akq;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double apk = A[p][k], aqk = A[q][k];
+    A[p][k] = c * apk - s * aqk;
+    A[q][k] = s * apk + c * aqk;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double vkp = V[k][p], vkq = V[k][q];
+    V[k][p] = c * vkp - s * vkq;
+    V[k][q] = s * vkp + c * vkq;
+  }
+}
+
+__device__ void smallest_eigenvector(double (&A)[3][3], double v[3]) {
   double V[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
   for (int sweep = 0; sweep < 50; ++sweep) {
     const double off = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
     if (off < 1e-30 * (A[0][0] * A[0][0] + A[1][1] * A[1][1] + A[2][2] * A[2][2]) + 1e-300) break;
-    for (int p = 0; p < 2; ++p)
-      for (int q = p + 1; q < 3; ++q) {
-        if (A[p][q] == 0.0) continue;
-        const double theta = (A[q][q] - A[p][p]) / (2.0 * A[p][q]);
-        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-        for (int k = 0; k < 3; ++k) {
-          const double akp = A[k][p], akq = A[k][q];
-          A[k][p] = c * akp - s * akq;
-          A[k][q] = s * akp + c * akq;
-        }
-        for (int k = 0; k < 3; ++k) {
-          const double apk = A[p][k], aqk = A[q][k];
-          A[p][k] = c * apk - s * aqk;
-          A[q][k] = s * apk + c * aqk;
-        }
-        for (int k = 0; k < 3; ++k) {
-          const double vkp = V[k][p], vkq = V[k][q];
-          V[k][p] = c * vkp - s * vkq;
-          V[k][q] = s * vkp + c * vkq;
-        }
-      }
+    jacobi_rotate(A, V, 0, 1);
+    jacobi_rotate(A, V, 0, 2);
+    jacobi_rotate(A, V, 1, 2);
   }
-  int m = 0;
-  if (A[1][1] < A[m][m]) m = 1;
-  if (A[2][2] < A[m][m]) m = 2;
-  v[0] = V[0][m];
-  v[1] = V[1][m];
-  v[2] = V[2][m];
+  const int m = (A[1][1] < A[0][0]) ? ((A[2][2] < A[1][1]) ? 2 : 1) : ((A[2][2] < A[0][0]) ? 2 : 0);
+  v[0] = m == 0 ? V[0][0] : (m == 1 ? V[0][1] : V[0][2]);
+  v[1] = m == 0 ? V[1][0] : (m == 1 ? V[1][1] : V[1][2]);
+  v[2] = m == 0 ? V[2][0] : (m == 1 ? V[2][1] : V[2][2]);
 }
 
-template <int KM>
+// (d, j) before (bd, bj): ascending distance, ties by lower index (oracles.hpp:24-35)
+__device__ __forceinline__ bool knn_before(double d, unsigned j, double bd, unsigned bj) {
+  return d < bd || (d == bd && j < bj);
+}
+
+// One thread per point; the exact top-K list lives in registers (K is a compile-time constant, the
+// insertion is an unrolled shift network).
+template <int K>
 __global__ void __launch_bounds__(128) cov_knn_kernel(const CovSeg* __restrict__ segs, const float* __restrict__ xyz,
                                                       const unsigned* __restrict__ start,
-                                                      const unsigned* __restrict__ sorted, int k,
-                                                      float* __restrict__ cov6) {
+                                                      const unsigned* __restrict__ sorted, float* __restrict__ cov6) {
   const CovSeg s = segs[blockIdx.y];
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += gridDim.x * blockDim.x) {
     const unsigned g = s.offset + i;
@@ -101,9 +110,10 @@ __global__ void __launch_bounds__(128) cov_knn_kernel(const CovSeg* __restrict__
     const int cx = cell_axis(q0, s.lo[0], s.cell, s.gx);
     const int cy = cell_axis(q1, s.lo[1], s.cell, s.gy);
     const int cz = cell_axis(q2, s.lo[2], s.cell, s.gz);
-    double bd[KM];
-    unsigned bi[KM];
-    int nb = 0;
+    double bd[K];
+    unsigned bi[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) bd[a] = INFINITY, bi[a] = 0xFFFFFFFFu;
     const int rmax = max(s.gx, max(s.gy, s.gz));
     for (int r = 0; r <= rmax; ++r) {
       for (int dx = -r; dx <= r; ++dx) {
@@ -117,48 +127,55 @@ __global__ void __launch_bounds__(128) cov_knn_kernel(const CovSeg* __restrict__
             const int z = cz + dz;
             if (z < 0 || z >= s.gz) continue;
             const unsigned c = s.cell_base + static_cast<unsigned>((x * s.gy + y) * s.gz + z);
-            for (unsigned t = start[c]; t < start[c + 1]; ++t) {
+            const unsigned t1 = start[c + 1];
+            for (unsigned t = start[c]; t < t1; ++t) {
               const unsigned j = sorted[t];
               const double d0 = xyz[3 * (size_t)j] - q0, d1 = xyz[3 * (size_t)j + 1] - q1,
                            d2 = xyz[3 * (size_t)j + 2] - q2;
               const double d = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
               const unsigned jl = j - s.offset;
-              // insert (d, jl) into the sorted top-k list (lexicographic: distance, then index)
-              if (nb == k && !(d < bd[k - 1] || (d == bd[k - 1] && jl < bi[k - 1]))) continue;
-              int pos = nb < k ? nb : k - 1;
-              while (pos > 0 && (d < bd[pos - 1] || (d == bd[pos - 1] && jl < bi[pos - 1]))) {
-                bd[pos] = bd[pos - 1];
-                bi[pos] = bi[pos - 1];
-                --pos;
+              if (!knn_before(d, jl, bd[K - 1], bi[K - 1])) continue;
+#pragma unroll
+              for (int a = K - 1; a > 0; --a) {
+                const bool shift = knn_before(d, jl, bd[a - 1], bi[a - 1]);
+                const bool here = !shift && knn_before(d, jl, bd[a], bi[a]);
+                bd[a] = shift ? bd[a - 1] : (here ? d : bd[a]);
+                bi[a] = shift ? bi[a - 1] : (here ? jl : bi[a]);
               }
-              bd[pos] = d;
-              bi[pos] = jl;
-              if (nb < k) ++nb;
+              if (knn_before(d, jl, bd[0], bi[0])) bd[0] = d, bi[0] = jl;
             }
           }
         }
       }
       // every unvisited point lies at least r·cell away from q
-      if (nb == k && bd[k - 1] <= (r * s.cell) * (r * s.cell)) break;
+      if (bd[K - 1] <= (r * s.cell) * (r * s.cell)) break;
     }
-    // neighbourhood covariance (point_cloud.cpp:62-71) in neighbour-index order
+    // neighbourhood covariance (point_cloud.cpp:62-71) in neighbour order
+    double P[K][3];
     double mean[3] = {0, 0, 0};
-    for (int a = 0; a < nb; ++a) {
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
       const size_t j = s.offset + bi[a];
-      mean[0] += xyz[3 * j];
-      mean[1] += xyz[3 * j + 1];
-      mean[2] += xyz[3 * j + 2];
+      P[a][0] = xyz[3 * j], P[a][1] = xyz[3 * j + 1], P[a][2] = xyz[3 * j + 2];
+      mean[0] += P[a][0];
+      mean[1] += P[a][1];
+      mean[2] += P[a][2];
     }
-    for (int a = 0; a < 3; ++a) mean[a] /= static_cast<double>(nb);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) mean[a] /= static_cast<double>(K);
     double C[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    for (int a = 0; a < nb; ++a) {
-      const size_t j = s.offset + bi[a];
-      const double d[3] = {xyz[3 * j] - mean[0], xyz[3 * j + 1] - mean[1], xyz[3 * j + 2] - mean[2]};
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      const double d[3] = {P[a][0] - mean[0], P[a][1] - mean[1], P[a][2] - mean[2]};
+#pragma unroll
       for (int r = 0; r < 3; ++r)
+#pragma unroll
         for (int c = 0; c < 3; ++c) C[r][c] += d[r] * d[c];
     }
+#pragma unroll
     for (int r = 0; r < 3; ++r)
-      for (int c = 0; c < 3; ++c) C[r][c] /= static_cast<double>(nb);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) C[r][c] /= static_cast<double>(K);
     double v[3];
     smallest_eigenvector(C, v);
     const double w = 1.0 - s.eps;
@@ -240,10 +257,20 @@ cudaError_t launch_cov_scatter(const CovSeg* segs, int m, unsigned max_n, const 
 cudaError_t launch_cov_knn(const CovSeg* segs, int m, unsigned max_n, const float* xyz, const unsigned* start,
                            const unsigned* sorted, int k, float* cov6, cudaStream_t s) {
   const dim3 grid(grid_for_cov(max_n, 128), m);
-  if (k <= 12)
-    cov_knn_kernel<12><<<grid, 128, 0, s>>>(segs, xyz, start, sorted, k, cov6);
-  else
-    cov_knn_kernel<kMaxK><<<grid, 128, 0, s>>>(segs, xyz, start, sorted, k, cov6);
+  switch (k) {
+#define VG_KNN_CASE(K) \
+  case K:              \
+    cov_knn_kernel<K><<<grid, 128, 0, s>>>(segs, xyz, start, sorted, cov6); \
+    break;
+    VG_KNN_CASE(4) VG_KNN_CASE(5) VG_KNN_CASE(6) VG_KNN_CASE(7) VG_KNN_CASE(8) VG_KNN_CASE(9) VG_KNN_CASE(10)
+    VG_KNN_CASE(11) VG_KNN_CASE(12) VG_KNN_CASE(13) VG_KNN_CASE(14) VG_KNN_CASE(15) VG_KNN_CASE(16)
+    VG_KNN_CASE(17) VG_KNN_CASE(18) VG_KNN_CASE(19) VG_KNN_CASE(20) VG_KNN_CASE(21) VG_KNN_CASE(22)
+    VG_KNN_CASE(23) VG_KNN_CASE(24) VG_KNN_CASE(25) VG_KNN_CASE(26) VG_KNN_CASE(27) VG_KNN_CASE(28)
+    VG_KNN_CASE(29) VG_KNN_CASE(30) VG_KNN_CASE(31) VG_KNN_CASE(32)
+#undef VG_KNN_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
