@@ -1403,7 +1403,7 @@ int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, con
     return o;
   };
   const size_t o_cell = carve(sizeof(unsigned) * total);
-  const size_t o_sorted = carve(sizeof(unsigned) * total);
+  const size_t o_sorted = carve(sizeof(float4) * total);
   const size_t o_cnt = carve(sizeof(unsigned) * (cells + 1));
   const size_t o_start = carve(sizeof(unsigned) * (cells + 1));
   const size_t o_cursor = carve(sizeof(unsigned) * cells);
@@ -1414,7 +1414,7 @@ int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, con
   if (int rc = ensure_scratch(ctx, off)) return rc;
   char* sb = static_cast<char*>(ctx->scratch);
   auto* d_cell = reinterpret_cast<unsigned*>(sb + o_cell);
-  auto* d_sorted = reinterpret_cast<unsigned*>(sb + o_sorted);
+  auto* d_sorted = reinterpret_cast<float4*>(sb + o_sorted);
   auto* d_cnt = reinterpret_cast<unsigned*>(sb + o_cnt);
   auto* d_start = reinterpret_cast<unsigned*>(sb + o_start);
   auto* d_cursor = reinterpret_cast<unsigned*>(sb + o_cursor);
@@ -1423,7 +1423,7 @@ int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, con
   VG_CUDA(cudaMemsetAsync(d_cursor, 0, sizeof(unsigned) * cells, s));
   VG_CUDA(launch_cov_count(d_segs, m, max_n, d_xyz, d_cell, d_cnt, s));
   VG_CUDA(cub::DeviceScan::ExclusiveSum(sb + o_temp, scan_bytes, d_cnt, d_start, static_cast<int>(cells + 1), s));
-  VG_CUDA(launch_cov_scatter(d_segs, m, max_n, d_cell, d_start, d_cursor, d_sorted, s));
+  VG_CUDA(launch_cov_scatter(d_segs, m, max_n, d_xyz, d_cell, d_start, d_cursor, d_sorted, s));
   stage("grid");
   VG_CUDA(launch_cov_knn(d_segs, m, max_n, d_xyz, d_start, d_sorted, k, d_cov, s));
   ctx->launches += 5;

@@ -39,14 +39,17 @@ __global__ void cov_count_kernel(const CovSeg* __restrict__ segs, const float* _
   }
 }
 
-__global__ void cov_scatter_kernel(const CovSeg* __restrict__ segs, const unsigned* __restrict__ cell_of,
-                                   const unsigned* __restrict__ start, unsigned* __restrict__ cursor,
-                                   unsigned* __restrict__ sorted) {
+// Cell-ordered copy of the points: (x, y, z, cloud-local index) so that a cell's candidates are one
+// contiguous run of 16-B records (the kNN scan reads them sequentially instead of gathering).
+__global__ void cov_scatter_kernel(const CovSeg* __restrict__ segs, const float* __restrict__ xyz,
+                                   const unsigned* __restrict__ cell_of, const unsigned* __restrict__ start,
+                                   unsigned* __restrict__ cursor, float4* __restrict__ sorted) {
   const CovSeg s = segs[blockIdx.y];
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += gridDim.x * blockDim.x) {
     const unsigned g = s.offset + i;
     const unsigned c = cell_of[g];
-    sorted[start[c] + atomicAdd(&cursor[c], 1u)] = g;
+    const float* p = xyz + 3 * (size_t)g;
+    sorted[start[c] + atomicAdd(&cursor[c], 1u)] = make_float4(p[0], p[1], p[2], __uint_as_float(i));
   }
 }
 
@@ -102,7 +105,7 @@ __device__ __forceinline__ bool knn_before(double d, unsigned j, double bd, unsi
 template <int K>
 __global__ void __launch_bounds__(128) cov_knn_kernel(const CovSeg* __restrict__ segs, const float* __restrict__ xyz,
                                                       const unsigned* __restrict__ start,
-                                                      const unsigned* __restrict__ sorted, float* __restrict__ cov6) {
+                                                      const float4* __restrict__ sorted, float* __restrict__ cov6) {
   const CovSeg s = segs[blockIdx.y];
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n; i += gridDim.x * blockDim.x) {
     const unsigned g = s.offset + i;
@@ -129,11 +132,10 @@ __global__ void __launch_bounds__(128) cov_knn_kernel(const CovSeg* __restrict__
             const unsigned c = s.cell_base + static_cast<unsigned>((x * s.gy + y) * s.gz + z);
             const unsigned t1 = start[c + 1];
             for (unsigned t = start[c]; t < t1; ++t) {
-              const unsigned j = sorted[t];
-              const double d0 = xyz[3 * (size_t)j] - q0, d1 = xyz[3 * (size_t)j + 1] - q1,
-                           d2 = xyz[3 * (size_t)j + 2] - q2;
+              const float4 P = __ldg(sorted + t);
+              const double d0 = P.x - q0, d1 = P.y - q1, d2 = P.z - q2;
               const double d = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
-              const unsigned jl = j - s.offset;
+              const unsigned jl = __float_as_uint(P.w);
               if (!knn_before(d, jl, bd[K - 1], bi[K - 1])) continue;
 #pragma unroll
               for (int a = K - 1; a > 0; --a) {
@@ -248,14 +250,14 @@ cudaError_t launch_cov_count(const CovSeg* segs, int m, unsigned max_n, const fl
   return cudaGetLastError();
 }
 
-cudaError_t launch_cov_scatter(const CovSeg* segs, int m, unsigned max_n, const unsigned* cell_of,
-                               const unsigned* start, unsigned* cursor, unsigned* sorted, cudaStream_t s) {
-  cov_scatter_kernel<<<dim3(grid_for_cov(max_n, 256), m), 256, 0, s>>>(segs, cell_of, start, cursor, sorted);
+cudaError_t launch_cov_scatter(const CovSeg* segs, int m, unsigned max_n, const float* xyz, const unsigned* cell_of,
+                               const unsigned* start, unsigned* cursor, float4* sorted, cudaStream_t s) {
+  cov_scatter_kernel<<<dim3(grid_for_cov(max_n, 256), m), 256, 0, s>>>(segs, xyz, cell_of, start, cursor, sorted);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cov_knn(const CovSeg* segs, int m, unsigned max_n, const float* xyz, const unsigned* start,
-                           const unsigned* sorted, int k, float* cov6, cudaStream_t s) {
+                           const float4* sorted, int k, float* cov6, cudaStream_t s) {
   const dim3 grid(grid_for_cov(max_n, 128), m);
   switch (k) {
 #define VG_KNN_CASE(K) \

@@ -159,10 +159,10 @@ cudaError_t launch_cov_bbox(const CovSeg* segs, int m, unsigned max_n, const flo
                             cudaStream_t s);
 cudaError_t launch_cov_count(const CovSeg* segs, int m, unsigned max_n, const float* xyz, unsigned* cell_of,
                              unsigned* cnt, cudaStream_t s);
-cudaError_t launch_cov_scatter(const CovSeg* segs, int m, unsigned max_n, const unsigned* cell_of,
-                               const unsigned* start, unsigned* cursor, unsigned* sorted, cudaStream_t s);
+cudaError_t launch_cov_scatter(const CovSeg* segs, int m, unsigned max_n, const float* xyz, const unsigned* cell_of,
+                               const unsigned* start, unsigned* cursor, float4* sorted, cudaStream_t s);
 cudaError_t launch_cov_knn(const CovSeg* segs, int m, unsigned max_n, const float* xyz, const unsigned* start,
-                           const unsigned* sorted, int k, float* cov6, cudaStream_t s);
+                           const float4* sorted, int k, float* cov6, cudaStream_t s);
 
 }  // namespace vgicp
 
