@@ -103,6 +103,37 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------------ CPU reference
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_serial_run(scans, links, budget_s: float, resolution: float = 1.0):
+    """The serial reference:: path (reference.cpp:39-110: plain sums, cofactor inverse) on ONE
+    core over `links` until the budget is spent. Returns (factors_done, seconds)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_ctypes as O
+
+    maps, done, elapsed = {}, 0, 0.0
+    for (i, j) in links:
+        if i not in maps:
+            maps[i] = O.OracleMap(scans.means[i].astype(np.float64), O.cov9(scans.cov6[i].astype(np.float64)),
+                                  resolution, serial=True)
+        sm, sc = scans.means[j].astype(np.float64), O.cov9(scans.cov6[j].astype(np.float64))
+        t0 = time.perf_counter()
+        O.linearize(sm, sc, maps[i], scans.odom[i], scans.odom[j], serial=True)
+        elapsed += time.perf_counter() - t0
+        done += 1
+        if elapsed >= budget_s:
+            break
+    return done, elapsed
+
+
 def cpu_reference_run(scans, links, threads: int, budget_s: float, resolution: float = 1.0, max_factors=None):
     """Time the oracle port (parallel ExecPolicy{threads, false}) over `links` until the budget
     is spent. Returns (factors_done, seconds, points_done)."""
@@ -193,6 +224,41 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------ C2 LM
+class _OracleGraph:
+    """The LM's factor interface (linearize_all / total_error) served by the CPU oracle port with
+    ExecPolicy{threads, false} — the reference arm of the C2 ms-per-LM-iteration comparison."""
+
+    def __init__(self, wl, threads):
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_ctypes as O
+
+        self.O, self.threads = O, threads
+        self._ij = np.array(wl.links, np.int64).reshape(-1, 2)
+        self.num_poses = len(wl.poses)
+        self.src = {}
+        self.maps = {}
+        for i, j in wl.links:
+            for k in (i, j):
+                if k not in self.src:
+                    self.src[k] = (wl.scans.means[k].astype(np.float64), O.cov9(wl.scans.cov6[k].astype(np.float64)))
+            if i not in self.maps:
+                self.maps[i] = O.OracleMap(*self.src[i], wl.resolution, threads=threads)
+
+    def linearize_raw(self, poses):
+        out = np.zeros((len(self._ij), 121))
+        inl = np.zeros(len(self._ij), np.int32)
+        for f, (i, j) in enumerate(self._ij):
+            r = self.O.linearize(*self.src[j], self.maps[i], poses[i], poses[j], threads=self.threads)
+            out[f], inl[f] = r["raw"], r["inliers"]
+        return out, inl
+
+    def total_error(self, poses):
+        e = 0.0
+        for i, j in self._ij:
+            e += self.O.evaluate(*self.src[j], self.maps[i], poses[i], poses[j], threads=self.threads)[0]
+        return e
+
+
 def run_lm_c2(ctx, threads):
     """BASELINE config C2: 100-frame circle, factors (k-d -> k), d = 1..3 (294 factors), full LM to
     convergence with default LmSettings (optimizer.hpp:12-21). Each iteration = assemble + damped
@@ -204,6 +270,17 @@ def run_lm_c2(ctx, threads):
     LM.optimize(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=2))  # warm-up
     poses, rep = LM.optimize(wl.graph, wl.poses)
     its = sorted(rep.iteration_seconds)
+    cpu = None
+    try:  # the same LM around the CPU oracle port (reference arm of "ms per LM iteration")
+        all_threads = os.cpu_count() or 1
+        og = _OracleGraph(wl, all_threads)
+        _, crep = LM.optimize(og, wl.poses, device_assembly=False, gpu_solve=False)
+        cits = sorted(crep.iteration_seconds)
+        cpu = {"ms_per_lm_iteration_median": 1e3 * cits[len(cits) // 2] if cits else None,
+               "iterations": crep.iterations, "final_error": crep.final_error, "cores": all_threads,
+               "kind": "port", "note": "oracle linearize / evaluate (ExecPolicy{cores, false}) + host banded solve"}
+    except Exception as e:
+        cpu = {"error": str(e)}
     return {
         "factors": wl.num_factors, "poses": len(wl.poses), "iterations": rep.iterations,
         "ms_per_lm_iteration_median": 1e3 * its[len(its) // 2] if its else None,
@@ -211,6 +288,7 @@ def run_lm_c2(ctx, threads):
         "reason": rep.reason,
         "note": "host LM (paper_2109_07073_b200/optimizer.py, banded Cholesky) around one linearize launch per "
                 "accepted step and one error launch per candidate; wall clock incl. H2D/D2H",
+        "cpu_port": cpu,
     }
 
 
@@ -535,7 +613,11 @@ def run_ours(args):
         threads_all = os.cpu_count() or 1
         n, dt, pts = cpu_reference_run(wl.scans, wl.links, threads_all, args.cpu_budget)
         cpu = {"value": n / dt, "unit": UNIT, "cores": threads_all, "kind": "port",
-               "sample": f"first {n} of {F} C3 factors in graph order ({pts} source points, {dt:.1f} s), oracle/ restatement, ExecPolicy{{{threads_all}, false}}"}
+               "sample": f"first {n} of {F} C3 factors in graph order ({pts} source points, {dt:.1f} s), oracle/ restatement, ExecPolicy{{{threads_all}, false}}",
+               "cpu_model": cpu_model()}
+        ns, dts = cpu_serial_run(wl.scans, wl.links, min(args.cpu_budget, 6.0))
+        cpu["serial_reference_path"] = {"value": ns / dts, "unit": UNIT, "cores": 1,
+                                        "sample": f"first {ns} C3 factors, reference:: serial path (reference.cpp:76-110)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
