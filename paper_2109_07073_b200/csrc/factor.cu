@@ -58,9 +58,7 @@ __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, f
 #endif
 constexpr int kILP = VG_ILP;                        // points per lane per tile (independent probes in flight)
 constexpr int kWarpTile = 32 * kILP;           // points per warp per tile
-constexpr int kTile = kFactorThreads * kILP;   // points per CTA tile
 static_assert(kFactorTile % kPointBlock == 0, "work items must start on a point block");
-constexpr int kRedStride = kFactorThreads + 1;  // padded column stride of the reduction transpose
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers --------------------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {

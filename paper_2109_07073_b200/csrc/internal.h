@@ -103,9 +103,12 @@ struct CovSeg {          // covariance preprocessing of one cloud
   double eps;
 };
 
-constexpr int kFactorThreads = 256;
+#ifndef VG_THREADS
+#define VG_THREADS 256
+#endif
+constexpr int kFactorThreads = VG_THREADS;
 constexpr int kFactorWarps = kFactorThreads / 32;
-constexpr int kFactorTile = 512;    // points per CTA tile (kFactorThreads x kILP)
+constexpr int kFactorTile = 512;    // work-item granularity in points (a multiple of the 64-point block)
 constexpr int kDefaultChunk = 20480;  // points per CTA work item (one item per typical 20k-point factor)
 constexpr int kLinAcc = 28;     // Q(6) P(9) Omega(6) b(6) error(1)
 constexpr int kPartialStride = 32;
