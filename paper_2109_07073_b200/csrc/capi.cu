@@ -287,6 +287,15 @@ static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov
   c->pb = reinterpret_cast<float4*>(base + na);
   c->pc = reinterpret_cast<float*>(base + 2 * na);
   c->sblk = reinterpret_cast<PointBlock*>(base + half);
+  for (size_t i = 0; i < n; ++i) {
+    const float* p = xyz + 3 * i;
+    if (!(std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]))) continue;
+    for (int a = 0; a < 3; ++a) {
+      if (c->lo[a] > c->hi[a]) c->lo[a] = c->hi[a] = p[a];
+      c->lo[a] = std::min(c->lo[a], p[a]);
+      c->hi[a] = std::max(c->hi[a], p[a]);
+    }
+  }
   if (n > 0) {
     if (int rc = ensure_pinned(ctx, bytes)) return rc;
     VG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -421,6 +430,7 @@ static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map*
   const size_t o_hot = carve(sizeof(VoxelStats) * total);  // compact hot records (V <= N)
   const size_t o_jobs = carve(sizeof(InsertJob) * m);
   const size_t o_ovf = carve(sizeof(int) * m);
+  const size_t o_cbox = carve(sizeof(int) * 6 * m);
   std::vector<int> offsets(m + 1);
   for (int k = 0; k < m; ++k) offsets[k] = static_cast<int>(segs[k].offset);
   offsets[m] = ntot;
@@ -449,6 +459,7 @@ static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map*
   auto* d_hot = reinterpret_cast<VoxelStats*>(sb + o_hot);
   auto* d_jobs = reinterpret_cast<InsertJob*>(sb + o_jobs);
   auto* d_ovf = reinterpret_cast<int*>(sb + o_ovf);
+  auto* d_cbox = reinterpret_cast<int*>(sb + o_cbox);
   void* d_temp = sb + o_temp;
   cudaStream_t s = ctx->stream;
 
@@ -510,9 +521,13 @@ static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map*
       cleanup();
       return rc;
     }
-    outs[k] = BuildOut{mp->keys, mp->counts, mp->mean64, mp->cov64, hbase[k], 0u};
+    outs[k] = BuildOut{d_cbox + 6 * k, mp->keys, mp->counts, mp->mean64, mp->cov64, hbase[k], 0u};
   }
+  std::vector<int> hbox(6 * m);
+  for (int k = 0; k < m; ++k)
+    for (int a = 0; a < 3; ++a) hbox[6 * k + a] = INT32_MAX, hbox[6 * k + 3 + a] = INT32_MIN;
   cudaError_t e = cudaMemcpyAsync(d_outs, outs.data(), sizeof(BuildOut) * m, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_cbox, hbox.data(), sizeof(int) * 6 * m, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
     e = launch_build_accumulate(d_segs, d_outs, m, max_n, d_k1, d_v1, d_heads, d_vidx, d_hot, s);
   if (e != cudaSuccess) {
@@ -576,13 +591,29 @@ static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map*
     }
     ctx->launches += 1;
   }
-  for (int k = 0; k < m; ++k) out[k] = maps[k];
+  e = cudaMemcpy(hbox.data(), d_cbox, sizeof(int) * 6 * m, cudaMemcpyDeviceToHost);  // stream already idle
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "voxel map bounds");
+  }
+  for (int k = 0; k < m; ++k) {
+    for (int a = 0; a < 3; ++a) maps[k]->cmin[a] = hbox[6 * k + a], maps[k]->cmax[a] = hbox[6 * k + 3 + a];
+    out[k] = maps[k];
+  }
   return VGICP_OK;
 }
 
 int vgicp_voxelmap_build(vgicp_ctx ctx, vgicp_cloud cloud, double resolution, vgicp_map* out) {
   if (!out) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
   return vgicp_voxelmap_build_batch(ctx, &cloud, &resolution, 1, out);
+}
+
+// inverse of the device-side monotone float -> uint map (cloud.cu / covariance.cu bounding boxes)
+static float unordered_host(unsigned u) {
+  const unsigned v = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+  float f;
+  std::memcpy(&f, &v, sizeof(f));
+  return f;
 }
 
 // RAII device buffer for temporaries of the fp64 / submap paths.
@@ -686,7 +717,11 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
     VG_CUDA(cub::DeviceRadixSort::SortPairs(temp, sort_bytes, codes, codes2, idx, perm, static_cast<int>(n), 0, 30, s));
     VG_CUDA(launch_cloud_fill(d_xyz, d_cov9, n, perm, c->pa, c->pb, c->pc, c->sblk, s));
     ctx->launches += 4;
+    unsigned hbox[6];
+    VG_CUDA(cudaMemcpyAsync(hbox, box, sizeof(hbox), cudaMemcpyDeviceToHost, s));
     VG_CUDA(cudaStreamSynchronize(s));
+    if (hbox[0] <= hbox[3])  // at least one finite point
+      for (int a = 0; a < 3; ++a) c->lo[a] = unordered_host(hbox[a]), c->hi[a] = unordered_host(hbox[3 + a]);
   }
   *out = c.release();
   return VGICP_OK;
@@ -849,38 +884,72 @@ int vgicp_voxel_key(double resolution, const double point[3], uint64_t* key) {
 }
 
 // ------------------------------------------------------------------------------------ overlap
+// Conservative, exact culling of an overlap probe: when the axis-aligned box of the transformed
+// cloud (its 8 box corners mapped by T, fp64) misses the map's occupied voxel region grown by one
+// voxel on every side, no point can land in an occupied voxel and the hit count is exactly 0.
+static bool overlap_disjoint(const vgicp_cloud_s* c, const double* T, const vgicp_map_s* m) {
+  if (c->lo[0] > c->hi[0]) return true;  // no finite point: every lookup misses
+  if (m->cmin[0] > m->cmax[0]) return true;
+  double wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int corner = 0; corner < 8; ++corner) {
+    const double p[3] = {(corner & 1) ? c->hi[0] : c->lo[0], (corner & 2) ? c->hi[1] : c->lo[1],
+                         (corner & 4) ? c->hi[2] : c->lo[2]};
+    for (int a = 0; a < 3; ++a) {
+      const double q = T[3 * a] * p[0] + T[3 * a + 1] * p[1] + T[3 * a + 2] * p[2] + T[9 + a];
+      wlo[a] = std::min(wlo[a], q);
+      whi[a] = std::max(whi[a], q);
+    }
+  }
+  for (int a = 0; a < 3; ++a) {
+    const double mlo = (m->cmin[a] - 1.0) * m->res, mhi = (m->cmax[a] + 2.0) * m->res;
+    if (!(whi[a] >= mlo && wlo[a] <= mhi)) return true;
+  }
+  return false;
+}
+
 int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* poses12, const vgicp_map* maps,
                         int m, uint64_t* hits) {
   if (!ctx || (m > 0 && (!clouds || !poses12 || !maps || !hits)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (m <= 0) return VGICP_OK;
-  std::vector<OverlapItem> items(m);
+  const bool no_cull = std::getenv("VGICP_OVERLAP_NOCULL") != nullptr;  // measurement switch (un-culled)
+  std::vector<OverlapItem> items;
+  std::vector<int> live;
+  items.reserve(m);
   unsigned max_n = 0;
   for (int k = 0; k < m; ++k) {
     if (!clouds[k] || !maps[k]) return fail(VGICP_E_INVALID_ARGUMENT, "null cloud or map");
     if (clouds[k]->ctx != ctx || maps[k]->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "handle of another context");
     if (clouds[k]->n == 0) return fail(VGICP_E_INVALID_ARGUMENT, "overlap_rate requires a nonempty cloud");
-    OverlapItem& it = items[k];
+    hits[k] = 0;
+    if (!no_cull && overlap_disjoint(clouds[k], poses12 + 12 * k, maps[k])) continue;
+    OverlapItem it;
     it.blk = clouds[k]->sblk;  // Morton order (hit counts are order-independent)
     it.map = maps[k]->dev();
     std::memcpy(it.T, poses12 + 12 * k, sizeof(double) * 12);
     it.n = static_cast<unsigned>(clouds[k]->n);
     it.pad = 0;
     max_n = std::max(max_n, it.n);
+    items.push_back(it);
+    live.push_back(k);
   }
+  const int ml = static_cast<int>(items.size());
+  if (ml == 0) return VGICP_OK;
   DeviceGuard g(ctx->device);
-  const size_t bi = align_up(sizeof(OverlapItem) * m, 256);
-  if (int rc = ensure_scratch(ctx, bi + sizeof(unsigned long long) * m)) return rc;
+  const size_t bi = align_up(sizeof(OverlapItem) * ml, 256);
+  if (int rc = ensure_scratch(ctx, bi + sizeof(unsigned long long) * ml)) return rc;
   char* sb = static_cast<char*>(ctx->scratch);
   auto* d_items = reinterpret_cast<OverlapItem*>(sb);
   auto* d_hits = reinterpret_cast<unsigned long long*>(sb + bi);
   cudaStream_t s = ctx->stream;
-  VG_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(OverlapItem) * m, cudaMemcpyHostToDevice, s));
-  VG_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long) * m, s));
-  VG_CUDA(launch_overlap(d_items, m, max_n, d_hits, s));
+  std::vector<uint64_t> h(ml);
+  VG_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(OverlapItem) * ml, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long) * ml, s));
+  VG_CUDA(launch_overlap(d_items, ml, max_n, d_hits, s));
   ctx->launches += 1;
-  VG_CUDA(cudaMemcpyAsync(hits, d_hits, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaMemcpyAsync(h.data(), d_hits, sizeof(uint64_t) * ml, cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaStreamSynchronize(s));
+  for (int q = 0; q < ml; ++q) hits[live[q]] = h[q];
   return VGICP_OK;
 }
 
@@ -1292,12 +1361,6 @@ static void parallel_copies(const std::vector<std::tuple<void*, const void*, siz
   for (auto& x : th) x.join();
 }
 
-static float unordered_host(unsigned u) {
-  const unsigned v = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
-  float f;
-  std::memcpy(&f, &v, sizeof(f));
-  return f;
-}
 
 int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, const size_t* n, int m, int k,
                                      double plane_epsilon, float* const* cov6) {

@@ -74,6 +74,7 @@ struct BuildSeg {
 };
 
 struct BuildOut {       // cold fp64 statistics of one map (ascending key order)
+  int* cbox;               // occupied voxel-coordinate bounds (min xyz, max xyz), atomics
   unsigned long long* keys;
   int* counts;
   double* mean64;
@@ -191,6 +192,7 @@ struct vgicp_cloud_s {
   float* pc = nullptr;
   vgicp::PointBlock* sblk = nullptr;  // Morton (Z-order) copy in 64-point blocks: streamed by the factor /
                                // overlap kernels so that consecutive points probe neighbouring voxels
+  float lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};  // bounding box of the finite points (lo > hi: none)
   std::atomic<int> refs{1};
 };
 
@@ -199,6 +201,7 @@ struct vgicp_map_s {
   double res = 1.0;
   double inv_res = 1.0;
   size_t voxels = 0;
+  int cmin[3] = {0, 0, 0}, cmax[3] = {-1, -1, -1};  // occupied voxel-coordinate bounds
   size_t total_points = 0;
   unsigned num_buckets = 0;
   unsigned shift = 0;

@@ -191,6 +191,13 @@ __global__ void build_accumulate_kernel(const BuildSeg* __restrict__ segs, const
       ms[0] = mean[0], ms[1] = mean[1], ms[2] = mean[2];
     }
     const double mean[3] = {ms[0], ms[1], ms[2]};
+    // occupied-region bounds (overlap culling)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int c = static_cast<int>(key_coord(key, a));
+      atomicMin(&o.cbox[a], c);
+      atomicMax(&o.cbox[3 + a], c);
+    }
     // cold fp64 statistics (ascending key order)
     o.keys[v] = key;
     o.counts[v] = count;

@@ -182,6 +182,25 @@ def test_overlap_37_of_100(ctx):  # test_voxelmap.cpp:171-183
     assert V.overlap_hits(qc, [O.IDENTITY], [V.GaussianVoxelMap(mc, 1.0)])[0] == 37
 
 
+def test_overlap_culling_is_exact(ctx):
+    """Probes whose transformed cloud box misses the map's occupied region are culled on the host
+    (hits exactly 0); near, far and grazing probes all match the oracle."""
+    rng = O.Rng(91)
+    means, covs = rng.gaussian_cloud(3000, 10.0)
+    c, m, c9 = gpu_cloud(ctx, means, covs)
+    g = V.GaussianVoxelMap(c, 1.0)
+    omap = O.OracleMap(m, c9, 1.0)
+    rels = [rng.random_pose(0.3, 3.0) for _ in range(20)]
+    for shift in (25.0, 29.0, 31.0, 35.0, 60.0, 1e4):  # around and beyond the map's extent
+        T = rng.random_pose(0.2, 0.0)
+        T[9] = shift
+        rels.append(T)
+    hits = V.overlap_hits([c] * len(rels), rels, [g] * len(rels))
+    for T, h in zip(rels, hits):
+        assert h == O.overlap_hits(m, T, omap)
+    assert hits[-1] == 0
+
+
 def test_overlap_batch_matches_serial(ctx):  # test_reference.cpp:59-69
     rng = O.Rng(82)
     mcl, mcov = rng.gaussian_cloud(3000, 15.0)
