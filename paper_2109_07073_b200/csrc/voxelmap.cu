@@ -301,9 +301,15 @@ __global__ void lookup_kernel(MapDev map, const double* __restrict__ pts, size_t
 // overlap_rate (voxelmap.cpp:119-135), batched: blockIdx.y walks (cloud, pose, map) items,
 // hits are integer-exact (warp-aggregated 64-bit atomics), so the result is exactly hits / N.
 // Each thread keeps kOverlapILP points' bucket pairs in flight (keys first, then all loads).
-constexpr int kOverlapILP = 4;
+#ifndef VG_OV_ILP
+#define VG_OV_ILP 4
+#endif
+#ifndef VG_OV_MINB
+#define VG_OV_MINB 1
+#endif
+constexpr int kOverlapILP = VG_OV_ILP;
 
-__global__ void __launch_bounds__(256) overlap_kernel(const OverlapItem* __restrict__ items, int m,
+__global__ void __launch_bounds__(256, VG_OV_MINB) overlap_kernel(const OverlapItem* __restrict__ items, int m,
                                                       unsigned long long* __restrict__ hits) {
   for (int k = blockIdx.y; k < m; k += gridDim.y) {
     const OverlapItem& it = items[k];
