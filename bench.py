@@ -306,8 +306,8 @@ def run_lm_c3(wl, max_iterations=30):
         "ms_per_lm_iteration_median": 1e3 * its[len(its) // 2] if its else None,
         "ms_total": 1e3 * rep.wall_time_seconds, "initial_error": rep.initial_error, "final_error": rep.final_error,
         "reason": rep.reason,
-        "note": "linearize + device assembly (S+P blocks D2H), dense cuSOLVER Cholesky per damping trial, "
-                "one evaluate launch per candidate; wall clock incl. H2D/D2H",
+        "note": "linearize + device assembly into a device buffer, dense cuSOLVER Cholesky per damping trial "
+                "(system never leaves the GPU), one evaluate launch per candidate; wall clock",
     }
 
 

@@ -180,6 +180,9 @@ int vgicp_graph_evaluate(vgicp_graph graph, const double* poses12, double* error
 int vgicp_graph_assembly_plan(vgicp_graph graph, const uint8_t* fixed, int* num_slots, int* num_pairs, int32_t* pairs);
 int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, double* diag, double* offdiag,
                                     double* rhs);
+/* Device-resident variant (enqueued on the context stream, no synchronisation): d_poses12 and
+ * d_assembled are device memory; d_assembled receives [diag S×36 | offdiag P×36 | rhs S×6]. */
+int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_poses12, double* d_assembled);
 
 /* Device-resident variants: every pointer is device memory of the context's device; the work
  * is enqueued on the context stream and the call returns without synchronising. */

@@ -1264,6 +1264,25 @@ int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, do
   return VGICP_OK;
 }
 
+int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_poses12, double* d_assembled) {
+  if (!graph || !d_poses12) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (!graph->plan) return fail(VGICP_E_INVALID_ARGUMENT, "no assembly plan (call vgicp_graph_assembly_plan)");
+  const int S = graph->num_slots, O = S + graph->num_pairs;
+  if (O > 0 && !d_assembled) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
+  DeviceGuard g(graph->ctx->device);
+  cudaStream_t s = graph->ctx->stream;
+  if (graph->num_items > 0) {
+    VG_CUDA(launch_factor(true, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
+                          graph->d_part_inl, graph->d_counters, graph->d_out, graph->d_out_inl, s));
+    graph->ctx->launches += 1;
+  } else if (graph->num_factors > 0) {
+    VG_CUDA(cudaMemsetAsync(graph->d_out, 0, sizeof(double) * VGICP_LINEARIZED_DOUBLES * graph->num_factors, s));
+  }
+  VG_CUDA(launch_assemble(graph->d_out_ptr, graph->d_contrib, S, O, graph->d_out, d_assembled, s));
+  graph->ctx->launches += O > 0 ? 1 : 0;
+  return VGICP_OK;
+}
+
 // Single-factor entry points: a one-factor graph over poses {target, source}.
 static int single_factor(vgicp_ctx ctx, const vgicp_factor_desc* factor, const double* T_target,
                          const double* T_source, bool linearize, double* out, int32_t* inliers) {

@@ -222,6 +222,9 @@ class _ReducedSolver:
         S = len(diag)
         m = 6 * S
         self.m, self.rhs = m, rhs.reshape(-1)
+        if not isinstance(diag, np.ndarray) and (bandwidth is not None and bandwidth < m // 4 or device is None):
+            diag, off, rhs = diag.cpu().numpy(), off.cpu().numpy(), rhs.cpu().numpy()  # host solvers
+            self.rhs = rhs.reshape(-1)
         self.banded = bandwidth is not None and bandwidth < m // 4
         self.gpu = device is not None and not self.banded and m > 0
         if self.banded:
@@ -244,17 +247,18 @@ class _ReducedSolver:
             import torch
 
             self.torch = torch
+            tens = lambda x: x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x)).to(device)  # noqa: E731
             Hs = torch.zeros((S, 6, S, 6), dtype=torch.float64, device=device)
             s_idx = torch.arange(S, device=device)
-            Hs[s_idx, :, s_idx, :] = torch.from_numpy(np.ascontiguousarray(diag)).to(device)
+            Hs[s_idx, :, s_idx, :] = tens(diag)
             if len(pairs):
                 a = torch.from_numpy(pairs[:, 0].astype(np.int64)).to(device)
                 b = torch.from_numpy(pairs[:, 1].astype(np.int64)).to(device)
-                O = torch.from_numpy(np.ascontiguousarray(off)).to(device)
+                O = tens(off)
                 Hs[a, :, b, :] = O
                 Hs[b, :, a, :] = O.transpose(1, 2)
             self.Hd = Hs.reshape(m, m)
-            self.bd = torch.from_numpy(np.ascontiguousarray(self.rhs)).to(device).reshape(-1, 1)
+            self.bd = tens(rhs).reshape(-1, 1)
             self.dg = torch.diagonal(self.Hd).clone()
         else:
             self.Hr, _ = slot_system(diag, off, pairs, rhs)
@@ -364,7 +368,22 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
     if device_assembly:
         plan = graph.assembly_plan(fixed_mask.astype(np.uint8))
 
+    banded = bandwidth is not None and bandwidth < (6 * int(active.sum())) // 4
+    dev = _gpu_device(graph) if (device_assembly and gpu_solve and not banded) else None
+    if dev is not None:  # device-resident system: no PCIe round trip of the assembled blocks
+        import torch
+
+        S, P = plan.num_slots, len(plan.pairs)
+        d_asm = torch.empty((S + P) * 36 + S * 6, dtype=torch.float64, device=dev)
+        d_poses = torch.empty((n, 12), dtype=torch.float64, device=dev)
+
     def linearize_system():
+        if dev is not None:
+            d_poses.copy_(torch.from_numpy(np.ascontiguousarray(poses)))
+            graph.linearize_assembled_device(d_poses.data_ptr(), d_asm.data_ptr())
+            graph.ctx.synchronize()  # the context stream may differ from torch's current stream
+            return (d_asm[: S * 36].view(S, 6, 6), d_asm[S * 36:(S + P) * 36].view(P, 6, 6),
+                    d_asm[(S + P) * 36:].view(S, 6))
         if device_assembly:
             diag, off, rhs = graph.linearize_assembled(poses)
             return diag, off, rhs
@@ -378,8 +397,7 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
     for it in range(settings.max_iterations):
         t_it = time.perf_counter()
         if device_assembly:
-            solver = _ReducedSolver(*system[:2], plan.pairs, system[2], bandwidth,
-                                    _gpu_device(graph) if gpu_solve else None)
+            solver = _ReducedSolver(*system[:2], plan.pairs, system[2], bandwidth, dev)
         else:
             H, b = system
         accepted = False

@@ -557,10 +557,7 @@ class FactorGraph(_Handle):
     def total_error(self, poses) -> float:
         """Σ factor errors in factor order (total_error, optimizer.cpp:66-75, matching part)."""
         err, _ = self.evaluate(poses)
-        s = 0.0
-        for e in err:
-            s += float(e)
-        return s
+        return float(np.cumsum(err)[-1]) if len(err) else 0.0  # sequential (not pairwise) summation
 
     # ---- device-side normal-equation assembly (block_solver.cpp:14-62) ----
     def assembly_plan(self, fixed) -> "AssemblyPlan":
@@ -593,6 +590,12 @@ class FactorGraph(_Handle):
         return diag.reshape(S, 6, 6), off.reshape(Np, 6, 6), rhs
 
     # device-resident variants (pointers are device addresses, e.g. torch tensor data_ptr())
+    def linearize_assembled_device(self, d_poses: int, d_assembled: int) -> None:
+        """[diag S×36 | offdiag P×36 | rhs S×6] into device memory (enqueued, not synchronised)."""
+        if getattr(self, "_plan", None) is None:
+            raise ValueError("no assembly plan (call assembly_plan first)")
+        check(_lib.load().vgicp_graph_linearize_assembled_device(self._h, C.c_void_p(d_poses), C.c_void_p(d_assembled)))
+
     def linearize_device(self, d_poses: int, d_out: int, d_inliers: int) -> None:
         check(_lib.load().vgicp_graph_linearize_device(self._h, C.c_void_p(d_poses), C.c_void_p(d_out), C.c_void_p(d_inliers)))
 
