@@ -177,6 +177,15 @@ class PointCloud(_Handle):
         self.means = m
         self.cov6 = c
 
+    @classmethod
+    def adopt(cls, ctx: Context, handle: C.c_void_p) -> "PointCloud":
+        """Wrap a device-only cloud handle returned by the C ABI (e.g. the submap cloud)."""
+        cloud = cls.__new__(cls)
+        _Handle.__init__(cloud, ctx, handle)
+        cloud.means = None
+        cloud.cov6 = None
+        return cloud
+
     def size(self) -> int:
         if self.means is not None:
             return len(self.means)
@@ -259,14 +268,7 @@ def build_submap(frames: Sequence[PointCloud], poses, downsample_resolution: flo
     ds, cl, mp = C.c_void_p(), C.c_void_p(), C.c_void_p()
     check(_lib.load().vgicp_submap_build(ctx.handle, hs, _ptr(P), m, float(downsample_resolution), float(map_resolution),
                                          C.byref(ds), C.byref(cl) if want_cloud else None, C.byref(mp)))
-    cloud = None
-    if want_cloud and cl.value:
-        cloud = PointCloud.__new__(PointCloud)
-        _Handle.__init__(cloud, ctx, cl)
-        n = C.c_size_t()
-        check(_lib.load().vgicp_cloud_size(cl, C.byref(n)))
-        cloud.means = None  # device-only (float32 copy of the float64 submap cloud)
-        cloud.cov6 = None
+    cloud = PointCloud.adopt(ctx, cl) if want_cloud and cl.value else None
     downs = GaussianVoxelMap(None, downsample_resolution, _handle=ds, _ctx=ctx) if ds.value else None
     return Submap(cloud, GaussianVoxelMap(None, map_resolution, _handle=mp, _ctx=ctx), downs)
 
