@@ -146,9 +146,19 @@ __device__ __forceinline__ unsigned bucket1(unsigned k0, unsigned k1, unsigned k
   const unsigned group = (h * 0x9E3779B1u) >> (shift + 3);
   return (group << 3) | (k0 & 1u) | ((k1 & 1u) << 1) | ((k2 & 1u) << 2);
 }
+#ifndef VG_B2_LOCAL
+#define VG_B2_LOCAL 0
+#endif
 __device__ __forceinline__ unsigned bucket2(unsigned k0, unsigned k1, unsigned k2, unsigned shift) {
   const unsigned h = (k0 * 2654435761u) ^ (k1 * 2246822519u) ^ (k2 * 3266489917u) ^ 0x5bd1e995u;
+#if VG_B2_LOCAL
+  // the alternative bucket lives in bucket1's 8-bucket group (same 128-B line), never bucket1 itself
+  const unsigned b1 = bucket1(k0, k1, k2, shift);
+  const unsigned r = 1u + ((h ^ (h >> 15)) * 0x85EBCA6Bu >> 29) % 7u;
+  return (b1 & ~7u) | ((b1 + r) & 7u);
+#else
   return ((h ^ (h >> 15)) * 0x85EBCA6Bu) >> shift;
+#endif
 }
 
 // Voxel key of q under resolution r; false when any axis is outside ±2^20 (or NaN). The three
@@ -178,7 +188,11 @@ struct BucketPair {
   uint4 b;
 };
 #ifndef VG_B2_HINT
+#if VG_B2_LOCAL
+#define VG_B2_HINT 0
+#else
 #define VG_B2_HINT 2
+#endif
 #endif
 // bucket2 is a random probe: optionally keep it out of L1 so that the spatially coherent bucket1
 // lines and slot statistics stay resident there.
