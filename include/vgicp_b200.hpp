@@ -176,6 +176,21 @@ class GaussianVoxelMap {
     check(vgicp_voxelmap_lookup(get(), points.data(), out.size(), out.data()));
     return out;
   }
+  // lookup (voxelmap.cpp:106-117) of one point: the populated voxel containing it, or nullptr
+  const GaussianVoxel* lookup(const Vec3& point) const {
+    const std::uint64_t key = lookup(std::vector<double>(point.begin(), point.end()))[0];
+    if (key == VGICP_KEY_MISS) return nullptr;
+    if (cache_.empty()) cache_ = voxels();  // immutable after construction (voxelmap.hpp:27)
+    const auto it = std::lower_bound(cache_.begin(), cache_.end(), key,
+                                     [](const auto& kv, std::uint64_t k) { return kv.first < k; });
+    return it != cache_.end() && it->first == key ? &it->second : nullptr;
+  }
+  // voxel_coord (voxelmap.cpp:45-55); throws std::out_of_range beyond ±2^20 voxels
+  std::array<int, 3> voxel_coord(const Vec3& point) const {
+    const std::uint64_t k = pack_key(resolution(), point);
+    return {static_cast<int>((k >> 42) & 0x1FFFFF) - (1 << 20), static_cast<int>((k >> 21) & 0x1FFFFF) - (1 << 20),
+            static_cast<int>(k & 0x1FFFFF) - (1 << 20)};
+  }
   static std::uint64_t pack_key(double resolution, const Vec3& point) {
     std::uint64_t k = 0;
     check(vgicp_voxel_key(resolution, point.data(), &k));
@@ -188,6 +203,7 @@ class GaussianVoxelMap {
   GaussianVoxelMap(const Context& ctx, vgicp_map m) : ctx_(ctx) { h_.reset(m, [](vgicp_map x) { vgicp_voxelmap_destroy(x); }); }
   Context ctx_;
   std::shared_ptr<vgicp_map_s> h_;
+  mutable std::vector<std::pair<std::uint64_t, GaussianVoxel>> cache_;  // host copy for single lookups
 };
 
 // transform_cloud (point_cloud.cpp:26-42), float64 on the device.

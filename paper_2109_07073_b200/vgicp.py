@@ -353,6 +353,26 @@ class GaussianVoxelMap(_Handle):
         check(_lib.load().vgicp_voxelmap_lookup(self._h, _ptr(p), len(p), _ptr(out)))
         return out
 
+    def lookup_voxel(self, point):
+        """GaussianVoxelMap::lookup (voxelmap.cpp:106-117) of one point: (mean, covariance, count)
+        of the populated voxel containing it, or None (out-of-range and NaN points miss)."""
+        key = int(self.lookup(point)[0])
+        if key == _lib.KEY_MISS:
+            return None
+        keys, counts, means, covs = self._exported()
+        i = int(np.searchsorted(keys, np.uint64(key)))
+        return means[i], covs[i], int(counts[i])
+
+    def _exported(self):
+        if getattr(self, "_export_cache", None) is None:
+            self._export_cache = self.export()  # immutable after construction (voxelmap.hpp:27)
+        return self._export_cache
+
+    def voxel_coord(self, point) -> tuple[int, int, int]:
+        """voxel_coord (voxelmap.cpp:45-55): floor(p / r) per axis; IndexError beyond ±2^20."""
+        k = GaussianVoxelMap.pack_key(self._resolution, point)
+        return tuple(int(((k >> sh) & 0x1FFFFF) - (1 << 20)) for sh in (42, 21, 0))
+
     @staticmethod
     def pack_key(resolution: float, point) -> int:
         """voxel_coord + pack_key (voxelmap.cpp:45-63); IndexError beyond ±2^20 voxels."""

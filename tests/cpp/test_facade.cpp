@@ -37,6 +37,16 @@ int main() {
   for (const auto& kv : map->voxels()) total += kv.second.count;
   REQUIRE(total == static_cast<std::size_t>(n));
 
+  // single-point lookup / voxel_coord (voxelmap.cpp:45-55, 106-117)
+  {
+    const Vec3 p0{xyz[0], xyz[1], xyz[2]};
+    const GaussianVoxel* v = map->lookup(p0);
+    REQUIRE(v != nullptr && v->count >= 1);
+    REQUIRE(map->lookup(Vec3{1e7, 0, 0}) == nullptr);
+    const auto c = map->voxel_coord(p0);
+    REQUIRE(c[0] == static_cast<int>(std::floor(p0[0] / 1.0)) && c[2] == static_cast<int>(std::floor(p0[2] / 1.0)));
+  }
+
   // overlap: self at identity = 1, far = 0 (test_voxelmap.cpp:138-149)
   REQUIRE(overlap_rate(*cloud, Pose::Identity(), *map) == 1.0);
   REQUIRE(overlap_rate(*cloud, Pose::from({1, 0, 0, 0, 1, 0, 0, 0, 1}, {500, 0, 0}), *map) == 0.0);

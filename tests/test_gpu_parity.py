@@ -135,6 +135,26 @@ def test_lookup_matches_oracle_near_faces(ctx, res):
     assert np.array_equal(g.lookup(probes), omap.lookup(probes))
 
 
+def test_single_point_lookup_and_voxel_coord(ctx):  # voxelmap.cpp:45-55, 106-117
+    rng = O.Rng(92)
+    means, covs = rng.gaussian_cloud(2000, 6.0)
+    c, m, c9 = gpu_cloud(ctx, means, covs)
+    g = V.GaussianVoxelMap(c, 0.5)
+    om = O.OracleMap(m, c9, 0.5)
+    ok, ocnt, omean, ocov = om.export()
+    index = {int(k): i for i, k in enumerate(ok)}
+    for p in list(m[:50]) + [rng.vector(10.0) for _ in range(50)] + [np.array([1e7, 0.0, 0.0])]:
+        v = g.lookup_voxel(p)
+        key = int(O.OracleMap.lookup(om, p[None])[0])
+        if key == int(MISS):
+            assert v is None
+        else:
+            i = index[key]
+            assert np.array_equal(v[0], omean[i]) and np.array_equal(v[1], ocov[i]) and v[2] == ocnt[i]
+        if abs(p[0]) < 1e5:
+            assert g.voxel_coord(p) == tuple(int(np.floor(x / 0.5)) for x in p)
+
+
 def test_range_and_invalid(ctx):  # test_voxelmap.cpp:185-188, voxelmap.cpp:67-72
     cloud, _, _ = gpu_cloud(ctx, [[2.0e6, 0, 0]], O.unit_covariances(1))
     with pytest.raises(IndexError):
