@@ -55,3 +55,59 @@ def gather_blocks(local, counts: Sequence[int], dst: int = 0, group=None):
     if rank != dst:
         return None
     return torch.cat([bufs[r][: int(counts[r])] for r in range(world)], dim=0)
+
+
+def all_gather_rows(local, counts: Sequence[int], group=None):
+    """All-gather per-rank [F_r, D] tensors in rank order: every rank gets the [ΣF_r, D] tensor.
+    Pads to max F_r so one collective suffices."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    fmax = max(int(c) for c in counts)
+    D = local.shape[1]
+    send = torch.zeros((fmax, D), dtype=local.dtype, device=local.device)
+    send[: local.shape[0]].copy_(local)
+    bufs = [torch.zeros_like(send) for _ in range(world)]
+    dist.all_gather(bufs, send, group=group)
+    return torch.cat([bufs[r][: int(counts[r])] for r in range(world)], dim=0)
+
+
+class ShardedFactorGraph:
+    """The LM's factor interface (linearize_all / total_error, optimizer.cpp:45-75) over a factor
+    list split into contiguous, point-balanced ranges across ranks.
+
+    Every rank owns a local graph for its range (a FactorGraph on its GPU; clouds and maps are
+    replicated, so no data-path exchange is needed to build it) and runs the SAME LM
+    (optimizer.optimize) on identical inputs: each linearization all-gathers the 121-double blocks
+    and each error evaluation all-gathers the per-factor errors, summed in global factor order on
+    every rank. The LM decisions are therefore identical everywhere (SPMD), and the collectives
+    per LM step are exactly the blocks and the errors — poses never need a broadcast.
+    """
+
+    def __init__(self, local_graph, ij_all, counts: Sequence[int], num_poses: int, group=None, device="cpu"):
+        self.local = local_graph
+        self._ij = np.asarray(ij_all, np.int64).reshape(-1, 2)
+        self.counts = [int(c) for c in counts]
+        self.num_poses = int(num_poses)
+        self.group = group
+        self.device = device
+        if sum(self.counts) != len(self._ij):
+            raise ValueError("per-rank factor counts do not tile the factor list")
+
+    def linearize_raw(self, poses):
+        import torch
+
+        raw, inl = self.local.linearize_raw(poses)
+        local = torch.from_numpy(np.concatenate([np.asarray(raw, np.float64),
+                                                 np.asarray(inl, np.float64)[:, None]], axis=1)).to(self.device)
+        full = all_gather_rows(local, self.counts, self.group).cpu().numpy()
+        return np.ascontiguousarray(full[:, :121]), full[:, 121].astype(np.int32)
+
+    def total_error(self, poses) -> float:
+        import torch
+
+        err, _ = self.local.evaluate(poses)
+        local = torch.from_numpy(np.asarray(err, np.float64).reshape(-1, 1)).to(self.device)
+        full = all_gather_rows(local, self.counts, self.group).cpu().numpy().reshape(-1)
+        return float(np.cumsum(full)[-1]) if len(full) else 0.0  # global factor order, sequential

@@ -1,5 +1,6 @@
-"""Multi-GPU host logic on CPU: balanced factor partition + world_size-2 gloo gather of the
-per-factor blocks to rank 0 (the N>1 path of bench.py)."""
+"""Multi-GPU host logic on CPU: balanced factor partition, world_size-2 gloo gather of the
+per-factor blocks to rank 0 (the N>1 path of bench.py), and the sharded LM with
+the CPU oracle standing in for each rank's GPU graph."""
 import os
 import socket
 
@@ -64,3 +65,134 @@ def test_gloo_gather_world2(F):
         assert p.exitcode == 0
     assert got.shape == (F, D)
     assert np.array_equal(got[:, 0], np.arange(F, dtype=np.float64))
+
+
+class _OracleShard:
+    """A rank's factor range served by the CPU oracle (stand-in for its FactorGraph)."""
+
+    def __init__(self, frames, maps, ij):
+        self.frames, self.maps, self.ij = frames, maps, np.asarray(ij).reshape(-1, 2)
+
+    def linearize_raw(self, poses):
+        import oracle_ctypes as O
+
+        out = np.zeros((len(self.ij), 121))
+        inl = np.zeros(len(self.ij), np.int32)
+        for f, (i, j) in enumerate(self.ij):
+            r = O.linearize(*self.frames[j], self.maps[i], poses[i], poses[j])
+            out[f], inl[f] = r["raw"], r["inliers"]
+        return out, inl
+
+    def evaluate(self, poses):
+        import oracle_ctypes as O
+
+        err = np.zeros(len(self.ij))
+        inl = np.zeros(len(self.ij), np.int32)
+        for f, (i, j) in enumerate(self.ij):
+            err[f], inl[f] = O.evaluate(*self.frames[j], self.maps[i], poses[i], poses[j])
+        return err, inl
+
+
+def _lm_problem():
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    import oracle_ctypes as O
+
+    rng = O.Rng(77)
+    base_m, base_c = rng.gaussian_cloud(1500, 6.0)
+    frames, truth = [], []
+    for k in range(5):
+        T = rng.random_pose(0.02, 0.2) if k else O.IDENTITY.copy()
+        # every frame observes the same structure from its own pose
+        m, c = O.transform_cloud(base_m, base_c, O.inverse(T))
+        frames.append((m.astype(np.float32).astype(np.float64), O.cov9(c.reshape(-1, 9))))
+        truth.append(T)
+    maps = [O.OracleMap(m, c, 1.0) for m, c in frames]
+    ij = [(i, j) for j in range(1, 5) for i in range(j)]
+    init = np.stack([O.compose(T, rng.random_pose(0.01, 0.05)) if k else T for k, T in enumerate(truth)])
+    return frames, maps, ij, init
+
+
+def _lm_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2109_07073_b200 import optimizer as LM
+    from paper_2109_07073_b200.sharding import ShardedFactorGraph
+
+    frames, maps, ij, init = _lm_problem()
+    parts = partition_factors([len(frames[j][0]) for _, j in ij], world)
+    b, e = parts[rank]
+    g = ShardedFactorGraph(_OracleShard(frames, maps, ij[b:e]), ij, [p[1] - p[0] for p in parts], len(init))
+    poses, rep = LM.optimize(g, init, settings=LM.LmSettings(max_iterations=5), device_assembly=False, gpu_solve=False)
+    q.put((rank, poses, rep.iterations, rep.final_error))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_sharded_lm_matches_single_process():
+    from paper_2109_07073_b200 import optimizer as LM
+
+    frames, maps, ij, init = _lm_problem()
+    single = _OracleShard(frames, maps, ij)
+
+    class _Full:
+        _ij = np.asarray(ij)
+        num_poses = len(init)
+
+        def linearize_raw(self, poses):
+            return single.linearize_raw(poses)
+
+        def total_error(self, poses):
+            err, _ = single.evaluate(poses)
+            return float(np.cumsum(err)[-1])
+
+    ref_poses, ref = LM.optimize(_Full(), init, settings=LM.LmSettings(max_iterations=5), device_assembly=False,
+                                 gpu_solve=False)
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, poses, its, err in results:
+        assert its == ref.iterations and err == ref.final_error  # identical decisions on every rank
+        assert np.array_equal(poses, ref_poses)
+
+
+@pytest.mark.gpu
+def test_sharded_graph_with_gpu_factor_graph_world1():
+    """ShardedFactorGraph around a GPU FactorGraph (world size 1, gloo): same LM as the bare graph."""
+    import paper_2109_07073_b200 as V
+    from paper_2109_07073_b200 import optimizer as LM
+    from paper_2109_07073_b200.sharding import ShardedFactorGraph
+
+    frames, maps, ij, init = _lm_problem()
+    ctx = V.default_context(0)
+    clouds = [V.PointCloud(m.astype(np.float32), V.cov6_from(c), ctx) for m, c in frames]
+    gmaps = V.GaussianVoxelMap.build_batch(clouds, 1.0)
+    graph = V.FactorGraph([V.MatchingCostFactor(i, j, clouds[j], gmaps[i]) for i, j in ij], len(init))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        sharded = ShardedFactorGraph(graph, ij, [len(ij)], len(init))
+        p1, r1 = LM.optimize(sharded, init, settings=LM.LmSettings(max_iterations=5), device_assembly=False,
+                             gpu_solve=False)
+        p2, r2 = LM.optimize(graph, init, settings=LM.LmSettings(max_iterations=5), device_assembly=False,
+                             gpu_solve=False)
+    finally:
+        dist.destroy_process_group()
+    assert r1.iterations == r2.iterations and r1.final_error == r2.final_error
+    assert np.array_equal(p1, p2)
