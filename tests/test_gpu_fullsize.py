@@ -92,3 +92,31 @@ def test_c3_maps_bit_exact_sample(c3):
         om = O.OracleMap(m, c, 1.0, threads=4, deterministic=True)
         for x, y in zip(c3.maps[k].export(), om.export()):
             assert np.array_equal(x, y)
+
+
+@pytest.fixture(scope="module")
+def c5():
+    """C5 shape at reduced frame count: 0.5 / 1 / 2 m maps round-robin over overlap-selected links."""
+    ctx = V.default_context(0)
+    return W.build_c5_workload(ctx, W.c5_spec(frames=150))
+
+
+def test_c5_multiresolution_sample_matches_oracle(c5):
+    raw, inl = c5.graph.linearize_raw(c5.poses)
+    err, inl2 = c5.graph.evaluate(c5.poses)
+    assert np.array_equal(inl, inl2)
+    F = c5.num_factors
+    sample = np.linspace(0, F - 1, 15).astype(int)
+    omaps = {}
+    for f in sample:
+        i, j = c5.links[f]
+        res = W.C5_RESOLUTIONS[f % 3]
+        if (i, res) not in omaps:
+            omaps[(i, res)] = O.OracleMap(*oracle_frame(c5, i), res)
+        ref = O.linearize(*oracle_frame(c5, j), omaps[(i, res)], c5.poses[i], c5.poses[j])
+        assert int(inl[f]) == ref["inliers"], (f, res)
+        got = dict(H_ii=raw[f, 0:36].reshape(6, 6), H_ij=raw[f, 36:72].reshape(6, 6), H_jj=raw[f, 72:108].reshape(6, 6),
+                   b_i=raw[f, 108:114], b_j=raw[f, 114:120], error=raw[f, 120])
+        d = rel_block_error(got, ref)
+        assert max(v for k, v in d.items() if k != "error") <= H_TOL, (f, res, d)
+        assert d["error"] <= ERR_TOL, (f, res, d)
