@@ -53,6 +53,9 @@ __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, f
 #ifndef VG_ILP
 #define VG_ILP 2
 #endif
+#ifndef VG_B2_LAZY
+#define VG_B2_LAZY 0  // read bucket2 only when bucket1 is full and misses
+#endif
 #ifndef VG_STAGES
 #define VG_STAGES 2
 #endif
@@ -438,12 +441,50 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
       b2[u] = bucket2(k0, k1, k2, map.shift);
       q0[u] = (float)qd0, q1[u] = (float)qd1, q2[u] = (float)qd2;
     }
+#if VG_B2_LAZY
+    // bucket1 first; the alternative bucket is read only when bucket1 is full and misses (a key
+    // lives in its bucket2 only if its bucket1 was full when it was placed, and slots never empty)
+    int sl[kILP];
+    {
+      uint4 A[kILP];
+#pragma unroll
+      for (int u = 0; u < kILP; ++u) A[u] = __ldg(reinterpret_cast<const uint4*>(map.keys + kBucket * b1[u]));
+      bool need2[kILP];
+      bool any2 = false;
+#pragma unroll
+      for (int u = 0; u < kILP; ++u) {
+        int s1 = -1;
+        s1 = (A[u].x == lo[u] && A[u].y == hi[u]) ? static_cast<int>(kBucket * b1[u]) : s1;
+        s1 = (A[u].z == lo[u] && A[u].w == hi[u]) ? static_cast<int>(kBucket * b1[u] + 1) : s1;
+        sl[u] = s1;
+        need2[u] = ok[u] && s1 < 0 && A[u].y != 0xFFFFFFFFu && A[u].w != 0xFFFFFFFFu;
+        any2 |= need2[u];
+      }
+      if (__any_sync(0xffffffffu, any2)) {
+#pragma unroll
+        for (int u = 0; u < kILP; ++u) {
+          if (need2[u]) {
+            const uint4 B = ldg_bucket2(map.keys + kBucket * b2[u]);
+            int s2 = -1;
+            s2 = (B.x == lo[u] && B.y == hi[u]) ? static_cast<int>(kBucket * b2[u]) : s2;
+            s2 = (B.z == lo[u] && B.w == hi[u]) ? static_cast<int>(kBucket * b2[u] + 1) : s2;
+            sl[u] = s2;
+          }
+        }
+      }
+    }
+#else
     BucketPair bp[kILP];
 #pragma unroll
     for (int u = 0; u < kILP; ++u) bp[u] = load_buckets(map.keys, b1[u], b2[u]);  // always in-bounds
+#endif
 #pragma unroll
     for (int u = 0; u < kILP; ++u) {
+#if VG_B2_LAZY
+      const int s = sl[u];
+#else
       const int s = match_buckets(bp[u], b1[u], b2[u], hi[u], lo[u]);
+#endif
       const bool hit = ok[u] && s >= 0;
       const unsigned ball = __ballot_sync(0xffffffffu, hit);
       if (hit) {
