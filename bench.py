@@ -343,9 +343,16 @@ def run_c5(ctx, steps=10):
     evm = sorted(a.elapsed_time(b) for a, b in ev)[steps // 2]
     pts = g.num_points()
     by_res = {str(r): sum(1 for k in range(F) if W.C5_RESOLUTIONS[k % 3] == r) for r in W.C5_RESOLUTIONS}
+    from paper_2109_07073_b200 import optimizer as LM
+
+    LM.optimize(g, wl.poses, settings=LM.LmSettings(max_iterations=1))  # warm-up (plan, solver)
+    _, rep = LM.optimize(g, wl.poses, settings=LM.LmSettings(max_iterations=10))
+    its = sorted(rep.iteration_seconds)
     out = {"frames": len(wl.clouds), "factors": F, "factors_by_resolution": by_res, "points": int(pts),
            "ms_linearize_kernel": lin, "ms_evaluate_kernel": evm, "factors_per_s": F / (lin * 1e-3),
            "points_per_s": pts / (lin * 1e-3), "inliers": int(d_inl.sum().item()),
+           "lm_ms_per_iteration_median": 1e3 * its[len(its) // 2] if its else None, "lm_iterations": rep.iterations,
+           "lm_reason": rep.reason,
            "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()},
            "note": "single GPU (the BASELINE config names 8xB200); one launch per pass over all resolutions"}
     del wl, g
