@@ -985,19 +985,36 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
       return fail(VGICP_E_INVALID_ARGUMENT, "factor variable index out of range");
   }
   DeviceGuard g(ctx->device);
+  // Work decomposition. Items are one CTA each; a launch runs in ~equal waves of `slots` resident
+  // CTAs. With many factors, the last wave's factors are cut into quarter chunks so the tail wave
+  // is short; with fewer factors than slots, every factor is cut finer so that the launch still
+  // fills the GPU (C1 / C2). VGICP_NO_TAIL_SPLIT=1 keeps uniform chunks.
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  const int slots = 2 * sms;
+  const bool split = std::getenv("VGICP_NO_TAIL_SPLIT") == nullptr;
+  uint64_t total_points = 0;
+  for (int f = 0; f < num_factors; ++f) total_points += factors[f].source->n;
+  auto round_chunk = [](uint64_t c) {
+    return static_cast<int>(std::max<uint64_t>(kFactorTile, (c + kFactorTile - 1) / kFactorTile * kFactorTile));
+  };
+  const int small_chunk = round_chunk(chunk / 4);
+  const int few_chunk =
+      std::min(chunk, round_chunk(total_points / std::max<uint64_t>(1, 2ull * static_cast<uint64_t>(slots))));
   std::vector<FactorDev> fd(num_factors);
   std::vector<WorkItem> items;
   uint64_t points = 0;
   for (int f = 0; f < num_factors; ++f) {
     const vgicp_factor_desc& d = factors[f];
     FactorDev& x = fd[f];
+    const int fchunk = !split ? chunk : (num_factors < slots ? few_chunk : (f >= num_factors - slots ? small_chunk : chunk));
     x.blk = d.source->sblk;  // Morton order: neighbouring lanes probe neighbouring voxels
     x.map = d.target->dev();
     x.n = static_cast<int>(d.source->n);
     x.tgt = d.target_index;
     x.src = d.source_index;
     x.item_begin = static_cast<int>(items.size());
-    for (int b = 0; b < x.n; b += chunk) items.push_back(WorkItem{f, b, std::min(x.n, b + chunk), 0});
+    for (int b = 0; b < x.n; b += fchunk) items.push_back(WorkItem{f, b, std::min(x.n, b + fchunk), 0});
     x.item_count = static_cast<int>(items.size()) - x.item_begin;
     x.pad = 0;
     points += d.source->n;
