@@ -334,6 +334,27 @@ def test_singular_combined_covariance_skipped(ctx):  # factors.cpp:108-110, :39-
     assert 0 < ref["inliers"] < n
 
 
+def test_factor_with_nonfinite_and_out_of_range_source_points(ctx):
+    """Source points that are NaN / Inf or land beyond ±2^20 voxels miss (lookup returns null,
+    voxelmap.cpp:110-112) and are skipped exactly like the oracle — no exception on this path."""
+    rng = O.Rng(93)
+    tm, tc = rng.gaussian_cloud(2000, 5.0)
+    sm, sc = rng.gaussian_cloud(2000, 5.0)
+    sm = sm.copy()
+    sm[::97] = np.nan
+    sm[5::101, 1] = np.inf
+    sm[7::103, 0] = 3.0e6  # beyond 2^20 voxels at 1 m
+    fac, smm, sc9, omap = factor_case(ctx, sm, sc, tm, tc, 1.0)
+    T = O.IDENTITY
+    lin = V.linearize_matching_cost(fac, T, T)
+    ref = O.linearize(smm, sc9, omap, T, T)
+    assert lin.inliers == ref["inliers"] and 0 < lin.inliers < len(sm)
+    d = rel_block_error(lin_dict(lin), ref)
+    assert max(d.values()) <= H_TOL, d
+    err, inl = V.evaluate_matching_cost(fac, T, T)
+    assert inl == ref["inliers"]
+
+
 def test_gicp_error_kat(ctx):  # test_factors.cpp:92-120 (fp64 kernel: bit-exact vs oracle)
     mean = np.array([1.0, 2.0, 3.0])
     half = 0.5 * np.eye(3)
