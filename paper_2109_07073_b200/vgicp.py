@@ -394,7 +394,8 @@ def overlap_hits(clouds, poses, maps) -> np.ndarray:
     """Exact hit counts of m (cloud, pose, map) probes in one launch."""
     maps = list(maps)
     m = len(maps)
-    if isinstance(clouds, PointCloud):
+    single_cloud = isinstance(clouds, PointCloud)
+    if single_cloud:
         clouds = [clouds] * m
     clouds = list(clouds)
     if len(clouds) != m:
@@ -406,9 +407,13 @@ def overlap_hits(clouds, poses, maps) -> np.ndarray:
     if m == 0:
         return hits
     ctx = maps[0].ctx
-    ch = (C.c_void_p * m)(*[c.handle for c in clouds])
-    mh = (C.c_void_p * m)(*[x.handle for x in maps])
-    check(_lib.load().vgicp_overlap_batch(ctx.handle, ch, _ptr(P), mh, m, _ptr(hits)))
+    # handle arrays as uint64 (pointer-sized) numpy arrays: cheap to build for thousands of maps
+    if single_cloud:
+        ch = np.full(m, clouds[0].handle.value, np.uint64)
+    else:
+        ch = np.fromiter((c.handle.value for c in clouds), dtype=np.uint64, count=m)
+    mh = np.fromiter((x.handle.value for x in maps), dtype=np.uint64, count=m)
+    check(_lib.load().vgicp_overlap_batch(ctx.handle, _ptr(ch), _ptr(P), _ptr(mh), m, _ptr(hits)))
     return hits
 
 
