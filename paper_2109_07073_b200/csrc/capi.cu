@@ -945,7 +945,12 @@ int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* 
   std::vector<uint64_t> h(ml);
   VG_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(OverlapItem) * ml, cudaMemcpyHostToDevice, s));
   VG_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long) * ml, s));
-  VG_CUDA(launch_overlap(d_items, ml, max_n, d_hits, s));
+  bool one_cloud = std::getenv("VGICP_OVERLAP_PERITEM") == nullptr;
+  for (int q = 1; q < ml && one_cloud; ++q) one_cloud = items[q].blk == items[0].blk;
+  if (one_cloud && ml > 1)
+    VG_CUDA(launch_overlap_multi(d_items, ml, items[0].n, d_hits, s));
+  else
+    VG_CUDA(launch_overlap(d_items, ml, max_n, d_hits, s));
   ctx->launches += 1;
   VG_CUDA(cudaMemcpyAsync(h.data(), d_hits, sizeof(uint64_t) * ml, cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaStreamSynchronize(s));

@@ -401,6 +401,81 @@ cudaError_t launch_lookup(MapDev map, const double* pts, size_t n, unsigned long
   return cudaGetLastError();
 }
 
+// One cloud against many maps (C4, and every per-frame factor-selection sweep): each thread loads
+// its points ONCE and probes a chunk of kOvMaps maps with them, two maps at a time; per-map hit
+// counts are summed in shared memory (integer atomics, exact) and added to the global count once
+// per CTA.
+constexpr int kOvPoints = 2;   // points per thread
+constexpr int kOvMaps = 32;    // maps per CTA
+
+__global__ void __launch_bounds__(256) overlap_multi_kernel(const OverlapItem* __restrict__ items, int m,
+                                                            unsigned long long* __restrict__ hits) {
+  __shared__ unsigned cnt[kOvMaps];
+  const OverlapItem& it0 = items[0];
+  const unsigned n = it0.n;
+  const PointBlock* __restrict__ blk = it0.blk;
+  const int m0 = blockIdx.y * kOvMaps;
+  const int mc = min(kOvMaps, m - m0);
+  if (threadIdx.x < kOvMaps) cnt[threadIdx.x] = 0;
+  float px[kOvPoints], py[kOvPoints], pz[kOvPoints];
+  bool in[kOvPoints];
+#pragma unroll
+  for (int u = 0; u < kOvPoints; ++u) {
+    const unsigned i = (blockIdx.x * kOvPoints + u) * blockDim.x + threadIdx.x;
+    const unsigned ic = min(i, n - 1);
+    const float4 a = __ldg(&blk[ic / kPointBlock].pa[ic % kPointBlock]);
+    px[u] = a.x, py[u] = a.y, pz[u] = a.z;
+    in[u] = i < n;
+  }
+  __syncthreads();
+  for (int k = 0; k < mc; k += 2) {
+    unsigned hi[2][kOvPoints], lo[2][kOvPoints], b1[2][kOvPoints], b2[2][kOvPoints];
+    bool ok[2][kOvPoints];
+    const MapDev* mp[2];
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const int kk = min(k + w, mc - 1);
+      const OverlapItem& it = items[m0 + kk];
+      mp[w] = &it.map;
+      const MapDev& map = it.map;
+#pragma unroll
+      for (int u = 0; u < kOvPoints; ++u) {
+        double q0, q1, q2, l0, l1, l2;
+        apply_pose_rn(it.T, px[u], py[u], pz[u], q0, q1, q2);
+        unsigned k0 = 0, k1 = 0, k2 = 0;
+        ok[w][u] = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && in[u] && (k + w < mc);
+        pack_key32(k0, k1, k2, hi[w][u], lo[w][u]);
+        b1[w][u] = bucket1(k0, k1, k2, map.shift);
+        b2[w][u] = bucket2(k0, k1, k2, map.shift);
+      }
+    }
+    BucketPair bp[2][kOvPoints];
+#pragma unroll
+    for (int w = 0; w < 2; ++w)
+#pragma unroll
+      for (int u = 0; u < kOvPoints; ++u) bp[w][u] = load_buckets(mp[w]->keys, b1[w][u], b2[w][u]);
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      unsigned c = 0;
+#pragma unroll
+      for (int u = 0; u < kOvPoints; ++u)
+        if (ok[w][u] && match_buckets(bp[w][u], b1[w][u], b2[w][u], hi[w][u], lo[w][u]) >= 0) ++c;
+      c = __reduce_add_sync(0xffffffffu, c);
+      if ((threadIdx.x & 31) == 0 && c) atomicAdd(&cnt[k + w < mc ? k + w : 0], c);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < mc && cnt[threadIdx.x])
+    atomicAdd(&hits[m0 + threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
+}
+
+cudaError_t launch_overlap_multi(const OverlapItem* items, int m, unsigned n, unsigned long long* hits, cudaStream_t s) {
+  if (m <= 0 || n == 0) return cudaSuccess;
+  const dim3 grid((n + 256 * kOvPoints - 1) / (256 * kOvPoints), (m + kOvMaps - 1) / kOvMaps);
+  overlap_multi_kernel<<<grid, 256, 0, s>>>(items, m, hits);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsigned long long* hits, cudaStream_t s) {
   const unsigned gy = m < 65535 ? m : 65535;
   overlap_kernel<<<dim3(grid_for(max_n, 256 * kOverlapILP, 1024), gy), 256, 0, s>>>(items, m, hits);
