@@ -58,6 +58,24 @@ void dfree(vgicp_ctx ctx, void* p) {
   if (p) cudaFreeAsync(p, ctx->stream);
 }
 
+// inverse of the device-side monotone float -> uint map (cloud.cu / covariance.cu bounding boxes)
+static float unordered_host(unsigned u) {
+  const unsigned v = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+  float f;
+  std::memcpy(&f, &v, sizeof(f));
+  return f;
+}
+
+// RAII device buffer for temporaries of the fp64 / submap paths.
+struct DevBuf {  // stream-ordered temporary: freed on the context stream after its last use
+  vgicp_ctx ctx;
+  void* p = nullptr;
+  explicit DevBuf(vgicp_ctx c) : ctx(c) {}
+  cudaError_t alloc(size_t bytes) { return dmalloc(ctx, &p, bytes); }
+  ~DevBuf() { dfree(ctx, p); }
+};
+
+
 int ensure_scratch(vgicp_ctx ctx, size_t bytes) {
   if (ctx->scratch_bytes >= bytes) return VGICP_OK;
   VG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -229,49 +247,16 @@ int vgicp_ctx_launch_count(vgicp_ctx ctx, uint64_t* launches) {
 }
 
 // ------------------------------------------------------------------------------------ clouds
-// Z-order permutation of the points (10 bits per axis over the bounding box). Deterministic:
-// ties keep input order.
-static std::vector<uint32_t> morton_order(const float* xyz, size_t n) {
-  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (size_t i = 0; i < n; ++i)
-    for (int a = 0; a < 3; ++a) {
-      const float v = xyz[3 * i + a];
-      if (std::isfinite(v)) {
-        lo[a] = std::min(lo[a], v);
-        hi[a] = std::max(hi[a], v);
-      }
-    }
-  auto spread = [](uint32_t x) {  // 10 bits -> every third bit
-    x &= 0x3FFu;
-    x = (x | (x << 16)) & 0x030000FFu;
-    x = (x | (x << 8)) & 0x0300F00Fu;
-    x = (x | (x << 4)) & 0x030C30C3u;
-    x = (x | (x << 2)) & 0x09249249u;
-    return x;
-  };
-  std::vector<std::pair<uint32_t, uint32_t>> code(n);
-  for (size_t i = 0; i < n; ++i) {
-    uint32_t c[3];
-    for (int a = 0; a < 3; ++a) {
-      const float ext = hi[a] - lo[a];
-      const float v = xyz[3 * i + a];
-      const float u = (std::isfinite(v) && ext > 0.f) ? (v - lo[a]) / ext : 0.f;
-      c[a] = static_cast<uint32_t>(std::min(1023.f, std::max(0.f, u * 1024.f)));
-    }
-    code[i] = {spread(c[0]) | (spread(c[1]) << 1) | (spread(c[2]) << 2), static_cast<uint32_t>(i)};
-  }
-  std::sort(code.begin(), code.end());
-  std::vector<uint32_t> perm(n);
-  for (size_t i = 0; i < n; ++i) perm[i] = code[i].second;
-  return perm;
-}
-
+// Float32 cloud upload: points (+ the 6 unique covariance entries) are staged through the pinned
+// buffer and the layout is built on the device (cloud.cu): input-order SoA for the builds and the
+// Morton-ordered 64-point blocks (finite bounding box, 10-bit Z-order codes, stable radix sort).
 static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov6, size_t n, vgicp_cloud* out) {
   if (!ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   if (n > 0 && !xyz) return fail(VGICP_E_INVALID_ARGUMENT, "null point array");
   if (n >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "cloud too large (>= 2^31 points)");
   DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->stream;
   auto c = std::make_unique<vgicp_cloud_s>();
   c->ctx = ctx;
   c->n = n;
@@ -280,57 +265,51 @@ static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov
   const size_t nc = align_up(n * sizeof(float), 256);
   const size_t half = na * 2 + nc;
   const size_t nblk = (n + kPointBlock - 1) / kPointBlock;
-  const size_t bytes = std::max<size_t>(half + nblk * sizeof(PointBlock), 256);
-  VG_CUDA(dmalloc(ctx, &c->block, bytes));
+  VG_CUDA(dmalloc(ctx, &c->block, std::max<size_t>(half + nblk * sizeof(PointBlock), 256)));
   char* base = static_cast<char*>(c->block);
   c->pa = reinterpret_cast<float4*>(base);
   c->pb = reinterpret_cast<float4*>(base + na);
   c->pc = reinterpret_cast<float*>(base + 2 * na);
   c->sblk = reinterpret_cast<PointBlock*>(base + half);
-  for (size_t i = 0; i < n; ++i) {
-    const float* p = xyz + 3 * i;
-    if (!(std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]))) continue;
-    for (int a = 0; a < 3; ++a) {
-      if (c->lo[a] > c->hi[a]) c->lo[a] = c->hi[a] = p[a];
-      c->lo[a] = std::min(c->lo[a], p[a]);
-      c->hi[a] = std::max(c->hi[a], p[a]);
-    }
+  if (n == 0) {
+    *out = c.release();
+    return VGICP_OK;
   }
-  if (n > 0) {
-    if (int rc = ensure_pinned(ctx, bytes)) return rc;
-    VG_CUDA(cudaStreamSynchronize(ctx->stream));
-    const std::vector<uint32_t> perm = morton_order(xyz, n);
-    char* h = static_cast<char*>(ctx->pinned);
-    float4* ha = reinterpret_cast<float4*>(h);
-    float4* hb = reinterpret_cast<float4*>(h + na);
-    float* hc = reinterpret_cast<float*>(h + 2 * na);
-    PointBlock* hblk = reinterpret_cast<PointBlock*>(h + half);
-    for (size_t d = 0; d < nblk * kPointBlock; ++d) {
-      const size_t i = d < n ? d : n - 1;  // input order (builds); padded tail repeats the last point
-      const size_t m = d < n ? perm[d] : perm[n - 1];  // Morton order (factor / overlap kernels)
-      float4 a[2], b[2];
-      float cz[2];
-      for (int copy = 0; copy < 2; ++copy) {
-        const size_t j = copy == 0 ? i : m;
-        const float* p = xyz + 3 * j;
-        const float* q = cov6 ? cov6 + 6 * j : nullptr;
-        a[copy] = make_float4(p[0], p[1], p[2], q ? q[0] : 0.f);
-        b[copy] = q ? make_float4(q[1], q[2], q[3], q[4]) : make_float4(0.f, 0.f, 0.f, 0.f);
-        cz[copy] = q ? q[5] : 0.f;
-      }
-      if (d < n) {
-        ha[d] = a[0];
-        hb[d] = b[0];
-        hc[d] = cz[0];
-      }
-      PointBlock& blk = hblk[d / kPointBlock];
-      blk.pa[d % kPointBlock] = a[1];
-      blk.pb[d % kPointBlock] = b[1];
-      blk.pc[d % kPointBlock] = cz[1];
-    }
-    VG_CUDA(cudaMemcpyAsync(c->block, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    VG_CUDA(cudaStreamSynchronize(ctx->stream));
-  }
+  size_t sort_bytes = 0;
+  VG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                          (const unsigned*)nullptr, (unsigned*)nullptr, static_cast<int>(n), 0, 30, s));
+  const size_t b_xyz = align_up(sizeof(float) * 3 * n, 256);
+  const size_t b_cov = c->has_cov ? align_up(sizeof(float) * 6 * n, 256) : 0;
+  const size_t b_vec = align_up(sizeof(unsigned) * n, 256);
+  DevBuf tmp(ctx);
+  VG_CUDA(tmp.alloc(b_xyz + b_cov + 256 + 4 * b_vec + sort_bytes));
+  char* t = static_cast<char*>(tmp.p);
+  auto* d_xyz = reinterpret_cast<float*>(t);
+  auto* d_cov = c->has_cov ? reinterpret_cast<float*>(t + b_xyz) : nullptr;
+  auto* box = reinterpret_cast<unsigned*>(t + b_xyz + b_cov);
+  auto* codes = reinterpret_cast<unsigned*>(t + b_xyz + b_cov + 256);
+  auto* idx = codes + b_vec / sizeof(unsigned);
+  auto* codes2 = idx + b_vec / sizeof(unsigned);
+  auto* perm = codes2 + b_vec / sizeof(unsigned);
+  void* temp = t + b_xyz + b_cov + 256 + 4 * b_vec;
+  if (int rc = ensure_pinned(ctx, b_xyz + b_cov)) return rc;
+  VG_CUDA(cudaStreamSynchronize(s));  // the pinned staging buffer is free
+  char* h = static_cast<char*>(ctx->pinned);
+  std::memcpy(h, xyz, sizeof(float) * 3 * n);
+  if (c->has_cov) std::memcpy(h + b_xyz, cov6, sizeof(float) * 6 * n);
+  VG_CUDA(cudaMemcpyAsync(d_xyz, h, b_xyz + b_cov, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemsetAsync(box, 0xFF, 3 * sizeof(unsigned), s));
+  VG_CUDA(cudaMemsetAsync(box + 3, 0, 3 * sizeof(unsigned), s));
+  VG_CUDA(launch_cloud_bbox(d_xyz, n, box, s));
+  VG_CUDA(launch_cloud_morton(d_xyz, n, box, codes, idx, s));
+  VG_CUDA(cub::DeviceRadixSort::SortPairs(temp, sort_bytes, codes, codes2, idx, perm, static_cast<int>(n), 0, 30, s));
+  VG_CUDA(launch_cloud_fill(d_xyz, d_cov, n, perm, c->pa, c->pb, c->pc, c->sblk, s));
+  ctx->launches += 4;
+  unsigned hbox[6];
+  VG_CUDA(cudaMemcpyAsync(hbox, box, sizeof(hbox), cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  if (hbox[0] <= hbox[3])  // at least one finite point
+    for (int a = 0; a < 3; ++a) c->lo[a] = unordered_host(hbox[a]), c->hi[a] = unordered_host(hbox[3 + a]);
   *out = c.release();
   return VGICP_OK;
 }
@@ -607,25 +586,6 @@ int vgicp_voxelmap_build(vgicp_ctx ctx, vgicp_cloud cloud, double resolution, vg
   if (!out) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
   return vgicp_voxelmap_build_batch(ctx, &cloud, &resolution, 1, out);
 }
-
-// inverse of the device-side monotone float -> uint map (cloud.cu / covariance.cu bounding boxes)
-static float unordered_host(unsigned u) {
-  const unsigned v = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
-  float f;
-  std::memcpy(&f, &v, sizeof(f));
-  return f;
-}
-
-// RAII device buffer for temporaries of the fp64 / submap paths.
-namespace {
-struct DevBuf {  // stream-ordered temporary: freed on the context stream after its last use
-  vgicp_ctx ctx;
-  void* p = nullptr;
-  explicit DevBuf(vgicp_ctx c) : ctx(c) {}
-  cudaError_t alloc(size_t bytes) { return dmalloc(ctx, &p, bytes); }
-  ~DevBuf() { dfree(ctx, p); }
-};
-}  // namespace
 
 int vgicp_voxelmap_build_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, double resolution,
                              vgicp_map* out) {

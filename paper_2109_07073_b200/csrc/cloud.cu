@@ -1,7 +1,7 @@
-// Device-side construction of a float32 cloud from float64 device arrays (the submap cloud of
-// vgicp_submap_build): float32 rounding, input-order SoA for builds, and the Morton-ordered
-// 64-point blocks for the probe kernels — the same layout vgicp_cloud_upload builds on the host
-// (Z-order code of 10 bits per axis over the finite bounding box, ties in input order).
+// Device-side construction of a cloud's layout (every vgicp_cloud_upload, and the submap cloud of
+// vgicp_submap_build from float64 device arrays): input-order SoA for the builds and the
+// Morton-ordered 64-point blocks for the probe kernels (Z-order code of 10 bits per axis over the
+// finite bounding box, stable radix sort: ties in input order).
 #include "internal.h"
 
 namespace vgicp {
@@ -16,7 +16,8 @@ __device__ __forceinline__ float unordered(unsigned u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
 }
 
-__global__ void bbox_kernel(const double* __restrict__ xyz, size_t n, unsigned* __restrict__ box) {
+template <typename T>
+__global__ void bbox_kernel(const T* __restrict__ xyz, size_t n, unsigned* __restrict__ box) {
   unsigned lo[3] = {~0u, ~0u, ~0u}, hi[3] = {0u, 0u, 0u};
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
 #pragma unroll
@@ -44,7 +45,8 @@ __device__ __forceinline__ unsigned spread10(unsigned x) {  // 10 bits -> every 
   return x;
 }
 
-__global__ void morton_kernel(const double* __restrict__ xyz, size_t n, const unsigned* __restrict__ box,
+template <typename T>
+__global__ void morton_kernel(const T* __restrict__ xyz, size_t n, const unsigned* __restrict__ box,
                               unsigned* __restrict__ codes, unsigned* __restrict__ idx) {
   float lo[3], ext[3];
 #pragma unroll
@@ -65,19 +67,49 @@ __global__ void morton_kernel(const double* __restrict__ xyz, size_t n, const un
   }
 }
 
-__global__ void fill_cloud_kernel(const double* __restrict__ xyz, const double* __restrict__ cov9, size_t n,
-                                  const unsigned* __restrict__ perm, float4* __restrict__ pa, float4* __restrict__ pb,
-                                  float* __restrict__ pc, PointBlock* __restrict__ blk, size_t padded) {
+// Source adaptors: float64 points + full 3×3 covariances (submap clouds) or float32 points + the
+// 6 unique covariance entries (uploads; nullptr = raw cloud, zero covariances).
+struct SrcF64 {
+  const double* xyz;
+  const double* cov9;
+  __device__ void get(size_t j, float4& a, float4& b, float& z) const {
+    const double* p = xyz + 3 * j;
+    const double* q = cov9 + 9 * j;
+    a = make_float4((float)p[0], (float)p[1], (float)p[2], (float)q[0]);
+    b = make_float4((float)q[1], (float)q[2], (float)q[4], (float)q[5]);
+    z = (float)q[8];
+  }
+};
+struct SrcF32 {
+  const float* xyz;
+  const float* cov6;
+  __device__ void get(size_t j, float4& a, float4& b, float& z) const {
+    const float* p = xyz + 3 * j;
+    if (cov6) {
+      const float* q = cov6 + 6 * j;
+      a = make_float4(p[0], p[1], p[2], q[0]);
+      b = make_float4(q[1], q[2], q[3], q[4]);
+      z = q[5];
+    } else {
+      a = make_float4(p[0], p[1], p[2], 0.f);
+      b = make_float4(0.f, 0.f, 0.f, 0.f);
+      z = 0.f;
+    }
+  }
+};
+
+template <typename Src>
+__global__ void fill_cloud_kernel(Src src, size_t n, const unsigned* __restrict__ perm, float4* __restrict__ pa,
+                                  float4* __restrict__ pb, float* __restrict__ pc, PointBlock* __restrict__ blk,
+                                  size_t padded) {
   for (size_t d = blockIdx.x * (size_t)blockDim.x + threadIdx.x; d < padded; d += (size_t)gridDim.x * blockDim.x) {
     const size_t dn = d < n ? d : n - 1;
 #pragma unroll
     for (int copy = 0; copy < 2; ++copy) {
       const size_t j = copy == 0 ? dn : perm[dn];
-      const double* p = xyz + 3 * j;
-      const double* q = cov9 + 9 * j;
-      const float4 a = make_float4((float)p[0], (float)p[1], (float)p[2], (float)q[0]);
-      const float4 b = make_float4((float)q[1], (float)q[2], (float)q[4], (float)q[5]);
-      const float z = (float)q[8];
+      float4 a, b;
+      float z;
+      src.get(j, a, b, z);
       if (copy == 0) {
         if (d < n) pa[d] = a, pb[d] = b, pc[d] = z;
       } else {
@@ -101,8 +133,17 @@ cudaError_t launch_cloud_bbox(const double* xyz, size_t n, unsigned* box, cudaSt
   bbox_kernel<<<grid_cloud(n), 256, 0, s>>>(xyz, n, box);
   return cudaGetLastError();
 }
+cudaError_t launch_cloud_bbox(const float* xyz, size_t n, unsigned* box, cudaStream_t s) {
+  bbox_kernel<<<grid_cloud(n), 256, 0, s>>>(xyz, n, box);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_cloud_morton(const double* xyz, size_t n, const unsigned* box, unsigned* codes, unsigned* idx,
+                                cudaStream_t s) {
+  morton_kernel<<<grid_cloud(n), 256, 0, s>>>(xyz, n, box, codes, idx);
+  return cudaGetLastError();
+}
+cudaError_t launch_cloud_morton(const float* xyz, size_t n, const unsigned* box, unsigned* codes, unsigned* idx,
                                 cudaStream_t s) {
   morton_kernel<<<grid_cloud(n), 256, 0, s>>>(xyz, n, box, codes, idx);
   return cudaGetLastError();
@@ -111,7 +152,13 @@ cudaError_t launch_cloud_morton(const double* xyz, size_t n, const unsigned* box
 cudaError_t launch_cloud_fill(const double* xyz, const double* cov9, size_t n, const unsigned* perm, float4* pa,
                               float4* pb, float* pc, PointBlock* blk, cudaStream_t s) {
   const size_t padded = (n + kPointBlock - 1) / kPointBlock * kPointBlock;
-  fill_cloud_kernel<<<grid_cloud(padded), 256, 0, s>>>(xyz, cov9, n, perm, pa, pb, pc, blk, padded);
+  fill_cloud_kernel<<<grid_cloud(padded), 256, 0, s>>>(SrcF64{xyz, cov9}, n, perm, pa, pb, pc, blk, padded);
+  return cudaGetLastError();
+}
+cudaError_t launch_cloud_fill(const float* xyz, const float* cov6, size_t n, const unsigned* perm, float4* pa,
+                              float4* pb, float* pc, PointBlock* blk, cudaStream_t s) {
+  const size_t padded = (n + kPointBlock - 1) / kPointBlock * kPointBlock;
+  fill_cloud_kernel<<<grid_cloud(padded), 256, 0, s>>>(SrcF32{xyz, cov6}, n, perm, pa, pb, pc, blk, padded);
   return cudaGetLastError();
 }
 

@@ -158,6 +158,11 @@ cudaError_t launch_cloud_morton(const double* xyz, size_t n, const unsigned* box
                                 cudaStream_t s);
 cudaError_t launch_cloud_fill(const double* xyz, const double* cov9, size_t n, const unsigned* perm, float4* pa,
                               float4* pb, float* pc, PointBlock* blk, cudaStream_t s);
+cudaError_t launch_cloud_bbox(const float* xyz, size_t n, unsigned* box, cudaStream_t s);
+cudaError_t launch_cloud_morton(const float* xyz, size_t n, const unsigned* box, unsigned* codes, unsigned* idx,
+                                cudaStream_t s);
+cudaError_t launch_cloud_fill(const float* xyz, const float* cov6, size_t n, const unsigned* perm, float4* pa,
+                              float4* pb, float* pc, PointBlock* blk, cudaStream_t s);
 // the same for fp64 host-provided input arrays (already on device)
 cudaError_t launch_transform64(const double* xyz, const double* cov9, size_t n, const double* T, double* out_xyz,
                                double* out_cov9, cudaStream_t s);
