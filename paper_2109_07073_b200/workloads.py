@@ -32,6 +32,17 @@ def pose_inv(T):
     return np.concatenate([Rt.reshape(9), -(Rt @ T[9:])])
 
 
+def relative_poses(poses, pairs) -> np.ndarray:
+    """T_i⁻¹·T_j for every (i, j) pair, vectorised (12-double poses)."""
+    P = np.asarray(poses, np.float64)
+    I = np.fromiter((p[0] for p in pairs), dtype=np.int64, count=len(pairs))
+    J = np.fromiter((p[1] for p in pairs), dtype=np.int64, count=len(pairs))
+    Rs = P[:, :9].reshape(-1, 3, 3)
+    R = np.einsum("kba,kbc->kac", Rs[I], Rs[J])  # R_iᵀ R_j
+    t = np.einsum("kba,kb->ka", Rs[I], P[J, 9:] - P[I, 9:])  # R_iᵀ (t_j - t_i)
+    return np.ascontiguousarray(np.concatenate([R.reshape(-1, 9), t], axis=1))
+
+
 def pose_mul(A, B):
     A = np.asarray(A, np.float64)
     B = np.asarray(B, np.float64)
@@ -126,7 +137,7 @@ def build_graph_workload(ctx: Context, spec: S.SceneSpec, resolution: float = 1.
     n = len(clouds)
     if links is None:
         pairs = [(i, j) for j in range(1, n) for i in range(j)]
-        rels = [pose_mul(pose_inv(scans.gt[i]), scans.gt[j]) for i, j in pairs]  # pipeline.cpp:138
+        rels = relative_poses(scans.gt, pairs)  # T_i⁻¹·T_j, pipeline.cpp:138
         hits = overlap_hits([clouds[j] for _, j in pairs], rels, [maps[i] for i, _ in pairs])
         overlaps = {p: float(h) / len(scans.means[p[1]]) for p, h in zip(pairs, hits)}
         links = select_links(overlaps, n, max_links, min_overlap)
@@ -164,15 +175,8 @@ def build_c5_workload(ctx: Context, spec: S.SceneSpec | None = None, max_links: 
     t2 = time.perf_counter()
     n = len(clouds)
     pairs = [(i, j) for j in range(1, n) for i in range(j)]
-    gt = np.asarray(scans.gt)
-    Rs = gt[:, :9].reshape(-1, 3, 3)
-    ts = gt[:, 9:]
-    I = np.array([p[0] for p in pairs])
-    J = np.array([p[1] for p in pairs])
-    R = np.einsum("kba,kbc->kac", Rs[I], Rs[J])  # R_iᵀ R_j
-    t = np.einsum("kba,kb->ka", Rs[I], ts[J] - ts[I])  # R_iᵀ (t_j - t_i)
-    rels = np.concatenate([R.reshape(-1, 9), t], axis=1)
-    hits = overlap_hits([clouds[j] for j in J], rels, [maps[1.0][i] for i in I])
+    rels = relative_poses(scans.gt, pairs)
+    hits = overlap_hits([clouds[j] for _, j in pairs], rels, [maps[1.0][i] for i, _ in pairs])
     overlaps = {p: float(h) / len(scans.means[p[1]]) for p, h in zip(pairs, hits)}
     links = select_links(overlaps, n, max_links, min_overlap)
     t3 = time.perf_counter()
