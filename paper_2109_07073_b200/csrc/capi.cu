@@ -895,25 +895,43 @@ int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* 
   }
   const int ml = static_cast<int>(items.size());
   if (ml == 0) return VGICP_OK;
+  // group the probes by cloud (stable): every chunk of <= 32 maps shares one cloud, whose points
+  // each thread loads once
+  std::vector<int> order(ml);
+  for (int q = 0; q < ml; ++q) order[q] = q;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return items[a].blk < items[b].blk; });
+  std::vector<OverlapItem> sorted(ml);
+  std::vector<int2> chunks;
+  for (int q = 0; q < ml; ++q) {
+    sorted[q] = items[order[q]];
+    if (q == 0 || sorted[q].blk != sorted[q - 1].blk || chunks.back().y == kOverlapMapsPerChunk)
+      chunks.push_back(make_int2(q, 0));
+    ++chunks.back().y;
+  }
+  const bool per_item = std::getenv("VGICP_OVERLAP_PERITEM") != nullptr;  // measurement switch
   DeviceGuard g(ctx->device);
   const size_t bi = align_up(sizeof(OverlapItem) * ml, 256);
-  if (int rc = ensure_scratch(ctx, bi + sizeof(unsigned long long) * ml)) return rc;
+  const size_t bc = align_up(sizeof(int2) * chunks.size(), 256);
+  if (int rc = ensure_scratch(ctx, bi + bc + sizeof(unsigned long long) * ml)) return rc;
   char* sb = static_cast<char*>(ctx->scratch);
   auto* d_items = reinterpret_cast<OverlapItem*>(sb);
-  auto* d_hits = reinterpret_cast<unsigned long long*>(sb + bi);
+  auto* d_chunks = reinterpret_cast<int2*>(sb + bi);
+  auto* d_hits = reinterpret_cast<unsigned long long*>(sb + bi + bc);
   cudaStream_t s = ctx->stream;
   std::vector<uint64_t> h(ml);
-  VG_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(OverlapItem) * ml, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemcpyAsync(d_items, sorted.data(), sizeof(OverlapItem) * ml, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemcpyAsync(d_chunks, chunks.data(), sizeof(int2) * chunks.size(), cudaMemcpyHostToDevice, s));
   VG_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long) * ml, s));
-  bool one_cloud = std::getenv("VGICP_OVERLAP_PERITEM") == nullptr;
-  for (int q = 1; q < ml && one_cloud; ++q) one_cloud = items[q].blk == items[0].blk;
-  if (one_cloud && ml > 1)
-    VG_CUDA(launch_overlap_multi(d_items, ml, items[0].n, d_hits, s));
-  else
+  if (per_item)
     VG_CUDA(launch_overlap(d_items, ml, max_n, d_hits, s));
+  else
+    VG_CUDA(launch_overlap_multi(d_items, d_chunks, static_cast<int>(chunks.size()), max_n, d_hits, s));
   ctx->launches += 1;
   VG_CUDA(cudaMemcpyAsync(h.data(), d_hits, sizeof(uint64_t) * ml, cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint64_t> hu(ml);
+  for (int q = 0; q < ml; ++q) hu[order[q]] = h[q];
+  h.swap(hu);
   for (int q = 0; q < ml; ++q) hits[live[q]] = h[q];
   return VGICP_OK;
 }

@@ -132,8 +132,11 @@ cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkIt
                           const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
                           int* out_inl, cudaStream_t s);
 cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s);
-// every item shares items[0]'s cloud (blk, n): points loaded once per thread, many maps probed
-cudaError_t launch_overlap_multi(const OverlapItem* items, int m, unsigned n, unsigned long long* hits, cudaStream_t s);
+// overlap probes grouped by cloud: chunk = (first item, count <= kOverlapMapsPerChunk) of items that
+// share one cloud; each thread loads its points once and probes the chunk's maps
+constexpr int kOverlapMapsPerChunk = 32;
+cudaError_t launch_overlap_multi(const OverlapItem* items, const int2* chunks, int num_chunks, unsigned max_n,
+                                 unsigned long long* hits, cudaStream_t s);
 // assemble_normal_equations (block_solver.cpp:14-62) from F×121 factor blocks: output o < S is
 // slot o's diagonal block (+ rhs), o >= S the off-diagonal pair o - S; contrib codes f·4 + kind
 // (0 H_ii/b_i, 1 H_jj/b_j, 2 H_ij, 3 H_ijᵀ) listed per output in factor order.

@@ -406,16 +406,19 @@ cudaError_t launch_lookup(MapDev map, const double* pts, size_t n, unsigned long
 // counts are summed in shared memory (integer atomics, exact) and added to the global count once
 // per CTA.
 constexpr int kOvPoints = 2;   // points per thread
-constexpr int kOvMaps = 32;    // maps per CTA
+constexpr int kOvMaps = kOverlapMapsPerChunk;  // maps per CTA
 
-__global__ void __launch_bounds__(256) overlap_multi_kernel(const OverlapItem* __restrict__ items, int m,
+__global__ void __launch_bounds__(256) overlap_multi_kernel(const OverlapItem* __restrict__ items,
+                                                            const int2* __restrict__ chunks,
                                                             unsigned long long* __restrict__ hits) {
   __shared__ unsigned cnt[kOvMaps];
-  const OverlapItem& it0 = items[0];
+  const int2 ch = chunks[blockIdx.y];  // (first item, count <= kOvMaps), one cloud per chunk
+  const OverlapItem& it0 = items[ch.x];
   const unsigned n = it0.n;
+  if (blockIdx.x * blockDim.x * kOvPoints >= n) return;
   const PointBlock* __restrict__ blk = it0.blk;
-  const int m0 = blockIdx.y * kOvMaps;
-  const int mc = min(kOvMaps, m - m0);
+  const int m0 = ch.x;
+  const int mc = ch.y;
   if (threadIdx.x < kOvMaps) cnt[threadIdx.x] = 0;
   float px[kOvPoints], py[kOvPoints], pz[kOvPoints];
   bool in[kOvPoints];
@@ -469,10 +472,13 @@ __global__ void __launch_bounds__(256) overlap_multi_kernel(const OverlapItem* _
     atomicAdd(&hits[m0 + threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
 }
 
-cudaError_t launch_overlap_multi(const OverlapItem* items, int m, unsigned n, unsigned long long* hits, cudaStream_t s) {
-  if (m <= 0 || n == 0) return cudaSuccess;
-  const dim3 grid((n + 256 * kOvPoints - 1) / (256 * kOvPoints), (m + kOvMaps - 1) / kOvMaps);
-  overlap_multi_kernel<<<grid, 256, 0, s>>>(items, m, hits);
+cudaError_t launch_overlap_multi(const OverlapItem* items, const int2* chunks, int num_chunks, unsigned max_n,
+                                 unsigned long long* hits, cudaStream_t s) {
+  if (num_chunks <= 0 || max_n == 0) return cudaSuccess;
+  for (int c0 = 0; c0 < num_chunks; c0 += 65535) {  // grid.y limit
+    const dim3 grid((max_n + 256 * kOvPoints - 1) / (256 * kOvPoints), std::min(65535, num_chunks - c0));
+    overlap_multi_kernel<<<grid, 256, 0, s>>>(items, chunks + c0, hits);
+  }
   return cudaGetLastError();
 }
 
