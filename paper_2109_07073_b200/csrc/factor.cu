@@ -423,13 +423,15 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
 #pragma unroll
     for (int q = 0; q < 12; ++q) Tr[q] = T[q];
     unsigned hi[kILP], lo[kILP], b1[kILP], b2[kILP];
-    float l0[kILP], l1[kILP], l2[kILP], q0[kILP], q1[kILP], q2[kILP];
+    float l0[kILP], l1[kILP], l2[kILP], q0[kILP], q1[kILP], q2[kILP], cxx[kILP];
     bool ok[kILP];
 #pragma unroll
     for (int u = 0; u < kILP; ++u) {
       const int p = u * 32 + lane;
       const int lp = min(p, tile_n - 1);  // clamped: every lane computes, in-range lanes count
       const float4 A = tb.pa[lp];
+      cxx[u] = A.w;  // error-only pass: kept in a register (the strided .w re-read at append time is
+                     // a 4-way bank conflict); the linearize pass re-reads it (no registers to spare)
       double qd0, qd1, qd2;
       apply_pose_rn(Tr, A.x, A.y, A.z, qd0, qd1, qd2);
       unsigned k0 = 0, k1 = 0, k2 = 0;
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
         const unsigned idx = (tail + __popc(ball & lane_lt)) % static_cast<unsigned>(kQueue);
         const float4 B = tb.pb[p];
         hq.a[idx] = make_float4(l0[u], l1[u], l2[u], q0[u]);
-        hq.b[idx] = make_float4(q1[u], q2[u], __int_as_float(s), tb.pa[p].w);
+        hq.b[idx] = make_float4(q1[u], q2[u], __int_as_float(s), kLinearize ? tb.pa[p].w : cxx[u]);
         hq.c[idx] = B;
         hq.d[idx] = tb.pc[p];
       }
