@@ -183,6 +183,12 @@ int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, do
 /* Device-resident variant (enqueued on the context stream, no synchronisation): d_poses12 and
  * d_assembled are device memory; d_assembled receives [diag S×36 | offdiag P×36 | rhs S×6]. */
 int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_poses12, double* d_assembled);
+/* Per-factor errors and inliers of the most recent vgicp_graph_linearize_assembled[_device] pass
+ * (the `error` / `inliers` members of each LinearizedFactor, factors.hpp:27-28), synchronous.
+ * They equal vgicp_graph_evaluate at the same poses bit for bit (same per-point arithmetic and
+ * reduction order), so an LM can score a candidate with the linearization it needs anyway if the
+ * candidate is accepted (total_error, optimizer.cpp:66-75 + linearize_all, :45-62). */
+int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* inliers);
 
 /* Device-resident variants: every pointer is device memory of the context's device; the work
  * is enqueued on the context stream and the call returns without synchronising. */

@@ -1110,15 +1110,16 @@ int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, doub
   return VGICP_OK;
 }
 
-// True when `p` is page-locked host memory (cudaHostAlloc / cudaHostRegister / torch pin_memory):
-// copies can then target it directly instead of going through the context's pinned staging.
-static bool is_pinned(const void* p) {
+// Device-visible alias of `p` when it is page-locked host memory (cudaHostAlloc / cudaHostRegister /
+// torch pin_memory; under UVA all of them are mapped), else null. Results can then be written by the
+// kernel straight into the caller's buffer over PCIe, overlapping the D2H with the launch.
+static void* mapped_alias(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
-    return false;
+    return nullptr;
   }
-  return a.type == cudaMemoryTypeHost;
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
 }
 
 static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses12, double* out, int32_t* inliers) {
@@ -1132,23 +1133,36 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
   const size_t pose_bytes = sizeof(double) * 12 * graph->num_poses;
   const size_t res_bytes = linearize ? sizeof(double) * VGICP_LINEARIZED_DOUBLES * nf : sizeof(double) * nf;
   const size_t inl_bytes = sizeof(int32_t) * nf;
-  const bool direct = is_pinned(out) && is_pinned(inliers);
-  if (int rc = ensure_pinned(ctx, align_up(pose_bytes, 256) + (direct ? 0 : align_up(res_bytes, 256) + inl_bytes)))
+  // Page-locked caller buffers: the kernel's epilogue stores each factor's block directly into host
+  // memory (zero-copy), so the result transfer overlaps the launch instead of following it.
+  // VGICP_E2E_STAGED=1 keeps the copy-after-kernel path (for measurement).
+  static const bool staged_only = [] {
+    const char* e = std::getenv("VGICP_E2E_STAGED");
+    return e && e[0] == '1';
+  }();
+  double* m_res = staged_only ? nullptr : static_cast<double*>(mapped_alias(out));
+  auto* m_inl = staged_only ? nullptr : static_cast<int32_t*>(mapped_alias(inliers));
+  const bool zero_copy = m_res && m_inl;
+  if (int rc = ensure_pinned(ctx, align_up(pose_bytes, 256) + (zero_copy ? 0 : align_up(res_bytes, 256) + inl_bytes)))
     return rc;
   char* h = static_cast<char*>(ctx->pinned);
   double* h_poses = reinterpret_cast<double*>(h);
-  double* h_res = direct ? out : reinterpret_cast<double*>(h + align_up(pose_bytes, 256));
-  auto* h_inl = direct ? inliers : reinterpret_cast<int32_t*>(h + align_up(pose_bytes, 256) + align_up(res_bytes, 256));
-  std::memcpy(h_poses, poses12, pose_bytes);
-  VG_CUDA(cudaMemcpyAsync(graph->d_poses, h_poses, pose_bytes, cudaMemcpyHostToDevice, s));
-  double* d_res = linearize ? graph->d_out : graph->d_err;
+  double* h_res = reinterpret_cast<double*>(h + align_up(pose_bytes, 256));
+  auto* h_inl = reinterpret_cast<int32_t*>(h + align_up(pose_bytes, 256) + align_up(res_bytes, 256));
+  const bool poses_pinned = mapped_alias(poses12) != nullptr;
+  if (!poses_pinned) std::memcpy(h_poses, poses12, pose_bytes);
+  VG_CUDA(cudaMemcpyAsync(graph->d_poses, poses_pinned ? poses12 : h_poses, pose_bytes, cudaMemcpyHostToDevice, s));
+  double* d_res = zero_copy ? m_res : (linearize ? graph->d_out : graph->d_err);
+  int32_t* d_inl = zero_copy ? m_inl : graph->d_out_inl;
   VG_CUDA(launch_factor(linearize, graph->d_factors, graph->d_items, graph->num_items, graph->d_poses,
-                        graph->d_partials, graph->d_part_inl, graph->d_counters, d_res, graph->d_out_inl, s));
+                        graph->d_partials, graph->d_part_inl, graph->d_counters, d_res, d_inl, s));
   ctx->launches += 1;
-  VG_CUDA(cudaMemcpyAsync(h_res, d_res, res_bytes, cudaMemcpyDeviceToHost, s));
-  VG_CUDA(cudaMemcpyAsync(h_inl, graph->d_out_inl, inl_bytes, cudaMemcpyDeviceToHost, s));
+  if (!zero_copy) {
+    VG_CUDA(cudaMemcpyAsync(h_res, d_res, res_bytes, cudaMemcpyDeviceToHost, s));
+    VG_CUDA(cudaMemcpyAsync(h_inl, d_inl, inl_bytes, cudaMemcpyDeviceToHost, s));
+  }
   VG_CUDA(cudaStreamSynchronize(s));
-  if (!direct) {
+  if (!zero_copy) {
     std::memcpy(out, h_res, res_bytes);
     std::memcpy(inliers, h_inl, inl_bytes);
   }
@@ -1280,6 +1294,28 @@ int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_po
   }
   VG_CUDA(launch_assemble(graph->d_out_ptr, graph->d_contrib, S, O, graph->d_out, d_assembled, s));
   graph->ctx->launches += O > 0 ? 1 : 0;
+  return VGICP_OK;
+}
+
+int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* inliers) {
+  if (!graph || (graph->num_factors > 0 && (!errors || !inliers)))
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  const int nf = graph->num_factors;
+  if (nf == 0) return VGICP_OK;
+  vgicp_ctx ctx = graph->ctx;
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const size_t err_bytes = sizeof(double) * nf;
+  if (int rc = ensure_pinned(ctx, align_up(err_bytes, 256) + sizeof(int32_t) * nf)) return rc;
+  auto* h_err = static_cast<double*>(ctx->pinned);
+  auto* h_inl = reinterpret_cast<int32_t*>(static_cast<char*>(ctx->pinned) + align_up(err_bytes, 256));
+  // strided gather of out[f·121 + 120] (the error member of each block)
+  VG_CUDA(cudaMemcpy2DAsync(h_err, sizeof(double), graph->d_out + (VGICP_LINEARIZED_DOUBLES - 1),
+                            sizeof(double) * VGICP_LINEARIZED_DOUBLES, sizeof(double), nf, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaMemcpyAsync(h_inl, graph->d_out_inl, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(errors, h_err, err_bytes);
+  std::memcpy(inliers, h_inl, sizeof(int32_t) * nf);
   return VGICP_OK;
 }
 

@@ -346,14 +346,26 @@ def graph_bandwidth(ij, active) -> int:
     return int(6 * np.max(np.abs(rank[ij[both, 0]] - rank[ij[both, 1]])) + 5)
 
 
+def _sequential_total(errors) -> float:
+    """Σ errors in factor order, left to right (total_error, optimizer.cpp:66-75)."""
+    return float(np.cumsum(errors)[-1]) if len(errors) else 0.0
+
+
 def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None = None, device_assembly: bool = True,
-             gpu_solve: bool = True):
+             gpu_solve: bool = True, speculative: bool = True):
     """Run LM on `graph` from `poses` (num_poses × 12). Returns (poses, OptimizerReport).
 
     With device_assembly the normal equations are assembled on the GPU right after the
     linearization (vgicp_graph_linearize_assembled, block_solver.cpp:14-62) and only the S + P
     distinct blocks cross PCIe; otherwise the F factor blocks are downloaded and assembled here.
-    With gpu_solve, systems too wide for the banded host solver are factorized on the GPU."""
+    With gpu_solve, systems too wide for the banded host solver are factorized on the GPU.
+
+    With speculative (device assembly only), every candidate is scored by LINEARIZING it instead of
+    evaluating it: the linearization's per-factor errors equal evaluate_matching_cost's bit for
+    bit (vgicp_graph_linearized_errors), so the accept/reject decisions and the trace are those of
+    the reference loop (optimizer.cpp:113-186), and an accepted candidate's system is already
+    assembled — one factor pass per accepted iteration instead of two (a rejected candidate costs
+    the linearize/evaluate difference, ~10%)."""
     settings = settings or LmSettings()
     t_start = time.perf_counter()
     report = OptimizerReport()
@@ -368,29 +380,34 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
     if device_assembly:
         plan = graph.assembly_plan(fixed_mask.astype(np.uint8))
 
+    spec = speculative and device_assembly and hasattr(graph, "linearized_errors")
     banded = bandwidth is not None and bandwidth < (6 * int(active.sum())) // 4
     dev = _gpu_device(graph) if (device_assembly and gpu_solve and not banded) else None
     if dev is not None:  # device-resident system: no PCIe round trip of the assembled blocks
         import torch
 
         S, P = plan.num_slots, len(plan.pairs)
-        d_asm = torch.empty((S + P) * 36 + S * 6, dtype=torch.float64, device=dev)
+        # two assembled-system buffers: the current system's solver keeps views into one while a
+        # speculative candidate linearization fills the other
+        d_asms = [torch.empty((S + P) * 36 + S * 6, dtype=torch.float64, device=dev) for _ in range(2 if spec else 1)]
         d_poses = torch.empty((n, 12), dtype=torch.float64, device=dev)
+    buf = 0
 
-    def linearize_system():
+    def linearize_system(at, which=0):
         if dev is not None:
-            d_poses.copy_(torch.from_numpy(np.ascontiguousarray(poses)))
+            d_asm = d_asms[which]
+            d_poses.copy_(torch.from_numpy(np.ascontiguousarray(at)))
             graph.linearize_assembled_device(d_poses.data_ptr(), d_asm.data_ptr())
             graph.ctx.synchronize()  # the context stream may differ from torch's current stream
             return (d_asm[: S * 36].view(S, 6, 6), d_asm[S * 36:(S + P) * 36].view(P, 6, 6),
                     d_asm[(S + P) * 36:].view(S, 6))
         if device_assembly:
-            diag, off, rhs = graph.linearize_assembled(poses)
+            diag, off, rhs = graph.linearize_assembled(at)
             return diag, off, rhs
-        return assemble(graph.linearize_raw(poses)[0], ij, n)
+        return assemble(graph.linearize_raw(at)[0], ij, n)
 
-    system = linearize_system()
-    current = graph.total_error(poses)
+    system = linearize_system(poses)
+    current = _sequential_total(graph.linearized_errors()[0]) if spec else graph.total_error(poses)
     report.initial_error = report.final_error = current
     lam = settings.lambda_init
     any_accepted = False
@@ -432,8 +449,14 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
             for v in act[cand_updates[act] >= ORTHONORMALIZE_EVERY]:
                 cand[v] = orthonormalized(cand[v])
                 cand_updates[v] = 0
-            cand_error = graph.total_error(cand)
+            if spec:
+                cand_system = linearize_system(cand, 1 - buf)
+                cand_error = _sequential_total(graph.linearized_errors()[0])
+            else:
+                cand_error = graph.total_error(cand)
             if cand_error < current:
+                if spec:
+                    system, buf = cand_system, 1 - buf
                 decrease = (current - cand_error) / max(current, 1e-300)
                 poses, updates = cand, cand_updates
                 any_accepted = accepted = True
@@ -451,7 +474,8 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
         if not accepted or report.reason == "converged_relative_error":
             report.iteration_seconds.append(time.perf_counter() - t_it)
             break
-        system = linearize_system()
+        if not spec:
+            system = linearize_system(poses)
         report.reason = "max_iterations"
         report.iteration_seconds.append(time.perf_counter() - t_it)
     if not report.aborted:

@@ -550,8 +550,9 @@ class FactorGraph(_Handle):
         return int(n.value)
 
     def linearize_raw(self, poses, out: np.ndarray | None = None, inliers: np.ndarray | None = None):
-        """F×121 blocks + F inliers. `out` / `inliers` may be preallocated (page-locked buffers,
-        e.g. from torch pin_memory, receive the device copy directly)."""
+        """F×121 blocks + F inliers. `out` / `inliers` may be preallocated; page-locked buffers (e.g.
+        from torch pin_memory) are written by the kernel's epilogue directly over PCIe (zero-copy:
+        the result transfer overlaps the launch), others through a staging copy."""
         P = poses_array(poses)
         if len(P) != self.num_poses:
             raise ValueError("pose count does not match the graph")
@@ -622,6 +623,14 @@ class FactorGraph(_Handle):
         if getattr(self, "_plan", None) is None:
             raise ValueError("no assembly plan (call assembly_plan first)")
         check(_lib.load().vgicp_graph_linearize_assembled_device(self._h, C.c_void_p(d_poses), C.c_void_p(d_assembled)))
+
+    def linearized_errors(self):
+        """(errors[F] float64, inliers[F] int32) of the latest assembled linearization — equal to
+        evaluate() at the same poses."""
+        err = np.zeros(self.num_factors())
+        inl = np.zeros(self.num_factors(), np.int32)
+        check(_lib.load().vgicp_graph_linearized_errors(self._h, _ptr(err), _ptr(inl)))
+        return err, inl
 
     def linearize_device(self, d_poses: int, d_out: int, d_inliers: int) -> None:
         check(_lib.load().vgicp_graph_linearize_device(self._h, C.c_void_p(d_poses), C.c_void_p(d_out), C.c_void_p(d_inliers)))

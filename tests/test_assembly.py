@@ -136,3 +136,68 @@ def test_gpu_lm_device_assembly_matches_host(V):
     assert r_dev.iterations == r_host.iterations and r_dev.reason == r_host.reason
     assert abs(r_dev.final_error - r_host.final_error) <= 1e-9 * max(1.0, r_host.final_error)
     assert np.abs(p_dev - p_host).max() < 1e-9
+
+
+@gpu
+@pytest.mark.parametrize("seed", [70, 71, 72])
+def test_gpu_linearized_errors_equal_evaluate(V, seed):
+    """The error / inlier members of an assembled linearization equal evaluate() bit for bit (the
+    speculative LM scores candidates with them)."""
+    graph, poses = graph_case(V, seed=seed)
+    graph.assembly_plan(np.zeros(len(poses), np.uint8))
+    rng = O.Rng(seed + 100)
+    for trial in range(3):
+        P = poses if trial == 0 else np.stack([O.compose(p, rng.random_pose(0.02, 0.2)) for p in poses])
+        graph.linearize_assembled(P)
+        err, inl = graph.linearized_errors()
+        e_ref, i_ref = graph.evaluate(P)
+        assert np.array_equal(inl, i_ref)
+        assert np.array_equal(err, e_ref), np.abs(err - e_ref).max()
+        raw, rinl = graph.linearize_raw(P)
+        assert np.array_equal(raw[:, 120], err) and np.array_equal(rinl, inl)
+
+
+@gpu
+@pytest.mark.parametrize("loop", [False, True])
+def test_gpu_lm_speculative_matches_plain(V, loop):
+    """Scoring candidates by linearization gives the reference loop's trace exactly (banded host
+    solve for a chain, dense GPU solve with a loop closure)."""
+    from paper_2109_07073_b200 import optimizer as LM
+
+    rng = O.Rng(73)
+    nframes = 8
+    clouds = []
+    for _ in range(nframes):
+        m, c = rng.gaussian_cloud(3000, 10.0)
+        clouds.append(V.PointCloud(m.astype(np.float32), V.cov6_from(c)))
+    maps = V.GaussianVoxelMap.build_batch(clouds, 1.0)
+    poses = np.stack([rng.random_pose(0.05, 0.5) for _ in range(nframes)])
+    factors = [V.MatchingCostFactor(j - 1, j, clouds[j], maps[j - 1]) for j in range(1, nframes)]
+    if loop:
+        factors.append(V.MatchingCostFactor(nframes - 1, 0, clouds[0], maps[nframes - 1]))
+    graph = V.FactorGraph(factors, nframes, chunk=2048)
+    p0, r0 = LM.optimize(graph, poses, speculative=False)
+    p1, r1 = LM.optimize(graph, poses, speculative=True)
+    assert r1.iterations == r0.iterations and r1.reason == r0.reason
+    assert r1.initial_error == r0.initial_error and r1.final_error == r0.final_error
+    assert [(t.error, t.accepted, t.lam) for t in r1.trace] == [(t.error, t.accepted, t.lam) for t in r0.trace]
+    assert np.array_equal(p1, p0)
+
+
+@gpu
+def test_gpu_linearize_zero_copy_pinned_buffers(V):
+    """Page-locked caller buffers receive the blocks straight from the kernel (zero-copy); the
+    result equals the staged path bit for bit, for linearize and evaluate."""
+    import torch
+
+    graph, poses = graph_case(V, seed=74)
+    F = graph.num_factors()
+    ref, ref_inl = graph.linearize_raw(poses)
+    out = torch.full((F, 121), float("nan"), dtype=torch.float64).pin_memory().numpy()
+    inl = torch.full((F,), -1, dtype=torch.int32).pin_memory().numpy()
+    P = torch.from_numpy(np.ascontiguousarray(poses)).pin_memory().numpy()
+    for _ in range(2):
+        graph.linearize_raw(P, out, inl)
+        assert np.array_equal(out, ref) and np.array_equal(inl, ref_inl)
+    err, einl = graph.evaluate(poses)
+    assert np.array_equal(err, ref[:, 120]) and np.array_equal(einl, ref_inl)
