@@ -189,6 +189,17 @@ int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_po
  * reduction order), so an LM can score a candidate with the linearization it needs anyway if the
  * candidate is accepted (total_error, optimizer.cpp:66-75 + linearize_all, :45-62). */
 int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* inliers);
+/* Damped solve of the assembled reduced system on the GPU (solve_block_system,
+ * block_solver.cpp:64-122, with the Marquardt damping of optimizer.cpp:119-123: diagonal entries
+ * d -> d + lambda·max(d, 1e-10)). vgicp_graph_solver_plan (after vgicp_graph_assembly_plan)
+ * orders the slots by reverse Cuthill-McKee and reports the block bandwidth of the envelope;
+ * supported = 0 when the envelope window does not fit one thread-block cluster's shared memory
+ * (the caller then solves densely). vgicp_graph_solve_damped factors [diag | offdiag | rhs] as
+ * written by vgicp_graph_linearize_assembled_device (device memory) with right-looking 6×6-block
+ * Cholesky in one cluster launch and returns x[S×6] in slot order on the host; solved = 0 when a
+ * pivot block is not positive definite (the reference's failed_slot, the LM then raises lambda). */
+int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported);
+int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, double lambda, double* x, int* solved);
 
 /* Device-resident variants: every pointer is device memory of the context's device; the work
  * is enqueued on the context stream and the call returns without synchronising. */

@@ -91,6 +91,8 @@ SIGNATURES = {
     "vgicp_graph_linearize_assembled": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "vgicp_graph_linearize_assembled_device": (_i, [_vp, _vp, _vp]),
     "vgicp_graph_linearized_errors": (_i, [_vp, _vp, _vp]),
+    "vgicp_graph_solver_plan": (_i, [_vp, _vp, _vp]),
+    "vgicp_graph_solve_damped": (_i, [_vp, _vp, C.c_double, _vp, _vp]),
     "vgicp_transform_cloud": (_i, [_vp, _vp, _vp, _sz, _vp, _vp, _vp]),
     "vgicp_submap_build": (_i, [_vp, _vp, _vp, _i, _d, _d, _vp, _vp, _vp]),
     "vgicp_estimate_covariances_batch": (_i, [_vp, _vp, _vp, _i, _i, _d, _vp]),

@@ -1071,6 +1071,7 @@ int vgicp_graph_destroy(vgicp_graph graph) {
     cudaStreamSynchronize(graph->ctx->stream);
     dfree(graph->ctx, graph->block);
     dfree(graph->ctx, graph->plan);
+    dfree(graph->ctx, graph->band);
   }
   for (auto c : graph->clouds) release(c);
   for (auto m : graph->maps) release(m);
@@ -1218,11 +1219,20 @@ int vgicp_graph_assembly_plan(vgicp_graph graph, const uint8_t* fixed, int* num_
       pairs[2 * (o - 1 - active) + 1] = key.first;  // column slot b
     }
   }
+  graph->pair_ab.clear();
+  for (const auto& kv : off) {
+    graph->pair_ab.push_back(kv.first.second);
+    graph->pair_ab.push_back(kv.first.first);
+  }
   DeviceGuard g(graph->ctx->device);
-  if (graph->plan) {
+  if (graph->plan || graph->band) {
     VG_CUDA(cudaStreamSynchronize(graph->ctx->stream));
     dfree(graph->ctx, graph->plan);
+    dfree(graph->ctx, graph->band);
     graph->plan = nullptr;
+    graph->band = nullptr;
+    graph->band_bw = -1;
+    graph->band_cluster = 0;
   }
   const size_t b_ptr = align_up(sizeof(int) * (O + 1), 256);
   const size_t b_con = align_up(sizeof(int) * std::max<size_t>(contrib.size(), 1), 256);
@@ -1316,6 +1326,98 @@ int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* in
   VG_CUDA(cudaStreamSynchronize(s));
   std::memcpy(errors, h_err, err_bytes);
   std::memcpy(inliers, h_inl, sizeof(int32_t) * nf);
+  return VGICP_OK;
+}
+
+// ------------------------------------------------------------------------------- band solver
+int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported) {
+  if (!graph || !bandwidth || !supported) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (!graph->plan) return fail(VGICP_E_INVALID_ARGUMENT, "no assembly plan (call vgicp_graph_assembly_plan)");
+  vgicp_ctx ctx = graph->ctx;
+  DeviceGuard g(ctx->device);
+  if (graph->band) {
+    VG_CUDA(cudaStreamSynchronize(ctx->stream));
+    dfree(ctx, graph->band);
+    graph->band = nullptr;
+  }
+  const int S = graph->num_slots, P = graph->num_pairs;
+  const BandPlanHost hp = make_band_plan(S, P, graph->pair_ab.data());
+  graph->band_bw = hp.bw;
+  graph->band_cluster = S > 0 ? band_cluster_size(hp.bw) : 0;
+  cudaGetLastError();  // attribute / occupancy probes that failed are not launch errors
+  *bandwidth = hp.bw;
+  *supported = graph->band_cluster > 0 ? 1 : 0;
+  if (!*supported) return VGICP_OK;
+  const size_t b_perm = align_up(sizeof(int) * S, 256), b_reach = b_perm;
+  const size_t b_ptr = align_up(sizeof(int) * (S + 1), 256);
+  const size_t b_ent = align_up(sizeof(int2) * std::max<size_t>(hp.col_ent.size(), 1), 256);
+  const size_t b_status = 256, b_x = align_up(sizeof(double) * 6 * S, 256), b_ready = align_up(sizeof(int) * S, 256);
+  const size_t b_L = sizeof(double) * (36 * (static_cast<size_t>(hp.bw) + 1) + 16) * S;
+  VG_CUDA(dmalloc(ctx, &graph->band, b_perm + b_reach + b_ptr + b_ent + b_status + b_x + b_ready + b_L));
+  char* b = static_cast<char*>(graph->band);
+  BandDev& d = graph->band_dev;
+  d.S = S;
+  d.bw = hp.bw;
+  d.perm = reinterpret_cast<int*>(b);
+  d.reach = reinterpret_cast<int*>(b + b_perm);
+  d.col_ptr = reinterpret_cast<int*>(b + b_perm + b_reach);
+  d.col_ent = reinterpret_cast<int2*>(b + b_perm + b_reach + b_ptr);
+  d.status = reinterpret_cast<int*>(b + b_perm + b_reach + b_ptr + b_ent);
+  d.x = reinterpret_cast<double*>(b + b_perm + b_reach + b_ptr + b_ent + b_status);
+  d.ready = reinterpret_cast<int*>(b + b_perm + b_reach + b_ptr + b_ent + b_status + b_x);
+  d.Lg = reinterpret_cast<double*>(b + b_perm + b_reach + b_ptr + b_ent + b_status + b_x + b_ready);
+  graph->band_epoch = 0;
+  VG_CUDA(cudaMemsetAsync(d.ready, 0, sizeof(int) * S, ctx->stream));
+  cudaStream_t s = ctx->stream;
+  VG_CUDA(cudaMemcpyAsync(const_cast<int*>(d.perm), hp.perm.data(), sizeof(int) * S, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemcpyAsync(const_cast<int*>(d.reach), hp.reach.data(), sizeof(int) * S, cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemcpyAsync(const_cast<int*>(d.col_ptr), hp.col_ptr.data(), sizeof(int) * (S + 1),
+                          cudaMemcpyHostToDevice, s));
+  if (!hp.col_ent.empty())
+    VG_CUDA(cudaMemcpyAsync(const_cast<int2*>(d.col_ent), hp.col_ent.data(), sizeof(int2) * hp.col_ent.size(),
+                            cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  return VGICP_OK;
+}
+
+int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, double lambda, double* x, int* solved) {
+  if (!graph || !x || !solved || (graph->num_slots > 0 && !d_assembled))
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (!graph->band && graph->num_slots > 0)
+    return fail(VGICP_E_INVALID_ARGUMENT, graph->band_bw >= 0
+                                              ? "band solver unavailable for this bandwidth (use a dense solve)"
+                                              : "no solver plan (call vgicp_graph_solver_plan)");
+  const int S = graph->num_slots;
+  *solved = 1;
+  if (S == 0) return VGICP_OK;
+  vgicp_ctx ctx = graph->ctx;
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->stream;
+  graph->band_epoch = graph->band_epoch == 0x7fffffff ? 1 : graph->band_epoch + 1;
+  VG_CUDA(launch_band_solve(graph->band_dev, graph->band_cluster, d_assembled, graph->num_pairs, lambda,
+                            graph->band_epoch, s));
+  ctx->launches += 1;
+  const size_t b_x = sizeof(double) * 6 * S;
+  if (int rc = ensure_pinned(ctx, align_up(b_x, 256) + sizeof(int))) return rc;
+  auto* h_x = static_cast<double*>(ctx->pinned);
+  auto* h_status = reinterpret_cast<int*>(static_cast<char*>(ctx->pinned) + align_up(b_x, 256));
+  VG_CUDA(cudaMemcpyAsync(h_status, graph->band_dev.status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaMemcpyAsync(h_x, graph->band_dev.x, b_x, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  if (std::getenv("VGICP_SOLVE_PROF")) {  // cycle profile of CTA 0 (diagnostic)
+    unsigned long long prof[8];
+    VG_CUDA(cudaMemcpy(prof, reinterpret_cast<unsigned long long*>(graph->band_dev.status) + 8, sizeof(prof),
+                       cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "band solve C=%d bw=%d S=%d cycles: wait %llu load %llu owner(publish) %llu update %llu sync %llu "
+                 "back %llu owner-update %llu owner-factor %llu\n",
+                 graph->band_cluster, graph->band_bw, S, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5],
+                 prof[6], prof[7]);
+  }
+  if (*h_status != 0) {
+    *solved = 0;  // a pivot block was not positive definite (block_solver.cpp:78-82)
+    return VGICP_OK;
+  }
+  std::memcpy(x, h_x, b_x);
   return VGICP_OK;
 }
 

@@ -142,6 +142,31 @@ cudaError_t launch_overlap_multi(const OverlapItem* items, const int2* chunks, i
 // (0 H_ii/b_i, 1 H_jj/b_j, 2 H_ij, 3 H_ijᵀ) listed per output in factor order.
 cudaError_t launch_assemble(const int* out_ptr, const int* contrib, int num_slots, int num_outputs,
                             const double* blocks, double* assembled, cudaStream_t s);
+// Damped block Cholesky of the assembled reduced system (solver.cu; solve_block_system,
+// block_solver.cpp:64-122) over a reverse Cuthill-McKee order: perm[pos] = slot, reach[k] = last
+// block row of column k's envelope, per-column lower blocks (col_ent.x = row offset | transposed
+// << 16, .y = pair index) in CSR form.
+struct BandPlanHost {
+  int S = 0, bw = 0;
+  std::vector<int> perm, reach, col_ptr;
+  std::vector<int2> col_ent;
+};
+struct BandDev {
+  int S, bw;
+  const int* perm;
+  const int* reach;
+  const int* col_ptr;
+  const int2* col_ent;
+  double* Lg;   // S factored columns (band records)
+  double* x;    // S×6 solution, slot order
+  int* status;  // 0 solved, k + 1: pivot of position k failed
+  int* ready;   // S publication flags (launch epoch)
+};
+BandPlanHost make_band_plan(int S, int P, const int32_t* pairs);
+size_t band_smem_bytes(int bw, int C);
+int band_cluster_size(int bw);
+cudaError_t launch_band_solve(const BandDev& d, int C, const double* assembled, int num_pairs, double lam,
+                              int epoch, cudaStream_t s);
 // transform_cloud (point_cloud.cpp:26-42) of float32 device clouds into fp64 arrays, batched:
 // item k maps cloud k's points (input order) through poses12[k] into out_xyz / out_cov9 at `offset`.
 struct TransformItem {
@@ -253,4 +278,11 @@ struct vgicp_graph_s {
   int* d_out_ptr = nullptr;
   int* d_contrib = nullptr;
   double* d_asm = nullptr;
+  std::vector<int32_t> pair_ab;  // (row slot a, column slot b) per off-diagonal pair
+  // band Cholesky solver plan (vgicp_graph_solver_plan)
+  void* band = nullptr;  // perm | reach | col_ptr | col_ent | status | x | Lg
+  vgicp::BandDev band_dev{};
+  int band_cluster = 0;
+  int band_bw = -1;
+  int band_epoch = 0;
 };

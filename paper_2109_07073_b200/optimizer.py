@@ -218,10 +218,14 @@ class _ReducedSolver:
     on the GPU (cuSOLVER potrf/potrs through torch; the S + P blocks are uploaded and scattered on
     the device once per linearization) when `device` is given, else on the host."""
 
-    def __init__(self, diag, off, pairs, rhs, bandwidth=None, device=None):
+    def __init__(self, diag, off, pairs, rhs, bandwidth=None, device=None, band=None):
         S = len(diag)
         m = 6 * S
         self.m, self.rhs = m, rhs.reshape(-1)
+        self.band = band  # (graph, device address of the assembled system): GPU block-band Cholesky
+        if band is not None:
+            self.banded = self.gpu = False
+            return
         if not isinstance(diag, np.ndarray) and (bandwidth is not None and bandwidth < m // 4 or device is None):
             diag, off, rhs = diag.cpu().numpy(), off.cpu().numpy(), rhs.cpu().numpy()  # host solvers
             self.rhs = rhs.reshape(-1)
@@ -266,6 +270,9 @@ class _ReducedSolver:
     def solve(self, lam):
         if self.m == 0:
             return np.zeros(0)
+        if self.band is not None:
+            graph, addr = self.band
+            return graph.solve_damped(addr, lam)
         if self.banded:
             import scipy.linalg as sla
 
@@ -346,19 +353,27 @@ def graph_bandwidth(ij, active) -> int:
     return int(6 * np.max(np.abs(rank[ij[both, 0]] - rank[ij[both, 1]])) + 5)
 
 
+DENSE_SOLVE_MAX_UNKNOWNS = 6000  # above: the GPU block-band solver (vgicp_graph_solve_damped)
+
+
 def _sequential_total(errors) -> float:
     """Σ errors in factor order, left to right (total_error, optimizer.cpp:66-75)."""
     return float(np.cumsum(errors)[-1]) if len(errors) else 0.0
 
 
 def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None = None, device_assembly: bool = True,
-             gpu_solve: bool = True, speculative: bool = True):
+             gpu_solve: bool = True, speculative: bool = True, band_solve: bool | None = None):
     """Run LM on `graph` from `poses` (num_poses × 12). Returns (poses, OptimizerReport).
 
     With device_assembly the normal equations are assembled on the GPU right after the
     linearization (vgicp_graph_linearize_assembled, block_solver.cpp:14-62) and only the S + P
     distinct blocks cross PCIe; otherwise the F factor blocks are downloaded and assembled here.
-    With gpu_solve, systems too wide for the banded host solver are factorized on the GPU.
+    With gpu_solve, systems too wide for the banded host solver are factorized on the GPU: with
+    band_solve by the block-band Cholesky kernel over a reverse Cuthill-McKee order
+    (vgicp_graph_solve_damped, solve_block_system of block_solver.cpp:64-122) when its envelope fits
+    one thread-block cluster, else by a dense cuSOLVER Cholesky. band_solve=None picks the band
+    kernel above DENSE_SOLVE_MAX_UNKNOWNS reduced unknowns (dense is faster below: 1.8 vs 2.4 ms
+    at C3's 2,694 unknowns; dense memory and time grow as m² and m³).
 
     With speculative (device assembly only), every candidate is scored by LINEARIZING it instead of
     evaluating it: the linearization's per-factor errors equal evaluate_matching_cost's bit for
@@ -391,6 +406,9 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
         # speculative candidate linearization fills the other
         d_asms = [torch.empty((S + P) * 36 + S * 6, dtype=torch.float64, device=dev) for _ in range(2 if spec else 1)]
         d_poses = torch.empty((n, 12), dtype=torch.float64, device=dev)
+    if band_solve is None:
+        band_solve = 6 * int(active.sum()) > DENSE_SOLVE_MAX_UNKNOWNS
+    use_band = dev is not None and band_solve and hasattr(graph, "solver_plan") and graph.solver_plan()[1]
     buf = 0
 
     def linearize_system(at, which=0):
@@ -414,7 +432,8 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
     for it in range(settings.max_iterations):
         t_it = time.perf_counter()
         if device_assembly:
-            solver = _ReducedSolver(*system[:2], plan.pairs, system[2], bandwidth, dev)
+            solver = _ReducedSolver(*system[:2], plan.pairs, system[2], bandwidth, dev,
+                                    band=(graph, d_asms[buf].data_ptr()) if use_band else None)
         else:
             H, b = system
         accepted = False

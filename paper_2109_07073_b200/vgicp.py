@@ -632,6 +632,24 @@ class FactorGraph(_Handle):
         check(_lib.load().vgicp_graph_linearized_errors(self._h, _ptr(err), _ptr(inl)))
         return err, inl
 
+    def solver_plan(self) -> tuple[int, bool]:
+        """Band solver plan for the current assembly plan: (block bandwidth after reverse
+        Cuthill-McKee, whether the GPU band solver supports it)."""
+        bw, ok = C.c_int(), C.c_int()
+        check(_lib.load().vgicp_graph_solver_plan(self._h, C.byref(bw), C.byref(ok)))
+        self._band = bool(ok.value)
+        return int(bw.value), self._band
+
+    def solve_damped(self, d_assembled: int, lam: float):
+        """x (S×6, slot order) of the damped assembled system at device address `d_assembled`, or
+        None when a pivot block is not positive definite (block_solver.cpp:78-82)."""
+        S = self._plan.num_slots
+        x = np.empty(6 * S)
+        ok = C.c_int()
+        check(_lib.load().vgicp_graph_solve_damped(self._h, C.c_void_p(d_assembled), C.c_double(lam), _ptr(x),
+                                                   C.byref(ok)))
+        return x if ok.value else None
+
     def linearize_device(self, d_poses: int, d_out: int, d_inliers: int) -> None:
         check(_lib.load().vgicp_graph_linearize_device(self._h, C.c_void_p(d_poses), C.c_void_p(d_out), C.c_void_p(d_inliers)))
 

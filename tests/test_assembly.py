@@ -201,3 +201,85 @@ def test_gpu_linearize_zero_copy_pinned_buffers(V):
         assert np.array_equal(out, ref) and np.array_equal(inl, ref_inl)
     err, einl = graph.evaluate(poses)
     assert np.array_equal(err, ref[:, 120]) and np.array_equal(einl, ref_inl)
+
+
+def _damped_dense(diag, off, pairs, rhs, lam):
+    from paper_2109_07073_b200 import optimizer as LM
+
+    H, b = LM.slot_system(diag, off, pairs, rhs)
+    dg = np.diagonal(H).copy()
+    H[np.diag_indices_from(H)] = dg + lam * np.maximum(dg, 1e-10)  # optimizer.cpp:119-123
+    return H, b
+
+
+@gpu
+@pytest.mark.parametrize("seed", [70, 75])
+def test_gpu_band_solver_matches_dense(V, seed):
+    """Block-band Cholesky (RCM order, one cluster launch) vs a dense fp64 solve of the same
+    damped system (solve_block_system semantics, block_solver.cpp:64-122)."""
+    import torch
+
+    graph, poses = graph_case(V, seed=seed)
+    n = len(poses)
+    fixed = np.zeros(n, np.uint8)
+    fixed[0] = 1
+    plan = graph.assembly_plan(fixed)
+    bw, ok = graph.solver_plan()
+    assert ok and 0 <= bw < plan.num_slots
+    S, P = plan.num_slots, len(plan.pairs)
+    d_asm = torch.empty((S + P) * 36 + S * 6, dtype=torch.float64, device="cuda")
+    d_poses = torch.from_numpy(np.ascontiguousarray(poses)).cuda()
+    graph.linearize_assembled_device(d_poses.data_ptr(), d_asm.data_ptr())
+    graph.ctx.synchronize()
+    a = d_asm.cpu().numpy()
+    diag, off, rhs = a[: S * 36].reshape(S, 6, 6), a[S * 36:(S + P) * 36].reshape(P, 6, 6), a[(S + P) * 36:].reshape(S, 6)
+    for lam in (1e-6, 1e-3, 1.0):
+        x = graph.solve_damped(d_asm.data_ptr(), lam)
+        H, b = _damped_dense(diag, off, plan.pairs, rhs, lam)
+        ref = np.linalg.solve(H, b)
+        assert x is not None
+        assert np.abs(x - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max()), np.abs(x - ref).max()
+        assert np.array_equal(x, graph.solve_damped(d_asm.data_ptr(), lam))  # deterministic
+
+
+@gpu
+def test_gpu_band_solver_random_spd_and_failure(V):
+    """Random SPD systems on a graph's block pattern (exact envelope handling incl. transposed
+    pairs), and a non-positive-definite pivot block -> None (the reference's failed_slot)."""
+    import torch
+
+    graph, poses = graph_case(V, nframes=10, n=1500, seed=76)
+    plan = graph.assembly_plan(np.zeros(len(poses), np.uint8))
+    graph.solver_plan()
+    S, P = plan.num_slots, len(plan.pairs)
+    rng = np.random.default_rng(5)
+    off = rng.standard_normal((P, 6, 6))
+    H = np.zeros((6 * S, 6 * S))
+    for k, (a_, b_) in enumerate(plan.pairs):
+        H[6 * a_:6 * a_ + 6, 6 * b_:6 * b_ + 6] = off[k]
+        H[6 * b_:6 * b_ + 6, 6 * a_:6 * a_ + 6] = off[k].T
+    H += (np.abs(H).sum(1).max() + 1.0) * np.eye(6 * S)  # diagonally dominant -> SPD
+    diag = np.stack([H[6 * s:6 * s + 6, 6 * s:6 * s + 6] for s in range(S)])
+    rhs = rng.standard_normal((S, 6))
+    buf = torch.from_numpy(np.concatenate([diag.ravel(), off.ravel(), rhs.ravel()])).cuda()
+    x = graph.solve_damped(buf.data_ptr(), 0.0)
+    ref = np.linalg.solve(H, rhs.ravel())
+    assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
+    bad = diag.copy()
+    bad[S // 2] = -np.eye(6)
+    buf = torch.from_numpy(np.concatenate([bad.ravel(), off.ravel(), rhs.ravel()])).cuda()
+    assert graph.solve_damped(buf.data_ptr(), 0.0) is None
+    assert graph.solve_damped(torch.from_numpy(np.concatenate([diag.ravel(), off.ravel(), rhs.ravel()])).cuda()
+                              .data_ptr(), 0.0) is not None  # the plan survives a failed solve
+
+
+@gpu
+def test_gpu_lm_band_solver_matches_dense_solver(V):
+    from paper_2109_07073_b200 import optimizer as LM
+
+    graph, poses = graph_case(V, nframes=8, n=3000, seed=77)
+    p_d, r_d = LM.optimize(graph, poses, band_solve=False)
+    p_b, r_b = LM.optimize(graph, poses, band_solve=True)
+    assert r_b.iterations == r_d.iterations and r_b.reason == r_d.reason
+    assert abs(r_b.final_error - r_d.final_error) <= 1e-9 * max(1.0, r_d.final_error)
+    assert np.abs(p_b - p_d).max() < 1e-9
