@@ -126,6 +126,7 @@ void release(vgicp_map m) {
     DeviceGuard g(m->ctx->device);
     dfree(m->ctx, m->cold);
     dfree(m->ctx, m->table);
+    dfree(m->ctx, m->occ_mem);
     delete m;
   }
 }
@@ -352,6 +353,49 @@ int vgicp_cloud_destroy(vgicp_cloud cloud) {
 // ------------------------------------------------------------------------------------ voxel maps
 static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map* out);
 
+// Occupancy bitmaps (overlap query) for freshly built maps: one word per 4×4×4 brick of the
+// occupied voxel box; maps whose box would need more than kOccMaxWords words keep hash probes.
+// `d_jobs` is device scratch for at least m OccJob records.
+constexpr size_t kOccMaxWords = size_t(1) << 22;  // 32 MB per map
+static_assert(sizeof(OccJob) <= sizeof(InsertJob), "occupancy jobs reuse the insert-job scratch");
+static int build_occupancy(vgicp_ctx ctx, vgicp_map* maps, int m, void* d_jobs, cudaStream_t s) {
+  if (std::getenv("VGICP_NO_OCCUPANCY")) return VGICP_OK;  // measurement switch (hash probes only)
+  std::vector<OccJob> jobs;
+  unsigned max_words = 0, max_v = 0;
+  for (int k = 0; k < m; ++k) {
+    vgicp_map mp = maps[k];
+    if (mp->voxels == 0 || mp->cmin[0] > mp->cmax[0]) continue;
+    unsigned e[3];
+    size_t words = 1;
+    for (int a = 0; a < 3; ++a) {
+      e[a] = static_cast<unsigned>(mp->cmax[a] - mp->cmin[a] + 1);
+      words *= (e[a] + 3) / 4;
+    }
+    if (words > kOccMaxWords) continue;
+    VG_CUDA(dmalloc(ctx, &mp->occ_mem, sizeof(unsigned long long) * words));
+    OccDev& o = mp->occ;
+    o.occ = static_cast<const unsigned long long*>(mp->occ_mem);
+    o.kx0 = static_cast<unsigned>(mp->cmin[0] + (1 << 20));
+    o.ky0 = static_cast<unsigned>(mp->cmin[1] + (1 << 20));
+    o.kz0 = static_cast<unsigned>(mp->cmin[2] + (1 << 20));
+    o.ex = e[0], o.ey = e[1], o.ez = e[2];
+    o.nby = (e[1] + 3) / 4, o.nbz = (e[2] + 3) / 4;
+    jobs.push_back(OccJob{mp->keys, static_cast<unsigned long long*>(mp->occ_mem), static_cast<unsigned>(mp->voxels),
+                          static_cast<unsigned>(words), o.kx0, o.ky0, o.kz0, o.nby, o.nbz, 0u});
+    max_words = std::max(max_words, static_cast<unsigned>(words));
+    max_v = std::max(max_v, static_cast<unsigned>(mp->voxels));
+  }
+  if (jobs.empty()) return VGICP_OK;
+  for (size_t j0 = 0; j0 < jobs.size(); j0 += static_cast<size_t>(m)) {  // d_jobs holds m records
+    const int nj = static_cast<int>(std::min(jobs.size() - j0, static_cast<size_t>(m)));
+    VG_CUDA(cudaMemcpyAsync(d_jobs, jobs.data() + j0, sizeof(OccJob) * nj, cudaMemcpyHostToDevice, s));
+    VG_CUDA(launch_occ_build(static_cast<const OccJob*>(d_jobs), nj, max_words, max_v, s));
+    ctx->launches += 2;
+    VG_CUDA(cudaStreamSynchronize(s));  // d_jobs is reused
+  }
+  return VGICP_OK;
+}
+
 int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* resolutions, int m,
                                vgicp_map* out) {
   if (!ctx || !out || (m > 0 && (!clouds || !resolutions))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
@@ -575,10 +619,13 @@ static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map*
     cleanup();
     return cuda_fail(e, "voxel map bounds");
   }
-  for (int k = 0; k < m; ++k) {
+  for (int k = 0; k < m; ++k)
     for (int a = 0; a < 3; ++a) maps[k]->cmin[a] = hbox[6 * k + a], maps[k]->cmax[a] = hbox[6 * k + 3 + a];
-    out[k] = maps[k];
+  if (int rc = build_occupancy(ctx, maps.data(), m, d_jobs, s)) {
+    cleanup();
+    return rc;
   }
+  for (int k = 0; k < m; ++k) out[k] = maps[k];
   return VGICP_OK;
 }
 
@@ -867,15 +914,49 @@ static bool overlap_disjoint(const vgicp_cloud_s* c, const double* T, const vgic
   return false;
 }
 
+// Overlap probe item k (cloud k's points through pose k against map k), written in place.
+static void fill_overlap_item(OverlapItem& it, const vgicp_cloud_s* c, const double* T, const vgicp_map_s* mp) {
+  it.blk = c->sblk;  // Morton order (hit counts are order-independent)
+  it.map = mp->dev();
+  it.occ = mp->occ;
+  std::memcpy(it.T, T, sizeof(double) * 12);
+  it.n = static_cast<unsigned>(c->n);
+  it.pad = 0;
+  OccScreen& sc = it.scr;
+  if (!it.occ.occ) {
+    sc.occ = nullptr;
+    return;
+  }
+  float tmax = 0.f;
+  for (int q = 0; q < 9; ++q) sc.R[q] = static_cast<float>(T[q]);
+  for (int q = 0; q < 3; ++q) sc.t[q] = static_cast<float>(T[9 + q]), tmax = std::max(tmax, std::fabs(sc.t[q]));
+  sc.inv_r = static_cast<float>(mp->inv_res);
+  sc.A2 = 5e-7f * sc.inv_r;
+  sc.C = sc.A2 * tmax + 1e-7f;
+  sc.cx0 = static_cast<int>(it.occ.kx0) - (1 << 20);
+  sc.cy0 = static_cast<int>(it.occ.ky0) - (1 << 20);
+  sc.cz0 = static_cast<int>(it.occ.kz0) - (1 << 20);
+  sc.ex = it.occ.ex, sc.ey = it.occ.ey, sc.ez = it.occ.ez, sc.nby = it.occ.nby, sc.nbz = it.occ.nbz;
+  sc.pad[0] = sc.pad[1] = 0u;
+  sc.occ = it.occ.occ;
+}
+
 int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* poses12, const vgicp_map* maps,
                         int m, uint64_t* hits) {
   if (!ctx || (m > 0 && (!clouds || !poses12 || !maps || !hits)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (m <= 0) return VGICP_OK;
   const bool no_cull = std::getenv("VGICP_OVERLAP_NOCULL") != nullptr;  // measurement switch (un-culled)
-  std::vector<OverlapItem> items;
+  const bool per_item = std::getenv("VGICP_OVERLAP_PERITEM") != nullptr;  // measurement switch
+  const bool verbose = std::getenv("VGICP_VERBOSE") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto ms_since = [](std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  };
+  // pass 1: validation and exact culling (probes whose transformed cloud box misses the map's
+  // occupied box: 0 hits, no launch work)
   std::vector<int> live;
-  items.reserve(m);
+  live.reserve(m);
   unsigned max_n = 0;
   for (int k = 0; k < m; ++k) {
     if (!clouds[k] || !maps[k]) return fail(VGICP_E_INVALID_ARGUMENT, "null cloud or map");
@@ -883,56 +964,68 @@ int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* 
     if (clouds[k]->n == 0) return fail(VGICP_E_INVALID_ARGUMENT, "overlap_rate requires a nonempty cloud");
     hits[k] = 0;
     if (!no_cull && overlap_disjoint(clouds[k], poses12 + 12 * k, maps[k])) continue;
-    OverlapItem it;
-    it.blk = clouds[k]->sblk;  // Morton order (hit counts are order-independent)
-    it.map = maps[k]->dev();
-    std::memcpy(it.T, poses12 + 12 * k, sizeof(double) * 12);
-    it.n = static_cast<unsigned>(clouds[k]->n);
-    it.pad = 0;
-    max_n = std::max(max_n, it.n);
-    items.push_back(it);
+    max_n = std::max(max_n, static_cast<unsigned>(clouds[k]->n));
     live.push_back(k);
   }
-  const int ml = static_cast<int>(items.size());
+  const int ml = static_cast<int>(live.size());
   if (ml == 0) return VGICP_OK;
-  // group the probes by cloud (stable): every chunk of <= 32 maps shares one cloud, whose points
-  // each thread loads once
-  std::vector<int> order(ml);
-  for (int q = 0; q < ml; ++q) order[q] = q;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return items[a].blk < items[b].blk; });
-  std::vector<OverlapItem> sorted(ml);
-  std::vector<int2> chunks;
-  for (int q = 0; q < ml; ++q) {
-    sorted[q] = items[order[q]];
-    if (q == 0 || sorted[q].blk != sorted[q - 1].blk || chunks.back().y == kOverlapMapsPerChunk)
-      chunks.push_back(make_int2(q, 0));
-    ++chunks.back().y;
-  }
-  const bool per_item = std::getenv("VGICP_OVERLAP_PERITEM") != nullptr;  // measurement switch
+  // Group the probes by cloud (stable), bitmap-carrying maps first within a cloud: every chunk of
+  // <= 32 maps shares one cloud (its points are loaded once) and one kernel. Callers usually pass
+  // probes grouped already (one frame against many maps), which skips the sort.
+  auto before = [&](int a, int b) {
+    const bool oa = maps[a]->occ.occ != nullptr, ob = maps[b]->occ.occ != nullptr;
+    return clouds[a]->sblk != clouds[b]->sblk ? clouds[a]->sblk < clouds[b]->sblk : (oa && !ob);
+  };
+  std::vector<int> order = live;  // order[q] = probe index of sorted position q
+  if (!std::is_sorted(order.begin(), order.end(), before)) std::stable_sort(order.begin(), order.end(), before);
+  const double t_items = ms_since(t_start);
   DeviceGuard g(ctx->device);
   const size_t bi = align_up(sizeof(OverlapItem) * ml, 256);
-  const size_t bc = align_up(sizeof(int2) * chunks.size(), 256);
-  if (int rc = ensure_scratch(ctx, bi + bc + sizeof(unsigned long long) * ml)) return rc;
+  const size_t bc = align_up(sizeof(int2) * (ml + 1), 256);
+  const size_t bh = sizeof(unsigned long long) * ml;
+  if (int rc = ensure_scratch(ctx, bi + bc + bh)) return rc;
+  if (int rc = ensure_pinned(ctx, bi + bc + bh)) return rc;
+  char* hp = static_cast<char*>(ctx->pinned);  // page-locked staging: one fast H2D / D2H each
+  auto* sorted = reinterpret_cast<OverlapItem*>(hp);
+  auto* hchunks = reinterpret_cast<int2*>(hp + bi);
+  auto* h = reinterpret_cast<unsigned long long*>(hp + bi + bc);
+  int n_occ = 0;  // occupancy chunks first, then hash-probe chunks
+  std::vector<int2> hash_chunks;
+  for (int q = 0; q < ml; ++q) {
+    const int k = order[q];
+    fill_overlap_item(sorted[q], clouds[k], poses12 + 12 * k, maps[k]);
+    const bool occ = sorted[q].occ.occ != nullptr;
+    int2* last = occ ? (n_occ ? &hchunks[n_occ - 1] : nullptr) : (hash_chunks.empty() ? nullptr : &hash_chunks.back());
+    if (!last || sorted[q].blk != sorted[last->x].blk || last->y == kOverlapMapsPerChunk) {
+      if (occ) last = &(hchunks[n_occ++] = make_int2(q, 0));
+      else last = &(hash_chunks.emplace_back(make_int2(q, 0)));
+    }
+    ++last->y;
+  }
+  const int n_hash = static_cast<int>(hash_chunks.size());
+  for (int c = 0; c < n_hash; ++c) hchunks[n_occ + c] = hash_chunks[c];
   char* sb = static_cast<char*>(ctx->scratch);
   auto* d_items = reinterpret_cast<OverlapItem*>(sb);
   auto* d_chunks = reinterpret_cast<int2*>(sb + bi);
   auto* d_hits = reinterpret_cast<unsigned long long*>(sb + bi + bc);
   cudaStream_t s = ctx->stream;
-  std::vector<uint64_t> h(ml);
-  VG_CUDA(cudaMemcpyAsync(d_items, sorted.data(), sizeof(OverlapItem) * ml, cudaMemcpyHostToDevice, s));
-  VG_CUDA(cudaMemcpyAsync(d_chunks, chunks.data(), sizeof(int2) * chunks.size(), cudaMemcpyHostToDevice, s));
-  VG_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long) * ml, s));
-  if (per_item)
+  const double t_pack = ms_since(t_start);
+  VG_CUDA(cudaMemcpyAsync(d_items, sorted, bi + sizeof(int2) * (n_occ + n_hash), cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemsetAsync(d_hits, 0, bh, s));
+  if (per_item) {
     VG_CUDA(launch_overlap(d_items, ml, max_n, d_hits, s));
-  else
-    VG_CUDA(launch_overlap_multi(d_items, d_chunks, static_cast<int>(chunks.size()), max_n, d_hits, s));
-  ctx->launches += 1;
-  VG_CUDA(cudaMemcpyAsync(h.data(), d_hits, sizeof(uint64_t) * ml, cudaMemcpyDeviceToHost, s));
+    ctx->launches += 1;
+  } else {
+    VG_CUDA(launch_overlap_occ(d_items, d_chunks, n_occ, max_n, d_hits, s));
+    VG_CUDA(launch_overlap_multi(d_items, d_chunks + n_occ, n_hash, max_n, d_hits, s));
+    ctx->launches += (n_occ > 0) + (n_hash > 0);
+  }
+  VG_CUDA(cudaMemcpyAsync(h, d_hits, bh, cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaStreamSynchronize(s));
-  std::vector<uint64_t> hu(ml);
-  for (int q = 0; q < ml; ++q) hu[order[q]] = h[q];
-  h.swap(hu);
-  for (int q = 0; q < ml; ++q) hits[live[q]] = h[q];
+  for (int q = 0; q < ml; ++q) hits[order[q]] = h[q];
+  if (verbose)
+    std::fprintf(stderr, "[vgicp] overlap batch: %d probes (%d live), cull+order %.3f ms, pack %.3f ms, gpu+sync %.3f ms\n",
+                 m, ml, t_items, t_pack - t_items, ms_since(t_start) - t_pack);
   return VGICP_OK;
 }
 

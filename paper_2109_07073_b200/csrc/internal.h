@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstddef>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -52,13 +53,41 @@ struct FactorDev {
   int pad;
 };
 
+// Per-map constants of the occupancy overlap kernel's fp32 screen (host-computed, staged in
+// shared memory per CTA): fl32(R), fl32(t), fl32(1/r), the margin δ = A2·|p|₁ + C (A2 = 5e-7/r,
+// C = A2·max|t| + 1e-7: a bound on |fl32 y - q/r| with the reference's fp64 rounding inside it),
+// the occupied box (unbiased voxel coordinates) and its bitmap.
+struct alignas(16) OccScreen {
+  float R[9];
+  float t[3];
+  float inv_r, A2, C;
+  int cx0, cy0, cz0;
+  unsigned ex, ey, ez, nby, nbz;
+  unsigned pad[2];
+  const unsigned long long* occ;
+};
+static_assert(sizeof(OccScreen) == 112, "OccScreen is staged as 7 uint4");
 struct OverlapItem {
   const PointBlock* blk;
   MapDev map;
+  OccDev occ;  // occupancy bitmap (occ.occ == nullptr: hash probes)
   double T[12];
   unsigned n;
   unsigned pad;
+  OccScreen scr;
 };
+static_assert(offsetof(OverlapItem, scr) % 16 == 0 && sizeof(OverlapItem) % 16 == 0, "OccScreen is read as uint4");
+cudaError_t launch_overlap_occ(const OverlapItem* items, const int2* chunks, int num_chunks, unsigned max_n,
+                               unsigned long long* hits, cudaStream_t s);
+// Occupancy bitmap build job for one map (cold keys -> bits).
+struct OccJob {
+  const unsigned long long* keys;
+  unsigned long long* occ;
+  unsigned V;
+  unsigned words;
+  unsigned kx0, ky0, kz0, nby, nbz, pad;
+};
+cudaError_t launch_occ_build(const OccJob* jobs, int m, unsigned max_words, unsigned max_v, cudaStream_t s);
 
 struct BuildSeg {
   const float4* pa;           // float32 device cloud (input order) ...
@@ -249,6 +278,8 @@ struct vgicp_map_s {
   unsigned long long* tkeys = nullptr;
   vgicp::SlotStatsA* sa = nullptr;
   vgicp::SlotStatsB* sb = nullptr;
+  void* occ_mem = nullptr;  // occupancy bitmap (overlap query), null when the box is too large
+  vgicp::OccDev occ{};
   std::atomic<int> refs{1};
   vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov64, res, inv_res, shift, 0u}; }
 };

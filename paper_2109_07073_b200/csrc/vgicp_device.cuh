@@ -54,6 +54,24 @@ struct MapDev {
   unsigned pad;
 };
 
+// Occupancy bitmap of a map's occupied voxel box, for the overlap query (occupancy is all it
+// needs): one 64-bit word per 4×4×4 brick of voxels, bricks row-major (z fastest), bit
+// (x&3)<<4 | (y&3)<<2 | (z&3) of the box-relative voxel coordinate. occ == nullptr: probe the hash.
+struct OccDev {
+  const unsigned long long* occ;
+  unsigned kx0, ky0, kz0;  // biased (key) coordinates of the box's lower corner
+  unsigned ex, ey, ez;     // box extent in voxels
+  unsigned nby, nbz;       // bricks along y and z
+};
+// Word index / bit of biased voxel coordinates; false outside the occupied box (= a miss).
+__device__ __forceinline__ bool occ_locate(const OccDev& o, unsigned k0, unsigned k1, unsigned k2, unsigned& word,
+                                           unsigned& bit) {
+  const unsigned rx = k0 - o.kx0, ry = k1 - o.ky0, rz = k2 - o.kz0;  // wraps to huge values below the box
+  word = ((rx >> 2) * o.nby + (ry >> 2)) * o.nbz + (rz >> 2);
+  bit = ((rx & 3u) << 4) | ((ry & 3u) << 2) | (rz & 3u);
+  return (rx < o.ex) & (ry < o.ey) & (rz < o.ez);
+}
+
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256).
 __device__ __forceinline__ void ldg256(const void* p, unsigned& r0, unsigned& r1, unsigned& r2, unsigned& r3,
                                        unsigned& r4, unsigned& r5, unsigned& r6, unsigned& r7) {

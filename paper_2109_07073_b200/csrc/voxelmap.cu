@@ -321,8 +321,29 @@ __global__ void __launch_bounds__(256, VG_OV_MINB) overlap_kernel(const OverlapI
 #pragma unroll
     for (int q = 0; q < 12; ++q) T[q] = it.T[q];
     const MapDev map = it.map;
+    const OccDev occ = it.occ;
     const PointBlock* __restrict__ blk = it.blk;
     unsigned count = 0;
+    if (occ.occ) {  // occupancy bitmap: one 8-byte word per probe, no key compare
+      for (unsigned base = first; base < n; base += kOverlapILP * stride) {
+        unsigned long long wv[kOverlapILP];
+        unsigned bit[kOverlapILP];
+#pragma unroll
+        for (int u = 0; u < kOverlapILP; ++u) {
+          const unsigned i = base + u * stride;
+          const unsigned ic = min(i, n - 1);
+          const float4 a = __ldg(&blk[ic / kPointBlock].pa[ic % kPointBlock]);
+          double q0, q1, q2, l0, l1, l2;
+          apply_pose_rn(T, a.x, a.y, a.z, q0, q1, q2);
+          unsigned k0 = 0, k1 = 0, k2 = 0, word = 0;
+          const bool ok = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && i < n &&
+                          occ_locate(occ, k0, k1, k2, word, bit[u]);
+          wv[u] = ok ? __ldg(occ.occ + word) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < kOverlapILP; ++u) count += static_cast<unsigned>((wv[u] >> bit[u]) & 1ull);
+      }
+    } else
     for (unsigned base = first; base < n; base += kOverlapILP * stride) {
       unsigned hi[kOverlapILP], lo[kOverlapILP], b1[kOverlapILP], b2[kOverlapILP];
       bool ok[kOverlapILP];
@@ -435,34 +456,52 @@ __global__ void __launch_bounds__(256) overlap_multi_kernel(const OverlapItem* _
     unsigned hi[2][kOvPoints], lo[2][kOvPoints], b1[2][kOvPoints], b2[2][kOvPoints];
     bool ok[2][kOvPoints];
     const MapDev* mp[2];
+    bool use_occ[2];
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
       const int kk = min(k + w, mc - 1);
       const OverlapItem& it = items[m0 + kk];
       mp[w] = &it.map;
       const MapDev& map = it.map;
+      use_occ[w] = it.occ.occ != nullptr;  // uniform over the CTA
 #pragma unroll
       for (int u = 0; u < kOvPoints; ++u) {
         double q0, q1, q2, l0, l1, l2;
         apply_pose_rn(it.T, px[u], py[u], pz[u], q0, q1, q2);
         unsigned k0 = 0, k1 = 0, k2 = 0;
         ok[w][u] = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && in[u] && (k + w < mc);
-        pack_key32(k0, k1, k2, hi[w][u], lo[w][u]);
-        b1[w][u] = bucket1(k0, k1, k2, map.shift);
-        b2[w][u] = bucket2(k0, k1, k2, map.shift);
+        if (use_occ[w]) {  // occupancy bitmap: word index in b1, bit in b2
+          ok[w][u] = ok[w][u] && occ_locate(it.occ, k0, k1, k2, b1[w][u], b2[w][u]);
+        } else {
+          pack_key32(k0, k1, k2, hi[w][u], lo[w][u]);
+          b1[w][u] = bucket1(k0, k1, k2, map.shift);
+          b2[w][u] = bucket2(k0, k1, k2, map.shift);
+        }
       }
     }
     BucketPair bp[2][kOvPoints];
 #pragma unroll
-    for (int w = 0; w < 2; ++w)
+    for (int w = 0; w < 2; ++w) {
+      if (use_occ[w]) {
+        const unsigned long long* occ = items[m0 + min(k + w, mc - 1)].occ.occ;
 #pragma unroll
-      for (int u = 0; u < kOvPoints; ++u) bp[w][u] = load_buckets(mp[w]->keys, b1[w][u], b2[w][u]);
+        for (int u = 0; u < kOvPoints; ++u) {
+          const unsigned long long v = ok[w][u] ? __ldg(occ + b1[w][u]) : 0ull;
+          bp[w][u].a.x = static_cast<unsigned>((v >> b2[w][u]) & 1ull);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kOvPoints; ++u) bp[w][u] = load_buckets(mp[w]->keys, b1[w][u], b2[w][u]);
+      }
+    }
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
       unsigned c = 0;
 #pragma unroll
       for (int u = 0; u < kOvPoints; ++u)
-        if (ok[w][u] && match_buckets(bp[w][u], b1[w][u], b2[w][u], hi[w][u], lo[w][u]) >= 0) ++c;
+        if (use_occ[w] ? bp[w][u].a.x != 0u
+                       : (ok[w][u] && match_buckets(bp[w][u], b1[w][u], b2[w][u], hi[w][u], lo[w][u]) >= 0))
+          ++c;
       c = __reduce_add_sync(0xffffffffu, c);
       if ((threadIdx.x & 31) == 0 && c) atomicAdd(&cnt[k + w < mc ? k + w : 0], c);
     }
@@ -470,6 +509,141 @@ __global__ void __launch_bounds__(256) overlap_multi_kernel(const OverlapItem* _
   __syncthreads();
   if (threadIdx.x < mc && cnt[threadIdx.x])
     atomicAdd(&hits[m0 + threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
+}
+
+// Occupancy bitmaps of a batch of maps: zero every word, then set one bit per voxel key.
+__global__ void occ_zero_kernel(const OccJob* __restrict__ jobs) {
+  const OccJob& j = jobs[blockIdx.y];
+  for (unsigned w = blockIdx.x * blockDim.x + threadIdx.x; w < j.words; w += gridDim.x * blockDim.x) j.occ[w] = 0ull;
+}
+__global__ void occ_set_kernel(const OccJob* __restrict__ jobs) {
+  const OccJob& j = jobs[blockIdx.y];
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < j.V; v += gridDim.x * blockDim.x) {
+    const unsigned long long key = j.keys[v];
+    const unsigned k0 = static_cast<unsigned>(key >> 42) & 0x1FFFFFu;
+    const unsigned k1 = static_cast<unsigned>(key >> 21) & 0x1FFFFFu;
+    const unsigned k2 = static_cast<unsigned>(key) & 0x1FFFFFu;
+    const unsigned rx = k0 - j.kx0, ry = k1 - j.ky0, rz = k2 - j.kz0;
+    const unsigned word = ((rx >> 2) * j.nby + (ry >> 2)) * j.nbz + (rz >> 2);
+    atomicOr(j.occ + word, 1ull << (((rx & 3u) << 4) | ((ry & 3u) << 2) | (rz & 3u)));
+  }
+}
+
+cudaError_t launch_occ_build(const OccJob* jobs, int m, unsigned max_words, unsigned max_v, cudaStream_t s) {
+  if (m <= 0) return cudaSuccess;
+  occ_zero_kernel<<<dim3(grid_for(max_words, 256, 1024), m), 256, 0, s>>>(jobs);
+  occ_set_kernel<<<dim3(grid_for(max_v, 256, 1024), m), 256, 0, s>>>(jobs);
+  return cudaGetLastError();
+}
+
+// Overlap of one cloud against a chunk of <= kOvMaps maps that all carry occupancy bitmaps.
+// Warp w of the CTA owns kOccPoints·32 consecutive Morton-ordered points. Per map (the host has
+// already culled maps whose box the whole cloud misses; finer in-kernel culling measured slower):
+//  * fp32 screen: q = fl32(R)·p + fl32(t), y = q·fl32(1/r); when frac(y) keeps a margin
+//    δ = 5e-7·(|p|₁ + max|t|)/r + 1e-7 from both faces on every axis (|fl32 y - q/r| is at most
+//    ~4.2e-7·(|p|₁ + |t|)/r: five fp32 roundings of the transform plus the 1/r and product
+//    roundings; the reference's own fp64 rounding is far inside), floor(y) IS the reference's
+//    floor(fl64(q64 / r)); otherwise (rare) the point takes the exact fp64 path;
+//  * one 8-byte bitmap word per probe.
+#ifndef VG_OCC_POINTS
+#define VG_OCC_POINTS 4
+#endif
+constexpr int kOccPoints = VG_OCC_POINTS;  // points per lane (amortise the per-map loads)
+// The reference's key of one point (fp64 transform + exact floor), out of line: the fp32 screen
+// keeps the kernel's registers for the common path.
+__device__ __noinline__ uint4 exact_probe_key(const double* T, float x, float y, float z, double res, double inv_res) {
+  double e0, e1, e2, l0, l1, l2;
+  apply_pose_rn(T, x, y, z, e0, e1, e2);
+  unsigned k0 = 0, k1 = 0, k2 = 0;
+  const bool ok = voxel_key(e0, e1, e2, res, inv_res, k0, k1, k2, l0, l1, l2);
+  return make_uint4(k0, k1, k2, ok ? 1u : 0u);
+}
+__global__ void __launch_bounds__(256, 4) overlap_occ_kernel(const OverlapItem* __restrict__ items,
+                                                             const int2* __restrict__ chunks,
+                                                             unsigned long long* __restrict__ hits) {
+  __shared__ unsigned cnt[kOvMaps];
+  __shared__ OccScreen scr[kOvMaps];
+  const int2 ch = chunks[blockIdx.y];
+  const unsigned n = items[ch.x].n;
+  if (blockIdx.x * (256 * kOccPoints) >= n) return;
+  for (int t = threadIdx.x; t < ch.y * 7; t += 256)  // stage the chunk's screens (7 × 16 B each)
+    reinterpret_cast<uint4*>(&scr[t / 7])[t % 7] = __ldg(reinterpret_cast<const uint4*>(&items[ch.x + t / 7].scr) + t % 7);
+  if (threadIdx.x < kOvMaps) cnt[threadIdx.x] = 0;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned base = blockIdx.x * (256 * kOccPoints) + warp * (32 * kOccPoints);
+  const PointBlock* __restrict__ blk = items[ch.x].blk;
+  float px[kOccPoints], py[kOccPoints], pz[kOccPoints], p1[kOccPoints];
+  unsigned in = 0;
+#pragma unroll
+  for (int u = 0; u < kOccPoints; ++u) {
+    const unsigned i = base + u * 32 + lane;
+    const unsigned ic = min(i, n - 1);
+    const float4 a = __ldg(&blk[ic / kPointBlock].pa[ic % kPointBlock]);
+    px[u] = a.x, py[u] = a.y, pz[u] = a.z;
+    p1[u] = fabsf(a.x) + fabsf(a.y) + fabsf(a.z);
+    in |= (i < n ? 1u : 0u) << u;
+  }
+  __syncthreads();
+  for (int k = 0; k < ch.y; ++k) {
+    const OccScreen& sc = scr[k];
+    unsigned word[kOccPoints], bit[kOccPoints];
+    unsigned ok = 0, need = 0;
+#pragma unroll
+    for (int u = 0; u < kOccPoints; ++u) {
+      const float q0 = fmaf(sc.R[2], pz[u], fmaf(sc.R[1], py[u], sc.R[0] * px[u])) + sc.t[0];
+      const float q1 = fmaf(sc.R[5], pz[u], fmaf(sc.R[4], py[u], sc.R[3] * px[u])) + sc.t[1];
+      const float q2 = fmaf(sc.R[8], pz[u], fmaf(sc.R[7], py[u], sc.R[6] * px[u])) + sc.t[2];
+      const float y0 = q0 * sc.inv_r, y1 = q1 * sc.inv_r, y2 = q2 * sc.inv_r;
+      const float c0 = floorf(y0), c1 = floorf(y1), c2 = floorf(y2);
+      const float h = 0.5f - fmaf(sc.A2, p1[u], sc.C);  // NaN / far points fail the test below
+      const bool sure = fabsf((y0 - c0) - 0.5f) <= h && fabsf((y1 - c1) - 0.5f) <= h && fabsf((y2 - c2) - 0.5f) <= h;
+      const unsigned rx = static_cast<unsigned>(__float2int_rz(c0) - sc.cx0);
+      const unsigned ry = static_cast<unsigned>(__float2int_rz(c1) - sc.cy0);
+      const unsigned rz = static_cast<unsigned>(__float2int_rz(c2) - sc.cz0);
+      word[u] = ((rx >> 2) * sc.nby + (ry >> 2)) * sc.nbz + (rz >> 2);
+      bit[u] = ((rx & 3u) << 4) | ((ry & 3u) << 2) | (rz & 3u);
+      const bool inside = (rx < sc.ex) & (ry < sc.ey) & (rz < sc.ez);
+      ok |= (sure && inside ? 1u : 0u) << u;
+      need |= (sure ? 0u : 1u) << u;
+    }
+    ok &= in;
+    need &= in;
+    if (__any_sync(0xffffffffu, need != 0u)) {  // rare: within the margin of a face, or non-finite
+      const OverlapItem& it = items[ch.x + k];
+#pragma unroll
+      for (int u = 0; u < kOccPoints; ++u) {
+        if (!((need >> u) & 1u)) continue;
+        const uint4 e = exact_probe_key(it.T, px[u], py[u], pz[u], it.map.res, it.map.inv_res);
+        const unsigned rx = e.x - (static_cast<unsigned>(sc.cx0) + (1u << 20));
+        const unsigned ry = e.y - (static_cast<unsigned>(sc.cy0) + (1u << 20));
+        const unsigned rz = e.z - (static_cast<unsigned>(sc.cz0) + (1u << 20));
+        word[u] = ((rx >> 2) * sc.nby + (ry >> 2)) * sc.nbz + (rz >> 2);
+        bit[u] = ((rx & 3u) << 4) | ((ry & 3u) << 2) | (rz & 3u);
+        ok |= (e.w != 0u && (rx < sc.ex) & (ry < sc.ey) & (rz < sc.ez) ? 1u : 0u) << u;
+      }
+    }
+    unsigned long long v[kOccPoints];
+#pragma unroll
+    for (int u = 0; u < kOccPoints; ++u) v[u] = ((ok >> u) & 1u) ? __ldg(sc.occ + word[u]) : 0ull;
+    unsigned c = 0;
+#pragma unroll
+    for (int u = 0; u < kOccPoints; ++u) c += static_cast<unsigned>((v[u] >> (bit[u] & 63u)) & 1ull);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0 && c) atomicAdd(&cnt[k], c);
+  }
+  __syncthreads();
+  if (threadIdx.x < ch.y && cnt[threadIdx.x])
+    atomicAdd(&hits[ch.x + threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
+}
+
+cudaError_t launch_overlap_occ(const OverlapItem* items, const int2* chunks, int num_chunks, unsigned max_n,
+                               unsigned long long* hits, cudaStream_t s) {
+  if (num_chunks <= 0 || max_n == 0) return cudaSuccess;
+  for (int c0 = 0; c0 < num_chunks; c0 += 65535) {
+    const dim3 grid((max_n + 256 * kOccPoints - 1) / (256 * kOccPoints), std::min(65535, num_chunks - c0));
+    overlap_occ_kernel<<<grid, 256, 0, s>>>(items, chunks + c0, hits);
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_overlap_multi(const OverlapItem* items, const int2* chunks, int num_chunks, unsigned max_n,

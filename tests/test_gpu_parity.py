@@ -235,6 +235,29 @@ def test_overlap_batch_matches_serial(ctx):  # test_reference.cpp:59-69
         assert r == O.overlap_rate(qm, rel, omap, serial=True)
 
 
+@pytest.mark.parametrize("res", [0.25, 1.0, 2.0])
+def test_overlap_occupancy_bitmap_equals_hash_probe(ctx, monkeypatch, res):
+    """Overlap through the maps' occupancy bitmaps (default) vs through the cuckoo-hash probes
+    (maps built with VGICP_NO_OCCUPANCY=1) vs the oracle: identical hit counts, including points
+    on brick / box faces, outside the occupied box and beyond the ±2^20 key range."""
+    rng = O.Rng(93)
+    means, covs = rng.gaussian_cloud(5000, 12.0)
+    means[:50] = np.round(means[:50] / res) * res  # exactly on voxel faces
+    c, m, c9 = gpu_cloud(ctx, means, covs)
+    g_occ = V.GaussianVoxelMap(c, res)
+    monkeypatch.setenv("VGICP_NO_OCCUPANCY", "1")
+    g_hash = V.GaussianVoxelMap(c, res)
+    monkeypatch.delenv("VGICP_NO_OCCUPANCY")
+    q, qm, _ = gpu_cloud(ctx, np.concatenate([rng.gaussian_cloud(3000, 14.0)[0], [[1e7, 0.0, 0.0], [-3e6, 1.0, 2.0]]]))
+    omap = O.OracleMap(m, c9, res)
+    rels = [rng.random_pose(0.3, 2.0) for _ in range(12)] + [O.IDENTITY]
+    h_occ = V.overlap_hits([q] * len(rels), rels, [g_occ] * len(rels))
+    h_hash = V.overlap_hits([q] * len(rels), rels, [g_hash] * len(rels))
+    assert list(h_occ) == list(h_hash)
+    for T, h in zip(rels, h_occ):
+        assert h == O.overlap_hits(qm, T, omap)
+
+
 # ------------------------------------------------------------------------------ factors
 def factor_case(ctx, sm, sc, tm, tc, res):
     src, smm, sc9 = gpu_cloud(ctx, sm, sc)
