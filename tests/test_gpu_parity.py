@@ -258,6 +258,51 @@ def test_overlap_occupancy_bitmap_equals_hash_probe(ctx, monkeypatch, res):
         assert h == O.overlap_hits(qm, T, omap)
 
 
+@pytest.mark.parametrize("res,shift", [(1.0, 0.0), (0.25, 1500.0), (2.0, -8000.0), (0.1, 300.0)])
+def test_overlap_fp32_screen_near_faces(ctx, res, shift):
+    """The occupancy kernel's fp32 screen must reproduce the reference's fp64 floor exactly: query
+    points are placed so that their transformed positions sit at 0, 1e-9 .. 1e-3 voxel from voxel
+    faces (large translations included), against a checkerboard map where any floor error flips
+    the occupancy of the point. Counts must equal the oracle's for every pose."""
+    rng = np.random.default_rng(int(res * 100) + int(abs(shift)))
+    # checkerboard map: voxel centres with (x + y + z) even, around the origin
+    g = np.arange(-12, 12)
+    cx, cy, cz = np.meshgrid(g, g, np.arange(-3, 3), indexing="ij")
+    even = ((cx + cy + cz) % 2) == 0
+    centres = (np.stack([cx[even], cy[even], cz[even]], 1) + 0.5) * res
+    map_pts = np.asarray(centres, np.float32).astype(np.float64)
+    mc, mm, mc9 = gpu_cloud(ctx, map_pts, O.unit_covariances(len(map_pts)))
+    gmap = V.GaussianVoxelMap(mc, res)
+    omap = O.OracleMap(mm, mc9, res)
+    eps = np.array([0.0, 1e-9, -1e-9, 1e-7, -1e-7, 1e-6, -1e-6, 1e-5, -1e-5, 1e-4, -1e-4, 1e-3, -1e-3])
+    rels, clouds, qms = [], [], []
+    for trial in range(6):
+        ang = rng.normal(size=3) * 0.4
+        th = np.linalg.norm(ang)
+        K = np.array([[0, -ang[2], ang[1]], [ang[2], 0, -ang[0]], [-ang[1], ang[0], 0]]) / max(th, 1e-12)
+        R = np.eye(3) + np.sin(th) * K + (1 - np.cos(th)) * K @ K
+        t = rng.normal(size=3) * 5.0 + np.array([shift, -0.5 * shift, 0.0])
+        T = np.concatenate([R.ravel(), t])
+        # targets in the map frame: near faces on one, two or three axes
+        k = rng.integers(-11, 11, size=(4000, 3)).astype(np.float64)
+        k[:, 2] = rng.integers(-3, 3, size=4000)
+        frac = rng.uniform(0.05, 0.95, size=(4000, 3))
+        on = rng.integers(0, 2, size=(4000, 3)).astype(bool)
+        frac[on] = rng.choice(eps, size=on.sum())
+        q = (k + frac) * res
+        p = (q - t) @ R  # R^T (q - t)
+        qm = np.asarray(p, np.float32).astype(np.float64)
+        c, qmm, _ = gpu_cloud(ctx, qm)
+        rels.append(T)
+        clouds.append(c)
+        qms.append(qmm)
+    hits = V.overlap_hits(clouds, rels, [gmap] * len(rels))
+    for T, qm, h in zip(rels, qms, hits):
+        ref = O.overlap_hits(qm, T, omap)
+        assert h == ref, (h, ref)
+        assert 0 < ref < len(qm)
+
+
 # ------------------------------------------------------------------------------ factors
 def factor_case(ctx, sm, sc, tm, tc, res):
     src, smm, sc9 = gpu_cloud(ctx, sm, sc)
