@@ -31,6 +31,8 @@ __all__ = [
     "GaussianVoxelMap",
     "overlap_rate",
     "overlap_rates",
+    "overlap_hits",
+    "MapSet",
     "MatchingCostFactor",
     "LinearizedFactor",
     "GicpErrorResult",
@@ -390,9 +392,27 @@ def overlap_rate(cloud: PointCloud, pose_rel, voxelmap: GaussianVoxelMap) -> flo
     return r.value
 
 
+class MapSet:
+    """A fixed sequence of voxel maps with its handle array built once (e.g. the keyframe maps a new
+    frame is swept against, pipeline.cpp:135-150): overlap_hits(cloud, poses, map_set) then skips
+    the per-call marshalling of thousands of handles."""
+
+    def __init__(self, maps):
+        self.maps = list(maps)
+        self.handles = np.fromiter((x.handle.value for x in self.maps), dtype=np.uint64, count=len(self.maps))
+        self.ctx = self.maps[0].ctx if self.maps else None
+
+    def __len__(self) -> int:
+        return len(self.maps)
+
+    def __iter__(self):
+        return iter(self.maps)
+
+
 def overlap_hits(clouds, poses, maps) -> np.ndarray:
-    """Exact hit counts of m (cloud, pose, map) probes in one launch."""
-    maps = list(maps)
+    """Exact hit counts of m (cloud, pose, map) probes in one launch. `maps` may be a MapSet."""
+    map_set = maps if isinstance(maps, MapSet) else None
+    maps = map_set.maps if map_set is not None else list(maps)
     m = len(maps)
     single_cloud = isinstance(clouds, PointCloud)
     if single_cloud:
@@ -412,13 +432,14 @@ def overlap_hits(clouds, poses, maps) -> np.ndarray:
         ch = np.full(m, clouds[0].handle.value, np.uint64)
     else:
         ch = np.fromiter((c.handle.value for c in clouds), dtype=np.uint64, count=m)
-    mh = np.fromiter((x.handle.value for x in maps), dtype=np.uint64, count=m)
+    mh = map_set.handles if map_set is not None else np.fromiter((x.handle.value for x in maps), dtype=np.uint64,
+                                                                  count=m)
     check(_lib.load().vgicp_overlap_batch(ctx.handle, _ptr(ch), _ptr(P), _ptr(mh), m, _ptr(hits)))
     return hits
 
 
 def overlap_rates(clouds, poses, maps) -> np.ndarray:
-    maps = list(maps)
+    maps = maps if isinstance(maps, MapSet) else list(maps)
     hits = overlap_hits(clouds, poses, maps)
     sizes = np.array([c.size() for c in ([clouds] * len(maps) if isinstance(clouds, PointCloud) else clouds)], np.float64)
     return hits.astype(np.float64) / sizes

@@ -233,6 +233,7 @@ def test_overlap_batch_matches_serial(ctx):  # test_reference.cpp:59-69
     rates = V.overlap_rates(qc, rels, [g] * 10)
     for rel, r in zip(rels, rates):
         assert r == O.overlap_rate(qm, rel, omap, serial=True)
+    assert np.array_equal(V.overlap_rates(qc, rels, V.MapSet([g] * 10)), rates)  # cached handle array
 
 
 @pytest.mark.parametrize("res", [0.25, 1.0, 2.0])
