@@ -12,6 +12,7 @@ from .vgicp import (
     GaussianVoxelMap,
     GicpErrorResult,
     LinearizedFactor,
+    MapSet,
     MatchingCostFactor,
     PointCloud,
     Submap,
@@ -38,6 +39,7 @@ __all__ = [
     "VgicpError",
     "Context",
     "FactorGraph",
+    "MapSet",
     "GaussianVoxelMap",
     "GicpErrorResult",
     "LinearizedFactor",

@@ -353,12 +353,12 @@ int vgicp_cloud_destroy(vgicp_cloud cloud) {
 // ------------------------------------------------------------------------------------ voxel maps
 static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map* out);
 
-// Occupancy bitmaps (overlap query) for freshly built maps: one word per 4×4×4 brick of the
-// occupied voxel box; maps whose box would need more than kOccMaxWords words keep hash probes.
-// `d_jobs` is device scratch for at least m OccJob records.
-constexpr size_t kOccMaxWords = size_t(1) << 22;  // 32 MB per map
-static_assert(sizeof(OccJob) <= sizeof(InsertJob), "occupancy jobs reuse the insert-job scratch");
-static int build_occupancy(vgicp_ctx ctx, vgicp_map* maps, int m, void* d_jobs, cudaStream_t s) {
+// Occupancy bitmaps + rank-ordered statistics for freshly built maps: one 16-B record per 4×4×4
+// brick of the occupied voxel box; maps whose box would need more than kOccMaxWords records keep
+// hash probes only. `hot` / `vbase` are the build's per-voxel fp32 statistics.
+constexpr size_t kOccMaxWords = size_t(1) << 21;  // 32 MB of records per map
+static int build_occupancy(vgicp_ctx ctx, vgicp_map* maps, int m, const VoxelStats* hot,
+                           const std::vector<unsigned>& vbase, cudaStream_t s) {
   if (std::getenv("VGICP_NO_OCCUPANCY")) return VGICP_OK;  // measurement switch (hash probes only)
   std::vector<OccJob> jobs;
   unsigned max_words = 0, max_v = 0;
@@ -372,27 +372,32 @@ static int build_occupancy(vgicp_ctx ctx, vgicp_map* maps, int m, void* d_jobs, 
       words *= (e[a] + 3) / 4;
     }
     if (words > kOccMaxWords) continue;
-    VG_CUDA(dmalloc(ctx, &mp->occ_mem, sizeof(unsigned long long) * words));
+    const size_t V = mp->voxels;
+    const size_t b_occ = align_up(sizeof(OccWord) * words, 256), b_ra = align_up(sizeof(SlotStatsA) * V, 256);
+    VG_CUDA(dmalloc(ctx, &mp->occ_mem, b_occ + b_ra + sizeof(SlotStatsB) * V));
+    char* base = static_cast<char*>(mp->occ_mem);
     OccDev& o = mp->occ;
-    o.occ = static_cast<const unsigned long long*>(mp->occ_mem);
+    o.occ = reinterpret_cast<const OccWord*>(base);
     o.kx0 = static_cast<unsigned>(mp->cmin[0] + (1 << 20));
     o.ky0 = static_cast<unsigned>(mp->cmin[1] + (1 << 20));
     o.kz0 = static_cast<unsigned>(mp->cmin[2] + (1 << 20));
     o.ex = e[0], o.ey = e[1], o.ez = e[2];
     o.nby = (e[1] + 3) / 4, o.nbz = (e[2] + 3) / 4;
-    jobs.push_back(OccJob{mp->keys, static_cast<unsigned long long*>(mp->occ_mem), static_cast<unsigned>(mp->voxels),
-                          static_cast<unsigned>(words), o.kx0, o.ky0, o.kz0, o.nby, o.nbz, 0u});
+    mp->ra = reinterpret_cast<SlotStatsA*>(base + b_occ);
+    mp->rb = reinterpret_cast<SlotStatsB*>(base + b_occ + b_ra);
+    jobs.push_back(OccJob{mp->keys, reinterpret_cast<OccWord*>(base), mp->ra, mp->rb, static_cast<unsigned>(V),
+                          static_cast<unsigned>(words), o.kx0, o.ky0, o.kz0, o.nby, o.nbz, vbase[k]});
     max_words = std::max(max_words, static_cast<unsigned>(words));
-    max_v = std::max(max_v, static_cast<unsigned>(mp->voxels));
+    max_v = std::max(max_v, static_cast<unsigned>(V));
   }
   if (jobs.empty()) return VGICP_OK;
-  for (size_t j0 = 0; j0 < jobs.size(); j0 += static_cast<size_t>(m)) {  // d_jobs holds m records
-    const int nj = static_cast<int>(std::min(jobs.size() - j0, static_cast<size_t>(m)));
-    VG_CUDA(cudaMemcpyAsync(d_jobs, jobs.data() + j0, sizeof(OccJob) * nj, cudaMemcpyHostToDevice, s));
-    VG_CUDA(launch_occ_build(static_cast<const OccJob*>(d_jobs), nj, max_words, max_v, s));
-    ctx->launches += 2;
-    VG_CUDA(cudaStreamSynchronize(s));  // d_jobs is reused
-  }
+  DevBuf d_jobs(ctx);
+  VG_CUDA(d_jobs.alloc(sizeof(OccJob) * jobs.size()));
+  VG_CUDA(cudaMemcpyAsync(d_jobs.p, jobs.data(), sizeof(OccJob) * jobs.size(), cudaMemcpyHostToDevice, s));
+  VG_CUDA(launch_occ_build(static_cast<const OccJob*>(d_jobs.p), static_cast<int>(jobs.size()), max_words, max_v, hot,
+                           s));
+  ctx->launches += 4;
+  VG_CUDA(cudaStreamSynchronize(s));  // the job array is freed on return
   return VGICP_OK;
 }
 
@@ -621,7 +626,7 @@ static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map*
   }
   for (int k = 0; k < m; ++k)
     for (int a = 0; a < 3; ++a) maps[k]->cmin[a] = hbox[6 * k + a], maps[k]->cmax[a] = hbox[6 * k + 3 + a];
-  if (int rc = build_occupancy(ctx, maps.data(), m, d_jobs, s)) {
+  if (int rc = build_occupancy(ctx, maps.data(), m, d_hot, hbase, s)) {
     cleanup();
     return rc;
   }
@@ -1080,12 +1085,16 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   std::vector<FactorDev> fd(num_factors);
   std::vector<WorkItem> items;
   uint64_t points = 0;
+  // rank lookups (occupancy bitmap + rank-ordered statistics) when every target map carries them;
+  // VGICP_NO_RANK=1 keeps the cuckoo-hash probes (measurement switch)
+  bool rank = std::getenv("VGICP_NO_RANK") == nullptr;
+  for (int f = 0; f < num_factors && rank; ++f) rank = factors[f].target->occ.occ != nullptr;
   for (int f = 0; f < num_factors; ++f) {
     const vgicp_factor_desc& d = factors[f];
     FactorDev& x = fd[f];
     const int fchunk = !split ? chunk : (num_factors < slots ? few_chunk : (f >= num_factors - slots ? small_chunk : chunk));
     x.blk = d.source->sblk;  // Morton order: neighbouring lanes probe neighbouring voxels
-    x.map = d.target->dev();
+    x.map = rank ? d.target->dev_rank() : d.target->dev();
     x.n = static_cast<int>(d.source->n);
     x.tgt = d.target_index;
     x.src = d.source_index;
@@ -1101,6 +1110,7 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   gr->num_poses = num_poses;
   gr->num_items = static_cast<int>(items.size());
   gr->num_points = points;
+  gr->rank_lookup = rank;
   const size_t nf = std::max(num_factors, 1), ni = std::max<size_t>(items.size(), 1);
   size_t off = 0;
   auto carve = [&](size_t bytes) {
@@ -1188,7 +1198,7 @@ int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, dou
   if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_out || !d_inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   DeviceGuard g(graph->ctx->device);
-  VG_CUDA(launch_factor(true, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
+  VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
                         graph->d_part_inl, graph->d_counters, d_out, d_inliers, graph->ctx->stream));
   graph->ctx->launches += graph->num_items > 0 ? 1 : 0;
   return VGICP_OK;
@@ -1198,7 +1208,7 @@ int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, doub
   if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_errors || !d_inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   DeviceGuard g(graph->ctx->device);
-  VG_CUDA(launch_factor(false, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
+  VG_CUDA(launch_factor(false, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
                         graph->d_part_inl, graph->d_counters, d_errors, d_inliers, graph->ctx->stream));
   graph->ctx->launches += graph->num_items > 0 ? 1 : 0;
   return VGICP_OK;
@@ -1248,7 +1258,7 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
   VG_CUDA(cudaMemcpyAsync(graph->d_poses, poses_pinned ? poses12 : h_poses, pose_bytes, cudaMemcpyHostToDevice, s));
   double* d_res = zero_copy ? m_res : (linearize ? graph->d_out : graph->d_err);
   int32_t* d_inl = zero_copy ? m_inl : graph->d_out_inl;
-  VG_CUDA(launch_factor(linearize, graph->d_factors, graph->d_items, graph->num_items, graph->d_poses,
+  VG_CUDA(launch_factor(linearize, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->d_poses,
                         graph->d_partials, graph->d_part_inl, graph->d_counters, d_res, d_inl, s));
   ctx->launches += 1;
   if (!zero_copy) {
@@ -1365,7 +1375,7 @@ int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, do
   std::memcpy(h, poses12, pose_bytes);
   VG_CUDA(cudaMemcpyAsync(graph->d_poses, h, pose_bytes, cudaMemcpyHostToDevice, s));
   if (graph->num_items > 0) {
-    VG_CUDA(launch_factor(true, graph->d_factors, graph->d_items, graph->num_items, graph->d_poses, graph->d_partials,
+    VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->d_poses, graph->d_partials,
                           graph->d_part_inl, graph->d_counters, graph->d_out, graph->d_out_inl, s));
     ctx->launches += 1;
   } else if (graph->num_factors > 0) {
@@ -1389,7 +1399,7 @@ int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_po
   DeviceGuard g(graph->ctx->device);
   cudaStream_t s = graph->ctx->stream;
   if (graph->num_items > 0) {
-    VG_CUDA(launch_factor(true, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
+    VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
                           graph->d_part_inl, graph->d_counters, graph->d_out, graph->d_out_inl, s));
     graph->ctx->launches += 1;
   } else if (graph->num_factors > 0) {

@@ -344,10 +344,13 @@ struct __align__(128) FactorSmem {
 };
 static_assert(sizeof(WarpTile) * kStages >= sizeof(double) * 180, "epilogue scratch must fit in the warp's ring");
 
-template <bool kLinearize>
 #ifndef VG_MINB
 #define VG_MINB 2
 #endif
+// kRank: the target maps carry occupancy bitmaps with brick ranks and rank-ordered statistics
+// (MapDev::sa / sb indexed by rank): a probe is ONE 16-B load of the brick record, spatially
+// coherent across the Morton-ordered lanes, instead of two hash-bucket loads (one of them random).
+template <bool kLinearize, bool kRank>
 __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
     const FactorDev* __restrict__ factors, const WorkItem* __restrict__ items, const double* __restrict__ poses,
     double* __restrict__ partials, int* __restrict__ part_inl, unsigned* __restrict__ counters,
@@ -438,11 +441,43 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
       double ld0, ld1, ld2;
       ok[u] = voxel_key(qd0, qd1, qd2, map.res, map.inv_res, k0, k1, k2, ld0, ld1, ld2) && (p < tile_n);
       l0[u] = (float)ld0, l1[u] = (float)ld1, l2[u] = (float)ld2;
-      pack_key32(k0, k1, k2, hi[u], lo[u]);
-      b1[u] = bucket1(k0, k1, k2, map.shift);
-      b2[u] = bucket2(k0, k1, k2, map.shift);
+      if constexpr (kRank) {  // biased voxel coordinates, located in the bitmap below
+        b1[u] = k0, b2[u] = k1, hi[u] = k2;
+      } else {
+        pack_key32(k0, k1, k2, hi[u], lo[u]);
+        b1[u] = bucket1(k0, k1, k2, map.shift);
+        b2[u] = bucket2(k0, k1, k2, map.shift);
+      }
       q0[u] = (float)qd0, q1[u] = (float)qd1, q2[u] = (float)qd2;
     }
+    if constexpr (kRank) {
+      // ---- rank lookups: brick record (bits, rank) of every point first, then the hit test ----
+      unsigned word[kILP], bit[kILP];
+      bool in_box[kILP];
+#pragma unroll
+      for (int u = 0; u < kILP; ++u) in_box[u] = ok[u] && occ_locate(map.occ, b1[u], b2[u], hi[u], word[u], bit[u]);
+      uint4 rec[kILP];
+#pragma unroll
+      for (int u = 0; u < kILP; ++u)
+        rec[u] = in_box[u] ? __ldg(reinterpret_cast<const uint4*>(map.occ.occ + word[u])) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int u = 0; u < kILP; ++u) {
+        const unsigned long long bits = (static_cast<unsigned long long>(rec[u].y) << 32) | rec[u].x;
+        const bool hit = (bits >> bit[u]) & 1ull;
+        const int s = static_cast<int>(rec[u].z + static_cast<unsigned>(__popcll(bits & ((1ull << bit[u]) - 1ull))));
+        const unsigned ball = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int p = u * 32 + lane;
+          const unsigned idx = (tail + __popc(ball & lane_lt)) % static_cast<unsigned>(kQueue);
+          const float4 B = tb.pb[p];
+          hq.a[idx] = make_float4(l0[u], l1[u], l2[u], q0[u]);
+          hq.b[idx] = make_float4(q1[u], q2[u], __int_as_float(s), kLinearize ? tb.pa[p].w : cxx[u]);
+          hq.c[idx] = B;
+          hq.d[idx] = tb.pc[p];
+        }
+        tail += __popc(ball);
+      }
+    } else {
 #if VG_B2_LAZY
     // bucket1 first; the alternative bucket is read only when bucket1 is full and misses (a key
     // lives in its bucket2 only if its bucket1 was full when it was placed, and slots never empty)
@@ -500,6 +535,7 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
       }
       tail += __popc(ball);
     }
+    }  // kRank
     __syncwarp();  // queue entries visible; the warp is done with this ring slot
     if (lane == 0 && k + kStages < my_tiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async refill
@@ -586,25 +622,27 @@ cudaError_t launch_assemble(const int* out_ptr, const int* contrib, int num_slot
   return cudaGetLastError();
 }
 
-cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkItem* items, int num_items,
+cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, const WorkItem* items, int num_items,
                           const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
                           int* out_inl, cudaStream_t s) {
   if (num_items <= 0) return cudaSuccess;
   constexpr size_t kSmem = sizeof(FactorSmem);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(factor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-    if (e != cudaSuccess) return e;
+    for (const void* k : {reinterpret_cast<const void*>(factor_kernel<true, false>),
+                          reinterpret_cast<const void*>(factor_kernel<false, false>),
+                          reinterpret_cast<const void*>(factor_kernel<true, true>),
+                          reinterpret_cast<const void*>(factor_kernel<false, true>)}) {
+      const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+      if (e != cudaSuccess) return e;
+    }
     configured = true;
   }
-  if (linearize)
-    factor_kernel<true><<<num_items, kFactorThreads, kSmem, s>>>(factors, items, poses, partials, part_inl, counters,
-                                                                out, out_inl);
-  else
-    factor_kernel<false><<<num_items, kFactorThreads, kSmem, s>>>(factors, items, poses, partials, part_inl,
-                                                                 counters, out, out_inl);
+  auto go = [&](auto kernel) {
+    kernel<<<num_items, kFactorThreads, kSmem, s>>>(factors, items, poses, partials, part_inl, counters, out, out_inl);
+  };
+  if (linearize) rank ? go(factor_kernel<true, true>) : go(factor_kernel<true, false>);
+  else rank ? go(factor_kernel<false, true>) : go(factor_kernel<false, false>);
   return cudaGetLastError();
 }
 

@@ -64,7 +64,7 @@ struct alignas(16) OccScreen {
   int cx0, cy0, cz0;
   unsigned ex, ey, ez, nby, nbz;
   unsigned pad[2];
-  const unsigned long long* occ;
+  const OccWord* occ;
 };
 static_assert(sizeof(OccScreen) == 112, "OccScreen is staged as 7 uint4");
 struct OverlapItem {
@@ -79,15 +79,19 @@ struct OverlapItem {
 static_assert(offsetof(OverlapItem, scr) % 16 == 0 && sizeof(OverlapItem) % 16 == 0, "OccScreen is read as uint4");
 cudaError_t launch_overlap_occ(const OverlapItem* items, const int2* chunks, int num_chunks, unsigned max_n,
                                unsigned long long* hits, cudaStream_t s);
-// Occupancy bitmap build job for one map (cold keys -> bits).
+// Occupancy bitmap build job for one map (cold keys -> bits -> brick ranks -> rank-ordered stats).
 struct OccJob {
   const unsigned long long* keys;
-  unsigned long long* occ;
+  OccWord* occ;
+  SlotStatsA* ra;
+  SlotStatsB* rb;
   unsigned V;
   unsigned words;
-  unsigned kx0, ky0, kz0, nby, nbz, pad;
+  unsigned kx0, ky0, kz0, nby, nbz;
+  unsigned vbase;  // first voxel of this map in the build's VoxelStats array
 };
-cudaError_t launch_occ_build(const OccJob* jobs, int m, unsigned max_words, unsigned max_v, cudaStream_t s);
+cudaError_t launch_occ_build(const OccJob* jobs, int m, unsigned max_words, unsigned max_v, const VoxelStats* hot,
+                             cudaStream_t s);
 
 struct BuildSeg {
   const float4* pa;           // float32 device cloud (input order) ...
@@ -157,7 +161,7 @@ cudaError_t launch_build_insert(const InsertJob* jobs, int m, unsigned max_v, in
 cudaError_t launch_build_place(const InsertJob* jobs, int m, unsigned max_v, const VoxelStats* hot, cudaStream_t s);
 cudaError_t launch_lookup(MapDev map, const double* pts, size_t n, unsigned long long* keys_out, cudaStream_t s);
 cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsigned long long* hits, cudaStream_t s);
-cudaError_t launch_factor(bool linearize, const FactorDev* factors, const WorkItem* items, int num_items,
+cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, const WorkItem* items, int num_items,
                           const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
                           int* out_inl, cudaStream_t s);
 cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s);
@@ -278,10 +282,14 @@ struct vgicp_map_s {
   unsigned long long* tkeys = nullptr;
   vgicp::SlotStatsA* sa = nullptr;
   vgicp::SlotStatsB* sb = nullptr;
-  void* occ_mem = nullptr;  // occupancy bitmap (overlap query), null when the box is too large
+  void* occ_mem = nullptr;  // occupancy bitmap + rank-ordered statistics; null when the box is too large
   vgicp::OccDev occ{};
+  vgicp::SlotStatsA* ra = nullptr;  // statistics by rank (brick order), for rank lookups
+  vgicp::SlotStatsB* rb = nullptr;
   std::atomic<int> refs{1};
-  vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov64, res, inv_res, shift, 0u}; }
+  vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov64, res, inv_res, shift, 0u, occ}; }
+  // rank lookups: slot statistics replaced by the rank-ordered copies (requires occ)
+  vgicp::MapDev dev_rank() const { return vgicp::MapDev{tkeys, ra, rb, cov64, res, inv_res, shift, 0u, occ}; }
 };
 
 struct vgicp_graph_s {
@@ -316,4 +324,5 @@ struct vgicp_graph_s {
   int band_cluster = 0;
   int band_bw = -1;
   int band_epoch = 0;
+  bool rank_lookup = false;  // factor kernels probe occupancy bitmaps (every target map has one)
 };

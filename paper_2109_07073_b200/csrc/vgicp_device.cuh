@@ -43,22 +43,19 @@ struct __align__(8) SlotStatsB {
   int vid;
 };
 
-struct MapDev {
-  const unsigned long long* keys;  // capacity = kBucket * num_buckets, kEmptyKey when free
-  const SlotStatsA* sa;            // per slot
-  const SlotStatsB* sb;            // per slot
-  const double* cov64;             // V×9 row-major fp64 covariances (cold)
-  double res;
-  double inv_res;
-  unsigned shift;                  // 32 - log2(num_buckets)
+// Occupancy bitmap of a map's occupied voxel box: one 16-B record per 4×4×4 brick of voxels
+// (bricks row-major, z fastest; bit (x&3)<<4 | (y&3)<<2 | (z&3) of the box-relative coordinate)
+// holding the brick's 64 occupancy bits and the rank of its first occupied voxel. The overlap query
+// needs only the bits; the factor kernels turn a hit into the voxel's rank (brick rank + popcount
+// of the lower bits), which indexes rank-ordered statistics — one coherent 16-B load per probe
+// instead of two hash-bucket loads. occ == nullptr: probe the hash table.
+struct __align__(16) OccWord {
+  unsigned long long bits;  // brick occupancy
+  unsigned rank;            // occupied voxels in all earlier bricks (rank of the brick's first voxel)
   unsigned pad;
 };
-
-// Occupancy bitmap of a map's occupied voxel box, for the overlap query (occupancy is all it
-// needs): one 64-bit word per 4×4×4 brick of voxels, bricks row-major (z fastest), bit
-// (x&3)<<4 | (y&3)<<2 | (z&3) of the box-relative voxel coordinate. occ == nullptr: probe the hash.
 struct OccDev {
-  const unsigned long long* occ;
+  const OccWord* occ;
   unsigned kx0, ky0, kz0;  // biased (key) coordinates of the box's lower corner
   unsigned ex, ey, ez;     // box extent in voxels
   unsigned nby, nbz;       // bricks along y and z
@@ -71,6 +68,18 @@ __device__ __forceinline__ bool occ_locate(const OccDev& o, unsigned k0, unsigne
   bit = ((rx & 3u) << 4) | ((ry & 3u) << 2) | (rz & 3u);
   return (rx < o.ex) & (ry < o.ey) & (rz < o.ez);
 }
+
+struct MapDev {
+  const unsigned long long* keys;  // capacity = kBucket * num_buckets, kEmptyKey when free
+  const SlotStatsA* sa;            // per slot
+  const SlotStatsB* sb;            // per slot
+  const double* cov64;             // V×9 row-major fp64 covariances (cold)
+  double res;
+  double inv_res;
+  unsigned shift;                  // 32 - log2(num_buckets)
+  unsigned pad;
+  OccDev occ;                      // occupancy bitmap; factor graphs in rank mode index sa / sb by rank
+};
 
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256).
 __device__ __forceinline__ void ldg256(const void* p, unsigned& r0, unsigned& r1, unsigned& r2, unsigned& r3,

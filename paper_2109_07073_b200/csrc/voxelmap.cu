@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(256, VG_OV_MINB) overlap_kernel(const OverlapI
           unsigned k0 = 0, k1 = 0, k2 = 0, word = 0;
           const bool ok = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && i < n &&
                           occ_locate(occ, k0, k1, k2, word, bit[u]);
-          wv[u] = ok ? __ldg(occ.occ + word) : 0ull;
+          wv[u] = ok ? __ldg(&occ.occ[word].bits) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < kOverlapILP; ++u) count += static_cast<unsigned>((wv[u] >> bit[u]) & 1ull);
@@ -456,52 +456,34 @@ __global__ void __launch_bounds__(256) overlap_multi_kernel(const OverlapItem* _
     unsigned hi[2][kOvPoints], lo[2][kOvPoints], b1[2][kOvPoints], b2[2][kOvPoints];
     bool ok[2][kOvPoints];
     const MapDev* mp[2];
-    bool use_occ[2];
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
       const int kk = min(k + w, mc - 1);
       const OverlapItem& it = items[m0 + kk];
       mp[w] = &it.map;
       const MapDev& map = it.map;
-      use_occ[w] = it.occ.occ != nullptr;  // uniform over the CTA
 #pragma unroll
       for (int u = 0; u < kOvPoints; ++u) {
         double q0, q1, q2, l0, l1, l2;
         apply_pose_rn(it.T, px[u], py[u], pz[u], q0, q1, q2);
         unsigned k0 = 0, k1 = 0, k2 = 0;
         ok[w][u] = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && in[u] && (k + w < mc);
-        if (use_occ[w]) {  // occupancy bitmap: word index in b1, bit in b2
-          ok[w][u] = ok[w][u] && occ_locate(it.occ, k0, k1, k2, b1[w][u], b2[w][u]);
-        } else {
-          pack_key32(k0, k1, k2, hi[w][u], lo[w][u]);
-          b1[w][u] = bucket1(k0, k1, k2, map.shift);
-          b2[w][u] = bucket2(k0, k1, k2, map.shift);
-        }
+        pack_key32(k0, k1, k2, hi[w][u], lo[w][u]);
+        b1[w][u] = bucket1(k0, k1, k2, map.shift);
+        b2[w][u] = bucket2(k0, k1, k2, map.shift);
       }
     }
     BucketPair bp[2][kOvPoints];
 #pragma unroll
-    for (int w = 0; w < 2; ++w) {
-      if (use_occ[w]) {
-        const unsigned long long* occ = items[m0 + min(k + w, mc - 1)].occ.occ;
+    for (int w = 0; w < 2; ++w)
 #pragma unroll
-        for (int u = 0; u < kOvPoints; ++u) {
-          const unsigned long long v = ok[w][u] ? __ldg(occ + b1[w][u]) : 0ull;
-          bp[w][u].a.x = static_cast<unsigned>((v >> b2[w][u]) & 1ull);
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < kOvPoints; ++u) bp[w][u] = load_buckets(mp[w]->keys, b1[w][u], b2[w][u]);
-      }
-    }
+      for (int u = 0; u < kOvPoints; ++u) bp[w][u] = load_buckets(mp[w]->keys, b1[w][u], b2[w][u]);
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
       unsigned c = 0;
 #pragma unroll
       for (int u = 0; u < kOvPoints; ++u)
-        if (use_occ[w] ? bp[w][u].a.x != 0u
-                       : (ok[w][u] && match_buckets(bp[w][u], b1[w][u], b2[w][u], hi[w][u], lo[w][u]) >= 0))
-          ++c;
+        if (ok[w][u] && match_buckets(bp[w][u], b1[w][u], b2[w][u], hi[w][u], lo[w][u]) >= 0) ++c;
       c = __reduce_add_sync(0xffffffffu, c);
       if ((threadIdx.x & 31) == 0 && c) atomicAdd(&cnt[k + w < mc ? k + w : 0], c);
     }
@@ -511,28 +493,87 @@ __global__ void __launch_bounds__(256) overlap_multi_kernel(const OverlapItem* _
     atomicAdd(&hits[m0 + threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
 }
 
-// Occupancy bitmaps of a batch of maps: zero every word, then set one bit per voxel key.
+// Occupancy bitmaps of a batch of maps: zero every record, set one bit per voxel key, rank the
+// bricks (exclusive prefix of their popcounts, one CTA per map), then scatter every voxel's fp32
+// statistics to its rank (rank-ordered copies of the hash table's slot statistics).
 __global__ void occ_zero_kernel(const OccJob* __restrict__ jobs) {
   const OccJob& j = jobs[blockIdx.y];
-  for (unsigned w = blockIdx.x * blockDim.x + threadIdx.x; w < j.words; w += gridDim.x * blockDim.x) j.occ[w] = 0ull;
+  for (unsigned w = blockIdx.x * blockDim.x + threadIdx.x; w < j.words; w += gridDim.x * blockDim.x)
+    j.occ[w] = OccWord{0ull, 0u, 0u};
+}
+__device__ __forceinline__ void occ_coords(const OccJob& j, unsigned long long key, unsigned& word, unsigned& bit) {
+  const unsigned k0 = static_cast<unsigned>(key >> 42) & 0x1FFFFFu;
+  const unsigned k1 = static_cast<unsigned>(key >> 21) & 0x1FFFFFu;
+  const unsigned k2 = static_cast<unsigned>(key) & 0x1FFFFFu;
+  const unsigned rx = k0 - j.kx0, ry = k1 - j.ky0, rz = k2 - j.kz0;
+  word = ((rx >> 2) * j.nby + (ry >> 2)) * j.nbz + (rz >> 2);
+  bit = ((rx & 3u) << 4) | ((ry & 3u) << 2) | (rz & 3u);
 }
 __global__ void occ_set_kernel(const OccJob* __restrict__ jobs) {
   const OccJob& j = jobs[blockIdx.y];
   for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < j.V; v += gridDim.x * blockDim.x) {
-    const unsigned long long key = j.keys[v];
-    const unsigned k0 = static_cast<unsigned>(key >> 42) & 0x1FFFFFu;
-    const unsigned k1 = static_cast<unsigned>(key >> 21) & 0x1FFFFFu;
-    const unsigned k2 = static_cast<unsigned>(key) & 0x1FFFFFu;
-    const unsigned rx = k0 - j.kx0, ry = k1 - j.ky0, rz = k2 - j.kz0;
-    const unsigned word = ((rx >> 2) * j.nby + (ry >> 2)) * j.nbz + (rz >> 2);
-    atomicOr(j.occ + word, 1ull << (((rx & 3u) << 4) | ((ry & 3u) << 2) | (rz & 3u)));
+    unsigned word, bit;
+    occ_coords(j, j.keys[v], word, bit);
+    atomicOr(&j.occ[word].bits, 1ull << bit);
+  }
+}
+__global__ void __launch_bounds__(1024) occ_rank_kernel(const OccJob* __restrict__ jobs) {
+  const OccJob& j = jobs[blockIdx.x];
+  __shared__ unsigned warp_sums[32];
+  __shared__ unsigned carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (unsigned w0 = 0; w0 < j.words; w0 += 1024) {
+    const unsigned w = w0 + threadIdx.x;
+    const unsigned c = w < j.words ? static_cast<unsigned>(__popcll(j.occ[w].bits)) : 0u;
+    unsigned x = c;  // inclusive warp scan
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= static_cast<unsigned>(off)) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned t = warp_sums[lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, t, off);
+        if (lane >= static_cast<unsigned>(off)) t += y;
+      }
+      warp_sums[lane] = t;  // inclusive prefix over warps
+    }
+    __syncthreads();
+    const unsigned before = carry + (warp ? warp_sums[warp - 1] : 0u) + (x - c);
+    if (w < j.words) j.occ[w].rank = before;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_sums[31];
+    __syncthreads();
+  }
+}
+__global__ void occ_place_kernel(const OccJob* __restrict__ jobs, const VoxelStats* __restrict__ hot) {
+  const OccJob& j = jobs[blockIdx.y];
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < j.V; v += gridDim.x * blockDim.x) {
+    unsigned word, bit;
+    occ_coords(j, j.keys[v], word, bit);
+    const OccWord o = j.occ[word];
+    const unsigned rank = o.rank + static_cast<unsigned>(__popcll(o.bits & ((1ull << bit) - 1ull)));
+    const VoxelStats h = hot[j.vbase + v];
+    SlotStatsA a;
+    a.mx = h.mx, a.my = h.my, a.mz = h.mz, a.cxx = h.cxx, a.cxy = h.cxy, a.cxz = h.cxz, a.cyy = h.cyy, a.cyz = h.cyz;
+    j.ra[rank] = a;
+    j.rb[rank] = SlotStatsB{h.czz, h.vid};
   }
 }
 
-cudaError_t launch_occ_build(const OccJob* jobs, int m, unsigned max_words, unsigned max_v, cudaStream_t s) {
+cudaError_t launch_occ_build(const OccJob* jobs, int m, unsigned max_words, unsigned max_v, const VoxelStats* hot,
+                             cudaStream_t s) {
   if (m <= 0) return cudaSuccess;
   occ_zero_kernel<<<dim3(grid_for(max_words, 256, 1024), m), 256, 0, s>>>(jobs);
   occ_set_kernel<<<dim3(grid_for(max_v, 256, 1024), m), 256, 0, s>>>(jobs);
+  occ_rank_kernel<<<m, 1024, 0, s>>>(jobs);
+  occ_place_kernel<<<dim3(grid_for(max_v, 256, 1024), m), 256, 0, s>>>(jobs, hot);
   return cudaGetLastError();
 }
 
@@ -624,7 +665,7 @@ __global__ void __launch_bounds__(256, 4) overlap_occ_kernel(const OverlapItem* 
     }
     unsigned long long v[kOccPoints];
 #pragma unroll
-    for (int u = 0; u < kOccPoints; ++u) v[u] = ((ok >> u) & 1u) ? __ldg(sc.occ + word[u]) : 0ull;
+    for (int u = 0; u < kOccPoints; ++u) v[u] = ((ok >> u) & 1u) ? __ldg(&sc.occ[word[u]].bits) : 0ull;
     unsigned c = 0;
 #pragma unroll
     for (int u = 0; u < kOccPoints; ++u) c += static_cast<unsigned>((v[u] >> (bit[u] & 63u)) & 1ull);
