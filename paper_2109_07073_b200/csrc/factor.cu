@@ -56,6 +56,9 @@ __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, f
 #ifndef VG_B2_LAZY
 #define VG_B2_LAZY 0  // read bucket2 only when bucket1 is full and misses
 #endif
+#ifndef VG_PREFETCH
+#define VG_PREFETCH 0  // rank lookups: L1 prefetch of a hit's statistics at append time (1: 32-B part, 2: both)
+#endif
 #ifndef VG_STAGES
 #define VG_STAGES 2
 #endif
@@ -468,6 +471,12 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
         const unsigned ball = __ballot_sync(0xffffffffu, hit);
         if (hit) {
           const int p = u * 32 + lane;
+#if VG_PREFETCH >= 1  // pull the hit's statistics into L1 now; the math phase gathers them soon after
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(map.sa + s));
+#endif
+#if VG_PREFETCH >= 2
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(map.sb + s));
+#endif
           const unsigned idx = (tail + __popc(ball & lane_lt)) % static_cast<unsigned>(kQueue);
           const float4 B = tb.pb[p];
           hq.a[idx] = make_float4(l0[u], l1[u], l2[u], q0[u]);
