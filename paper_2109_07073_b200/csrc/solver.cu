@@ -10,7 +10,9 @@
 // Kernel: one thread-block cluster of C CTAs (the cluster launch guarantees co-residency). Column k
 // is owned by CTA k mod C and lives in its shared memory from the step it is first touched until
 // it is factored. Step j: every CTA receives panel j (L_jj, L_ij, y_j) — the owner from its own
-// shared memory, the others from L2 once the owner's release flag carries this launch's epoch;
+// shared memory, the owner of column j+1 (the only CTA on the dependency chain) over DSMEM from the
+// owner's slot after a release flag in its own shared memory, the others from L2 once the owner's
+// global release flag carries this launch's epoch;
 // the owner of column j+1 applies panel j to it first, factors it (6×6 Cholesky, TRSM of the
 // sub-diagonal blocks and of the augmented row) and publishes it (global memory + flag); every
 // CTA applies panel j to its other columns in the window. No cluster barrier inside the loop:
@@ -18,11 +20,13 @@
 // Afterwards CTA 0 runs the backward substitution (one warp, columns TMA-prefetched two ahead).
 // Fixed operation order everywhere: results are deterministic.
 //
-// Measured on C3 (449 slots, RCM block bandwidth 31, 16-CTA cluster): 2.4 ms per damped solve vs
-// 1.8 ms for the dense cuSOLVER potrf/potrs of the 2,694-dim system — the 449-step dependency
-// chain (panel hand-off through L2 + 6×6 pivots) costs ~5k cycles per step. The dense path stays
-// the LM's default up to 6,000 unknowns; the band solver takes over beyond (memory O(S·bw) instead
-// of O(S²), time O(S·bw²) instead of O(S³)).
+// Measured on C3 (449 slots, RCM block bandwidth 31, 16-CTA cluster): 1.86 ms per damped solve vs
+// 1.84 ms for the dense cuSOLVER potrf/potrs of the 2,694-dim system. The 449-step dependency chain
+// costs ~4.3k cycles per step (DSMEM hand-off to the next owner ~1.2k, its update + 6×6 Cholesky +
+// TRSM ~3.1k) and the backward substitution ~1.3k per step. The dense path stays the LM's default
+// up to 6,000 unknowns; the band solver takes over beyond (memory O(S·bw) instead of O(S²), time
+// O(S·bw²) instead of O(S³)). Build with -DVG_SOLVE_PROF=1 for a per-phase cycle profile
+// (printed with VGICP_SOLVE_PROF=1).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -39,6 +43,9 @@ namespace vgicp {
 namespace {
 
 constexpr int kSolveThreads = 256;
+#ifndef VG_SOLVE_PROF
+#define VG_SOLVE_PROF 0
+#endif
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -129,22 +136,21 @@ __device__ void update_columns(const SolveArgs& a, double* slots, const double* 
   const int cs = col_stride(a.d.bw);
   const int aug = col_aug(a.d.bw);
   if (lo > hi) return;
-  // tasks per column: (R - k + 1)·6 rows + 1 augmented row
-  int counts[16];
-  int ncol = 0, total = 0;
-  for (int k = lo; k <= hi && ncol < 16; k += C) {
-    counts[ncol++] = (R - k + 1) * 6 + 1;
-    total += counts[ncol - 1];
-  }
+  // tasks of the c-th column k = lo + c·C: (R - k + 1)·6 entry rows + 1 augmented row (decreasing
+  // by 6·C per column; no per-thread array, which would live in local memory)
+  const int ncol = (hi - lo) / C + 1;
+  const int first = (R - lo + 1) * 6 + 1;
+  const int total = ncol * first - 3 * C * ncol * (ncol - 1);
   for (int t = threadIdx.x; t < total; t += kSolveThreads) {
-    int c = 0, u = t;
-    while (u >= counts[c]) u -= counts[c++];
+    int c = 0, u = t, cnt = first;
+    while (u >= cnt) u -= cnt, cnt -= 6 * C, ++c;
     const int k = lo + c * C;
+    const int counts_c = cnt;
     double* col = slots + (size_t)((k / C) % a.ns) * cs;
     const double* Lk = pj + 36 * (k - j);
     const double* Li;
     double* dst;
-    if (u < counts[c] - 1) {
+    if (u < counts_c - 1) {
       const int b = u / 6, r = u % 6;  // block row i = k + b, entry row r
       Li = pj + 36 * (k + b - j) + 6 * r;
       dst = col + 36 * b + 6 * r;
@@ -179,31 +185,35 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
 __device__ void factor_column(const SolveArgs& a, double* col, int k) {
   const int aug = col_aug(a.d.bw);
   double* inv = col + aug + 8;
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double row[6];
+  if (threadIdx.x == 0) {  // one thread: the pivot chain is short, shuffles would only add latency
+    double L[6][6];
 #pragma unroll
-    for (int c = 0; c < 6; ++c) row[c] = lane < 6 ? col[6 * lane + c] : 0.0;
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+      for (int c = 0; c <= r; ++c) L[r][c] = col[6 * r + c];
     bool failed = false;
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
-      // lane c: pivot; lanes > c: column entries
-      double s = row[c];
+      double piv = L[c][c];
 #pragma unroll
-      for (int m = 0; m < c; ++m) s -= row[m] * __shfl_sync(0xffffffffu, row[m], c);
-      const double piv = __shfl_sync(0xffffffffu, s, c);
-      if (!(piv > 0.0)) failed = true;  // warp-uniform
+      for (int m = 0; m < c; ++m) piv -= L[c][m] * L[c][m];
+      failed |= !(piv > 0.0);
       const double il = rsqrt_fast(piv);
-      const double l = piv * il;
-      if (lane == c) row[c] = l;
-      if (lane > c && lane < 6) row[c] = s * il;
-      if (lane == 0) inv[c] = il;
-    }
-    if (lane < 6) {
+      L[c][c] = piv * il;
+      inv[c] = il;
 #pragma unroll
-      for (int c = 0; c < 6; ++c) col[6 * lane + c] = c <= lane ? row[c] : 0.0;
+      for (int r = c + 1; r < 6; ++r) {
+        double v = L[r][c];
+#pragma unroll
+        for (int m = 0; m < c; ++m) v -= L[r][m] * L[c][m];
+        L[r][c] = v * il;
+      }
     }
-    if (lane == 0) col[aug + 6] = failed ? 1.0 : 0.0;
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) col[6 * r + c] = c <= r ? L[r][c] : 0.0;
+    col[aug + 6] = failed ? 1.0 : 0.0;
   }
   __syncthreads();
   if (col[aug + 6] != 0.0) return;
@@ -224,6 +234,86 @@ __device__ void factor_column(const SolveArgs& a, double* col, int k) {
   __syncthreads();
 }
 
+// Column n1 on the dependency chain, at step j: panel j applied to it (when it reaches n1) and the
+// column factored, overlapped — warp 0 updates the diagonal block and runs the 6×6 Cholesky while
+// the other warps update the sub-diagonal rows and the augmented row; then every thread solves
+// its TRSM rows. Same arithmetic (and order per entry) as update_columns + factor_column.
+__device__ void chain_column(const SolveArgs& a, double* col, const double* pj, int j, int n1, int R, bool upd) {
+  const int aug = col_aug(a.d.bw);
+  double* inv = col + aug + 8;
+  const double* Lk = pj + 36 * (n1 - j);  // L_{n1,j}
+  auto upd_row = [&](double* dst, const double* Li) {
+    const double l0 = Li[0], l1 = Li[1], l2 = Li[2], l3 = Li[3], l4 = Li[4], l5 = Li[5];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const double* m = Lk + 6 * q;
+      const double s = ((((l0 * m[0] + l1 * m[1]) + l2 * m[2]) + l3 * m[3]) + l4 * m[4]) + l5 * m[5];
+      dst[q] -= s;
+    }
+  };
+  if (threadIdx.x < 32) {
+    if (upd && threadIdx.x < 6) upd_row(col + 6 * threadIdx.x, Lk + 6 * threadIdx.x);
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      double L[6][6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) L[r][c] = col[6 * r + c];
+      bool failed = false;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        double piv = L[c][c];
+#pragma unroll
+        for (int m = 0; m < c; ++m) piv -= L[c][m] * L[c][m];
+        failed |= !(piv > 0.0);
+        const double il = rsqrt_fast(piv);
+        L[c][c] = piv * il;
+        inv[c] = il;
+#pragma unroll
+        for (int r = c + 1; r < 6; ++r) {
+          double v = L[r][c];
+#pragma unroll
+          for (int m = 0; m < c; ++m) v -= L[r][m] * L[c][m];
+          L[r][c] = v * il;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) col[6 * r + c] = c <= r ? L[r][c] : 0.0;
+      col[aug + 6] = failed ? 1.0 : 0.0;
+    }
+  } else if (upd) {
+    const int rows = (R - n1) * 6;  // sub-diagonal entry rows touched by panel j, then the aug row
+    for (int t = threadIdx.x - 32; t <= rows; t += kSolveThreads - 32) {
+      if (t < rows) {
+        const int b = 1 + t / 6, r = t % 6;
+        upd_row(col + 36 * b + 6 * r, pj + 36 * (n1 + b - j) + 6 * r);
+      } else {
+        upd_row(col + aug, pj + aug);
+      }
+    }
+  }
+  __syncthreads();
+  if (col[aug + 6] != 0.0) return;
+  const int nrows = (a.d.reach[n1] - n1) * 6 + 1;
+  for (int t = threadIdx.x; t < nrows; t += kSolveThreads) {
+    double* v = t < nrows - 1 ? col + 36 + 6 * t : col + aug;
+    double x[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      double s = v[c];
+#pragma unroll
+      for (int r = 0; r < c; ++r) s -= x[r] * col[6 * c + r];
+      x[c] = s * inv[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) v[c] = x[c];
+  }
+  __syncthreads();
+}
+
 __device__ void copy_record(double* __restrict__ dst, const double* __restrict__ src, int n) {
   const double2* s = reinterpret_cast<const double2*>(src);
   double2* o = reinterpret_cast<double2*>(dst);
@@ -232,7 +322,7 @@ __device__ void copy_record(double* __restrict__ dst, const double* __restrict__
 
 __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs a) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) unsigned long long bbars[2];
+  __shared__ __align__(8) unsigned long long bbars[3];
   cg::cluster_group cluster = cg::this_cluster();  // a cluster launch guarantees the CTAs are co-resident
   const BandDev& d = a.d;
   const int C = static_cast<int>(cluster.num_blocks());
@@ -246,10 +336,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
   const auto panel_bytes = [&](int k) { return static_cast<unsigned>(sizeof(double) * (rec_len(k) + 16)); };
   const auto slot_of = [&](int k) { return slots + (size_t)((k / C) % a.ns) * cs; };
 
+  __shared__ int crit_flag;  // written remotely by owner(j) when column j is factored (value j)
   if (threadIdx.x == 0) {
     bar_init(&bbars[0]);
     bar_init(&bbars[1]);
+    bar_init(&bbars[2]);
+    crit_flag = -1;
   }
+  cluster.sync();  // every CTA's flag is initialised before any remote release can reach it
 
   int next = rank;  // next owned column not yet loaded
   auto ensure_loaded = [&](int limit) {
@@ -261,7 +355,18 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
     }
   };
   // Factored column k -> global memory, then a release flag (ready[k] = this launch's epoch).
+  // Factored column k is published twice: to owner(k+1) — the only CTA on the dependency chain —
+  // by a release store into ITS shared-memory flag (it then pulls the record from this CTA's slot
+  // over DSMEM; the slot stays intact until owner(k+1) has published k+1, by the chain itself), and
+  // to everybody else through L2 (record + release flag in global memory).
   auto publish = [&](int k) {
+    // factor_column ended with a CTA barrier: the slot is complete; release it to owner(k+1) first
+    if (threadIdx.x == 0 && k + 1 < S && (k + 1) % C != rank) {
+      const unsigned remote = static_cast<unsigned>(__cvta_generic_to_shared(&crit_flag));
+      unsigned raddr;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(remote), "r"((k + 1) % C));
+      asm volatile("st.release.cluster.shared::cluster.b32 [%0], %1;" ::"r"(raddr), "r"(k) : "memory");
+    }
     const double* col = slot_of(k);
     double* g = d.Lg + (size_t)k * cs;
     copy_record(g, col, rec_len(k));
@@ -277,6 +382,18 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
       const double* col = slot_of(j);
       copy_record(pj, col, rec_len(j));
       copy_record(pj + aug, col + aug, 16);
+    } else if (j + 1 < S && (j + 1) % C == rank) {  // on the chain: local flag, then a DSMEM pull
+      if (threadIdx.x == 0) {
+        const unsigned f = static_cast<unsigned>(__cvta_generic_to_shared(&crit_flag));
+        int v;
+        do {
+          asm volatile("ld.acquire.cluster.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(f) : "memory");
+        } while (v != j);
+      }
+      __syncthreads();
+      const double* src = cluster.map_shared_rank(slot_of(j), j % C);
+      copy_record(pj, src, rec_len(j));
+      copy_record(pj + aug, src + aug, 16);
     } else {
       if (threadIdx.x == 0) {
         int v;
@@ -304,9 +421,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
     }
   }
   int failed_at = -1;
-  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // rank 0 / thread 0 cycle profile (VGICP_SOLVE_PROF)
+#if VG_SOLVE_PROF  // rank 0 / thread 0 cycle profile, read by VGICP_SOLVE_PROF=1 (diagnostic build)
+  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t0 = clock64(), t1;
 #define VG_TICK(q) (t1 = clock64(), tp[q] += t1 - t0, t0 = t1)
+#else
+#define VG_TICK(q) ((void)0)
+#endif
   for (int j = 0; j < S; ++j) {
     const int R = d.reach[j];
     const int n1 = j + 1;
@@ -316,22 +437,19 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
       failed_at = j;
       break;
     }
-    ensure_loaded(max(R, n1 < S ? n1 : -1));
-    VG_TICK(1);
     // owned columns in (j, R]
     int lo = j + 1 + ((rank - (j + 1)) % C + C) % C;
-    if (n1 < S && n1 % C == rank) {
-      if (n1 <= R) {
-        update_columns(a, slots, pj, j, R, n1, n1, C);
-        __syncthreads();
-      }
+    if (n1 < S && n1 % C == rank) {  // on the chain: only column n1 must be resident first
+      ensure_loaded(n1);
       VG_TICK(6);
-      factor_column(a, slot_of(n1), n1);
+      chain_column(a, slot_of(n1), pj, j, n1, R, n1 <= R);
       VG_TICK(7);
       publish(n1);
       lo = n1 + C;
     }
     VG_TICK(2);
+    ensure_loaded(max(R, n1 < S ? n1 : -1));
+    VG_TICK(1);
     update_columns(a, slots, pj, j, R, lo, R, C);
     __syncthreads();
     VG_TICK(3);
@@ -339,69 +457,94 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
   if (failed_at >= 0 && rank == 0 && threadIdx.x == 0) *d.status = failed_at + 1;
   cluster.sync();  // every column published
   VG_TICK(4);
-  if (failed_at >= 0 || rank != 0 || threadIdx.x >= 32) return;
 
-  // ---- backward substitution Lᵀx = y (block_solver.cpp:108-114) by warp 0 of CTA 0: columns from
-  //      the last one, each prefetched two ahead into shared memory by bulk copies; x kept in a
-  //      ring of bw + 1 block rows; partial sums in a fixed lane order + xor tree ----
-  const int lane = threadIdx.x;
-  double* buf[2] = {slots, slots + cs};
-  double* xr = slots + 2 * (size_t)cs;  // (bw + 1) × 6
-  const int W = d.bw + 1;
-  auto fetch = [&](int k) {
-    const int q = (S - 1 - k) & 1;
+  // ---- backward substitution Lᵀx = y (block_solver.cpp:108-114) on CTA 0, pipelined over two
+  //      roles: x_k = L_kk⁻ᵀ(y_k - P_k - L_{k+1,k}ᵀ x_{k+1}) is the only dependent step (warp 0),
+  //      while warps 1..6 form P_{k-1} = Σ_{b>=2} L_{k-1+b,k-1}ᵀ x_{k-1+b} (all of those x are
+  //      known) for the next step. Columns stream through a ring of 3 shared-memory buffers by bulk
+  //      copies; x lives in a ring of bw + 1 block rows. Fixed orders: deterministic. ----
+  if (failed_at >= 0 || rank != 0) return;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const auto buf = [&](int q) { return slots + (size_t)q * cs; };  // ring slot q of 3
+  double* xr = slots + 3 * (size_t)cs;  // W × 6 (W <= 2·(bw + 1) <= a record's length)
+  __shared__ double Pbuf[2][6];
+  __shared__ double vbuf[6];
+  int W = 1;  // x ring: power of two >= bw + 1, so ring indices are masks
+  while (W < d.bw + 1) W <<= 1;
+  const int wm = W - 1;
+  auto fetch = [&](int k) {  // column k -> ring slot (S - 1 - k) % 3, barrier of that slot
+    const int q = (S - 1 - k) % 3;
     bar_expect(&bbars[q], panel_bytes(k));
-    bulk_copy(buf[q], d.Lg + (size_t)k * cs, static_cast<unsigned>(sizeof(double) * rec_len(k)), &bbars[q]);
-    bulk_copy(buf[q] + aug, d.Lg + (size_t)k * cs + aug, static_cast<unsigned>(sizeof(double) * 16), &bbars[q]);
+    bulk_copy(buf(q), d.Lg + (size_t)k * cs, static_cast<unsigned>(sizeof(double) * rec_len(k)), &bbars[q]);
+    bulk_copy(buf(q) + aug, d.Lg + (size_t)k * cs + aug, static_cast<unsigned>(sizeof(double) * 16), &bbars[q]);
   };
-  asm volatile("fence.proxy.async;" ::: "memory");  // Lg / slots were written by generic stores
-  __syncwarp();
-  if (lane == 0) {
-    if (S > 0) fetch(S - 1);
-    if (S > 1) fetch(S - 2);
+  auto wait_col = [&](int k) {
+    const int u = S - 1 - k;
+    bar_wait(&bbars[u % 3], static_cast<unsigned>((u / 3) & 1));
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async;" ::: "memory");  // Lg / slots were written by generic stores
+    for (int k = S - 1; k >= 0 && k >= S - 3; --k) fetch(k);
   }
+  if (threadIdx.x < 6) Pbuf[(S - 1) & 1][threadIdx.x] = 0.0;  // column S-1 has no rows below
+  __syncthreads();
   for (int k = S - 1; k >= 0; --k) {
-    const int q = (S - 1 - k) & 1;
-    bar_wait(&bbars[q], static_cast<unsigned>(((S - 1 - k) >> 1) & 1));
-    const double* L = buf[q];
-    const int nb = d.reach[k] - k;
-    double s[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int t = lane; t < 6 * nb; t += 32) {
-      const int bb = 1 + t / 6, r = t % 6;
-      const double xv = xr[((k + bb) % W) * 6 + r];
-      const double* Lr = L + 36 * bb + 6 * r;  // row r of L_{k+bb,k}
+    wait_col(k);
+    if (k > 0) wait_col(k - 1);
+    const double* L = buf((S - 1 - k) % 3);
+    if (warp == 0) {  // the chain: x_k
+      const int nb = d.reach[k] - k;
+      if (lane < 6) {  // lane c: v_c = y_c - P_c - (L_{k+1,k}ᵀ x_{k+1})_c
+        double t = 0.0;
+        if (nb >= 1) {
+          const double* x1 = xr + ((k + 1) & wm) * 6;
 #pragma unroll
-      for (int c = 0; c < 6; ++c) s[c] += Lr[c] * xv;
+          for (int r = 0; r < 6; ++r) t += L[36 + 6 * r + lane] * x1[r];
+        }
+        vbuf[lane] = L[aug + lane] - Pbuf[k & 1][lane] - t;
+      }
+      __syncwarp();
+      double x[6];  // every lane solves L_kkᵀ x = v in registers (no shuffles on the chain)
+#pragma unroll
+      for (int c = 5; c >= 0; --c) {
+        double w = vbuf[c];
+#pragma unroll
+        for (int r = c + 1; r < 6; ++r) w -= L[6 * r + c] * x[r];
+        x[c] = w * L[aug + 8 + c];
+      }
+      if (lane < 6) {
+        double xc = x[0];
+#pragma unroll
+        for (int c = 1; c < 6; ++c) xc = lane == c ? x[c] : xc;
+        xr[(k & wm) * 6 + lane] = xc;
+        d.x[(size_t)d.perm[k] * 6 + lane] = xc;
+      }
+    } else if (warp <= 6 && k > 0) {  // P_{k-1}, component c = warp - 1
+      const int c = warp - 1;
+      const int k1 = k - 1;
+      const double* L1 = buf((S - 1 - k1) % 3);
+      const int nb1 = d.reach[k1] - k1;
+      double sum = 0.0;
+      for (int t = lane; t < 6 * (nb1 - 1); t += 32) {  // blocks b = 2 .. nb1
+        const int bb = 2 + t / 6, r = t % 6;
+        sum += L1[36 * bb + 6 * r + c] * xr[((k1 + bb) & wm) * 6 + r];
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      if (lane == 0) Pbuf[k1 & 1][c] = sum;
     }
-#pragma unroll
-    for (int c = 0; c < 6; ++c) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) s[c] += __shfl_xor_sync(0xffffffffu, s[c], off);
-    }
-    double x[6];
-#pragma unroll
-    for (int c = 5; c >= 0; --c) {
-      double v = L[aug + c] - s[c];
-#pragma unroll
-      for (int r = c + 1; r < 6; ++r) v -= L[6 * r + c] * x[r];
-      x[c] = v * L[aug + 8 + c];
-    }
-    if (lane < 6) {
-      double xc = x[0];
-#pragma unroll
-      for (int c = 1; c < 6; ++c) xc = lane == c ? x[c] : xc;
-      xr[(k % W) * 6 + lane] = xc;
-      d.x[(size_t)d.perm[k] * 6 + lane] = xc;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0 && k >= 2) fetch(k - 2);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads of buf before its refill
+    __syncthreads();
+    if (threadIdx.x == 0 && k >= 3) fetch(k - 3);  // into column k's (now free) ring slot
   }
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     *d.status = 0;
+#if VG_SOLVE_PROF
     VG_TICK(5);
     unsigned long long* prof = reinterpret_cast<unsigned long long*>(d.status) + 8;
     for (int q = 0; q < 8; ++q) prof[q] = static_cast<unsigned long long>(tp[q]);
+#endif
   }
 #undef VG_TICK
 }
@@ -511,7 +654,7 @@ BandPlanHost make_band_plan(int S, int P, const int32_t* pairs) {
 }
 
 size_t band_smem_bytes(int bw, int C) {
-  const int ns = std::max(bw / C + 1, 3);  // >= 3: the backward substitution reuses the slot area
+  const int ns = std::max(bw / C + 1, 4);  // >= 4: the backward substitution reuses the slot area
   const size_t rec = sizeof(double) * col_stride(bw);
   return (ns + 1) * rec;
 }
@@ -556,7 +699,7 @@ cudaError_t launch_band_solve(const BandDev& d, int C, const double* assembled, 
   a.off = assembled + (size_t)d.S * 36;
   a.rhs = assembled + (size_t)(d.S + num_pairs) * 36;
   a.lam = lam;
-  a.ns = std::max(d.bw / C + 1, 3);
+  a.ns = std::max(d.bw / C + 1, 4);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(kSolveThreads);
