@@ -23,8 +23,9 @@
 // Measured on C3 (449 slots, RCM block bandwidth 31, 16-CTA cluster): 1.86 ms per damped solve vs
 // 1.84 ms for the dense cuSOLVER potrf/potrs of the 2,694-dim system. The 449-step dependency chain
 // costs ~4.3k cycles per step (DSMEM hand-off to the next owner ~1.2k, its update + 6×6 Cholesky +
-// TRSM ~3.1k) and the backward substitution ~1.3k per step. The dense path stays the LM's default
-// up to 6,000 unknowns; the band solver takes over beyond (memory O(S·bw) instead of O(S²), time
+// TRSM ~3.1k) and the backward substitution ~1.3k per step. C5 (999 slots, bandwidth 47): 4.1 ms vs
+// 5.3 ms dense. The dense path stays the LM's default up to 3,000 unknowns; the band solver takes
+// over beyond (memory O(S·bw) instead of O(S²), time
 // O(S·bw²) instead of O(S³)). Build with -DVG_SOLVE_PROF=1 for a per-phase cycle profile
 // (printed with VGICP_SOLVE_PROF=1).
 #include <cooperative_groups.h>
