@@ -270,6 +270,13 @@ def run_lm_c2(ctx, threads):
     LM.optimize(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=2))  # warm-up
     poses, rep = LM.optimize(wl.graph, wl.poses)
     its = sorted(rep.iteration_seconds)
+    LM.optimize_native(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=2))  # warm-up
+    _, nrep = LM.optimize_native(wl.graph, wl.poses)
+    nits = sorted(nrep.iteration_seconds)
+    native = {"ms_per_lm_iteration_median": 1e3 * nits[len(nits) // 2] if nits else None,
+              "iterations": nrep.iterations, "final_error": nrep.final_error, "reason": nrep.reason,
+              "band_solver": nrep.band_solver,
+              "note": "native LM (vgicp_graph_optimize): device linearize + assembly, device block-band Cholesky"}
     cpu = None
     try:  # the same LM around the CPU oracle port (reference arm of "ms per LM iteration")
         all_threads = os.cpu_count() or 1
@@ -289,34 +296,40 @@ def run_lm_c2(ctx, threads):
         "note": "host LM (paper_2109_07073_b200/optimizer.py, banded Cholesky) around one linearize + device "
                 "assembly launch per candidate (speculative: its errors score the candidate); wall clock incl. H2D/D2H",
         "cpu_port": cpu,
+        "native": native,
     }
 
 
 def run_lm_c3(wl, max_iterations=30):
-    """Full LM on the C3 graph itself (4,445 factors, 450 poses) from the odometry initial guess:
-    device linearization + device assembly, dense GPU Cholesky of the 2,694-dim reduced system
-    (loop closures make it non-banded), one error launch per candidate; wall clock."""
+    """Full LM on the C3 graph itself (4,445 factors, 450 poses) from the odometry initial guess.
+    Primary: the native loop in the library (vgicp_graph_optimize: device linearization + assembly
+    of every candidate, its errors as total_error, device block-band Cholesky, host retraction).
+    Beside it: the Python mirror (speculative, dense cuSOLVER Cholesky) and the reference loop order."""
     from paper_2109_07073_b200 import optimizer as LM
 
+    med = lambda r: 1e3 * sorted(r.iteration_seconds)[len(r.iteration_seconds) // 2] if r.iteration_seconds else None  # noqa: E731
+    LM.optimize_native(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=2))  # warm-up
+    _, rep = LM.optimize_native(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=max_iterations))
     LM.optimize(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=2))  # warm-up
-    poses, rep = LM.optimize(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=max_iterations))
-    its = sorted(rep.iteration_seconds)
+    _, srep = LM.optimize(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=max_iterations))
     _, prep = LM.optimize(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=max_iterations),
                           speculative=False)
-    pits = sorted(prep.iteration_seconds)
     return {
         "factors": wl.num_factors, "poses": len(wl.poses), "iterations": rep.iterations,
-        "ms_per_lm_iteration_median": 1e3 * its[len(its) // 2] if its else None,
+        "ms_per_lm_iteration_median": med(rep), "ms_per_lm_iteration_mean": 1e3 * rep.wall_time_seconds / max(1, rep.iterations),
         "ms_total": 1e3 * rep.wall_time_seconds, "initial_error": rep.initial_error, "final_error": rep.final_error,
-        "reason": rep.reason,
-        "note": "speculative LM: each candidate is linearized + device-assembled (its errors equal evaluate's "
-                "bit for bit), so an accepted step needs no second factor pass; dense cuSOLVER Cholesky per "
-                "damping trial (system never leaves the GPU); wall clock",
-        "plain_loop": {"ms_per_lm_iteration_median": 1e3 * pits[len(pits) // 2] if pits else None,
-                       "iterations": prep.iterations, "final_error": prep.final_error,
-                       "identical_trace": [t.error for t in prep.trace] == [t.error for t in rep.trace],
+        "reason": rep.reason, "solves": rep.solves, "linearizations": rep.linearizations,
+        "note": "native LM (vgicp_graph_optimize): each candidate linearized + device-assembled (its errors equal "
+                "evaluate's bit for bit, so an accepted step needs no second pass), device block-band Cholesky "
+                "per damping trial, host retraction; wall clock",
+        "python_speculative": {"ms_per_lm_iteration_median": med(srep), "iterations": srep.iterations,
+                               "final_error": srep.final_error, "ms_total": 1e3 * srep.wall_time_seconds,
+                               "note": "paper_2109_07073_b200/optimizer.py, dense cuSOLVER Cholesky"},
+        "plain_loop": {"ms_per_lm_iteration_median": med(prep), "iterations": prep.iterations,
+                       "final_error": prep.final_error,
+                       "identical_trace": [t.error for t in prep.trace] == [t.error for t in srep.trace],
                        "note": "reference loop order: one evaluate launch per candidate + a re-linearization "
-                               "per accepted step"},
+                               "per accepted step (Python)"},
     }
 
 
@@ -354,14 +367,17 @@ def run_c5(ctx, steps=10):
     by_res = {str(r): sum(1 for k in range(F) if W.C5_RESOLUTIONS[k % 3] == r) for r in W.C5_RESOLUTIONS}
     from paper_2109_07073_b200 import optimizer as LM
 
-    LM.optimize(g, wl.poses, settings=LM.LmSettings(max_iterations=1))  # warm-up (plan, solver)
-    _, rep = LM.optimize(g, wl.poses, settings=LM.LmSettings(max_iterations=10))
+    LM.optimize_native(g, wl.poses, settings=LM.LmSettings(max_iterations=1))  # warm-up (plan, solver)
+    _, rep = LM.optimize_native(g, wl.poses, settings=LM.LmSettings(max_iterations=10))
     its = sorted(rep.iteration_seconds)
+    _, prep = LM.optimize(g, wl.poses, settings=LM.LmSettings(max_iterations=10))
+    pits = sorted(prep.iteration_seconds)
     out = {"frames": len(wl.clouds), "factors": F, "factors_by_resolution": by_res, "points": int(pts),
            "ms_linearize_kernel": lin, "ms_evaluate_kernel": evm, "factors_per_s": F / (lin * 1e-3),
            "points_per_s": pts / (lin * 1e-3), "inliers": int(d_inl.sum().item()),
            "lm_ms_per_iteration_median": 1e3 * its[len(its) // 2] if its else None, "lm_iterations": rep.iterations,
-           "lm_reason": rep.reason,
+           "lm_reason": rep.reason, "lm_note": "native LM (vgicp_graph_optimize), device block-band Cholesky",
+           "lm_python_ms_per_iteration_median": 1e3 * pits[len(pits) // 2] if pits else None,
            "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()},
            "note": "single GPU (the BASELINE config names 8xB200); one launch per pass over all resolutions"}
     del wl, g

@@ -201,6 +201,43 @@ int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* in
 int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported);
 int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, double lambda, double* x, int* solved);
 
+/* ---------------------------------------------------------------- native Levenberg-Marquardt */
+/* optimize (optimizer.cpp:88-194) for a graph whose factors are all matching-cost factors, in the
+ * library: every candidate is linearized + assembled on the device and scored by its per-factor
+ * errors (= total_error), the damped system is solved on the device (block-band Cholesky) or on the
+ * host, Pose::retract (se3.cpp:93-105) on the host. Same damping schedule, acceptance rule,
+ * termination reasons and gauge anchoring (effective_fixed_mask, optimizer.cpp:24-43) as the
+ * reference. poses12 (num_poses × 12) is updated in place unless the solve aborts; fixed (may be
+ * NULL) marks user-fixed poses; updates (may be NULL) carries each pose's
+ * updates_since_orthonormalization in and out. trace (may be NULL) receives up to max_trace
+ * IterationRecords as 5 doubles (iteration, error, lambda, step_norm, accepted);
+ * iteration_seconds (may be NULL, >= max_iterations entries) the wall time of each outer iteration. */
+typedef struct vgicp_lm_settings { /* LmSettings, optimizer.hpp:12-21 */
+  int max_iterations;
+  double lambda_init, lambda_increase, lambda_decrease, lambda_max;
+  double relative_error_decrease, step_norm_tolerance;
+} vgicp_lm_settings;
+enum { /* TerminationReason, optimizer.hpp:23-29 (same order) */
+  VGICP_LM_CONVERGED_RELATIVE_ERROR = 0,
+  VGICP_LM_CONVERGED_STEP_NORM = 1,
+  VGICP_LM_MAX_ITERATIONS = 2,
+  VGICP_LM_LAMBDA_LIMIT = 3,
+  VGICP_LM_SOLVER_ABORT = 4
+};
+typedef struct vgicp_lm_report { /* OptimizerReport, optimizer.hpp:41-50 (+ counters) */
+  int iterations;               /* accepted re-linearizations */
+  double initial_error, final_error;
+  int reason;                   /* VGICP_LM_* */
+  int aborted;
+  double wall_time_seconds;
+  int trace_length;             /* records produced (may exceed max_trace) */
+  int iteration_count_timed;    /* entries written to iteration_seconds */
+  int solves, linearizations, band_solver;
+} vgicp_lm_report;
+int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const uint8_t* fixed, int32_t* updates,
+                         const vgicp_lm_settings* settings, vgicp_lm_report* report, double* trace, int max_trace,
+                         double* iteration_seconds);
+
 /* Device-resident variants: every pointer is device memory of the context's device; the work
  * is enqueued on the context stream and the call returns without synchronising. */
 int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, double* d_out, int32_t* d_inliers);

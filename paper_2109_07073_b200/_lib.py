@@ -33,6 +33,22 @@ class NoDeviceError(VgicpError):
     pass
 
 
+class LmSettingsC(C.Structure):  # vgicp_lm_settings
+    _fields_ = [("max_iterations", C.c_int), ("lambda_init", C.c_double), ("lambda_increase", C.c_double),
+                ("lambda_decrease", C.c_double), ("lambda_max", C.c_double),
+                ("relative_error_decrease", C.c_double), ("step_norm_tolerance", C.c_double)]
+
+
+class LmReportC(C.Structure):  # vgicp_lm_report
+    _fields_ = [("iterations", C.c_int), ("initial_error", C.c_double), ("final_error", C.c_double),
+                ("reason", C.c_int), ("aborted", C.c_int), ("wall_time_seconds", C.c_double),
+                ("trace_length", C.c_int), ("iteration_count_timed", C.c_int), ("solves", C.c_int),
+                ("linearizations", C.c_int), ("band_solver", C.c_int)]
+
+
+LM_REASONS = ["converged_relative_error", "converged_step_norm", "max_iterations", "lambda_limit", "solver_abort"]
+
+
 class FactorDesc(C.Structure):
     _fields_ = [
         ("target_index", C.c_int32),
@@ -93,6 +109,7 @@ SIGNATURES = {
     "vgicp_graph_linearized_errors": (_i, [_vp, _vp, _vp]),
     "vgicp_graph_solver_plan": (_i, [_vp, _vp, _vp]),
     "vgicp_graph_solve_damped": (_i, [_vp, _vp, C.c_double, _vp, _vp]),
+    "vgicp_graph_optimize": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
     "vgicp_transform_cloud": (_i, [_vp, _vp, _vp, _sz, _vp, _vp, _vp]),
     "vgicp_submap_build": (_i, [_vp, _vp, _vp, _i, _d, _d, _vp, _vp, _vp]),
     "vgicp_estimate_covariances_batch": (_i, [_vp, _vp, _vp, _i, _i, _d, _vp]),

@@ -1,0 +1,355 @@
+// Native Levenberg-Marquardt for graphs of matching-cost factors (optimizer.cpp:88-194), driving
+// the device path: every candidate is linearized + assembled on the GPU (one launch + the assembly
+// launch); its per-factor errors — bit-identical to evaluate_matching_cost — give total_error
+// (summed in factor order, optimizer.cpp:66-75), so an accepted candidate's normal equations are
+// already assembled for the next iteration; the damped system is solved on the GPU by the
+// block-band Cholesky (solve_block_system, block_solver.cpp:64-122) when its envelope fits a
+// cluster, else on the host. Retraction, damping schedule, acceptance and termination follow
+// optimizer.cpp:113-186 and se3.cpp:46-105 exactly.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+namespace vgicp {
+namespace {
+
+constexpr double kSmallAngle = 1e-8;    // se3.cpp:10
+constexpr int kOrthonormalizeEvery = 50;  // se3.cpp:11
+
+// T = (R row-major 9, t 3)
+void se3_exp(const double* xi, double* T) {  // se3.cpp:46-78
+  const double w0 = xi[0], w1 = xi[1], w2 = xi[2];
+  const double th = std::sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+  const double W[9] = {0.0, -w2, w1, w2, 0.0, -w0, -w1, w0, 0.0};
+  double WW[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) WW[3 * r + c] = W[3 * r] * W[c] + W[3 * r + 1] * W[3 + c] + W[3 * r + 2] * W[6 + c];
+  double a, b, cc;
+  if (th < kSmallAngle) {
+    a = 1.0, b = 0.5, cc = 1.0 / 6.0;
+  } else {
+    a = std::sin(th) / th;
+    b = (1.0 - std::cos(th)) / (th * th);
+    cc = (th - std::sin(th)) / (th * th * th);
+  }
+  double J[9];
+  for (int k = 0; k < 9; ++k) {
+    const double I = (k % 4 == 0) ? 1.0 : 0.0;
+    T[k] = I + a * W[k] + b * WW[k];
+    J[k] = I + b * W[k] + cc * WW[k];
+  }
+  for (int r = 0; r < 3; ++r) T[9 + r] = J[3 * r] * xi[3] + J[3 * r + 1] * xi[4] + J[3 * r + 2] * xi[5];
+}
+
+void compose(const double* A, const double* B, double* out) {  // se3.cpp:42-44
+  double R[9], t[3];
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) R[3 * r + c] = A[3 * r] * B[c] + A[3 * r + 1] * B[3 + c] + A[3 * r + 2] * B[6 + c];
+    t[r] = A[3 * r] * B[9] + A[3 * r + 1] * B[10] + A[3 * r + 2] * B[11] + A[9 + r];
+  }
+  std::memcpy(out, R, sizeof(R));
+  std::memcpy(out + 9, t, sizeof(t));
+}
+
+// Orthogonal polar factor of the rotation block (se3.cpp:80-91 takes U·Vᵀ of the SVD): Newton's
+// iteration X <- (X + X⁻ᵀ)/2 converges quadratically to it from a near-rotation.
+void orthonormalize(double* T) {
+  double X[9];
+  std::memcpy(X, T, sizeof(X));
+  for (int it = 0; it < 8; ++it) {
+    const double c00 = X[4] * X[8] - X[5] * X[7], c01 = X[5] * X[6] - X[3] * X[8], c02 = X[3] * X[7] - X[4] * X[6];
+    const double c10 = X[2] * X[7] - X[1] * X[8], c11 = X[0] * X[8] - X[2] * X[6], c12 = X[1] * X[6] - X[0] * X[7];
+    const double c20 = X[1] * X[5] - X[2] * X[4], c21 = X[2] * X[3] - X[0] * X[5], c22 = X[0] * X[4] - X[1] * X[3];
+    const double det = X[0] * c00 + X[1] * c01 + X[2] * c02;
+    if (!(std::fabs(det) > 0.0)) return;
+    const double id = 1.0 / det;  // X⁻ᵀ = cofactor matrix / det
+    const double Y[9] = {c00 * id, c01 * id, c02 * id, c10 * id, c11 * id, c12 * id, c20 * id, c21 * id, c22 * id};
+    double diff = 0.0;
+    for (int k = 0; k < 9; ++k) {
+      const double v = 0.5 * (X[k] + Y[k]);
+      diff = std::max(diff, std::fabs(v - X[k]));
+      X[k] = v;
+    }
+    if (diff < 1e-16) break;
+  }
+  std::memcpy(T, X, sizeof(X));
+}
+
+// Dense Cholesky solve of the damped slot-order system on the host (fallback when the band
+// solver does not support the envelope). Returns false when not positive definite.
+bool host_solve(int S, int P, const std::vector<int32_t>& pairs, const double* asmb, double lam,
+                std::vector<double>& x) {
+  const int m = 6 * S;
+  std::vector<double> A(static_cast<size_t>(m) * m, 0.0), b(m);
+  const double* diag = asmb;
+  const double* off = asmb + static_cast<size_t>(S) * 36;
+  const double* rhs = asmb + static_cast<size_t>(S + P) * 36;
+  for (int s = 0; s < S; ++s)
+    for (int r = 0; r < 6; ++r) {
+      for (int c = 0; c < 6; ++c) A[static_cast<size_t>(6 * s + r) * m + 6 * s + c] = diag[36 * s + 6 * r + c];
+      b[6 * s + r] = rhs[6 * s + r];
+    }
+  for (int q = 0; q < P; ++q) {
+    const int a = pairs[2 * q], bb = pairs[2 * q + 1];
+    for (int r = 0; r < 6; ++r)
+      for (int c = 0; c < 6; ++c) {
+        const double v = off[36 * q + 6 * r + c];
+        A[static_cast<size_t>(6 * a + r) * m + 6 * bb + c] = v;
+        A[static_cast<size_t>(6 * bb + c) * m + 6 * a + r] = v;
+      }
+  }
+  for (int k = 0; k < m; ++k) {
+    double& d = A[static_cast<size_t>(k) * m + k];
+    d = d + lam * std::max(d, 1e-10);
+  }
+  for (int j = 0; j < m; ++j) {  // in-place lower Cholesky
+    double* Lj = &A[static_cast<size_t>(j) * m];
+    double d = Lj[j];
+    for (int k = 0; k < j; ++k) d -= Lj[k] * Lj[k];
+    if (!(d > 0.0)) return false;
+    const double l = std::sqrt(d);
+    Lj[j] = l;
+    for (int i = j + 1; i < m; ++i) {
+      double* Li = &A[static_cast<size_t>(i) * m];
+      double v = Li[j];
+      for (int k = 0; k < j; ++k) v -= Li[k] * Lj[k];
+      Li[j] = v / l;
+    }
+  }
+  x.assign(m, 0.0);
+  for (int i = 0; i < m; ++i) {
+    double v = b[i];
+    for (int k = 0; k < i; ++k) v -= A[static_cast<size_t>(i) * m + k] * x[k];
+    x[i] = v / A[static_cast<size_t>(i) * m + i];
+  }
+  for (int i = m - 1; i >= 0; --i) {
+    double v = x[i];
+    for (int k = i + 1; k < m; ++k) v -= A[static_cast<size_t>(k) * m + i] * x[k];
+    x[i] = v / A[static_cast<size_t>(i) * m + i];
+  }
+  return true;
+}
+
+struct DeviceScope {  // selects the context's device for the call, restores the caller's
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+struct PoolBuffer {  // stream-ordered device temporary (the context's pool)
+  cudaStream_t s;
+  void* p = nullptr;
+  explicit PoolBuffer(cudaStream_t st) : s(st) {}
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, s); }
+  ~PoolBuffer() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+int find_root(std::vector<int>& parent, int x) {
+  while (parent[x] != x) x = parent[x] = parent[parent[x]];
+  return x;
+}
+
+}  // namespace
+}  // namespace vgicp
+
+using namespace vgicp;
+
+extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const uint8_t* fixed_in, int32_t* updates,
+                                    const vgicp_lm_settings* settings_in, vgicp_lm_report* report, double* trace,
+                                    int max_trace, double* iteration_seconds) {
+  if (!graph || !report || (graph->num_poses > 0 && !poses12)) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  const auto t_start = std::chrono::steady_clock::now();
+  auto seconds = [&]() { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(); };
+  vgicp_lm_settings st{50, 1e-5, 10.0, 0.1, 1e10, 1e-6, 1e-8};  // optimizer.hpp:12-21
+  if (settings_in) st = *settings_in;
+  std::memset(report, 0, sizeof(*report));
+  report->reason = VGICP_LM_MAX_ITERATIONS;
+  const int n = graph->num_poses;
+  const int nf = graph->num_factors;
+  if (n == 0) {
+    report->reason = VGICP_LM_CONVERGED_STEP_NORM;
+    return VGICP_OK;
+  }
+  // effective fixed mask (optimizer.cpp:24-43): the first pose of every component without a fixed pose
+  std::vector<int> parent(n);
+  for (int v = 0; v < n; ++v) parent[v] = v;
+  for (int f = 0; f < nf; ++f) parent[find_root(parent, graph->tgt_idx[f])] = find_root(parent, graph->src_idx[f]);
+  std::vector<uint8_t> fixed(n, 0), has(n, 0);
+  for (int v = 0; v < n; ++v) fixed[v] = fixed_in ? (fixed_in[v] ? 1 : 0) : 0;
+  for (int v = 0; v < n; ++v)
+    if (fixed[v]) has[find_root(parent, v)] = 1;
+  for (int v = 0; v < n; ++v) {
+    const int r = find_root(parent, v);
+    if (!has[r]) fixed[v] = 1, has[r] = 1;
+  }
+  int S = 0, P = 0;
+  if (int rc = vgicp_graph_assembly_plan(graph, fixed.data(), &S, &P, nullptr)) return rc;
+  std::vector<int32_t> pairs(2 * static_cast<size_t>(P));
+  if (P > 0 && (vgicp_graph_assembly_plan(graph, fixed.data(), &S, &P, pairs.data()) != VGICP_OK))
+    return VGICP_E_CUDA;
+  std::vector<int> var_of_slot(S);
+  {
+    int active = 0;
+    for (int v = 0; v < n; ++v) active += fixed[v] ? 0 : 1;
+    for (int v = 0, rank = 0; v < n; ++v)
+      if (!fixed[v]) var_of_slot[active - 1 - rank++] = v;  // block_solver.cpp:26-34
+  }
+  int bw = 0, band = 0;
+  if (S > 0)
+    if (int rc = vgicp_graph_solver_plan(graph, &bw, &band)) return rc;
+
+  vgicp_ctx ctx = graph->ctx;
+  DeviceScope g(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const size_t asm_doubles = static_cast<size_t>(S + P) * 36 + static_cast<size_t>(S) * 6;
+  PoolBuffer d_buf(s);
+  VG_CUDA(d_buf.alloc(sizeof(double) * (2 * std::max<size_t>(asm_doubles, 1) + 12 * static_cast<size_t>(n))));
+  double* d_asm[2] = {static_cast<double*>(d_buf.p), static_cast<double*>(d_buf.p) + std::max<size_t>(asm_doubles, 1)};
+  double* d_poses = static_cast<double*>(d_buf.p) + 2 * std::max<size_t>(asm_doubles, 1);
+  std::vector<double> err(nf);
+  std::vector<int32_t> inl(nf);
+  std::vector<double> host_asm;
+  int solves = 0, lins = 0;
+  // linearize + assemble `at` into d_asm[which]; returns the total error (factor order)
+  auto linearize = [&](const std::vector<double>& at, int which, double* total) -> int {
+    VG_CUDA(cudaMemcpyAsync(d_poses, at.data(), sizeof(double) * 12 * n, cudaMemcpyHostToDevice, s));
+    if (int rc = vgicp_graph_linearize_assembled_device(graph, d_poses, d_asm[which])) return rc;
+    if (int rc = vgicp_graph_linearized_errors(graph, err.data(), inl.data())) return rc;
+    double e = 0.0;
+    for (int f = 0; f < nf; ++f) e += err[f];
+    *total = e;
+    ++lins;
+    return VGICP_OK;
+  };
+  std::vector<double> x;
+  auto solve = [&](int which, double lam, bool* ok) -> int {
+    ++solves;
+    x.assign(6 * static_cast<size_t>(S), 0.0);
+    if (S == 0) {
+      *ok = true;
+      return VGICP_OK;
+    }
+    if (band) {
+      int solved = 0;
+      if (int rc = vgicp_graph_solve_damped(graph, d_asm[which], lam, x.data(), &solved)) return rc;
+      *ok = solved != 0;
+      return VGICP_OK;
+    }
+    host_asm.resize(asm_doubles);
+    VG_CUDA(cudaMemcpyAsync(host_asm.data(), d_asm[which], sizeof(double) * asm_doubles, cudaMemcpyDeviceToHost, s));
+    VG_CUDA(cudaStreamSynchronize(s));
+    *ok = host_solve(S, P, pairs, host_asm.data(), lam, x);
+    return VGICP_OK;
+  };
+
+  std::vector<double> poses(poses12, poses12 + 12 * static_cast<size_t>(n));
+  std::vector<int32_t> upd(n, 0);
+  if (updates) std::copy(updates, updates + n, upd.begin());
+  int buf = 0;
+  double current = 0.0;
+  if (int rc = linearize(poses, buf, &current)) return rc;
+  report->initial_error = report->final_error = current;
+  double lam = st.lambda_init;
+  bool any_accepted = false;
+  int ntrace = 0;
+  auto record = [&](int it, double e, double l, double step, bool acc) {
+    if (trace && ntrace < max_trace) {
+      double* r = trace + 5 * static_cast<size_t>(ntrace);
+      r[0] = it, r[1] = e, r[2] = l, r[3] = step, r[4] = acc ? 1.0 : 0.0;
+    }
+    ++ntrace;
+  };
+  std::vector<double> cand(poses.size());
+  std::vector<int32_t> cand_upd(n);
+  double t_prev = seconds();
+  for (int it = 0; it < st.max_iterations; ++it) {
+    bool accepted = false;
+    while (true) {
+      bool ok = false;
+      if (int rc = solve(buf, lam, &ok)) return rc;
+      if (!ok) {
+        lam *= st.lambda_increase;
+        if (lam > st.lambda_max) {
+          if (!any_accepted) {
+            report->aborted = 1;
+            report->reason = VGICP_LM_SOLVER_ABORT;
+          } else {
+            report->reason = VGICP_LM_LAMBDA_LIMIT;
+          }
+          break;
+        }
+        continue;
+      }
+      double step_sq = 0.0;
+      for (double v : x) step_sq += v * v;
+      const double step_norm = std::sqrt(step_sq);
+      if (step_norm < st.step_norm_tolerance) {
+        record(it, current, lam, step_norm, false);
+        report->reason = VGICP_LM_CONVERGED_STEP_NORM;
+        break;
+      }
+      cand = poses;
+      cand_upd = upd;
+      for (int sl = 0; sl < S; ++sl) {  // Pose::retract (se3.cpp:93-105)
+        const int v = var_of_slot[sl];
+        double E[12];
+        se3_exp(&x[6 * static_cast<size_t>(sl)], E);
+        compose(&poses[12 * static_cast<size_t>(v)], E, &cand[12 * static_cast<size_t>(v)]);
+        if (++cand_upd[v] >= kOrthonormalizeEvery) {
+          orthonormalize(&cand[12 * static_cast<size_t>(v)]);
+          cand_upd[v] = 0;
+        }
+      }
+      double cand_error = 0.0;
+      if (int rc = linearize(cand, 1 - buf, &cand_error)) return rc;
+      if (cand_error < current) {
+        const double decrease = (current - cand_error) / std::max(current, 1e-300);
+        poses.swap(cand);
+        upd.swap(cand_upd);
+        buf = 1 - buf;  // the candidate's system is the next iteration's
+        any_accepted = accepted = true;
+        record(it, cand_error, lam, step_norm, true);
+        current = cand_error;
+        lam = std::max(lam * st.lambda_decrease, 1e-12);
+        ++report->iterations;
+        if (decrease < st.relative_error_decrease) report->reason = VGICP_LM_CONVERGED_RELATIVE_ERROR;
+        break;
+      }
+      record(it, current, lam, step_norm, false);
+      lam *= st.lambda_increase;
+      if (lam > st.lambda_max) {
+        report->reason = VGICP_LM_LAMBDA_LIMIT;
+        break;
+      }
+    }
+    const double t_now = seconds();
+    if (iteration_seconds) iteration_seconds[it] = t_now - t_prev;
+    t_prev = t_now;
+    report->iteration_count_timed = it + 1;
+    if (!accepted || report->reason == VGICP_LM_CONVERGED_RELATIVE_ERROR) break;
+    report->reason = VGICP_LM_MAX_ITERATIONS;
+  }
+  if (!report->aborted) {
+    std::copy(poses.begin(), poses.end(), poses12);
+    if (updates) std::copy(upd.begin(), upd.end(), updates);
+    report->final_error = current;
+  }
+  report->trace_length = ntrace;
+  report->solves = solves;
+  report->linearizations = lins;
+  report->band_solver = band;
+  report->wall_time_seconds = seconds();
+  return VGICP_OK;
+}

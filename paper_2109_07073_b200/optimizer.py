@@ -501,3 +501,44 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
         report.final_error = current
     report.wall_time_seconds = time.perf_counter() - t_start
     return poses, report
+
+
+def optimize_native(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None = None, updates=None,
+                    max_trace: int = 4096):
+    """The same Levenberg-Marquardt run natively in the library (vgicp_graph_optimize): device
+    linearization + assembly of every candidate (its errors are total_error), device block-band
+    Cholesky (host Cholesky when the envelope is too wide), host retraction — no Python in the loop.
+    Returns (poses, OptimizerReport); the graph's assembly plan is replaced by the effective mask's
+    (call assembly_plan again before using linearize_assembled)."""
+    import ctypes as C
+
+    from . import _lib
+
+    settings = settings or LmSettings()
+    P = np.array(poses_array(poses), dtype=np.float64, copy=True)
+    n = len(P)
+    if n != graph.num_poses:
+        raise ValueError("pose count does not match the graph")
+    fx = None if fixed is None else np.ascontiguousarray(np.asarray(fixed, dtype=np.uint8).reshape(-1))
+    upd = np.zeros(n, np.int32) if updates is None else np.ascontiguousarray(np.asarray(updates, np.int32))
+    st = _lib.LmSettingsC(settings.max_iterations, settings.lambda_init, settings.lambda_increase,
+                          settings.lambda_decrease, settings.lambda_max, settings.relative_error_decrease,
+                          settings.step_norm_tolerance)
+    rep = _lib.LmReportC()
+    trace = np.zeros((max_trace, 5))
+    its = np.zeros(max(1, settings.max_iterations))
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _lib.check(_lib.load().vgicp_graph_optimize(graph._h, ptr(P), ptr(fx) if fx is not None else None, ptr(upd),
+                                                C.byref(st), C.byref(rep), ptr(trace), max_trace, ptr(its)))
+    graph._plan = None  # the library now holds the effective mask's plan
+    report = OptimizerReport(iterations=rep.iterations, initial_error=rep.initial_error, final_error=rep.final_error,
+                             reason=_lib.LM_REASONS[rep.reason], wall_time_seconds=rep.wall_time_seconds,
+                             aborted=bool(rep.aborted),
+                             diagnostic="linear solve failed at maximum damping; poses unchanged" if rep.aborted else "")
+    report.trace = [IterationRecord(int(r[0]), float(r[1]), float(r[2]), float(r[3]), bool(r[4]))
+                    for r in trace[:min(rep.trace_length, max_trace)]]
+    report.iteration_seconds = list(its[:rep.iteration_count_timed])
+    report.solves, report.linearizations, report.band_solver = rep.solves, rep.linearizations, bool(rep.band_solver)
+    if updates is not None:
+        np.asarray(updates)[...] = upd
+    return P, report

@@ -283,3 +283,63 @@ def test_gpu_lm_band_solver_matches_dense_solver(V):
     assert r_b.iterations == r_d.iterations and r_b.reason == r_d.reason
     assert abs(r_b.final_error - r_d.final_error) <= 1e-9 * max(1.0, r_d.final_error)
     assert np.abs(p_b - p_d).max() < 1e-9
+
+
+def _lm_graph(V, loop, seed=78, nframes=8):
+    rng = O.Rng(seed)
+    clouds = []
+    for _ in range(nframes):
+        m, c = rng.gaussian_cloud(3000, 10.0)
+        clouds.append(V.PointCloud(m.astype(np.float32), V.cov6_from(c)))
+    maps = V.GaussianVoxelMap.build_batch(clouds, 1.0)
+    poses = np.stack([rng.random_pose(0.05, 0.5) for _ in range(nframes)])
+    factors = [V.MatchingCostFactor(j - d, j, clouds[j], maps[j - d]) for j in range(1, nframes) for d in (1, 2)
+               if j - d >= 0]
+    if loop:
+        factors.append(V.MatchingCostFactor(nframes - 1, 0, clouds[0], maps[nframes - 1]))
+    return V.FactorGraph(factors, nframes, chunk=2048), poses
+
+
+@gpu
+@pytest.mark.parametrize("loop", [False, True])
+@pytest.mark.parametrize("host_solve", [False, True])
+def test_gpu_native_lm_matches_python_lm(V, monkeypatch, loop, host_solve):
+    """vgicp_graph_optimize (the LM loop in the library) takes the reference loop's decisions: same
+    accepted / rejected sequence, λ schedule, termination reason; errors and poses to 1e-9 (the
+    solvers differ in rounding: band or host Cholesky vs the Python LM's)."""
+    from paper_2109_07073_b200 import optimizer as LM
+
+    if host_solve:
+        monkeypatch.setenv("VGICP_NO_BAND_SOLVER", "1")
+    graph, poses = _lm_graph(V, loop)
+    p_py, r_py = LM.optimize(graph, poses, band_solve=False)
+    p_nat, r_nat = LM.optimize_native(graph, poses)
+    assert r_nat.band_solver == (not host_solve)
+    assert r_nat.iterations == r_py.iterations and r_nat.reason == r_py.reason
+    assert [(t.accepted, t.lam) for t in r_nat.trace] == [(t.accepted, t.lam) for t in r_py.trace]
+    for a, b in zip(r_nat.trace, r_py.trace):
+        assert abs(a.error - b.error) <= 1e-9 * max(1.0, b.error)
+    assert r_nat.initial_error == r_py.initial_error
+    assert abs(r_nat.final_error - r_py.final_error) <= 1e-9 * max(1.0, r_py.final_error)
+    assert np.abs(p_nat - p_py).max() < 1e-9
+    assert r_nat.linearizations == len(r_nat.trace) + 1 - sum(1 for t in r_nat.trace if t.step_norm < 1e-8)
+
+
+@gpu
+def test_gpu_native_lm_fixed_and_updates(V):
+    """User-fixed poses stay put, updates_since_orthonormalization counts accepted retractions and
+    wraps at 50 (se3.cpp:93-105), max_iterations bounds the run."""
+    from paper_2109_07073_b200 import optimizer as LM
+
+    graph, poses = _lm_graph(V, True, seed=79)
+    fixed = np.zeros(len(poses), np.uint8)
+    fixed[[0, 3]] = 1
+    upd = np.full(len(poses), 48, np.int32)
+    p, r = LM.optimize_native(graph, poses, fixed=fixed, settings=LM.LmSettings(max_iterations=3), updates=upd)
+    assert r.iterations <= 3 and r.iterations >= 1
+    assert np.array_equal(p[[0, 3]], poses[[0, 3]])
+    moved = np.flatnonzero(fixed == 0)
+    assert np.all(upd[[0, 3]] == 48)
+    assert np.all(upd[moved] == (48 + r.iterations) % 50)
+    R = p[moved, :9].reshape(-1, 3, 3)
+    assert np.abs(R @ R.transpose(0, 2, 1) - np.eye(3)).max() < 1e-12  # orthonormalized on the wrap
