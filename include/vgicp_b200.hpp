@@ -411,6 +411,47 @@ class MatchingCostBatch {
     return s;
   }
   std::size_t size() const { return factors_.size(); }
+  // optimize (optimizer.cpp:88-194) for this graph of matching factors, in the library
+  // (vgicp_graph_optimize); `poses` updated in place unless the solve aborts (like graph.poses).
+  struct IterationRecord {  // optimizer.hpp:33-39
+    int iteration = 0;
+    double error = 0.0, lambda = 0.0, step_norm = 0.0;
+    bool accepted = false;
+  };
+  struct OptimizerReport {  // optimizer.hpp:41-50 (reason: VGICP_LM_*, TerminationReason order)
+    int iterations = 0;
+    double initial_error = 0.0, final_error = 0.0;
+    std::vector<IterationRecord> trace;
+    int reason = VGICP_LM_MAX_ITERATIONS;
+    double wall_time_seconds = 0.0;
+    bool aborted = false;
+  };
+  OptimizerReport optimize(std::vector<Pose>& poses, const std::vector<std::uint8_t>& fixed = {},
+                           const vgicp_lm_settings* settings = nullptr) const {
+    std::vector<double> P = flatten(poses);
+    if (!fixed.empty() && static_cast<int>(fixed.size()) != num_poses_)
+      throw std::invalid_argument("fixed mask size does not match");
+    const int max_trace = 4 * (settings ? settings->max_iterations : 50) + 64;
+    std::vector<double> trace(5 * static_cast<std::size_t>(max_trace));
+    vgicp_lm_report rep{};
+    check(vgicp_graph_optimize(h_.get(), P.data(), fixed.empty() ? nullptr : fixed.data(), nullptr, settings, &rep,
+                               trace.data(), max_trace, nullptr));
+    OptimizerReport out;
+    out.iterations = rep.iterations;
+    out.initial_error = rep.initial_error;
+    out.final_error = rep.final_error;
+    out.reason = rep.reason;
+    out.wall_time_seconds = rep.wall_time_seconds;
+    out.aborted = rep.aborted != 0;
+    for (int k = 0; k < std::min(rep.trace_length, max_trace); ++k) {
+      const double* r = trace.data() + 5 * k;
+      out.trace.push_back({static_cast<int>(r[0]), r[1], r[2], r[3], r[4] != 0.0});
+    }
+    if (!out.aborted)
+      for (std::size_t k = 0; k < poses.size(); ++k)
+        for (int q = 0; q < 12; ++q) poses[k].m[q] = P[12 * k + q];
+    return out;
+  }
   // linearize_all + assemble_normal_equations (block_solver.cpp:14-62) with the assembly on the
   // device (matching factors only); bit-identical to assembling linearize()'s blocks on the host.
   BlockSystem linearize_assembled(const std::vector<Pose>& poses, const std::vector<std::uint8_t>& fixed) const {

@@ -125,6 +125,26 @@ int main() {
     }
   }
 
+  // native LM (optimizer.cpp:88-194): the error never increases along the trace, the fixed pose
+  // stays put, accepted records carry the new error
+  {
+    MatchingCostBatch b3(ctx, {MatchingCostFactor(0, 1, cloud, map), MatchingCostFactor(1, 2, cloud, map),
+                               MatchingCostFactor(2, 0, cloud, map)}, 3);
+    std::vector<Pose> poses = {Pose::Identity(), Pose::from({1, 0, 0, 0, 1, 0, 0, 0, 1}, {0.2, -0.1, 0.05}),
+                               Pose::from({1, 0, 0, 0, 1, 0, 0, 0, 1}, {-0.1, 0.15, 0})};
+    const Pose p0 = poses[0];
+    const auto rep = b3.optimize(poses, {1, 0, 0});
+    REQUIRE(!rep.aborted && rep.iterations >= 1 && rep.final_error <= rep.initial_error);
+    double last = rep.initial_error;
+    for (const auto& r : rep.trace)
+      if (r.accepted) {
+        REQUIRE(r.error < last);
+        last = r.error;
+      }
+    REQUIRE(last == rep.final_error && std::abs(b3.total_error(poses) - rep.final_error) <= 1e-9 * rep.final_error);
+    for (int q = 0; q < 12; ++q) REQUIRE(poses[0].m[q] == p0.m[q]);
+  }
+
   // submap path (§8f #2): transform_cloud, voxel_downsample, build_submap
   {
     HostCloud hc;
