@@ -457,10 +457,10 @@ def run_c4(ctx, n_maps=4000, points=20000, reps=5):
             "ms_per_sweep_unculled": ms_all, "probes_per_s_unculled": probes / (ms_all * 1e-3),
             "maps_probed": int(np.sum(hits > 0)),
             "maps_over_0.025": int(np.sum(hits / len(seq.scans[n_maps]) > 0.025)), "build_seconds": round(t_build, 2),
-            "note": "overlap_hits over a MapSet (keyframe handles cached) through the C ABI, incl. H2D of the per-map "
-                    "(pose, map) items and D2H of the hit counts; maps carry occupancy bitmaps (fp32-screened exact "
-                    "keys); the default call culls (exactly) the maps whose occupied box the transformed cloud box "
-                    "misses"}
+            "note": "overlap_hits over a MapSet (vgicp_overlap_mapset: the keyframe maps' descriptors stay on the "
+                    "device, per-probe items are built and exactly culled on the device from the uploaded poses), "
+                    "incl. H2D of the 4,000 poses and D2H of the hit counts; maps carry occupancy bitmaps "
+                    "(fp32-screened exact keys); unculled = the generic host-built path with culling off"}
 
 
 def run_covariances(ctx, scans, reps=3):

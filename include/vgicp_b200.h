@@ -58,6 +58,7 @@ typedef struct vgicp_ctx_s* vgicp_ctx;
 typedef struct vgicp_cloud_s* vgicp_cloud;
 typedef struct vgicp_map_s* vgicp_map;
 typedef struct vgicp_graph_s* vgicp_graph;
+typedef struct vgicp_mapset_s* vgicp_mapset;
 
 /* MatchingCostFactor (include/vgicp/factors.hpp:36-45): the older frame owns the map
  * (target), the newer frame supplies the points (source). */
@@ -137,6 +138,14 @@ int vgicp_overlap_rate(vgicp_ctx ctx, vgicp_cloud cloud, const double pose_rel[1
 /* m independent (cloud, pose, map) probes in one launch; hits[k] is the exact hit count. */
 int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* poses12, const vgicp_map* maps,
                         int m, uint64_t* hits);
+/* A fixed sequence of maps kept on the device (the keyframe database of pipeline.cpp:135-150):
+ * vgicp_overlap_mapset sweeps ONE cloud against all of them — per-probe items are built and culled
+ * on the device from the m poses (rel12: T_map⁻¹·T_cloud, m × 12), so a sweep costs one pose upload,
+ * two launches and the hit download. Results equal vgicp_overlap_batch's. The set holds references
+ * to its maps. */
+int vgicp_mapset_create(vgicp_ctx ctx, const vgicp_map* maps, int m, vgicp_mapset* out);
+int vgicp_mapset_destroy(vgicp_mapset set);
+int vgicp_overlap_mapset(vgicp_ctx ctx, vgicp_cloud cloud, const double* rel12, vgicp_mapset set, uint64_t* hits);
 
 /* ---------------------------------------------------------------- matching cost factors */
 /* linearize_matching_cost (factors.cpp:90-148) for one factor. */

@@ -110,6 +110,9 @@ SIGNATURES = {
     "vgicp_graph_solver_plan": (_i, [_vp, _vp, _vp]),
     "vgicp_graph_solve_damped": (_i, [_vp, _vp, C.c_double, _vp, _vp]),
     "vgicp_graph_optimize": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
+    "vgicp_mapset_create": (_i, [_vp, _vp, C.c_int, _vp]),
+    "vgicp_mapset_destroy": (_i, [_vp]),
+    "vgicp_overlap_mapset": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "vgicp_transform_cloud": (_i, [_vp, _vp, _vp, _sz, _vp, _vp, _vp]),
     "vgicp_submap_build": (_i, [_vp, _vp, _vp, _i, _d, _d, _vp, _vp, _vp]),
     "vgicp_estimate_covariances_batch": (_i, [_vp, _vp, _vp, _i, _i, _d, _vp]),

@@ -1034,6 +1034,91 @@ int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* 
   return VGICP_OK;
 }
 
+// ------------------------------------------------------------------------------- map sets
+int vgicp_mapset_create(vgicp_ctx ctx, const vgicp_map* maps, int m, vgicp_mapset* out) {
+  if (!ctx || !out || (m > 0 && !maps) || m < 0) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  auto set = std::make_unique<vgicp_mapset_s>();
+  set->ctx = ctx;
+  std::vector<OverlapItem> templ(m);
+  for (int k = 0; k < m; ++k) {
+    if (!maps[k]) return fail(VGICP_E_INVALID_ARGUMENT, "null map");
+    if (maps[k]->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "handle of another context");
+    set->all_occ = set->all_occ && maps[k]->occ.occ != nullptr;
+  }
+  DeviceGuard g(ctx->device);
+  if (set->all_occ && m > 0) {
+    static const double kIdentity[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+    vgicp_cloud_s dummy;  // the template carries no cloud; fill_overlap_item needs one for blk / n
+    for (int k = 0; k < m; ++k) fill_overlap_item(templ[k], &dummy, kIdentity, maps[k]);
+    const int nch = (m + kOverlapMapsPerChunk - 1) / kOverlapMapsPerChunk;
+    const size_t bt = align_up(sizeof(OverlapItem) * m, 256), bc = align_up(sizeof(int2) * nch, 256);
+    const size_t bh = align_up(sizeof(unsigned long long) * m, 256), bp = align_up(sizeof(double) * 12 * m + 64, 256);
+    VG_CUDA(dmalloc(ctx, &set->block, 2 * bt + bc + bh + bp));
+    char* b = static_cast<char*>(set->block);
+    set->d_templates = reinterpret_cast<OverlapItem*>(b);
+    set->d_items = reinterpret_cast<OverlapItem*>(b + bt);
+    set->d_chunks = reinterpret_cast<int2*>(b + 2 * bt);
+    set->d_hits = reinterpret_cast<unsigned long long*>(b + 2 * bt + bc);
+    set->d_poses = reinterpret_cast<double*>(b + 2 * bt + bc + bh);
+    VG_CUDA(cudaMemcpyAsync(set->d_templates, templ.data(), sizeof(OverlapItem) * m, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  for (int k = 0; k < m; ++k) {
+    maps[k]->refs.fetch_add(1);
+    set->maps.push_back(maps[k]);
+  }
+  *out = set.release();
+  return VGICP_OK;
+}
+
+int vgicp_mapset_destroy(vgicp_mapset set) {
+  if (!set) return VGICP_OK;
+  {
+    DeviceGuard g(set->ctx->device);
+    cudaStreamSynchronize(set->ctx->stream);
+    dfree(set->ctx, set->block);
+  }
+  for (auto mp : set->maps) release(mp);
+  delete set;
+  return VGICP_OK;
+}
+
+int vgicp_overlap_mapset(vgicp_ctx ctx, vgicp_cloud cloud, const double* rel12, vgicp_mapset set, uint64_t* hits) {
+  if (!ctx || !cloud || !set || (!set->maps.empty() && (!rel12 || !hits)))
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (cloud->ctx != ctx || set->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "handle of another context");
+  if (cloud->n == 0) return fail(VGICP_E_INVALID_ARGUMENT, "overlap_rate requires a nonempty cloud");
+  const int m = static_cast<int>(set->maps.size());
+  if (m == 0) return VGICP_OK;
+  if (!set->all_occ || std::getenv("VGICP_OVERLAP_PERITEM") || std::getenv("VGICP_OVERLAP_NOCULL")) {
+    std::vector<vgicp_cloud> clouds(m, cloud);  // generic path (maps without bitmaps, measurement switches)
+    return vgicp_overlap_batch(ctx, clouds.data(), rel12, set->maps.data(), m, hits);
+  }
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const size_t bp = sizeof(double) * 12 * m;
+  if (int rc = ensure_pinned(ctx, align_up(bp + 6 * sizeof(float), 256) + sizeof(unsigned long long) * m)) return rc;
+  char* hp = static_cast<char*>(ctx->pinned);
+  std::memcpy(hp, rel12, bp);
+  float* hbox = reinterpret_cast<float*>(hp + bp);
+  for (int a = 0; a < 3; ++a) hbox[a] = cloud->lo[a], hbox[3 + a] = cloud->hi[a];
+  auto* h = reinterpret_cast<unsigned long long*>(hp + align_up(bp + 6 * sizeof(float), 256));
+  VG_CUDA(cudaMemcpyAsync(set->d_poses, hp, bp + 6 * sizeof(float), cudaMemcpyHostToDevice, s));
+  VG_CUDA(cudaMemsetAsync(set->d_hits, 0, sizeof(unsigned long long) * m, s));
+  const float* d_box = reinterpret_cast<const float*>(reinterpret_cast<const char*>(set->d_poses) + bp);
+  VG_CUDA(launch_mapset_prepare(set->d_templates, m, set->d_poses, cloud->sblk, static_cast<unsigned>(cloud->n), d_box,
+                                set->d_items, set->d_chunks, s));
+  const int nch = (m + kOverlapMapsPerChunk - 1) / kOverlapMapsPerChunk;
+  VG_CUDA(launch_overlap_occ(set->d_items, set->d_chunks, nch, static_cast<unsigned>(cloud->n), set->d_hits, s));
+  ctx->launches += 2;
+  VG_CUDA(cudaMemcpyAsync(h, set->d_hits, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(hits, h, sizeof(uint64_t) * m);
+  return VGICP_OK;
+}
+
 int vgicp_overlap_rate(vgicp_ctx ctx, vgicp_cloud cloud, const double pose_rel[12], vgicp_map map, double* rate) {
   if (!rate || !cloud || !map || !pose_rel) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   uint64_t hits = 0;

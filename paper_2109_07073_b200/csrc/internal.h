@@ -79,6 +79,11 @@ struct OverlapItem {
 static_assert(offsetof(OverlapItem, scr) % 16 == 0 && sizeof(OverlapItem) % 16 == 0, "OccScreen is read as uint4");
 cudaError_t launch_overlap_occ(const OverlapItem* items, const int2* chunks, int num_chunks, unsigned max_n,
                                unsigned long long* hits, cudaStream_t s);
+// Device-side item preparation for a map set swept by one cloud: item k = templates[k] + pose k
+// (fp64 T, fp32 screen, exact culling against the cloud box -> n = 0 when culled); chunks of 32.
+cudaError_t launch_mapset_prepare(const OverlapItem* templates, int m, const double* poses12, const PointBlock* blk,
+                                  unsigned n, const float* cloud_box, OverlapItem* items, int2* chunks,
+                                  cudaStream_t s);
 // Occupancy bitmap build job for one map (cold keys -> bits -> brick ranks -> rank-ordered stats).
 struct OccJob {
   const unsigned long long* keys;
@@ -290,6 +295,18 @@ struct vgicp_map_s {
   vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov64, res, inv_res, shift, 0u, occ}; }
   // rank lookups: slot statistics replaced by the rank-ordered copies (requires occ)
   vgicp::MapDev dev_rank() const { return vgicp::MapDev{tkeys, ra, rb, cov64, res, inv_res, shift, 0u, occ}; }
+};
+
+struct vgicp_mapset_s {
+  vgicp_ctx ctx = nullptr;
+  std::vector<vgicp_map> maps;
+  bool all_occ = true;            // every map carries an occupancy bitmap (device path)
+  void* block = nullptr;          // templates | items | chunks | hits | poses
+  vgicp::OverlapItem* d_templates = nullptr;
+  vgicp::OverlapItem* d_items = nullptr;
+  int2* d_chunks = nullptr;
+  unsigned long long* d_hits = nullptr;
+  double* d_poses = nullptr;
 };
 
 struct vgicp_graph_s {

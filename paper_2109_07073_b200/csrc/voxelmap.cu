@@ -604,11 +604,14 @@ __global__ void __launch_bounds__(256, 4) overlap_occ_kernel(const OverlapItem* 
                                                              unsigned long long* __restrict__ hits) {
   __shared__ unsigned cnt[kOvMaps];
   __shared__ OccScreen scr[kOvMaps];
+  __shared__ unsigned live_n[kOvMaps];
   const int2 ch = chunks[blockIdx.y];
-  const unsigned n = items[ch.x].n;
+  unsigned n = 0;  // points of the chunk's cloud (items culled on the device carry n = 0)
+  for (int q = 0; q < ch.y; ++q) n = max(n, items[ch.x + q].n);
   if (blockIdx.x * (256 * kOccPoints) >= n) return;
   for (int t = threadIdx.x; t < ch.y * 7; t += 256)  // stage the chunk's screens (7 × 16 B each)
     reinterpret_cast<uint4*>(&scr[t / 7])[t % 7] = __ldg(reinterpret_cast<const uint4*>(&items[ch.x + t / 7].scr) + t % 7);
+  if (threadIdx.x < ch.y) live_n[threadIdx.x] = items[ch.x + threadIdx.x].n;
   if (threadIdx.x < kOvMaps) cnt[threadIdx.x] = 0;
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned base = blockIdx.x * (256 * kOccPoints) + warp * (32 * kOccPoints);
@@ -626,6 +629,7 @@ __global__ void __launch_bounds__(256, 4) overlap_occ_kernel(const OverlapItem* 
   }
   __syncthreads();
   for (int k = 0; k < ch.y; ++k) {
+    if (live_n[k] == 0u) continue;  // culled on the device (map-set sweeps): exactly 0 hits
     const OccScreen& sc = scr[k];
     unsigned word[kOccPoints], bit[kOccPoints];
     unsigned ok = 0, need = 0;
@@ -675,6 +679,65 @@ __global__ void __launch_bounds__(256, 4) overlap_occ_kernel(const OverlapItem* 
   __syncthreads();
   if (threadIdx.x < ch.y && cnt[threadIdx.x])
     atomicAdd(&hits[ch.x + threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
+}
+
+// Item k of a map-set sweep: the map's template + pose k; fp32 screen constants as the host path
+// computes them (fl32 of the fp64 values, same margin formula); exact culling of the cloud box
+// (8 corners in fp64) against the map's occupied box grown by one voxel -> n = 0 (no work).
+__global__ void mapset_prepare_kernel(const OverlapItem* __restrict__ templates, int m,
+                                      const double* __restrict__ poses12, const PointBlock* blk, unsigned n,
+                                      const float* __restrict__ box, OverlapItem* __restrict__ items,
+                                      int2* __restrict__ chunks) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  OverlapItem it = templates[k];
+  const double* T = poses12 + 12 * k;
+#pragma unroll
+  for (int q = 0; q < 12; ++q) it.T[q] = T[q];
+  it.blk = blk;
+  it.n = n;
+  float tmax = 0.f;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) it.scr.R[q] = __double2float_rn(T[q]);
+#pragma unroll
+  for (int q = 0; q < 3; ++q) it.scr.t[q] = __double2float_rn(T[9 + q]), tmax = fmaxf(tmax, fabsf(it.scr.t[q]));
+  it.scr.inv_r = __double2float_rn(it.map.inv_res);
+  it.scr.A2 = __fmul_rn(5e-7f, it.scr.inv_r);
+  it.scr.C = __fadd_rn(__fmul_rn(it.scr.A2, tmax), 1e-7f);
+  // culling (the host's overlap_disjoint): the cloud box has no finite point when lo > hi
+  bool live = box[0] <= box[3];
+  if (live) {
+    double wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int c = 0; c < 8; ++c) {
+      const double p0 = (c & 1) ? box[3] : box[0], p1 = (c & 2) ? box[4] : box[1], p2 = (c & 4) ? box[5] : box[2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double q = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(T[3 * a], p0), __dmul_rn(T[3 * a + 1], p1)),
+                                             __dmul_rn(T[3 * a + 2], p2)),
+                                   T[9 + a]);
+        wlo[a] = fmin(wlo[a], q);
+        whi[a] = fmax(whi[a], q);
+      }
+    }
+    const int cmin[3] = {it.scr.cx0, it.scr.cy0, it.scr.cz0};
+    const unsigned ext[3] = {it.scr.ex, it.scr.ey, it.scr.ez};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double mlo = (cmin[a] - 1.0) * it.map.res, mhi = (cmin[a] + static_cast<int>(ext[a]) + 1.0) * it.map.res;
+      live = live && (whi[a] >= mlo && wlo[a] <= mhi);
+    }
+  }
+  if (!live) it.n = 0;  // culled: exactly 0 hits
+  items[k] = it;
+  if (k % kOvMaps == 0) chunks[k / kOvMaps] = make_int2(k, min(kOvMaps, m - k));
+}
+
+cudaError_t launch_mapset_prepare(const OverlapItem* templates, int m, const double* poses12, const PointBlock* blk,
+                                  unsigned n, const float* cloud_box, OverlapItem* items, int2* chunks,
+                                  cudaStream_t s) {
+  if (m <= 0) return cudaSuccess;
+  mapset_prepare_kernel<<<(m + 127) / 128, 128, 0, s>>>(templates, m, poses12, blk, n, cloud_box, items, chunks);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_overlap_occ(const OverlapItem* items, const int2* chunks, int num_chunks, unsigned max_n,

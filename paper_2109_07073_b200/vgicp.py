@@ -401,6 +401,22 @@ class MapSet:
         self.maps = list(maps)
         self.handles = np.fromiter((x.handle.value for x in self.maps), dtype=np.uint64, count=len(self.maps))
         self.ctx = self.maps[0].ctx if self.maps else None
+        self._h = None
+        if self.maps:  # device-resident copy (vgicp_mapset): single-cloud sweeps build their items on the GPU
+            h = C.c_void_p()
+            check(_lib.load().vgicp_mapset_create(self.ctx.handle, _ptr(self.handles), len(self.maps), C.byref(h)))
+            self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().vgicp_mapset_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def __len__(self) -> int:
         return len(self.maps)
@@ -427,6 +443,9 @@ def overlap_hits(clouds, poses, maps) -> np.ndarray:
     if m == 0:
         return hits
     ctx = maps[0].ctx
+    if map_set is not None and single_cloud and map_set._h is not None:
+        check(_lib.load().vgicp_overlap_mapset(ctx.handle, clouds[0].handle, _ptr(P), map_set._h, _ptr(hits)))
+        return hits
     # handle arrays as uint64 (pointer-sized) numpy arrays: cheap to build for thousands of maps
     if single_cloud:
         ch = np.full(m, clouds[0].handle.value, np.uint64)

@@ -233,7 +233,7 @@ def test_overlap_batch_matches_serial(ctx):  # test_reference.cpp:59-69
     rates = V.overlap_rates(qc, rels, [g] * 10)
     for rel, r in zip(rels, rates):
         assert r == O.overlap_rate(qm, rel, omap, serial=True)
-    assert np.array_equal(V.overlap_rates(qc, rels, V.MapSet([g] * 10)), rates)  # cached handle array
+    assert np.array_equal(V.overlap_rates(qc, rels, V.MapSet([g] * 10)), rates)  # device map set
 
 
 @pytest.mark.parametrize("res", [0.25, 1.0, 2.0])
@@ -302,6 +302,40 @@ def test_overlap_fp32_screen_near_faces(ctx, res, shift):
         ref = O.overlap_hits(qm, T, omap)
         assert h == ref, (h, ref)
         assert 0 < ref < len(qm)
+
+
+def test_overlap_mapset_sweep_matches_batch(ctx, monkeypatch):
+    """vgicp_overlap_mapset (items built and culled on the device) equals vgicp_overlap_batch and the
+    oracle: near, far (culled), grazing poses, maps of three resolutions, a map set without bitmaps."""
+    rng = O.Rng(95)
+    maps, omaps = [], []
+    for k, res in enumerate([0.5, 1.0, 2.0, 1.0, 0.5]):
+        means, covs = rng.gaussian_cloud(2500, 10.0 + 3 * k)
+        c, m, c9 = gpu_cloud(ctx, means, covs)
+        maps.append(V.GaussianVoxelMap(c, res))
+        omaps.append(O.OracleMap(m, c9, res))
+    q, qm, _ = gpu_cloud(ctx, rng.gaussian_cloud(4000, 12.0)[0])
+    rels = []
+    for k in range(len(maps)):
+        T = rng.random_pose(0.3, 2.0)
+        if k == 2:
+            T[9] = 1e4  # far: culled on the device
+        rels.append(T)
+    rels_all = rels * 8  # 40 probes: two chunks of 32
+    maps_all = maps * 8
+    ms = V.MapSet(maps_all)
+    h_set = V.overlap_hits(q, rels_all, ms)
+    h_batch = V.overlap_hits(q, rels_all, maps_all)
+    assert list(h_set) == list(h_batch)
+    for T, om, h in zip(rels_all, omaps * 8, h_set):
+        assert h == O.overlap_hits(qm, T, om)
+    assert h_set[2] == 0
+    monkeypatch.setenv("VGICP_NO_OCCUPANCY", "1")  # maps without bitmaps: the generic path
+    g_hash = V.GaussianVoxelMap(gpu_cloud(ctx, *rng.gaussian_cloud(2000, 9.0))[0], 1.0)
+    monkeypatch.delenv("VGICP_NO_OCCUPANCY")
+    mixed = V.MapSet([g_hash] + maps)
+    hm = V.overlap_hits(q, [rels[0]] + rels, mixed)
+    assert list(hm[1:]) == list(h_batch[:5])
 
 
 # ------------------------------------------------------------------------------ factors
