@@ -278,6 +278,38 @@ inline std::vector<double> overlap_rates(const PointCloud& cloud, const std::vec
   return out;
 }
 
+// A keyframe database kept on the device (vgicp_mapset): sweeps of one new frame against all its
+// maps build and cull their probe items on the GPU (pipeline.cpp:135-150 with the submap list fixed).
+class KeyframeSet {
+ public:
+  KeyframeSet(const Context& ctx, const std::vector<const GaussianVoxelMap*>& maps) : ctx_(ctx) {
+    std::vector<vgicp_map> mh;
+    for (const auto* m : maps) mh.push_back(m->get());
+    vgicp_mapset h = nullptr;
+    check(vgicp_mapset_create(ctx.get(), mh.data(), static_cast<int>(mh.size()), &h));
+    h_.reset(h, [](vgicp_mapset x) { vgicp_mapset_destroy(x); });
+    size_ = maps.size();
+  }
+  // exact hits / N of `cloud` through poses[k] (T_map⁻¹·T_cloud) against map k
+  std::vector<double> overlap_rates(const PointCloud& cloud, const std::vector<Pose>& poses) const {
+    if (poses.size() != size_) throw std::invalid_argument("poses and maps differ in length");
+    std::vector<double> P(12 * size_);
+    for (std::size_t k = 0; k < size_; ++k)
+      for (int q = 0; q < 12; ++q) P[12 * k + q] = poses[k].m[q];
+    std::vector<std::uint64_t> hits(size_);
+    check(vgicp_overlap_mapset(ctx_.get(), cloud.get(), P.data(), h_.get(), hits.data()));
+    std::vector<double> out(size_);
+    for (std::size_t k = 0; k < size_; ++k) out[k] = static_cast<double>(hits[k]) / static_cast<double>(cloud.size());
+    return out;
+  }
+  std::size_t size() const { return size_; }
+
+ private:
+  Context ctx_;
+  std::shared_ptr<vgicp_mapset_s> h_;
+  std::size_t size_ = 0;
+};
+
 struct LinearizedFactor {  // factors.hpp:19-29
   int i = -1;
   int j = -1;

@@ -125,6 +125,14 @@ int main() {
     }
   }
 
+  // keyframe set sweep == per-map overlap_rate
+  {
+    KeyframeSet set(ctx, {map.get(), map.get()});
+    const auto r = set.overlap_rates(*cloud, {Pose::Identity(), T});
+    REQUIRE(r.size() == 2 && r[0] == overlap_rate(*cloud, Pose::Identity(), *map) &&
+            r[1] == overlap_rate(*cloud, T, *map));
+  }
+
   // native LM (optimizer.cpp:88-194): the error never increases along the trace, the fixed pose
   // stays put, accepted records carry the new error
   {
