@@ -1600,6 +1600,12 @@ int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, doubl
                  "back %llu owner-update %llu owner-factor %llu\n",
                  graph->band_cluster, graph->band_bw, S, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5],
                  prof[6], prof[7]);
+    unsigned long long cprof[5];
+    VG_CUDA(cudaMemcpy(cprof, reinterpret_cast<unsigned long long*>(graph->band_dev.status) + 24, sizeof(cprof),
+                       cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "  chain column (rank 0): diag-update %llu chol %llu sync1 %llu trsm %llu sync2 %llu\n",
+                 cprof[0], cprof[1], cprof[2], cprof[3], cprof[4]);
+    VG_CUDA(cudaMemset(reinterpret_cast<unsigned long long*>(graph->band_dev.status) + 24, 0, sizeof(cprof)));
   }
   if (*h_status != 0) {
     *solved = 0;  // a pivot block was not positive definite (block_solver.cpp:78-82)

@@ -240,6 +240,14 @@ __device__ void factor_column(const SolveArgs& a, double* col, int k) {
 // the other warps update the sub-diagonal rows and the augmented row; then every thread solves
 // its TRSM rows. Same arithmetic (and order per entry) as update_columns + factor_column.
 __device__ void chain_column(const SolveArgs& a, double* col, const double* pj, int j, int n1, int R, bool upd) {
+#if VG_SOLVE_PROF
+  unsigned long long* cp = reinterpret_cast<unsigned long long*>(a.d.status) + 24;
+  long long c0 = clock64();
+  const bool prof = cooperative_groups::this_cluster().block_rank() == 0 && threadIdx.x == 0;
+#define VG_CTICK(q) do { if (prof) { const long long c1 = clock64(); cp[q] += c1 - c0; c0 = c1; } } while (0)
+#else
+#define VG_CTICK(q) ((void)0)
+#endif
   const int aug = col_aug(a.d.bw);
   double* inv = col + aug + 8;
   const double* Lk = pj + 36 * (n1 - j);  // L_{n1,j}
@@ -255,6 +263,7 @@ __device__ void chain_column(const SolveArgs& a, double* col, const double* pj, 
   if (threadIdx.x < 32) {
     if (upd && threadIdx.x < 6) upd_row(col + 6 * threadIdx.x, Lk + 6 * threadIdx.x);
     __syncwarp();
+    VG_CTICK(0);
     if (threadIdx.x == 0) {
       double L[6][6];
 #pragma unroll
@@ -285,6 +294,7 @@ __device__ void chain_column(const SolveArgs& a, double* col, const double* pj, 
         for (int c = 0; c < 6; ++c) col[6 * r + c] = c <= r ? L[r][c] : 0.0;
       col[aug + 6] = failed ? 1.0 : 0.0;
     }
+    VG_CTICK(1);
   } else if (upd) {
     const int rows = (R - n1) * 6;  // sub-diagonal entry rows touched by panel j, then the aug row
     for (int t = threadIdx.x - 32; t <= rows; t += kSolveThreads - 32) {
@@ -297,6 +307,7 @@ __device__ void chain_column(const SolveArgs& a, double* col, const double* pj, 
     }
   }
   __syncthreads();
+  VG_CTICK(2);
   if (col[aug + 6] != 0.0) return;
   const int nrows = (a.d.reach[n1] - n1) * 6 + 1;
   for (int t = threadIdx.x; t < nrows; t += kSolveThreads) {
@@ -312,7 +323,10 @@ __device__ void chain_column(const SolveArgs& a, double* col, const double* pj, 
 #pragma unroll
     for (int c = 0; c < 6; ++c) v[c] = x[c];
   }
+  VG_CTICK(3);
   __syncthreads();
+  VG_CTICK(4);
+#undef VG_CTICK
 }
 
 __device__ void copy_record(double* __restrict__ dst, const double* __restrict__ src, int n) {
