@@ -261,15 +261,26 @@ __device__ void chain_column(const SolveArgs& a, double* col, const double* pj, 
     }
   };
   if (threadIdx.x < 32) {
-    if (upd && threadIdx.x < 6) upd_row(col + 6 * threadIdx.x, Lk + 6 * threadIdx.x);
-    __syncwarp();
     VG_CTICK(0);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // diagonal update fused into the Cholesky thread (no smem round trip)
       double L[6][6];
 #pragma unroll
       for (int r = 0; r < 6; ++r)
 #pragma unroll
         for (int c = 0; c <= r; ++c) L[r][c] = col[6 * r + c];
+      if (upd) {
+        double K[6][6];
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int q = 0; q < 6; ++q) K[r][q] = Lk[6 * r + q];
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int c = 0; c <= r; ++c)  // same per-entry order as update_columns
+            L[r][c] -= ((((K[r][0] * K[c][0] + K[r][1] * K[c][1]) + K[r][2] * K[c][2]) + K[r][3] * K[c][3]) +
+                        K[r][4] * K[c][4]) + K[r][5] * K[c][5];
+      }
       bool failed = false;
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
