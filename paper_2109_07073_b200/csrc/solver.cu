@@ -20,14 +20,11 @@
 // Afterwards CTA 0 runs the backward substitution (one warp, columns TMA-prefetched two ahead).
 // Fixed operation order everywhere: results are deterministic.
 //
-// Measured on C3 (449 slots, RCM block bandwidth 31, 16-CTA cluster): 1.86 ms per damped solve vs
-// 1.84 ms for the dense cuSOLVER potrf/potrs of the 2,694-dim system. The 449-step dependency chain
-// costs ~4.3k cycles per step (DSMEM hand-off to the next owner ~1.2k, its update + 6×6 Cholesky +
-// TRSM ~3.1k) and the backward substitution ~1.3k per step. C5 (999 slots, bandwidth 47): 4.1 ms vs
-// 5.3 ms dense. The dense path stays the LM's default up to 3,000 unknowns; the band solver takes
-// over beyond (memory O(S·bw) instead of O(S²), time
-// O(S·bw²) instead of O(S³)). Build with -DVG_SOLVE_PROF=1 for a per-phase cycle profile
-// (printed with VGICP_SOLVE_PROF=1).
+// Measured on C3 (449 slots, RCM block bandwidth 31, 16-CTA cluster): 1.62 ms per damped solve vs
+// 1.84 ms for the dense cuSOLVER potrf/potrs of the 2,694-dim system; C5 (999 slots, bandwidth 47):
+// 3.8 ms vs 5.3 ms. The 449-step dependency chain bounds it (per step: DSMEM hand-off to the next
+// owner, its diagonal update + 6×6 Cholesky + TRSM). The LM uses it above 2,000 unknowns (dense
+// below). Build with -DVG_SOLVE_PROF=1 for a per-phase cycle profile (VGICP_SOLVE_PROF=1 prints it).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -47,6 +44,7 @@ constexpr int kSolveThreads = 256;
 #ifndef VG_SOLVE_PROF
 #define VG_SOLVE_PROF 0
 #endif
+
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -169,16 +167,9 @@ __device__ void update_columns(const SolveArgs& a, double* slots, const double* 
   }
 }
 
-// 1/sqrt(x) for the pivots: MUFU fp32 estimate + two fp64 Newton steps (~1 ulp), IEEE fallback
-// outside the fp32 range.
-__device__ __forceinline__ double rsqrt_fast(double x) {
-  if (!(x > 1e-30 && x < 1e30)) return 1.0 / sqrt(x);
-  double y = static_cast<double>(rsqrtf(static_cast<float>(x)));
-  const double hx = 0.5 * x;
-  y = y * (1.5 - hx * y * y);
-  y = y * (1.5 - hx * y * y);
-  return y;
-}
+// 1/sqrt(x) for the pivots: libdevice's fp64 rsqrt (MUFU.RSQ64H seed + refinement) — measured
+// faster on the pivot chain than an fp32-seeded Newton pair (C3 solve 1.72 -> 1.62 ms).
+__device__ __forceinline__ double rsqrt_fast(double x) { return rsqrt(x); }
 
 // Factor column k in place (all threads of the CTA): 6×6 Cholesky of the diagonal block (warp
 // 0; a pivot that is not > 0 fails like Eigen::LLT, block_solver.cpp:78-82), then

@@ -353,7 +353,7 @@ def graph_bandwidth(ij, active) -> int:
     return int(6 * np.max(np.abs(rank[ij[both, 0]] - rank[ij[both, 1]])) + 5)
 
 
-DENSE_SOLVE_MAX_UNKNOWNS = 3000  # above: the GPU block-band solver (vgicp_graph_solve_damped)
+DENSE_SOLVE_MAX_UNKNOWNS = 2000  # above: the GPU block-band solver (vgicp_graph_solve_damped)
 
 
 def _sequential_total(errors) -> float:
@@ -372,8 +372,8 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
     band_solve by the block-band Cholesky kernel over a reverse Cuthill-McKee order
     (vgicp_graph_solve_damped, solve_block_system of block_solver.cpp:64-122) when its envelope fits
     one thread-block cluster, else by a dense cuSOLVER Cholesky. band_solve=None picks the band
-    kernel above DENSE_SOLVE_MAX_UNKNOWNS reduced unknowns (measured: 1.86 vs 1.84 ms at C3's 2,694
-    unknowns, 4.1 vs 5.3 ms at C5's 5,994; dense memory and time grow as m² and m³).
+    kernel above DENSE_SOLVE_MAX_UNKNOWNS reduced unknowns (measured: 1.62 vs 1.84 ms at C3's 2,694
+    unknowns, 3.8 vs 5.3 ms at C5's 5,994; dense memory and time grow as m² and m³).
 
     With speculative (device assembly only), every candidate is scored by LINEARIZING it instead of
     evaluating it: the linearization's per-factor errors equal evaluate_matching_cost's bit for
