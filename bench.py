@@ -324,7 +324,7 @@ def run_lm_c3(wl, max_iterations=30):
                 "per damping trial, host retraction; wall clock",
         "python_speculative": {"ms_per_lm_iteration_median": med(srep), "iterations": srep.iterations,
                                "final_error": srep.final_error, "ms_total": 1e3 * srep.wall_time_seconds,
-                               "note": "paper_2109_07073_b200/optimizer.py, dense cuSOLVER Cholesky"},
+                               "note": "paper_2109_07073_b200/optimizer.py (Python loop), same device kernels"},
         "plain_loop": {"ms_per_lm_iteration_median": med(prep), "iterations": prep.iterations,
                        "final_error": prep.final_error,
                        "identical_trace": [t.error for t in prep.trace] == [t.error for t in srep.trace],
