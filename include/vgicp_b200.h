@@ -214,7 +214,9 @@ int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, doubl
 /* optimize (optimizer.cpp:88-194) for a graph whose factors are all matching-cost factors, in the
  * library: every candidate is linearized + assembled on the device and scored by its per-factor
  * errors (= total_error), the damped system is solved on the device (block-band Cholesky) or on the
- * host, Pose::retract (se3.cpp:93-105) on the host. Same damping schedule, acceptance rule,
+ * host (a dense O(m³) Cholesky: meant for small systems — the band solver covers envelopes up to ~80
+ * blocks after reverse Cuthill-McKee, e.g. C5's 1,000 poses need 47), Pose::retract (se3.cpp:93-105)
+ * on the host. Same damping schedule, acceptance rule,
  * termination reasons and gauge anchoring (effective_fixed_mask, optimizer.cpp:24-43) as the
  * reference. poses12 (num_poses × 12) is updated in place unless the solve aborts; fixed (may be
  * NULL) marks user-fixed poses; updates (may be NULL) carries each pose's
