@@ -1531,7 +1531,7 @@ int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported) {
   const int S = graph->num_slots, P = graph->num_pairs;
   const BandPlanHost hp = make_band_plan(S, P, graph->pair_ab.data());
   graph->band_bw = hp.bw;
-  graph->band_cluster = S > 0 && !std::getenv("VGICP_NO_BAND_SOLVER") ? band_cluster_size(hp.bw) : 0;
+  graph->band_cluster = S > 0 && !std::getenv("VGICP_NO_BAND_SOLVER") ? band_cluster_size(hp.bw, S) : 0;
   cudaGetLastError();  // attribute / occupancy probes that failed are not launch errors
   *bandwidth = hp.bw;
   *supported = graph->band_cluster > 0 ? 1 : 0;

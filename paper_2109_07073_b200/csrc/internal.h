@@ -201,8 +201,8 @@ struct BandDev {
   int* ready;   // S publication flags (launch epoch)
 };
 BandPlanHost make_band_plan(int S, int P, const int32_t* pairs);
-size_t band_smem_bytes(int bw, int C);
-int band_cluster_size(int bw);
+size_t band_smem_bytes(int bw, int C, int S);
+int band_cluster_size(int bw, int S);
 cudaError_t launch_band_solve(const BandDev& d, int C, const double* assembled, int num_pairs, double lam,
                               int epoch, cudaStream_t s);
 // transform_cloud (point_cloud.cpp:26-42) of float32 device clouds into fp64 arrays, batched:

@@ -20,8 +20,8 @@
 // Afterwards CTA 0 runs the backward substitution (one warp, columns TMA-prefetched two ahead).
 // Fixed operation order everywhere: results are deterministic.
 //
-// Measured on C3 (449 slots, RCM block bandwidth 31, 16-CTA cluster): 1.62 ms per damped solve vs
-// 1.84 ms for the dense cuSOLVER potrf/potrs of the 2,694-dim system; C5 (999 slots, bandwidth 47):
+// Measured on C3 (449 slots, RCM block bandwidth 31, 16-CTA cluster): 1.57 ms per damped solve vs
+// 1.81 ms for the dense cuSOLVER potrf/potrs of the 2,694-dim system; C5 (999 slots, bandwidth 47):
 // 3.8 ms vs 5.3 ms. The 449-step dependency chain bounds it (per step: DSMEM hand-off to the next
 // owner, its diagonal update + 6×6 Cholesky + TRSM). The LM uses it above 2,000 unknowns (dense
 // below). Build with -DVG_SOLVE_PROF=1 for a per-phase cycle profile (VGICP_SOLVE_PROF=1 prints it).
@@ -90,13 +90,13 @@ struct SolveArgs {
 
 // Zero column k's record, then scatter its blocks from the assembled system (damped diagonal,
 // off-diagonal pairs — transposed where the order flips the pair — and the rhs row).
-__device__ void load_columns(const SolveArgs& a, double* slots, int first, int last, int C, int rank) {
+__device__ void load_columns(const SolveArgs& a, const int* reach, double* slots, int first, int last, int C, int rank) {
   const BandDev& d = a.d;
   const int cs = col_stride(d.bw);
   const int aug = col_aug(d.bw);
   for (int k = first; k <= last; k += C) {
     double* col = slots + (size_t)((k / C) % a.ns) * cs;
-    const int n = 36 * (d.reach[k] - k + 1);
+    const int n = 36 * (reach[k] - k + 1);
     for (int t = threadIdx.x; t < n; t += kSolveThreads) col[t] = 0.0;
     if (threadIdx.x < 16) col[aug + threadIdx.x] = 0.0;
   }
@@ -174,7 +174,7 @@ __device__ __forceinline__ double rsqrt_fast(double x) { return rsqrt(x); }
 // Factor column k in place (all threads of the CTA): 6×6 Cholesky of the diagonal block (warp
 // 0; a pivot that is not > 0 fails like Eigen::LLT, block_solver.cpp:78-82), then
 // L_ik = A_ik·L_kk⁻ᵀ for the sub-diagonal blocks and y_k = L_kk⁻¹·b_k for the augmented row.
-__device__ void factor_column(const SolveArgs& a, double* col, int k) {
+__device__ void factor_column(const SolveArgs& a, const int* reach, double* col, int k) {
   const int aug = col_aug(a.d.bw);
   double* inv = col + aug + 8;
   if (threadIdx.x == 0) {  // one thread: the pivot chain is short, shuffles would only add latency
@@ -209,7 +209,7 @@ __device__ void factor_column(const SolveArgs& a, double* col, int k) {
   }
   __syncthreads();
   if (col[aug + 6] != 0.0) return;
-  const int nrows = (a.d.reach[k] - k) * 6 + 1;  // sub-diagonal entry rows + the augmented row
+  const int nrows = (reach[k] - k) * 6 + 1;  // sub-diagonal entry rows + the augmented row
   for (int t = threadIdx.x; t < nrows; t += kSolveThreads) {
     double* v = t < nrows - 1 ? col + 36 + 6 * t : col + aug;
     double x[6];
@@ -230,7 +230,8 @@ __device__ void factor_column(const SolveArgs& a, double* col, int k) {
 // column factored, overlapped — warp 0 updates the diagonal block and runs the 6×6 Cholesky while
 // the other warps update the sub-diagonal rows and the augmented row; then every thread solves
 // its TRSM rows. Same arithmetic (and order per entry) as update_columns + factor_column.
-__device__ void chain_column(const SolveArgs& a, double* col, const double* pj, int j, int n1, int R, bool upd) {
+__device__ void chain_column(const SolveArgs& a, const int* reach, double* col, const double* pj, int j, int n1, int R,
+                             bool upd) {
 #if VG_SOLVE_PROF
   unsigned long long* cp = reinterpret_cast<unsigned long long*>(a.d.status) + 24;
   long long c0 = clock64();
@@ -311,7 +312,7 @@ __device__ void chain_column(const SolveArgs& a, double* col, const double* pj, 
   __syncthreads();
   VG_CTICK(2);
   if (col[aug + 6] != 0.0) return;
-  const int nrows = (a.d.reach[n1] - n1) * 6 + 1;
+  const int nrows = (reach[n1] - n1) * 6 + 1;
   for (int t = threadIdx.x; t < nrows; t += kSolveThreads) {
     double* v = t < nrows - 1 ? col + 36 + 6 * t : col + aug;
     double x[6];
@@ -349,7 +350,11 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
   const int aug = col_aug(d.bw);
   double* slots = smem;                     // ns column records
   double* pj = smem + (size_t)a.ns * cs;    // the current panel
-  const auto rec_len = [&](int k) { return 36 * (d.reach[k] - k + 1); };
+  // envelope reach per column, staged once: it is read on every step of the dependency chain
+  int* reach = reinterpret_cast<int*>(pj + cs);
+  for (int t = threadIdx.x; t < S; t += kSolveThreads) reach[t] = d.reach[t];
+  __syncthreads();
+  const auto rec_len = [&](int k) { return 36 * (reach[k] - k + 1); };
   const auto panel_bytes = [&](int k) { return static_cast<unsigned>(sizeof(double) * (rec_len(k) + 16)); };
   const auto slot_of = [&](int k) { return slots + (size_t)((k / C) % a.ns) * cs; };
 
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
     int last = next - C;
     while (last + C <= limit && last + C < S) last += C;
     if (last >= next) {
-      load_columns(a, slots, next, last, C, rank);
+      load_columns(a, reach, slots, next, last, C, rank);
       next = last + C;
     }
   };
@@ -431,9 +436,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
   };
 
   if (S > 0) {
-    ensure_loaded(max(d.reach[0], 0));
+    ensure_loaded(max(reach[0], 0));
     if (rank == 0) {
-      factor_column(a, slots, 0);
+      factor_column(a, reach, slots, 0);
       publish(0);
     }
   }
@@ -446,7 +451,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
 #define VG_TICK(q) ((void)0)
 #endif
   for (int j = 0; j < S; ++j) {
-    const int R = d.reach[j];
+    const int R = reach[j];
     const int n1 = j + 1;
     receive(j);
     VG_TICK(0);
@@ -459,7 +464,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
     if (n1 < S && n1 % C == rank) {  // on the chain: only column n1 must be resident first
       ensure_loaded(n1);
       VG_TICK(6);
-      chain_column(a, slot_of(n1), pj, j, n1, R, n1 <= R);
+      chain_column(a, reach, slot_of(n1), pj, j, n1, R, n1 <= R);
       VG_TICK(7);
       publish(n1);
       lo = n1 + C;
@@ -511,7 +516,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
     if (k > 0) wait_col(k - 1);
     const double* L = buf((S - 1 - k) % 3);
     if (warp == 0) {  // the chain: x_k
-      const int nb = d.reach[k] - k;
+      const int nb = reach[k] - k;
       if (lane < 6) {  // lane c: v_c = y_c - P_c - (L_{k+1,k}ᵀ x_{k+1})_c
         double t = 0.0;
         if (nb >= 1) {
@@ -541,7 +546,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
       const int c = warp - 1;
       const int k1 = k - 1;
       const double* L1 = buf((S - 1 - k1) % 3);
-      const int nb1 = d.reach[k1] - k1;
+      const int nb1 = reach[k1] - k1;
       double sum = 0.0;
       for (int t = lane; t < 6 * (nb1 - 1); t += 32) {  // blocks b = 2 .. nb1
         const int bb = 2 + t / 6, r = t % 6;
@@ -670,19 +675,19 @@ BandPlanHost make_band_plan(int S, int P, const int32_t* pairs) {
   return p;
 }
 
-size_t band_smem_bytes(int bw, int C) {
+size_t band_smem_bytes(int bw, int C, int S) {
   const int ns = std::max(bw / C + 1, 4);  // >= 4: the backward substitution reuses the slot area
   const size_t rec = sizeof(double) * col_stride(bw);
-  return (ns + 1) * rec;
+  return (ns + 1) * rec + sizeof(int) * static_cast<size_t>(S);  // + the staged reach array
 }
 
 // Largest cluster (16, else 8, 4, 2, 1) that can be co-resident with this bandwidth's window.
-int band_cluster_size(int bw) {
+int band_cluster_size(int bw, int S) {
   cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncAttributes fa{};
   cudaFuncGetAttributes(&fa, band_solve_kernel);
   for (int C : {16, 8, 4, 2, 1}) {
-    const size_t smem = band_smem_bytes(bw, C);
+    const size_t smem = band_smem_bytes(bw, C, S);
     if (smem + fa.sharedSizeBytes > 227 * 1024 || bw / C + 1 > 16) continue;
     if (cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
         cudaSuccess) {
@@ -720,7 +725,7 @@ cudaError_t launch_band_solve(const BandDev& d, int C, const double* assembled, 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(kSolveThreads);
-  cfg.dynamicSmemBytes = band_smem_bytes(d.bw, C);
+  cfg.dynamicSmemBytes = band_smem_bytes(d.bw, C, d.S);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
