@@ -276,7 +276,8 @@ def run_lm_c2(ctx, threads):
     native = {"ms_per_lm_iteration_median": 1e3 * nits[len(nits) // 2] if nits else None,
               "iterations": nrep.iterations, "final_error": nrep.final_error, "reason": nrep.reason,
               "band_solver": nrep.band_solver,
-              "note": "native LM (vgicp_graph_optimize): device linearize + assembly, device block-band Cholesky"}
+              "note": "native LM (vgicp_graph_optimize): device linearize + assembly; the chain's narrow system "
+                      "is solved by a host band Cholesky (device band solver when band_solver is true)"}
     cpu = None
     try:  # the same LM around the CPU oracle port (reference arm of "ms per LM iteration")
         all_threads = os.cpu_count() or 1

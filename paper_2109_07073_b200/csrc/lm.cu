@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -156,6 +157,61 @@ struct PoolBuffer {  // stream-ordered device temporary (the context's pool)
   }
 };
 
+// Banded Cholesky solve in slot order (narrow systems, e.g. odometry chains): the damped system in
+// lower band storage of half-bandwidth w (scalars), LAPACK dpbtrf/dpbtrs arithmetic without
+// blocking. O(m·w²); false when not positive definite.
+bool host_band_solve(int S, int P, const std::vector<int32_t>& pairs, const double* asmb, double lam, int w,
+                     std::vector<double>& x) {
+  const int m = 6 * S;
+  const int W = w + 1;
+  std::vector<double> B(static_cast<size_t>(m) * W, 0.0), b(m);  // B[i*W + (i - j)] = A(i, j), i >= j
+  auto at = [&](int i, int j) -> double& { return B[static_cast<size_t>(i) * W + (i - j)]; };
+  const double* diag = asmb;
+  const double* off = asmb + static_cast<size_t>(S) * 36;
+  const double* rhs = asmb + static_cast<size_t>(S + P) * 36;
+  for (int s = 0; s < S; ++s)
+    for (int r = 0; r < 6; ++r) {
+      for (int c = 0; c <= r; ++c) at(6 * s + r, 6 * s + c) = diag[36 * s + 6 * r + c];
+      b[6 * s + r] = rhs[6 * s + r];
+    }
+  for (int q = 0; q < P; ++q) {  // (row a, col b) block, a > b
+    const int a = pairs[2 * q], bb = pairs[2 * q + 1];
+    for (int r = 0; r < 6; ++r)
+      for (int c = 0; c < 6; ++c) at(6 * a + r, 6 * bb + c) = off[36 * q + 6 * r + c];
+  }
+  for (int k = 0; k < m; ++k) {
+    double& d = at(k, k);
+    d = d + lam * std::max(d, 1e-10);
+  }
+  for (int j = 0; j < m; ++j) {
+    double d = at(j, j);
+    const int k0 = std::max(0, j - w);
+    for (int k = k0; k < j; ++k) d -= at(j, k) * at(j, k);
+    if (!(d > 0.0)) return false;
+    const double l = std::sqrt(d);
+    at(j, j) = l;
+    const int i1 = std::min(m - 1, j + w);
+    for (int i = j + 1; i <= i1; ++i) {
+      double v = at(i, j);
+      const int kk = std::max(k0, i - w);
+      for (int k = kk; k < j; ++k) v -= at(i, k) * at(j, k);
+      at(i, j) = v / l;
+    }
+  }
+  x.assign(m, 0.0);
+  for (int i = 0; i < m; ++i) {
+    double v = b[i];
+    for (int k = std::max(0, i - w); k < i; ++k) v -= at(i, k) * x[k];
+    x[i] = v / at(i, i);
+  }
+  for (int i = m - 1; i >= 0; --i) {
+    double v = x[i];
+    for (int k = i + 1; k <= std::min(m - 1, i + w); ++k) v -= at(k, i) * x[k];
+    x[i] = v / at(i, i);
+  }
+  return true;
+}
+
 int find_root(std::vector<int>& parent, int x) {
   while (parent[x] != x) x = parent[x] = parent[parent[x]];
   return x;
@@ -209,6 +265,14 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
   int bw = 0, band = 0;
   if (S > 0)
     if (int rc = vgicp_graph_solver_plan(graph, &bw, &band)) return rc;
+  // Narrow systems in slot order (odometry chains: a factor links nearby variables) are cheaper on
+  // the host — one small D2H and an O(m·w²) band Cholesky — than a cluster launch whose dependency
+  // chain runs over every slot.
+  int slot_bw = 0;
+  for (int q = 0; q < P; ++q) slot_bw = std::max(slot_bw, pairs[2 * q] - pairs[2 * q + 1]);
+  const int host_w = 6 * slot_bw + 5;
+  const bool host_band = S > 0 && static_cast<double>(6 * S) * host_w * host_w <= 2.0e6 &&
+                         !std::getenv("VGICP_LM_NO_HOST_BAND");  // (test switch: force the device solver)
 
   vgicp_ctx ctx = graph->ctx;
   DeviceScope g(ctx->device);
@@ -241,7 +305,7 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
       *ok = true;
       return VGICP_OK;
     }
-    if (band) {
+    if (band && !host_band) {
       int solved = 0;
       if (int rc = vgicp_graph_solve_damped(graph, d_asm[which], lam, x.data(), &solved)) return rc;
       *ok = solved != 0;
@@ -250,7 +314,8 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
     host_asm.resize(asm_doubles);
     VG_CUDA(cudaMemcpyAsync(host_asm.data(), d_asm[which], sizeof(double) * asm_doubles, cudaMemcpyDeviceToHost, s));
     VG_CUDA(cudaStreamSynchronize(s));
-    *ok = host_solve(S, P, pairs, host_asm.data(), lam, x);
+    *ok = host_band ? host_band_solve(S, P, pairs, host_asm.data(), lam, host_w, x)
+                    : host_solve(S, P, pairs, host_asm.data(), lam, x);
     return VGICP_OK;
   };
 
@@ -349,7 +414,7 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
   report->trace_length = ntrace;
   report->solves = solves;
   report->linearizations = lins;
-  report->band_solver = band;
+  report->band_solver = band && !host_band;
   report->wall_time_seconds = seconds();
   return VGICP_OK;
 }

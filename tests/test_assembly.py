@@ -302,19 +302,21 @@ def _lm_graph(V, loop, seed=78, nframes=8):
 
 @gpu
 @pytest.mark.parametrize("loop", [False, True])
-@pytest.mark.parametrize("host_solve", [False, True])
-def test_gpu_native_lm_matches_python_lm(V, monkeypatch, loop, host_solve):
+@pytest.mark.parametrize("solver", ["host_band", "gpu_band", "host_dense"])
+def test_gpu_native_lm_matches_python_lm(V, monkeypatch, loop, solver):
     """vgicp_graph_optimize (the LM loop in the library) takes the reference loop's decisions: same
     accepted / rejected sequence, λ schedule, termination reason; errors and poses to 1e-9 (the
-    solvers differ in rounding: band or host Cholesky vs the Python LM's)."""
+    solvers differ in rounding: host band / device band / host dense Cholesky vs the Python LM's)."""
     from paper_2109_07073_b200 import optimizer as LM
 
-    if host_solve:
+    if solver != "host_band":
+        monkeypatch.setenv("VGICP_LM_NO_HOST_BAND", "1")
+    if solver == "host_dense":
         monkeypatch.setenv("VGICP_NO_BAND_SOLVER", "1")
     graph, poses = _lm_graph(V, loop)
     p_py, r_py = LM.optimize(graph, poses, band_solve=False)
     p_nat, r_nat = LM.optimize_native(graph, poses)
-    assert r_nat.band_solver == (not host_solve)
+    assert r_nat.band_solver == (solver == "gpu_band")
     assert r_nat.iterations == r_py.iterations and r_nat.reason == r_py.reason
     assert [(t.accepted, t.lam) for t in r_nat.trace] == [(t.accepted, t.lam) for t in r_py.trace]
     for a, b in zip(r_nat.trace, r_py.trace):
