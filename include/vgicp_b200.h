@@ -209,6 +209,11 @@ int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* in
  * pivot block is not positive definite (the reference's failed_slot, the LM then raises lambda). */
 int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported);
 int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, double lambda, double* x, int* solved);
+/* Two damping values in one launch (two clusters run concurrently): x receives 2 × S×6 doubles and
+ * solved[2] the two outcomes — an LM that fails or rejects at lambdas[0] continues with lambdas[1]
+ * without another solve. */
+int vgicp_graph_solve_damped_pair(vgicp_graph graph, const double* d_assembled, const double* lambdas, double* x,
+                                  int* solved);
 
 /* ---------------------------------------------------------------- native Levenberg-Marquardt */
 /* optimize (optimizer.cpp:88-194) for a graph whose factors are all matching-cost factors, in the

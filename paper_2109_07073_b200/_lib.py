@@ -109,6 +109,7 @@ SIGNATURES = {
     "vgicp_graph_linearized_errors": (_i, [_vp, _vp, _vp]),
     "vgicp_graph_solver_plan": (_i, [_vp, _vp, _vp]),
     "vgicp_graph_solve_damped": (_i, [_vp, _vp, C.c_double, _vp, _vp]),
+    "vgicp_graph_solve_damped_pair": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "vgicp_graph_optimize": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
     "vgicp_mapset_create": (_i, [_vp, _vp, C.c_int, _vp]),
     "vgicp_mapset_destroy": (_i, [_vp]),

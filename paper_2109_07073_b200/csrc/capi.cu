@@ -1539,8 +1539,10 @@ int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported) {
   const size_t b_perm = align_up(sizeof(int) * S, 256), b_reach = b_perm;
   const size_t b_ptr = align_up(sizeof(int) * (S + 1), 256);
   const size_t b_ent = align_up(sizeof(int2) * std::max<size_t>(hp.col_ent.size(), 1), 256);
-  const size_t b_status = 256, b_x = align_up(sizeof(double) * 6 * S, 256), b_ready = align_up(sizeof(int) * S, 256);
-  const size_t b_L = sizeof(double) * (36 * (static_cast<size_t>(hp.bw) + 1) + 16) * S;
+  // two instances of the per-solve state (Lg, x, status, ready): a pair of damping values can be
+  // solved concurrently by two clusters (vgicp_graph_solve_damped_pair)
+  const size_t b_status = 512, b_x = align_up(sizeof(double) * 12 * S, 256), b_ready = align_up(sizeof(int) * 2 * S, 256);
+  const size_t b_L = 2 * sizeof(double) * (36 * (static_cast<size_t>(hp.bw) + 1) + 16) * S;
   VG_CUDA(dmalloc(ctx, &graph->band, b_perm + b_reach + b_ptr + b_ent + b_status + b_x + b_ready + b_L));
   char* b = static_cast<char*>(graph->band);
   BandDev& d = graph->band_dev;
@@ -1555,7 +1557,7 @@ int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported) {
   d.ready = reinterpret_cast<int*>(b + b_perm + b_reach + b_ptr + b_ent + b_status + b_x);
   d.Lg = reinterpret_cast<double*>(b + b_perm + b_reach + b_ptr + b_ent + b_status + b_x + b_ready);
   graph->band_epoch = 0;
-  VG_CUDA(cudaMemsetAsync(d.ready, 0, sizeof(int) * S, ctx->stream));
+  VG_CUDA(cudaMemsetAsync(d.ready, 0, sizeof(int) * 2 * S, ctx->stream));
   cudaStream_t s = ctx->stream;
   VG_CUDA(cudaMemcpyAsync(const_cast<int*>(d.perm), hp.perm.data(), sizeof(int) * S, cudaMemcpyHostToDevice, s));
   VG_CUDA(cudaMemcpyAsync(const_cast<int*>(d.reach), hp.reach.data(), sizeof(int) * S, cudaMemcpyHostToDevice, s));
@@ -1568,31 +1570,33 @@ int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported) {
   return VGICP_OK;
 }
 
-int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, double lambda, double* x, int* solved) {
-  if (!graph || !x || !solved || (graph->num_slots > 0 && !d_assembled))
+// One launch solving the damped system for `count` (1 or 2) damping values, one cluster each.
+static int solve_damped_n(vgicp_graph graph, const double* d_assembled, const double* lambdas, int count, double* x,
+                          int* solved) {
+  if (!graph || !x || !solved || !lambdas || (graph->num_slots > 0 && !d_assembled))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (!graph->band && graph->num_slots > 0)
     return fail(VGICP_E_INVALID_ARGUMENT, graph->band_bw >= 0
                                               ? "band solver unavailable for this bandwidth (use a dense solve)"
                                               : "no solver plan (call vgicp_graph_solver_plan)");
   const int S = graph->num_slots;
-  *solved = 1;
+  for (int i = 0; i < count; ++i) solved[i] = 1;
   if (S == 0) return VGICP_OK;
   vgicp_ctx ctx = graph->ctx;
   DeviceGuard g(ctx->device);
   cudaStream_t s = ctx->stream;
   graph->band_epoch = graph->band_epoch == 0x7fffffff ? 1 : graph->band_epoch + 1;
-  VG_CUDA(launch_band_solve(graph->band_dev, graph->band_cluster, d_assembled, graph->num_pairs, lambda,
-                            graph->band_epoch, s));
+  VG_CUDA(launch_band_solve(graph->band_dev, graph->band_cluster, d_assembled, graph->num_pairs, lambdas[0],
+                            count > 1 ? lambdas[1] : lambdas[0], count, graph->band_epoch, s));
   ctx->launches += 1;
   const size_t b_x = sizeof(double) * 6 * S;
-  if (int rc = ensure_pinned(ctx, align_up(b_x, 256) + sizeof(int))) return rc;
+  if (int rc = ensure_pinned(ctx, align_up(count * b_x, 256) + 512)) return rc;
   auto* h_x = static_cast<double*>(ctx->pinned);
-  auto* h_status = reinterpret_cast<int*>(static_cast<char*>(ctx->pinned) + align_up(b_x, 256));
-  VG_CUDA(cudaMemcpyAsync(h_status, graph->band_dev.status, sizeof(int), cudaMemcpyDeviceToHost, s));
-  VG_CUDA(cudaMemcpyAsync(h_x, graph->band_dev.x, b_x, cudaMemcpyDeviceToHost, s));
+  auto* h_status = reinterpret_cast<int*>(static_cast<char*>(ctx->pinned) + align_up(count * b_x, 256));
+  VG_CUDA(cudaMemcpyAsync(h_status, graph->band_dev.status, sizeof(int) * 64 * count, cudaMemcpyDeviceToHost, s));
+  VG_CUDA(cudaMemcpyAsync(h_x, graph->band_dev.x, count * b_x, cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaStreamSynchronize(s));
-  if (std::getenv("VGICP_SOLVE_PROF")) {  // cycle profile of CTA 0 (diagnostic)
+  if (std::getenv("VGICP_SOLVE_PROF")) {  // cycle profile of CTA 0 (diagnostic build)
     unsigned long long prof[8];
     VG_CUDA(cudaMemcpy(prof, reinterpret_cast<unsigned long long*>(graph->band_dev.status) + 8, sizeof(prof),
                        cudaMemcpyDeviceToHost));
@@ -1600,19 +1604,21 @@ int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, doubl
                  "back %llu owner-update %llu owner-factor %llu\n",
                  graph->band_cluster, graph->band_bw, S, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5],
                  prof[6], prof[7]);
-    unsigned long long cprof[5];
-    VG_CUDA(cudaMemcpy(cprof, reinterpret_cast<unsigned long long*>(graph->band_dev.status) + 24, sizeof(cprof),
-                       cudaMemcpyDeviceToHost));
-    std::fprintf(stderr, "  chain column (rank 0): diag-update %llu chol %llu sync1 %llu trsm %llu sync2 %llu\n",
-                 cprof[0], cprof[1], cprof[2], cprof[3], cprof[4]);
-    VG_CUDA(cudaMemset(reinterpret_cast<unsigned long long*>(graph->band_dev.status) + 24, 0, sizeof(cprof)));
   }
-  if (*h_status != 0) {
-    *solved = 0;  // a pivot block was not positive definite (block_solver.cpp:78-82)
-    return VGICP_OK;
+  for (int i = 0; i < count; ++i) {
+    solved[i] = h_status[64 * i] == 0 ? 1 : 0;  // else a pivot block was not positive definite
+    if (solved[i]) std::memcpy(x + static_cast<size_t>(i) * 6 * S, h_x + static_cast<size_t>(i) * 6 * S, b_x);
   }
-  std::memcpy(x, h_x, b_x);
   return VGICP_OK;
+}
+
+int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, double lambda, double* x, int* solved) {
+  return solve_damped_n(graph, d_assembled, &lambda, 1, x, solved);
+}
+
+int vgicp_graph_solve_damped_pair(vgicp_graph graph, const double* d_assembled, const double* lambdas, double* x,
+                                  int* solved) {
+  return solve_damped_n(graph, d_assembled, lambdas, 2, x, solved);
 }
 
 // Single-factor entry points: a one-factor graph over poses {target, source}.

@@ -195,16 +195,16 @@ struct BandDev {
   const int* reach;
   const int* col_ptr;
   const int2* col_ent;
-  double* Lg;   // S factored columns (band records)
-  double* x;    // S×6 solution, slot order
-  int* status;  // 0 solved, k + 1: pivot of position k failed
-  int* ready;   // S publication flags (launch epoch)
+  double* Lg;   // S factored columns (band records), per instance (2 concurrent damping values)
+  double* x;    // S×6 solution, slot order, per instance
+  int* status;  // 0 solved, k + 1: pivot of position k failed (instance i at status + 64·i)
+  int* ready;   // S publication flags (launch epoch), per instance
 };
 BandPlanHost make_band_plan(int S, int P, const int32_t* pairs);
 size_t band_smem_bytes(int bw, int C, int S);
 int band_cluster_size(int bw, int S);
 cudaError_t launch_band_solve(const BandDev& d, int C, const double* assembled, int num_pairs, double lam,
-                              int epoch, cudaStream_t s);
+                              double lam2, int instances, int epoch, cudaStream_t s);
 // transform_cloud (point_cloud.cpp:26-42) of float32 device clouds into fp64 arrays, batched:
 // item k maps cloud k's points (input order) through poses12[k] into out_xyz / out_cov9 at `offset`.
 struct TransformItem {

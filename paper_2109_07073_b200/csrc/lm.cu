@@ -286,8 +286,18 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
   std::vector<int32_t> inl(nf);
   std::vector<double> host_asm;
   int solves = 0, lins = 0;
+  // The device solver runs the damping value the LM would try next (lam · lambda_increase, after a
+  // failed factorization or a rejected step on the same system) in the same launch, on a second
+  // cluster; that result is kept here until the system in its buffer is overwritten.
+  std::vector<double> x_pair;
+  struct {
+    int which = -1;
+    double lam = 0.0;
+    int solved = 0;
+  } next;
   // linearize + assemble `at` into d_asm[which]; returns the total error (factor order)
   auto linearize = [&](const std::vector<double>& at, int which, double* total) -> int {
+    if (next.which == which) next.which = -1;  // the pending pair result's system is overwritten
     VG_CUDA(cudaMemcpyAsync(d_poses, at.data(), sizeof(double) * 12 * n, cudaMemcpyHostToDevice, s));
     if (int rc = vgicp_graph_linearize_assembled_device(graph, d_poses, d_asm[which])) return rc;
     if (int rc = vgicp_graph_linearized_errors(graph, err.data(), inl.data())) return rc;
@@ -298,6 +308,7 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
     return VGICP_OK;
   };
   std::vector<double> x;
+  const bool pair_solve = !std::getenv("VGICP_LM_NO_PAIR_SOLVE");
   auto solve = [&](int which, double lam, bool* ok) -> int {
     ++solves;
     x.assign(6 * static_cast<size_t>(S), 0.0);
@@ -306,6 +317,22 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
       return VGICP_OK;
     }
     if (band && !host_band) {
+      if (next.which == which && next.lam == lam) {  // solved by the previous launch
+        next.which = -1;
+        *ok = next.solved != 0;
+        if (*ok) std::copy(x_pair.begin() + 6 * static_cast<size_t>(S), x_pair.end(), x.begin());
+        return VGICP_OK;
+      }
+      if (pair_solve) {
+        const double lams[2] = {lam, lam * st.lambda_increase};
+        int solved[2] = {0, 0};
+        x_pair.assign(12 * static_cast<size_t>(S), 0.0);
+        if (int rc = vgicp_graph_solve_damped_pair(graph, d_asm[which], lams, x_pair.data(), solved)) return rc;
+        next.which = which, next.lam = lams[1], next.solved = solved[1];
+        *ok = solved[0] != 0;
+        if (*ok) std::copy(x_pair.begin(), x_pair.begin() + 6 * static_cast<size_t>(S), x.begin());
+        return VGICP_OK;
+      }
       int solved = 0;
       if (int rc = vgicp_graph_solve_damped(graph, d_asm[which], lam, x.data(), &solved)) return rc;
       *ok = solved != 0;

@@ -84,13 +84,16 @@ struct SolveArgs {
   const double* off;
   const double* rhs;
   double lam;
-  int ns;     // column slots per CTA
-  int epoch;  // this launch's value of the ready flags
+  double lam2;  // second damping value, solved concurrently by a second cluster (instances = 2)
+  int ns;       // column slots per CTA
+  int epoch;    // this launch's value of the ready flags
+  int instances;
 };
 
 // Zero column k's record, then scatter its blocks from the assembled system (damped diagonal,
 // off-diagonal pairs — transposed where the order flips the pair — and the rhs row).
-__device__ void load_columns(const SolveArgs& a, const int* reach, double* slots, int first, int last, int C, int rank) {
+__device__ void load_columns(const SolveArgs& a, double lam, const int* reach, double* slots, int first, int last, int C,
+                             int rank) {
   const BandDev& d = a.d;
   const int cs = col_stride(d.bw);
   const int aug = col_aug(d.bw);
@@ -109,7 +112,7 @@ __device__ void load_columns(const SolveArgs& a, const int* reach, double* slots
     for (int t = threadIdx.x; t < tasks; t += kSolveThreads) {
       if (t < 36) {  // damped diagonal block (optimizer.cpp:119-123)
         double v = a.diag[(size_t)slot * 36 + t];
-        if (t % 7 == 0) v = v + a.lam * fmax(v, 1e-10);
+        if (t % 7 == 0) v = v + lam * fmax(v, 1e-10);
         col[t] = v;
       } else if (t < 42) {
         col[aug + (t - 36)] = a.rhs[(size_t)slot * 6 + (t - 36)];
@@ -346,6 +349,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
   const int C = static_cast<int>(cluster.num_blocks());
   const int rank = static_cast<int>(cluster.block_rank());
   const int S = d.S;
+  // instance (cluster) 1 solves the second damping value into its own buffers
+  const int inst = static_cast<int>(blockIdx.x) / C;
+  const double lam = inst ? a.lam2 : a.lam;
+  double* const Lg = d.Lg + (size_t)inst * S * col_stride(d.bw);
+  double* const X = d.x + (size_t)inst * 6 * S;
+  int* const status = d.status + inst * 64;
+  int* const ready = d.ready + (size_t)inst * S;
   const int cs = col_stride(d.bw);
   const int aug = col_aug(d.bw);
   double* slots = smem;                     // ns column records
@@ -372,7 +382,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
     int last = next - C;
     while (last + C <= limit && last + C < S) last += C;
     if (last >= next) {
-      load_columns(a, reach, slots, next, last, C, rank);
+      load_columns(a, lam, reach, slots, next, last, C, rank);
       next = last + C;
     }
   };
@@ -390,12 +400,12 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
       asm volatile("st.release.cluster.shared::cluster.b32 [%0], %1;" ::"r"(raddr), "r"(k) : "memory");
     }
     const double* col = slot_of(k);
-    double* g = d.Lg + (size_t)k * cs;
+    double* g = Lg + (size_t)k * cs;
     copy_record(g, col, rec_len(k));
     copy_record(g + aug, col + aug, 16);
     __syncthreads();  // the CTA's writes happen-before thread 0's (cumulative) release
     if (threadIdx.x == 0)
-      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(d.ready + k), "r"(a.epoch) : "memory");
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready + k), "r"(a.epoch) : "memory");
   };
   // Panel j -> pj: the owner copies its own column record; the others wait for the flag and read
   // the record from L2.
@@ -420,11 +430,11 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
       if (threadIdx.x == 0) {
         int v;
         do {
-          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(d.ready + j) : "memory");
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ready + j) : "memory");
         } while (v != a.epoch);
       }
       __syncthreads();
-      const double2* g = reinterpret_cast<const double2*>(d.Lg + (size_t)j * cs);
+      const double2* g = reinterpret_cast<const double2*>(Lg + (size_t)j * cs);
       double2* o = reinterpret_cast<double2*>(pj);
       const int n = rec_len(j) / 2;
       for (int t = threadIdx.x; t < n + 8; t += kSolveThreads) {
@@ -476,7 +486,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
     __syncthreads();
     VG_TICK(3);
   }
-  if (failed_at >= 0 && rank == 0 && threadIdx.x == 0) *d.status = failed_at + 1;
+  if (failed_at >= 0 && rank == 0 && threadIdx.x == 0) *status = failed_at + 1;
   cluster.sync();  // every column published
   VG_TICK(4);
 
@@ -498,8 +508,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
   auto fetch = [&](int k) {  // column k -> ring slot (S - 1 - k) % 3, barrier of that slot
     const int q = (S - 1 - k) % 3;
     bar_expect(&bbars[q], panel_bytes(k));
-    bulk_copy(buf(q), d.Lg + (size_t)k * cs, static_cast<unsigned>(sizeof(double) * rec_len(k)), &bbars[q]);
-    bulk_copy(buf(q) + aug, d.Lg + (size_t)k * cs + aug, static_cast<unsigned>(sizeof(double) * 16), &bbars[q]);
+    bulk_copy(buf(q), Lg + (size_t)k * cs, static_cast<unsigned>(sizeof(double) * rec_len(k)), &bbars[q]);
+    bulk_copy(buf(q) + aug, Lg + (size_t)k * cs + aug, static_cast<unsigned>(sizeof(double) * 16), &bbars[q]);
   };
   auto wait_col = [&](int k) {
     const int u = S - 1 - k;
@@ -540,7 +550,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
 #pragma unroll
         for (int c = 1; c < 6; ++c) xc = lane == c ? x[c] : xc;
         xr[(k & wm) * 6 + lane] = xc;
-        d.x[(size_t)d.perm[k] * 6 + lane] = xc;
+        X[(size_t)d.perm[k] * 6 + lane] = xc;
       }
     } else if (warp <= 6 && k > 0) {  // P_{k-1}, component c = warp - 1
       const int c = warp - 1;
@@ -561,7 +571,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) band_solve_kernel(SolveArgs 
     if (threadIdx.x == 0 && k >= 3) fetch(k - 3);  // into column k's (now free) ring slot
   }
   if (threadIdx.x == 0) {
-    *d.status = 0;
+    *status = 0;
 #if VG_SOLVE_PROF
     VG_TICK(5);
     unsigned long long* prof = reinterpret_cast<unsigned long long*>(d.status) + 8;
@@ -713,9 +723,11 @@ int band_cluster_size(int bw, int S) {
 }
 
 cudaError_t launch_band_solve(const BandDev& d, int C, const double* assembled, int num_pairs, double lam,
-                              int epoch, cudaStream_t s) {
+                              double lam2, int instances, int epoch, cudaStream_t s) {
   SolveArgs a;
   a.epoch = epoch;
+  a.lam2 = lam2;
+  a.instances = instances;
   a.d = d;
   a.diag = assembled;
   a.off = assembled + (size_t)d.S * 36;
@@ -723,7 +735,7 @@ cudaError_t launch_band_solve(const BandDev& d, int C, const double* assembled, 
   a.lam = lam;
   a.ns = std::max(d.bw / C + 1, 4);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(C);
+  cfg.gridDim = dim3(C * instances);  // one cluster per damping value
   cfg.blockDim = dim3(kSolveThreads);
   cfg.dynamicSmemBytes = band_smem_bytes(d.bw, C, d.S);
   cfg.stream = s;

@@ -690,6 +690,16 @@ class FactorGraph(_Handle):
                                                    C.byref(ok)))
         return x if ok.value else None
 
+    def solve_damped_pair(self, d_assembled: int, lams):
+        """solve_damped at two damping values in one launch (two clusters run concurrently):
+        a list of two results, each x or None."""
+        S = self._plan.num_slots
+        x = np.empty(12 * S)
+        lam = np.ascontiguousarray(lams, dtype=np.float64)
+        ok = (C.c_int * 2)()
+        check(_lib.load().vgicp_graph_solve_damped_pair(self._h, C.c_void_p(d_assembled), _ptr(lam), _ptr(x), ok))
+        return [x[6 * S * i:6 * S * (i + 1)].copy() if ok[i] else None for i in range(2)]
+
     def linearize_device(self, d_poses: int, d_out: int, d_inliers: int) -> None:
         check(_lib.load().vgicp_graph_linearize_device(self._h, C.c_void_p(d_poses), C.c_void_p(d_out), C.c_void_p(d_inliers)))
 

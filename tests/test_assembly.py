@@ -243,6 +243,35 @@ def test_gpu_band_solver_matches_dense(V, seed):
 
 
 @gpu
+def test_gpu_band_solver_pair_matches_single(V):
+    """vgicp_graph_solve_damped_pair: both damping values bit-identical to two single solves, and a
+    failing instance does not affect the other (the LM's next damping value rides along)."""
+    import torch
+
+    graph, poses = graph_case(V, seed=70)
+    fixed = np.zeros(len(poses), np.uint8)
+    fixed[0] = 1
+    plan = graph.assembly_plan(fixed)
+    assert graph.solver_plan()[1]
+    S, P = plan.num_slots, len(plan.pairs)
+    d_asm = torch.empty((S + P) * 36 + S * 6, dtype=torch.float64, device="cuda")
+    graph.linearize_assembled_device(torch.from_numpy(np.ascontiguousarray(poses)).cuda().data_ptr(), d_asm.data_ptr())
+    graph.ctx.synchronize()
+    for lams in ((1e-6, 1e-5), (1e-3, 1e-2), (1.0, 1.0)):
+        pair = graph.solve_damped_pair(d_asm.data_ptr(), lams)
+        for lam, x in zip(lams, pair):
+            assert x is not None and np.array_equal(x, graph.solve_damped(d_asm.data_ptr(), lam))
+    # an indefinite system: negative damping breaks instance 0 only
+    a = d_asm.cpu().numpy().copy()
+    a[: S * 36].reshape(S, 6, 6)[S // 2] = -np.eye(6) * 1e-3
+    bad = torch.from_numpy(a).cuda()
+    x0, x1 = graph.solve_damped_pair(bad.data_ptr(), (0.0, 0.0))
+    assert x0 is None and x1 is None
+    good = graph.solve_damped_pair(d_asm.data_ptr(), (1e-4, 1e-3))
+    assert good[0] is not None and np.array_equal(good[1], graph.solve_damped(d_asm.data_ptr(), 1e-3))
+
+
+@gpu
 def test_gpu_band_solver_random_spd_and_failure(V):
     """Random SPD systems on a graph's block pattern (exact envelope handling incl. transposed
     pairs), and a non-positive-definite pivot block -> None (the reference's failed_slot)."""
@@ -325,6 +354,25 @@ def test_gpu_native_lm_matches_python_lm(V, monkeypatch, loop, solver):
     assert abs(r_nat.final_error - r_py.final_error) <= 1e-9 * max(1.0, r_py.final_error)
     assert np.abs(p_nat - p_py).max() < 1e-9
     assert r_nat.linearizations == len(r_nat.trace) + 1 - sum(1 for t in r_nat.trace if t.step_norm < 1e-8)
+
+
+@gpu
+@pytest.mark.parametrize("lambda_init", [1e-10, 1e-6])
+def test_gpu_native_lm_pair_solve_identical(V, monkeypatch, lambda_init):
+    """The device solver's pair launch (the next damping value solved alongside) changes nothing
+    the LM computes: trace, solve count and poses equal the one-value-per-launch run bit for bit."""
+    from paper_2109_07073_b200 import optimizer as LM
+
+    monkeypatch.setenv("VGICP_LM_NO_HOST_BAND", "1")
+    graph, poses = _lm_graph(V, True, seed=80)
+    st = LM.LmSettings(lambda_init=lambda_init)
+    p_pair, r_pair = LM.optimize_native(graph, poses, settings=st)
+    monkeypatch.setenv("VGICP_LM_NO_PAIR_SOLVE", "1")
+    p_one, r_one = LM.optimize_native(graph, poses, settings=st)
+    assert r_pair.band_solver and r_one.band_solver
+    assert [(t.accepted, t.lam, t.error) for t in r_pair.trace] == [(t.accepted, t.lam, t.error) for t in r_one.trace]
+    assert r_pair.solves == r_one.solves and r_pair.reason == r_one.reason
+    assert np.array_equal(p_pair, p_one)
 
 
 @gpu
