@@ -108,6 +108,8 @@ bwp, okp = g.solver_plan()
 print("band solver plan: bandwidth", bwp, "supported", okp)
 if okp:
     t("band solve (RCM block Cholesky, x to host)", lambda: g.solve_damped(d_asm.data_ptr(), lam))
+    t("band solve pair (lam, 10·lam: two clusters, one launch)",
+      lambda: g.solve_damped_pair(d_asm.data_ptr(), (lam, 10 * lam)))
     xb = g.solve_damped(d_asm.data_ptr(), lam)
     ref = sol.solve(lam)
     print("band vs dense max rel diff", float(np.abs(xb - ref).max() / np.abs(ref).max()))
