@@ -21,7 +21,8 @@
  *    Pose{rotation, translation} of include/vgicp/se3.hpp:33-56.
  *  - Point means are float32 (KITTI .bin precision, src/io.cpp:50); covariances are the six
  *    unique float32 entries (xx, xy, xz, yy, yz, zz) of a symmetric 3×3. The _f64 upload
- *    variant accepts the reference's double layout and rounds to that contract.
+ *    variant accepts the reference's double layout and keeps float64 values when they are not
+ *    float32-exact (float64 clouds).
  *  - A linearized factor is VGICP_LINEARIZED_DOUBLES doubles, the fields of LinearizedFactor
  *    (include/vgicp/factors.hpp:19-29) in order: H_ii(6×6) H_ij(6×6) H_jj(6×6) b_i(6) b_j(6)
  *    error(1), matrices row-major; inlier counts are returned separately as int32.
@@ -85,8 +86,14 @@ int vgicp_ctx_launch_count(vgicp_ctx ctx, uint64_t* launches);
 /* ---------------------------------------------------------------- point clouds (PointCloud,
  * include/vgicp/point_cloud.hpp:21-37). cov6 may be NULL for a raw cloud (overlap only). */
 int vgicp_cloud_upload(vgicp_ctx ctx, const float* xyz, const float* cov6, size_t n, vgicp_cloud* out);
-/* Reference layout: n×3 double means, n×9 double covariances (may be NULL); rounded to float32. */
+/* Reference layout: n×3 double means, n×9 double covariances (may be NULL). Float32-exact inputs
+ * with symmetric covariances take the float32 layout; any other input (e.g. submap clouds, the output
+ * of transform_cloud + voxel_downsample, pipeline.cpp:100-111) is a float64 cloud: its exact values
+ * drive every key, correspondence, overlap hit and map statistic (bit-exact against the reference's
+ * double arithmetic); only the per-hit H/b algebra reads float32 copies. */
 int vgicp_cloud_upload_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, vgicp_cloud* out);
+/* 1 when the cloud keeps float64 values (see vgicp_cloud_upload_f64), else 0. */
+int vgicp_cloud_is_f64(vgicp_cloud cloud, int* f64);
 int vgicp_cloud_size(vgicp_cloud cloud, size_t* n);
 int vgicp_cloud_has_covariances(vgicp_cloud cloud, int* has);
 int vgicp_cloud_destroy(vgicp_cloud cloud);
@@ -127,7 +134,7 @@ int vgicp_transform_cloud(vgicp_ctx ctx, const double* xyz, const double* cov9, 
  * voxel_downsample'd at downsample_resolution (skipped when <= 0), and the submap's voxel map built
  * at map_resolution from the float64 downsampled cloud. Optional outputs: out_downsampled (the
  * downsample map: export() = the submap cloud in float64, ascending key order) and out_cloud (that
- * cloud as a float32 device cloud, the source of submap-level factors). */
+ * cloud as a float64 device cloud, the source of submap-level factors and overlap probes). */
 int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* poses12, int m,
                        double downsample_resolution, double map_resolution, vgicp_map* out_downsampled,
                        vgicp_cloud* out_cloud, vgicp_map* out_map);

@@ -117,6 +117,7 @@ void release(vgicp_cloud c) {
   if (c && c->refs.fetch_sub(1) == 1) {
     DeviceGuard g(c->ctx->device);
     dfree(c->ctx, c->block);
+    dfree(c->ctx, c->block64);
     delete c;
   }
 }
@@ -319,18 +320,53 @@ int vgicp_cloud_upload(vgicp_ctx ctx, const float* xyz, const float* cov6, size_
   return cloud_upload_packed(ctx, xyz, cov6, n, out);
 }
 
+static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const double* d_cov9, size_t n, bool keep64,
+                                 vgicp_cloud* out);
+
+// Reference layout (PointCloud, point_cloud.hpp:21-37: n×3 double means, n×9 double covariances).
+// Float32-exact inputs with symmetric covariances (KITTI scans, io.cpp:50) take the float32 layout
+// unchanged; anything else (submap clouds: transform_cloud + voxel_downsample output,
+// pipeline.cpp:100-111) is kept in float64 as well, so keys / correspondences / overlap hits and map
+// statistics built from it are those of the reference's double arithmetic.
 int vgicp_cloud_upload_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, vgicp_cloud* out) {
+  if (!ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
   if (n > 0 && !xyz) return fail(VGICP_E_INVALID_ARGUMENT, "null point array");
-  std::vector<float> p(3 * n), c(cov9 ? 6 * n : 0);
-  for (size_t i = 0; i < 3 * n; ++i) p[i] = static_cast<float>(xyz[i]);
-  if (cov9) {
-    for (size_t i = 0; i < n; ++i) {
-      const double* m = cov9 + 9 * i;
-      const int idx[6] = {0, 1, 2, 4, 5, 8};
-      for (int k = 0; k < 6; ++k) c[6 * i + k] = static_cast<float>(m[idx[k]]);
-    }
+  if (n >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "cloud too large (>= 2^31 points)");
+  auto f32_exact = [](double v) { return static_cast<double>(static_cast<float>(v)) == v; };
+  bool exact = true;
+  for (size_t i = 0; i < 3 * n && exact; ++i) exact = f32_exact(xyz[i]);
+  for (size_t i = 0; cov9 && i < n && exact; ++i) {
+    const double* m = cov9 + 9 * i;
+    for (int k = 0; k < 9 && exact; ++k) exact = f32_exact(m[k]);
+    exact = exact && m[1] == m[3] && m[2] == m[6] && m[5] == m[7];
   }
-  return cloud_upload_packed(ctx, p.data(), cov9 ? c.data() : nullptr, n, out);
+  if (exact || n == 0) {
+    std::vector<float> p(3 * n), c(cov9 ? 6 * n : 0);
+    for (size_t i = 0; i < 3 * n; ++i) p[i] = static_cast<float>(xyz[i]);
+    if (cov9) {
+      for (size_t i = 0; i < n; ++i) {
+        const double* m = cov9 + 9 * i;
+        const int idx[6] = {0, 1, 2, 4, 5, 8};
+        for (int k = 0; k < 6; ++k) c[6 * i + k] = static_cast<float>(m[idx[k]]);
+      }
+    }
+    return cloud_upload_packed(ctx, p.data(), cov9 ? c.data() : nullptr, n, out);
+  }
+  DeviceGuard g(ctx->device);
+  DevBuf buf(ctx);
+  VG_CUDA(buf.alloc(n * (cov9 ? 12 : 3) * sizeof(double)));
+  double* d_xyz = static_cast<double*>(buf.p);
+  double* d_cov = cov9 ? d_xyz + 3 * n : nullptr;
+  VG_CUDA(cudaMemcpyAsync(d_xyz, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  if (cov9) VG_CUDA(cudaMemcpyAsync(d_cov, cov9, n * 9 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  return cloud_from_device_f64(ctx, d_xyz, d_cov, n, true, out);  // synchronises before returning
+}
+
+int vgicp_cloud_is_f64(vgicp_cloud cloud, int* f64) {
+  if (!cloud || !f64) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *f64 = cloud->f64 ? 1 : 0;
+  return VGICP_OK;
 }
 
 int vgicp_cloud_size(vgicp_cloud cloud, size_t* n) {
@@ -417,8 +453,12 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
   std::vector<BuildSeg> segs(m);
   for (int k = 0; k < m; ++k) {
     const vgicp_cloud c = clouds[k];
-    segs[k] = BuildSeg{c->pa, c->pb, c->pc, nullptr, nullptr, 0ull, static_cast<unsigned>(c->n), 0u, resolutions[k],
-                       1.0 / resolutions[k]};
+    // float64 clouds accumulate their exact float64 means / covariances (all 9 entries, as
+    // VoxelAccumulator does); float32-exact clouds their float32 layout (identical values)
+    segs[k] = c->f64 ? BuildSeg{nullptr, nullptr, nullptr, c->m64, c->c64, 0ull, static_cast<unsigned>(c->n), 0u,
+                                resolutions[k], 1.0 / resolutions[k]}
+                     : BuildSeg{c->pa, c->pb, c->pc, nullptr, nullptr, 0ull, static_cast<unsigned>(c->n), 0u,
+                                resolutions[k], 1.0 / resolutions[k]};
   }
   return build_segments(ctx, segs, out);
 }
@@ -688,15 +728,18 @@ int vgicp_transform_cloud(vgicp_ctx ctx, const double* xyz, const double* cov9, 
   return VGICP_OK;
 }
 
-// float32 device cloud (same layout as cloud_upload_packed) from float64 device arrays.
-static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const double* d_cov9, size_t n, vgicp_cloud* out) {
+// Device cloud (same layout as cloud_upload_packed) from float64 device arrays (d_cov9 may be null:
+// a raw cloud). keep64: the cloud also keeps the float64 values (exact input-order copies for builds /
+// transforms + Morton-ordered float64 means for the probe kernels), i.e. it is a float64 cloud.
+static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const double* d_cov9, size_t n, bool keep64,
+                                 vgicp_cloud* out) {
   *out = nullptr;
   if (n >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "cloud too large (>= 2^31 points)");
   cudaStream_t s = ctx->stream;
   auto c = std::make_unique<vgicp_cloud_s>();
   c->ctx = ctx;
   c->n = n;
-  c->has_cov = n > 0;
+  c->has_cov = n > 0 && d_cov9 != nullptr;
   const size_t na = align_up(n * sizeof(float4), 256);
   const size_t nc = align_up(n * sizeof(float), 256);
   const size_t half = na * 2 + nc;
@@ -707,6 +750,18 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
   c->pb = reinterpret_cast<float4*>(base + na);
   c->pc = reinterpret_cast<float*>(base + 2 * na);
   c->sblk = reinterpret_cast<PointBlock*>(base + half);
+  if (keep64 && n > 0) {
+    const size_t bm = align_up(n * 3 * sizeof(double), 256);
+    const size_t bc = c->has_cov ? align_up(n * 9 * sizeof(double), 256) : 0;
+    VG_CUDA(dmalloc(ctx, &c->block64, bm + bc + nblk * sizeof(PointBlock64)));
+    char* b64 = static_cast<char*>(c->block64);
+    c->f64 = true;
+    c->m64 = reinterpret_cast<double*>(b64);
+    c->c64 = c->has_cov ? reinterpret_cast<double*>(b64 + bm) : nullptr;
+    c->blk64 = reinterpret_cast<PointBlock64*>(b64 + bm + bc);
+    VG_CUDA(cudaMemcpyAsync(c->m64, d_xyz, n * 3 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (c->has_cov) VG_CUDA(cudaMemcpyAsync(c->c64, d_cov9, n * 9 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
   if (n > 0) {
     size_t sort_bytes = 0;
     VG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
@@ -727,7 +782,7 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
     VG_CUDA(launch_cloud_bbox(d_xyz, n, box, s));
     VG_CUDA(launch_cloud_morton(d_xyz, n, box, codes, idx, s));
     VG_CUDA(cub::DeviceRadixSort::SortPairs(temp, sort_bytes, codes, codes2, idx, perm, static_cast<int>(n), 0, 30, s));
-    VG_CUDA(launch_cloud_fill(d_xyz, d_cov9, n, perm, c->pa, c->pb, c->pc, c->sblk, s));
+    VG_CUDA(launch_cloud_fill(d_xyz, d_cov9, n, perm, c->pa, c->pb, c->pc, c->sblk, c->blk64, s));
     ctx->launches += 4;
     unsigned hbox[6];
     VG_CUDA(cudaMemcpyAsync(hbox, box, sizeof(hbox), cudaMemcpyDeviceToHost, s));
@@ -784,6 +839,8 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
     it.pa = frames[k]->pa;
     it.pb = frames[k]->pb;
     it.pc = frames[k]->pc;
+    it.xyz64 = frames[k]->m64;  // float64 frames transform their exact values
+    it.cov9 = frames[k]->c64;
     it.offset = off;
     it.n = static_cast<unsigned>(frames[k]->n);
     it.pad = 0;
@@ -821,7 +878,7 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
   // 4. the submap cloud as a float32 device cloud (source of submap-level factors), built on the
   //    device from the float64 arrays (no host round trip)
   if (out_cloud) {
-    if (int rc = cloud_from_device_f64(ctx, src_xyz, src_cov, src_n, out_cloud)) {
+    if (int rc = cloud_from_device_f64(ctx, src_xyz, src_cov, src_n, true, out_cloud)) {
       release(ds);
       release(mp);
       return rc;
@@ -922,6 +979,7 @@ static bool overlap_disjoint(const vgicp_cloud_s* c, const double* T, const vgic
 // Overlap probe item k (cloud k's points through pose k against map k), written in place.
 static void fill_overlap_item(OverlapItem& it, const vgicp_cloud_s* c, const double* T, const vgicp_map_s* mp) {
   it.blk = c->sblk;  // Morton order (hit counts are order-independent)
+  it.blk64 = c->blk64;
   it.map = mp->dev();
   it.occ = mp->occ;
   std::memcpy(it.T, T, sizeof(double) * 12);
@@ -936,7 +994,7 @@ static void fill_overlap_item(OverlapItem& it, const vgicp_cloud_s* c, const dou
   for (int q = 0; q < 9; ++q) sc.R[q] = static_cast<float>(T[q]);
   for (int q = 0; q < 3; ++q) sc.t[q] = static_cast<float>(T[9 + q]), tmax = std::max(tmax, std::fabs(sc.t[q]));
   sc.inv_r = static_cast<float>(mp->inv_res);
-  sc.A2 = 5e-7f * sc.inv_r;
+  sc.A2 = (c->f64 ? kScreenA64 : kScreenA) * sc.inv_r;
   sc.C = sc.A2 * tmax + 1e-7f;
   sc.cx0 = static_cast<int>(it.occ.kx0) - (1 << 20);
   sc.cy0 = static_cast<int>(it.occ.ky0) - (1 << 20);
@@ -1108,8 +1166,8 @@ int vgicp_overlap_mapset(vgicp_ctx ctx, vgicp_cloud cloud, const double* rel12, 
   VG_CUDA(cudaMemcpyAsync(set->d_poses, hp, bp + 6 * sizeof(float), cudaMemcpyHostToDevice, s));
   VG_CUDA(cudaMemsetAsync(set->d_hits, 0, sizeof(unsigned long long) * m, s));
   const float* d_box = reinterpret_cast<const float*>(reinterpret_cast<const char*>(set->d_poses) + bp);
-  VG_CUDA(launch_mapset_prepare(set->d_templates, m, set->d_poses, cloud->sblk, static_cast<unsigned>(cloud->n), d_box,
-                                set->d_items, set->d_chunks, s));
+  VG_CUDA(launch_mapset_prepare(set->d_templates, m, set->d_poses, cloud->sblk, cloud->blk64,
+                                static_cast<unsigned>(cloud->n), d_box, set->d_items, set->d_chunks, s));
   const int nch = (m + kOverlapMapsPerChunk - 1) / kOverlapMapsPerChunk;
   VG_CUDA(launch_overlap_occ(set->d_items, set->d_chunks, nch, static_cast<unsigned>(cloud->n), set->d_hits, s));
   ctx->launches += 2;
@@ -1128,6 +1186,11 @@ int vgicp_overlap_rate(vgicp_ctx ctx, vgicp_cloud cloud, const double pose_rel[1
 }
 
 // ------------------------------------------------------------------------------------ graphs
+// kernels one factor pass launches: one for the float32-cloud items, one for the float64-cloud items
+static int factor_launches(const vgicp_graph_s* g) {
+  return (g->f64_begin > 0 ? 1 : 0) + (g->num_items > g->f64_begin ? 1 : 0);
+}
+
 int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses, int chunk,
                        vgicp_graph* out) {
   if (!ctx || !out || (num_factors > 0 && !factors)) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
@@ -1174,26 +1237,35 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   // VGICP_NO_RANK=1 keeps the cuckoo-hash probes (measurement switch)
   bool rank = std::getenv("VGICP_NO_RANK") == nullptr;
   for (int f = 0; f < num_factors && rank; ++f) rank = factors[f].target->occ.occ != nullptr;
-  for (int f = 0; f < num_factors; ++f) {
-    const vgicp_factor_desc& d = factors[f];
-    FactorDev& x = fd[f];
-    const int fchunk = !split ? chunk : (num_factors < slots ? few_chunk : (f >= num_factors - slots ? small_chunk : chunk));
-    x.blk = d.source->sblk;  // Morton order: neighbouring lanes probe neighbouring voxels
-    x.map = rank ? d.target->dev_rank() : d.target->dev();
-    x.n = static_cast<int>(d.source->n);
-    x.tgt = d.target_index;
-    x.src = d.source_index;
-    x.item_begin = static_cast<int>(items.size());
-    for (int b = 0; b < x.n; b += fchunk) items.push_back(WorkItem{f, b, std::min(x.n, b + fchunk), 0});
-    x.item_count = static_cast<int>(items.size()) - x.item_begin;
-    x.pad = 0;
-    points += d.source->n;
+  // items of float32-exact source clouds first, then those of float64 clouds (their own launch)
+  int f64_begin = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) f64_begin = static_cast<int>(items.size());
+    for (int f = 0; f < num_factors; ++f) {
+      const vgicp_factor_desc& d = factors[f];
+      if (d.source->f64 != (pass == 1)) continue;
+      FactorDev& x = fd[f];
+      const int fchunk =
+          !split ? chunk : (num_factors < slots ? few_chunk : (f >= num_factors - slots ? small_chunk : chunk));
+      x.blk = d.source->sblk;  // Morton order: neighbouring lanes probe neighbouring voxels
+      x.blk64 = d.source->blk64;
+      x.map = rank ? d.target->dev_rank() : d.target->dev();
+      x.n = static_cast<int>(d.source->n);
+      x.tgt = d.target_index;
+      x.src = d.source_index;
+      x.item_begin = static_cast<int>(items.size());
+      for (int b = 0; b < x.n; b += fchunk) items.push_back(WorkItem{f, b, std::min(x.n, b + fchunk), 0});
+      x.item_count = static_cast<int>(items.size()) - x.item_begin;
+      x.pad = 0;
+      points += d.source->n;
+    }
   }
   auto gr = std::make_unique<vgicp_graph_s>();
   gr->ctx = ctx;
   gr->num_factors = num_factors;
   gr->num_poses = num_poses;
   gr->num_items = static_cast<int>(items.size());
+  gr->f64_begin = f64_begin;
   gr->num_points = points;
   gr->rank_lookup = rank;
   const size_t nf = std::max(num_factors, 1), ni = std::max<size_t>(items.size(), 1);
@@ -1283,9 +1355,9 @@ int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, dou
   if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_out || !d_inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   DeviceGuard g(graph->ctx->device);
-  VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
+  VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, d_poses12, graph->d_partials,
                         graph->d_part_inl, graph->d_counters, d_out, d_inliers, graph->ctx->stream));
-  graph->ctx->launches += graph->num_items > 0 ? 1 : 0;
+  graph->ctx->launches += factor_launches(graph);
   return VGICP_OK;
 }
 
@@ -1293,9 +1365,9 @@ int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, doub
   if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_errors || !d_inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   DeviceGuard g(graph->ctx->device);
-  VG_CUDA(launch_factor(false, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
+  VG_CUDA(launch_factor(false, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, d_poses12, graph->d_partials,
                         graph->d_part_inl, graph->d_counters, d_errors, d_inliers, graph->ctx->stream));
-  graph->ctx->launches += graph->num_items > 0 ? 1 : 0;
+  graph->ctx->launches += factor_launches(graph);
   return VGICP_OK;
 }
 
@@ -1343,9 +1415,9 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
   VG_CUDA(cudaMemcpyAsync(graph->d_poses, poses_pinned ? poses12 : h_poses, pose_bytes, cudaMemcpyHostToDevice, s));
   double* d_res = zero_copy ? m_res : (linearize ? graph->d_out : graph->d_err);
   int32_t* d_inl = zero_copy ? m_inl : graph->d_out_inl;
-  VG_CUDA(launch_factor(linearize, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->d_poses,
+  VG_CUDA(launch_factor(linearize, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, graph->d_poses,
                         graph->d_partials, graph->d_part_inl, graph->d_counters, d_res, d_inl, s));
-  ctx->launches += 1;
+  ctx->launches += factor_launches(graph);
   if (!zero_copy) {
     VG_CUDA(cudaMemcpyAsync(h_res, d_res, res_bytes, cudaMemcpyDeviceToHost, s));
     VG_CUDA(cudaMemcpyAsync(h_inl, d_inl, inl_bytes, cudaMemcpyDeviceToHost, s));
@@ -1460,9 +1532,9 @@ int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, do
   std::memcpy(h, poses12, pose_bytes);
   VG_CUDA(cudaMemcpyAsync(graph->d_poses, h, pose_bytes, cudaMemcpyHostToDevice, s));
   if (graph->num_items > 0) {
-    VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->d_poses, graph->d_partials,
+    VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, graph->d_poses, graph->d_partials,
                           graph->d_part_inl, graph->d_counters, graph->d_out, graph->d_out_inl, s));
-    ctx->launches += 1;
+    ctx->launches += factor_launches(graph);
   } else if (graph->num_factors > 0) {
     VG_CUDA(cudaMemsetAsync(graph->d_out, 0, sizeof(double) * VGICP_LINEARIZED_DOUBLES * graph->num_factors, s));
   }
@@ -1484,9 +1556,9 @@ int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_po
   DeviceGuard g(graph->ctx->device);
   cudaStream_t s = graph->ctx->stream;
   if (graph->num_items > 0) {
-    VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, d_poses12, graph->d_partials,
+    VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, d_poses12, graph->d_partials,
                           graph->d_part_inl, graph->d_counters, graph->d_out, graph->d_out_inl, s));
-    graph->ctx->launches += 1;
+    graph->ctx->launches += factor_launches(graph);
   } else if (graph->num_factors > 0) {
     VG_CUDA(cudaMemsetAsync(graph->d_out, 0, sizeof(double) * VGICP_LINEARIZED_DOUBLES * graph->num_factors, s));
   }

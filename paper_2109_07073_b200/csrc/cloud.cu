@@ -2,6 +2,8 @@
 // vgicp_submap_build from float64 device arrays): input-order SoA for the builds and the
 // Morton-ordered 64-point blocks for the probe kernels (Z-order code of 10 bits per axis over the
 // finite bounding box, stable radix sort: ties in input order).
+#include <type_traits>
+
 #include "internal.h"
 
 namespace vgicp {
@@ -71,13 +73,22 @@ __global__ void morton_kernel(const T* __restrict__ xyz, size_t n, const unsigne
 // 6 unique covariance entries (uploads; nullptr = raw cloud, zero covariances).
 struct SrcF64 {
   const double* xyz;
-  const double* cov9;
+  const double* cov9;  // nullptr: raw cloud
   __device__ void get(size_t j, float4& a, float4& b, float& z) const {
     const double* p = xyz + 3 * j;
-    const double* q = cov9 + 9 * j;
-    a = make_float4((float)p[0], (float)p[1], (float)p[2], (float)q[0]);
-    b = make_float4((float)q[1], (float)q[2], (float)q[4], (float)q[5]);
-    z = (float)q[8];
+    if (cov9) {
+      const double* q = cov9 + 9 * j;
+      a = make_float4((float)p[0], (float)p[1], (float)p[2], (float)q[0]);
+      b = make_float4((float)q[1], (float)q[2], (float)q[4], (float)q[5]);
+      z = (float)q[8];
+    } else {
+      a = make_float4((float)p[0], (float)p[1], (float)p[2], 0.f);
+      b = make_float4(0.f, 0.f, 0.f, 0.f);
+      z = 0.f;
+    }
+  }
+  __device__ void get64(size_t j, double& x, double& y, double& w) const {
+    x = xyz[3 * j], y = xyz[3 * j + 1], w = xyz[3 * j + 2];
   }
 };
 struct SrcF32 {
@@ -90,7 +101,7 @@ struct SrcF32 {
       a = make_float4(p[0], p[1], p[2], q[0]);
       b = make_float4(q[1], q[2], q[3], q[4]);
       z = q[5];
-    } else {
+    } else {  // raw cloud
       a = make_float4(p[0], p[1], p[2], 0.f);
       b = make_float4(0.f, 0.f, 0.f, 0.f);
       z = 0.f;
@@ -101,7 +112,7 @@ struct SrcF32 {
 template <typename Src>
 __global__ void fill_cloud_kernel(Src src, size_t n, const unsigned* __restrict__ perm, float4* __restrict__ pa,
                                   float4* __restrict__ pb, float* __restrict__ pc, PointBlock* __restrict__ blk,
-                                  size_t padded) {
+                                  PointBlock64* __restrict__ blk64, size_t padded) {
   for (size_t d = blockIdx.x * (size_t)blockDim.x + threadIdx.x; d < padded; d += (size_t)gridDim.x * blockDim.x) {
     const size_t dn = d < n ? d : n - 1;
 #pragma unroll
@@ -117,6 +128,12 @@ __global__ void fill_cloud_kernel(Src src, size_t n, const unsigned* __restrict_
         B.pa[d % kPointBlock] = a;
         B.pb[d % kPointBlock] = b;
         B.pc[d % kPointBlock] = z;
+        if constexpr (std::is_same<Src, SrcF64>::value) {
+          if (blk64) {  // the exact float64 means, same Morton position
+            PointBlock64& B64 = blk64[d / kPointBlock];
+            src.get64(j, B64.x[d % kPointBlock], B64.y[d % kPointBlock], B64.z[d % kPointBlock]);
+          }
+        }
       }
     }
   }
@@ -150,15 +167,15 @@ cudaError_t launch_cloud_morton(const float* xyz, size_t n, const unsigned* box,
 }
 
 cudaError_t launch_cloud_fill(const double* xyz, const double* cov9, size_t n, const unsigned* perm, float4* pa,
-                              float4* pb, float* pc, PointBlock* blk, cudaStream_t s) {
+                              float4* pb, float* pc, PointBlock* blk, PointBlock64* blk64, cudaStream_t s) {
   const size_t padded = (n + kPointBlock - 1) / kPointBlock * kPointBlock;
-  fill_cloud_kernel<<<grid_cloud(padded), 256, 0, s>>>(SrcF64{xyz, cov9}, n, perm, pa, pb, pc, blk, padded);
+  fill_cloud_kernel<<<grid_cloud(padded), 256, 0, s>>>(SrcF64{xyz, cov9}, n, perm, pa, pb, pc, blk, blk64, padded);
   return cudaGetLastError();
 }
 cudaError_t launch_cloud_fill(const float* xyz, const float* cov6, size_t n, const unsigned* perm, float4* pa,
                               float4* pb, float* pc, PointBlock* blk, cudaStream_t s) {
   const size_t padded = (n + kPointBlock - 1) / kPointBlock * kPointBlock;
-  fill_cloud_kernel<<<grid_cloud(padded), 256, 0, s>>>(SrcF32{xyz, cov6}, n, perm, pa, pb, pc, blk, padded);
+  fill_cloud_kernel<<<grid_cloud(padded), 256, 0, s>>>(SrcF32{xyz, cov6}, n, perm, pa, pb, pc, blk, nullptr, padded);
   return cudaGetLastError();
 }
 

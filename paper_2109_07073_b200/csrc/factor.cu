@@ -12,6 +12,8 @@
 // arrival counter) sums the factor's partials in item order and expands, in fp64,
 //   H_ts = -H_tt·Ad,  H_ss = AdᵀH_tt·Ad,  b_s = -Adᵀb_t,  Ad = Ad(T_ts) (se3.cpp:107-113),
 // which is exact algebra because B = -A·Ad(T_ts). Fixed orders everywhere => deterministic.
+#include <atomic>
+
 #include "exact_math.cuh"
 #include "internal.h"
 
@@ -353,11 +355,14 @@ static_assert(sizeof(WarpTile) * kStages >= sizeof(double) * 180, "epilogue scra
 // kRank: the target maps carry occupancy bitmaps with brick ranks and rank-ordered statistics
 // (MapDev::sa / sb indexed by rank): a probe is ONE 16-B load of the brick record, spatially
 // coherent across the Morton-ordered lanes, instead of two hash-bucket loads (one of them random).
-template <bool kLinearize, bool kRank>
+// kF64: the launch's items belong to float64 source clouds (their float64 means are transformed
+// instead of the float32 tile copies); such items follow the float32 ones and run in their own
+// launch, so the float32 kernel keeps its register budget. item_base: first item of this launch.
+template <bool kLinearize, bool kRank, bool kF64>
 __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
-    const FactorDev* __restrict__ factors, const WorkItem* __restrict__ items, const double* __restrict__ poses,
-    double* __restrict__ partials, int* __restrict__ part_inl, unsigned* __restrict__ counters,
-    double* __restrict__ out, int* __restrict__ out_inl) {
+    const FactorDev* __restrict__ factors, const WorkItem* __restrict__ items, int item_base,
+    const double* __restrict__ poses, double* __restrict__ partials, int* __restrict__ part_inl,
+    unsigned* __restrict__ counters, double* __restrict__ out, int* __restrict__ out_inl) {
   constexpr int kAcc = kLinearize ? kLinAcc : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   FactorSmem& sm = *reinterpret_cast<FactorSmem*>(smem_raw);
@@ -365,9 +370,12 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const WorkItem w = items[blockIdx.x];
+  const WorkItem w = items[blockIdx.x];  // `items` starts at this launch's first item
   const FactorDev* __restrict__ fp = factors + w.factor;
   const PointBlock* __restrict__ gblk = fp->blk + w.begin / kPointBlock;
+  // float64 means of the same blocks when the cloud is not float32-exact (submap clouds): the
+  // transform reads them instead of the tile's float32 copies (warp-uniform branch)
+  const PointBlock64* __restrict__ gblk64 = kF64 ? fp->blk64 + w.begin / kPointBlock : nullptr;
   // Warp `warp` processes the item's 64-point tiles warp, warp + kWarps, ... (balanced, no CTA
   // barrier in the loop); lane 0 streams them into the warp's ring with TMA bulk copies.
   const int ntiles_all = (w.end - w.begin + kWarpTile - 1) / kWarpTile;
@@ -438,8 +446,13 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
       const float4 A = tb.pa[lp];
       cxx[u] = A.w;  // error-only pass: kept in a register (the strided .w re-read at append time is
                      // a 4-way bank conflict); the linearize pass re-reads it (no registers to spare)
+      double px = A.x, py = A.y, pz = A.z;
+      if constexpr (kF64) {
+        const PointBlock64* __restrict__ b64 = gblk64 + warp + k * kWarps;
+        px = __ldg(&b64->x[lp]), py = __ldg(&b64->y[lp]), pz = __ldg(&b64->z[lp]);
+      }
       double qd0, qd1, qd2;
-      apply_pose_rn(Tr, A.x, A.y, A.z, qd0, qd1, qd2);
+      apply_pose_rn(Tr, px, py, pz, qd0, qd1, qd2);
       unsigned k0 = 0, k1 = 0, k2 = 0;
       double ld0, ld1, ld2;
       ok[u] = voxel_key(qd0, qd1, qd2, map.res, map.inv_res, k0, k1, k2, ld0, ld1, ld2) && (p < tile_n);
@@ -561,7 +574,7 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
   if (head + lane < tail) consume((head + lane) % static_cast<unsigned>(kQueue));  // the last partial batch
   __syncwarp();  // this warp is done with its ring (no CTA-wide barrier after the prologue)
 
-  finish_factor<kLinearize>(acc, inl, lane, (size_t)blockIdx.x * kWarps + warp, kWarps, w, fp, sm.T,
+  finish_factor<kLinearize>(acc, inl, lane, (size_t)(item_base + blockIdx.x) * kWarps + warp, kWarps, w, fp, sm.T,
                             reinterpret_cast<double*>(&sm.u.ring[warp][0]), partials, part_inl, counters, out, out_inl);
 }
 
@@ -632,26 +645,47 @@ cudaError_t launch_assemble(const int* out_ptr, const int* contrib, int num_slot
 }
 
 cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, const WorkItem* items, int num_items,
-                          const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
-                          int* out_inl, cudaStream_t s) {
+                          int f64_begin, const double* poses, double* partials, int* part_inl, unsigned* counters,
+                          double* out, int* out_inl, cudaStream_t s) {
   if (num_items <= 0) return cudaSuccess;
   constexpr size_t kSmem = sizeof(FactorSmem);
-  static bool configured = false;
-  if (!configured) {
-    for (const void* k : {reinterpret_cast<const void*>(factor_kernel<true, false>),
-                          reinterpret_cast<const void*>(factor_kernel<false, false>),
-                          reinterpret_cast<const void*>(factor_kernel<true, true>),
-                          reinterpret_cast<const void*>(factor_kernel<false, true>)}) {
+  // the > 48 KB shared-memory opt-in is a per-device function attribute: set it once per device
+  // (a context on another GPU of the same process needs its own), thread-safely
+  static std::atomic<unsigned long long> configured{0ull};
+  int dev = 0;
+  if (const cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    for (const void* k : {reinterpret_cast<const void*>(factor_kernel<true, false, false>),
+                          reinterpret_cast<const void*>(factor_kernel<false, false, false>),
+                          reinterpret_cast<const void*>(factor_kernel<true, true, false>),
+                          reinterpret_cast<const void*>(factor_kernel<false, true, false>),
+                          reinterpret_cast<const void*>(factor_kernel<true, false, true>),
+                          reinterpret_cast<const void*>(factor_kernel<false, false, true>),
+                          reinterpret_cast<const void*>(factor_kernel<true, true, true>),
+                          reinterpret_cast<const void*>(factor_kernel<false, true, true>)}) {
       const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
       if (e != cudaSuccess) return e;
     }
-    configured = true;
+    configured.fetch_or(bit, std::memory_order_acq_rel);
   }
-  auto go = [&](auto kernel) {
-    kernel<<<num_items, kFactorThreads, kSmem, s>>>(factors, items, poses, partials, part_inl, counters, out, out_inl);
+  f64_begin = f64_begin < 0 ? num_items : (f64_begin > num_items ? num_items : f64_begin);
+  auto go = [&](auto kernel, int base, int count) {
+    if (count > 0)
+      kernel<<<count, kFactorThreads, kSmem, s>>>(factors, items + base, base, poses, partials, part_inl, counters,
+                                                  out, out_inl);
   };
-  if (linearize) rank ? go(factor_kernel<true, true>) : go(factor_kernel<true, false>);
-  else rank ? go(factor_kernel<false, true>) : go(factor_kernel<false, false>);
+  auto both = [&](auto k32, auto k64) {
+    go(k32, 0, f64_begin);
+    go(k64, f64_begin, num_items - f64_begin);
+  };
+  if (linearize) {
+    if (rank) both(factor_kernel<true, true, false>, factor_kernel<true, true, true>);
+    else both(factor_kernel<true, false, false>, factor_kernel<true, false, true>);
+  } else {
+    if (rank) both(factor_kernel<false, true, false>, factor_kernel<false, true, true>);
+    else both(factor_kernel<false, false, false>, factor_kernel<false, false, true>);
+  }
   return cudaGetLastError();
 }
 

@@ -41,9 +41,19 @@ struct PointBlock {
   float pc[kPointBlock];   // c_zz
 };
 static_assert(sizeof(PointBlock) % 128 == 0, "blocks must stay 128-B aligned");
+// Clouds whose means are not float32-exact (submap clouds: transform_cloud + voxel_downsample output,
+// pipeline.cpp:100-111; any float64 upload) also keep their float64 means in the same Morton blocks,
+// SoA per block: x[64] | y[64] | z[64] (1,536 B). The probe kernels transform THESE values, so keys,
+// correspondences and overlap hits stay bit-exact against the reference's double arithmetic.
+struct PointBlock64 {
+  double x[kPointBlock];
+  double y[kPointBlock];
+  double z[kPointBlock];
+};
 
 struct FactorDev {
   const PointBlock* blk;
+  const PointBlock64* blk64;  // float64 means of the same blocks, or nullptr (float32-exact cloud)
   MapDev map;
   int n;
   int tgt;
@@ -69,6 +79,7 @@ struct alignas(16) OccScreen {
 static_assert(sizeof(OccScreen) == 112, "OccScreen is staged as 7 uint4");
 struct OverlapItem {
   const PointBlock* blk;
+  const PointBlock64* blk64;  // float64 means (nullptr: the float32 means are exact)
   MapDev map;
   OccDev occ;  // occupancy bitmap (occ.occ == nullptr: hash probes)
   double T[12];
@@ -82,8 +93,12 @@ cudaError_t launch_overlap_occ(const OverlapItem* items, const int2* chunks, int
 // Device-side item preparation for a map set swept by one cloud: item k = templates[k] + pose k
 // (fp64 T, fp32 screen, exact culling against the cloud box -> n = 0 when culled); chunks of 32.
 cudaError_t launch_mapset_prepare(const OverlapItem* templates, int m, const double* poses12, const PointBlock* blk,
-                                  unsigned n, const float* cloud_box, OverlapItem* items, int2* chunks,
-                                  cudaStream_t s);
+                                  const PointBlock64* blk64, unsigned n, const float* cloud_box, OverlapItem* items,
+                                  int2* chunks, cudaStream_t s);
+// Screen margin coefficient of the occupancy overlap kernel: |fl32 y - q/r| <= ~4.2e-7·|p|₁/r for
+// float32 means, + 6e-8·|p|₁/r when the float32 means are roundings of float64 ones.
+constexpr float kScreenA = 5e-7f;
+constexpr float kScreenA64 = 6e-7f;
 // Occupancy bitmap build job for one map (cold keys -> bits -> brick ranks -> rank-ordered stats).
 struct OccJob {
   const unsigned long long* keys;
@@ -166,9 +181,11 @@ cudaError_t launch_build_insert(const InsertJob* jobs, int m, unsigned max_v, in
 cudaError_t launch_build_place(const InsertJob* jobs, int m, unsigned max_v, const VoxelStats* hot, cudaStream_t s);
 cudaError_t launch_lookup(MapDev map, const double* pts, size_t n, unsigned long long* keys_out, cudaStream_t s);
 cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsigned long long* hits, cudaStream_t s);
+// items [0, f64_begin) belong to float32-exact source clouds, [f64_begin, num_items) to float64 clouds
+// (one launch each; the float64 launch transforms the exact float64 means)
 cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, const WorkItem* items, int num_items,
-                          const double* poses, double* partials, int* part_inl, unsigned* counters, double* out,
-                          int* out_inl, cudaStream_t s);
+                          int f64_begin, const double* poses, double* partials, int* part_inl, unsigned* counters,
+                          double* out, int* out_inl, cudaStream_t s);
 cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s);
 // overlap probes grouped by cloud: chunk = (first item, count <= kOverlapMapsPerChunk) of items that
 // share one cloud; each thread loads its points once and probes the chunk's maps
@@ -211,6 +228,8 @@ struct TransformItem {
   const float4* pa;
   const float4* pb;
   const float* pc;
+  const double* xyz64;  // float64 means (n×3) + covariances (n×9) of a float64 cloud, else nullptr
+  const double* cov9;
   unsigned long long offset;
   unsigned n;
   unsigned pad;
@@ -223,7 +242,7 @@ cudaError_t launch_cloud_bbox(const double* xyz, size_t n, unsigned* box, cudaSt
 cudaError_t launch_cloud_morton(const double* xyz, size_t n, const unsigned* box, unsigned* codes, unsigned* idx,
                                 cudaStream_t s);
 cudaError_t launch_cloud_fill(const double* xyz, const double* cov9, size_t n, const unsigned* perm, float4* pa,
-                              float4* pb, float* pc, PointBlock* blk, cudaStream_t s);
+                              float4* pb, float* pc, PointBlock* blk, PointBlock64* blk64, cudaStream_t s);
 cudaError_t launch_cloud_bbox(const float* xyz, size_t n, unsigned* box, cudaStream_t s);
 cudaError_t launch_cloud_morton(const float* xyz, size_t n, const unsigned* box, unsigned* codes, unsigned* idx,
                                 cudaStream_t s);
@@ -266,6 +285,13 @@ struct vgicp_cloud_s {
   vgicp::PointBlock* sblk = nullptr;  // Morton (Z-order) copy in 64-point blocks: streamed by the factor /
                                // overlap kernels so that consecutive points probe neighbouring voxels
   float lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};  // bounding box of the finite points (lo > hi: none)
+  // float64 clouds (means not float32-exact): exact input-order arrays for builds / transforms and
+  // the Morton-ordered float64 means for the probe kernels; all nullptr for float32-exact clouds
+  bool f64 = false;
+  void* block64 = nullptr;  // m64 | c64 | blk64
+  double* m64 = nullptr;    // n×3 input order
+  double* c64 = nullptr;    // n×9 input order (nullptr for a raw cloud)
+  vgicp::PointBlock64* blk64 = nullptr;
   std::atomic<int> refs{1};
 };
 
@@ -314,6 +340,7 @@ struct vgicp_graph_s {
   int num_factors = 0;
   int num_poses = 0;
   int num_items = 0;
+  int f64_begin = 0;  // first work item of a float64 source cloud (items of float32 clouds come first)
   uint64_t num_points = 0;
   void* block = nullptr;  // factors | items | partials | part_inl | counters | poses | out | out_inl | err
   vgicp::FactorDev* d_factors = nullptr;

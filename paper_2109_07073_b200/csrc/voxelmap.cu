@@ -298,6 +298,19 @@ __global__ void lookup_kernel(MapDev map, const double* __restrict__ pts, size_t
   }
 }
 
+// Point i of a cloud's Morton-ordered blocks as float64: the exact float64 means of a float64 cloud,
+// else the float32 means (exact by the cloud's contract).
+__device__ __forceinline__ void load_point64(const PointBlock* __restrict__ blk, const PointBlock64* __restrict__ blk64,
+                                             unsigned i, double& x, double& y, double& z) {
+  if (blk64) {
+    const PointBlock64& b = blk64[i / kPointBlock];
+    x = __ldg(&b.x[i % kPointBlock]), y = __ldg(&b.y[i % kPointBlock]), z = __ldg(&b.z[i % kPointBlock]);
+  } else {
+    const float4 a = __ldg(&blk[i / kPointBlock].pa[i % kPointBlock]);
+    x = a.x, y = a.y, z = a.z;
+  }
+}
+
 // overlap_rate (voxelmap.cpp:119-135), batched: blockIdx.y walks (cloud, pose, map) items,
 // hits are integer-exact (warp-aggregated 64-bit atomics), so the result is exactly hits / N.
 // Each thread keeps kOverlapILP points' bucket pairs in flight (keys first, then all loads).
@@ -323,6 +336,7 @@ __global__ void __launch_bounds__(256, VG_OV_MINB) overlap_kernel(const OverlapI
     const MapDev map = it.map;
     const OccDev occ = it.occ;
     const PointBlock* __restrict__ blk = it.blk;
+    const PointBlock64* __restrict__ blk64 = it.blk64;
     unsigned count = 0;
     if (occ.occ) {  // occupancy bitmap: one 8-byte word per probe, no key compare
       for (unsigned base = first; base < n; base += kOverlapILP * stride) {
@@ -332,9 +346,9 @@ __global__ void __launch_bounds__(256, VG_OV_MINB) overlap_kernel(const OverlapI
         for (int u = 0; u < kOverlapILP; ++u) {
           const unsigned i = base + u * stride;
           const unsigned ic = min(i, n - 1);
-          const float4 a = __ldg(&blk[ic / kPointBlock].pa[ic % kPointBlock]);
-          double q0, q1, q2, l0, l1, l2;
-          apply_pose_rn(T, a.x, a.y, a.z, q0, q1, q2);
+          double px, py, pz, q0, q1, q2, l0, l1, l2;
+          load_point64(blk, blk64, ic, px, py, pz);
+          apply_pose_rn(T, px, py, pz, q0, q1, q2);
           unsigned k0 = 0, k1 = 0, k2 = 0, word = 0;
           const bool ok = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && i < n &&
                           occ_locate(occ, k0, k1, k2, word, bit[u]);
@@ -351,9 +365,9 @@ __global__ void __launch_bounds__(256, VG_OV_MINB) overlap_kernel(const OverlapI
       for (int u = 0; u < kOverlapILP; ++u) {
         const unsigned i = base + u * stride;
         const unsigned ic = min(i, n - 1);
-        const float4 a = __ldg(&blk[ic / kPointBlock].pa[ic % kPointBlock]);
-        double q0, q1, q2, l0, l1, l2;
-        apply_pose_rn(T, a.x, a.y, a.z, q0, q1, q2);
+        double px, py, pz, q0, q1, q2, l0, l1, l2;
+        load_point64(blk, blk64, ic, px, py, pz);
+        apply_pose_rn(T, px, py, pz, q0, q1, q2);
         unsigned k0 = 0, k1 = 0, k2 = 0;
         ok[u] = voxel_key(q0, q1, q2, map.res, map.inv_res, k0, k1, k2, l0, l1, l2) && i < n;
         pack_key32(k0, k1, k2, hi[u], lo[u]);
@@ -441,14 +455,13 @@ __global__ void __launch_bounds__(256) overlap_multi_kernel(const OverlapItem* _
   const int m0 = ch.x;
   const int mc = ch.y;
   if (threadIdx.x < kOvMaps) cnt[threadIdx.x] = 0;
-  float px[kOvPoints], py[kOvPoints], pz[kOvPoints];
+  double px[kOvPoints], py[kOvPoints], pz[kOvPoints];
   bool in[kOvPoints];
 #pragma unroll
   for (int u = 0; u < kOvPoints; ++u) {
     const unsigned i = (blockIdx.x * kOvPoints + u) * blockDim.x + threadIdx.x;
     const unsigned ic = min(i, n - 1);
-    const float4 a = __ldg(&blk[ic / kPointBlock].pa[ic % kPointBlock]);
-    px[u] = a.x, py[u] = a.y, pz[u] = a.z;
+    load_point64(blk, it0.blk64, ic, px[u], py[u], pz[u]);
     in[u] = i < n;
   }
   __syncthreads();
@@ -592,7 +605,7 @@ cudaError_t launch_occ_build(const OccJob* jobs, int m, unsigned max_words, unsi
 constexpr int kOccPoints = VG_OCC_POINTS;  // points per lane (amortise the per-map loads)
 // The reference's key of one point (fp64 transform + exact floor), out of line: the fp32 screen
 // keeps the kernel's registers for the common path.
-__device__ __noinline__ uint4 exact_probe_key(const double* T, float x, float y, float z, double res, double inv_res) {
+__device__ __noinline__ uint4 exact_probe_key(const double* T, double x, double y, double z, double res, double inv_res) {
   double e0, e1, e2, l0, l1, l2;
   apply_pose_rn(T, x, y, z, e0, e1, e2);
   unsigned k0 = 0, k1 = 0, k2 = 0;
@@ -658,7 +671,9 @@ __global__ void __launch_bounds__(256, 4) overlap_occ_kernel(const OverlapItem* 
 #pragma unroll
       for (int u = 0; u < kOccPoints; ++u) {
         if (!((need >> u) & 1u)) continue;
-        const uint4 e = exact_probe_key(it.T, px[u], py[u], pz[u], it.map.res, it.map.inv_res);
+        double ex = px[u], ey = py[u], ez = pz[u];
+        if (it.blk64) load_point64(blk, it.blk64, min(base + u * 32 + lane, n - 1), ex, ey, ez);  // exact means
+        const uint4 e = exact_probe_key(it.T, ex, ey, ez, it.map.res, it.map.inv_res);
         const unsigned rx = e.x - (static_cast<unsigned>(sc.cx0) + (1u << 20));
         const unsigned ry = e.y - (static_cast<unsigned>(sc.cy0) + (1u << 20));
         const unsigned rz = e.z - (static_cast<unsigned>(sc.cz0) + (1u << 20));
@@ -685,9 +700,9 @@ __global__ void __launch_bounds__(256, 4) overlap_occ_kernel(const OverlapItem* 
 // computes them (fl32 of the fp64 values, same margin formula); exact culling of the cloud box
 // (8 corners in fp64) against the map's occupied box grown by one voxel -> n = 0 (no work).
 __global__ void mapset_prepare_kernel(const OverlapItem* __restrict__ templates, int m,
-                                      const double* __restrict__ poses12, const PointBlock* blk, unsigned n,
-                                      const float* __restrict__ box, OverlapItem* __restrict__ items,
-                                      int2* __restrict__ chunks) {
+                                      const double* __restrict__ poses12, const PointBlock* blk,
+                                      const PointBlock64* blk64, unsigned n, const float* __restrict__ box,
+                                      OverlapItem* __restrict__ items, int2* __restrict__ chunks) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m) return;
   OverlapItem it = templates[k];
@@ -695,6 +710,7 @@ __global__ void mapset_prepare_kernel(const OverlapItem* __restrict__ templates,
 #pragma unroll
   for (int q = 0; q < 12; ++q) it.T[q] = T[q];
   it.blk = blk;
+  it.blk64 = blk64;
   it.n = n;
   float tmax = 0.f;
 #pragma unroll
@@ -702,7 +718,7 @@ __global__ void mapset_prepare_kernel(const OverlapItem* __restrict__ templates,
 #pragma unroll
   for (int q = 0; q < 3; ++q) it.scr.t[q] = __double2float_rn(T[9 + q]), tmax = fmaxf(tmax, fabsf(it.scr.t[q]));
   it.scr.inv_r = __double2float_rn(it.map.inv_res);
-  it.scr.A2 = __fmul_rn(5e-7f, it.scr.inv_r);
+  it.scr.A2 = __fmul_rn(blk64 ? kScreenA64 : kScreenA, it.scr.inv_r);
   it.scr.C = __fadd_rn(__fmul_rn(it.scr.A2, tmax), 1e-7f);
   // culling (the host's overlap_disjoint): the cloud box has no finite point when lo > hi
   bool live = box[0] <= box[3];
@@ -733,10 +749,11 @@ __global__ void mapset_prepare_kernel(const OverlapItem* __restrict__ templates,
 }
 
 cudaError_t launch_mapset_prepare(const OverlapItem* templates, int m, const double* poses12, const PointBlock* blk,
-                                  unsigned n, const float* cloud_box, OverlapItem* items, int2* chunks,
-                                  cudaStream_t s) {
+                                  const PointBlock64* blk64, unsigned n, const float* cloud_box, OverlapItem* items,
+                                  int2* chunks, cudaStream_t s) {
   if (m <= 0) return cudaSuccess;
-  mapset_prepare_kernel<<<(m + 127) / 128, 128, 0, s>>>(templates, m, poses12, blk, n, cloud_box, items, chunks);
+  mapset_prepare_kernel<<<(m + 127) / 128, 128, 0, s>>>(templates, m, poses12, blk, blk64, n, cloud_box, items,
+                                                        chunks);
   return cudaGetLastError();
 }
 
@@ -792,11 +809,19 @@ __global__ void transform_kernel(const TransformItem* __restrict__ items, double
 #pragma unroll
   for (int q = 0; q < 12; ++q) T[q] = it.T[q];
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < it.n; i += gridDim.x * blockDim.x) {
+    const size_t o = it.offset + i;
+    if (it.xyz64) {  // float64 frame: its exact values
+      double C[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) C[e] = it.cov9[9 * (size_t)i + e];
+      transform_point(T, it.xyz64[3 * (size_t)i], it.xyz64[3 * (size_t)i + 1], it.xyz64[3 * (size_t)i + 2], C,
+                      out_xyz + 3 * o, out_cov9 + 9 * o);
+      continue;
+    }
     const float4 a = __ldg(it.pa + i);
     const float4 b = __ldg(it.pb + i);
     const double czz = __ldg(it.pc + i);
     const double C[9] = {a.w, b.x, b.y, b.x, b.z, b.w, b.y, b.w, czz};
-    const size_t o = it.offset + i;
     transform_point(T, a.x, a.y, a.z, C, out_xyz + 3 * o, out_cov9 + 9 * o);
   }
 }

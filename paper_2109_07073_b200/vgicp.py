@@ -163,21 +163,74 @@ class _Handle:
 
 # ------------------------------------------------------------------------------------ clouds
 class PointCloud(_Handle):
-    """Device-resident PointCloud (point_cloud.hpp:21-37): float32 means + 6 unique cov floats."""
+    """Device-resident PointCloud (point_cloud.hpp:21-37).
+
+    float32 means + the 6 unique float32 covariance entries (KITTI precision, io.cpp:50). Means or
+    covariances given as float64 values that are not float32-exact (submap clouds: transform_cloud +
+    voxel_downsample output, pipeline.cpp:100-111) make a float64 cloud (vgicp_cloud_upload_f64): its
+    exact values drive every key, correspondence, overlap hit and map statistic, as in the reference.
+    """
 
     _destroy = "vgicp_cloud_destroy"
 
     def __init__(self, means, covariances=None, ctx: Context | None = None):
         ctx = ctx or default_context()
-        m = np.ascontiguousarray(np.asarray(means, dtype=np.float32).reshape(-1, 3))
-        c = None if covariances is None else cov6_from(covariances)
-        if c is not None and len(c) != len(m):
+        m64 = np.asarray(means)
+        m64 = m64.reshape(-1, 3) if m64.size else m64.reshape(0, 3)
+        c64 = None if covariances is None else np.asarray(covariances)
+        if c64 is not None and len(c64.reshape(len(c64), -1)) != len(m64):
             raise ValueError("covariance count does not match point count")
         h = C.c_void_p()
+        if self._needs_f64(m64, c64):
+            mm = np.ascontiguousarray(m64, dtype=np.float64)
+            cc = None
+            if c64 is not None:
+                cc = np.asarray(c64, np.float64)
+                if cc.ndim == 3:
+                    cc = cc.reshape(len(cc), 9)
+                elif cc.shape[-1] == 6:  # unique entries -> full symmetric matrix
+                    cc = cc[:, [0, 1, 2, 1, 3, 4, 2, 4, 5]]
+                cc = np.ascontiguousarray(cc)
+            check(_lib.load().vgicp_cloud_upload_f64(ctx.handle, _ptr(mm), _ptr(cc) if cc is not None else None,
+                                                     len(mm), C.byref(h)))
+            super().__init__(ctx, h)
+            self.means, self.cov6 = mm, (None if cc is None else cov6_from(cc))
+            return
+        m = np.ascontiguousarray(m64, dtype=np.float32)
+        c = None if c64 is None else cov6_from(c64)
         check(_lib.load().vgicp_cloud_upload(ctx.handle, _ptr(m), _ptr(c) if c is not None else None, len(m), C.byref(h)))
         super().__init__(ctx, h)
         self.means = m
         self.cov6 = c
+
+    @staticmethod
+    def _needs_f64(means: np.ndarray, covs) -> bool:
+        """True when a float64 input does not survive the float32 round trip (or a 3×3 covariance is
+        not exactly symmetric): such clouds keep their float64 values on the device."""
+        def inexact(a):
+            a = np.asarray(a)
+            if a.dtype != np.float64 or a.size == 0:
+                return False
+            with np.errstate(over="ignore", invalid="ignore"):
+                r = a.astype(np.float32).astype(np.float64)
+            return not np.array_equal(r, a, equal_nan=True)
+        if inexact(means):
+            return True
+        if covs is None:
+            return False
+        c = np.asarray(covs)
+        if inexact(c):
+            return True
+        if c.dtype == np.float64 and c.size and (c.ndim == 3 or c.shape[-1] == 9):
+            f = c.reshape(len(c), 9)
+            return not (np.array_equal(f[:, 1], f[:, 3]) and np.array_equal(f[:, 2], f[:, 6])
+                        and np.array_equal(f[:, 5], f[:, 7]))
+        return False
+
+    def is_f64(self) -> bool:
+        v = C.c_int()
+        check(_lib.load().vgicp_cloud_is_f64(self._h, C.byref(v)))
+        return bool(v.value)
 
     @classmethod
     def adopt(cls, ctx: Context, handle: C.c_void_p) -> "PointCloud":

@@ -159,20 +159,39 @@ def test_gpu_submap_build_bit_exact(V, ds_res):
 
 @gpu
 def test_gpu_submap_cloud_as_factor_source(V):
-    """The float32 submap cloud is a regular factor source (float-rounded fp64 submap points)."""
+    """The submap cloud is a float64 device cloud (its means are transform_cloud + voxel_downsample
+    output, not float32-exact: pipeline.cpp:100-111) and a factor source / overlap probe exactly as
+    the reference uses it (:139, :141): inliers and overlap hits equal the oracle fed the float64
+    submap cloud `om` itself, blocks within the float32-algebra tolerance."""
+    from helpers import lin_dict, rel_block_error
+
     frames64, poses, clouds = submap_case(V, nframes=3, n=4000, seed=31)
     sub_a = V.build_submap(clouds, poses, 0.25, 1.0)
     sub_b = V.build_submap(clouds[1:], poses[1:], 0.25, 1.0)
     om, oc, _ = O.submap(frames64[1:], poses[1:], 0.25, 1.0)
-    m32 = om.astype(np.float32).astype(np.float64)
-    c32 = O.cov9(np.asarray(oc).reshape(-1, 9)[:, [0, 1, 2, 4, 5, 8]].astype(np.float32).astype(np.float64))
+    oc9 = np.asarray(oc).reshape(-1, 9)
+    assert sub_b.cloud.is_f64() and sub_b.cloud.size() == len(om)
+    assert not np.array_equal(om, om.astype(np.float32).astype(np.float64))
     _, _, omap_a = O.submap(frames64, poses, 0.25, 1.0)
     fac = V.MatchingCostFactor(0, 1, sub_b.cloud, sub_a.voxels)
-    Ta, Tb = IDENT, O.IDENTITY
-    lin = V.linearize_matching_cost(fac, Ta, Tb)
-    ref = O.linearize(m32, c32, omap_a, Ta, Tb)
-    assert lin.inliers == ref["inliers"] and lin.inliers > 0
-    assert abs(lin.error - ref["error"]) <= 1e-5 * max(1.0, abs(ref["error"]))
+    rng = O.Rng(77)
+    for Ta, Tb in [(IDENT, O.IDENTITY), (rng.random_pose(0.01, 0.1), rng.random_pose(0.01, 0.1))]:
+        lin = V.linearize_matching_cost(fac, Ta, Tb)
+        err, inl = V.evaluate_matching_cost(fac, Ta, Tb)
+        ref = O.linearize(om, oc9, omap_a, Ta, Tb)
+        assert lin.inliers == ref["inliers"] == inl and lin.inliers > 0
+        e = rel_block_error(lin_dict(lin), ref)
+        assert max(e.values()) <= 1e-5, e
+        rel = O.compose(O.inverse(Ta), Tb)
+        assert int(V.overlap_hits([sub_b.cloud], [rel], [sub_a.voxels])[0]) == O.overlap_hits(om, rel, omap_a)
+    # a map built from the submap cloud equals the reference's GaussianVoxelMap(submap cloud)
+    gk, gcnt, gm, gc = V.GaussianVoxelMap(sub_b.cloud, 0.5).export()
+    ok_, ocnt, omm, occ = O.OracleMap(om, oc9, 0.5).export()
+    assert np.array_equal(gk, ok_) and np.array_equal(gcnt, ocnt) and np.array_equal(gm, omm) and np.array_equal(gc, occ)
+    # the submap cloud as a frame of another submap transforms its exact float64 values
+    sub_c = V.build_submap([sub_b.cloud], [poses[0]], 0.0, 1.0)
+    _, _, omap_c = O.submap([(om, oc9)], [poses[0]], 0.0, 1.0)
+    assert_export_equal(sub_c.voxels, omap_c)
 
 
 @gpu
