@@ -11,7 +11,9 @@ same step (the host solver's input, north star). Rank 0 prints one JSON line.
 
 --impl reference times the reference's CPU implementation of the path — the oracle port
 (oracle/, a restatement of proj/src/factors.cpp + voxelmap.cpp; the reference itself needs Eigen
-and cannot be built here) — with every host thread, on a bounded sample of the same workload.
+and cannot be built here) — with every host thread, one full C3 linearize pass (all factors) per
+step, inputs from the same generator (oracle/synthetic.cpp) and links from the same overlap rule;
+that arm never loads the product library.
 """
 from __future__ import annotations
 
@@ -31,6 +33,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "VGICP factor linearizations/sec (C3 dense graph)"
+C3_WORKLOAD = "C3 KITTI-00-shaped dense graph (figure-eight, 450 frames x 20k pts, 1.0 m voxels, <=10 links/frame)"
 UNIT = "factors/s"
 BYTES_PER_POINT = 36  # fp32 mean (12 B) + 6 unique fp32 covariance entries (24 B), SURVEY §8(d)
 BYTES_PER_HIT = 44  # 8 B key + 12 B voxel mean + 24 B voxel covariance
@@ -168,57 +171,84 @@ def cpu_reference_run(scans, links, threads: int, budget_s: float, resolution: f
     return done, elapsed, pts
 
 
-def reference_links(scans, frames, max_links=10, min_overlap=0.025, resolution=1.0, threads=0):
-    """Factor-creation rule on the oracle (pipeline.cpp:135-141) for frames in `frames`."""
+def reference_links(scans, threads=0, max_links=10, min_overlap=0.025, resolution=1.0):
+    """The C3 factor-creation rule (pipeline.cpp:135-141) on the oracle port: every frame j against
+    every predecessor's map at the ground-truth relative pose, its <= 10 highest-overlap predecessors
+    with overlap > 0.025 (the same exact hit counts as the GPU sweep of the ours arm, hence the same
+    links). Probes run pair-parallel on `threads` host threads (ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_ctypes as O
-    from paper_2109_07073_b200.workloads import pose_inv, pose_mul, select_links
+    from bench_workloads.workloads import relative_poses, select_links
 
-    maps = {}
-    overlaps = {}
-    for j in frames:
-        mj = scans.means[j].astype(np.float64)
-        for i in range(j):
-            if i not in maps:
-                maps[i] = O.OracleMap(scans.means[i].astype(np.float64), O.cov9(scans.cov6[i].astype(np.float64)), resolution, threads=threads)
-            rel = pose_mul(pose_inv(scans.gt[i]), scans.gt[j])
-            overlaps[(i, j)] = O.overlap_rate(mj, rel, maps[i], threads=threads)
-    links = select_links(overlaps, max(frames) + 1, max_links, min_overlap)
-    return [l for l in links if l[1] in set(frames)]
+    n = len(scans.means)
+    pts = [m.astype(np.float64) for m in scans.means]
+    maps = [O.OracleMap(pts[i], O.cov9(scans.cov6[i].astype(np.float64)), resolution, threads=threads)
+            for i in range(n)]
+    pairs = [(i, j) for j in range(1, n) for i in range(j)]
+    rels = relative_poses(scans.gt, pairs)
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        ov = list(ex.map(lambda k: O.overlap_rate(pts[pairs[k][1]], rels[k], maps[pairs[k][0]], threads=1),
+                         range(len(pairs)), chunksize=256))
+    return select_links(dict(zip(pairs, ov)), n, max_links, min_overlap), maps
 
 
 def run_reference(args):
+    """Reference arm: the reference's CPU implementation of the path (the oracle port of
+    factors.cpp / voxelmap.cpp with ExecPolicy{all cores, false}; the reference itself needs Eigen
+    and cannot be built here) on the SAME workload as the ours arm: the full C3 graph (450 frames,
+    the same generator and seed, links by the same overlap rule). One step = one linearize pass over
+    all factors; maps and inputs are resident (built before the timed region), as in the ours arm.
+    Nothing of the product library is loaded: inputs come from oracle/ (synthetic.cpp restatement)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from paper_2109_07073_b200 import workloads as W
+    from bench_workloads import workloads as W
 
     threads = os.cpu_count() or 1
     os.environ.setdefault("OMP_PROC_BIND", "close")
+    t0 = time.perf_counter()
     spec = W.c3_spec(args.frames, args.points, seed=1)
-    sample_frames = list(range(11, 11 + 20))  # frames with a full set of 10 predecessors
-    scans = W.make_scans(spec, frames_needed=range(0, max(sample_frames) + 1), threads=threads)
-    links = reference_links(scans, sample_frames, threads=threads)
-    # one step = the whole bounded sample (≈200 factors)
+    scans = W.make_scans(spec, threads=threads)  # host covariances (point_cloud.cpp:44-83 restated)
+    t1 = time.perf_counter()
+    links, maps = reference_links(scans, threads=threads)
+    t2 = time.perf_counter()
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_ctypes as O
+
+    src = {}
+    for _, j in links:
+        if j not in src:
+            src[j] = (scans.means[j].astype(np.float64), O.cov9(scans.cov6[j].astype(np.float64)))
+    npts = sum(len(src[j][0]) for _, j in links)
+
+    def one_pass():
+        t = time.perf_counter()
+        for i, j in links:
+            O.linearize(*src[j], maps[i], scans.odom[i], scans.odom[j], threads=threads)
+        return time.perf_counter() - t
+
     for _ in range(args.warmup):
-        cpu_reference_run(scans, links, threads, 1e9)
-    times = []
-    pts = 0
-    for _ in range(args.steps):
-        n, dt, pts = cpu_reference_run(scans, links, threads, 1e9)
-        times.append(dt)
+        one_pass()
+    times = [one_pass() for _ in range(args.steps)]
     t = sum(times)
-    value = len(links) * args.steps / t
+    F = len(links)
+    value = F * args.steps / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C3 KITTI-00-shaped dense graph (figure-eight, 450 frames x 20k pts, 1.0 m voxels, <=10 links/frame)",
-                   "sample": f"{len(links)} factors of frames {sample_frames[0]}-{sample_frames[-1]} per step"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{len(links)} factors x {args.steps} steps (oracle/ restatement, ExecPolicy{{{threads}, false}})"},
+        "config": {"workload": C3_WORKLOAD, "factors": F, "points_per_pass": npts, "frames": args.frames,
+                   "points_per_scan": args.points,
+                   "sample": f"the whole C3 graph ({F} factors, {npts} source points) every step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+                         "sample": f"all {F} C3 factors x {args.steps} steps (oracle/ restatement of factors.cpp:90-148, "
+                                   f"ExecPolicy{{{threads}, false}})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "points_per_s": pts * args.steps / t,
+        "points_per_s": npts * args.steps / t,
+        "ms_per_step_min": 1e3 * min(times), "ms_per_step_max": 1e3 * max(times),
+        "build_seconds": {"scans_and_covariances": round(t1 - t0, 2), "maps_and_overlap_selection": round(t2 - t1, 2)},
     }
     print(json.dumps(line), flush=True)
 
@@ -264,7 +294,7 @@ def run_lm_c2(ctx, threads):
     convergence with default LmSettings (optimizer.hpp:12-21). Each iteration = assemble + damped
     solve (+ retries) + candidate error launch(es) + re-linearization launch, wall clock."""
     from paper_2109_07073_b200 import optimizer as LM
-    from paper_2109_07073_b200 import workloads as W
+    from bench_workloads import workloads as W
 
     wl = W.build_graph_workload(ctx, W.c2_spec(), links=W.c2_links(100), threads=threads)
     LM.optimize(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=2))  # warm-up
@@ -274,6 +304,7 @@ def run_lm_c2(ctx, threads):
     _, nrep = LM.optimize_native(wl.graph, wl.poses)
     nits = sorted(nrep.iteration_seconds)
     native = {"ms_per_lm_iteration_median": 1e3 * nits[len(nits) // 2] if nits else None,
+              "ms_per_lm_iteration_mean": 1e3 * sum(nits) / len(nits) if nits else None,
               "iterations": nrep.iterations, "final_error": nrep.final_error, "reason": nrep.reason,
               "band_solver": nrep.band_solver,
               "note": "native LM (vgicp_graph_optimize): device linearize + assembly; the chain's narrow system "
@@ -292,6 +323,7 @@ def run_lm_c2(ctx, threads):
     return {
         "factors": wl.num_factors, "poses": len(wl.poses), "iterations": nrep.iterations,
         "ms_per_lm_iteration_median": native["ms_per_lm_iteration_median"],
+        "ms_per_lm_iteration_mean": native["ms_per_lm_iteration_mean"],
         "ms_total": 1e3 * nrep.wall_time_seconds, "initial_error": nrep.initial_error,
         "final_error": nrep.final_error, "reason": nrep.reason,
         "note": native["note"] + "; wall clock incl. H2D/D2H",
@@ -310,6 +342,7 @@ def run_lm_c3(wl, max_iterations=30):
     from paper_2109_07073_b200 import optimizer as LM
 
     med = lambda r: 1e3 * sorted(r.iteration_seconds)[len(r.iteration_seconds) // 2] if r.iteration_seconds else None  # noqa: E731
+    mean = lambda r: 1e3 * sum(r.iteration_seconds) / len(r.iteration_seconds) if r.iteration_seconds else None  # noqa: E731
     LM.optimize_native(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=2))  # warm-up
     _, rep = LM.optimize_native(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=max_iterations))
     LM.optimize(wl.graph, wl.poses, settings=LM.LmSettings(max_iterations=2))  # warm-up
@@ -318,7 +351,8 @@ def run_lm_c3(wl, max_iterations=30):
                           speculative=False)
     return {
         "factors": wl.num_factors, "poses": len(wl.poses), "iterations": rep.iterations,
-        "ms_per_lm_iteration_median": med(rep), "ms_per_lm_iteration_mean": 1e3 * rep.wall_time_seconds / max(1, rep.iterations),
+        "ms_per_lm_iteration_median": med(rep), "ms_per_lm_iteration_mean": mean(rep),
+        "ms_per_accepted_iteration": 1e3 * rep.wall_time_seconds / max(1, rep.iterations),
         "ms_total": 1e3 * rep.wall_time_seconds, "initial_error": rep.initial_error, "final_error": rep.final_error,
         "reason": rep.reason, "solves": rep.solves, "linearizations": rep.linearizations,
         "note": "native LM (vgicp_graph_optimize): each candidate linearized + device-assembled (its errors equal "
@@ -339,7 +373,7 @@ def run_c5(ctx, steps=10):
     """BASELINE config C5 on one GPU: 1,000-frame loop-closing graph, ~10k factors over 0.5 / 1 /
     2 m maps; device-timed linearize / evaluate launches with resident inputs."""
     import torch
-    from paper_2109_07073_b200 import workloads as W
+    from bench_workloads import workloads as W
 
     wl = W.build_c5_workload(ctx)
     g = wl.graph
@@ -393,7 +427,7 @@ def run_c1(ctx, threads, reps=50):
     each through the host C ABI (pinned H2D of the poses, D2H of the block), wall clock."""
     import paper_2109_07073_b200 as V
     from paper_2109_07073_b200 import optimizer as LM
-    from paper_2109_07073_b200 import workloads as W
+    from bench_workloads import workloads as W
 
     sc = W.make_scans(W.c1_spec(), threads=threads, ctx=ctx)
     tgt = V.PointCloud(sc.means[0], sc.cov6[0], ctx)
@@ -424,8 +458,8 @@ def run_c4(ctx, n_maps=4000, points=20000, reps=5):
     """BASELINE config C4: one new frame against n_maps keyframe voxel maps (1.0 m), the overlap
     query of keyframe / factor creation (pipeline.cpp:135-150) as ONE batched launch."""
     import paper_2109_07073_b200 as V
-    from paper_2109_07073_b200 import synthetic as S
-    from paper_2109_07073_b200 import workloads as W
+    from bench_workloads import synthetic as S
+    from bench_workloads import workloads as W
 
     t0 = time.perf_counter()
     seq = S.generate(S.SceneSpec(shape="figure_eight", frames=n_maps + 1, radius=50.0, points_per_scan=points, seed=4))
@@ -484,7 +518,7 @@ def run_submap(ctx, wl, threads, frames=20, reps=5):
     """Submap creation (pipeline.cpp:92-114, config.hpp defaults: 20-frame window, 0.25 m
     downsample, 1.0 m map) from C3 frames 0..19: GPU through the C ABI vs the oracle port."""
     import paper_2109_07073_b200 as V
-    from paper_2109_07073_b200 import workloads as W
+    from bench_workloads import workloads as W
 
     clouds = wl.clouds[:frames]
     poses = np.stack([W.pose_mul(W.pose_inv(wl.scans.gt[0]), wl.scans.gt[k]) for k in range(frames)])
@@ -525,7 +559,7 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
 
     import paper_2109_07073_b200 as V
-    from paper_2109_07073_b200 import workloads as W
+    from bench_workloads import workloads as W
 
     ctx = V.Context(local, stream=stream.cuda_stream)
     threads = max(1, (os.cpu_count() or 1) // max(world, 1))
@@ -642,10 +676,11 @@ def run_ours(args):
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    traffic = None
+    traffic = traffic_src = None
     tf = ROOT / "profiles" / "linearize_dram_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+    if tf.exists():  # DRAM bytes need ncu: the committed `--set full` capture of this kernel, not this run
+        tj = json.loads(tf.read_text())
+        traffic, traffic_src = tj.get("bytes_per_launch"), tj.get("source", str(tf.relative_to(ROOT)))
     data_bytes = sum(36 * len(m) for m in wl.scans.means) + sum(48 * int(m.size()) * 2 for m in wl.maps)
 
     lm = lm3 = c1 = c4 = cov = sub = c5 = None
@@ -676,7 +711,7 @@ def run_ours(args):
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {
-            "workload": "C3 KITTI-00-shaped dense graph (figure-eight, 450 frames x 20k pts, 1.0 m voxels, <=10 links/frame)",
+            "workload": C3_WORKLOAD,
             "factors_per_gpu": F, "points_per_gpu": P, "frames": args.frames, "points_per_scan": args.points,
             "parallelism": f"factor-sharded x{world} (one graph per rank) + NCCL gather to rank 0" if world > 1 else "single GPU",
             "l2": f"no flush: resident inputs {data_bytes / 1e6:.0f} MB > 126 MB L2",
@@ -690,8 +725,12 @@ def run_ours(args):
         "e2e": {"value": F_all / (e2e_ms * 1e-3) if e2e_ms else None, "unit": UNIT,
                 "h2d_bytes_per_step": int(wl.poses.nbytes), "d2h_bytes_per_step": int(F * (V.LINEARIZED_DOUBLES * 8 + 4)),
                 "ms_per_step": e2e_ms, "path": "vgicp_graph_linearize (C ABI, page-locked host poses in / blocks out, synchronous)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src,
+        "roofline": {"bound": "latency/LSU", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "traffic_source": f"ncu --set full, not this run ({traffic_src})",
+                     "bound_evidence": ("frac is the SURVEY 8(d) algorithmic bytes over the HBM peak; measured DRAM "
+                                        "traffic is ~1/8 of them (each cloud / map is re-read by ~10 factors from L2), "
+                                        "so the kernel is bound by gather latency and the LSU pipe, not HBM bandwidth"),
+                     "peak_source": peak_src,
                      "bytes_alg_per_launch": bytes_alg,
                      "bytes_alg_formula": "36*sum(N_f) + 44*sum(inliers_f) + 116*F (SURVEY 8d)"},
         "cpu_baseline": cpu,

@@ -1,9 +1,10 @@
 """Benchmark input pipeline: seeded synthetic KITTI-shaped scans + covariance preprocessing.
 
-Thin ctypes wrapper over lib/libvgicp_synth.so (csrc/host/synthetic.cpp), a host-side restatement
-of the reference's generate_synthetic_sequence (proj/src/synthetic.cpp:121-213) and
-estimate_covariances (proj/src/point_cloud.cpp:44-83). Not on the accelerated path: this is the
-one-time preprocessing that produces the inputs SURVEY.md §8(d) specifies.
+Thin ctypes wrapper over oracle/_build/libvgicp_synth.so (oracle/synthetic.cpp), the oracle's
+restatement of the reference's generate_synthetic_sequence (proj/src/synthetic.cpp:121-213) and
+estimate_covariances (proj/src/point_cloud.cpp:44-83), SURVEY.md §8(c). Benchmark / test input
+generation only, outside every timed region: the product package never imports it, and both bench
+arms (ours and --impl reference) generate identical scans with it.
 """
 from __future__ import annotations
 
@@ -13,9 +14,9 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import PKG
+from pathlib import Path
 
-LIB_PATH = PKG / "lib" / "libvgicp_synth.so"
+LIB_PATH = Path(__file__).resolve().parents[1] / "oracle" / "_build" / "libvgicp_synth.so"
 
 SHAPES = {"line": 0, "circle": 1, "figure_eight": 2, "figure-eight": 2}
 
@@ -67,7 +68,7 @@ def _load():
     global _LIB
     if _LIB is None:
         if not LIB_PATH.exists():
-            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build()")
+            raise ImportError(f"{LIB_PATH} missing: run `make -C oracle` (or __graft_entry__.build())")
         lib = C.CDLL(str(LIB_PATH))
         lib.vs_generate.restype = C.c_int
         lib.vs_generate.argtypes = [C.POINTER(_Spec), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]

@@ -21,8 +21,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import synthetic as S
-from .vgicp import (Context, FactorGraph, GaussianVoxelMap, MatchingCostFactor, PointCloud, estimate_covariances_batch,
-                    overlap_hits)
+
+# The product package is imported lazily (only by the builders that upload to a device), so the
+# reference bench arm — scans, host covariances, link selection on the oracle — never loads it.
 
 
 def pose_inv(T):
@@ -58,7 +59,7 @@ class Scans:
     odom: np.ndarray
 
 
-def make_scans(spec: S.SceneSpec, frames_needed=None, threads: int = 0, ctx: Context | None = None) -> Scans:
+def make_scans(spec: S.SceneSpec, frames_needed=None, threads: int = 0, ctx=None) -> Scans:
     """Generate the scans and their plane-regularised covariances (k=10, eps=1e-3, as
     run_pipeline.cpp:131). With a context the covariances come from the batched GPU kernel
     (estimate_covariances_batch), otherwise from the host preprocessing (synthetic.cpp)."""
@@ -66,6 +67,8 @@ def make_scans(spec: S.SceneSpec, frames_needed=None, threads: int = 0, ctx: Con
     idx = list(range(len(seq.scans)) if frames_needed is None else frames_needed)
     covs = [None] * len(seq.scans)
     if ctx is not None:
+        from paper_2109_07073_b200.vgicp import estimate_covariances_batch
+
         for k, c in zip(idx, estimate_covariances_batch([seq.scans[k] for k in idx], 10, 1e-3, ctx)):
             covs[k] = c
     else:
@@ -105,13 +108,13 @@ def select_links(overlaps: dict, frames: int, max_links: int = 10, min_overlap: 
 
 @dataclass
 class GraphWorkload:
-    ctx: Context
+    ctx: object  # paper_2109_07073_b200.Context
     scans: Scans
     clouds: list
     maps: list
     links: list  # (target i, source j)
     factors: list
-    graph: FactorGraph
+    graph: object  # paper_2109_07073_b200.FactorGraph
     poses: np.ndarray  # num_poses × 12 (initial guesses: drifted odometry)
     resolution: float
     build_seconds: dict = field(default_factory=dict)
@@ -124,9 +127,11 @@ class GraphWorkload:
         return self.graph.num_points()
 
 
-def build_graph_workload(ctx: Context, spec: S.SceneSpec, resolution: float = 1.0, max_links: int = 10,
+def build_graph_workload(ctx, spec: S.SceneSpec, resolution: float = 1.0, max_links: int = 10,
                          min_overlap: float = 0.025, links=None, chunk: int = 0, threads: int = 0,
                          gpu_covariances: bool = True) -> GraphWorkload:
+    from paper_2109_07073_b200.vgicp import FactorGraph, GaussianVoxelMap, MatchingCostFactor, PointCloud, overlap_hits
+
     t0 = time.perf_counter()
     scans = make_scans(spec, threads=threads, ctx=ctx if gpu_covariances else None)
     t1 = time.perf_counter()
@@ -161,10 +166,12 @@ def c5_spec(frames=1000, points=20000, seed=5) -> S.SceneSpec:
                        drift=(0.0, 0.0, np.deg2rad(0.1), 0.01, 0.0, 0.0))
 
 
-def build_c5_workload(ctx: Context, spec: S.SceneSpec | None = None, max_links: int = 10, min_overlap: float = 0.025,
+def build_c5_workload(ctx, spec: S.SceneSpec | None = None, max_links: int = 10, min_overlap: float = 0.025,
                       chunk: int = 0) -> GraphWorkload:
     """C5: every frame gets 0.5 / 1 / 2 m maps; links by the overlap rule on the 1 m maps; link k
     uses the map of resolution C5_RESOLUTIONS[k % 3]."""
+    from paper_2109_07073_b200.vgicp import FactorGraph, GaussianVoxelMap, MatchingCostFactor, PointCloud, overlap_hits
+
     spec = spec or c5_spec()
     t0 = time.perf_counter()
     scans = make_scans(spec, ctx=ctx)

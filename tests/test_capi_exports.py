@@ -60,8 +60,9 @@ def test_host_voxel_key_matches_oracle():
 
 
 def test_package_has_no_oracle_dependency():
-    """The product path never imports, includes or links the checker (oracle/)."""
+    """The product path never imports, includes or links the checker (oracle/) or the benchmark
+    input generator that lives beside it (bench_workloads/, oracle/synthetic.cpp)."""
     pkg = ROOT / "paper_2109_07073_b200"
-    bad = re.compile(r"(import\s+oracle|oracle_ctypes|vgicp_oracle|liboracle|oracle/_build|#include\s+[<\"].*oracle)")
+    bad = re.compile(r"(import\s+oracle|oracle_ctypes|vgicp_oracle|liboracle|oracle/_build|bench_workloads|libvgicp_synth|#include\s+[<\"].*oracle)")
     for f in [*pkg.rglob("*.py"), *pkg.rglob("*.cu"), *pkg.rglob("*.cuh"), *pkg.rglob("*.h"), *pkg.rglob("Makefile")]:
         assert not bad.search(f.read_text()), f

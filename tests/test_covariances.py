@@ -162,7 +162,7 @@ def test_gpu_validation(V):
 @gpu
 def test_gpu_c3_scan_matches_host_preprocessing(V):
     """A full C3 scan (20k points): GPU vs the host preprocessing used by the workload builder."""
-    from paper_2109_07073_b200 import synthetic as S, workloads as W
+    from bench_workloads import synthetic as S, workloads as W
 
     seq = S.generate(W.c3_spec(frames=2))
     p = seq.scans[1]

@@ -13,7 +13,7 @@ import oracle_ctypes as O
 from helpers import rel_block_error
 
 V = pytest.importorskip("paper_2109_07073_b200")
-from paper_2109_07073_b200 import workloads as W  # noqa: E402
+from bench_workloads import workloads as W  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 

@@ -167,7 +167,7 @@ def test_chain_lm_reduces_error_and_drift():
     """A short C2-style chain (circle, 3 links per frame): LM on the GPU factors lowers the total
     error and moves the drifted odometry toward ground truth."""
     import paper_2109_07073_b200 as V
-    from paper_2109_07073_b200 import workloads as W
+    from bench_workloads import workloads as W
 
     spec = W.c2_spec(frames=12, points=5000)
     ctx = V.default_context(0)
@@ -197,7 +197,7 @@ def test_batched_se3_matches_scalar():
 
 def test_banded_solve_matches_dense():
     rng = np.random.default_rng(5)
-    from paper_2109_07073_b200 import workloads as W
+    from bench_workloads import workloads as W
 
     ij = np.array(W.c2_links(30))
     raw = np.zeros((len(ij), 121))

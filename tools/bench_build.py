@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 
 import paper_2109_07073_b200 as V
-from paper_2109_07073_b200 import workloads as W
+from bench_workloads import workloads as W
 
 ctx = V.Context(0)
 t = time.perf_counter()

@@ -4,7 +4,8 @@ import numpy as np
 sys.path.insert(0, ".")
 import torch
 import paper_2109_07073_b200 as V
-from paper_2109_07073_b200 import workloads as W, synthetic as S, _lib
+from bench_workloads import workloads as W, synthetic as S
+from paper_2109_07073_b200 import _lib
 ctx = V.default_context()
 n_maps = 4000
 seq = S.generate(S.SceneSpec(shape="figure_eight", frames=n_maps + 1, radius=50.0, points_per_scan=20000, seed=4))

@@ -4,7 +4,8 @@ import numpy as np
 sys.path.insert(0, ".")
 import torch
 import paper_2109_07073_b200 as V
-from paper_2109_07073_b200 import workloads as W, optimizer as LM
+from bench_workloads import workloads as W
+from paper_2109_07073_b200 import optimizer as LM
 ctx = V.default_context()
 wl = W.build_graph_workload(ctx, W.c3_spec())
 g, poses = wl.graph, wl.poses

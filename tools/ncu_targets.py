@@ -4,7 +4,7 @@ import sys
 import numpy as np
 sys.path.insert(0, ".")
 import paper_2109_07073_b200 as V
-from paper_2109_07073_b200 import workloads as W
+from bench_workloads import workloads as W
 
 ctx = V.default_context()
 wl = W.build_graph_workload(ctx, W.c3_spec())

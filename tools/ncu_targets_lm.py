@@ -9,7 +9,7 @@ import torch  # noqa: E402
 
 import paper_2109_07073_b200 as V  # noqa: E402
 from paper_2109_07073_b200 import optimizer as LM  # noqa: E402
-from paper_2109_07073_b200 import workloads as W  # noqa: E402
+from bench_workloads import workloads as W  # noqa: E402
 
 ctx = V.default_context()
 wl = W.build_graph_workload(ctx, W.c3_spec())

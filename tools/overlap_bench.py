@@ -4,7 +4,7 @@ import numpy as np
 sys.path.insert(0, ".")
 import torch
 import paper_2109_07073_b200 as V
-from paper_2109_07073_b200 import workloads as W
+from bench_workloads import workloads as W
 ctx = V.default_context()
 sc = W.make_scans(W.c3_spec(frames=120), ctx=ctx)
 clouds = [V.PointCloud(m, c, ctx) for m, c in zip(sc.means, sc.cov6)]

@@ -13,7 +13,7 @@ import torch  # noqa: E402
 
 import paper_2109_07073_b200 as V  # noqa: E402
 from paper_2109_07073_b200 import optimizer as LM  # noqa: E402
-from paper_2109_07073_b200 import workloads as W  # noqa: E402
+from bench_workloads import workloads as W  # noqa: E402
 
 cus = C.CDLL("libcusolver.so.11")
 csp = C.CDLL("libcusparse.so.12")

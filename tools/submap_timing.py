@@ -6,7 +6,7 @@ import numpy as np
 
 sys.path.insert(0, ".")
 import paper_2109_07073_b200 as V
-from paper_2109_07073_b200 import workloads as W
+from bench_workloads import workloads as W
 
 ctx = V.default_context()
 sc = W.make_scans(W.c3_spec(frames=20), ctx=ctx)
