@@ -226,9 +226,10 @@ int vgicp_graph_solve_damped_pair(vgicp_graph graph, const double* d_assembled, 
 /* optimize (optimizer.cpp:88-194) for a graph whose factors are all matching-cost factors, in the
  * library: every candidate is linearized + assembled on the device and scored by its per-factor
  * errors (= total_error), the damped system is solved on the device (block-band Cholesky) or on the
- * host (a dense O(m³) Cholesky: meant for small systems — the band solver covers envelopes up to ~80
- * blocks after reverse Cuthill-McKee, e.g. C5's 1,000 poses need 47), Pose::retract (se3.cpp:93-105)
- * on the host. Same damping schedule, acceptance rule,
+ * host (a band Cholesky: in slot order for narrow systems such as odometry chains, in the reverse
+ * Cuthill-McKee order when the envelope is too wide for the device kernel — the device kernel covers
+ * envelopes up to ~80 blocks, e.g. C5's 1,000 poses need 47; systems whose host band storage would
+ * exceed ~4 GB return VGICP_E_OUT_OF_MEMORY), Pose::retract (se3.cpp:93-105) on the host. Same damping schedule, acceptance rule,
  * termination reasons and gauge anchoring (effective_fixed_mask, optimizer.cpp:24-43) as the
  * reference. poses12 (num_poses × 12) is updated in place unless the solve aborts; fixed (may be
  * NULL) marks user-fixed poses; updates (may be NULL) carries each pose's

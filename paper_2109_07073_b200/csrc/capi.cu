@@ -38,6 +38,24 @@ int cuda_fail(cudaError_t err, const char* what) {
   return err == cudaErrorMemoryAllocation ? VGICP_E_OUT_OF_MEMORY : VGICP_E_CUDA;
 }
 
+int api_exception() noexcept {
+  try {
+    throw;
+  } catch (const std::bad_alloc&) {
+    g_error = "host allocation failed";
+    return VGICP_E_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    try {
+      g_error = std::string("internal error: ") + e.what();
+    } catch (...) {
+    }
+    return VGICP_E_CUDA;
+  } catch (...) {
+    g_error = "internal error";
+    return VGICP_E_CUDA;
+  }
+}
+
 namespace {
 
 constexpr double kKeyBiasD = 1048576.0;
@@ -175,7 +193,7 @@ const char* vgicp_last_error(void) { return g_error.c_str(); }
 
 const char* vgicp_version(void) { return "vgicp_b200 0.1 (sm_100a)"; }
 
-int vgicp_device_count(int* count) {
+int vgicp_device_count(int* count) try {
   if (!count) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
   int n = 0;
   const cudaError_t e = cudaGetDeviceCount(&n);
@@ -185,9 +203,11 @@ int vgicp_device_count(int* count) {
   }
   *count = n;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_ctx_create(int device, void* stream, vgicp_ctx* out) {
+int vgicp_ctx_create(int device, void* stream, vgicp_ctx* out) try {
   if (!out) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
   *out = nullptr;
   int n = 0;
@@ -215,9 +235,11 @@ int vgicp_ctx_create(int device, void* stream, vgicp_ctx* out) {
   }
   *out = ctx.release();
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_ctx_destroy(vgicp_ctx ctx) {
+int vgicp_ctx_destroy(vgicp_ctx ctx) try {
   if (!ctx) return VGICP_OK;
   DeviceGuard g(ctx->device);
   cudaStreamSynchronize(ctx->stream);
@@ -227,25 +249,33 @@ int vgicp_ctx_destroy(vgicp_ctx ctx) {
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_ctx_stream(vgicp_ctx ctx, void** stream) {
+int vgicp_ctx_stream(vgicp_ctx ctx, void** stream) try {
   if (!ctx || !stream) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *stream = ctx->stream;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_ctx_synchronize(vgicp_ctx ctx) {
+int vgicp_ctx_synchronize(vgicp_ctx ctx) try {
   if (!ctx) return fail(VGICP_E_INVALID_ARGUMENT, "null context");
   DeviceGuard g(ctx->device);
   VG_CUDA(cudaStreamSynchronize(ctx->stream));
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_ctx_launch_count(vgicp_ctx ctx, uint64_t* launches) {
+int vgicp_ctx_launch_count(vgicp_ctx ctx, uint64_t* launches) try {
   if (!ctx || !launches) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *launches = ctx->launches;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 // ------------------------------------------------------------------------------------ clouds
@@ -316,8 +346,10 @@ static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov
   return VGICP_OK;
 }
 
-int vgicp_cloud_upload(vgicp_ctx ctx, const float* xyz, const float* cov6, size_t n, vgicp_cloud* out) {
+int vgicp_cloud_upload(vgicp_ctx ctx, const float* xyz, const float* cov6, size_t n, vgicp_cloud* out) try {
   return cloud_upload_packed(ctx, xyz, cov6, n, out);
+} catch (...) {
+  return api_exception();
 }
 
 static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const double* d_cov9, size_t n, bool keep64,
@@ -328,7 +360,7 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
 // unchanged; anything else (submap clouds: transform_cloud + voxel_downsample output,
 // pipeline.cpp:100-111) is kept in float64 as well, so keys / correspondences / overlap hits and map
 // statistics built from it are those of the reference's double arithmetic.
-int vgicp_cloud_upload_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, vgicp_cloud* out) {
+int vgicp_cloud_upload_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, vgicp_cloud* out) try {
   if (!ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   if (n > 0 && !xyz) return fail(VGICP_E_INVALID_ARGUMENT, "null point array");
@@ -361,29 +393,39 @@ int vgicp_cloud_upload_f64(vgicp_ctx ctx, const double* xyz, const double* cov9,
   VG_CUDA(cudaMemcpyAsync(d_xyz, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   if (cov9) VG_CUDA(cudaMemcpyAsync(d_cov, cov9, n * 9 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   return cloud_from_device_f64(ctx, d_xyz, d_cov, n, true, out);  // synchronises before returning
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_cloud_is_f64(vgicp_cloud cloud, int* f64) {
+int vgicp_cloud_is_f64(vgicp_cloud cloud, int* f64) try {
   if (!cloud || !f64) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *f64 = cloud->f64 ? 1 : 0;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_cloud_size(vgicp_cloud cloud, size_t* n) {
+int vgicp_cloud_size(vgicp_cloud cloud, size_t* n) try {
   if (!cloud || !n) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *n = cloud->n;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_cloud_has_covariances(vgicp_cloud cloud, int* has) {
+int vgicp_cloud_has_covariances(vgicp_cloud cloud, int* has) try {
   if (!cloud || !has) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *has = cloud->has_cov ? 1 : 0;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_cloud_destroy(vgicp_cloud cloud) {
+int vgicp_cloud_destroy(vgicp_cloud cloud) try {
   release(cloud);
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 // ------------------------------------------------------------------------------------ voxel maps
@@ -438,7 +480,7 @@ static int build_occupancy(vgicp_ctx ctx, vgicp_map* maps, int m, const VoxelSta
 }
 
 int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* resolutions, int m,
-                               vgicp_map* out) {
+                               vgicp_map* out) try {
   if (!ctx || !out || (m > 0 && (!clouds || !resolutions))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (m <= 0) return VGICP_OK;
   for (int k = 0; k < m; ++k) out[k] = nullptr;
@@ -461,6 +503,8 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
                                 resolutions[k], 1.0 / resolutions[k]};
   }
   return build_segments(ctx, segs, out);
+} catch (...) {
+  return api_exception();
 }
 
 // Batched build core: segments are float32 device clouds or fp64 device arrays (BuildSeg).
@@ -674,13 +718,15 @@ static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map*
   return VGICP_OK;
 }
 
-int vgicp_voxelmap_build(vgicp_ctx ctx, vgicp_cloud cloud, double resolution, vgicp_map* out) {
+int vgicp_voxelmap_build(vgicp_ctx ctx, vgicp_cloud cloud, double resolution, vgicp_map* out) try {
   if (!out) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
   return vgicp_voxelmap_build_batch(ctx, &cloud, &resolution, 1, out);
+} catch (...) {
+  return api_exception();
 }
 
 int vgicp_voxelmap_build_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, double resolution,
-                             vgicp_map* out) {
+                             vgicp_map* out) try {
   if (!ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   // GaussianVoxelMap ctor validation order (voxelmap.cpp:67-72)
@@ -700,10 +746,12 @@ int vgicp_voxelmap_build_f64(vgicp_ctx ctx, const double* xyz, const double* cov
   const int rc = build_segments(ctx, segs, out);
   VG_CUDA(cudaStreamSynchronize(ctx->stream));
   return rc;
+} catch (...) {
+  return api_exception();
 }
 
 int vgicp_transform_cloud(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, const double pose[12],
-                          double* out_xyz, double* out_cov9) {
+                          double* out_xyz, double* out_cov9) try {
   if (!ctx || !pose || (n > 0 && (!xyz || !out_xyz))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (n == 0) return VGICP_OK;
   const bool cov = cov9 && out_cov9;
@@ -726,6 +774,8 @@ int vgicp_transform_cloud(vgicp_ctx ctx, const double* xyz, const double* cov9, 
   if (cov) VG_CUDA(cudaMemcpyAsync(out_cov9, d_cout, n * 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaStreamSynchronize(s));
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 // Device cloud (same layout as cloud_upload_packed) from float64 device arrays (d_cov9 may be null:
@@ -796,7 +846,7 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
 
 int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* poses12, int m,
                        double downsample_resolution, double map_resolution, vgicp_map* out_downsampled,
-                       vgicp_cloud* out_cloud, vgicp_map* out_map) {
+                       vgicp_cloud* out_cloud, vgicp_map* out_map) try {
   if (!ctx || !out_map || (m > 0 && (!frames || !poses12))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out_map = nullptr;
   if (out_downsampled) *out_downsampled = nullptr;
@@ -890,32 +940,42 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
   else release(ds);
   *out_map = mp;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_voxelmap_destroy(vgicp_map map) {
+int vgicp_voxelmap_destroy(vgicp_map map) try {
   release(map);
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_voxelmap_size(vgicp_map map, size_t* voxels) {
+int vgicp_voxelmap_size(vgicp_map map, size_t* voxels) try {
   if (!map || !voxels) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *voxels = map->voxels;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_voxelmap_resolution(vgicp_map map, double* resolution) {
+int vgicp_voxelmap_resolution(vgicp_map map, double* resolution) try {
   if (!map || !resolution) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *resolution = map->res;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_voxelmap_total_points(vgicp_map map, size_t* total) {
+int vgicp_voxelmap_total_points(vgicp_map map, size_t* total) try {
   if (!map || !total) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *total = map->total_points;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_voxelmap_export(vgicp_map map, uint64_t* keys, int32_t* counts, double* means, double* covs) {
+int vgicp_voxelmap_export(vgicp_map map, uint64_t* keys, int32_t* counts, double* means, double* covs) try {
   if (!map) return fail(VGICP_E_INVALID_ARGUMENT, "null map");
   DeviceGuard g(map->ctx->device);
   cudaStream_t s = map->ctx->stream;
@@ -927,9 +987,11 @@ int vgicp_voxelmap_export(vgicp_map map, uint64_t* keys, int32_t* counts, double
   if (covs) VG_CUDA(cudaMemcpyAsync(covs, map->cov64, sizeof(double) * 9 * V, cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaStreamSynchronize(s));
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_voxelmap_lookup(vgicp_map map, const double* points, size_t n, uint64_t* keys_out) {
+int vgicp_voxelmap_lookup(vgicp_map map, const double* points, size_t n, uint64_t* keys_out) try {
   if (!map || (n > 0 && (!points || !keys_out))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (n == 0) return VGICP_OK;
   vgicp_ctx ctx = map->ctx;
@@ -945,11 +1007,15 @@ int vgicp_voxelmap_lookup(vgicp_map map, const double* points, size_t n, uint64_
   VG_CUDA(cudaMemcpyAsync(keys_out, d_keys, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
   VG_CUDA(cudaStreamSynchronize(ctx->stream));
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_voxel_key(double resolution, const double point[3], uint64_t* key) {
+int vgicp_voxel_key(double resolution, const double point[3], uint64_t* key) try {
   if (!point || !key) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   return host_voxel_key(resolution, point, key);
+} catch (...) {
+  return api_exception();
 }
 
 // ------------------------------------------------------------------------------------ overlap
@@ -1005,7 +1071,7 @@ static void fill_overlap_item(OverlapItem& it, const vgicp_cloud_s* c, const dou
 }
 
 int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* poses12, const vgicp_map* maps,
-                        int m, uint64_t* hits) {
+                        int m, uint64_t* hits) try {
   if (!ctx || (m > 0 && (!clouds || !poses12 || !maps || !hits)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (m <= 0) return VGICP_OK;
@@ -1090,10 +1156,12 @@ int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* 
     std::fprintf(stderr, "[vgicp] overlap batch: %d probes (%d live), cull+order %.3f ms, pack %.3f ms, gpu+sync %.3f ms\n",
                  m, ml, t_items, t_pack - t_items, ms_since(t_start) - t_pack);
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 // ------------------------------------------------------------------------------- map sets
-int vgicp_mapset_create(vgicp_ctx ctx, const vgicp_map* maps, int m, vgicp_mapset* out) {
+int vgicp_mapset_create(vgicp_ctx ctx, const vgicp_map* maps, int m, vgicp_mapset* out) try {
   if (!ctx || !out || (m > 0 && !maps) || m < 0) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   auto set = std::make_unique<vgicp_mapset_s>();
@@ -1129,9 +1197,11 @@ int vgicp_mapset_create(vgicp_ctx ctx, const vgicp_map* maps, int m, vgicp_mapse
   }
   *out = set.release();
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_mapset_destroy(vgicp_mapset set) {
+int vgicp_mapset_destroy(vgicp_mapset set) try {
   if (!set) return VGICP_OK;
   {
     DeviceGuard g(set->ctx->device);
@@ -1141,9 +1211,11 @@ int vgicp_mapset_destroy(vgicp_mapset set) {
   for (auto mp : set->maps) release(mp);
   delete set;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_overlap_mapset(vgicp_ctx ctx, vgicp_cloud cloud, const double* rel12, vgicp_mapset set, uint64_t* hits) {
+int vgicp_overlap_mapset(vgicp_ctx ctx, vgicp_cloud cloud, const double* rel12, vgicp_mapset set, uint64_t* hits) try {
   if (!ctx || !cloud || !set || (!set->maps.empty() && (!rel12 || !hits)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (cloud->ctx != ctx || set->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "handle of another context");
@@ -1175,14 +1247,18 @@ int vgicp_overlap_mapset(vgicp_ctx ctx, vgicp_cloud cloud, const double* rel12, 
   VG_CUDA(cudaStreamSynchronize(s));
   std::memcpy(hits, h, sizeof(uint64_t) * m);
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_overlap_rate(vgicp_ctx ctx, vgicp_cloud cloud, const double pose_rel[12], vgicp_map map, double* rate) {
+int vgicp_overlap_rate(vgicp_ctx ctx, vgicp_cloud cloud, const double pose_rel[12], vgicp_map map, double* rate) try {
   if (!rate || !cloud || !map || !pose_rel) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   uint64_t hits = 0;
   if (int rc = vgicp_overlap_batch(ctx, &cloud, pose_rel, &map, 1, &hits)) return rc;
   *rate = static_cast<double>(hits) / static_cast<double>(cloud->n);  // voxelmap.cpp:134
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 // ------------------------------------------------------------------------------------ graphs
@@ -1192,7 +1268,7 @@ static int factor_launches(const vgicp_graph_s* g) {
 }
 
 int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses, int chunk,
-                       vgicp_graph* out) {
+                       vgicp_graph* out) try {
   if (!ctx || !out || (num_factors > 0 && !factors)) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   if (num_factors < 0 || num_poses < 0) return fail(VGICP_E_INVALID_ARGUMENT, "negative size");
@@ -1279,7 +1355,7 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   const size_t o_i = carve(sizeof(WorkItem) * ni);
   const size_t o_p = carve(sizeof(double) * kPartialStride * kFactorWarps * ni);  // one partial per warp
   const size_t o_pi = carve(sizeof(int) * kFactorWarps * ni);
-  const size_t o_c = carve(sizeof(unsigned) * nf);
+  const size_t o_c = carve(sizeof(unsigned long long) * nf);
   const size_t o_pose = carve(sizeof(double) * 12 * std::max(num_poses, 1));
   const size_t o_out = carve(sizeof(double) * VGICP_LINEARIZED_DOUBLES * nf);
   const size_t o_oi = carve(sizeof(int) * nf);
@@ -1290,7 +1366,7 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   gr->d_items = reinterpret_cast<WorkItem*>(b + o_i);
   gr->d_partials = reinterpret_cast<double*>(b + o_p);
   gr->d_part_inl = reinterpret_cast<int*>(b + o_pi);
-  gr->d_counters = reinterpret_cast<unsigned*>(b + o_c);
+  gr->d_counters = reinterpret_cast<unsigned long long*>(b + o_c);
   gr->d_poses = reinterpret_cast<double*>(b + o_pose);
   gr->d_out = reinterpret_cast<double*>(b + o_out);
   gr->d_out_inl = reinterpret_cast<int*>(b + o_oi);
@@ -1306,7 +1382,7 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
     step(cudaMemcpyAsync(gr->d_items, items.data(), sizeof(WorkItem) * items.size(), cudaMemcpyHostToDevice, s),
          "upload items");
   }
-  step(cudaMemsetAsync(gr->d_counters, 0, sizeof(unsigned) * nf, s), "zero counters");
+  step(cudaMemsetAsync(gr->d_counters, 0, sizeof(unsigned long long) * nf, s), "zero counters");
   step(cudaStreamSynchronize(s), "graph create");
   if (rc != VGICP_OK) {
     dfree(ctx, gr->block);
@@ -1322,9 +1398,11 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   }
   *out = gr.release();
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_graph_destroy(vgicp_graph graph) {
+int vgicp_graph_destroy(vgicp_graph graph) try {
   if (!graph) return VGICP_OK;
   {
     DeviceGuard g(graph->ctx->device);
@@ -1337,38 +1415,48 @@ int vgicp_graph_destroy(vgicp_graph graph) {
   for (auto m : graph->maps) release(m);
   delete graph;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_graph_num_factors(vgicp_graph graph, int* n) {
+int vgicp_graph_num_factors(vgicp_graph graph, int* n) try {
   if (!graph || !n) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *n = graph->num_factors;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_graph_num_points(vgicp_graph graph, uint64_t* points) {
+int vgicp_graph_num_points(vgicp_graph graph, uint64_t* points) try {
   if (!graph || !points) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *points = graph->num_points;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, double* d_out, int32_t* d_inliers) {
+int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, double* d_out, int32_t* d_inliers) try {
   if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_out || !d_inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   DeviceGuard g(graph->ctx->device);
   VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, d_poses12, graph->d_partials,
-                        graph->d_part_inl, graph->d_counters, d_out, d_inliers, graph->ctx->stream));
+                        graph->d_part_inl, graph->d_counters, graph->next_epoch(), d_out, d_inliers, graph->ctx->stream));
   graph->ctx->launches += factor_launches(graph);
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, double* d_errors, int32_t* d_inliers) {
+int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, double* d_errors, int32_t* d_inliers) try {
   if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_errors || !d_inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   DeviceGuard g(graph->ctx->device);
   VG_CUDA(launch_factor(false, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, d_poses12, graph->d_partials,
-                        graph->d_part_inl, graph->d_counters, d_errors, d_inliers, graph->ctx->stream));
+                        graph->d_part_inl, graph->d_counters, graph->next_epoch(), d_errors, d_inliers, graph->ctx->stream));
   graph->ctx->launches += factor_launches(graph);
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 // Device-visible alias of `p` when it is page-locked host memory (cudaHostAlloc / cudaHostRegister /
@@ -1416,7 +1504,7 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
   double* d_res = zero_copy ? m_res : (linearize ? graph->d_out : graph->d_err);
   int32_t* d_inl = zero_copy ? m_inl : graph->d_out_inl;
   VG_CUDA(launch_factor(linearize, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, graph->d_poses,
-                        graph->d_partials, graph->d_part_inl, graph->d_counters, d_res, d_inl, s));
+                        graph->d_partials, graph->d_part_inl, graph->d_counters, graph->next_epoch(), d_res, d_inl, s));
   ctx->launches += factor_launches(graph);
   if (!zero_copy) {
     VG_CUDA(cudaMemcpyAsync(h_res, d_res, res_bytes, cudaMemcpyDeviceToHost, s));
@@ -1430,17 +1518,21 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
   return VGICP_OK;
 }
 
-int vgicp_graph_linearize(vgicp_graph graph, const double* poses12, double* out, int32_t* inliers) {
+int vgicp_graph_linearize(vgicp_graph graph, const double* poses12, double* out, int32_t* inliers) try {
   return graph_run_host(graph, true, poses12, out, inliers);
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_graph_evaluate(vgicp_graph graph, const double* poses12, double* errors, int32_t* inliers) {
+int vgicp_graph_evaluate(vgicp_graph graph, const double* poses12, double* errors, int32_t* inliers) try {
   return graph_run_host(graph, false, poses12, errors, inliers);
+} catch (...) {
+  return api_exception();
 }
 
 // ------------------------------------------------------------------------------------ assembly
 int vgicp_graph_assembly_plan(vgicp_graph graph, const uint8_t* fixed, int* num_slots, int* num_pairs,
-                              int32_t* pairs) {
+                              int32_t* pairs) try {
   if (!graph || !num_slots || !num_pairs || (graph->num_poses > 0 && !fixed))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   const int n = graph->num_poses;
@@ -1513,10 +1605,12 @@ int vgicp_graph_assembly_plan(vgicp_graph graph, const uint8_t* fixed, int* num_
   *num_slots = active;
   *num_pairs = P;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, double* diag, double* offdiag,
-                                    double* rhs) {
+                                    double* rhs) try {
   if (!graph || !poses12) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (!graph->plan) return fail(VGICP_E_INVALID_ARGUMENT, "no assembly plan (call vgicp_graph_assembly_plan)");
   const int S = graph->num_slots, P = graph->num_pairs, O = S + P;
@@ -1533,7 +1627,7 @@ int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, do
   VG_CUDA(cudaMemcpyAsync(graph->d_poses, h, pose_bytes, cudaMemcpyHostToDevice, s));
   if (graph->num_items > 0) {
     VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, graph->d_poses, graph->d_partials,
-                          graph->d_part_inl, graph->d_counters, graph->d_out, graph->d_out_inl, s));
+                          graph->d_part_inl, graph->d_counters, graph->next_epoch(), graph->d_out, graph->d_out_inl, s));
     ctx->launches += factor_launches(graph);
   } else if (graph->num_factors > 0) {
     VG_CUDA(cudaMemsetAsync(graph->d_out, 0, sizeof(double) * VGICP_LINEARIZED_DOUBLES * graph->num_factors, s));
@@ -1546,9 +1640,11 @@ int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, do
   if (P > 0) std::memcpy(offdiag, h_asm + 36 * static_cast<size_t>(S), sizeof(double) * 36 * P);
   if (S > 0) std::memcpy(rhs, h_asm + 36 * static_cast<size_t>(O), sizeof(double) * 6 * S);
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_poses12, double* d_assembled) {
+int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_poses12, double* d_assembled) try {
   if (!graph || !d_poses12) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (!graph->plan) return fail(VGICP_E_INVALID_ARGUMENT, "no assembly plan (call vgicp_graph_assembly_plan)");
   const int S = graph->num_slots, O = S + graph->num_pairs;
@@ -1557,7 +1653,7 @@ int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_po
   cudaStream_t s = graph->ctx->stream;
   if (graph->num_items > 0) {
     VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, d_poses12, graph->d_partials,
-                          graph->d_part_inl, graph->d_counters, graph->d_out, graph->d_out_inl, s));
+                          graph->d_part_inl, graph->d_counters, graph->next_epoch(), graph->d_out, graph->d_out_inl, s));
     graph->ctx->launches += factor_launches(graph);
   } else if (graph->num_factors > 0) {
     VG_CUDA(cudaMemsetAsync(graph->d_out, 0, sizeof(double) * VGICP_LINEARIZED_DOUBLES * graph->num_factors, s));
@@ -1565,9 +1661,11 @@ int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_po
   VG_CUDA(launch_assemble(graph->d_out_ptr, graph->d_contrib, S, O, graph->d_out, d_assembled, s));
   graph->ctx->launches += O > 0 ? 1 : 0;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
-int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* inliers) {
+int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* inliers) try {
   if (!graph || (graph->num_factors > 0 && (!errors || !inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   const int nf = graph->num_factors;
@@ -1587,10 +1685,12 @@ int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* in
   std::memcpy(errors, h_err, err_bytes);
   std::memcpy(inliers, h_inl, sizeof(int32_t) * nf);
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 // ------------------------------------------------------------------------------- band solver
-int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported) {
+int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported) try {
   if (!graph || !bandwidth || !supported) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (!graph->plan) return fail(VGICP_E_INVALID_ARGUMENT, "no assembly plan (call vgicp_graph_assembly_plan)");
   vgicp_ctx ctx = graph->ctx;
@@ -1640,6 +1740,8 @@ int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported) {
                             cudaMemcpyHostToDevice, s));
   VG_CUDA(cudaStreamSynchronize(s));
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 // One launch solving the damped system for `count` (1 or 2) damping values, one cluster each.
@@ -1684,13 +1786,17 @@ static int solve_damped_n(vgicp_graph graph, const double* d_assembled, const do
   return VGICP_OK;
 }
 
-int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, double lambda, double* x, int* solved) {
+int vgicp_graph_solve_damped(vgicp_graph graph, const double* d_assembled, double lambda, double* x, int* solved) try {
   return solve_damped_n(graph, d_assembled, &lambda, 1, x, solved);
+} catch (...) {
+  return api_exception();
 }
 
 int vgicp_graph_solve_damped_pair(vgicp_graph graph, const double* d_assembled, const double* lambdas, double* x,
-                                  int* solved) {
+                                  int* solved) try {
   return solve_damped_n(graph, d_assembled, lambdas, 2, x, solved);
+} catch (...) {
+  return api_exception();
 }
 
 // Single-factor entry points: a one-factor graph over poses {target, source}.
@@ -1715,18 +1821,22 @@ static int single_factor(vgicp_ctx ctx, const vgicp_factor_desc* factor, const d
 
 int vgicp_linearize_matching_cost(vgicp_ctx ctx, const vgicp_factor_desc* factor, const double T_target[12],
                                   const double T_source[12], double out[VGICP_LINEARIZED_DOUBLES],
-                                  int32_t* inliers) {
+                                  int32_t* inliers) try {
   return single_factor(ctx, factor, T_target, T_source, true, out, inliers);
+} catch (...) {
+  return api_exception();
 }
 
 int vgicp_evaluate_matching_cost(vgicp_ctx ctx, const vgicp_factor_desc* factor, const double T_target[12],
-                                 const double T_source[12], double* error, int32_t* inliers) {
+                                 const double T_source[12], double* error, int32_t* inliers) try {
   return single_factor(ctx, factor, T_target, T_source, false, error, inliers);
+} catch (...) {
+  return api_exception();
 }
 
 int vgicp_gicp_error(vgicp_ctx ctx, const double source_mean[3], const double source_cov[9],
                      const double target_mean[3], const double target_cov[9], const double T[12], double* error,
-                     double residual[3], double information[9], int* valid) {
+                     double residual[3], double information[9], int* valid) try {
   if (!ctx || !source_mean || !source_cov || !target_mean || !target_cov || !T || !error || !residual ||
       !information || !valid)
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
@@ -1751,6 +1861,8 @@ int vgicp_gicp_error(vgicp_ctx ctx, const double source_mean[3], const double so
   std::memcpy(information, h + 44, 9 * sizeof(double));
   *valid = h[53] != 0.0 ? 1 : 0;
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 // ------------------------------------------------------------------------------------ preprocessing
@@ -1792,7 +1904,7 @@ static void parallel_copies(const std::vector<std::tuple<void*, const void*, siz
 
 
 int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, const size_t* n, int m, int k,
-                                     double plane_epsilon, float* const* cov6) {
+                                     double plane_epsilon, float* const* cov6) try {
   if (!ctx || (m > 0 && (!xyz || !n || !cov6))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (m <= 0) return VGICP_OK;
   // estimate_covariances validation (point_cloud.cpp:47-53)
@@ -1930,11 +2042,15 @@ int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, con
   }
   stage("stage-out");
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }
 
 int vgicp_estimate_covariances(vgicp_ctx ctx, const float* xyz, size_t n, int k, double plane_epsilon,
-                               float* cov6) {
+                               float* cov6) try {
   return vgicp_estimate_covariances_batch(ctx, &xyz, &n, 1, k, plane_epsilon, &cov6);
+} catch (...) {
+  return api_exception();
 }
 
 }  // extern "C"

@@ -7,9 +7,9 @@
 //         H_tt = AᵀΩA with A = [-[q]x | I] as Q = -[q]xΩ[q]x (6), P = [q]xΩ (9), Ω (6),
 //         b_t = [-q×Ωe; -Ωe] (6), error eᵀΩe  -> 28 fp32 accumulators + int inliers
 //   near-singular M (fp32 Sylvester test without margin) -> the oracle-identical fp64 LDLT path
-// Reduction without float atomics: per-thread fp32 -> warp shuffle in fp64 ->
-// shared-memory CTA sum in fp64 -> one partial per CTA; the last CTA of a factor (integer
-// arrival counter) sums the factor's partials in item order and expands, in fp64,
+// Reduction without float atomics: per-thread fp32 -> warp butterfly in fp64 -> one
+// partial per warp; the last warp of a factor (integer arrival counter, tagged with the launch's
+// epoch) sums the factor's partials in (item, warp) order and expands, in fp64,
 //   H_ts = -H_tt·Ad,  H_ss = AdᵀH_tt·Ad,  b_s = -Adᵀb_t,  Ad = Ad(T_ts) (se3.cpp:107-113),
 // which is exact algebra because B = -A·Ad(T_ts). Fixed orders everywhere => deterministic.
 #include <atomic>
@@ -207,8 +207,8 @@ template <bool kLinearize>
 __device__ __forceinline__ void finish_factor(const float* acc, int inl, int lane, size_t gw, int parts,
                                               const WorkItem& w, const FactorDev* __restrict__ fp, const double* T,
                                               double* ws, double* __restrict__ partials, int* __restrict__ part_inl,
-                                              unsigned* __restrict__ counters, double* __restrict__ out,
-                                              int* __restrict__ out_inl) {
+                                              unsigned long long* __restrict__ counters, unsigned epoch,
+                                              double* __restrict__ out, int* __restrict__ out_inl) {
   constexpr int kAcc = kLinearize ? kLinAcc : 1;
   // ---- warp reduction: fp64 butterfly over the 32 lanes, fixed order; one partial per warp
   //      (no float atomics). Once per ~2,500 points per warp, so its cost is negligible. ----
@@ -223,8 +223,22 @@ __device__ __forceinline__ void finish_factor(const float* acc, int inl, int lan
   if (lane == 0) part_inl[gw] = inl;
   __threadfence();
   __syncwarp();
+  // Arrival counter = (epoch << 32) | arrivals; the electing warp clears it. A counter still tagged
+  // with an older epoch (left behind by an aborted launch) restarts at 1, so a later launch never
+  // inherits stale arrivals.
   unsigned last = 0;
-  if (lane == 0) last = (atomicAdd(&counters[w.factor], 1u) + 1u == (unsigned)(fp->item_count * parts)) ? 1u : 0u;
+  if (lane == 0) {
+    unsigned long long* c = &counters[w.factor];
+    unsigned long long seen = *reinterpret_cast<volatile unsigned long long*>(c), want;
+    for (;;) {
+      want = (static_cast<unsigned>(seen >> 32) == epoch) ? seen + 1ull
+                                                          : ((static_cast<unsigned long long>(epoch) << 32) | 1ull);
+      const unsigned long long prev = atomicCAS(c, seen, want);
+      if (prev == seen) break;
+      seen = prev;
+    }
+    last = (static_cast<unsigned>(want) == static_cast<unsigned>(fp->item_count * parts)) ? 1u : 0u;
+  }
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
   __threadfence();
@@ -245,7 +259,7 @@ __device__ __forceinline__ void finish_factor(const float* acc, int inl, int lan
   int tinl = 0;
   if (lane == 0) {
     for (int g = 0; g < gc; ++g) tinl += __ldcg(&part_inl[gb + g]);
-    counters[w.factor] = 0u;  // ready for the next launch
+    counters[w.factor] = 0ull;  // clean for the next launch (also one replaying the same epoch)
   }
   __syncwarp();
 
@@ -362,7 +376,7 @@ template <bool kLinearize, bool kRank, bool kF64>
 __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
     const FactorDev* __restrict__ factors, const WorkItem* __restrict__ items, int item_base,
     const double* __restrict__ poses, double* __restrict__ partials, int* __restrict__ part_inl,
-    unsigned* __restrict__ counters, double* __restrict__ out, int* __restrict__ out_inl) {
+    unsigned long long* __restrict__ counters, unsigned epoch, double* __restrict__ out, int* __restrict__ out_inl) {
   constexpr int kAcc = kLinearize ? kLinAcc : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   FactorSmem& sm = *reinterpret_cast<FactorSmem*>(smem_raw);
@@ -575,7 +589,8 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
   __syncwarp();  // this warp is done with its ring (no CTA-wide barrier after the prologue)
 
   finish_factor<kLinearize>(acc, inl, lane, (size_t)(item_base + blockIdx.x) * kWarps + warp, kWarps, w, fp, sm.T,
-                            reinterpret_cast<double*>(&sm.u.ring[warp][0]), partials, part_inl, counters, out, out_inl);
+                            reinterpret_cast<double*>(&sm.u.ring[warp][0]), partials, part_inl, counters, epoch, out,
+                            out_inl);
 }
 
 // gicp_error (factors.cpp:75-88) in fp64, bit-identical to the oracle.
@@ -645,8 +660,8 @@ cudaError_t launch_assemble(const int* out_ptr, const int* contrib, int num_slot
 }
 
 cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, const WorkItem* items, int num_items,
-                          int f64_begin, const double* poses, double* partials, int* part_inl, unsigned* counters,
-                          double* out, int* out_inl, cudaStream_t s) {
+                          int f64_begin, const double* poses, double* partials, int* part_inl,
+                          unsigned long long* counters, unsigned epoch, double* out, int* out_inl, cudaStream_t s) {
   if (num_items <= 0) return cudaSuccess;
   constexpr size_t kSmem = sizeof(FactorSmem);
   // the > 48 KB shared-memory opt-in is a per-device function attribute: set it once per device
@@ -673,7 +688,7 @@ cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, c
   auto go = [&](auto kernel, int base, int count) {
     if (count > 0)
       kernel<<<count, kFactorThreads, kSmem, s>>>(factors, items + base, base, poses, partials, part_inl, counters,
-                                                  out, out_inl);
+                                                  epoch, out, out_inl);
   };
   auto both = [&](auto k32, auto k64) {
     go(k32, 0, f64_begin);

@@ -17,6 +17,10 @@ namespace vgicp {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t err, const char* what);
+// Every extern "C" entry point is a function-try-block ending in `catch (...) { return
+// api_exception(); }`: no C++ exception crosses the ABI (std::bad_alloc -> VGICP_E_OUT_OF_MEMORY,
+// anything else -> VGICP_E_CUDA with the message in vgicp_last_error()).
+int api_exception() noexcept;
 
 #define VG_CUDA(call)                                  \
   do {                                                 \
@@ -184,8 +188,8 @@ cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsi
 // items [0, f64_begin) belong to float32-exact source clouds, [f64_begin, num_items) to float64 clouds
 // (one launch each; the float64 launch transforms the exact float64 means)
 cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, const WorkItem* items, int num_items,
-                          int f64_begin, const double* poses, double* partials, int* part_inl, unsigned* counters,
-                          double* out, int* out_inl, cudaStream_t s);
+                          int f64_begin, const double* poses, double* partials, int* part_inl,
+                          unsigned long long* counters, unsigned epoch, double* out, int* out_inl, cudaStream_t s);
 cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s);
 // overlap probes grouped by cloud: chunk = (first item, count <= kOverlapMapsPerChunk) of items that
 // share one cloud; each thread loads its points once and probes the chunk's maps
@@ -347,7 +351,9 @@ struct vgicp_graph_s {
   vgicp::WorkItem* d_items = nullptr;
   double* d_partials = nullptr;
   int* d_part_inl = nullptr;
-  unsigned* d_counters = nullptr;
+  unsigned long long* d_counters = nullptr;  // per-factor arrival counters, tagged with the launch epoch
+  unsigned epoch = 0;                         // last factor-pass epoch (never 0 after the first pass)
+  unsigned next_epoch() { return epoch = (epoch == 0xFFFFFFFFu ? 1u : epoch + 1u); }
   double* d_poses = nullptr;
   double* d_out = nullptr;
   int* d_out_inl = nullptr;

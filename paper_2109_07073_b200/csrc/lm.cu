@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "internal.h"
@@ -80,61 +81,6 @@ void orthonormalize(double* T) {
   std::memcpy(T, X, sizeof(X));
 }
 
-// Dense Cholesky solve of the damped slot-order system on the host (fallback when the band
-// solver does not support the envelope). Returns false when not positive definite.
-bool host_solve(int S, int P, const std::vector<int32_t>& pairs, const double* asmb, double lam,
-                std::vector<double>& x) {
-  const int m = 6 * S;
-  std::vector<double> A(static_cast<size_t>(m) * m, 0.0), b(m);
-  const double* diag = asmb;
-  const double* off = asmb + static_cast<size_t>(S) * 36;
-  const double* rhs = asmb + static_cast<size_t>(S + P) * 36;
-  for (int s = 0; s < S; ++s)
-    for (int r = 0; r < 6; ++r) {
-      for (int c = 0; c < 6; ++c) A[static_cast<size_t>(6 * s + r) * m + 6 * s + c] = diag[36 * s + 6 * r + c];
-      b[6 * s + r] = rhs[6 * s + r];
-    }
-  for (int q = 0; q < P; ++q) {
-    const int a = pairs[2 * q], bb = pairs[2 * q + 1];
-    for (int r = 0; r < 6; ++r)
-      for (int c = 0; c < 6; ++c) {
-        const double v = off[36 * q + 6 * r + c];
-        A[static_cast<size_t>(6 * a + r) * m + 6 * bb + c] = v;
-        A[static_cast<size_t>(6 * bb + c) * m + 6 * a + r] = v;
-      }
-  }
-  for (int k = 0; k < m; ++k) {
-    double& d = A[static_cast<size_t>(k) * m + k];
-    d = d + lam * std::max(d, 1e-10);
-  }
-  for (int j = 0; j < m; ++j) {  // in-place lower Cholesky
-    double* Lj = &A[static_cast<size_t>(j) * m];
-    double d = Lj[j];
-    for (int k = 0; k < j; ++k) d -= Lj[k] * Lj[k];
-    if (!(d > 0.0)) return false;
-    const double l = std::sqrt(d);
-    Lj[j] = l;
-    for (int i = j + 1; i < m; ++i) {
-      double* Li = &A[static_cast<size_t>(i) * m];
-      double v = Li[j];
-      for (int k = 0; k < j; ++k) v -= Li[k] * Lj[k];
-      Li[j] = v / l;
-    }
-  }
-  x.assign(m, 0.0);
-  for (int i = 0; i < m; ++i) {
-    double v = b[i];
-    for (int k = 0; k < i; ++k) v -= A[static_cast<size_t>(i) * m + k] * x[k];
-    x[i] = v / A[static_cast<size_t>(i) * m + i];
-  }
-  for (int i = m - 1; i >= 0; --i) {
-    double v = x[i];
-    for (int k = i + 1; k < m; ++k) v -= A[static_cast<size_t>(k) * m + i] * x[k];
-    x[i] = v / A[static_cast<size_t>(i) * m + i];
-  }
-  return true;
-}
-
 struct DeviceScope {  // selects the context's device for the call, restores the caller's
   int prev = -1;
   explicit DeviceScope(int dev) {
@@ -157,11 +103,13 @@ struct PoolBuffer {  // stream-ordered device temporary (the context's pool)
   }
 };
 
-// Banded Cholesky solve in slot order (narrow systems, e.g. odometry chains): the damped system in
-// lower band storage of half-bandwidth w (scalars), LAPACK dpbtrf/dpbtrs arithmetic without
-// blocking. O(m·w²); false when not positive definite.
+// Banded Cholesky solve of the damped system on the host: lower band storage of half-bandwidth w
+// (scalars), LAPACK dpbtrf/dpbtrs arithmetic without blocking, O(m·w²); false when not positive
+// definite. pos[slot] = the slot's block position in the factored order: the identity (slot order)
+// for narrow systems such as odometry chains, the reverse Cuthill-McKee order of the solver plan
+// when the envelope is too wide for the device band kernel. x is returned in slot order.
 bool host_band_solve(int S, int P, const std::vector<int32_t>& pairs, const double* asmb, double lam, int w,
-                     std::vector<double>& x) {
+                     const std::vector<int>& pos, std::vector<double>& x) {
   const int m = 6 * S;
   const int W = w + 1;
   std::vector<double> B(static_cast<size_t>(m) * W, 0.0), b(m);  // B[i*W + (i - j)] = A(i, j), i >= j
@@ -171,13 +119,18 @@ bool host_band_solve(int S, int P, const std::vector<int32_t>& pairs, const doub
   const double* rhs = asmb + static_cast<size_t>(S + P) * 36;
   for (int s = 0; s < S; ++s)
     for (int r = 0; r < 6; ++r) {
-      for (int c = 0; c <= r; ++c) at(6 * s + r, 6 * s + c) = diag[36 * s + 6 * r + c];
-      b[6 * s + r] = rhs[6 * s + r];
+      const int p = pos[s];
+      for (int c = 0; c <= r; ++c) at(6 * p + r, 6 * p + c) = diag[36 * s + 6 * r + c];
+      b[6 * p + r] = rhs[6 * s + r];
     }
-  for (int q = 0; q < P; ++q) {  // (row a, col b) block, a > b
-    const int a = pairs[2 * q], bb = pairs[2 * q + 1];
+  for (int q = 0; q < P; ++q) {  // (row a, col b) block of the slot-order system
+    const int pa = pos[pairs[2 * q]], pb = pos[pairs[2 * q + 1]];
     for (int r = 0; r < 6; ++r)
-      for (int c = 0; c < 6; ++c) at(6 * a + r, 6 * bb + c) = off[36 * q + 6 * r + c];
+      for (int c = 0; c < 6; ++c) {
+        const double v = off[36 * q + 6 * r + c];
+        if (pa > pb) at(6 * pa + r, 6 * pb + c) = v;
+        else at(6 * pb + c, 6 * pa + r) = v;  // the transposed block below the diagonal
+      }
   }
   for (int k = 0; k < m; ++k) {
     double& d = at(k, k);
@@ -209,6 +162,10 @@ bool host_band_solve(int S, int P, const std::vector<int32_t>& pairs, const doub
     for (int k = i + 1; k <= std::min(m - 1, i + w); ++k) v -= at(k, i) * x[k];
     x[i] = v / at(i, i);
   }
+  std::vector<double> xs(m);
+  for (int s = 0; s < S; ++s)
+    for (int r = 0; r < 6; ++r) xs[6 * s + r] = x[6 * pos[s] + r];
+  x.swap(xs);
   return true;
 }
 
@@ -224,7 +181,7 @@ using namespace vgicp;
 
 extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const uint8_t* fixed_in, int32_t* updates,
                                     const vgicp_lm_settings* settings_in, vgicp_lm_report* report, double* trace,
-                                    int max_trace, double* iteration_seconds) {
+                                    int max_trace, double* iteration_seconds) try {
   if (!graph || !report || (graph->num_poses > 0 && !poses12)) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   const auto t_start = std::chrono::steady_clock::now();
   auto seconds = [&]() { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(); };
@@ -270,9 +227,21 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
   // chain runs over every slot.
   int slot_bw = 0;
   for (int q = 0; q < P; ++q) slot_bw = std::max(slot_bw, pairs[2 * q] - pairs[2 * q + 1]);
-  const int host_w = 6 * slot_bw + 5;
+  int host_w = 6 * slot_bw + 5;
   const bool host_band = S > 0 && static_cast<double>(6 * S) * host_w * host_w <= 2.0e6 &&
                          !std::getenv("VGICP_LM_NO_HOST_BAND");  // (test switch: force the device solver)
+  std::vector<int> host_pos(S);
+  for (int sl = 0; sl < S; ++sl) host_pos[sl] = sl;  // slot order
+  if (S > 0 && !band && !host_band) {
+    // the envelope is too wide for one cluster: host band solve in the plan's reverse Cuthill-McKee
+    // order (O(m·w²) time, O(m·w) memory), refused beyond ~4 GB of band storage
+    const BandPlanHost hp = make_band_plan(S, P, pairs.data());
+    for (int k = 0; k < S; ++k) host_pos[hp.perm[k]] = k;
+    host_w = 6 * hp.bw + 5;
+    if (static_cast<double>(6 * S) * (host_w + 1) > 5.0e8)
+      return fail(VGICP_E_OUT_OF_MEMORY, "reduced system too wide for the host band fallback (" + std::to_string(S) +
+                                             " slots, block bandwidth " + std::to_string(hp.bw) + ")");
+  }
 
   vgicp_ctx ctx = graph->ctx;
   DeviceScope g(ctx->device);
@@ -341,8 +310,7 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
     host_asm.resize(asm_doubles);
     VG_CUDA(cudaMemcpyAsync(host_asm.data(), d_asm[which], sizeof(double) * asm_doubles, cudaMemcpyDeviceToHost, s));
     VG_CUDA(cudaStreamSynchronize(s));
-    *ok = host_band ? host_band_solve(S, P, pairs, host_asm.data(), lam, host_w, x)
-                    : host_solve(S, P, pairs, host_asm.data(), lam, x);
+    *ok = host_band_solve(S, P, pairs, host_asm.data(), lam, host_w, host_pos, x);
     return VGICP_OK;
   };
 
@@ -444,4 +412,6 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
   report->band_solver = band && !host_band;
   report->wall_time_seconds = seconds();
   return VGICP_OK;
+} catch (...) {
+  return api_exception();
 }

@@ -739,6 +739,15 @@ cudaError_t launch_band_solve(const BandDev& d, int C, const double* assembled, 
   cfg.blockDim = dim3(kSolveThreads);
   cfg.dynamicSmemBytes = band_smem_bytes(d.bw, C, d.S);
   cfg.stream = s;
+  // the > 48 KB opt-in is a per-function (per-device) attribute shared by every graph: set it for
+  // THIS launch's size (another graph's plan may have left a smaller limit behind)
+  if (const cudaError_t e = cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      e != cudaSuccess)
+    return e;
+  if (const cudaError_t e = cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(cfg.dynamicSmemBytes));
+      e != cudaSuccess)
+    return e;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;

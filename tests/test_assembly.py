@@ -267,6 +267,11 @@ def test_gpu_band_solver_pair_matches_single(V):
     bad = torch.from_numpy(a).cuda()
     x0, x1 = graph.solve_damped_pair(bad.data_ptr(), (0.0, 0.0))
     assert x0 is None and x1 is None
+    # mixed outcome (what the LM's pair cache relies on): instance 0 fails, the damping rescues
+    # instance 1 (-1e-3 + 1e8·max(-1e-3, 1e-10) > 0), whose x and status stay its own
+    x0, x1 = graph.solve_damped_pair(bad.data_ptr(), (0.0, 1e8))
+    assert x0 is None and x1 is not None
+    assert np.array_equal(x1, graph.solve_damped(bad.data_ptr(), 1e8))
     good = graph.solve_damped_pair(d_asm.data_ptr(), (1e-4, 1e-3))
     assert good[0] is not None and np.array_equal(good[1], graph.solve_damped(d_asm.data_ptr(), 1e-3))
 
@@ -331,16 +336,17 @@ def _lm_graph(V, loop, seed=78, nframes=8):
 
 @gpu
 @pytest.mark.parametrize("loop", [False, True])
-@pytest.mark.parametrize("solver", ["host_band", "gpu_band", "host_dense"])
+@pytest.mark.parametrize("solver", ["host_band", "gpu_band", "host_rcm_band"])
 def test_gpu_native_lm_matches_python_lm(V, monkeypatch, loop, solver):
     """vgicp_graph_optimize (the LM loop in the library) takes the reference loop's decisions: same
     accepted / rejected sequence, λ schedule, termination reason; errors and poses to 1e-9 (the
-    solvers differ in rounding: host band / device band / host dense Cholesky vs the Python LM's)."""
+    solvers differ in rounding: host band in slot order / device band / host band in RCM order — the
+    fallback when the envelope is too wide for the device kernel — vs the Python LM's)."""
     from paper_2109_07073_b200 import optimizer as LM
 
     if solver != "host_band":
         monkeypatch.setenv("VGICP_LM_NO_HOST_BAND", "1")
-    if solver == "host_dense":
+    if solver == "host_rcm_band":
         monkeypatch.setenv("VGICP_NO_BAND_SOLVER", "1")
     graph, poses = _lm_graph(V, loop)
     p_py, r_py = LM.optimize(graph, poses, band_solve=False)
