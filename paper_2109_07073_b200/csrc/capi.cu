@@ -146,6 +146,7 @@ void release(vgicp_map m) {
     dfree(m->ctx, m->cold);
     dfree(m->ctx, m->table);
     dfree(m->ctx, m->occ_mem);
+    release(m->src);
     delete m;
   }
 }
@@ -479,6 +480,303 @@ static int build_occupancy(vgicp_ctx ctx, vgicp_map* maps, int m, const VoxelSta
   return VGICP_OK;
 }
 
+// ---- hand-written build of float32 clouds (build.cu) ----------------------------------------
+// Occupied voxel box of a float32 cloud at resolution r, exactly: floor(fl(x / r)) is monotone in x,
+// so the box of the finite bounding box is the box of the voxels (what the build would find). false
+// when the cloud has no finite point; out_of_range when a bound lies beyond ±2^20 voxels.
+static bool fast_box(const vgicp_cloud_s* c, double r, int cmin[3], int cmax[3], bool* out_of_range) {
+  *out_of_range = false;
+  if (c->lo[0] > c->hi[0]) return false;
+  for (int a = 0; a < 3; ++a) {
+    const double l = std::floor(static_cast<double>(c->lo[a]) / r), h = std::floor(static_cast<double>(c->hi[a]) / r);
+    if (!(l >= -kKeyBiasD && h < kKeyBiasD)) {
+      *out_of_range = true;
+      return false;
+    }
+    cmin[a] = static_cast<int>(l);
+    cmax[a] = static_cast<int>(h);
+  }
+  return true;
+}
+
+static size_t fast_words(const int cmin[3], const int cmax[3]) {
+  size_t words = 1;
+  for (int a = 0; a < 3; ++a) words *= static_cast<size_t>((cmax[a] - cmin[a] + 1 + 3) / 4);
+  return words;
+}
+
+// Export buffers of a single-map rebuild (rank order).
+struct FastExport {
+  unsigned long long* keys = nullptr;
+  int* counts = nullptr;
+  double* mean64 = nullptr;
+  double* cov9 = nullptr;
+  unsigned V = 0;
+  void* mem = nullptr;
+};
+
+// Builds maps of float32 clouds clouds[k] at res[k] with the hand-written kernels: zero + mark,
+// rank, (sync: V per map, range errors), order, accumulate. With `exp` (one map): export mode — the
+// key-ordered statistics are written to device buffers in rank order (exp->mem, freed by the caller).
+static int build_fast(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* res, int m, vgicp_map* out,
+                      FastExport* exp) {
+  cudaStream_t s = ctx->stream;
+  std::vector<FastBuildJob> jobs(m);
+  std::vector<vgicp_map> maps(m, nullptr);
+  auto cleanup = [&]() {
+    for (auto* mp : maps) release(mp);
+  };
+  unsigned long long total = 0;
+  unsigned max_n = 0, max_words = 0;
+  for (int k = 0; k < m; ++k) {
+    const vgicp_cloud c = clouds[k];
+    int cmin[3], cmax[3];
+    bool oor = false;
+    if (!fast_box(c, res[k], cmin, cmax, &oor)) {
+      cleanup();
+      return fail(oor || c->n > 0 ? VGICP_E_OUT_OF_RANGE : VGICP_E_INVALID_ARGUMENT,
+                  "point beyond the +-2^20 voxel-per-axis range limit");
+    }
+    auto* mp = new vgicp_map_s();
+    maps[k] = mp;
+    mp->ctx = ctx;
+    mp->res = res[k];
+    mp->inv_res = 1.0 / res[k];
+    mp->total_points = c->n;
+    mp->fast = true;
+    mp->cov_stride = 6;
+    c->refs.fetch_add(1);
+    mp->src = c;
+    for (int a = 0; a < 3; ++a) mp->cmin[a] = cmin[a], mp->cmax[a] = cmax[a];
+    const size_t words = fast_words(cmin, cmax);
+    VG_CUDA(dmalloc(ctx, &mp->occ_mem, sizeof(OccWord) * words));
+    OccDev& o = mp->occ;
+    o.occ = static_cast<const OccWord*>(mp->occ_mem);
+    o.kx0 = static_cast<unsigned>(cmin[0] + (1 << 20));
+    o.ky0 = static_cast<unsigned>(cmin[1] + (1 << 20));
+    o.kz0 = static_cast<unsigned>(cmin[2] + (1 << 20));
+    o.ex = static_cast<unsigned>(cmax[0] - cmin[0] + 1);
+    o.ey = static_cast<unsigned>(cmax[1] - cmin[1] + 1);
+    o.ez = static_cast<unsigned>(cmax[2] - cmin[2] + 1);
+    o.nby = (o.ey + 3) / 4, o.nbz = (o.ez + 3) / 4;
+    FastBuildJob& j = jobs[k];
+    j = FastBuildJob{};
+    j.pa = c->pa, j.pb = c->pb, j.pc = c->pc;
+    j.n = static_cast<unsigned>(c->n);
+    j.pt_off = static_cast<unsigned>(total);
+    j.vx_off = static_cast<unsigned>(total + k);  // V + 1 <= n + 1 offsets per map
+    j.res = mp->res, j.inv_res = mp->inv_res;
+    j.kx0 = o.kx0, j.ky0 = o.ky0, j.kz0 = o.kz0, j.ex = o.ex, j.ey = o.ey, j.ez = o.ez, j.nby = o.nby, j.nbz = o.nbz;
+    j.words = static_cast<unsigned>(words);
+    j.occ = static_cast<OccWord*>(mp->occ_mem);
+    total += c->n;
+    max_n = std::max(max_n, j.n);
+    max_words = std::max(max_words, j.words);
+  }
+  if (total + m >= (1ull << 32)) {
+    cleanup();
+    return fail(VGICP_E_INVALID_ARGUMENT, "batched build exceeds 2^32 points");
+  }
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t o_jobs = carve(sizeof(FastBuildJob) * m);
+  const size_t o_idx = carve(sizeof(int) * m);
+  const size_t o_err = carve(sizeof(int) * m);
+  const size_t o_vc = carve(sizeof(unsigned) * m);
+  const size_t o_code = carve(sizeof(unsigned) * total);
+  const size_t o_list = carve(sizeof(unsigned) * total);
+  const size_t o_offs = carve(sizeof(unsigned) * (total + m));
+  const size_t o_gcnt = carve(sizeof(unsigned) * (total + m));
+  if (int rc = ensure_scratch(ctx, off)) {
+    cleanup();
+    return rc;
+  }
+  char* sb = static_cast<char*>(ctx->scratch);
+  auto* d_jobs = reinterpret_cast<FastBuildJob*>(sb + o_jobs);
+  auto* d_idx = reinterpret_cast<int*>(sb + o_idx);
+  auto* d_err = reinterpret_cast<int*>(sb + o_err);
+  auto* d_vc = reinterpret_cast<unsigned*>(sb + o_vc);
+  auto* d_code = reinterpret_cast<unsigned*>(sb + o_code);
+  auto* d_list = reinterpret_cast<unsigned*>(sb + o_list);
+  auto* d_offs = reinterpret_cast<unsigned*>(sb + o_offs);
+  auto* d_gcnt = reinterpret_cast<unsigned*>(sb + o_gcnt);
+  int rc = VGICP_OK;
+  auto step = [&](cudaError_t e, const char* what) {
+    if (rc == VGICP_OK && e != cudaSuccess) rc = cuda_fail(e, what);
+  };
+  step(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(FastBuildJob) * m, cudaMemcpyHostToDevice, s), "build jobs");
+  step(cudaMemsetAsync(d_err, 0, sizeof(int) * m, s), "build flags");
+  if (rc == VGICP_OK) step(launch_fast_mark(d_jobs, m, max_n, max_words, d_code, d_err, s), "build mark");
+  if (rc == VGICP_OK) step(launch_fast_rank(d_jobs, m, d_vc, s), "build rank");
+  std::vector<int> herr(m);
+  std::vector<unsigned> hv(m);
+  step(cudaMemcpyAsync(herr.data(), d_err, sizeof(int) * m, cudaMemcpyDeviceToHost, s), "build flags");
+  step(cudaMemcpyAsync(hv.data(), d_vc, sizeof(unsigned) * m, cudaMemcpyDeviceToHost, s), "build counts");
+  step(cudaStreamSynchronize(s), "build rank");
+  if (rc != VGICP_OK) {
+    cleanup();
+    return rc;
+  }
+  ctx->launches += 3;  // zero, mark, rank
+  for (int k = 0; k < m; ++k)
+    if (herr[k]) {
+      cleanup();
+      return fail(VGICP_E_OUT_OF_RANGE, "point beyond the +-2^20 voxel-per-axis range limit");
+    }
+  // per-map voxel arrays: ra | rb | cov6 (rank order)
+  unsigned max_v = 0, smem_v = fast_order_smem_voxels(ctx->device);
+  std::vector<int> in_smem, in_global;
+  for (int k = 0; k < m; ++k) {
+    vgicp_map mp = maps[k];
+    const size_t V = hv[k];
+    mp->voxels = V;
+    const size_t b_ra = align_up(sizeof(SlotStatsA) * V, 256), b_rb = align_up(sizeof(SlotStatsB) * V, 256);
+    if (const cudaError_t e = dmalloc(ctx, &mp->cold, std::max<size_t>(b_ra + b_rb + sizeof(double) * 6 * V, 256));
+        e != cudaSuccess) {
+      cleanup();
+      return cuda_fail(e, "cudaMallocAsync(voxel map)");
+    }
+    char* b = static_cast<char*>(mp->cold);
+    mp->ra = reinterpret_cast<SlotStatsA*>(b);
+    mp->rb = reinterpret_cast<SlotStatsB*>(b + b_ra);
+    mp->cov64 = reinterpret_cast<double*>(b + b_ra + b_rb);
+    jobs[k].V = static_cast<unsigned>(V);
+    jobs[k].ra = mp->ra, jobs[k].rb = mp->rb, jobs[k].cov6 = mp->cov64;
+    max_v = std::max(max_v, jobs[k].V);
+    (V <= smem_v ? in_smem : in_global).push_back(k);
+  }
+  if (exp) {  // single map: key-ordered statistics in rank order
+    const size_t V = hv[0];
+    exp->V = static_cast<unsigned>(V);
+    VG_CUDA(dmalloc(ctx, &exp->mem, std::max<size_t>(V * (8 + 4 + 24 + 72) + 1024, 256)));
+    char* b = static_cast<char*>(exp->mem);
+    exp->keys = reinterpret_cast<unsigned long long*>(b);
+    exp->counts = reinterpret_cast<int*>(b + align_up(8 * V, 256));
+    exp->mean64 = reinterpret_cast<double*>(b + align_up(8 * V, 256) + align_up(4 * V, 256));
+    exp->cov9 = exp->mean64 + 3 * V;
+    jobs[0].keys = exp->keys, jobs[0].counts = exp->counts, jobs[0].mean64 = exp->mean64, jobs[0].cov9 = exp->cov9;
+  }
+  std::vector<int> order(in_smem);
+  order.insert(order.end(), in_global.begin(), in_global.end());
+  unsigned smem_max = 0;
+  for (int k : in_smem) smem_max = std::max(smem_max, jobs[k].V);
+  step(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(FastBuildJob) * m, cudaMemcpyHostToDevice, s), "build jobs");
+  step(cudaMemcpyAsync(d_idx, order.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s), "build jobs");
+  if (rc == VGICP_OK && !in_smem.empty())
+    step(launch_fast_order(d_jobs, d_idx, static_cast<int>(in_smem.size()), std::max(1u, smem_max), d_code, d_list,
+                           d_offs, d_gcnt, s),
+         "build order");
+  if (rc == VGICP_OK && !in_global.empty())
+    step(launch_fast_order(d_jobs, d_idx + in_smem.size(), static_cast<int>(in_global.size()), 0u, d_code, d_list,
+                           d_offs, d_gcnt, s),
+         "build order (global cursors)");
+  if (rc == VGICP_OK) step(launch_fast_accumulate(d_jobs, m, max_v, d_list, d_offs, exp != nullptr, s), "build accumulate");
+  step(cudaStreamSynchronize(s), "build");
+  if (rc != VGICP_OK) {
+    cleanup();
+    return rc;
+  }
+  ctx->launches += (in_smem.empty() ? 0 : 1) + (in_global.empty() ? 0 : 1) + 1;
+  for (int k = 0; k < m; ++k) out[k] = maps[k];
+  return VGICP_OK;
+}
+
+// The key-ordered statistics of a hand-built map (export, on-demand hash table): the same kernels
+// rerun on the map's source cloud in export mode, then ordered by key on the host.
+static int fast_export(vgicp_map map, std::vector<uint64_t>* keys, std::vector<int32_t>* counts,
+                       std::vector<double>* means, std::vector<double>* covs, std::vector<unsigned>* rank_of_sorted) {
+  vgicp_ctx ctx = map->ctx;
+  vgicp_map tmp = nullptr;
+  FastExport ex;
+  const double r = map->res;
+  if (int rc = build_fast(ctx, &map->src, &r, 1, &tmp, &ex)) {
+    dfree(ctx, ex.mem);
+    return rc;
+  }
+  const size_t V = ex.V;
+  std::vector<uint64_t> k(V);
+  std::vector<int32_t> c(V);
+  std::vector<double> mu(3 * V), cv(9 * V);
+  cudaStream_t s = ctx->stream;
+  int rc = VGICP_OK;
+  if (V > 0) {
+    cudaError_t e = cudaMemcpyAsync(k.data(), ex.keys, 8 * V, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && counts) e = cudaMemcpyAsync(c.data(), ex.counts, 4 * V, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && means) e = cudaMemcpyAsync(mu.data(), ex.mean64, 24 * V, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && covs) e = cudaMemcpyAsync(cv.data(), ex.cov9, 72 * V, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "voxel map export");
+  }
+  dfree(ctx, ex.mem);
+  release(tmp);
+  if (rc != VGICP_OK) return rc;
+  std::vector<unsigned> perm(V);
+  for (size_t v = 0; v < V; ++v) perm[v] = static_cast<unsigned>(v);
+  std::sort(perm.begin(), perm.end(), [&](unsigned a, unsigned b) { return k[a] < k[b]; });
+  if (keys) {
+    keys->resize(V);
+    for (size_t q = 0; q < V; ++q) (*keys)[q] = k[perm[q]];
+  }
+  if (counts) {
+    counts->resize(V);
+    for (size_t q = 0; q < V; ++q) (*counts)[q] = c[perm[q]];
+  }
+  if (means) {
+    means->resize(3 * V);
+    for (size_t q = 0; q < V; ++q) std::memcpy(&(*means)[3 * q], &mu[3 * perm[q]], 24);
+  }
+  if (covs) {
+    covs->resize(9 * V);
+    for (size_t q = 0; q < V; ++q) std::memcpy(&(*covs)[9 * q], &cv[9 * perm[q]], 72);
+  }
+  if (rank_of_sorted) rank_of_sorted->swap(perm);
+  return VGICP_OK;
+}
+
+// Hash table of a hand-built map, on demand (lookups, hash-probe measurement modes): keys in rank
+// order, cuckoo insertion (rebuilt with twice the buckets on overflow), slot <- rank statistics.
+static int ensure_table(vgicp_map mp) {
+  if (mp->table || mp->voxels == 0 || !mp->fast) return VGICP_OK;
+  std::vector<uint64_t> sorted;
+  std::vector<unsigned> rank;
+  if (int rc = fast_export(mp, &sorted, nullptr, nullptr, nullptr, &rank)) return rc;
+  const size_t V = mp->voxels;
+  std::vector<unsigned long long> by_rank(V);
+  for (size_t q = 0; q < V; ++q) by_rank[rank[q]] = sorted[q];
+  vgicp_ctx ctx = mp->ctx;
+  cudaStream_t s = ctx->stream;
+  DevBuf buf(ctx);
+  VG_CUDA(buf.alloc(align_up(8 * V, 256) + 256 + sizeof(InsertJob)));
+  auto* d_keys = static_cast<unsigned long long*>(buf.p);
+  auto* d_ovf = reinterpret_cast<int*>(static_cast<char*>(buf.p) + align_up(8 * V, 256));
+  auto* d_job = reinterpret_cast<InsertJob*>(static_cast<char*>(buf.p) + align_up(8 * V, 256) + 256);
+  VG_CUDA(cudaMemcpyAsync(d_keys, by_rank.data(), 8 * V, cudaMemcpyHostToDevice, s));
+  unsigned buckets = std::max(16u, next_pow2((2ull * V + kBucket - 1) / kBucket));  // load <= 0.5
+  for (int attempt = 0;; ++attempt) {
+    if (attempt > 8) return fail(VGICP_E_CUDA, "voxel hash table insertion did not converge");
+    if (int rc = alloc_table(mp, buckets, s)) return rc;
+    InsertJob job{mp->tkeys, mp->sa, mp->sb, d_keys, 0u, static_cast<unsigned>(V), mp->shift, 0u};
+    int ovf = 0;
+    VG_CUDA(cudaMemcpyAsync(d_job, &job, sizeof(job), cudaMemcpyHostToDevice, s));
+    VG_CUDA(cudaMemsetAsync(d_ovf, 0, sizeof(int), s));
+    VG_CUDA(launch_build_insert(d_job, 1, static_cast<unsigned>(V), d_ovf, s));
+    VG_CUDA(cudaMemcpyAsync(&ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
+    VG_CUDA(cudaStreamSynchronize(s));
+    ctx->launches += 1;
+    if (!ovf) {
+      VG_CUDA(launch_place_rank(d_job, static_cast<unsigned>(V), mp->ra, mp->rb, s));
+      VG_CUDA(cudaStreamSynchronize(s));
+      ctx->launches += 1;
+      return VGICP_OK;
+    }
+    buckets *= 2;
+  }
+}
+
 int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* resolutions, int m,
                                vgicp_map* out) try {
   if (!ctx || !out || (m > 0 && (!clouds || !resolutions))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
@@ -492,6 +790,42 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
       return fail(VGICP_E_INVALID_ARGUMENT, "voxel map construction requires per-point covariances");
   }
   DeviceGuard g(ctx->device);
+  // float32 clouds whose occupied box has a bitmap of <= kOccMaxWords records take the hand-written
+  // build (build.cu); float64 clouds and sprawling boxes the sort-based one below
+  // (VGICP_SORTED_BUILD=1 forces the latter: measurement / cross-check switch)
+  const bool sorted_only = std::getenv("VGICP_SORTED_BUILD") != nullptr;
+  std::vector<int> fast_idx, slow_idx;
+  for (int k = 0; k < m; ++k) {
+    const vgicp_cloud c = clouds[k];
+    int cmin[3], cmax[3];
+    bool oor = false;
+    const bool boxed = fast_box(c, resolutions[k], cmin, cmax, &oor);
+    if (oor) return fail(VGICP_E_OUT_OF_RANGE, "point beyond the +-2^20 voxel-per-axis range limit");
+    const bool fast = !sorted_only && !c->f64 && boxed && fast_words(cmin, cmax) <= kOccMaxWords;
+    (fast ? fast_idx : slow_idx).push_back(k);
+  }
+  if (!fast_idx.empty()) {
+    std::vector<vgicp_cloud> fc;
+    std::vector<double> fr;
+    for (int k : fast_idx) fc.push_back(clouds[k]), fr.push_back(resolutions[k]);
+    std::vector<vgicp_map> fm(fast_idx.size(), nullptr);
+    if (int rc = build_fast(ctx, fc.data(), fr.data(), static_cast<int>(fc.size()), fm.data(), nullptr)) return rc;
+    if (slow_idx.empty()) {
+      for (size_t q = 0; q < fast_idx.size(); ++q) out[fast_idx[q]] = fm[q];
+      return VGICP_OK;
+    }
+    std::vector<vgicp_cloud> sc;
+    std::vector<double> sr;
+    for (int k : slow_idx) sc.push_back(clouds[k]), sr.push_back(resolutions[k]);
+    std::vector<vgicp_map> sm(slow_idx.size(), nullptr);
+    if (int rc = vgicp_voxelmap_build_batch(ctx, sc.data(), sr.data(), static_cast<int>(sc.size()), sm.data())) {
+      for (auto* mp : fm) release(mp);
+      return rc;
+    }
+    for (size_t q = 0; q < fast_idx.size(); ++q) out[fast_idx[q]] = fm[q];
+    for (size_t q = 0; q < slow_idx.size(); ++q) out[slow_idx[q]] = sm[q];
+    return VGICP_OK;
+  }
   std::vector<BuildSeg> segs(m);
   for (int k = 0; k < m; ++k) {
     const vgicp_cloud c = clouds[k];
@@ -981,6 +1315,19 @@ int vgicp_voxelmap_export(vgicp_map map, uint64_t* keys, int32_t* counts, double
   cudaStream_t s = map->ctx->stream;
   const size_t V = map->voxels;
   if (V == 0) return VGICP_OK;
+  if (map->fast) {  // rank-numbered map: recompute the key-ordered statistics with the same kernels
+    std::vector<uint64_t> k;
+    std::vector<int32_t> c;
+    std::vector<double> mu, cv;
+    if (int rc = fast_export(map, keys ? &k : nullptr, counts ? &c : nullptr, means ? &mu : nullptr,
+                             covs ? &cv : nullptr, nullptr))
+      return rc;
+    if (keys) std::memcpy(keys, k.data(), sizeof(uint64_t) * V);
+    if (counts) std::memcpy(counts, c.data(), sizeof(int32_t) * V);
+    if (means) std::memcpy(means, mu.data(), sizeof(double) * 3 * V);
+    if (covs) std::memcpy(covs, cv.data(), sizeof(double) * 9 * V);
+    return VGICP_OK;
+  }
   if (keys) VG_CUDA(cudaMemcpyAsync(keys, map->keys, sizeof(uint64_t) * V, cudaMemcpyDeviceToHost, s));
   if (counts) VG_CUDA(cudaMemcpyAsync(counts, map->counts, sizeof(int32_t) * V, cudaMemcpyDeviceToHost, s));
   if (means) VG_CUDA(cudaMemcpyAsync(means, map->mean64, sizeof(double) * 3 * V, cudaMemcpyDeviceToHost, s));
@@ -996,6 +1343,7 @@ int vgicp_voxelmap_lookup(vgicp_map map, const double* points, size_t n, uint64_
   if (n == 0) return VGICP_OK;
   vgicp_ctx ctx = map->ctx;
   DeviceGuard g(ctx->device);
+  if (int rc = ensure_table(map)) return rc;
   const size_t bp = align_up(sizeof(double) * 3 * n, 256);
   if (int rc = ensure_scratch(ctx, bp + sizeof(uint64_t) * n)) return rc;
   char* sb = static_cast<char*>(ctx->scratch);
@@ -1313,6 +1661,9 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   // VGICP_NO_RANK=1 keeps the cuckoo-hash probes (measurement switch)
   bool rank = std::getenv("VGICP_NO_RANK") == nullptr;
   for (int f = 0; f < num_factors && rank; ++f) rank = factors[f].target->occ.occ != nullptr;
+  if (!rank)  // hash probes: hand-built maps get their table now
+    for (int f = 0; f < num_factors; ++f)
+      if (int rc = ensure_table(factors[f].target)) return rc;
   // items of float32-exact source clouds first, then those of float64 clouds (their own launch)
   int f64_begin = 0;
   for (int pass = 0; pass < 2; ++pass) {

@@ -36,10 +36,19 @@ __device__ __forceinline__ double relative_pose_entry(const double* Tt, const do
 }
 
 // Rare path: M near singular in fp32 -> recompute M and the LDLT decision in fp64 exactly as
-// the oracle (factors.cpp:38-46, :107) and return Omega as fp32.
+// the oracle (factors.cpp:38-46, :107) and return Omega as fp32. c = the voxel's fp64 covariance:
+// 9 entries (stride 9) or the 6 unique entries of an exactly symmetric one (stride 6).
 __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, float sxz, float syy, float syz,
-                                        float szz, const double* Ct, float* om) {
+                                        float szz, const double* c, unsigned stride, float* om) {
   const double Cs[9] = {sxx, sxy, sxz, sxy, syy, syz, sxz, syz, szz};
+  double Ct[9];
+  if (stride == 6) {
+    Ct[0] = c[0], Ct[1] = c[1], Ct[2] = c[2], Ct[3] = c[1], Ct[4] = c[3], Ct[5] = c[4], Ct[6] = c[2], Ct[7] = c[4],
+    Ct[8] = c[5];
+  } else {
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Ct[e] = c[e];
+  }
   double M[9], O[9];
   combined_cov_rn(T, Cs, Ct, M);
   if (!invert_covariance_rn(M, O)) return false;
@@ -150,7 +159,9 @@ __device__ __forceinline__ void hit_math(const float* Rf, const double* T, const
     o22 = a22 * inv;
   } else {
     float om[6];
-    if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.y), om)) return;
+    if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64 + (size_t)map.cov_stride * __float_as_int(v2.y),
+                    map.cov_stride, om))
+      return;
     o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
   }
   const float w0 = o00 * e0 + o01 * e1 + o02 * e2;

@@ -117,6 +117,47 @@ struct OccJob {
 cudaError_t launch_occ_build(const OccJob* jobs, int m, unsigned max_words, unsigned max_v, const VoxelStats* hot,
                              cudaStream_t s);
 
+struct InsertJob;
+// Hand-written build of one float32 cloud's map (build.cu). The occupied voxel box is known before
+// any device work (floor(p/r) is monotone, so the box of the cloud's finite bounding box IS the box
+// of its voxels), so the map's occupancy bitmap exists from the start: voxels are numbered by rank
+// (brick order), never sorted by key.
+struct FastBuildJob {
+  const float4* pa;  // float32 cloud, input order (x y z c_xx | c_xy c_xz c_yy c_yz | c_zz)
+  const float4* pb;
+  const float* pc;
+  unsigned n;        // points
+  unsigned V;        // voxels (known after the rank pass)
+  unsigned pt_off;   // first point of this map in the batch's per-point scratch
+  unsigned vx_off;   // first CSR offset of this map in the batch's per-voxel scratch (V + 1 entries)
+  double res, inv_res;
+  unsigned kx0, ky0, kz0;  // biased key coordinates of the box's lower corner
+  unsigned ex, ey, ez;     // box extent in voxels
+  unsigned nby, nbz, words;
+  OccWord* occ;            // the map's bitmap (words records)
+  SlotStatsA* ra;          // outputs by rank: voxel-local fp32 statistics ...
+  SlotStatsB* rb;          //   ... (c_zz, rank)
+  double* cov6;            //   ... and the fp64 covariance's 6 unique entries
+  unsigned long long* keys;  // export mode (else nullptr): packed key, count, fp64 mean and the 9-entry
+  int* counts;               //   covariance by rank
+  double* mean64;
+  double* cov9;
+};
+cudaError_t launch_fast_mark(const FastBuildJob* jobs, int m, unsigned max_n, unsigned max_words, unsigned* code,
+                             int* err, cudaStream_t s);
+cudaError_t launch_fast_rank(const FastBuildJob* jobs, int m, unsigned* vcount, cudaStream_t s);
+// count + scan + stable input-order scatter, one CTA per map; `idx` lists the jobs of this launch;
+// smem_v > 0: per-voxel cursors in shared memory for maps with V <= smem_v, else in `gcnt`
+cudaError_t launch_fast_order(const FastBuildJob* jobs, const int* idx, int count, unsigned smem_v, unsigned* code,
+                              unsigned* list, unsigned* offs, unsigned* gcnt, cudaStream_t s);
+cudaError_t launch_fast_accumulate(const FastBuildJob* jobs, int m, unsigned max_v, const unsigned* list,
+                                   const unsigned* offs, bool export_mode, cudaStream_t s);
+unsigned fast_order_smem_voxels(int device);
+// hash table of a rank-numbered map, built on demand (lookups, hash-probe measurement modes):
+// cuckoo insert of keys[rank], then each slot receives ra / rb of its rank
+cudaError_t launch_place_rank(const InsertJob* job, unsigned V, const SlotStatsA* ra, const SlotStatsB* rb,
+                              cudaStream_t s);
+
 struct BuildSeg {
   const float4* pa;           // float32 device cloud (input order) ...
   const float4* pb;
@@ -322,9 +363,16 @@ struct vgicp_map_s {
   vgicp::SlotStatsA* ra = nullptr;  // statistics by rank (brick order), for rank lookups
   vgicp::SlotStatsB* rb = nullptr;
   std::atomic<int> refs{1};
-  vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov64, res, inv_res, shift, 0u, occ}; }
+  // Maps of float32 clouds built by the hand-written path (build.cu): voxels numbered by rank only
+  // (ra / rb / cov64 with 6 entries per voxel, `cold` holds them), no key-ordered arrays and no hash
+  // table until one is needed (ensure_table); export recomputes the key-ordered statistics from `src`
+  // with the same kernels.
+  bool fast = false;
+  vgicp_cloud src = nullptr;  // the source cloud (kept alive: export / on-demand hash table)
+  unsigned cov_stride = 9;
+  vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov64, res, inv_res, shift, cov_stride, occ}; }
   // rank lookups: slot statistics replaced by the rank-ordered copies (requires occ)
-  vgicp::MapDev dev_rank() const { return vgicp::MapDev{tkeys, ra, rb, cov64, res, inv_res, shift, 0u, occ}; }
+  vgicp::MapDev dev_rank() const { return vgicp::MapDev{tkeys, ra, rb, cov64, res, inv_res, shift, cov_stride, occ}; }
 };
 
 struct vgicp_mapset_s {

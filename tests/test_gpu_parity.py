@@ -589,3 +589,66 @@ def test_graph_validation(ctx):
     g = V.FactorGraph(factors, 3)
     with pytest.raises(ValueError):
         g.linearize(poses[:2])
+
+
+# ------------------------------------------------------------------------------ hand-written build
+def _sorted_build(monkeypatch, clouds, res):
+    monkeypatch.setenv("VGICP_SORTED_BUILD", "1")
+    try:
+        return V.GaussianVoxelMap.build_batch(clouds, res)
+    finally:
+        monkeypatch.delenv("VGICP_SORTED_BUILD")
+
+
+def test_handwritten_build_equals_sorted_build(ctx, monkeypatch):
+    """The rank-numbered hand-written build (build.cu: bitmap + stable counting sort + Kahan) and the
+    sort-based build give bit-identical exports (keys, counts, fp64 means / covariances) and
+    bit-identical factor results, overlap hits and lookups — on a batch of mixed sizes and
+    resolutions, dense voxels (hundreds of points), and a map whose voxel count exceeds the
+    shared-memory cursor array (global-cursor variant)."""
+    rng = O.Rng(401)
+    clouds, res = [], []
+    for k in range(6):
+        means, covs = rng.gaussian_cloud(800 + 700 * k, 4.0 + 6 * k)
+        clouds.append(gpu_cloud(ctx, means, covs)[0])
+        res.append([0.25, 0.5, 1.0, 2.0, 0.7, 1.3][k])
+    dense = np.repeat(np.array([rng.vector(0.4) for _ in range(20)]), 150, axis=0)  # 150 points per voxel
+    dense = dense + np.random.default_rng(3).uniform(-0.01, 0.01, dense.shape)
+    clouds.append(gpu_cloud(ctx, dense, O.unit_covariances(len(dense)))[0])
+    res.append(1.0)
+    big = np.random.default_rng(4).uniform(-60, 60, size=(70000, 3))  # V ~ 70k > smem cursors
+    clouds.append(gpu_cloud(ctx, big, O.unit_covariances(len(big)))[0])
+    res.append(0.5)
+    fast = V.GaussianVoxelMap.build_batch(clouds, res)
+    slow = _sorted_build(monkeypatch, clouds, res)
+    for f, s in zip(fast, slow):
+        assert f.size() == s.size() and f.total_points() == s.total_points()
+        for x, y in zip(f.export(), s.export()):
+            assert np.array_equal(x, y)
+    # factors: target maps from each build, same sources / poses -> identical blocks
+    poses = np.stack([rng.random_pose(0.05, 0.5) for _ in range(len(clouds))])
+    def graph(maps):
+        fs = [V.MatchingCostFactor(k, k + 1, clouds[k + 1], maps[k]) for k in range(5)]
+        return V.FactorGraph(fs, len(clouds))
+    ra, ia = graph(fast).linearize_raw(poses)
+    rb, ib = graph(slow).linearize_raw(poses)
+    assert np.array_equal(ia, ib) and np.array_equal(ra, rb)
+    rels = [O.compose(O.inverse(poses[k]), poses[k + 1]) for k in range(5)]
+    assert np.array_equal(V.overlap_hits([clouds[k + 1] for k in range(5)], rels, fast[:5]),
+                          V.overlap_hits([clouds[k + 1] for k in range(5)], rels, slow[:5]))
+    probes = np.concatenate([big[:3000], big[:3000] + 0.3])
+    assert np.array_equal(fast[-1].lookup(probes), slow[-1].lookup(probes))  # on-demand hash table
+
+
+def test_handwritten_build_hash_mode_equals_rank_mode(ctx, monkeypatch):
+    """VGICP_NO_RANK=1 makes the factor kernels probe the on-demand cuckoo table of hand-built maps:
+    the same blocks as the rank lookups, bit for bit."""
+    rng = O.Rng(402)
+    clouds = [gpu_cloud(ctx, *rng.gaussian_cloud(3000, 10.0))[0] for _ in range(3)]
+    maps = V.GaussianVoxelMap.build_batch(clouds, [1.0, 1.0, 1.0])
+    poses = np.stack([rng.random_pose(0.05, 0.5) for _ in range(3)])
+    fs = [V.MatchingCostFactor(0, 1, clouds[1], maps[0]), V.MatchingCostFactor(1, 2, clouds[2], maps[1])]
+    ra, ia = V.FactorGraph(fs, 3).linearize_raw(poses)
+    monkeypatch.setenv("VGICP_NO_RANK", "1")
+    rb, ib = V.FactorGraph(fs, 3).linearize_raw(poses)
+    assert np.array_equal(ia, ib) and np.array_equal(ra, rb)
