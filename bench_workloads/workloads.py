@@ -135,7 +135,7 @@ def build_graph_workload(ctx, spec: S.SceneSpec, resolution: float = 1.0, max_li
     t0 = time.perf_counter()
     scans = make_scans(spec, threads=threads, ctx=ctx if gpu_covariances else None)
     t1 = time.perf_counter()
-    clouds = [PointCloud(m, c, ctx) for m, c in zip(scans.means, scans.cov6)]
+    clouds = PointCloud.upload_batch(scans.means, scans.cov6, ctx)
     maps = GaussianVoxelMap.build_batch(clouds, resolution)
     ctx.synchronize()
     t2 = time.perf_counter()
@@ -176,7 +176,7 @@ def build_c5_workload(ctx, spec: S.SceneSpec | None = None, max_links: int = 10,
     t0 = time.perf_counter()
     scans = make_scans(spec, ctx=ctx)
     t1 = time.perf_counter()
-    clouds = [PointCloud(m, c, ctx) for m, c in zip(scans.means, scans.cov6)]
+    clouds = PointCloud.upload_batch(scans.means, scans.cov6, ctx)
     maps = {r: GaussianVoxelMap.build_batch(clouds, r) for r in C5_RESOLUTIONS}
     ctx.synchronize()
     t2 = time.perf_counter()

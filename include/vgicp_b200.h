@@ -86,6 +86,10 @@ int vgicp_ctx_launch_count(vgicp_ctx ctx, uint64_t* launches);
 /* ---------------------------------------------------------------- point clouds (PointCloud,
  * include/vgicp/point_cloud.hpp:21-37). cov6 may be NULL for a raw cloud (overlap only). */
 int vgicp_cloud_upload(vgicp_ctx ctx, const float* xyz, const float* cov6, size_t n, vgicp_cloud* out);
+/* m clouds in one call (one staged copy, one launch per layout stage for the whole batch): out[k] equals
+ * vgicp_cloud_upload(xyz[k], cov6[k] (cov6 or cov6[k] may be NULL), n[k]). All-or-nothing. */
+int vgicp_cloud_upload_batch(vgicp_ctx ctx, const float* const* xyz, const float* const* cov6, const size_t* n, int m,
+                             vgicp_cloud* out);
 /* Reference layout: n×3 double means, n×9 double covariances (may be NULL). Float32-exact inputs
  * with symmetric covariances take the float32 layout; any other input (e.g. submap clouds, the output
  * of transform_cloud + voxel_downsample, pipeline.cpp:100-111) is a float64 cloud: its exact values

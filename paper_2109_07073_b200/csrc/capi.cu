@@ -353,6 +353,122 @@ int vgicp_cloud_upload(vgicp_ctx ctx, const float* xyz, const float* cov6, size_
   return api_exception();
 }
 
+static void parallel_copies(const std::vector<std::tuple<void*, const void*, size_t>>& copies);
+
+// m float32 clouds in one staged H2D and one launch per stage (bounding boxes + Morton codes, one
+// segmented stable radix sort, fill) instead of ~8 launches per cloud. Same layout as m single
+// uploads: the stable sort of the same codes is the same permutation.
+int vgicp_cloud_upload_batch(vgicp_ctx ctx, const float* const* xyz, const float* const* cov6, const size_t* n, int m,
+                             vgicp_cloud* out) try {
+  if (!ctx || (m > 0 && (!xyz || !n || !out))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (m <= 0) return VGICP_OK;
+  for (int k = 0; k < m; ++k) out[k] = nullptr;
+  unsigned long long total = 0;
+  unsigned max_n = 0;
+  for (int k = 0; k < m; ++k) {
+    if (n[k] > 0 && !xyz[k]) return fail(VGICP_E_INVALID_ARGUMENT, "null point array");
+    total += n[k];
+    max_n = std::max<unsigned>(max_n, static_cast<unsigned>(std::min<size_t>(n[k], UINT32_MAX)));
+  }
+  if (total >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "batch too large (>= 2^31 points)");
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->stream;
+  std::vector<vgicp_cloud> clouds(m, nullptr);
+  auto cleanup = [&]() {
+    for (auto* c : clouds) release(c);
+  };
+  std::vector<UploadSeg> segs(m);
+  unsigned long long off = 0;
+  for (int k = 0; k < m; ++k) {
+    auto* c = new vgicp_cloud_s();
+    clouds[k] = c;
+    c->ctx = ctx;
+    c->n = n[k];
+    c->has_cov = cov6 && cov6[k] && n[k] > 0;
+    const size_t na = align_up(n[k] * sizeof(float4), 256), nc = align_up(n[k] * sizeof(float), 256);
+    const size_t half = 2 * na + nc, nblk = (n[k] + kPointBlock - 1) / kPointBlock;
+    if (const cudaError_t e = dmalloc(ctx, &c->block, std::max<size_t>(half + nblk * sizeof(PointBlock), 256));
+        e != cudaSuccess) {
+      cleanup();
+      return cuda_fail(e, "cudaMallocAsync(cloud)");
+    }
+    char* base = static_cast<char*>(c->block);
+    c->pa = reinterpret_cast<float4*>(base);
+    c->pb = reinterpret_cast<float4*>(base + na);
+    c->pc = reinterpret_cast<float*>(base + 2 * na);
+    c->sblk = reinterpret_cast<PointBlock*>(base + half);
+    segs[k] = UploadSeg{nullptr, nullptr, static_cast<unsigned>(off), static_cast<unsigned>(n[k]), c->pa, c->pb, c->pc,
+                        c->sblk};
+    off += n[k];
+  }
+  if (total > 0) {
+    const size_t b_xyz = align_up(sizeof(float) * 3 * total, 256), b_cov = align_up(sizeof(float) * 6 * total, 256);
+    const size_t b_vec = align_up(sizeof(unsigned) * total, 256);
+    size_t sort_bytes = 0;
+    std::vector<int> seg_off(m + 1);
+    for (int k = 0; k < m; ++k) seg_off[k] = static_cast<int>(segs[k].offset);
+    seg_off[m] = static_cast<int>(total);
+    VG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, sort_bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                                     (const unsigned*)nullptr, (unsigned*)nullptr,
+                                                     static_cast<int>(total), m, (const int*)nullptr,
+                                                     (const int*)nullptr, 0, 30, s));
+    const size_t b_segs = align_up(sizeof(UploadSeg) * m, 256), b_box = align_up(sizeof(unsigned) * 6 * m, 256);
+    const size_t b_off = align_up(sizeof(int) * (m + 1), 256);
+    DevBuf tmp(ctx);
+    VG_CUDA(tmp.alloc(b_xyz + b_cov + 4 * b_vec + b_segs + b_box + b_off + sort_bytes));
+    char* t = static_cast<char*>(tmp.p);
+    auto* d_xyz = reinterpret_cast<float*>(t);
+    auto* d_cov = reinterpret_cast<float*>(t + b_xyz);
+    auto* codes = reinterpret_cast<unsigned*>(t + b_xyz + b_cov);
+    auto* idx = codes + b_vec / sizeof(unsigned);
+    auto* codes2 = idx + b_vec / sizeof(unsigned);
+    auto* perm = codes2 + b_vec / sizeof(unsigned);
+    auto* d_segs = reinterpret_cast<UploadSeg*>(t + b_xyz + b_cov + 4 * b_vec);
+    auto* d_box = reinterpret_cast<unsigned*>(t + b_xyz + b_cov + 4 * b_vec + b_segs);
+    auto* d_off = reinterpret_cast<int*>(t + b_xyz + b_cov + 4 * b_vec + b_segs + b_box);
+    void* temp = t + b_xyz + b_cov + 4 * b_vec + b_segs + b_box + b_off;
+    for (int k = 0; k < m; ++k) {
+      segs[k].xyz = d_xyz + 3 * static_cast<size_t>(segs[k].offset);
+      segs[k].cov6 = clouds[k]->has_cov ? d_cov + 6 * static_cast<size_t>(segs[k].offset) : nullptr;
+    }
+    if (int rc = ensure_pinned(ctx, b_xyz + b_cov)) {
+      cleanup();
+      return rc;
+    }
+    VG_CUDA(cudaStreamSynchronize(s));  // the pinned staging buffer is free
+    char* h = static_cast<char*>(ctx->pinned);
+    std::vector<std::tuple<void*, const void*, size_t>> cp;
+    for (int k = 0; k < m; ++k) {
+      if (n[k] == 0) continue;
+      cp.emplace_back(h + sizeof(float) * 3 * segs[k].offset, xyz[k], sizeof(float) * 3 * n[k]);
+      if (clouds[k]->has_cov) cp.emplace_back(h + b_xyz + sizeof(float) * 6 * segs[k].offset, cov6[k], sizeof(float) * 6 * n[k]);
+    }
+    parallel_copies(cp);
+    std::vector<unsigned> hbox(6 * m);
+    for (int k = 0; k < m; ++k)
+      for (int a = 0; a < 3; ++a) hbox[6 * k + a] = ~0u, hbox[6 * k + 3 + a] = 0u;
+    VG_CUDA(cudaMemcpyAsync(d_xyz, h, b_xyz + b_cov, cudaMemcpyHostToDevice, s));
+    VG_CUDA(cudaMemcpyAsync(d_segs, segs.data(), sizeof(UploadSeg) * m, cudaMemcpyHostToDevice, s));
+    VG_CUDA(cudaMemcpyAsync(d_box, hbox.data(), sizeof(unsigned) * 6 * m, cudaMemcpyHostToDevice, s));
+    VG_CUDA(cudaMemcpyAsync(d_off, seg_off.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice, s));
+    VG_CUDA(launch_upload_batch_prepare(d_segs, m, max_n, d_box, codes, idx, s));
+    VG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(temp, sort_bytes, codes, codes2, idx, perm, static_cast<int>(total),
+                                                     m, d_off, d_off + 1, 0, 30, s));
+    VG_CUDA(launch_upload_batch_fill(d_segs, m, max_n, perm, s));
+    ctx->launches += 4;  // bbox, morton, segmented sort (counted once), fill
+    VG_CUDA(cudaMemcpyAsync(hbox.data(), d_box, sizeof(unsigned) * 6 * m, cudaMemcpyDeviceToHost, s));
+    VG_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k < m; ++k)
+      if (hbox[6 * k] <= hbox[6 * k + 3])  // at least one finite point
+        for (int a = 0; a < 3; ++a)
+          clouds[k]->lo[a] = unordered_host(hbox[6 * k + a]), clouds[k]->hi[a] = unordered_host(hbox[6 * k + 3 + a]);
+  }
+  for (int k = 0; k < m; ++k) out[k] = clouds[k];
+  return VGICP_OK;
+} catch (...) {
+  return api_exception();
+}
+
 static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const double* d_cov9, size_t n, bool keep64,
                                  vgicp_cloud* out);
 
@@ -518,8 +634,39 @@ struct FastExport {
 // Builds maps of float32 clouds clouds[k] at res[k] with the hand-written kernels: zero + mark,
 // rank, (sync: V per map, range errors), order, accumulate. With `exp` (one map): export mode — the
 // key-ordered statistics are written to device buffers in rank order (exp->mem, freed by the caller).
+static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* res, int m, int m_smem,
+                              vgicp_map* out, FastExport* exp);
+
+// Jobs are ordered so that the maps whose bitmap fits in shared memory come first (one fused
+// zero + mark + rank launch for them, the global-atomic kernels for the rest).
 static int build_fast(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* res, int m, vgicp_map* out,
                       FastExport* exp) {
+  const unsigned smem_words = fast_markrank_smem_words(ctx->device);
+  std::vector<int> perm;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int k = 0; k < m; ++k) {
+      int cmin[3], cmax[3];
+      bool oor = false;
+      const bool fits = fast_box(clouds[k], res[k], cmin, cmax, &oor) && fast_words(cmin, cmax) <= smem_words;
+      if (fits == (pass == 0)) perm.push_back(k);
+    }
+  int m_smem = 0;
+  for (int k = 0; k < m; ++k) {
+    int cmin[3], cmax[3];
+    bool oor = false;
+    m_smem += fast_box(clouds[k], res[k], cmin, cmax, &oor) && fast_words(cmin, cmax) <= smem_words ? 1 : 0;
+  }
+  std::vector<vgicp_cloud> pc(m);
+  std::vector<double> pr(m);
+  for (int q = 0; q < m; ++q) pc[q] = clouds[perm[q]], pr[q] = res[perm[q]];
+  std::vector<vgicp_map> pm(m, nullptr);
+  if (int rc = build_fast_ordered(ctx, pc.data(), pr.data(), m, m_smem, pm.data(), exp)) return rc;
+  for (int q = 0; q < m; ++q) out[perm[q]] = pm[q];
+  return VGICP_OK;
+}
+
+static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* res, int m, int m_smem,
+                              vgicp_map* out, FastExport* exp) {
   cudaStream_t s = ctx->stream;
   std::vector<FastBuildJob> jobs(m);
   std::vector<vgicp_map> maps(m, nullptr);
@@ -590,7 +737,7 @@ static int build_fast(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* re
   const size_t o_code = carve(sizeof(unsigned) * total);
   const size_t o_list = carve(sizeof(unsigned) * total);
   const size_t o_offs = carve(sizeof(unsigned) * (total + m));
-  const size_t o_gcnt = carve(sizeof(unsigned) * (total + m));
+  const size_t o_gcnt = carve(sizeof(unsigned) * 2 * (total + m));  // per-point ranks | global cursors
   if (int rc = ensure_scratch(ctx, off)) {
     cleanup();
     return rc;
@@ -610,8 +757,24 @@ static int build_fast(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* re
   };
   step(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(FastBuildJob) * m, cudaMemcpyHostToDevice, s), "build jobs");
   step(cudaMemsetAsync(d_err, 0, sizeof(int) * m, s), "build flags");
-  if (rc == VGICP_OK) step(launch_fast_mark(d_jobs, m, max_n, max_words, d_code, d_err, s), "build mark");
-  if (rc == VGICP_OK) step(launch_fast_rank(d_jobs, m, d_vc, s), "build rank");
+  unsigned max_words_smem = 0, max_words_glob = 0, max_n_glob = 0;
+  for (int k = 0; k < m; ++k) {
+    if (k < m_smem) {
+      max_words_smem = std::max(max_words_smem, jobs[k].words);
+    } else {
+      max_words_glob = std::max(max_words_glob, jobs[k].words);
+      max_n_glob = std::max(max_n_glob, jobs[k].n);
+    }
+  }
+  (void)max_words;
+  (void)max_n;
+  if (rc == VGICP_OK && m_smem > 0)
+    step(launch_fast_markrank_smem(d_jobs, m_smem, max_words_smem, d_code, d_err, d_vc, s), "build mark+rank");
+  if (rc == VGICP_OK && m > m_smem) {
+    step(launch_fast_mark(d_jobs + m_smem, m - m_smem, max_n_glob, max_words_glob, d_code, d_err + m_smem, s),
+         "build mark");
+    if (rc == VGICP_OK) step(launch_fast_rank(d_jobs + m_smem, m - m_smem, d_vc + m_smem, s), "build rank");
+  }
   std::vector<int> herr(m);
   std::vector<unsigned> hv(m);
   step(cudaMemcpyAsync(herr.data(), d_err, sizeof(int) * m, cudaMemcpyDeviceToHost, s), "build flags");
@@ -621,7 +784,7 @@ static int build_fast(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* re
     cleanup();
     return rc;
   }
-  ctx->launches += 3;  // zero, mark, rank
+  ctx->launches += (m_smem > 0 ? 1 : 0) + (m > m_smem ? 3 : 0);  // mark+rank | zero, mark, rank
   for (int k = 0; k < m; ++k)
     if (herr[k]) {
       cleanup();
@@ -629,7 +792,8 @@ static int build_fast(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* re
     }
   // per-map voxel arrays: ra | rb | cov6 (rank order)
   unsigned max_v = 0, smem_v = fast_order_smem_voxels(ctx->device);
-  std::vector<int> in_smem, in_global;
+  const unsigned sort_n = std::getenv("VGICP_BUILD_SCATTER") ? 0u : fast_sort_max_points(ctx->device);
+  std::vector<int> in_sort, in_smem, in_global;
   for (int k = 0; k < m; ++k) {
     vgicp_map mp = maps[k];
     const size_t V = hv[k];
@@ -647,7 +811,7 @@ static int build_fast(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* re
     jobs[k].V = static_cast<unsigned>(V);
     jobs[k].ra = mp->ra, jobs[k].rb = mp->rb, jobs[k].cov6 = mp->cov64;
     max_v = std::max(max_v, jobs[k].V);
-    (V <= smem_v ? in_smem : in_global).push_back(k);
+    (jobs[k].n <= sort_n ? in_sort : V <= smem_v ? in_smem : in_global).push_back(k);
   }
   if (exp) {  // single map: key-ordered statistics in rank order
     const size_t V = hv[0];
@@ -660,27 +824,32 @@ static int build_fast(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* re
     exp->cov9 = exp->mean64 + 3 * V;
     jobs[0].keys = exp->keys, jobs[0].counts = exp->counts, jobs[0].mean64 = exp->mean64, jobs[0].cov9 = exp->cov9;
   }
-  std::vector<int> order(in_smem);
+  std::vector<int> order(in_sort);
+  order.insert(order.end(), in_smem.begin(), in_smem.end());
   order.insert(order.end(), in_global.begin(), in_global.end());
-  unsigned smem_max = 0;
+  unsigned smem_max = 0, sort_max = 0;
   for (int k : in_smem) smem_max = std::max(smem_max, jobs[k].V);
+  for (int k : in_sort) sort_max = std::max(sort_max, jobs[k].n);
   step(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(FastBuildJob) * m, cudaMemcpyHostToDevice, s), "build jobs");
   step(cudaMemcpyAsync(d_idx, order.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s), "build jobs");
+  if (rc == VGICP_OK && !in_sort.empty())
+    step(launch_fast_sort(d_jobs, d_idx, static_cast<int>(in_sort.size()), sort_max, d_code, d_list, d_offs, s),
+         "build sort");
   if (rc == VGICP_OK && !in_smem.empty())
-    step(launch_fast_order(d_jobs, d_idx, static_cast<int>(in_smem.size()), std::max(1u, smem_max), d_code, d_list,
-                           d_offs, d_gcnt, s),
+    step(launch_fast_order(d_jobs, d_idx + in_sort.size(), static_cast<int>(in_smem.size()), std::max(1u, smem_max),
+                           d_code, d_gcnt, d_list, d_offs, d_gcnt + total + m, s),
          "build order");
   if (rc == VGICP_OK && !in_global.empty())
-    step(launch_fast_order(d_jobs, d_idx + in_smem.size(), static_cast<int>(in_global.size()), 0u, d_code, d_list,
-                           d_offs, d_gcnt, s),
+    step(launch_fast_order(d_jobs, d_idx + in_sort.size() + in_smem.size(), static_cast<int>(in_global.size()), 0u,
+                           d_code, d_gcnt, d_list, d_offs, d_gcnt + total + m, s),
          "build order (global cursors)");
-  if (rc == VGICP_OK) step(launch_fast_accumulate(d_jobs, m, max_v, d_list, d_offs, exp != nullptr, s), "build accumulate");
+  if (rc == VGICP_OK) step(launch_fast_accumulate(d_jobs, m, max_v, d_list, d_offs, d_code, exp != nullptr, s), "build accumulate");
   step(cudaStreamSynchronize(s), "build");
   if (rc != VGICP_OK) {
     cleanup();
     return rc;
   }
-  ctx->launches += (in_smem.empty() ? 0 : 1) + (in_global.empty() ? 0 : 1) + 1;
+  ctx->launches += (in_sort.empty() ? 0 : 1) + (in_smem.empty() ? 0 : 1) + (in_global.empty() ? 0 : 1) + 1;
   for (int k = 0; k < m; ++k) out[k] = maps[k];
   return VGICP_OK;
 }

@@ -2,6 +2,7 @@
 // vgicp_submap_build from float64 device arrays): input-order SoA for the builds and the
 // Morton-ordered 64-point blocks for the probe kernels (Z-order code of 10 bits per axis over the
 // finite bounding box, stable radix sort: ties in input order).
+#include <algorithm>
 #include <type_traits>
 
 #include "internal.h"
@@ -144,7 +145,100 @@ unsigned grid_cloud(size_t n) {
   return static_cast<unsigned>(g == 0 ? 1 : (g < 4096 ? g : 4096));
 }
 
+// Batched float32 uploads (one launch per stage for all clouds; blockIdx.y = cloud).
+__global__ void bbox_batch_kernel(const UploadSeg* __restrict__ segs, unsigned* __restrict__ boxes) {
+  const UploadSeg& g = segs[blockIdx.y];
+  const float* __restrict__ xyz = g.xyz;
+  unsigned lo[3] = {~0u, ~0u, ~0u}, hi[3] = {0u, 0u, 0u};
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = xyz[3 * (size_t)i + a];
+      if (isfinite(v)) {
+        lo[a] = min(lo[a], ordered(v));
+        hi[a] = max(hi[a], ordered(v));
+      }
+    }
+  }
+  unsigned* box = boxes + 6 * blockIdx.y;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    atomicMin(&box[a], lo[a]);
+    atomicMax(&box[3 + a], hi[a]);
+  }
+}
+
+__global__ void morton_batch_kernel(const UploadSeg* __restrict__ segs, const unsigned* __restrict__ boxes,
+                                    unsigned* __restrict__ codes, unsigned* __restrict__ idx) {
+  const UploadSeg& g = segs[blockIdx.y];
+  const unsigned* box = boxes + 6 * blockIdx.y;
+  float lo[3], ext[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = unordered(box[a]);
+    ext[a] = unordered(box[3 + a]) - lo[a];
+  }
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    unsigned c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = g.xyz[3 * (size_t)i + a];
+      const float u = (isfinite(v) && ext[a] > 0.f) ? (v - lo[a]) / ext[a] : 0.f;
+      c[a] = static_cast<unsigned>(fminf(1023.f, fmaxf(0.f, u * 1024.f)));
+    }
+    codes[g.offset + i] = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
+    idx[g.offset + i] = i;
+  }
+}
+
+__global__ void fill_batch_kernel(const UploadSeg* __restrict__ segs, const unsigned* __restrict__ perm) {
+  const UploadSeg& g = segs[blockIdx.y];
+  const unsigned n = g.n;
+  const unsigned padded = (n + kPointBlock - 1) / kPointBlock * kPointBlock;
+  const SrcF32 src{g.xyz, g.cov6};
+  for (unsigned d = blockIdx.x * blockDim.x + threadIdx.x; d < padded; d += gridDim.x * blockDim.x) {
+    const unsigned dn = d < n ? d : n - 1;
+#pragma unroll
+    for (int copy = 0; copy < 2; ++copy) {
+      const unsigned j = copy == 0 ? dn : perm[g.offset + dn];
+      float4 a, b;
+      float z;
+      src.get(j, a, b, z);
+      if (copy == 0) {
+        if (d < n) g.pa[d] = a, g.pb[d] = b, g.pc[d] = z;
+      } else {
+        PointBlock& B = g.blk[d / kPointBlock];
+        B.pa[d % kPointBlock] = a;
+        B.pb[d % kPointBlock] = b;
+        B.pc[d % kPointBlock] = z;
+      }
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_upload_batch_prepare(const UploadSeg* segs, int m, unsigned max_n, unsigned* boxes, unsigned* codes,
+                                        unsigned* idx, cudaStream_t s) {
+  if (m <= 0 || max_n == 0) return cudaSuccess;
+  const unsigned gx = std::min<unsigned>((max_n + 255) / 256, 64);
+  for (int m0 = 0; m0 < m; m0 += 65535) {
+    const unsigned mm = static_cast<unsigned>(std::min(65535, m - m0));
+    bbox_batch_kernel<<<dim3(gx, mm), 256, 0, s>>>(segs + m0, boxes + 6 * m0);
+    morton_batch_kernel<<<dim3(gx, mm), 256, 0, s>>>(segs + m0, boxes + 6 * m0, codes, idx);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_upload_batch_fill(const UploadSeg* segs, int m, unsigned max_n, const unsigned* perm, cudaStream_t s) {
+  if (m <= 0 || max_n == 0) return cudaSuccess;
+  const unsigned gx = std::min<unsigned>((max_n + kPointBlock + 255) / 256, 64);
+  for (int m0 = 0; m0 < m; m0 += 65535) {
+    const unsigned mm = static_cast<unsigned>(std::min(65535, m - m0));
+    fill_batch_kernel<<<dim3(gx, mm), 256, 0, s>>>(segs + m0, perm);
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t launch_cloud_bbox(const double* xyz, size_t n, unsigned* box, cudaStream_t s) {
   bbox_kernel<<<grid_cloud(n), 256, 0, s>>>(xyz, n, box);

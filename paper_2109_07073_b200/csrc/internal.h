@@ -146,12 +146,22 @@ struct FastBuildJob {
 cudaError_t launch_fast_mark(const FastBuildJob* jobs, int m, unsigned max_n, unsigned max_words, unsigned* code,
                              int* err, cudaStream_t s);
 cudaError_t launch_fast_rank(const FastBuildJob* jobs, int m, unsigned* vcount, cudaStream_t s);
+// zero + mark + rank in one CTA per map for jobs[0, count), whose bitmaps (<= max_words records)
+// fit in shared memory; err / vcount are indexed like jobs
+cudaError_t launch_fast_markrank_smem(const FastBuildJob* jobs, int count, unsigned max_words, unsigned* code,
+                                      int* err, unsigned* vcount, cudaStream_t s);
+unsigned fast_markrank_smem_words(int device);
 // count + scan + stable input-order scatter, one CTA per map; `idx` lists the jobs of this launch;
 // smem_v > 0: per-voxel cursors in shared memory for maps with V <= smem_v, else in `gcnt`
-cudaError_t launch_fast_order(const FastBuildJob* jobs, const int* idx, int count, unsigned smem_v, unsigned* code,
-                              unsigned* list, unsigned* offs, unsigned* gcnt, cudaStream_t s);
+cudaError_t launch_fast_order(const FastBuildJob* jobs, const int* idx, int count, unsigned smem_v, const unsigned* code,
+                              unsigned* rank, unsigned* list, unsigned* offs, unsigned* gcnt, cudaStream_t s);
+// the same result (list, offs) by a shared-memory LSD radix sort, one CTA per map, for maps of
+// <= fast_sort_max_points() points (the serial-scatter order kernel covers larger ones)
+cudaError_t launch_fast_sort(const FastBuildJob* jobs, const int* idx, int count, unsigned max_n, const unsigned* code,
+                             unsigned* list, unsigned* offs, cudaStream_t s);
+unsigned fast_sort_max_points(int device);
 cudaError_t launch_fast_accumulate(const FastBuildJob* jobs, int m, unsigned max_v, const unsigned* list,
-                                   const unsigned* offs, bool export_mode, cudaStream_t s);
+                                   const unsigned* offs, const unsigned* code, bool export_mode, cudaStream_t s);
 unsigned fast_order_smem_voxels(int device);
 // hash table of a rank-numbered map, built on demand (lookups, hash-probe measurement modes):
 // cuckoo insert of keys[rank], then each slot receives ra / rb of its rank
@@ -293,6 +303,22 @@ cudaError_t launch_cloud_morton(const float* xyz, size_t n, const unsigned* box,
                                 cudaStream_t s);
 cudaError_t launch_cloud_fill(const float* xyz, const float* cov6, size_t n, const unsigned* perm, float4* pa,
                               float4* pb, float* pc, PointBlock* blk, cudaStream_t s);
+// Batched float32 upload (vgicp_cloud_upload_batch): per cloud, the staged device input and its
+// destination layout. prepare = bounding boxes (boxes[6k], pre-set to empty) + Morton codes / local
+// indices at `offset`; fill = input-order SoA + Morton blocks from the per-cloud sorted permutation.
+struct UploadSeg {
+  const float* xyz;   // staged n×3 (device)
+  const float* cov6;  // staged n×6 (device) or nullptr (raw cloud)
+  unsigned offset;    // first point of this cloud in the batch (codes / permutation arrays)
+  unsigned n;
+  float4* pa;
+  float4* pb;
+  float* pc;
+  PointBlock* blk;
+};
+cudaError_t launch_upload_batch_prepare(const UploadSeg* segs, int m, unsigned max_n, unsigned* boxes, unsigned* codes,
+                                        unsigned* idx, cudaStream_t s);
+cudaError_t launch_upload_batch_fill(const UploadSeg* segs, int m, unsigned max_n, const unsigned* perm, cudaStream_t s);
 // the same for fp64 host-provided input arrays (already on device)
 cudaError_t launch_transform64(const double* xyz, const double* cov9, size_t n, const double* T, double* out_xyz,
                                double* out_cov9, cudaStream_t s);

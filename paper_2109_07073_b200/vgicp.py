@@ -227,6 +227,41 @@ class PointCloud(_Handle):
                         and np.array_equal(f[:, 5], f[:, 7]))
         return False
 
+    @classmethod
+    def upload_batch(cls, means_list, covariances_list=None, ctx: Context | None = None) -> list["PointCloud"]:
+        """Many float32 clouds in one vgicp_cloud_upload_batch call (one staged copy, one launch per
+        layout stage for the batch); identical to PointCloud(m, c) per cloud. Clouds that need float64
+        storage (see _needs_f64) are uploaded one by one."""
+        ctx = ctx or default_context()
+        covs = list(covariances_list) if covariances_list is not None else [None] * len(means_list)
+        if len(covs) != len(means_list):
+            raise ValueError("one covariance array per cloud")
+        out: list = [None] * len(means_list)
+        batch = []
+        for k, (m, c) in enumerate(zip(means_list, covs)):
+            m64 = np.asarray(m)
+            m64 = m64.reshape(-1, 3) if m64.size else m64.reshape(0, 3)
+            c64 = None if c is None else np.asarray(c)
+            if c64 is not None and len(c64.reshape(len(c64), -1)) != len(m64):
+                raise ValueError("covariance count does not match point count")
+            if cls._needs_f64(m64, c64):
+                out[k] = cls(m64, c64, ctx)
+            else:
+                batch.append((k, np.ascontiguousarray(m64, dtype=np.float32), None if c64 is None else cov6_from(c64)))
+        if batch:
+            nb = len(batch)
+            xyz = (C.c_void_p * nb)(*[b[1].ctypes.data for b in batch])
+            cv = (C.c_void_p * nb)(*[b[2].ctypes.data if b[2] is not None else None for b in batch])
+            ns = (C.c_size_t * nb)(*[len(b[1]) for b in batch])
+            hs = (C.c_void_p * nb)()
+            check(_lib.load().vgicp_cloud_upload_batch(ctx.handle, xyz, cv, ns, nb, hs))
+            for (k, m, c), h in zip(batch, hs):
+                cloud = cls.__new__(cls)
+                _Handle.__init__(cloud, ctx, C.c_void_p(h))
+                cloud.means, cloud.cov6 = m, c
+                out[k] = cloud
+        return out
+
     def is_f64(self) -> bool:
         v = C.c_int()
         check(_lib.load().vgicp_cloud_is_f64(self._h, C.byref(v)))

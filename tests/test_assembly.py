@@ -268,10 +268,11 @@ def test_gpu_band_solver_pair_matches_single(V):
     x0, x1 = graph.solve_damped_pair(bad.data_ptr(), (0.0, 0.0))
     assert x0 is None and x1 is None
     # mixed outcome (what the LM's pair cache relies on): instance 0 fails, the damping rescues
-    # instance 1 (-1e-3 + 1e8·max(-1e-3, 1e-10) > 0), whose x and status stay its own
-    x0, x1 = graph.solve_damped_pair(bad.data_ptr(), (0.0, 1e8))
+    # instance 1 (the broken block becomes -1e-3 + 1e18·max(-1e-3, 1e-10) = 1e8, far above its
+    # couplings), whose x and status stay its own
+    x0, x1 = graph.solve_damped_pair(bad.data_ptr(), (0.0, 1e18))
     assert x0 is None and x1 is not None
-    assert np.array_equal(x1, graph.solve_damped(bad.data_ptr(), 1e8))
+    assert np.array_equal(x1, graph.solve_damped(bad.data_ptr(), 1e18))
     good = graph.solve_damped_pair(d_asm.data_ptr(), (1e-4, 1e-3))
     assert good[0] is not None and np.array_equal(good[1], graph.solve_damped(d_asm.data_ptr(), 1e-3))
 

@@ -621,10 +621,16 @@ def test_handwritten_build_equals_sorted_build(ctx, monkeypatch):
     res.append(0.5)
     fast = V.GaussianVoxelMap.build_batch(clouds, res)
     slow = _sorted_build(monkeypatch, clouds, res)
-    for f, s in zip(fast, slow):
+    monkeypatch.setenv("VGICP_BUILD_SCATTER", "1")  # warp-serial scatter instead of the shared-memory radix sort
+    scatter = V.GaussianVoxelMap.build_batch(clouds, res)
+    monkeypatch.delenv("VGICP_BUILD_SCATTER")
+    monkeypatch.setenv("VGICP_SORT_5BIT", "1")  # 5-bit digits (3 passes) instead of 4-bit
+    four = V.GaussianVoxelMap.build_batch(clouds, res)
+    monkeypatch.delenv("VGICP_SORT_5BIT")
+    for f, s, w, q in zip(fast, slow, scatter, four):
         assert f.size() == s.size() and f.total_points() == s.total_points()
-        for x, y in zip(f.export(), s.export()):
-            assert np.array_equal(x, y)
+        for x, y, z, u in zip(f.export(), s.export(), w.export(), q.export()):
+            assert np.array_equal(x, y) and np.array_equal(x, z) and np.array_equal(x, u)
     # factors: target maps from each build, same sources / poses -> identical blocks
     poses = np.stack([rng.random_pose(0.05, 0.5) for _ in range(len(clouds))])
     def graph(maps):
@@ -652,3 +658,37 @@ def test_handwritten_build_hash_mode_equals_rank_mode(ctx, monkeypatch):
     monkeypatch.setenv("VGICP_NO_RANK", "1")
     rb, ib = V.FactorGraph(fs, 3).linearize_raw(poses)
     assert np.array_equal(ia, ib) and np.array_equal(ra, rb)
+
+
+def test_upload_batch_equals_single_uploads(ctx):
+    """vgicp_cloud_upload_batch (one staged copy, one segmented sort for all Morton orders) gives the
+    same device layout as one vgicp_cloud_upload per cloud: bit-identical factor blocks, overlap hits
+    and maps; raw (covariance-free) and empty clouds included."""
+    rng = O.Rng(403)
+    ms, cs = [], []
+    for k in range(5):
+        m, c = rng.gaussian_cloud(700 + 900 * k, 8.0)
+        m32, _, c6 = contract_inputs(m, c)
+        ms.append(m32)
+        cs.append(c6)
+    raw = rng.gaussian_cloud(500, 8.0)[0].astype(np.float32)
+    batch = V.PointCloud.upload_batch(ms + [raw, np.zeros((0, 3), np.float32)], cs + [None, None], ctx)
+    single = [V.PointCloud(m, c, ctx) for m, c in zip(ms, cs)]
+    assert [len(b) for b in batch] == [len(m) for m in ms] + [500, 0]
+    assert not batch[5].has_covariances() and batch[0].has_covariances()
+    poses = np.stack([rng.random_pose(0.05, 0.5) for _ in range(5)])
+    def run(clouds):
+        maps = V.GaussianVoxelMap.build_batch(clouds[:5], [1.0] * 5)
+        fs = [V.MatchingCostFactor(k, k + 1, clouds[k + 1], maps[k]) for k in range(4)]
+        raw_out, inl = V.FactorGraph(fs, 5).linearize_raw(poses)
+        rels = [O.compose(O.inverse(poses[k]), poses[k + 1]) for k in range(4)]
+        hits = V.overlap_hits([clouds[k + 1] for k in range(4)], rels, maps[:4])
+        return raw_out, inl, hits, [m.export() for m in maps]
+    a, b = run(batch), run(single)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    for x, y in zip(a[3], b[3]):
+        for u, w in zip(x, y):
+            assert np.array_equal(u, w)
+    rel = O.compose(O.inverse(poses[0]), poses[1])
+    maps = V.GaussianVoxelMap.build_batch(batch[:1], [1.0])
+    assert V.overlap_hits([batch[5]], [rel], maps)[0] == V.overlap_hits([V.PointCloud(raw, None, ctx)], [rel], maps)[0]

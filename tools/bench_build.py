@@ -17,7 +17,7 @@ t = time.perf_counter()
 sc = W.make_scans(W.c3_spec(), ctx=ctx)
 print(f"scans+covariances {time.perf_counter() - t:.2f} s")
 t = time.perf_counter()
-clouds = [V.PointCloud(m, c, ctx) for m, c in zip(sc.means, sc.cov6)]
+clouds = V.PointCloud.upload_batch(sc.means, sc.cov6, ctx)
 ctx.synchronize()
 print(f"upload 450 clouds {time.perf_counter() - t:.3f} s")
 for mode in (["fast"] if profile else ["fast", "sorted", "fast"]):
