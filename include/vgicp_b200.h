@@ -179,6 +179,24 @@ int vgicp_gicp_error(vgicp_ctx ctx, const double source_mean[3], const double so
 int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses, int chunk,
                        vgicp_graph* out);
 int vgicp_graph_destroy(vgicp_graph graph);
+/* The graph of factors [first, first + count) of the list, with the work decomposition of the WHOLE
+ * list (so every per-factor block is bit-identical to vgicp_graph_create's): one rank's share of a
+ * factor graph split across processes. Its blocks are indexed 0..count-1 (factor first + k at k);
+ * plan / assemble / solve with a whole-list graph (vgicp_graph_assemble_device). */
+int vgicp_graph_create_range(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses,
+                             int chunk, int first, int count, vgicp_graph* out);
+/* Multi-GPU split of ONE graph behind the C ABI (the loops of optimizer.cpp:53-56 /
+ * :68-70 over factors): factors[r] is the factor list with context r's handles — the same factors,
+ * their clouds / maps replicated on context r's device (contexts may share a device). Shard r
+ * linearizes a contiguous, point-balanced factor range with the whole list's work decomposition;
+ * context 0 is the root: it plans, assembles — its assembly kernel reads the shards' blocks in place
+ * over peer memory (NVLink) — and solves, so assembled systems, errors and the native LM's trace are
+ * bit-identical to a single-context graph. Every vgicp_graph_* call accepts the result (the
+ * _device variants take and return root-device memory). At most 8 shards. */
+int vgicp_graph_create_sharded(const vgicp_ctx* ctxs, int num_shards, const vgicp_factor_desc* const* factors,
+                               int num_factors, int num_poses, int chunk, vgicp_graph* out);
+int vgicp_graph_num_shards(vgicp_graph graph, int* num_shards);
+int vgicp_graph_shard_range(vgicp_graph graph, int shard, int* first, int* count);
 int vgicp_graph_num_factors(vgicp_graph graph, int* num_factors);
 /* Σ source points over the graph's factors (the per-pass point-evaluation count). */
 int vgicp_graph_num_points(vgicp_graph graph, uint64_t* points);
@@ -209,6 +227,10 @@ int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_po
  * reduction order), so an LM can score a candidate with the linearization it needs anyway if the
  * candidate is accepted (total_error, optimizer.cpp:66-75 + linearize_all, :45-62). */
 int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* inliers);
+/* Assembly (as vgicp_graph_linearize_assembled_device) of externally provided blocks: d_blocks holds
+ * num_factors × VGICP_LINEARIZED_DOUBLES doubles in factor order on the context's device — e.g. the
+ * blocks of every rank's vgicp_graph_create_range share, gathered over NCCL. */
+int vgicp_graph_assemble_device(vgicp_graph graph, const double* d_blocks, double* d_assembled);
 /* Damped solve of the assembled reduced system on the GPU (solve_block_system,
  * block_solver.cpp:64-122, with the Marquardt damping of optimizer.cpp:119-123: diagonal entries
  * d -> d + lambda·max(d, 1e-10)). vgicp_graph_solver_plan (after vgicp_graph_assembly_plan)

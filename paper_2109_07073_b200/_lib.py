@@ -97,6 +97,11 @@ SIGNATURES = {
     "vgicp_gicp_error": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _PD, _vp, _vp, C.POINTER(_i)]),
     "vgicp_graph_create": (_i, [_vp, _vp, _i, _i, _i, C.POINTER(_vp)]),
     "vgicp_graph_destroy": (_i, [_vp]),
+    "vgicp_graph_create_range": (_i, [_vp, _vp, _i, _i, _i, _i, _i, C.POINTER(_vp)]),
+    "vgicp_graph_create_sharded": (_i, [_vp, _i, _vp, _i, _i, _i, C.POINTER(_vp)]),
+    "vgicp_graph_num_shards": (_i, [_vp, C.POINTER(_i)]),
+    "vgicp_graph_shard_range": (_i, [_vp, _i, C.POINTER(_i), C.POINTER(_i)]),
+    "vgicp_graph_assemble_device": (_i, [_vp, _vp, _vp]),
     "vgicp_graph_num_factors": (_i, [_vp, C.POINTER(_i)]),
     "vgicp_graph_num_points": (_i, [_vp, C.POINTER(C.c_uint64)]),
     "vgicp_graph_linearize": (_i, [_vp, _vp, _vp, _vp]),

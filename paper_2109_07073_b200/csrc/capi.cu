@@ -1784,13 +1784,21 @@ static int factor_launches(const vgicp_graph_s* g) {
   return (g->f64_begin > 0 ? 1 : 0) + (g->num_items > g->f64_begin ? 1 : 0);
 }
 
-int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses, int chunk,
-                       vgicp_graph* out) try {
-  if (!ctx || !out || (num_factors > 0 && !factors)) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
-  *out = nullptr;
-  if (num_factors < 0 || num_poses < 0) return fail(VGICP_E_INVALID_ARGUMENT, "negative size");
-  if (chunk <= 0) chunk = kDefaultChunk;
-  chunk = std::max(kFactorTile, (chunk + kFactorTile - 1) / kFactorTile * kFactorTile);
+// Work decomposition of a factor list (items in launch order: float32-cloud items first, then
+// float64-cloud items; each factor's items contiguous). Items are one CTA each; a launch runs in
+// ~equal waves of `slots` resident CTAs. With many factors, the last wave's factors are cut into
+// quarter chunks so the tail wave is short; with fewer factors than slots, every factor is cut
+// finer so that the launch still fills the GPU (C1 / C2). VGICP_NO_TAIL_SPLIT=1 keeps uniform
+// chunks. A shard of a sharded graph uses the decomposition of the WHOLE list, so its per-factor
+// blocks are bit-identical to a single-device graph's.
+struct Decomp {
+  std::vector<FactorDev> fd;
+  std::vector<WorkItem> items;
+  int f64_begin = 0;
+  bool rank = false;
+};
+
+static int validate_factors(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses) {
   // MatchingCostFactor ctor validation (factors.cpp:57-66)
   for (int f = 0; f < num_factors; ++f) {
     const vgicp_factor_desc& d = factors[f];
@@ -1806,11 +1814,25 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
     if (d.target_index < 0 || d.target_index >= num_poses || d.source_index < 0 || d.source_index >= num_poses)
       return fail(VGICP_E_INVALID_ARGUMENT, "factor variable index out of range");
   }
-  DeviceGuard g(ctx->device);
-  // Work decomposition. Items are one CTA each; a launch runs in ~equal waves of `slots` resident
-  // CTAs. With many factors, the last wave's factors are cut into quarter chunks so the tail wave
-  // is short; with fewer factors than slots, every factor is cut finer so that the launch still
-  // fills the GPU (C1 / C2). VGICP_NO_TAIL_SPLIT=1 keeps uniform chunks.
+  return VGICP_OK;
+}
+
+// Factor kernels probe the cuckoo tables (not the bitmaps) unless every target map has a bitmap
+// (and VGICP_NO_RANK is unset): hand-built maps get their table, on demand, before descriptors
+// capture their device pointers.
+static bool use_rank_lookups(const vgicp_factor_desc* factors, int num_factors) {
+  bool rank = std::getenv("VGICP_NO_RANK") == nullptr;
+  for (int f = 0; f < num_factors && rank; ++f) rank = factors[f].target->occ.occ != nullptr;
+  return rank;
+}
+static int ensure_tables_for_hash_mode(const vgicp_factor_desc* factors, int num_factors) {
+  if (use_rank_lookups(factors, num_factors)) return VGICP_OK;
+  for (int f = 0; f < num_factors; ++f)
+    if (int rc = ensure_table(factors[f].target)) return rc;
+  return VGICP_OK;
+}
+
+static void decompose(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int chunk, Decomp& g) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   const int slots = 2 * sms;
@@ -1823,48 +1845,66 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   const int small_chunk = round_chunk(chunk / 4);
   const int few_chunk =
       std::min(chunk, round_chunk(total_points / std::max<uint64_t>(1, 2ull * static_cast<uint64_t>(slots))));
-  std::vector<FactorDev> fd(num_factors);
-  std::vector<WorkItem> items;
-  uint64_t points = 0;
+  g.fd.assign(num_factors, FactorDev{});
+  g.items.clear();
   // rank lookups (occupancy bitmap + rank-ordered statistics) when every target map carries them;
   // VGICP_NO_RANK=1 keeps the cuckoo-hash probes (measurement switch)
-  bool rank = std::getenv("VGICP_NO_RANK") == nullptr;
-  for (int f = 0; f < num_factors && rank; ++f) rank = factors[f].target->occ.occ != nullptr;
-  if (!rank)  // hash probes: hand-built maps get their table now
-    for (int f = 0; f < num_factors; ++f)
-      if (int rc = ensure_table(factors[f].target)) return rc;
+  g.rank = use_rank_lookups(factors, num_factors);
   // items of float32-exact source clouds first, then those of float64 clouds (their own launch)
-  int f64_begin = 0;
   for (int pass = 0; pass < 2; ++pass) {
-    if (pass == 1) f64_begin = static_cast<int>(items.size());
+    if (pass == 1) g.f64_begin = static_cast<int>(g.items.size());
     for (int f = 0; f < num_factors; ++f) {
       const vgicp_factor_desc& d = factors[f];
       if (d.source->f64 != (pass == 1)) continue;
-      FactorDev& x = fd[f];
+      FactorDev& x = g.fd[f];
       const int fchunk =
           !split ? chunk : (num_factors < slots ? few_chunk : (f >= num_factors - slots ? small_chunk : chunk));
       x.blk = d.source->sblk;  // Morton order: neighbouring lanes probe neighbouring voxels
       x.blk64 = d.source->blk64;
-      x.map = rank ? d.target->dev_rank() : d.target->dev();
+      x.map = g.rank ? d.target->dev_rank() : d.target->dev();
       x.n = static_cast<int>(d.source->n);
       x.tgt = d.target_index;
       x.src = d.source_index;
-      x.item_begin = static_cast<int>(items.size());
-      for (int b = 0; b < x.n; b += fchunk) items.push_back(WorkItem{f, b, std::min(x.n, b + fchunk), 0});
-      x.item_count = static_cast<int>(items.size()) - x.item_begin;
+      x.item_begin = static_cast<int>(g.items.size());
+      for (int b = 0; b < x.n; b += fchunk) g.items.push_back(WorkItem{f, b, std::min(x.n, b + fchunk), 0});
+      x.item_count = static_cast<int>(g.items.size()) - x.item_begin;
       x.pad = 0;
-      points += d.source->n;
+    }
+  }
+}
+
+// The graph of factors [first, first + count) of `factors` under the decomposition `g` of the whole
+// list: local factor k is global factor first + k (its items keep their chunking; indices relabelled).
+static int graph_from(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_poses, const Decomp& g, int first,
+                      int count, vgicp_graph* out) {
+  std::vector<FactorDev> fd(count);
+  std::vector<WorkItem> items;
+  int f64_begin = 0;
+  uint64_t points = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) f64_begin = static_cast<int>(items.size());
+    const int i0 = pass == 0 ? 0 : g.f64_begin, i1 = pass == 0 ? g.f64_begin : static_cast<int>(g.items.size());
+    for (int i = i0; i < i1; ++i) {
+      const WorkItem& w = g.items[i];
+      if (w.factor < first || w.factor >= first + count) continue;
+      const int k = w.factor - first;
+      if (i == g.fd[w.factor].item_begin) {
+        fd[k] = g.fd[w.factor];
+        fd[k].item_begin = static_cast<int>(items.size());
+        points += static_cast<uint64_t>(fd[k].n);
+      }
+      items.push_back(WorkItem{k, w.begin, w.end, 0});
     }
   }
   auto gr = std::make_unique<vgicp_graph_s>();
   gr->ctx = ctx;
-  gr->num_factors = num_factors;
+  gr->num_factors = count;
   gr->num_poses = num_poses;
   gr->num_items = static_cast<int>(items.size());
   gr->f64_begin = f64_begin;
   gr->num_points = points;
-  gr->rank_lookup = rank;
-  const size_t nf = std::max(num_factors, 1), ni = std::max<size_t>(items.size(), 1);
+  gr->rank_lookup = g.rank;
+  const size_t nf = std::max(count, 1), ni = std::max<size_t>(items.size(), 1);
   size_t off = 0;
   auto carve = [&](size_t bytes) {
     const size_t o = off;
@@ -1896,11 +1936,12 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
   auto step = [&](cudaError_t e, const char* what) {
     if (rc == VGICP_OK && e != cudaSuccess) rc = cuda_fail(e, what);
   };
-  if (num_factors > 0) {
-    step(cudaMemcpyAsync(gr->d_factors, fd.data(), sizeof(FactorDev) * num_factors, cudaMemcpyHostToDevice, s),
+  if (count > 0) {
+    step(cudaMemcpyAsync(gr->d_factors, fd.data(), sizeof(FactorDev) * count, cudaMemcpyHostToDevice, s),
          "upload factors");
-    step(cudaMemcpyAsync(gr->d_items, items.data(), sizeof(WorkItem) * items.size(), cudaMemcpyHostToDevice, s),
-         "upload items");
+    if (!items.empty())
+      step(cudaMemcpyAsync(gr->d_items, items.data(), sizeof(WorkItem) * items.size(), cudaMemcpyHostToDevice, s),
+           "upload items");
   }
   step(cudaMemsetAsync(gr->d_counters, 0, sizeof(unsigned long long) * nf, s), "zero counters");
   step(cudaStreamSynchronize(s), "graph create");
@@ -1908,15 +1949,202 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
     dfree(ctx, gr->block);
     return rc;
   }
-  for (int f = 0; f < num_factors; ++f) {
-    factors[f].source->refs.fetch_add(1);
-    factors[f].target->refs.fetch_add(1);
-    gr->clouds.push_back(factors[f].source);
-    gr->maps.push_back(factors[f].target);
-    gr->tgt_idx.push_back(factors[f].target_index);
-    gr->src_idx.push_back(factors[f].source_index);
+  for (int k = 0; k < count; ++k) {
+    const vgicp_factor_desc& d = factors[first + k];
+    d.source->refs.fetch_add(1);
+    d.target->refs.fetch_add(1);
+    gr->clouds.push_back(d.source);
+    gr->maps.push_back(d.target);
+    gr->tgt_idx.push_back(d.target_index);
+    gr->src_idx.push_back(d.source_index);
   }
   *out = gr.release();
+  return VGICP_OK;
+}
+
+static int graph_create_range(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses,
+                              int chunk, int first, int count, vgicp_graph* out) {
+  if (!ctx || !out || (num_factors > 0 && !factors)) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (num_factors < 0 || num_poses < 0) return fail(VGICP_E_INVALID_ARGUMENT, "negative size");
+  if (first < 0 || count < 0 || first + count > num_factors)
+    return fail(VGICP_E_INVALID_ARGUMENT, "factor range outside the factor list");
+  if (chunk <= 0) chunk = kDefaultChunk;
+  chunk = std::max(kFactorTile, (chunk + kFactorTile - 1) / kFactorTile * kFactorTile);
+  if (int rc = validate_factors(ctx, factors, num_factors, num_poses)) return rc;
+  DeviceGuard g(ctx->device);
+  if (int rc = ensure_tables_for_hash_mode(factors, num_factors)) return rc;
+  Decomp d;
+  decompose(ctx, factors, num_factors, chunk, d);
+  return graph_from(ctx, factors, num_poses, d, first, count, out);
+}
+
+int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses, int chunk,
+                       vgicp_graph* out) try {
+  return graph_create_range(ctx, factors, num_factors, num_poses, chunk, 0, num_factors, out);
+} catch (...) {
+  return api_exception();
+}
+
+int vgicp_graph_create_range(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_factors, int num_poses,
+                             int chunk, int first, int count, vgicp_graph* out) try {
+  return graph_create_range(ctx, factors, num_factors, num_poses, chunk, first, count, out);
+} catch (...) {
+  return api_exception();
+}
+
+// Contiguous [begin, end) factor ranges, one per shard, balanced by Σ source points (the split of
+// paper_2109_07073_b200/sharding.py: partition_factors).
+static std::vector<int> partition_bounds(const vgicp_factor_desc* factors, int F, int n) {
+  std::vector<double> cum(F);
+  double run = 0.0;
+  for (int f = 0; f < F; ++f) cum[f] = (run += static_cast<double>(factors[f].source->n));
+  std::vector<int> bounds{0};
+  for (int r = 1; r < n; ++r) {
+    const double target = run * r / n;
+    int b = static_cast<int>(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+    if (b < F && std::fabs(cum[b] - target) < std::fabs((b > 0 ? cum[b - 1] : 0.0) - target)) b = b + 1;
+    bounds.push_back(std::min(std::max(b, bounds.back()), F));
+  }
+  bounds.push_back(F);
+  return bounds;
+}
+
+int vgicp_graph_create_sharded(const vgicp_ctx* ctxs, int num_shards, const vgicp_factor_desc* const* factors,
+                               int num_factors, int num_poses, int chunk, vgicp_graph* out) try {
+  if (!ctxs || !out || !factors || num_shards <= 0) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (num_shards > kMaxShards) return fail(VGICP_E_INVALID_ARGUMENT, "at most 8 shards (one per device of a box)");
+  if (num_factors < 0 || num_poses < 0) return fail(VGICP_E_INVALID_ARGUMENT, "negative size");
+  for (int r = 0; r < num_shards; ++r) {
+    if (!ctxs[r] || (num_factors > 0 && !factors[r])) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+    if (int rc = validate_factors(ctxs[r], factors[r], num_factors, num_poses)) return rc;
+    for (int f = 0; f < num_factors; ++f)  // the lists must describe the same factors
+      if (factors[r][f].target_index != factors[0][f].target_index ||
+          factors[r][f].source_index != factors[0][f].source_index ||
+          factors[r][f].source->n != factors[0][f].source->n)
+        return fail(VGICP_E_INVALID_ARGUMENT, "shard factor lists differ");
+  }
+  if (chunk <= 0) chunk = kDefaultChunk;
+  chunk = std::max(kFactorTile, (chunk + kFactorTile - 1) / kFactorTile * kFactorTile);
+  vgicp_ctx root = ctxs[0];
+  for (int r = 0; r < num_shards; ++r) {
+    DeviceGuard gr(ctxs[r]->device);
+    if (int rc = ensure_tables_for_hash_mode(factors[r], num_factors)) return rc;
+  }
+  DeviceGuard g(root->device);
+  Decomp d;
+  decompose(root, factors[0], num_factors, chunk, d);  // the whole list's decomposition, for every shard
+  const std::vector<int> bounds = partition_bounds(factors[0], num_factors, num_shards);
+  auto parent = std::make_unique<vgicp_graph_s>();
+  auto cleanup = [&]() {
+    for (auto* sh : parent->shards) vgicp_graph_destroy(sh);
+    parent->shards.clear();
+  };
+  for (int r = 0; r < num_shards; ++r) {
+    Decomp dr;
+    const Decomp* use = &d;
+    if (r > 0) {  // the same chunking, with this shard's own device pointers
+      dr = d;
+      for (int f = 0; f < num_factors; ++f) {
+        const vgicp_factor_desc& x = factors[r][f];
+        dr.fd[f].blk = x.source->sblk;
+        dr.fd[f].blk64 = x.source->blk64;
+        dr.fd[f].map = d.rank ? x.target->dev_rank() : x.target->dev();
+      }
+      use = &dr;
+    }
+    DeviceGuard gr(ctxs[r]->device);
+    vgicp_graph sh = nullptr;
+    if (int rc = graph_from(ctxs[r], factors[r], num_poses, *use, bounds[r], bounds[r + 1] - bounds[r], &sh)) {
+      cleanup();
+      return rc;
+    }
+    parent->shards.push_back(sh);
+    parent->shard_first.push_back(bounds[r]);
+    cudaEvent_t ev = nullptr;
+    if (const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming); e != cudaSuccess) {
+      cleanup();
+      return cuda_fail(e, "cudaEventCreate");
+    }
+    parent->shard_events.push_back(ev);
+  }
+  parent->shard_first.push_back(num_factors);
+  // the root's assembly kernel reads the shards' blocks over peer memory (NVLink) when it can
+  parent->peer_ok = true;
+  for (int r = 1; r < num_shards; ++r) {
+    const int dev = ctxs[r]->device;
+    if (dev == root->device) continue;
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, root->device, dev);
+    if (!can) {
+      parent->peer_ok = false;
+      continue;
+    }
+    const cudaError_t e = cudaDeviceEnablePeerAccess(dev, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) parent->peer_ok = false;
+    cudaGetLastError();
+  }
+  if (std::getenv("VGICP_SHARD_COPY")) parent->peer_ok = false;  // measurement switch: gather by peer copies
+  if (const cudaError_t e = cudaEventCreateWithFlags(&parent->root_event, cudaEventDisableTiming); e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "cudaEventCreate");
+  }
+  parent->ctx = root;
+  parent->num_factors = num_factors;
+  parent->num_poses = num_poses;
+  parent->rank_lookup = d.rank;
+  for (auto* sh : parent->shards) parent->num_points += sh->num_points;
+  const size_t nf = std::max(num_factors, 1);
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t o_pose = carve(sizeof(double) * 12 * std::max(num_poses, 1));
+  const size_t o_out = carve(sizeof(double) * VGICP_LINEARIZED_DOUBLES * nf);
+  const size_t o_oi = carve(sizeof(int) * nf);
+  const size_t o_err = carve(sizeof(double) * nf);
+  if (const cudaError_t e = dmalloc(root, &parent->block, off); e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "cudaMallocAsync(graph)");
+  }
+  char* b = static_cast<char*>(parent->block);
+  parent->d_poses = reinterpret_cast<double*>(b + o_pose);
+  parent->d_out = reinterpret_cast<double*>(b + o_out);
+  parent->d_out_inl = reinterpret_cast<int*>(b + o_oi);
+  parent->d_err = reinterpret_cast<double*>(b + o_err);
+  for (int f = 0; f < num_factors; ++f) {
+    parent->tgt_idx.push_back(factors[0][f].target_index);
+    parent->src_idx.push_back(factors[0][f].source_index);
+  }
+  *out = parent.release();
+  return VGICP_OK;
+} catch (...) {
+  return api_exception();
+}
+
+int vgicp_graph_num_shards(vgicp_graph graph, int* num_shards) try {
+  if (!graph || !num_shards) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *num_shards = graph->shards.empty() ? 1 : static_cast<int>(graph->shards.size());
+  return VGICP_OK;
+} catch (...) {
+  return api_exception();
+}
+
+int vgicp_graph_shard_range(vgicp_graph graph, int shard, int* first, int* count) try {
+  if (!graph || !first || !count) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (graph->shards.empty()) {
+    if (shard != 0) return fail(VGICP_E_INVALID_ARGUMENT, "shard index out of range");
+    *first = 0;
+    *count = graph->num_factors;
+    return VGICP_OK;
+  }
+  if (shard < 0 || shard >= static_cast<int>(graph->shards.size()))
+    return fail(VGICP_E_INVALID_ARGUMENT, "shard index out of range");
+  *first = graph->shard_first[shard];
+  *count = graph->shard_first[shard + 1] - graph->shard_first[shard];
   return VGICP_OK;
 } catch (...) {
   return api_exception();
@@ -1924,7 +2152,10 @@ int vgicp_graph_create(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_
 
 int vgicp_graph_destroy(vgicp_graph graph) try {
   if (!graph) return VGICP_OK;
-  {
+  for (auto* sh : graph->shards) vgicp_graph_destroy(sh);
+  for (size_t r = 0; r < graph->shard_events.size(); ++r) cudaEventDestroy(graph->shard_events[r]);
+  if (graph->root_event) cudaEventDestroy(graph->root_event);
+  if (graph->ctx) {
     DeviceGuard g(graph->ctx->device);
     cudaStreamSynchronize(graph->ctx->stream);
     dfree(graph->ctx, graph->block);
@@ -1955,14 +2186,62 @@ int vgicp_graph_num_points(vgicp_graph graph, uint64_t* points) try {
   return api_exception();
 }
 
+// One factor pass (linearize or evaluate) at device poses d_poses12 (root memory). A plain graph
+// launches on its stream into d_res / d_inl. A sharded graph: the root stream marks the poses ready,
+// every shard waits for that, pulls the poses to its device, launches its range into its own
+// buffers and marks its event; the root stream waits for all shards. Then, when d_res != nullptr,
+// the shards' results are gathered into d_res / d_inl (root memory, factor order) on the root
+// stream; the assembly instead reads them in place over peer memory.
+static int graph_pass(vgicp_graph g, bool linearize, const double* d_poses12, double* d_res, int32_t* d_inl) {
+  if (g->shards.empty()) {
+    DeviceGuard dg(g->ctx->device);
+    if (g->num_items > 0) {
+      VG_CUDA(launch_factor(linearize, g->rank_lookup, g->d_factors, g->d_items, g->num_items, g->f64_begin, d_poses12,
+                            g->d_partials, g->d_part_inl, g->d_counters, g->next_epoch(), d_res, d_inl, g->ctx->stream));
+      g->ctx->launches += factor_launches(g);
+    } else if (g->num_factors > 0 && d_res) {  // zero-hit-free degenerate graph: all-zero blocks
+      VG_CUDA(cudaMemsetAsync(d_res, 0, sizeof(double) * (linearize ? VGICP_LINEARIZED_DOUBLES : 1) * g->num_factors,
+                              g->ctx->stream));
+    }
+    return VGICP_OK;
+  }
+  vgicp_ctx root = g->ctx;
+  cudaStream_t s0 = root->stream;
+  const size_t pose_bytes = sizeof(double) * 12 * g->num_poses;
+  {
+    DeviceGuard dg(root->device);
+    VG_CUDA(cudaEventRecord(g->root_event, s0));
+  }
+  for (size_t r = 0; r < g->shards.size(); ++r) {
+    vgicp_graph sh = g->shards[r];
+    DeviceGuard dg(sh->ctx->device);
+    cudaStream_t sr = sh->ctx->stream;
+    VG_CUDA(cudaStreamWaitEvent(sr, g->root_event, 0));
+    if (pose_bytes) VG_CUDA(cudaMemcpyAsync(sh->d_poses, d_poses12, pose_bytes, cudaMemcpyDefault, sr));
+    if (int rc = graph_pass(sh, linearize, sh->d_poses, linearize ? sh->d_out : sh->d_err, sh->d_out_inl)) return rc;
+    VG_CUDA(cudaEventRecord(g->shard_events[r], sr));
+  }
+  DeviceGuard dg(root->device);
+  for (size_t r = 0; r < g->shards.size(); ++r) VG_CUDA(cudaStreamWaitEvent(s0, g->shard_events[r], 0));
+  if (d_res) {
+    const size_t per = linearize ? VGICP_LINEARIZED_DOUBLES : 1;
+    for (size_t r = 0; r < g->shards.size(); ++r) {
+      vgicp_graph sh = g->shards[r];
+      if (sh->num_factors == 0) continue;
+      const size_t f0 = static_cast<size_t>(g->shard_first[r]);
+      VG_CUDA(cudaMemcpyAsync(d_res + f0 * per, linearize ? sh->d_out : sh->d_err, sizeof(double) * per * sh->num_factors,
+                              cudaMemcpyDefault, s0));
+      if (d_inl)
+        VG_CUDA(cudaMemcpyAsync(d_inl + f0, sh->d_out_inl, sizeof(int32_t) * sh->num_factors, cudaMemcpyDefault, s0));
+    }
+  }
+  return VGICP_OK;
+}
+
 int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, double* d_out, int32_t* d_inliers) try {
   if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_out || !d_inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
-  DeviceGuard g(graph->ctx->device);
-  VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, d_poses12, graph->d_partials,
-                        graph->d_part_inl, graph->d_counters, graph->next_epoch(), d_out, d_inliers, graph->ctx->stream));
-  graph->ctx->launches += factor_launches(graph);
-  return VGICP_OK;
+  return graph_pass(graph, true, d_poses12, d_out, d_inliers);
 } catch (...) {
   return api_exception();
 }
@@ -1970,11 +2249,7 @@ int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, dou
 int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, double* d_errors, int32_t* d_inliers) try {
   if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_errors || !d_inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
-  DeviceGuard g(graph->ctx->device);
-  VG_CUDA(launch_factor(false, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, d_poses12, graph->d_partials,
-                        graph->d_part_inl, graph->d_counters, graph->next_epoch(), d_errors, d_inliers, graph->ctx->stream));
-  graph->ctx->launches += factor_launches(graph);
-  return VGICP_OK;
+  return graph_pass(graph, false, d_poses12, d_errors, d_inliers);
 } catch (...) {
   return api_exception();
 }
@@ -2000,7 +2275,8 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
   const int nf = graph->num_factors;
   if (nf == 0) return VGICP_OK;
   const size_t pose_bytes = sizeof(double) * 12 * graph->num_poses;
-  const size_t res_bytes = linearize ? sizeof(double) * VGICP_LINEARIZED_DOUBLES * nf : sizeof(double) * nf;
+  const size_t per = linearize ? VGICP_LINEARIZED_DOUBLES : 1;
+  const size_t res_bytes = sizeof(double) * per * nf;
   const size_t inl_bytes = sizeof(int32_t) * nf;
   // Page-locked caller buffers: the kernel's epilogue stores each factor's block directly into host
   // memory (zero-copy), so the result transfer overlaps the launch instead of following it.
@@ -2011,7 +2287,7 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
   }();
   double* m_res = staged_only ? nullptr : static_cast<double*>(mapped_alias(out));
   auto* m_inl = staged_only ? nullptr : static_cast<int32_t*>(mapped_alias(inliers));
-  const bool zero_copy = m_res && m_inl;
+  const bool zero_copy = m_res && m_inl && graph->shards.empty();
   if (int rc = ensure_pinned(ctx, align_up(pose_bytes, 256) + (zero_copy ? 0 : align_up(res_bytes, 256) + inl_bytes)))
     return rc;
   char* h = static_cast<char*>(ctx->pinned);
@@ -2021,11 +2297,30 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
   const bool poses_pinned = mapped_alias(poses12) != nullptr;
   if (!poses_pinned) std::memcpy(h_poses, poses12, pose_bytes);
   VG_CUDA(cudaMemcpyAsync(graph->d_poses, poses_pinned ? poses12 : h_poses, pose_bytes, cudaMemcpyHostToDevice, s));
+  if (!graph->shards.empty()) {
+    // every shard's results go straight from its device to the host staging, on its own stream
+    if (int rc = graph_pass(graph, linearize, graph->d_poses, nullptr, nullptr)) return rc;
+    for (size_t r = 0; r < graph->shards.size(); ++r) {
+      vgicp_graph sh = graph->shards[r];
+      if (sh->num_factors == 0) continue;
+      DeviceGuard dg(sh->ctx->device);
+      const size_t f0 = static_cast<size_t>(graph->shard_first[r]);
+      VG_CUDA(cudaMemcpyAsync(h_res + f0 * per, linearize ? sh->d_out : sh->d_err, sizeof(double) * per * sh->num_factors,
+                              cudaMemcpyDeviceToHost, sh->ctx->stream));
+      VG_CUDA(cudaMemcpyAsync(h_inl + f0, sh->d_out_inl, sizeof(int32_t) * sh->num_factors, cudaMemcpyDeviceToHost,
+                              sh->ctx->stream));
+    }
+    for (auto* sh : graph->shards) {
+      DeviceGuard dg(sh->ctx->device);
+      VG_CUDA(cudaStreamSynchronize(sh->ctx->stream));
+    }
+    std::memcpy(out, h_res, res_bytes);
+    std::memcpy(inliers, h_inl, inl_bytes);
+    return VGICP_OK;
+  }
   double* d_res = zero_copy ? m_res : (linearize ? graph->d_out : graph->d_err);
   int32_t* d_inl = zero_copy ? m_inl : graph->d_out_inl;
-  VG_CUDA(launch_factor(linearize, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, graph->d_poses,
-                        graph->d_partials, graph->d_part_inl, graph->d_counters, graph->next_epoch(), d_res, d_inl, s));
-  ctx->launches += factor_launches(graph);
+  if (int rc = graph_pass(graph, linearize, graph->d_poses, d_res, d_inl)) return rc;
   if (!zero_copy) {
     VG_CUDA(cudaMemcpyAsync(h_res, d_res, res_bytes, cudaMemcpyDeviceToHost, s));
     VG_CUDA(cudaMemcpyAsync(h_inl, d_inl, inl_bytes, cudaMemcpyDeviceToHost, s));
@@ -2129,6 +2424,21 @@ int vgicp_graph_assembly_plan(vgicp_graph graph, const uint8_t* fixed, int* num_
   return api_exception();
 }
 
+// Linearization pass + device assembly into d_asm (root memory), enqueued on the root stream. A
+// sharded graph's assembly kernel reads the shards' blocks in place over peer memory (NVLink), or,
+// without peer access, from the root copy that graph_pass gathers.
+static int linearize_assemble(vgicp_graph graph, const double* d_poses12, double* d_asm) {
+  const int S = graph->num_slots, O = S + graph->num_pairs;
+  const bool gather = !graph->shards.empty() && !graph->peer_ok;
+  if (int rc = graph_pass(graph, true, d_poses12, graph->shards.empty() || gather ? graph->d_out : nullptr,
+                          graph->shards.empty() || gather ? graph->d_out_inl : nullptr))
+    return rc;
+  DeviceGuard g(graph->ctx->device);
+  VG_CUDA(launch_assemble(graph->d_out_ptr, graph->d_contrib, S, O, graph->blocks(), d_asm, graph->ctx->stream));
+  graph->ctx->launches += O > 0 ? 1 : 0;
+  return VGICP_OK;
+}
+
 int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, double* diag, double* offdiag,
                                     double* rhs) try {
   if (!graph || !poses12) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
@@ -2145,15 +2455,7 @@ int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, do
   double* h_asm = reinterpret_cast<double*>(h + align_up(pose_bytes, 256));
   std::memcpy(h, poses12, pose_bytes);
   VG_CUDA(cudaMemcpyAsync(graph->d_poses, h, pose_bytes, cudaMemcpyHostToDevice, s));
-  if (graph->num_items > 0) {
-    VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, graph->d_poses, graph->d_partials,
-                          graph->d_part_inl, graph->d_counters, graph->next_epoch(), graph->d_out, graph->d_out_inl, s));
-    ctx->launches += factor_launches(graph);
-  } else if (graph->num_factors > 0) {
-    VG_CUDA(cudaMemsetAsync(graph->d_out, 0, sizeof(double) * VGICP_LINEARIZED_DOUBLES * graph->num_factors, s));
-  }
-  VG_CUDA(launch_assemble(graph->d_out_ptr, graph->d_contrib, S, O, graph->d_out, graph->d_asm, s));
-  ctx->launches += O > 0 ? 1 : 0;
+  if (int rc = linearize_assemble(graph, graph->d_poses, graph->d_asm)) return rc;
   VG_CUDA(cudaMemcpyAsync(h_asm, graph->d_asm, asm_bytes, cudaMemcpyDeviceToHost, s));
   VG_CUDA(cudaStreamSynchronize(s));
   if (S > 0) std::memcpy(diag, h_asm, sizeof(double) * 36 * S);
@@ -2169,16 +2471,24 @@ int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_po
   if (!graph->plan) return fail(VGICP_E_INVALID_ARGUMENT, "no assembly plan (call vgicp_graph_assembly_plan)");
   const int S = graph->num_slots, O = S + graph->num_pairs;
   if (O > 0 && !d_assembled) return fail(VGICP_E_INVALID_ARGUMENT, "null output");
+  return linearize_assemble(graph, d_poses12, d_assembled);
+} catch (...) {
+  return api_exception();
+}
+
+int vgicp_graph_assemble_device(vgicp_graph graph, const double* d_blocks, double* d_assembled) try {
+  if (!graph) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  if (!graph->plan) return fail(VGICP_E_INVALID_ARGUMENT, "no assembly plan (call vgicp_graph_assembly_plan)");
+  const int S = graph->num_slots, O = S + graph->num_pairs;
+  if (O > 0 && (!d_assembled || (graph->num_factors > 0 && !d_blocks)))
+    return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  ShardBlocks b{};
+  b.n = 1;
+  b.first[0] = 0;
+  b.first[1] = graph->num_factors;
+  b.out[0] = d_blocks;
   DeviceGuard g(graph->ctx->device);
-  cudaStream_t s = graph->ctx->stream;
-  if (graph->num_items > 0) {
-    VG_CUDA(launch_factor(true, graph->rank_lookup, graph->d_factors, graph->d_items, graph->num_items, graph->f64_begin, d_poses12, graph->d_partials,
-                          graph->d_part_inl, graph->d_counters, graph->next_epoch(), graph->d_out, graph->d_out_inl, s));
-    graph->ctx->launches += factor_launches(graph);
-  } else if (graph->num_factors > 0) {
-    VG_CUDA(cudaMemsetAsync(graph->d_out, 0, sizeof(double) * VGICP_LINEARIZED_DOUBLES * graph->num_factors, s));
-  }
-  VG_CUDA(launch_assemble(graph->d_out_ptr, graph->d_contrib, S, O, graph->d_out, d_assembled, s));
+  VG_CUDA(launch_assemble(graph->d_out_ptr, graph->d_contrib, S, O, b, d_assembled, graph->ctx->stream));
   graph->ctx->launches += O > 0 ? 1 : 0;
   return VGICP_OK;
 } catch (...) {
@@ -2197,11 +2507,25 @@ int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* in
   if (int rc = ensure_pinned(ctx, align_up(err_bytes, 256) + sizeof(int32_t) * nf)) return rc;
   auto* h_err = static_cast<double*>(ctx->pinned);
   auto* h_inl = reinterpret_cast<int32_t*>(static_cast<char*>(ctx->pinned) + align_up(err_bytes, 256));
-  // strided gather of out[f·121 + 120] (the error member of each block)
-  VG_CUDA(cudaMemcpy2DAsync(h_err, sizeof(double), graph->d_out + (VGICP_LINEARIZED_DOUBLES - 1),
-                            sizeof(double) * VGICP_LINEARIZED_DOUBLES, sizeof(double), nf, cudaMemcpyDeviceToHost, s));
-  VG_CUDA(cudaMemcpyAsync(h_inl, graph->d_out_inl, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, s));
-  VG_CUDA(cudaStreamSynchronize(s));
+  // strided gather of out[f·121 + 120] (the error member of each block): from the graph's blocks, or
+  // from every shard's own blocks, each on its stream (after its last pass)
+  const std::vector<vgicp_graph> parts = graph->shards.empty() ? std::vector<vgicp_graph>{graph} : graph->shards;
+  for (size_t r = 0; r < parts.size(); ++r) {
+    vgicp_graph sh = parts[r];
+    if (sh->num_factors == 0) continue;
+    const size_t f0 = graph->shards.empty() ? 0 : static_cast<size_t>(graph->shard_first[r]);
+    DeviceGuard dg(sh->ctx->device);
+    cudaStream_t sr = sh->ctx->stream;
+    VG_CUDA(cudaMemcpy2DAsync(h_err + f0, sizeof(double), sh->d_out + (VGICP_LINEARIZED_DOUBLES - 1),
+                              sizeof(double) * VGICP_LINEARIZED_DOUBLES, sizeof(double), sh->num_factors,
+                              cudaMemcpyDeviceToHost, sr));
+    VG_CUDA(cudaMemcpyAsync(h_inl + f0, sh->d_out_inl, sizeof(int32_t) * sh->num_factors, cudaMemcpyDeviceToHost, sr));
+  }
+  for (auto* sh : parts) {
+    DeviceGuard dg(sh->ctx->device);
+    VG_CUDA(cudaStreamSynchronize(sh->ctx->stream));
+  }
+  (void)s;
   std::memcpy(errors, h_err, err_bytes);
   std::memcpy(inliers, h_inl, sizeof(int32_t) * nf);
   return VGICP_OK;

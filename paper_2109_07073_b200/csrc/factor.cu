@@ -641,14 +641,17 @@ __global__ void gicp_error_kernel(const double* __restrict__ in, double* __restr
 // factor order starting from zero — the reference's `block += H` sequence, so the assembled system
 // is bit-identical to a host assembly of the same factor blocks.
 __global__ void assemble_kernel(const int* __restrict__ out_ptr, const int* __restrict__ contrib, int num_slots,
-                                int num_outputs, const double* __restrict__ blocks, double* __restrict__ assembled) {
+                                int num_outputs, const ShardBlocks blocks, double* __restrict__ assembled) {
   const int o = blockIdx.x;
   const int t = threadIdx.x;
   if (t >= 42 || (t >= 36 && o >= num_slots)) return;
   double sum = 0.0;
   for (int c = out_ptr[o]; c < out_ptr[o + 1]; ++c) {
     const int code = contrib[c];
-    const double* B = blocks + (size_t)(code >> 2) * VGICP_LINEARIZED_DOUBLES;
+    const int f = code >> 2;
+    int r = 0;  // the shard holding factor f (a peer device's memory for a sharded graph)
+    while (r + 1 < blocks.n && f >= blocks.first[r + 1]) ++r;
+    const double* B = blocks.out[r] + (size_t)(f - blocks.first[r]) * VGICP_LINEARIZED_DOUBLES;
     const int kind = code & 3;
     double v;
     if (t < 36) {
@@ -664,7 +667,7 @@ __global__ void assemble_kernel(const int* __restrict__ out_ptr, const int* __re
 }  // namespace
 
 cudaError_t launch_assemble(const int* out_ptr, const int* contrib, int num_slots, int num_outputs,
-                            const double* blocks, double* assembled, cudaStream_t s) {
+                            const ShardBlocks& blocks, double* assembled, cudaStream_t s) {
   if (num_outputs <= 0) return cudaSuccess;
   assemble_kernel<<<num_outputs, 64, 0, s>>>(out_ptr, contrib, num_slots, num_outputs, blocks, assembled);
   return cudaGetLastError();

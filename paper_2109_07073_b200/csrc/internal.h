@@ -250,8 +250,16 @@ cudaError_t launch_overlap_multi(const OverlapItem* items, const int2* chunks, i
 // assemble_normal_equations (block_solver.cpp:14-62) from F×121 factor blocks: output o < S is
 // slot o's diagonal block (+ rhs), o >= S the off-diagonal pair o - S; contrib codes f·4 + kind
 // (0 H_ii/b_i, 1 H_jj/b_j, 2 H_ij, 3 H_ijᵀ) listed per output in factor order.
+// The blocks of factors [first[r], first[r + 1]) live at out[r] (factor first[r] + k at row k): the
+// shards of a sharded graph, read over peer memory; a plain graph is one shard.
+constexpr int kMaxShards = 8;
+struct ShardBlocks {
+  int n;
+  int first[kMaxShards + 1];
+  const double* out[kMaxShards];
+};
 cudaError_t launch_assemble(const int* out_ptr, const int* contrib, int num_slots, int num_outputs,
-                            const double* blocks, double* assembled, cudaStream_t s);
+                            const ShardBlocks& blocks, double* assembled, cudaStream_t s);
 // Damped block Cholesky of the assembled reduced system (solver.cu; solve_block_system,
 // block_solver.cpp:64-122) over a reverse Cuthill-McKee order: perm[pos] = slot, reach[k] = last
 // block row of column k's envelope, per-column lower blocks (col_ent.x = row offset | transposed
@@ -449,4 +457,26 @@ struct vgicp_graph_s {
   int band_bw = -1;
   int band_epoch = 0;
   bool rank_lookup = false;  // factor kernels probe occupancy bitmaps (every target map has one)
+  // sharded graph (vgicp_graph_create_sharded): the shards are plain graphs, each on its own
+  // context, linearizing factors [shard_first[r], shard_first[r + 1]); this graph (on shard 0's
+  // context, the root) plans, assembles (reading the shards' blocks over peer memory) and solves
+  std::vector<vgicp_graph> shards;
+  std::vector<int> shard_first;
+  std::vector<cudaEvent_t> shard_events;  // on each shard's stream: its pass is done
+  cudaEvent_t root_event = nullptr;       // on the root stream: the poses are in place
+  bool peer_ok = true;                    // the root can read every shard's memory directly
+  vgicp::ShardBlocks blocks() const {
+    vgicp::ShardBlocks b{};
+    if (shards.empty()) {
+      b.n = 1;
+      b.first[0] = 0;
+      b.first[1] = num_factors;
+      b.out[0] = d_out;
+      return b;
+    }
+    b.n = static_cast<int>(shards.size());
+    for (int r = 0; r <= b.n; ++r) b.first[r] = shard_first[r];
+    for (int r = 0; r < b.n; ++r) b.out[r] = peer_ok ? shards[r]->d_out : d_out + (size_t)shard_first[r] * 121;
+    return b;
+  }
 };

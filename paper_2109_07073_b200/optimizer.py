@@ -414,9 +414,12 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
     def linearize_system(at, which=0):
         if dev is not None:
             d_asm = d_asms[which]
-            d_poses.copy_(torch.from_numpy(np.ascontiguousarray(at)))
-            graph.linearize_assembled_device(d_poses.data_ptr(), d_asm.data_ptr())
-            graph.ctx.synchronize()  # the context stream may differ from torch's current stream
+            if hasattr(graph, "linearize_assembled_at"):  # a graph split across processes (sharding.py)
+                graph.linearize_assembled_at(at, d_asm.data_ptr())
+            else:
+                d_poses.copy_(torch.from_numpy(np.ascontiguousarray(at)))
+                graph.linearize_assembled_device(d_poses.data_ptr(), d_asm.data_ptr())
+                graph.ctx.synchronize()  # the context stream may differ from torch's current stream
             return (d_asm[: S * 36].view(S, 6, 6), d_asm[S * 36:(S + P) * 36].view(P, 6, 6),
                     d_asm[(S + P) * 36:].view(S, 6))
         if device_assembly:

@@ -669,6 +669,63 @@ class FactorGraph(_Handle):
         self.num_poses = int(num_poses)
         self._ij = np.array([[f.target_index, f.source_index] for f in self.factors], np.int64).reshape(-1, 2)
 
+    @classmethod
+    def _adopt(cls, ctx: "Context", handle: C.c_void_p, factors, num_poses: int, keep=()) -> "FactorGraph":
+        g = cls.__new__(cls)
+        _Handle.__init__(g, ctx, handle)
+        g.factors = list(factors)
+        g.num_poses = int(num_poses)
+        g._ij = np.array([[f.target_index, f.source_index] for f in g.factors], np.int64).reshape(-1, 2)
+        g._keep = keep  # handles the C graph references (replicated clouds / maps of other shards)
+        return g
+
+    @classmethod
+    def create_range(cls, factors: Sequence[MatchingCostFactor], num_poses: int, first: int, count: int,
+                     chunk: int = 0, ctx: "Context | None" = None) -> "FactorGraph":
+        """vgicp_graph_create_range: factors [first, first + count) of the list under the WHOLE list's
+        work decomposition (per-factor blocks bit-identical to FactorGraph(factors)); one rank's share
+        of a graph split across processes. Its blocks are indexed 0..count-1."""
+        factors = list(factors)
+        ctx = ctx or (factors[0].source_points.ctx if factors else default_context())
+        descs = (FactorDesc * max(len(factors), 1))(*[f.desc() for f in factors])
+        h = C.c_void_p()
+        check(_lib.load().vgicp_graph_create_range(ctx.handle, descs, len(factors), int(num_poses), int(chunk),
+                                                   int(first), int(count), C.byref(h)))
+        return cls._adopt(ctx, h, factors[first:first + count], num_poses, keep=(factors,))
+
+    @classmethod
+    def sharded(cls, factor_lists: Sequence[Sequence[MatchingCostFactor]], num_poses: int,
+                chunk: int = 0) -> "FactorGraph":
+        """vgicp_graph_create_sharded: ONE graph split over several contexts (devices).
+        factor_lists[r] holds the same factors with context r's handles (clouds / maps replicated);
+        context 0 is the root. Every method works as on a single-context graph, with bit-identical
+        results (the root's assembly reads the shards' blocks over peer memory)."""
+        lists = [list(fl) for fl in factor_lists]
+        if not lists or any(len(fl) != len(lists[0]) for fl in lists):
+            raise ValueError("one factor list of equal length per shard")
+        ctxs = [fl[0].source_points.ctx if fl else default_context() for fl in lists]
+        n = len(lists[0])
+        arrays = [(FactorDesc * max(n, 1))(*[f.desc() for f in fl]) for fl in lists]
+        ptrs = (C.c_void_p * len(lists))(*[C.cast(a, C.c_void_p) for a in arrays])
+        hs = (C.c_void_p * len(lists))(*[c.handle for c in ctxs])
+        h = C.c_void_p()
+        check(_lib.load().vgicp_graph_create_sharded(hs, len(lists), ptrs, n, int(num_poses), int(chunk), C.byref(h)))
+        return cls._adopt(ctxs[0], h, lists[0], num_poses, keep=(lists, ctxs))
+
+    def num_shards(self) -> int:
+        v = C.c_int()
+        check(_lib.load().vgicp_graph_num_shards(self._h, C.byref(v)))
+        return int(v.value)
+
+    def shard_range(self, shard: int) -> tuple[int, int]:
+        a, b = C.c_int(), C.c_int()
+        check(_lib.load().vgicp_graph_shard_range(self._h, int(shard), C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
+    def assemble_device(self, d_blocks: int, d_assembled: int) -> None:
+        """vgicp_graph_assemble_device: assemble F×121 blocks given in device memory (factor order)."""
+        check(_lib.load().vgicp_graph_assemble_device(self._h, C.c_void_p(d_blocks), C.c_void_p(d_assembled)))
+
     def num_factors(self) -> int:
         return len(self.factors)
 

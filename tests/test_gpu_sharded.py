@@ -1,0 +1,126 @@
+"""Multi-GPU split of ONE graph behind the C ABI, exercised on one GPU: several
+contexts on device 0 stand in for the devices of a box (the code path is the same — per-shard
+streams, cross-stream events, the root's assembly kernel reading the shards' blocks through their
+device pointers). Bar: bit-identical to the single-context graph — blocks, errors, assembled
+systems and the native LM's trace and poses."""
+import numpy as np
+import pytest
+import torch
+
+import oracle_ctypes as O
+
+V = pytest.importorskip("paper_2109_07073_b200")
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(ctxs, nframes=9, n=2500, seed=501):
+    """The same clouds / maps replicated on every context; factors (j-d -> j) plus loop closures."""
+    rng = O.Rng(seed)
+    data = []
+    for _ in range(nframes):
+        m, c = rng.gaussian_cloud(n, 10.0)
+        data.append((m.astype(np.float32), V.cov6_from(c)))
+    links = [(j - d, j) for j in range(1, nframes) for d in (1, 2) if j - d >= 0] + [(nframes - 1, 0), (5, 1)]
+    lists = []
+    for ctx in ctxs:
+        clouds = V.PointCloud.upload_batch([d[0] for d in data], [d[1] for d in data], ctx)
+        maps = V.GaussianVoxelMap.build_batch(clouds, [1.0] * nframes)
+        lists.append([V.MatchingCostFactor(i, j, clouds[j], maps[i]) for i, j in links])
+    poses = np.stack([rng.random_pose(0.05, 0.5) for _ in range(nframes)])
+    return lists, poses
+
+
+@pytest.fixture(scope="module")
+def ctxs():
+    return [V.default_context(0), V.Context(0), V.Context(0)]
+
+
+def test_range_graphs_tile_the_full_graph(ctxs):
+    lists, poses = _problem(ctxs[:1])
+    full = V.FactorGraph(lists[0], len(poses))
+    F = full.num_factors()
+    ref_raw, ref_inl = full.linearize_raw(poses)
+    ref_err, _ = full.evaluate(poses)
+    for cuts in ([0, F], [0, 5, F], [0, 1, 7, 12, F]):
+        raws, inls, errs = [], [], []
+        for a, b in zip(cuts, cuts[1:]):
+            g = V.FactorGraph.create_range(lists[0], len(poses), a, b - a)
+            assert g.num_factors() == b - a
+            r, i = g.linearize_raw(poses)
+            raws.append(r), inls.append(i), errs.append(g.evaluate(poses)[0])
+        assert np.array_equal(np.concatenate(raws), ref_raw) and np.array_equal(np.concatenate(inls), ref_inl)
+        assert np.array_equal(np.concatenate(errs), ref_err)
+
+
+@pytest.mark.parametrize("shards,copy", [(2, False), (3, False), (2, True)])
+def test_sharded_graph_bit_identical(ctxs, monkeypatch, shards, copy):
+    if copy:  # gather by peer copies instead of reading the shards' blocks in place
+        monkeypatch.setenv("VGICP_SHARD_COPY", "1")
+    use = ctxs[:shards]
+    lists, poses = _problem(use)
+    full = V.FactorGraph(lists[0], len(poses))
+    sh = V.FactorGraph.sharded(lists, len(poses))
+    assert sh.num_shards() == shards
+    ranges = [sh.shard_range(r) for r in range(shards)]
+    assert ranges[0][0] == 0 and sum(c for _, c in ranges) == full.num_factors()
+    assert sh.num_points() == full.num_points()
+    a, ai = full.linearize_raw(poses)
+    b, bi = sh.linearize_raw(poses)
+    assert np.array_equal(a, b) and np.array_equal(ai, bi)
+    assert np.array_equal(full.evaluate(poses)[0], sh.evaluate(poses)[0])
+    # device variants return root-device memory
+    F = full.num_factors()
+    dp = torch.from_numpy(np.ascontiguousarray(poses)).cuda()
+    d1 = torch.empty((F, 121), dtype=torch.float64, device="cuda")
+    d2 = torch.empty_like(d1)
+    i1 = torch.empty(F, dtype=torch.int32, device="cuda")
+    i2 = torch.empty_like(i1)
+    torch.cuda.synchronize()
+    full.linearize_device(dp.data_ptr(), d1.data_ptr(), i1.data_ptr())
+    sh.linearize_device(dp.data_ptr(), d2.data_ptr(), i2.data_ptr())
+    full.ctx.synchronize()
+    sh.ctx.synchronize()
+    assert torch.equal(d1, d2) and torch.equal(i1, i2)
+    # assembled systems (the root reads the shards' blocks) and the linearization's errors
+    fixed = np.zeros(len(poses), np.uint8)
+    fixed[0] = 1
+    full.assembly_plan(fixed)
+    sh.assembly_plan(fixed)
+    for x, y in zip(full.linearize_assembled(poses), sh.linearize_assembled(poses)):
+        assert np.array_equal(x, y)
+    assert np.array_equal(full.linearized_errors()[0], sh.linearized_errors()[0])
+    # the native LM (vgicp_graph_optimize) on the sharded graph: the same trace and poses
+    from paper_2109_07073_b200 import optimizer as LM
+
+    monkeypatch.setenv("VGICP_LM_NO_HOST_BAND", "1")  # the device band solver on the root
+    p1, r1 = LM.optimize_native(full, poses)
+    p2, r2 = LM.optimize_native(sh, poses)
+    assert [(t.error, t.lam, t.accepted) for t in r1.trace] == [(t.error, t.lam, t.accepted) for t in r2.trace]
+    assert r1.reason == r2.reason and r1.final_error == r2.final_error and np.array_equal(p1, p2)
+
+
+def test_assemble_external_blocks_equals_device_assembly(ctxs):
+    """vgicp_graph_assemble_device over blocks produced elsewhere (here: the concatenated range
+    graphs' blocks, as gathered over NCCL from the ranks) == linearize_assembled_device."""
+    lists, poses = _problem(ctxs[:1])
+    full = V.FactorGraph(lists[0], len(poses))
+    plan = full.assembly_plan(np.eye(1, len(poses), dtype=np.uint8)[0])
+    S, P = plan.num_slots, len(plan.pairs)
+    F = full.num_factors()
+    dp = torch.from_numpy(np.ascontiguousarray(poses)).cuda()
+    a1 = torch.empty((S + P) * 36 + S * 6, dtype=torch.float64, device="cuda")
+    a2 = torch.empty_like(a1)
+    torch.cuda.synchronize()
+    full.linearize_assembled_device(dp.data_ptr(), a1.data_ptr())
+    full.ctx.synchronize()
+    blocks = torch.empty((F, 121), dtype=torch.float64, device="cuda")
+    inl = torch.empty(F, dtype=torch.int32, device="cuda")
+    half = F // 2
+    for a, b in ((0, half), (half, F)):
+        g = V.FactorGraph.create_range(lists[0], len(poses), a, b - a)
+        g.linearize_device(dp.data_ptr(), blocks[a:b].data_ptr(), inl[a:b].data_ptr())
+        g.ctx.synchronize()
+    full.assemble_device(blocks.data_ptr(), a2.data_ptr())
+    full.ctx.synchronize()
+    assert torch.equal(a1, a2)

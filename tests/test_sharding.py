@@ -196,3 +196,88 @@ def test_sharded_graph_with_gpu_factor_graph_world1():
         dist.destroy_process_group()
     assert r1.iterations == r2.iterations and r1.final_error == r2.final_error
     assert np.array_equal(p1, p2)
+
+
+class _OracleRankShare:
+    """A rank's share served by the CPU oracle: blocks(poses) -> [count, 122] rows (block + inliers),
+    the RankShare interface (stand-in for FactorGraph.create_range on the rank's GPU)."""
+
+    device = "cpu"
+
+    def __init__(self, frames, maps, ij):
+        self.inner = _OracleShard(frames, maps, ij)
+
+    def blocks(self, poses):
+        raw, inl = self.inner.linearize_raw(poses.numpy())
+        return torch.from_numpy(np.concatenate([raw, inl[:, None].astype(np.float64)], axis=1))
+
+
+def _gathered_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2109_07073_b200 import optimizer as LM
+    from paper_2109_07073_b200.sharding import GatheredGraph
+
+    frames, maps, ij, init = _lm_problem()
+    parts = partition_factors([len(frames[j][0]) for _, j in ij], world)
+    b, e = parts[rank]
+    g = GatheredGraph(_OracleRankShare(frames, maps, ij[b:e]), [p[1] - p[0] for p in parts], len(init), ij)
+    if rank == 0:
+        poses, rep = LM.optimize(g, init, settings=LM.LmSettings(max_iterations=5), device_assembly=False,
+                                 gpu_solve=False)
+        raw, inl = g.linearize_raw(poses)  # one more gathered step: the blocks themselves
+        g.stop()
+        q.put((poses, rep.iterations, rep.final_error, [(t.error, t.lam, t.accepted) for t in rep.trace], raw, inl))
+    else:
+        q.put(("served", g.serve()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_gathered_lm_world2_matches_single_process():
+    """One process per device (the torchrun path): rank 1 serves its share's linearizations, rank 0
+    gathers every step's blocks in factor order and runs the LM on them — the gathered blocks, the
+    trace and the poses equal the single-process run bit for bit (world size 2, gloo)."""
+    from paper_2109_07073_b200 import optimizer as LM
+
+    frames, maps, ij, init = _lm_problem()
+    single = _OracleShard(frames, maps, ij)
+
+    class _Full:
+        _ij = np.asarray(ij)
+        num_poses = len(init)
+
+        def linearize_raw(self, poses):
+            return single.linearize_raw(poses)
+
+        def total_error(self, poses):
+            raw, _ = single.linearize_raw(poses)
+            return float(np.cumsum(raw[:, 120])[-1])
+
+    ref_poses, ref = LM.optimize(_Full(), init, settings=LM.LmSettings(max_iterations=5), device_assembly=False,
+                                 gpu_solve=False)
+    ref_raw, ref_inl = single.linearize_raw(ref_poses)
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gathered_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    root = [r for r in results if not isinstance(r[0], str)][0]
+    served = [r for r in results if isinstance(r[0], str)][0]
+    poses, its, err, trace, raw, inl = root
+    assert its == ref.iterations and err == ref.final_error
+    assert trace == [(t.error, t.lam, t.accepted) for t in ref.trace]
+    assert np.array_equal(poses, ref_poses)
+    assert np.array_equal(raw, ref_raw) and np.array_equal(inl, ref_inl)
+    assert served[1] >= ref.iterations + 1  # rank 1 linearized its share at every step
