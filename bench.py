@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--no-extra", action="store_true", help="skip the C1 / C4 legs")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu / e2e legs)")
     p.add_argument("--no-c5", action="store_true", help="skip the C5 (1,000-frame multi-resolution) leg")
+    p.add_argument("--strong", action="store_true",
+                   help="run the strong-scaling legs (one C3 / C5 graph split across the ranks) also at N=1")
     return p.parse_args()
 
 
@@ -545,6 +547,66 @@ def run_submap(ctx, wl, threads, frames=20, reps=5):
     return out
 
 
+# ------------------------------------------------------------------------------ strong scaling
+def run_strong(wl, world, rank, dev, lm_iterations=30, steps=20):
+    """ONE graph split across the torchrun ranks (north star: 'factors shard across the
+    GPUs ... blocks gathered to the host solver over NVLink/NCCL'): rank r linearizes its contiguous,
+    point-balanced factor range (FactorGraph.create_range: the whole list's work decomposition, so the
+    blocks are bit-identical to one GPU's), every step's [F_r, 122] rows are gathered to rank 0 over one
+    NCCL gather, and rank 0 assembles them on its device and runs the LM (sharding.GatheredGraph). Wall
+    clock on rank 0; every step is synchronous across ranks, so it is the max over ranks."""
+    import torch
+
+    import paper_2109_07073_b200 as V
+    from paper_2109_07073_b200 import optimizer as LM
+    from paper_2109_07073_b200.sharding import GatheredGraph, RankShare, partition_factors
+
+    F = wl.num_factors
+    parts = partition_factors([len(wl.scans.means[j]) for _, j in wl.links], world)
+    first, end = parts[rank]
+    share_graph = V.FactorGraph.create_range(wl.factors, len(wl.poses), first, end - first, ctx=wl.ctx)
+    gg = GatheredGraph(RankShare(share_graph, first, end - first, dev), [b - a for a, b in parts], len(wl.poses),
+                       wl.links, root_graph=wl.graph if rank == 0 else None)
+    if rank != 0:
+        gg.serve()
+        return None
+    P = np.ascontiguousarray(wl.poses)
+    for _ in range(3):
+        gg._step(P)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        rows = gg._step(P)
+    torch.cuda.synchronize()
+    ms_pass = 1e3 * (time.perf_counter() - t0) / steps
+    ref_raw, ref_inl = wl.graph.linearize_raw(P)  # the same blocks from the whole graph on rank 0
+    identical = bool(np.array_equal(rows[:, :121].cpu().numpy(), ref_raw) and
+                     np.array_equal(rows[:, 121].cpu().numpy().astype(np.int32), ref_inl))
+    LM.optimize(gg, P, settings=LM.LmSettings(max_iterations=2))  # warm-up (plan, solver)
+    _, rep = LM.optimize(gg, P, settings=LM.LmSettings(max_iterations=lm_iterations))
+    its = sorted(rep.iteration_seconds)
+    gg.stop()
+    return {"factors": F, "ranks": world, "shares": [b - a for a, b in parts], "ms_per_linearize_pass": ms_pass,
+            "factors_per_s": F / (ms_pass * 1e-3), "blocks_identical_to_single_gpu": identical,
+            "lm_iterations": rep.iterations, "lm_reason": rep.reason, "lm_final_error": rep.final_error,
+            "ms_per_lm_iteration_median": 1e3 * its[len(its) // 2] if its else None,
+            "ms_per_lm_iteration_mean": 1e3 * sum(its) / len(its) if its else None,
+            "note": "one C3 graph split over the ranks: broadcast poses -> per-rank share linearize (one launch) -> "
+                    "NCCL gather of the F x 122 rows to rank 0 -> device assembly + damped solve on rank 0; "
+                    "wall clock on rank 0 (synchronous steps = max over ranks)"}
+
+
+def run_strong_c5(ctx, world, rank, dev, lm_iterations=10, steps=10):
+    """BASELINE config C5 (10,000 factors over 0.5 / 1 / 2 m maps, named at 8xB200) split across the
+    torchrun ranks like run_strong."""
+    from bench_workloads import workloads as W
+
+    wl = W.build_c5_workload(ctx)
+    out = run_strong(wl, world, rank, dev, lm_iterations=lm_iterations, steps=steps)
+    del wl
+    return out
+
+
 # ------------------------------------------------------------------------------ ours
 def run_ours(args):
     import torch
@@ -564,7 +626,9 @@ def run_ours(args):
     ctx = V.Context(local, stream=stream.cuda_stream)
     threads = max(1, (os.cpu_count() or 1) // max(world, 1))
     t_build0 = time.perf_counter()
-    wl = W.build_graph_workload(ctx, W.c3_spec(args.frames, args.points, seed=1 + rank), chunk=args.chunk, threads=threads)
+    # every rank builds the same C3 graph (seed 1): weak scaling runs one whole copy per rank, and the
+    # strong-scaling leg splits this one graph across the ranks
+    wl = W.build_graph_workload(ctx, W.c3_spec(args.frames, args.points, seed=1), chunk=args.chunk, threads=threads)
     t_build = time.perf_counter() - t_build0
     graph = wl.graph
     F = wl.num_factors
@@ -664,8 +728,18 @@ def run_ours(args):
     else:
         F_all, P_all, inl_all = float(F), float(P), float(inliers)
     ms_max, k_avg, eval_avg, e2e_ms = (float(x) for x in vals.tolist())
+    # strong scaling (every rank takes part; rank 0 reports): one C3 / C5 graph split across the ranks
+    strong = strong_c5 = None
+    if (world > 1 or args.strong) and not args.profile:
+        if not dist.is_initialized():  # N=1 with --strong: a one-rank NCCL group
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        strong = run_strong(wl, world, rank, dev, lm_iterations=30)
+        if not args.no_c5:
+            strong_c5 = run_strong_c5(ctx, world, rank, dev)
     if rank != 0:
-        if world > 1:
+        if dist.is_initialized():
             dist.destroy_process_group()
         return
 
@@ -741,12 +815,14 @@ def run_ours(args):
         "covariances_c3": cov,
         "submap_c3": sub,
         "c5_multires": c5,
+        "strong_c3": strong,
+        "strong_c5": strong_c5,
         "clocks": clk,
         "inlier_fraction": inliers / P,
         "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()} | {"total": round(t_build, 3)},
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -255,6 +255,18 @@ class GatheredGraph:
         self.root.ctx.synchronize()
 
 
+    def linearize_assembled(self, poses):
+        """Host copy of the assembled system (diag S×6×6, offdiag P×6×6, rhs S×6) at host poses."""
+        import torch
+
+        plan = self.root._plan
+        S, P = plan.num_slots, len(plan.pairs)
+        d_asm = torch.empty((S + P) * 36 + S * 6 + 1, dtype=torch.float64, device=self._device())
+        self.linearize_assembled_at(poses, d_asm.data_ptr())
+        a = d_asm.cpu().numpy()
+        return a[: S * 36].reshape(S, 6, 6), a[S * 36:(S + P) * 36].reshape(P, 6, 6), a[(S + P) * 36:(S + P) * 36 + S * 6].reshape(S, 6)
+
+
 def poses_array_np(poses) -> np.ndarray:
     P = np.asarray(poses, np.float64)
     return np.ascontiguousarray(P.reshape(-1, 12))

@@ -124,3 +124,38 @@ def test_assemble_external_blocks_equals_device_assembly(ctxs):
     full.assemble_device(blocks.data_ptr(), a2.data_ptr())
     full.ctx.synchronize()
     assert torch.equal(a1, a2)
+
+
+def test_gathered_graph_nccl_world1_matches_graph(ctxs):
+    """The torchrun path (sharding.GatheredGraph over NCCL) at world size 1 on this GPU: RankShare
+    (create_range) + the gather + the root's assembly of the gathered blocks give the same LM as the
+    graph itself, bit for bit."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2109_07073_b200 import optimizer as LM
+    from paper_2109_07073_b200.sharding import GatheredGraph, RankShare
+
+    lists, poses = _problem(ctxs[:1])
+    full = V.FactorGraph(lists[0], len(poses))
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(sock.getsockname()[1])
+    sock.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        F = full.num_factors()
+        share = RankShare(V.FactorGraph.create_range(lists[0], len(poses), 0, F), 0, F, torch.device("cuda", 0))
+        gg = GatheredGraph(share, [F], len(poses), full._ij, root_graph=full)
+        p1, r1 = LM.optimize(gg, poses)
+        raw, inl = gg.linearize_raw(poses)
+        gg.stop()
+    finally:
+        dist.destroy_process_group()
+    p2, r2 = LM.optimize(full, poses)
+    assert [(t.error, t.lam, t.accepted) for t in r1.trace] == [(t.error, t.lam, t.accepted) for t in r2.trace]
+    assert np.array_equal(p1, p2)
+    ref_raw, ref_inl = full.linearize_raw(poses)
+    assert np.array_equal(raw, ref_raw) and np.array_equal(inl, ref_inl)
