@@ -362,7 +362,7 @@ def _sequential_total(errors) -> float:
 
 
 def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None = None, device_assembly: bool = True,
-             gpu_solve: bool = True, speculative: bool = True, band_solve: bool | None = None):
+             gpu_solve: bool = True, speculative: bool = True, band_solve: bool | None = None, on_accept=None):
     """Run LM on `graph` from `poses` (num_poses × 12). Returns (poses, OptimizerReport).
 
     With device_assembly the normal equations are assembled on the GPU right after the
@@ -483,6 +483,8 @@ def optimize(graph: FactorGraph, poses, fixed=None, settings: LmSettings | None 
                 poses, updates = cand, cand_updates
                 any_accepted = accepted = True
                 report.trace.append(IterationRecord(it, cand_error, lam, step_norm, True))
+                if on_accept is not None:  # (iteration, accepted poses, damping used) — test / tooling hook
+                    on_accept(it, poses.copy(), lam)
                 current = cand_error
                 lam = max(lam * settings.lambda_decrease, 1e-12)
                 report.iterations += 1
