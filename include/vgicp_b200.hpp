@@ -75,6 +75,14 @@ class Context {
   std::shared_ptr<vgicp_ctx_s> h_;
 };
 
+// The reference's host PointCloud layout (point_cloud.hpp:21-37) for the float64 submap path.
+struct HostCloud {
+  std::vector<Vec3> means;
+  std::vector<Mat3> covariances;  // empty or one per point (row-major)
+  std::size_t size() const { return means.size(); }
+  bool has_covariances() const { return !covariances.empty() && covariances.size() == means.size(); }
+};
+
 // Device-resident PointCloud (point_cloud.hpp:21-37). means: n×3, cov6: n×(xx xy xz yy yz zz).
 class PointCloud {
  public:
@@ -85,6 +93,19 @@ class PointCloud {
     vgicp_cloud c = nullptr;
     check(vgicp_cloud_upload(ctx.get(), xyz.data(), cov6.empty() ? nullptr : cov6.data(), n, &c));
     h_.reset(c, [](vgicp_cloud x) { vgicp_cloud_destroy(x); });
+  }
+  // The reference's double layout: float32-exact clouds take the float32 layout, any other (submap
+  // clouds) is kept in float64 too, so keys / correspondences / overlap hits stay bit-exact.
+  PointCloud(const Context& ctx, const HostCloud& cloud) : ctx_(ctx) {
+    vgicp_cloud c = nullptr;
+    check(vgicp_cloud_upload_f64(ctx.get(), cloud.means.empty() ? nullptr : cloud.means[0].data(),
+                                 cloud.has_covariances() ? cloud.covariances[0].data() : nullptr, cloud.size(), &c));
+    h_.reset(c, [](vgicp_cloud x) { vgicp_cloud_destroy(x); });
+  }
+  bool is_f64() const {
+    int v = 0;
+    check(vgicp_cloud_is_f64(get(), &v));
+    return v != 0;
   }
   std::size_t size() const {
     std::size_t n = 0;
@@ -106,14 +127,6 @@ class PointCloud {
   PointCloud(const Context& ctx, vgicp_cloud c) : ctx_(ctx) { h_.reset(c, [](vgicp_cloud x) { vgicp_cloud_destroy(x); }); }
   Context ctx_;
   std::shared_ptr<vgicp_cloud_s> h_;
-};
-
-// The reference's host PointCloud layout (point_cloud.hpp:21-37) for the float64 submap path.
-struct HostCloud {
-  std::vector<Vec3> means;
-  std::vector<Mat3> covariances;  // empty or one per point (row-major)
-  std::size_t size() const { return means.size(); }
-  bool has_covariances() const { return !covariances.empty() && covariances.size() == means.size(); }
 };
 
 struct GaussianVoxel {  // voxelmap.hpp:18-22
@@ -415,6 +428,32 @@ class MatchingCostBatch {
     check(vgicp_graph_create(ctx.get(), d.data(), static_cast<int>(d.size()), num_poses, chunk, &g));
     h_.reset(g, [](vgicp_graph x) { vgicp_graph_destroy(x); });
   }
+  // ONE batch split over several devices (vgicp_graph_create_sharded): per_device[r] holds the same
+  // factors built on contexts[r] (clouds / maps replicated); every method below returns bit-identical
+  // results to the single-device batch.
+  MatchingCostBatch(const std::vector<Context>& contexts, const std::vector<std::vector<MatchingCostFactor>>& per_device,
+                    int num_poses, int chunk = 0)
+      : ctx_(contexts.at(0)), factors_(per_device.at(0)), num_poses_(num_poses), replicas_(per_device) {
+    if (contexts.size() != per_device.size()) throw std::invalid_argument("one factor list per context");
+    std::vector<std::vector<vgicp_factor_desc>> d(per_device.size());
+    std::vector<const vgicp_factor_desc*> lists;
+    std::vector<vgicp_ctx> cs;
+    for (std::size_t r = 0; r < per_device.size(); ++r) {
+      if (per_device[r].size() != factors_.size()) throw std::invalid_argument("factor lists differ in length");
+      for (const auto& f : per_device[r]) d[r].push_back(f.desc());
+      lists.push_back(d[r].data());
+      cs.push_back(contexts[r].get());
+    }
+    vgicp_graph g = nullptr;
+    check(vgicp_graph_create_sharded(cs.data(), static_cast<int>(cs.size()), lists.data(),
+                                     static_cast<int>(factors_.size()), num_poses, chunk, &g));
+    h_.reset(g, [](vgicp_graph x) { vgicp_graph_destroy(x); });
+  }
+  int num_shards() const {
+    int n = 0;
+    check(vgicp_graph_num_shards(h_.get(), &n));
+    return n;
+  }
   // linearize_all (optimizer.cpp:45-62), matching part, factor order
   std::vector<LinearizedFactor> linearize(const std::vector<Pose>& poses) const {
     const std::vector<double> P = flatten(poses);
@@ -526,6 +565,7 @@ class MatchingCostBatch {
   Context ctx_;
   std::vector<MatchingCostFactor> factors_;
   int num_poses_;
+  std::vector<std::vector<MatchingCostFactor>> replicas_;  // keeps the other devices' handles alive
   std::shared_ptr<vgicp_graph_s> h_;
 };
 

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) fast_mark_kernel(const FastBuildJob* __re
       if (ok) {
         word = ((rx >> 2) * nby + (ry >> 2)) * nbz + (rz >> 2);
         bit = ((rx & 3u) << 4) | ((ry & 3u) << 2) | (rz & 3u);
+        VG_CHECK(word < j.words);
       } else {
         bad = true;
       }
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(kMarkThreads) fast_markrank_smem_kernel(const 
       if (ok) {
         const unsigned word = ((rx >> 2) * nby + (ry >> 2)) * nbz + (rz >> 2);
         const unsigned bit = ((rx & 3u) << 4) | ((ry & 3u) << 2) | (rz & 3u);
+        VG_CHECK(word < words);
         atomicOr(&sbits[2 * word + (bit >> 5)], 1u << (bit & 31u));
         c = (word << 6) | bit;
       } else {
@@ -284,6 +286,7 @@ __global__ void __launch_bounds__(kOrderThreads) fast_order_kernel(const FastBui
       const unsigned i = base + u * kOrderThreads + threadIdx.x;
       if (i >= n) continue;
       const unsigned r = o[u].rank + static_cast<unsigned>(__popcll(o[u].bits & ((1ull << (c[u] & 63u)) - 1ull)));
+      VG_CHECK(r < V);
       pc[i] = r;
       atomicAdd(const_cast<unsigned*>(cnt + r), 1u);
     }
@@ -326,6 +329,7 @@ __global__ void __launch_bounds__(kOrderThreads) fast_order_kernel(const FastBui
       __syncwarp();
       if (i < n && (peers & lt) == 0u) cnt[r] += static_cast<unsigned>(__popc(peers));
       __syncwarp();
+      VG_CHECK(i >= n || pos < n);
       if (i < n) pl[pos] = i;
     }
 #pragma unroll
@@ -427,8 +431,12 @@ __global__ void __launch_bounds__(kRadixThreads) fast_sort_kernel(const FastBuil
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const unsigned i = base + u * kRadixThreads + threadIdx.x;
-      if (i < n)
-        src[i] = ((o[u].rank + static_cast<unsigned>(__popcll(o[u].bits & ((1ull << (c[u] & 63u)) - 1ull)))) << 16) | i;
+      if (i < n) {
+        VG_CHECK((c[u] >> 6) < j.words);
+        const unsigned r = o[u].rank + static_cast<unsigned>(__popcll(o[u].bits & ((1ull << (c[u] & 63u)) - 1ull)));
+        VG_CHECK(r < V && ((o[u].bits >> (c[u] & 63u)) & 1ull));
+        src[i] = (r << 16) | i;
+      }
     }
   }
   unsigned bits = 0;
@@ -447,6 +455,7 @@ __global__ void __launch_bounds__(kRadixThreads) fast_sort_kernel(const FastBuil
     for (unsigned i = b0; i < e0; ++i) {
       const unsigned key = src[i];
       unsigned short& slot = cnt[((key >> shift) & (kDigits - 1u)) * kRadixThreads + threadIdx.x];
+      VG_CHECK(slot < n);
       dst[slot] = key;
       ++slot;
     }
@@ -502,6 +511,7 @@ __global__ void __launch_bounds__(kAccThreads, 3) fast_accumulate_kernel(const F
   const unsigned nb = __shfl_down_sync(0xffffffffu, b, 1);
   const unsigned e = lane + 1 < nv ? nb : re;
   const unsigned rb = __shfl_sync(0xffffffffu, b, 0);
+  VG_CHECK(!act || (b < e && e <= j.n));  // every voxel holds >= 1 point
   // VoxelAccumulator::add (voxelmap.cpp:28-32) with KahanSum, component-wise; float32 clouds have
   // symmetric covariances, so the 6 unique second-moment sums equal the reference's 9 bit for bit
   double ms[3] = {0, 0, 0}, mc[3] = {0, 0, 0};
@@ -511,6 +521,8 @@ __global__ void __launch_bounds__(kAccThreads, 3) fast_accumulate_kernel(const F
     unsigned p[kStage / 32];
 #pragma unroll
     for (int u = 0; u < kStage / 32; ++u) p[u] = lane + 32 * u < cn ? pl[c0 + lane + 32 * u] : 0u;
+#pragma unroll
+    for (int u = 0; u < kStage / 32; ++u) VG_CHECK(p[u] < j.n);
 #pragma unroll
     for (int u = 0; u < kStage / 32; ++u) {
       if (lane + 32 * u < cn) {

@@ -249,6 +249,7 @@ __device__ __forceinline__ void finish_factor(const float* acc, int inl, int lan
       seen = prev;
     }
     last = (static_cast<unsigned>(want) == static_cast<unsigned>(fp->item_count * parts)) ? 1u : 0u;
+    VG_CHECK(static_cast<unsigned>(want) <= static_cast<unsigned>(fp->item_count * parts));
   }
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
@@ -397,6 +398,7 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
   const int warp = tid >> 5;
   const WorkItem w = items[blockIdx.x];  // `items` starts at this launch's first item
   const FactorDev* __restrict__ fp = factors + w.factor;
+  VG_CHECK(w.begin >= 0 && w.begin < w.end && w.end <= fp->n && w.begin % kPointBlock == 0);
   const PointBlock* __restrict__ gblk = fp->blk + w.begin / kPointBlock;
   // float64 means of the same blocks when the cloud is not float32-exact (submap clouds): the
   // transform reads them instead of the tile's float32 copies (warp-uniform branch)
@@ -651,6 +653,7 @@ __global__ void assemble_kernel(const int* __restrict__ out_ptr, const int* __re
     const int f = code >> 2;
     int r = 0;  // the shard holding factor f (a peer device's memory for a sharded graph)
     while (r + 1 < blocks.n && f >= blocks.first[r + 1]) ++r;
+    VG_CHECK(f >= blocks.first[r] && f < blocks.first[r + 1]);
     const double* B = blocks.out[r] + (size_t)(f - blocks.first[r]) * VGICP_LINEARIZED_DOUBLES;
     const int kind = code & 3;
     double v;

@@ -15,6 +15,25 @@
 
 namespace vgicp {
 
+// Device-side bounds checks of the debug build (make -C paper_2109_07073_b200/csrc debug, loaded with
+// VGICP_LIB=.../lib_debug/libvgicp_b200.so): a violated index invariant prints its site and traps the
+// kernel (the launch then fails with cudaErrorLaunchFailure / illegal instruction instead of reading
+// or writing out of bounds). Compiled out of the product build.
+#ifdef VGICP_DEBUG_BOUNDS
+#define VG_CHECK(cond)                                                                                  \
+  do {                                                                                                  \
+    if (!(cond)) {                                                                                      \
+      printf("VG_CHECK failed %s:%d block (%d,%d) thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, blockIdx.y, \
+             threadIdx.x, #cond);                                                                       \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define VG_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 constexpr unsigned long long kEmptyKey = ~0ull;  // valid keys use 63 bits (voxelmap.cpp:57-63)
 constexpr int kKeyBits = 21;                     // voxelmap.cpp:12
 constexpr double kKeyBias = 1048576.0;           // 2^20, voxelmap.cpp:13

@@ -168,6 +168,51 @@ int main() {
     REQUIRE(sub.cloud.has_covariances() && sub.voxels.size() > 0 && sub.voxels.total_points() == sub.cloud.size());
   }
 
+  // float64 host clouds keep their double values (not float32-exact -> a float64 device cloud)
+  {
+    HostCloud hc;
+    for (int i = 0; i < 500; ++i) {
+      hc.means.push_back({0.1 * i + 1e-9, 0.3 * (i % 11), 0.01 * (i % 17)});
+      hc.covariances.push_back({1, 0, 0, 0, 1, 0, 0, 0, 1e-3});
+    }
+    PointCloud c64(ctx, hc);
+    REQUIRE(c64.is_f64() && c64.size() == 500 && c64.has_covariances());
+    HostCloud h32;
+    for (int i = 0; i < 100; ++i) {
+      h32.means.push_back({static_cast<double>(xyz[3 * i]), static_cast<double>(xyz[3 * i + 1]), static_cast<double>(xyz[3 * i + 2])});
+      h32.covariances.push_back({1, 0, 0, 0, 1, 0, 0, 0, 1.0 / 1024});  // float32-exact (1e-3 is not)
+    }
+    REQUIRE(!PointCloud(ctx, h32).is_f64());
+  }
+
+  // ONE batch split over two contexts (two "devices"; here both on device 0): bit-identical blocks,
+  // errors and LM result (vgicp_graph_create_sharded)
+  {
+    Context ctx2(0);
+    auto cloud2 = std::make_shared<PointCloud>(ctx2, xyz, cov);
+    auto map2 = std::make_shared<GaussianVoxelMap>(*cloud2, 1.0);
+    auto mk = [&](const std::shared_ptr<PointCloud>& c, const std::shared_ptr<GaussianVoxelMap>& m) {
+      return std::vector<MatchingCostFactor>{MatchingCostFactor(0, 1, c, m), MatchingCostFactor(1, 2, c, m),
+                                             MatchingCostFactor(2, 0, c, m), MatchingCostFactor(0, 2, c, m)};
+    };
+    MatchingCostBatch single(ctx, mk(cloud, map), 3);
+    MatchingCostBatch sharded({ctx, ctx2}, {mk(cloud, map), mk(cloud2, map2)}, 3);
+    REQUIRE(sharded.num_shards() == 2);
+    const std::vector<Pose> poses = {Pose::Identity(), Pose::from({1, 0, 0, 0, 1, 0, 0, 0, 1}, {0.2, -0.1, 0.05}),
+                                     Pose::from({1, 0, 0, 0, 1, 0, 0, 0, 1}, {-0.1, 0.15, 0})};
+    const auto a = single.linearize(poses), b = sharded.linearize(poses);
+    for (std::size_t k = 0; k < a.size(); ++k) {
+      REQUIRE(a[k].inliers == b[k].inliers && a[k].error == b[k].error);
+      for (int e = 0; e < 36; ++e) REQUIRE(a[k].H_ij[e] == b[k].H_ij[e] && a[k].H_jj[e] == b[k].H_jj[e]);
+    }
+    REQUIRE(single.total_error(poses) == sharded.total_error(poses));
+    std::vector<Pose> p1 = poses, p2 = poses;
+    const auto r1 = single.optimize(p1, {1, 0, 0}), r2 = sharded.optimize(p2, {1, 0, 0});
+    REQUIRE(r1.final_error == r2.final_error && r1.iterations == r2.iterations);
+    for (int k = 0; k < 3; ++k)
+      for (int q = 0; q < 12; ++q) REQUIRE(p1[k].m[q] == p2[k].m[q]);
+  }
+
   std::printf("facade ok: voxels=%zu inliers=%d error=%.6f launches=%llu\n", map->size(), lin.inliers, lin.error,
               static_cast<unsigned long long>(ctx.launch_count()));
   return 0;
