@@ -17,9 +17,9 @@
 //   fast_accumulate  thread per voxel: Kahan fp64 sums over its list in input order — exactly the
 //                    reference's per-shard order (voxelmap.cpp:87-94), hence bit-identical statistics
 //                    — finalize, and write the rank-ordered fp32 voxel-local statistics (ra / rb,
-//                    the factor kernels' gather targets) and the fp64 covariance (6 unique entries,
-//                    the near-singular fallback). Key-ordered arrays (keys, counts, fp64 means) are
-//                    produced only on demand (export mode), by the same kernels.
+//                    the factor kernels' gather targets) and the fp64 covariance (the near-singular
+//                    fallback). Key-ordered arrays (keys, counts, fp64 means) are produced only on
+//                    demand (export mode), by the same kernels.
 //
 // Algorithmic bytes: 36 B per input point + 48 B per voxel written.
 #include <algorithm>
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kAccThreads, 3) fast_accumulate_kernel(const F
   __shared__ float4 sA[kAccWarps][kStage];
   __shared__ float4 sB[kAccWarps][kStage];
   __shared__ float sZ[kAccWarps][kStage];
-  __shared__ double stage[kAccWarps][32 * 6];  // the warp's fp64 covariances, written out coalesced
+  __shared__ double stage[kAccWarps][32 * 9];  // the warp's fp64 covariances, written out coalesced
   const FastBuildJob& j = jobs[blockIdx.y];
   const unsigned V = j.V;
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -590,8 +590,11 @@ __global__ void __launch_bounds__(kAccThreads, 3) fast_accumulate_kernel(const F
     a.cyz = static_cast<float>(cov[4]);
     j.ra[v] = a;
     j.rb[v] = SlotStatsB{static_cast<float>(cov[5]), static_cast<int>(v)};
+    {
+      const int full[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};  // row-major 3×3 from the unique entries
 #pragma unroll
-    for (int q = 0; q < 6; ++q) stage[warp][6 * lane + q] = cov[q];
+      for (int q = 0; q < 9; ++q) stage[warp][9 * lane + q] = cov[full[q]];
+    }
     if constexpr (kExport) {
       unsigned hi, lo;
       pack_key32(k0, k1, k2, hi, lo);
@@ -600,16 +603,12 @@ __global__ void __launch_bounds__(kAccThreads, 3) fast_accumulate_kernel(const F
       j.mean64[3 * static_cast<size_t>(v) + 0] = mean[0];
       j.mean64[3 * static_cast<size_t>(v) + 1] = mean[1];
       j.mean64[3 * static_cast<size_t>(v) + 2] = mean[2];
-      double* c9 = j.cov9 + 9 * static_cast<size_t>(v);
-      c9[0] = cov[0], c9[1] = cov[1], c9[2] = cov[2];
-      c9[3] = cov[1], c9[4] = cov[3], c9[5] = cov[4];
-      c9[6] = cov[2], c9[7] = cov[4], c9[8] = cov[5];
     }
   }
   __syncwarp();
-  // the warp's covariances leave as one contiguous, coalesced run of 6·nv doubles
-  double* __restrict__ dst = j.cov6 + 6 * static_cast<size_t>(v0);
-  for (unsigned t = lane; t < 6 * nv; t += 32) dst[t] = stage[warp][t];
+  // the warp's covariances leave as one contiguous, coalesced run of 9·nv doubles
+  double* __restrict__ dst = j.cov9 + 9 * static_cast<size_t>(v0);
+  for (unsigned t = lane; t < 9 * nv; t += 32) dst[t] = stage[warp][t];
 }
 
 // Hash table of a rank-numbered map (on demand): slot <- the statistics of its key's rank.

@@ -691,7 +691,6 @@ static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const do
     mp->inv_res = 1.0 / res[k];
     mp->total_points = c->n;
     mp->fast = true;
-    mp->cov_stride = 6;
     c->refs.fetch_add(1);
     mp->src = c;
     for (int a = 0; a < 3; ++a) mp->cmin[a] = cmin[a], mp->cmax[a] = cmax[a];
@@ -790,7 +789,7 @@ static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const do
       cleanup();
       return fail(VGICP_E_OUT_OF_RANGE, "point beyond the +-2^20 voxel-per-axis range limit");
     }
-  // per-map voxel arrays: ra | rb | cov6 (rank order)
+  // per-map voxel arrays: ra | rb | cov64 (rank order)
   unsigned max_v = 0, smem_v = fast_order_smem_voxels(ctx->device);
   const unsigned sort_n = std::getenv("VGICP_BUILD_SCATTER") ? 0u : fast_sort_max_points(ctx->device);
   std::vector<int> in_sort, in_smem, in_global;
@@ -799,7 +798,7 @@ static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const do
     const size_t V = hv[k];
     mp->voxels = V;
     const size_t b_ra = align_up(sizeof(SlotStatsA) * V, 256), b_rb = align_up(sizeof(SlotStatsB) * V, 256);
-    if (const cudaError_t e = dmalloc(ctx, &mp->cold, std::max<size_t>(b_ra + b_rb + sizeof(double) * 6 * V, 256));
+    if (const cudaError_t e = dmalloc(ctx, &mp->cold, std::max<size_t>(b_ra + b_rb + sizeof(double) * 9 * V, 256));
         e != cudaSuccess) {
       cleanup();
       return cuda_fail(e, "cudaMallocAsync(voxel map)");
@@ -809,20 +808,20 @@ static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const do
     mp->rb = reinterpret_cast<SlotStatsB*>(b + b_ra);
     mp->cov64 = reinterpret_cast<double*>(b + b_ra + b_rb);
     jobs[k].V = static_cast<unsigned>(V);
-    jobs[k].ra = mp->ra, jobs[k].rb = mp->rb, jobs[k].cov6 = mp->cov64;
+    jobs[k].ra = mp->ra, jobs[k].rb = mp->rb, jobs[k].cov9 = mp->cov64;
     max_v = std::max(max_v, jobs[k].V);
     (jobs[k].n <= sort_n ? in_sort : V <= smem_v ? in_smem : in_global).push_back(k);
   }
   if (exp) {  // single map: key-ordered statistics in rank order
     const size_t V = hv[0];
     exp->V = static_cast<unsigned>(V);
-    VG_CUDA(dmalloc(ctx, &exp->mem, std::max<size_t>(V * (8 + 4 + 24 + 72) + 1024, 256)));
+    VG_CUDA(dmalloc(ctx, &exp->mem, std::max<size_t>(V * (8 + 4 + 24) + 1024, 256)));
     char* b = static_cast<char*>(exp->mem);
     exp->keys = reinterpret_cast<unsigned long long*>(b);
     exp->counts = reinterpret_cast<int*>(b + align_up(8 * V, 256));
     exp->mean64 = reinterpret_cast<double*>(b + align_up(8 * V, 256) + align_up(4 * V, 256));
-    exp->cov9 = exp->mean64 + 3 * V;
-    jobs[0].keys = exp->keys, jobs[0].counts = exp->counts, jobs[0].mean64 = exp->mean64, jobs[0].cov9 = exp->cov9;
+    exp->cov9 = maps[0]->cov64;  // the rebuilt map's own rank-ordered fp64 covariances
+    jobs[0].keys = exp->keys, jobs[0].counts = exp->counts, jobs[0].mean64 = exp->mean64;
   }
   std::vector<int> order(in_sort);
   order.insert(order.end(), in_smem.begin(), in_smem.end());
@@ -1915,7 +1914,7 @@ static int graph_from(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_p
   const size_t o_i = carve(sizeof(WorkItem) * ni);
   const size_t o_p = carve(sizeof(double) * kPartialStride * kFactorWarps * ni);  // one partial per warp
   const size_t o_pi = carve(sizeof(int) * kFactorWarps * ni);
-  const size_t o_c = carve(sizeof(unsigned long long) * nf);
+  const size_t o_c = carve(sizeof(unsigned) * nf);
   const size_t o_pose = carve(sizeof(double) * 12 * std::max(num_poses, 1));
   const size_t o_out = carve(sizeof(double) * VGICP_LINEARIZED_DOUBLES * nf);
   const size_t o_oi = carve(sizeof(int) * nf);
@@ -1926,7 +1925,7 @@ static int graph_from(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_p
   gr->d_items = reinterpret_cast<WorkItem*>(b + o_i);
   gr->d_partials = reinterpret_cast<double*>(b + o_p);
   gr->d_part_inl = reinterpret_cast<int*>(b + o_pi);
-  gr->d_counters = reinterpret_cast<unsigned long long*>(b + o_c);
+  gr->d_counters = reinterpret_cast<unsigned*>(b + o_c);
   gr->d_poses = reinterpret_cast<double*>(b + o_pose);
   gr->d_out = reinterpret_cast<double*>(b + o_out);
   gr->d_out_inl = reinterpret_cast<int*>(b + o_oi);
@@ -1943,7 +1942,7 @@ static int graph_from(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_p
       step(cudaMemcpyAsync(gr->d_items, items.data(), sizeof(WorkItem) * items.size(), cudaMemcpyHostToDevice, s),
            "upload items");
   }
-  step(cudaMemsetAsync(gr->d_counters, 0, sizeof(unsigned long long) * nf, s), "zero counters");
+  step(cudaMemsetAsync(gr->d_counters, 0, sizeof(unsigned) * nf, s), "zero counters");
   step(cudaStreamSynchronize(s), "graph create");
   if (rc != VGICP_OK) {
     dfree(ctx, gr->block);
@@ -2197,7 +2196,7 @@ static int graph_pass(vgicp_graph g, bool linearize, const double* d_poses12, do
     DeviceGuard dg(g->ctx->device);
     if (g->num_items > 0) {
       VG_CUDA(launch_factor(linearize, g->rank_lookup, g->d_factors, g->d_items, g->num_items, g->f64_begin, d_poses12,
-                            g->d_partials, g->d_part_inl, g->d_counters, g->next_epoch(), d_res, d_inl, g->ctx->stream));
+                            g->d_partials, g->d_part_inl, g->d_counters, g->num_factors, d_res, d_inl, g->ctx->stream));
       g->ctx->launches += factor_launches(g);
     } else if (g->num_factors > 0 && d_res) {  // zero-hit-free degenerate graph: all-zero blocks
       VG_CUDA(cudaMemsetAsync(d_res, 0, sizeof(double) * (linearize ? VGICP_LINEARIZED_DOUBLES : 1) * g->num_factors,

@@ -8,8 +8,8 @@
 //         b_t = [-q×Ωe; -Ωe] (6), error eᵀΩe  -> 28 fp32 accumulators + int inliers
 //   near-singular M (fp32 Sylvester test without margin) -> the oracle-identical fp64 LDLT path
 // Reduction without float atomics: per-thread fp32 -> warp butterfly in fp64 -> one
-// partial per warp; the last warp of a factor (integer arrival counter, tagged with the launch's
-// epoch) sums the factor's partials in (item, warp) order and expands, in fp64,
+// partial per warp; the last warp of a factor (integer arrival counter) sums the factor's partials in
+// (item, warp) order and expands, in fp64,
 //   H_ts = -H_tt·Ad,  H_ss = AdᵀH_tt·Ad,  b_s = -Adᵀb_t,  Ad = Ad(T_ts) (se3.cpp:107-113),
 // which is exact algebra because B = -A·Ad(T_ts). Fixed orders everywhere => deterministic.
 #include <atomic>
@@ -36,19 +36,10 @@ __device__ __forceinline__ double relative_pose_entry(const double* Tt, const do
 }
 
 // Rare path: M near singular in fp32 -> recompute M and the LDLT decision in fp64 exactly as
-// the oracle (factors.cpp:38-46, :107) and return Omega as fp32. c = the voxel's fp64 covariance:
-// 9 entries (stride 9) or the 6 unique entries of an exactly symmetric one (stride 6).
+// the oracle (factors.cpp:38-46, :107) and return Omega as fp32.
 __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, float sxz, float syy, float syz,
-                                        float szz, const double* c, unsigned stride, float* om) {
+                                        float szz, const double* Ct, float* om) {
   const double Cs[9] = {sxx, sxy, sxz, sxy, syy, syz, sxz, syz, szz};
-  double Ct[9];
-  if (stride == 6) {
-    Ct[0] = c[0], Ct[1] = c[1], Ct[2] = c[2], Ct[3] = c[1], Ct[4] = c[3], Ct[5] = c[4], Ct[6] = c[2], Ct[7] = c[4],
-    Ct[8] = c[5];
-  } else {
-#pragma unroll
-    for (int e = 0; e < 9; ++e) Ct[e] = c[e];
-  }
   double M[9], O[9];
   combined_cov_rn(T, Cs, Ct, M);
   if (!invert_covariance_rn(M, O)) return false;
@@ -159,9 +150,7 @@ __device__ __forceinline__ void hit_math(const float* Rf, const double* T, const
     o22 = a22 * inv;
   } else {
     float om[6];
-    if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64 + (size_t)map.cov_stride * __float_as_int(v2.y),
-                    map.cov_stride, om))
-      return;
+    if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.y), om)) return;
     o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
   }
   const float w0 = o00 * e0 + o01 * e1 + o02 * e2;
@@ -218,8 +207,8 @@ template <bool kLinearize>
 __device__ __forceinline__ void finish_factor(const float* acc, int inl, int lane, size_t gw, int parts,
                                               const WorkItem& w, const FactorDev* __restrict__ fp, const double* T,
                                               double* ws, double* __restrict__ partials, int* __restrict__ part_inl,
-                                              unsigned long long* __restrict__ counters, unsigned epoch,
-                                              double* __restrict__ out, int* __restrict__ out_inl) {
+                                              unsigned* __restrict__ counters, double* __restrict__ out,
+                                              int* __restrict__ out_inl) {
   constexpr int kAcc = kLinearize ? kLinAcc : 1;
   // ---- warp reduction: fp64 butterfly over the 32 lanes, fixed order; one partial per warp
   //      (no float atomics). Once per ~2,500 points per warp, so its cost is negligible. ----
@@ -234,22 +223,13 @@ __device__ __forceinline__ void finish_factor(const float* acc, int inl, int lan
   if (lane == 0) part_inl[gw] = inl;
   __threadfence();
   __syncwarp();
-  // Arrival counter = (epoch << 32) | arrivals; the electing warp clears it. A counter still tagged
-  // with an older epoch (left behind by an aborted launch) restarts at 1, so a later launch never
-  // inherits stale arrivals.
+  // Integer arrival counter; the electing warp clears it for the next launch. (A launch that fails to
+  // start leaves it untouched; launch_factor clears the counters after any launch error.)
   unsigned last = 0;
   if (lane == 0) {
-    unsigned long long* c = &counters[w.factor];
-    unsigned long long seen = *reinterpret_cast<volatile unsigned long long*>(c), want;
-    for (;;) {
-      want = (static_cast<unsigned>(seen >> 32) == epoch) ? seen + 1ull
-                                                          : ((static_cast<unsigned long long>(epoch) << 32) | 1ull);
-      const unsigned long long prev = atomicCAS(c, seen, want);
-      if (prev == seen) break;
-      seen = prev;
-    }
-    last = (static_cast<unsigned>(want) == static_cast<unsigned>(fp->item_count * parts)) ? 1u : 0u;
-    VG_CHECK(static_cast<unsigned>(want) <= static_cast<unsigned>(fp->item_count * parts));
+    const unsigned arrived = atomicAdd(&counters[w.factor], 1u) + 1u;
+    VG_CHECK(arrived <= static_cast<unsigned>(fp->item_count * parts));
+    last = arrived == static_cast<unsigned>(fp->item_count * parts) ? 1u : 0u;
   }
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
@@ -271,7 +251,7 @@ __device__ __forceinline__ void finish_factor(const float* acc, int inl, int lan
   int tinl = 0;
   if (lane == 0) {
     for (int g = 0; g < gc; ++g) tinl += __ldcg(&part_inl[gb + g]);
-    counters[w.factor] = 0ull;  // clean for the next launch (also one replaying the same epoch)
+    counters[w.factor] = 0u;  // ready for the next launch
   }
   __syncwarp();
 
@@ -388,7 +368,7 @@ template <bool kLinearize, bool kRank, bool kF64>
 __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
     const FactorDev* __restrict__ factors, const WorkItem* __restrict__ items, int item_base,
     const double* __restrict__ poses, double* __restrict__ partials, int* __restrict__ part_inl,
-    unsigned long long* __restrict__ counters, unsigned epoch, double* __restrict__ out, int* __restrict__ out_inl) {
+    unsigned* __restrict__ counters, double* __restrict__ out, int* __restrict__ out_inl) {
   constexpr int kAcc = kLinearize ? kLinAcc : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   FactorSmem& sm = *reinterpret_cast<FactorSmem*>(smem_raw);
@@ -602,8 +582,7 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
   __syncwarp();  // this warp is done with its ring (no CTA-wide barrier after the prologue)
 
   finish_factor<kLinearize>(acc, inl, lane, (size_t)(item_base + blockIdx.x) * kWarps + warp, kWarps, w, fp, sm.T,
-                            reinterpret_cast<double*>(&sm.u.ring[warp][0]), partials, part_inl, counters, epoch, out,
-                            out_inl);
+                            reinterpret_cast<double*>(&sm.u.ring[warp][0]), partials, part_inl, counters, out, out_inl);
 }
 
 // gicp_error (factors.cpp:75-88) in fp64, bit-identical to the oracle.
@@ -677,8 +656,8 @@ cudaError_t launch_assemble(const int* out_ptr, const int* contrib, int num_slot
 }
 
 cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, const WorkItem* items, int num_items,
-                          int f64_begin, const double* poses, double* partials, int* part_inl,
-                          unsigned long long* counters, unsigned epoch, double* out, int* out_inl, cudaStream_t s) {
+                          int f64_begin, const double* poses, double* partials, int* part_inl, unsigned* counters,
+                          int num_factors, double* out, int* out_inl, cudaStream_t s) {
   if (num_items <= 0) return cudaSuccess;
   constexpr size_t kSmem = sizeof(FactorSmem);
   // the > 48 KB shared-memory opt-in is a per-device function attribute: set it once per device
@@ -705,7 +684,7 @@ cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, c
   auto go = [&](auto kernel, int base, int count) {
     if (count > 0)
       kernel<<<count, kFactorThreads, kSmem, s>>>(factors, items + base, base, poses, partials, part_inl, counters,
-                                                  epoch, out, out_inl);
+                                                  out, out_inl);
   };
   auto both = [&](auto k32, auto k64) {
     go(k32, 0, f64_begin);
@@ -718,7 +697,10 @@ cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, c
     if (rank) both(factor_kernel<false, true, false>, factor_kernel<false, true, true>);
     else both(factor_kernel<false, false, false>, factor_kernel<false, false, true>);
   }
-  return cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && num_factors > 0)  // a launch that did not run must not leave arrivals behind
+    cudaMemsetAsync(counters, 0, sizeof(unsigned) * num_factors, s);
+  return e;
 }
 
 cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s) {

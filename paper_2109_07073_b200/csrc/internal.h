@@ -137,11 +137,10 @@ struct FastBuildJob {
   OccWord* occ;            // the map's bitmap (words records)
   SlotStatsA* ra;          // outputs by rank: voxel-local fp32 statistics ...
   SlotStatsB* rb;          //   ... (c_zz, rank)
-  double* cov6;            //   ... and the fp64 covariance's 6 unique entries
-  unsigned long long* keys;  // export mode (else nullptr): packed key, count, fp64 mean and the 9-entry
-  int* counts;               //   covariance by rank
+  double* cov9;            //   ... and the fp64 covariance (9 entries, row-major; the near-singular path)
+  unsigned long long* keys;  // export mode (else nullptr): packed key, count and fp64 mean by rank
+  int* counts;
   double* mean64;
-  double* cov9;
 };
 cudaError_t launch_fast_mark(const FastBuildJob* jobs, int m, unsigned max_n, unsigned max_words, unsigned* code,
                              int* err, cudaStream_t s);
@@ -239,8 +238,8 @@ cudaError_t launch_overlap(const OverlapItem* items, int m, unsigned max_n, unsi
 // items [0, f64_begin) belong to float32-exact source clouds, [f64_begin, num_items) to float64 clouds
 // (one launch each; the float64 launch transforms the exact float64 means)
 cudaError_t launch_factor(bool linearize, bool rank, const FactorDev* factors, const WorkItem* items, int num_items,
-                          int f64_begin, const double* poses, double* partials, int* part_inl,
-                          unsigned long long* counters, unsigned epoch, double* out, int* out_inl, cudaStream_t s);
+                          int f64_begin, const double* poses, double* partials, int* part_inl, unsigned* counters,
+                          int num_factors, double* out, int* out_inl, cudaStream_t s);
 cudaError_t launch_gicp_error(const double* in, double* out, cudaStream_t s);
 // overlap probes grouped by cloud: chunk = (first item, count <= kOverlapMapsPerChunk) of items that
 // share one cloud; each thread loads its points once and probes the chunk's maps
@@ -398,15 +397,14 @@ struct vgicp_map_s {
   vgicp::SlotStatsB* rb = nullptr;
   std::atomic<int> refs{1};
   // Maps of float32 clouds built by the hand-written path (build.cu): voxels numbered by rank only
-  // (ra / rb / cov64 with 6 entries per voxel, `cold` holds them), no key-ordered arrays and no hash
+  // (ra / rb / cov64 by rank, `cold` holds them), no key-ordered arrays and no hash
   // table until one is needed (ensure_table); export recomputes the key-ordered statistics from `src`
   // with the same kernels.
   bool fast = false;
   vgicp_cloud src = nullptr;  // the source cloud (kept alive: export / on-demand hash table)
-  unsigned cov_stride = 9;
-  vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov64, res, inv_res, shift, cov_stride, occ}; }
+  vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov64, res, inv_res, shift, 0u, occ}; }
   // rank lookups: slot statistics replaced by the rank-ordered copies (requires occ)
-  vgicp::MapDev dev_rank() const { return vgicp::MapDev{tkeys, ra, rb, cov64, res, inv_res, shift, cov_stride, occ}; }
+  vgicp::MapDev dev_rank() const { return vgicp::MapDev{tkeys, ra, rb, cov64, res, inv_res, shift, 0u, occ}; }
 };
 
 struct vgicp_mapset_s {
@@ -433,9 +431,7 @@ struct vgicp_graph_s {
   vgicp::WorkItem* d_items = nullptr;
   double* d_partials = nullptr;
   int* d_part_inl = nullptr;
-  unsigned long long* d_counters = nullptr;  // per-factor arrival counters, tagged with the launch epoch
-  unsigned epoch = 0;                         // last factor-pass epoch (never 0 after the first pass)
-  unsigned next_epoch() { return epoch = (epoch == 0xFFFFFFFFu ? 1u : epoch + 1u); }
+  unsigned* d_counters = nullptr;  // per-factor arrival counters (cleared by each factor's last warp)
   double* d_poses = nullptr;
   double* d_out = nullptr;
   int* d_out_inl = nullptr;

@@ -92,11 +92,11 @@ struct MapDev {
   const unsigned long long* keys;  // capacity = kBucket * num_buckets, kEmptyKey when free
   const SlotStatsA* sa;            // per slot
   const SlotStatsB* sb;            // per slot
-  const double* cov64;             // fp64 covariances by voxel id: V×9 row-major, or V×6 unique entries
-  double res;                      //   (xx xy xz yy yz zz) for maps of float32 clouds (exactly symmetric)
+  const double* cov64;             // V×9 row-major fp64 covariances by voxel id (cold)
+  double res;
   double inv_res;
   unsigned shift;                  // 32 - log2(num_buckets)
-  unsigned cov_stride;             // 9 or 6 doubles per voxel in cov64
+  unsigned pad;
   OccDev occ;                      // occupancy bitmap; factor graphs in rank mode index sa / sb by rank
 };
 
