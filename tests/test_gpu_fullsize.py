@@ -31,6 +31,18 @@ def oracle_frame(wl, k):
     return wl.scans.means[k].astype(np.float64), O.cov9(wl.scans.cov6[k].astype(np.float64))
 
 
+def test_c3_links_equal_the_oracle_selection_fixture(c3):
+    """The GPU overlap sweep selects exactly the factor list the oracle's overlap_rate selects
+    (tests/golden/c3_links.npy, made by tests/golden/make_c3_links.py; the reference bench arm
+    reads it): bit-exact hit counts -> the same links."""
+    from pathlib import Path
+
+    fx = Path(__file__).resolve().parent / "golden" / "c3_links.npy"
+    if not fx.exists():
+        pytest.skip("fixture not generated")
+    assert np.array_equal(np.load(fx), np.array(c3.links, np.int32).reshape(-1, 2))
+
+
 def test_c3_shape(c3):
     assert 4000 <= c3.num_factors <= 4500
     assert c3.num_points() == sum(len(c3.scans.means[j]) for _, j in c3.links)
