@@ -265,11 +265,83 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
     int solved = 0;
   } next;
   // linearize + assemble `at` into d_asm[which]; returns the total error (factor order)
+  // VGICP_LM_CUDA_GRAPH=1: a candidate's linearization — poses H2D, the factor pass, the device
+  // assembly into d_asm[which], the per-factor errors and inliers D2H — becomes one CUDA graph per
+  // assembly buffer (captured on the second use, replayed after): one graph launch and one
+  // synchronisation per candidate. Measured (tools/lm_cuda_graph_ab.py, profiles/lm_cuda_graph_r02.log):
+  // no change in ms per iteration on C2 / C3 / C5 — the loop is kernel-bound (linearize + band
+  // solve), not launch-bound — and ~3 ms of capture + instantiation per run, so it is off by default.
+  // Plain graphs only (a sharded graph's pass spans several devices' streams).
+  const bool use_cuda_graph = graph->shards.empty() && nf > 0 && std::getenv("VGICP_LM_CUDA_GRAPH") != nullptr;
+  struct PinnedHost {
+    void* p = nullptr;
+    ~PinnedHost() {
+      if (p) cudaFreeHost(p);
+    }
+  } pin;
+  double* h_poses = nullptr;
+  double* h_err = nullptr;
+  int32_t* h_inl = nullptr;
+  cudaGraphExec_t cg_exec[2] = {nullptr, nullptr};
+  uint64_t cg_launches[2] = {0, 0};
+  int cg_uses[2] = {0, 0};
+  struct GraphExecs {
+    cudaGraphExec_t* e;
+    ~GraphExecs() {
+      for (int k = 0; k < 2; ++k)
+        if (e[k]) cudaGraphExecDestroy(e[k]);
+    }
+  } cg_guard{cg_exec};
+  if (use_cuda_graph) {
+    const size_t bp = sizeof(double) * 12 * n, be = sizeof(double) * nf;
+    VG_CUDA(cudaMallocHost(&pin.p, bp + be + sizeof(int32_t) * nf + 64));
+    h_poses = static_cast<double*>(pin.p);
+    h_err = reinterpret_cast<double*>(static_cast<char*>(pin.p) + bp);
+    h_inl = reinterpret_cast<int32_t*>(static_cast<char*>(pin.p) + bp + be);
+  }
+  auto enqueue_linearization = [&](int which) -> int {
+    VG_CUDA(cudaMemcpyAsync(d_poses, h_poses, sizeof(double) * 12 * n, cudaMemcpyHostToDevice, s));
+    if (int rc = vgicp_graph_linearize_assembled_device(graph, d_poses, d_asm[which])) return rc;
+    VG_CUDA(cudaMemcpy2DAsync(h_err, sizeof(double), graph->d_out + (VGICP_LINEARIZED_DOUBLES - 1),
+                              sizeof(double) * VGICP_LINEARIZED_DOUBLES, sizeof(double), nf, cudaMemcpyDeviceToHost,
+                              s));
+    VG_CUDA(cudaMemcpyAsync(h_inl, graph->d_out_inl, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, s));
+    return VGICP_OK;
+  };
   auto linearize = [&](const std::vector<double>& at, int which, double* total) -> int {
     if (next.which == which) next.which = -1;  // the pending pair result's system is overwritten
-    VG_CUDA(cudaMemcpyAsync(d_poses, at.data(), sizeof(double) * 12 * n, cudaMemcpyHostToDevice, s));
-    if (int rc = vgicp_graph_linearize_assembled_device(graph, d_poses, d_asm[which])) return rc;
-    if (int rc = vgicp_graph_linearized_errors(graph, err.data(), inl.data())) return rc;
+    if (use_cuda_graph) {
+      std::memcpy(h_poses, at.data(), sizeof(double) * 12 * n);
+      if (cg_exec[which]) {
+        VG_CUDA(cudaGraphLaunch(cg_exec[which], s));
+        ctx->launches += cg_launches[which];
+      } else if (cg_uses[which]++ == 0) {  // first use: direct (configures the kernels' attributes)
+        if (int rc = enqueue_linearization(which)) return rc;
+      } else {
+        const uint64_t l0 = ctx->launches;
+        cudaGraph_t cg = nullptr;
+        VG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const int rc = enqueue_linearization(which);
+        const cudaError_t ce = cudaStreamEndCapture(s, &cg);
+        if (rc) {
+          if (cg) cudaGraphDestroy(cg);
+          return rc;
+        }
+        VG_CUDA(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&cg_exec[which], cg, 0);
+        cudaGraphDestroy(cg);
+        VG_CUDA(ie);
+        cg_launches[which] = ctx->launches - l0;
+        VG_CUDA(cudaGraphLaunch(cg_exec[which], s));
+      }
+      VG_CUDA(cudaStreamSynchronize(s));
+      std::copy(h_err, h_err + nf, err.begin());
+      std::copy(h_inl, h_inl + nf, inl.begin());
+    } else {
+      VG_CUDA(cudaMemcpyAsync(d_poses, at.data(), sizeof(double) * 12 * n, cudaMemcpyHostToDevice, s));
+      if (int rc = vgicp_graph_linearize_assembled_device(graph, d_poses, d_asm[which])) return rc;
+      if (int rc = vgicp_graph_linearized_errors(graph, err.data(), inl.data())) return rc;
+    }
     double e = 0.0;
     for (int f = 0; f < nf; ++f) e += err[f];
     *total = e;

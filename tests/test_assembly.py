@@ -400,3 +400,19 @@ def test_gpu_native_lm_fixed_and_updates(V):
     assert np.all(upd[moved] == (48 + r.iterations) % 50)
     R = p[moved, :9].reshape(-1, 3, 3)
     assert np.abs(R @ R.transpose(0, 2, 1) - np.eye(3)).max() < 1e-12  # orthonormalized on the wrap
+
+
+@gpu
+def test_gpu_native_lm_cuda_graph_identical(V, monkeypatch):
+    """The native LM's candidate linearizations replayed as CUDA graphs (captured on the second use
+    of each assembly buffer) change nothing: trace, solves and poses equal the per-call path."""
+    from paper_2109_07073_b200 import optimizer as LM
+
+    graph, poses = _lm_graph(V, True, seed=81)
+    monkeypatch.setenv("VGICP_LM_CUDA_GRAPH", "1")
+    p1, r1 = LM.optimize_native(graph, poses)
+    monkeypatch.delenv("VGICP_LM_CUDA_GRAPH")
+    p2, r2 = LM.optimize_native(graph, poses)
+    assert [(t.accepted, t.lam, t.error) for t in r1.trace] == [(t.accepted, t.lam, t.error) for t in r2.trace]
+    assert r1.linearizations == r2.linearizations and r1.linearizations >= 3
+    assert np.array_equal(p1, p2)
