@@ -344,6 +344,9 @@ struct HitQueue {
   float4 c[kQueue];  // c_xy c_xz c_yy c_yz
   float d[kQueue];   // c_zz
 };
+#ifndef VG_MAP_SMEM
+#define VG_MAP_SMEM 1  // the linearize kernel reads the work item's map descriptor from shared memory
+#endif
 struct __align__(128) FactorSmem {
   union {
     WarpTile ring[kWarps][kStages];
@@ -352,6 +355,9 @@ struct __align__(128) FactorSmem {
   unsigned long long bar[kWarps][kStages];
   double T[12];
   float Rf[9];
+#if VG_MAP_SMEM
+  MapDev map;
+#endif
 };
 static_assert(sizeof(WarpTile) * kStages >= sizeof(double) * 180, "epilogue scratch must fit in the warp's ring");
 
@@ -401,11 +407,22 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
     for (int k = 0; k < kStages && k < my_tiles; ++k) issue_tile(k);
   }
   if (tid < 12) sm.T[tid] = relative_pose_entry(poses + 12 * fp->tgt, poses + 12 * fp->src, tid);
+#if VG_MAP_SMEM
+  static_assert(sizeof(MapDev) % 4 == 0, "MapDev is copied as words");
+  if (tid >= 32 && tid < 32 + static_cast<int>(sizeof(MapDev) / 4))
+    reinterpret_cast<unsigned*>(&sm.map)[tid - 32] = reinterpret_cast<const unsigned*>(&fp->map)[tid - 32];
+#endif
   __syncthreads();
   if (tid < 9) sm.Rf[tid] = (float)sm.T[tid];
   __syncthreads();
 
-  const MapDev map = fp->map;
+  // The linearize kernel reads the map descriptor (20 words) from shared memory instead of holding it
+  // in registers: it then fits its 128 registers without spills or rematerialised reloads (C3
+  // linearize 1.350 -> 1.317 ms); the error-only kernel has registers to spare and is faster with
+  // the register copy (1.110 vs 1.172 ms).
+  MapDev map_regs;
+  if constexpr (!(kLinearize && VG_MAP_SMEM)) map_regs = fp->map;
+  const MapDev& map = (kLinearize && VG_MAP_SMEM) ? sm.map : map_regs;
   const double* T = sm.T;  // T_ts stays in shared memory (broadcast reads)
   HitQueue& hq = sm.hq[warp];
   const unsigned lane_lt = (1u << lane) - 1u;
@@ -440,9 +457,16 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
     // ---- probe phase: kILP points per lane — fp64 transform (reference op order, T_ts in
     //      registers for this tile only), exact key, both bucket loads of all points issued before
     //      any compare ----
+#ifndef VG_T_REGS
+#define VG_T_REGS 1
+#endif
+#if VG_T_REGS
     double Tr[12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) Tr[q] = T[q];
+#else
+    const double* Tr = T;  // broadcast shared-memory reads inside the transform
+#endif
     unsigned hi[kILP], lo[kILP], b1[kILP], b2[kILP];
     float l0[kILP], l1[kILP], l2[kILP], q0[kILP], q1[kILP], q2[kILP], cxx[kILP];
     bool ok[kILP];
