@@ -59,7 +59,7 @@ __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, f
 #define VG_B2_LAZY 0  // read bucket2 only when bucket1 is full and misses
 #endif
 #ifndef VG_PREFETCH
-#define VG_PREFETCH 0  // rank lookups: L1 prefetch of a hit's statistics at append time (1: 32-B part, 2: both)
+#define VG_PREFETCH 2  // rank lookups: L1 prefetch of a hit's statistics at append time (1: 32-B part, 2: both)
 #endif
 #ifndef VG_STAGES
 #define VG_STAGES 2
