@@ -196,6 +196,15 @@ def reference_links(scans, threads=0, max_links=10, min_overlap=0.025, resolutio
     return select_links(dict(zip(pairs, ov)), n, max_links, min_overlap), maps
 
 
+def loaded_native_libraries() -> list:
+    """Repo shared objects mapped into this process (the reference arm must show only oracle/)."""
+    try:
+        libs = {line.split()[-1] for line in open("/proc/self/maps") if line.rstrip().endswith(".so")}
+    except OSError:
+        return []
+    return sorted(str(Path(x).relative_to(ROOT)) for x in libs if x.startswith(str(ROOT)))
+
+
 def run_reference(args):
     """Reference arm: the reference's CPU implementation of the path (the oracle port of
     factors.cpp / voxelmap.cpp with ExecPolicy{all cores, false}; the reference itself needs Eigen
@@ -263,6 +272,7 @@ def run_reference(args):
         "ms_per_step_min": 1e3 * min(times), "ms_per_step_max": 1e3 * max(times),
         "build_seconds": {"scans_and_covariances": round(t1 - t0, 2), "maps_and_links": round(t2 - t1, 2)},
         "links": link_source,
+        "native_libraries": loaded_native_libraries(),
     }
     print(json.dumps(line), flush=True)
 
