@@ -348,6 +348,7 @@ static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov
 }
 
 int vgicp_cloud_upload(vgicp_ctx ctx, const float* xyz, const float* cov6, size_t n, vgicp_cloud* out) try {
+  NvtxRange nvtx_("vgicp_cloud_upload");
   return cloud_upload_packed(ctx, xyz, cov6, n, out);
 } catch (...) {
   return api_exception();
@@ -360,6 +361,7 @@ static void parallel_copies(const std::vector<std::tuple<void*, const void*, siz
 // uploads: the stable sort of the same codes is the same permutation.
 int vgicp_cloud_upload_batch(vgicp_ctx ctx, const float* const* xyz, const float* const* cov6, const size_t* n, int m,
                              vgicp_cloud* out) try {
+  NvtxRange nvtx_("vgicp_cloud_upload_batch");
   if (!ctx || (m > 0 && (!xyz || !n || !out))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (m <= 0) return VGICP_OK;
   for (int k = 0; k < m; ++k) out[k] = nullptr;
@@ -478,6 +480,7 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
 // pipeline.cpp:100-111) is kept in float64 as well, so keys / correspondences / overlap hits and map
 // statistics built from it are those of the reference's double arithmetic.
 int vgicp_cloud_upload_f64(vgicp_ctx ctx, const double* xyz, const double* cov9, size_t n, vgicp_cloud* out) try {
+  NvtxRange nvtx_("vgicp_cloud_upload_f64");
   if (!ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   if (n > 0 && !xyz) return fail(VGICP_E_INVALID_ARGUMENT, "null point array");
@@ -947,6 +950,7 @@ static int ensure_table(vgicp_map mp) {
 
 int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* resolutions, int m,
                                vgicp_map* out) try {
+  NvtxRange nvtx_("vgicp_voxelmap_build_batch");
   if (!ctx || !out || (m > 0 && (!clouds || !resolutions))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (m <= 0) return VGICP_OK;
   for (int k = 0; k < m; ++k) out[k] = nullptr;
@@ -1349,6 +1353,7 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
 int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* poses12, int m,
                        double downsample_resolution, double map_resolution, vgicp_map* out_downsampled,
                        vgicp_cloud* out_cloud, vgicp_map* out_map) try {
+  NvtxRange nvtx_("vgicp_submap_build");
   if (!ctx || !out_map || (m > 0 && (!frames || !poses12))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out_map = nullptr;
   if (out_downsampled) *out_downsampled = nullptr;
@@ -1478,6 +1483,7 @@ int vgicp_voxelmap_total_points(vgicp_map map, size_t* total) try {
 }
 
 int vgicp_voxelmap_export(vgicp_map map, uint64_t* keys, int32_t* counts, double* means, double* covs) try {
+  NvtxRange nvtx_("vgicp_voxelmap_export");
   if (!map) return fail(VGICP_E_INVALID_ARGUMENT, "null map");
   DeviceGuard g(map->ctx->device);
   cudaStream_t s = map->ctx->stream;
@@ -1588,6 +1594,7 @@ static void fill_overlap_item(OverlapItem& it, const vgicp_cloud_s* c, const dou
 
 int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* poses12, const vgicp_map* maps,
                         int m, uint64_t* hits) try {
+  NvtxRange nvtx_("vgicp_overlap_batch");
   if (!ctx || (m > 0 && (!clouds || !poses12 || !maps || !hits)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (m <= 0) return VGICP_OK;
@@ -1732,6 +1739,7 @@ int vgicp_mapset_destroy(vgicp_mapset set) try {
 }
 
 int vgicp_overlap_mapset(vgicp_ctx ctx, vgicp_cloud cloud, const double* rel12, vgicp_mapset set, uint64_t* hits) try {
+  NvtxRange nvtx_("vgicp_overlap_mapset");
   if (!ctx || !cloud || !set || (!set->maps.empty() && (!rel12 || !hits)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (cloud->ctx != ctx || set->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "handle of another context");
@@ -2011,6 +2019,7 @@ static std::vector<int> partition_bounds(const vgicp_factor_desc* factors, int F
 
 int vgicp_graph_create_sharded(const vgicp_ctx* ctxs, int num_shards, const vgicp_factor_desc* const* factors,
                                int num_factors, int num_poses, int chunk, vgicp_graph* out) try {
+  NvtxRange nvtx_("vgicp_graph_create_sharded");
   if (!ctxs || !out || !factors || num_shards <= 0) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   if (num_shards > kMaxShards) return fail(VGICP_E_INVALID_ARGUMENT, "at most 8 shards (one per device of a box)");
@@ -2238,6 +2247,7 @@ static int graph_pass(vgicp_graph g, bool linearize, const double* d_poses12, do
 }
 
 int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, double* d_out, int32_t* d_inliers) try {
+  NvtxRange nvtx_("vgicp_graph_linearize_device");
   if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_out || !d_inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   return graph_pass(graph, true, d_poses12, d_out, d_inliers);
@@ -2246,6 +2256,7 @@ int vgicp_graph_linearize_device(vgicp_graph graph, const double* d_poses12, dou
 }
 
 int vgicp_graph_evaluate_device(vgicp_graph graph, const double* d_poses12, double* d_errors, int32_t* d_inliers) try {
+  NvtxRange nvtx_("vgicp_graph_evaluate_device");
   if (!graph || (graph->num_factors > 0 && (!d_poses12 || !d_errors || !d_inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   return graph_pass(graph, false, d_poses12, d_errors, d_inliers);
@@ -2333,12 +2344,14 @@ static int graph_run_host(vgicp_graph graph, bool linearize, const double* poses
 }
 
 int vgicp_graph_linearize(vgicp_graph graph, const double* poses12, double* out, int32_t* inliers) try {
+  NvtxRange nvtx_("vgicp_graph_linearize");
   return graph_run_host(graph, true, poses12, out, inliers);
 } catch (...) {
   return api_exception();
 }
 
 int vgicp_graph_evaluate(vgicp_graph graph, const double* poses12, double* errors, int32_t* inliers) try {
+  NvtxRange nvtx_("vgicp_graph_evaluate");
   return graph_run_host(graph, false, poses12, errors, inliers);
 } catch (...) {
   return api_exception();
@@ -2466,6 +2479,7 @@ int vgicp_graph_linearize_assembled(vgicp_graph graph, const double* poses12, do
 }
 
 int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_poses12, double* d_assembled) try {
+  NvtxRange nvtx_("vgicp_graph_linearize_assembled_device");
   if (!graph || !d_poses12) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (!graph->plan) return fail(VGICP_E_INVALID_ARGUMENT, "no assembly plan (call vgicp_graph_assembly_plan)");
   const int S = graph->num_slots, O = S + graph->num_pairs;
@@ -2476,6 +2490,7 @@ int vgicp_graph_linearize_assembled_device(vgicp_graph graph, const double* d_po
 }
 
 int vgicp_graph_assemble_device(vgicp_graph graph, const double* d_blocks, double* d_assembled) try {
+  NvtxRange nvtx_("vgicp_graph_assemble_device");
   if (!graph) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (!graph->plan) return fail(VGICP_E_INVALID_ARGUMENT, "no assembly plan (call vgicp_graph_assembly_plan)");
   const int S = graph->num_slots, O = S + graph->num_pairs;
@@ -2495,6 +2510,7 @@ int vgicp_graph_assemble_device(vgicp_graph graph, const double* d_blocks, doubl
 }
 
 int vgicp_graph_linearized_errors(vgicp_graph graph, double* errors, int32_t* inliers) try {
+  NvtxRange nvtx_("vgicp_graph_linearized_errors");
   if (!graph || (graph->num_factors > 0 && (!errors || !inliers)))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   const int nf = graph->num_factors;
@@ -2590,6 +2606,7 @@ int vgicp_graph_solver_plan(vgicp_graph graph, int* bandwidth, int* supported) t
 // One launch solving the damped system for `count` (1 or 2) damping values, one cluster each.
 static int solve_damped_n(vgicp_graph graph, const double* d_assembled, const double* lambdas, int count, double* x,
                           int* solved) {
+  NvtxRange nvtx_(count > 1 ? "vgicp_graph_solve_damped_pair" : "vgicp_graph_solve_damped");
   if (!graph || !x || !solved || !lambdas || (graph->num_slots > 0 && !d_assembled))
     return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (!graph->band && graph->num_slots > 0)
@@ -2748,6 +2765,7 @@ static void parallel_copies(const std::vector<std::tuple<void*, const void*, siz
 
 int vgicp_estimate_covariances_batch(vgicp_ctx ctx, const float* const* xyz, const size_t* n, int m, int k,
                                      double plane_epsilon, float* const* cov6) try {
+  NvtxRange nvtx_("vgicp_estimate_covariances_batch");
   if (!ctx || (m > 0 && (!xyz || !n || !cov6))) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   if (m <= 0) return VGICP_OK;
   // estimate_covariances validation (point_cloud.cpp:47-53)

@@ -9,10 +9,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/vgicp_b200.h"
 #include "vgicp_device.cuh"
 
 namespace vgicp {
+
+// NVTX range around a C ABI operation (header-only NVTX3: a no-op unless a profiler is attached),
+// so nsys / ncu timelines show builds, overlap sweeps, factor passes, solves and LM iterations.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);

@@ -406,7 +406,9 @@ extern "C" int vgicp_graph_optimize(vgicp_graph graph, double* poses12, const ui
   std::vector<double> cand(poses.size());
   std::vector<int32_t> cand_upd(n);
   double t_prev = seconds();
+  NvtxRange nvtx_run("vgicp_graph_optimize");
   for (int it = 0; it < st.max_iterations; ++it) {
+    NvtxRange nvtx_it("LM iteration");
     bool accepted = false;
     while (true) {
       bool ok = false;
