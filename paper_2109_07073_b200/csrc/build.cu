@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kAccThreads, 3) fast_accumulate_kernel(const F
   __shared__ float4 sA[kAccWarps][kStage];
   __shared__ float4 sB[kAccWarps][kStage];
   __shared__ float sZ[kAccWarps][kStage];
-  __shared__ double stage[kAccWarps][32 * 9];  // the warp's fp64 covariances, written out coalesced
+  __shared__ __align__(16) double stage[kAccWarps][32 * 9];  // the warp's fp64 covariances, written out coalesced
   const FastBuildJob& j = jobs[blockIdx.y];
   const unsigned V = j.V;
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -606,9 +606,12 @@ __global__ void __launch_bounds__(kAccThreads, 3) fast_accumulate_kernel(const F
     }
   }
   __syncwarp();
-  // the warp's covariances leave as one contiguous, coalesced run of 9·nv doubles
-  double* __restrict__ dst = j.cov9 + 9 * static_cast<size_t>(v0);
-  for (unsigned t = lane; t < 9 * nv; t += 32) dst[t] = stage[warp][t];
+  // the warp's covariances leave as one contiguous, coalesced run of 9·nv doubles, 16 B per store
+  // (v0 is a multiple of 32, so the run starts 16-B aligned)
+  double2* __restrict__ dst = reinterpret_cast<double2*>(j.cov9 + 9 * static_cast<size_t>(v0));
+  const double2* src2 = reinterpret_cast<const double2*>(stage[warp]);
+  for (unsigned t = lane; t < (9 * nv) / 2; t += 32) dst[t] = src2[t];
+  if ((9 * nv) % 2 && lane == 0) j.cov9[9 * static_cast<size_t>(v0) + 9 * nv - 1] = stage[warp][9 * nv - 1];
 }
 
 // Hash table of a rank-numbered map (on demand): slot <- the statistics of its key's rank.
