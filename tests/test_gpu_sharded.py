@@ -21,7 +21,9 @@ def _problem(ctxs, nframes=9, n=2500, seed=501):
     for _ in range(nframes):
         m, c = rng.gaussian_cloud(n, 10.0)
         data.append((m.astype(np.float32), V.cov6_from(c)))
-    links = [(j - d, j) for j in range(1, nframes) for d in (1, 2) if j - d >= 0] + [(nframes - 1, 0), (5, 1)]
+    links = [(j - d, j) for j in range(1, nframes) for d in (1, 2) if j - d >= 0] + [(nframes - 1, 0)]
+    if nframes > 5:
+        links.append((5, 1))
     lists = []
     for ctx in ctxs:
         clouds = V.PointCloud.upload_batch([d[0] for d in data], [d[1] for d in data], ctx)
@@ -159,3 +161,54 @@ def test_gathered_graph_nccl_world1_matches_graph(ctxs):
     assert np.array_equal(p1, p2)
     ref_raw, ref_inl = full.linearize_raw(poses)
     assert np.array_equal(raw, ref_raw) and np.array_equal(inl, ref_inl)
+
+
+def test_sharded_edge_cases(ctxs):
+    """More shards than needed (an empty range), range graphs of zero factors, mismatched factor
+    lists (validation), and a one-shard sharded graph — all behave like the plain graph."""
+    lists, poses = _problem(ctxs[:3], nframes=3, n=800, seed=502)
+    two = [fl[:2] for fl in lists]  # 2 factors over 3 shards: at least one shard is empty
+    full = V.FactorGraph(two[0], len(poses))
+    sh = V.FactorGraph.sharded(two, len(poses))
+    counts = [sh.shard_range(r)[1] for r in range(3)]
+    assert sum(counts) == 2 and 0 in counts
+    a, ai = full.linearize_raw(poses)
+    b, bi = sh.linearize_raw(poses)
+    assert np.array_equal(a, b) and np.array_equal(ai, bi)
+    one = V.FactorGraph.sharded(two[:1], len(poses))
+    assert one.num_shards() == 1 and np.array_equal(one.linearize_raw(poses)[0], a)
+    empty = V.FactorGraph.create_range(lists[0], len(poses), 1, 0)
+    assert empty.num_factors() == 0 and empty.linearize_raw(poses)[0].shape == (0, 121)
+    with pytest.raises(ValueError):
+        V.FactorGraph.create_range(lists[0], len(poses), 2, len(lists[0]))  # beyond the list
+    with pytest.raises(ValueError):  # the shards' lists must describe the same factors
+        V.FactorGraph.sharded([lists[0], lists[1][::-1]], len(poses))
+
+
+def test_mixed_float32_float64_batch_build(ctxs):
+    """One build_batch call with float32 clouds (hand-written build) and float64 clouds (sort-based
+    build) interleaved returns every map in its slot, identical to single builds."""
+    rng = O.Rng(503)
+    clouds = []
+    for k in range(6):
+        m, c = rng.gaussian_cloud(600 + 200 * k, 6.0)
+        if k % 2:
+            clouds.append(V.PointCloud(m + 1e-7, c, ctxs[0]))  # not float32-exact -> float64 cloud
+        else:
+            clouds.append(V.PointCloud(m.astype(np.float32), V.cov6_from(c), ctxs[0]))
+    assert [c.is_f64() for c in clouds] == [False, True] * 3
+    res = [1.0, 0.5, 2.0, 1.0, 0.7, 1.3]
+    batch = V.GaussianVoxelMap.build_batch(clouds, res)
+    for c, r, b in zip(clouds, res, batch):
+        s = V.GaussianVoxelMap(c, r)
+        assert b.resolution() == r
+        for x, y in zip(b.export(), s.export()):
+            assert np.array_equal(x, y)
+
+
+def test_upload_batch_all_empty_and_single(ctxs):
+    out = V.PointCloud.upload_batch([np.zeros((0, 3), np.float32)] * 3, None, ctxs[0])
+    assert [len(c) for c in out] == [0, 0, 0]
+    m = np.random.default_rng(6).uniform(-5, 5, (100, 3)).astype(np.float32)
+    one = V.PointCloud.upload_batch([m], [np.tile(np.array([1, 0, 0, 1, 0, 1], np.float32), (100, 1))], ctxs[0])
+    assert len(one) == 1 and len(one[0]) == 100 and one[0].has_covariances()
