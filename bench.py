@@ -682,13 +682,24 @@ def run_ours(args):
 
     clocks = Clocks(local)
     if not args.profile:
-        # sample clocks under sustained load: ~1.5 s of untimed steps, then the timed region
+        # sample clocks under sustained load: ~1.5 s of untimed steps, then the timed region. The step
+        # count is fixed from the slowest rank's step time (every rank must issue the same number of
+        # collectives: a per-rank time-based loop would desynchronise the gathers under torchrun)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(5):
+            step()
+        torch.cuda.synchronize()
+        per = torch.tensor([(time.perf_counter() - t0) / 5], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(per, op=dist.ReduceOp.MAX)
+        n_load = max(1, min(5000, int(1.5 / max(float(per.item()), 1e-6))))
         clocks.start()
-        t_load = time.perf_counter()
-        while time.perf_counter() - t_load < 1.5:
-            for _ in range(20):
-                step()
-            torch.cuda.synchronize()
+        for k in range(n_load):
+            step()
+            if k % 20 == 19:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
     launches0 = ctx.launch_count()
     if world > 1:
         dist.barrier()
