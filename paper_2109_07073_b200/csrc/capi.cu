@@ -118,6 +118,22 @@ int ensure_pinned(vgicp_ctx ctx, size_t bytes) {
   return VGICP_OK;
 }
 
+// Runs `f` when the scope ends unless dismissed: error paths (including VG_CUDA early returns)
+// release what a partially completed call allocated.
+template <typename F>
+struct ScopeFail {
+  F f;
+  bool armed = true;
+  ~ScopeFail() {
+    if (armed) f();
+  }
+  void dismiss() { armed = false; }
+};
+template <typename F>
+ScopeFail<F> on_failure(F f) {
+  return ScopeFail<F>{f};
+}
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -377,8 +393,9 @@ int vgicp_cloud_upload_batch(vgicp_ctx ctx, const float* const* xyz, const float
   cudaStream_t s = ctx->stream;
   std::vector<vgicp_cloud> clouds(m, nullptr);
   auto cleanup = [&]() {
-    for (auto* c : clouds) release(c);
+    for (auto*& c : clouds) release(c), c = nullptr;
   };
+  auto guard = on_failure(cleanup);
   std::vector<UploadSeg> segs(m);
   unsigned long long off = 0;
   for (int k = 0; k < m; ++k) {
@@ -465,6 +482,7 @@ int vgicp_cloud_upload_batch(vgicp_ctx ctx, const float* const* xyz, const float
         for (int a = 0; a < 3; ++a)
           clouds[k]->lo[a] = unordered_host(hbox[6 * k + a]), clouds[k]->hi[a] = unordered_host(hbox[6 * k + 3 + a]);
   }
+  guard.dismiss();
   for (int k = 0; k < m; ++k) out[k] = clouds[k];
   return VGICP_OK;
 } catch (...) {
@@ -674,8 +692,9 @@ static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const do
   std::vector<FastBuildJob> jobs(m);
   std::vector<vgicp_map> maps(m, nullptr);
   auto cleanup = [&]() {
-    for (auto* mp : maps) release(mp);
+    for (auto*& mp : maps) release(mp), mp = nullptr;
   };
+  auto guard = on_failure(cleanup);
   unsigned long long total = 0;
   unsigned max_n = 0, max_words = 0;
   for (int k = 0; k < m; ++k) {
@@ -852,6 +871,7 @@ static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const do
     return rc;
   }
   ctx->launches += (in_sort.empty() ? 0 : 1) + (in_smem.empty() ? 0 : 1) + (in_global.empty() ? 0 : 1) + 1;
+  guard.dismiss();
   for (int k = 0; k < m; ++k) out[k] = maps[k];
   return VGICP_OK;
 }
@@ -2048,6 +2068,10 @@ int vgicp_graph_create_sharded(const vgicp_ctx* ctxs, int num_shards, const vgic
   auto cleanup = [&]() {
     for (auto* sh : parent->shards) vgicp_graph_destroy(sh);
     parent->shards.clear();
+    for (auto ev : parent->shard_events) cudaEventDestroy(ev);
+    parent->shard_events.clear();
+    if (parent->root_event) cudaEventDestroy(parent->root_event);
+    parent->root_event = nullptr;
   };
   for (int r = 0; r < num_shards; ++r) {
     Decomp dr;
