@@ -78,6 +78,9 @@ int vgicp_device_count(int* count);
 /* One context per device; it owns a CUDA stream (or adopts `stream` when non-NULL). */
 int vgicp_ctx_create(int device, void* stream, vgicp_ctx* out);
 int vgicp_ctx_destroy(vgicp_ctx ctx);
+/* One context per device of devices[0, n) (each with its own stream): the contexts of a sharded
+ * graph. All-or-nothing. */
+int vgicp_ctx_create_multi(const int* devices, int n, vgicp_ctx* out);
 int vgicp_ctx_stream(vgicp_ctx ctx, void** stream);
 int vgicp_ctx_synchronize(vgicp_ctx ctx);
 /* Kernels this context has launched so far (bench evidence for gpu_launches). */
@@ -101,6 +104,9 @@ int vgicp_cloud_is_f64(vgicp_cloud cloud, int* f64);
 int vgicp_cloud_size(vgicp_cloud cloud, size_t* n);
 int vgicp_cloud_has_covariances(vgicp_cloud cloud, int* has);
 int vgicp_cloud_destroy(vgicp_cloud cloud);
+/* The cloud's device layout copied to ctx's device (peer copy over NVLink; through the host when the
+ * devices cannot reach each other): the replicas of a sharded graph, identical in every bit. */
+int vgicp_cloud_replicate(vgicp_cloud cloud, vgicp_ctx ctx, vgicp_cloud* out);
 
 /* ---------------------------------------------------------------- Gaussian voxel maps */
 /* GaussianVoxelMap(cloud, resolution) — voxelmap.cpp:65-104. Errors: resolution <= 0 or a
@@ -111,6 +117,9 @@ int vgicp_voxelmap_build(vgicp_ctx ctx, vgicp_cloud cloud, double resolution, vg
 int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* resolutions, int m,
                                vgicp_map* out);
 int vgicp_voxelmap_destroy(vgicp_map map);
+/* The map (bitmap, statistics, tables) copied to ctx's device — one transfer per map instead of a
+ * rebuild per device (maps are immutable); factor results are bit-identical. */
+int vgicp_voxelmap_replicate(vgicp_map map, vgicp_ctx ctx, vgicp_map* out);
 int vgicp_voxelmap_size(vgicp_map map, size_t* voxels);                 /* voxelmap.hpp:36 */
 int vgicp_voxelmap_resolution(vgicp_map map, double* resolution);       /* voxelmap.hpp:35 */
 int vgicp_voxelmap_total_points(vgicp_map map, size_t* total_points);   /* voxelmap.hpp:49 */

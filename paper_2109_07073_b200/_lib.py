@@ -77,6 +77,9 @@ SIGNATURES = {
     "vgicp_cloud_upload": (_i, [_vp, _vp, _vp, _sz, C.POINTER(_vp)]),
     "vgicp_cloud_upload_f64": (_i, [_vp, _vp, _vp, _sz, C.POINTER(_vp)]),
     "vgicp_cloud_upload_batch": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
+    "vgicp_cloud_replicate": (_i, [_vp, _vp, C.POINTER(_vp)]),
+    "vgicp_voxelmap_replicate": (_i, [_vp, _vp, C.POINTER(_vp)]),
+    "vgicp_ctx_create_multi": (_i, [_vp, _i, _vp]),
     "vgicp_cloud_is_f64": (_i, [_vp, C.POINTER(_i)]),
     "vgicp_cloud_size": (_i, [_vp, C.POINTER(_sz)]),
     "vgicp_cloud_has_covariances": (_i, [_vp, C.POINTER(_i)]),

@@ -17,6 +17,7 @@
 #include <new>
 #include <thread>
 #include <tuple>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -134,6 +135,19 @@ ScopeFail<F> on_failure(F f) {
   return ScopeFail<F>{f};
 }
 
+template <typename T>
+T* relocate(T* p, const void* old_base, void* new_base) {
+  if (!p) return nullptr;
+  return reinterpret_cast<T*>(static_cast<char*>(new_base) +
+                              (reinterpret_cast<const char*>(p) - static_cast<const char*>(old_base)));
+}
+cudaError_t copy_whole(vgicp_ctx dst, void** out, const void* src, int src_device, size_t bytes) {
+  *out = nullptr;
+  if (!src || !bytes) return cudaSuccess;
+  if (const cudaError_t e = dmalloc(dst, out, bytes); e != cudaSuccess) return e;
+  return cudaMemcpyPeerAsync(*out, dst->device, src, src_device, bytes, dst->stream);
+}
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -178,7 +192,8 @@ int alloc_table(vgicp_map mp, unsigned buckets, cudaStream_t s) {
   const size_t cap = static_cast<size_t>(kBucket) * buckets;
   const size_t b_keys = align_up(sizeof(unsigned long long) * cap, 256);
   const size_t b_sa = align_up(sizeof(SlotStatsA) * cap, 256);
-  VG_CUDA(dmalloc(mp->ctx, &mp->table, b_keys + b_sa + sizeof(SlotStatsB) * cap));
+  mp->table_bytes = b_keys + b_sa + sizeof(SlotStatsB) * cap;
+  VG_CUDA(dmalloc(mp->ctx, &mp->table, mp->table_bytes));
   mp->tkeys = static_cast<unsigned long long*>(mp->table);
   mp->sa = reinterpret_cast<SlotStatsA*>(static_cast<char*>(mp->table) + b_keys);
   mp->sb = reinterpret_cast<SlotStatsB*>(static_cast<char*>(mp->table) + b_keys + b_sa);
@@ -270,6 +285,19 @@ int vgicp_ctx_destroy(vgicp_ctx ctx) try {
   return api_exception();
 }
 
+int vgicp_ctx_create_multi(const int* devices, int n, vgicp_ctx* out) try {
+  if (!devices || !out || n <= 0) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  for (int k = 0; k < n; ++k) out[k] = nullptr;
+  for (int k = 0; k < n; ++k)
+    if (int rc = vgicp_ctx_create(devices[k], nullptr, &out[k])) {
+      for (int q = 0; q < k; ++q) vgicp_ctx_destroy(out[q]), out[q] = nullptr;
+      return rc;
+    }
+  return VGICP_OK;
+} catch (...) {
+  return api_exception();
+}
+
 int vgicp_ctx_stream(vgicp_ctx ctx, void** stream) try {
   if (!ctx || !stream) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *stream = ctx->stream;
@@ -314,7 +342,8 @@ static int cloud_upload_packed(vgicp_ctx ctx, const float* xyz, const float* cov
   const size_t nc = align_up(n * sizeof(float), 256);
   const size_t half = na * 2 + nc;
   const size_t nblk = (n + kPointBlock - 1) / kPointBlock;
-  VG_CUDA(dmalloc(ctx, &c->block, std::max<size_t>(half + nblk * sizeof(PointBlock), 256)));
+  c->block_bytes = std::max<size_t>(half + nblk * sizeof(PointBlock), 256);
+  VG_CUDA(dmalloc(ctx, &c->block, c->block_bytes));
   char* base = static_cast<char*>(c->block);
   c->pa = reinterpret_cast<float4*>(base);
   c->pb = reinterpret_cast<float4*>(base + na);
@@ -406,7 +435,8 @@ int vgicp_cloud_upload_batch(vgicp_ctx ctx, const float* const* xyz, const float
     c->has_cov = cov6 && cov6[k] && n[k] > 0;
     const size_t na = align_up(n[k] * sizeof(float4), 256), nc = align_up(n[k] * sizeof(float), 256);
     const size_t half = 2 * na + nc, nblk = (n[k] + kPointBlock - 1) / kPointBlock;
-    if (const cudaError_t e = dmalloc(ctx, &c->block, std::max<size_t>(half + nblk * sizeof(PointBlock), 256));
+    c->block_bytes = std::max<size_t>(half + nblk * sizeof(PointBlock), 256);
+    if (const cudaError_t e = dmalloc(ctx, &c->block, c->block_bytes);
         e != cudaSuccess) {
       cleanup();
       return cuda_fail(e, "cudaMallocAsync(cloud)");
@@ -590,7 +620,8 @@ static int build_occupancy(vgicp_ctx ctx, vgicp_map* maps, int m, const VoxelSta
     if (words > kOccMaxWords) continue;
     const size_t V = mp->voxels;
     const size_t b_occ = align_up(sizeof(OccWord) * words, 256), b_ra = align_up(sizeof(SlotStatsA) * V, 256);
-    VG_CUDA(dmalloc(ctx, &mp->occ_mem, b_occ + b_ra + sizeof(SlotStatsB) * V));
+    mp->occ_bytes = b_occ + b_ra + sizeof(SlotStatsB) * V;
+    VG_CUDA(dmalloc(ctx, &mp->occ_mem, mp->occ_bytes));
     char* base = static_cast<char*>(mp->occ_mem);
     OccDev& o = mp->occ;
     o.occ = reinterpret_cast<const OccWord*>(base);
@@ -717,7 +748,8 @@ static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const do
     mp->src = c;
     for (int a = 0; a < 3; ++a) mp->cmin[a] = cmin[a], mp->cmax[a] = cmax[a];
     const size_t words = fast_words(cmin, cmax);
-    VG_CUDA(dmalloc(ctx, &mp->occ_mem, sizeof(OccWord) * words));
+    mp->occ_bytes = sizeof(OccWord) * words;
+    VG_CUDA(dmalloc(ctx, &mp->occ_mem, mp->occ_bytes));
     OccDev& o = mp->occ;
     o.occ = static_cast<const OccWord*>(mp->occ_mem);
     o.kx0 = static_cast<unsigned>(cmin[0] + (1 << 20));
@@ -820,7 +852,8 @@ static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const do
     const size_t V = hv[k];
     mp->voxels = V;
     const size_t b_ra = align_up(sizeof(SlotStatsA) * V, 256), b_rb = align_up(sizeof(SlotStatsB) * V, 256);
-    if (const cudaError_t e = dmalloc(ctx, &mp->cold, std::max<size_t>(b_ra + b_rb + sizeof(double) * 9 * V, 256));
+    mp->cold_bytes = std::max<size_t>(b_ra + b_rb + sizeof(double) * 9 * V, 256);
+    if (const cudaError_t e = dmalloc(ctx, &mp->cold, mp->cold_bytes);
         e != cudaSuccess) {
       cleanup();
       return cuda_fail(e, "cudaMallocAsync(voxel map)");
@@ -1145,7 +1178,8 @@ static int build_segments(vgicp_ctx ctx, std::vector<BuildSeg>& segs, vgicp_map*
     const size_t b_counts = align_up(sizeof(int) * V, 256);
     const size_t b_mean = align_up(sizeof(double) * 3 * V, 256);
     const size_t b_cov = align_up(sizeof(double) * 9 * V, 256);
-    const cudaError_t e = dmalloc(ctx, &mp->cold, std::max<size_t>(b_keys + b_counts + b_mean + b_cov, 256));
+    mp->cold_bytes = std::max<size_t>(b_keys + b_counts + b_mean + b_cov, 256);
+    const cudaError_t e = dmalloc(ctx, &mp->cold, mp->cold_bytes);
     if (e != cudaSuccess) {
       cleanup();
       return cuda_fail(e, "cudaMallocAsync(voxel map)");
@@ -1320,7 +1354,8 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
   const size_t nc = align_up(n * sizeof(float), 256);
   const size_t half = na * 2 + nc;
   const size_t nblk = (n + kPointBlock - 1) / kPointBlock;
-  VG_CUDA(dmalloc(ctx, &c->block, std::max<size_t>(half + nblk * sizeof(PointBlock), 256)));
+  c->block_bytes = std::max<size_t>(half + nblk * sizeof(PointBlock), 256);
+  VG_CUDA(dmalloc(ctx, &c->block, c->block_bytes));
   char* base = static_cast<char*>(c->block);
   c->pa = reinterpret_cast<float4*>(base);
   c->pb = reinterpret_cast<float4*>(base + na);
@@ -1329,7 +1364,8 @@ static int cloud_from_device_f64(vgicp_ctx ctx, const double* d_xyz, const doubl
   if (keep64 && n > 0) {
     const size_t bm = align_up(n * 3 * sizeof(double), 256);
     const size_t bc = c->has_cov ? align_up(n * 9 * sizeof(double), 256) : 0;
-    VG_CUDA(dmalloc(ctx, &c->block64, bm + bc + nblk * sizeof(PointBlock64)));
+    c->block64_bytes = bm + bc + nblk * sizeof(PointBlock64);
+    VG_CUDA(dmalloc(ctx, &c->block64, c->block64_bytes));
     char* b64 = static_cast<char*>(c->block64);
     c->f64 = true;
     c->m64 = reinterpret_cast<double*>(b64);
@@ -1466,6 +1502,102 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
   if (out_downsampled) *out_downsampled = ds;
   else release(ds);
   *out_map = mp;
+  return VGICP_OK;
+} catch (...) {
+  return api_exception();
+}
+
+// ------------------------------------------------------------------------------- replication
+// A handle's device state copied whole to another context's device (peer copy over NVLink, or
+// through the host without peer access), internal pointers relocated: the replicated clouds / maps
+// of a sharded graph (one transfer per map instead of a rebuild per device).
+
+static int cloud_replicate(vgicp_cloud src, vgicp_ctx dst, vgicp_cloud* out) {
+  *out = nullptr;
+  VG_CUDA(cudaStreamSynchronize(src->ctx->stream));  // the source layout is complete
+  DeviceGuard g(dst->device);
+  auto c = std::make_unique<vgicp_cloud_s>();
+  c->ctx = dst;
+  c->n = src->n;
+  c->has_cov = src->has_cov;
+  c->f64 = src->f64;
+  for (int a = 0; a < 3; ++a) c->lo[a] = src->lo[a], c->hi[a] = src->hi[a];
+  auto guard = on_failure([&]() {
+    dfree(dst, c->block);
+    dfree(dst, c->block64);
+  });
+  VG_CUDA(copy_whole(dst, &c->block, src->block, src->ctx->device, src->block_bytes));
+  VG_CUDA(copy_whole(dst, &c->block64, src->block64, src->ctx->device, src->block64_bytes));
+  c->block_bytes = src->block_bytes, c->block64_bytes = src->block64_bytes;
+  c->pa = relocate(src->pa, src->block, c->block);
+  c->pb = relocate(src->pb, src->block, c->block);
+  c->pc = relocate(src->pc, src->block, c->block);
+  c->sblk = relocate(src->sblk, src->block, c->block);
+  c->m64 = relocate(src->m64, src->block64, c->block64);
+  c->c64 = relocate(src->c64, src->block64, c->block64);
+  c->blk64 = relocate(src->blk64, src->block64, c->block64);
+  guard.dismiss();
+  *out = c.release();
+  return VGICP_OK;
+}
+
+int vgicp_cloud_replicate(vgicp_cloud cloud, vgicp_ctx ctx, vgicp_cloud* out) try {
+  if (!cloud || !ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  NvtxRange nvtx_("vgicp_cloud_replicate");
+  return cloud_replicate(cloud, ctx, out);
+} catch (...) {
+  return api_exception();
+}
+
+int vgicp_voxelmap_replicate(vgicp_map map, vgicp_ctx ctx, vgicp_map* out) try {
+  if (!map || !ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  NvtxRange nvtx_("vgicp_voxelmap_replicate");
+  VG_CUDA(cudaStreamSynchronize(map->ctx->stream));
+  DeviceGuard g(ctx->device);
+  auto m = std::make_unique<vgicp_map_s>();
+  m->ctx = ctx;
+  m->res = map->res, m->inv_res = map->inv_res, m->voxels = map->voxels, m->total_points = map->total_points;
+  for (int a = 0; a < 3; ++a) m->cmin[a] = map->cmin[a], m->cmax[a] = map->cmax[a];
+  m->num_buckets = map->num_buckets, m->shift = map->shift, m->fast = map->fast;
+  auto guard = on_failure([&]() {
+    dfree(ctx, m->cold);
+    dfree(ctx, m->table);
+    dfree(ctx, m->occ_mem);
+    release(m->src);
+  });
+  const int sd = map->ctx->device;
+  VG_CUDA(copy_whole(ctx, &m->cold, map->cold, sd, map->cold_bytes));
+  VG_CUDA(copy_whole(ctx, &m->table, map->table, sd, map->table_bytes));
+  VG_CUDA(copy_whole(ctx, &m->occ_mem, map->occ_mem, sd, map->occ_bytes));
+  m->cold_bytes = map->cold_bytes, m->table_bytes = map->table_bytes, m->occ_bytes = map->occ_bytes;
+  // every device pointer lies in one of the three allocations
+  auto any = [&](auto* p) -> decltype(p) {
+    using T = std::remove_pointer_t<decltype(p)>;
+    if (!p) return nullptr;
+    const char* c = reinterpret_cast<const char*>(p);
+    auto in = [&](const void* base, size_t bytes) {
+      return base && c >= static_cast<const char*>(base) && c < static_cast<const char*>(base) + bytes;
+    };
+    if (in(map->cold, map->cold_bytes)) return relocate(const_cast<std::remove_const_t<T>*>(p), map->cold, m->cold);
+    if (in(map->table, map->table_bytes)) return relocate(const_cast<std::remove_const_t<T>*>(p), map->table, m->table);
+    return relocate(const_cast<std::remove_const_t<T>*>(p), map->occ_mem, m->occ_mem);
+  };
+  m->keys = any(map->keys);
+  m->counts = any(map->counts);
+  m->mean64 = any(map->mean64);
+  m->cov64 = any(map->cov64);
+  m->tkeys = any(map->tkeys);
+  m->sa = any(map->sa);
+  m->sb = any(map->sb);
+  m->ra = any(map->ra);
+  m->rb = any(map->rb);
+  m->occ = map->occ;
+  m->occ.occ = any(map->occ.occ);
+  if (map->src)
+    if (int rc = cloud_replicate(map->src, ctx, &m->src)) return rc;
+  guard.dismiss();
+  *out = m.release();
   return VGICP_OK;
 } catch (...) {
   return api_exception();

@@ -368,6 +368,7 @@ struct vgicp_cloud_s {
   size_t n = 0;
   bool has_cov = false;
   void* block = nullptr;  // single allocation: pa | pb | pc (input order) | Morton-ordered PointBlocks
+  size_t block_bytes = 0, block64_bytes = 0;  // allocation sizes (replication copies them whole)
   float4* pa = nullptr;   // input order: voxel-map builds accumulate in this order (voxelmap.cpp:87-94)
   float4* pb = nullptr;
   float* pc = nullptr;
@@ -395,6 +396,7 @@ struct vgicp_map_s {
   unsigned shift = 0;
   void* cold = nullptr;   // keys | counts | mean64 | cov64
   void* table = nullptr;  // tkeys | stats
+  size_t cold_bytes = 0, table_bytes = 0, occ_bytes = 0;  // allocation sizes (replication copies them whole)
   unsigned long long* keys = nullptr;
   int* counts = nullptr;
   double* mean64 = nullptr;

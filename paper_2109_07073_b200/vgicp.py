@@ -262,6 +262,14 @@ class PointCloud(_Handle):
                 out[k] = cloud
         return out
 
+    def replicate(self, ctx: "Context") -> "PointCloud":
+        """vgicp_cloud_replicate: this cloud's device layout copied to ctx's device (bit-identical)."""
+        h = C.c_void_p()
+        check(_lib.load().vgicp_cloud_replicate(self._h, ctx.handle, C.byref(h)))
+        cloud = PointCloud.adopt(ctx, h)
+        cloud.means, cloud.cov6 = self.means, self.cov6
+        return cloud
+
     def is_f64(self) -> bool:
         v = C.c_int()
         check(_lib.load().vgicp_cloud_is_f64(self._h, C.byref(v)))
@@ -378,6 +386,13 @@ class GaussianVoxelMap(_Handle):
         super().__init__(cloud.ctx if cloud is not None else _ctx, h)
         self.cloud = cloud  # keeps the source alive for callers that re-derive stats
         self._resolution = float(resolution)
+
+    def replicate(self, ctx: "Context", cloud: "PointCloud | None" = None) -> "GaussianVoxelMap":
+        """vgicp_voxelmap_replicate: the map copied to ctx's device (one transfer, bit-identical
+        statistics) instead of a rebuild there."""
+        h = C.c_void_p()
+        check(_lib.load().vgicp_voxelmap_replicate(self._h, ctx.handle, C.byref(h)))
+        return GaussianVoxelMap(None, self._resolution, _handle=h, _ctx=ctx)
 
     @staticmethod
     def from_arrays(means, covariances, resolution: float, ctx: Context | None = None) -> "GaussianVoxelMap":
@@ -711,6 +726,26 @@ class FactorGraph(_Handle):
         h = C.c_void_p()
         check(_lib.load().vgicp_graph_create_sharded(hs, len(lists), ptrs, n, int(num_poses), int(chunk), C.byref(h)))
         return cls._adopt(ctxs[0], h, lists[0], num_poses, keep=(lists, ctxs))
+
+    @classmethod
+    def sharded_replicas(cls, factors: Sequence[MatchingCostFactor], num_poses: int, contexts: Sequence["Context"],
+                         chunk: int = 0) -> "FactorGraph":
+        """The factors' clouds and maps replicated (vgicp_cloud_replicate / vgicp_voxelmap_replicate,
+        each shared handle once) from contexts[0] onto the other contexts, then ONE sharded graph."""
+        factors = list(factors)
+        lists = [factors]
+        for ctx in contexts[1:]:
+            clouds, maps = {}, {}
+            rep = []
+            for f in factors:
+                c, m = f.source_points, f.target_voxels
+                if id(c) not in clouds:
+                    clouds[id(c)] = c.replicate(ctx)
+                if id(m) not in maps:
+                    maps[id(m)] = m.replicate(ctx)
+                rep.append(MatchingCostFactor(f.target_index, f.source_index, clouds[id(c)], maps[id(m)]))
+            lists.append(rep)
+        return cls.sharded(lists, num_poses, chunk=chunk)
 
     def num_shards(self) -> int:
         v = C.c_int()

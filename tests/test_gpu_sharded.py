@@ -212,3 +212,39 @@ def test_upload_batch_all_empty_and_single(ctxs):
     m = np.random.default_rng(6).uniform(-5, 5, (100, 3)).astype(np.float32)
     one = V.PointCloud.upload_batch([m], [np.tile(np.array([1, 0, 0, 1, 0, 1], np.float32), (100, 1))], ctxs[0])
     assert len(one) == 1 and len(one[0]) == 100 and one[0].has_covariances()
+
+
+def test_replicated_clouds_maps_and_sharded_graph(ctxs):
+    """vgicp_cloud_replicate / vgicp_voxelmap_replicate copy the device state whole: the replicas
+    export the same maps, give the same factor blocks, and a sharded graph over replicas (the usual
+    way to build one: upload / build once, replicate) equals the single-context graph bit for bit —
+    hand-built and sort-based (float64) maps, hash-table and rank lookups alike."""
+    import os
+
+    lists, poses = _problem(ctxs[:1], nframes=6, n=1500, seed=504)
+    f0 = lists[0]
+    full = V.FactorGraph(f0, len(poses))
+    m0 = f0[0].target_voxels
+    r1 = m0.replicate(ctxs[1])
+    for x, y in zip(m0.export(), r1.export()):
+        assert np.array_equal(x, y)
+    pts = np.random.default_rng(8).uniform(-10, 10, (500, 3))
+    assert np.array_equal(m0.lookup(pts), r1.lookup(pts))  # hash table built on demand on the replica
+    sh = V.FactorGraph.sharded_replicas(f0, len(poses), ctxs[:3])
+    assert sh.num_shards() == 3
+    a, ai = full.linearize_raw(poses)
+    b, bi = sh.linearize_raw(poses)
+    assert np.array_equal(a, b) and np.array_equal(ai, bi)
+    # a float64 (sort-based) map and its cloud replicate too
+    rng = O.Rng(505)
+    m, c = rng.gaussian_cloud(800, 5.0)
+    c64 = V.PointCloud(m + 1e-7, c, ctxs[0])
+    g64 = V.GaussianVoxelMap(c64, 0.5)
+    g64r = g64.replicate(ctxs[2])
+    for x, y in zip(g64.export(), g64r.export()):
+        assert np.array_equal(x, y)
+    src = f0[1].source_points
+    fa = V.FactorGraph([V.MatchingCostFactor(0, 1, c64, m0)], 2).linearize_raw(poses[:2])
+    fb = V.FactorGraph([V.MatchingCostFactor(0, 1, c64.replicate(ctxs[1]), r1)], 2).linearize_raw(poses[:2])
+    assert np.array_equal(fa[0], fb[0]) and np.array_equal(fa[1], fb[1])
+    assert src is not None
