@@ -122,6 +122,12 @@ class PointCloud {
   const Context& context() const { return ctx_; }
   // takes ownership of a handle returned by the C ABI (e.g. vgicp_submap_build)
   static PointCloud adopt(const Context& ctx, vgicp_cloud c) { return PointCloud(ctx, c); }
+  // this cloud's device layout copied to another context's device (vgicp_cloud_replicate)
+  PointCloud replicate(const Context& ctx) const {
+    vgicp_cloud c = nullptr;
+    check(vgicp_cloud_replicate(get(), ctx.get(), &c));
+    return PointCloud(ctx, c);
+  }
 
  private:
   PointCloud(const Context& ctx, vgicp_cloud c) : ctx_(ctx) { h_.reset(c, [](vgicp_cloud x) { vgicp_cloud_destroy(x); }); }
@@ -133,6 +139,9 @@ struct GaussianVoxel {  // voxelmap.hpp:18-22
   Vec3 mean{};
   Mat3 covariance{};
   int count = 0;
+  bool operator==(const GaussianVoxel& o) const {
+    return mean == o.mean && covariance == o.covariance && count == o.count;
+  }
 };
 
 // GaussianVoxelMap (voxelmap.hpp:28-56): immutable after construction.
@@ -152,6 +161,12 @@ class GaussianVoxelMap {
     h_.reset(m, [](vgicp_map x) { vgicp_voxelmap_destroy(x); });
   }
   static GaussianVoxelMap adopt(const Context& ctx, vgicp_map m) { return GaussianVoxelMap(ctx, m); }
+  // the map copied to another context's device (vgicp_voxelmap_replicate): one transfer, no rebuild
+  GaussianVoxelMap replicate(const Context& ctx) const {
+    vgicp_map m = nullptr;
+    check(vgicp_voxelmap_replicate(get(), ctx.get(), &m));
+    return GaussianVoxelMap(ctx, m);
+  }
   double resolution() const {
     double r = 0;
     check(vgicp_voxelmap_resolution(get(), &r));

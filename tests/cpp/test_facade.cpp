@@ -189,8 +189,9 @@ int main() {
   // errors and LM result (vgicp_graph_create_sharded)
   {
     Context ctx2(0);
-    auto cloud2 = std::make_shared<PointCloud>(ctx2, xyz, cov);
-    auto map2 = std::make_shared<GaussianVoxelMap>(*cloud2, 1.0);
+    auto cloud2 = std::make_shared<PointCloud>(cloud->replicate(ctx2));  // replicas: one copy each
+    auto map2 = std::make_shared<GaussianVoxelMap>(map->replicate(ctx2));
+    REQUIRE(map2->size() == map->size() && map2->voxels() == map->voxels());
     auto mk = [&](const std::shared_ptr<PointCloud>& c, const std::shared_ptr<GaussianVoxelMap>& m) {
       return std::vector<MatchingCostFactor>{MatchingCostFactor(0, 1, c, m), MatchingCostFactor(1, 2, c, m),
                                              MatchingCostFactor(2, 0, c, m), MatchingCostFactor(0, 2, c, m)};
