@@ -1,5 +1,7 @@
-// C ABI (include/vgicp_b200.h): contexts, handles, validation and launch orchestration.
-// Host code only; the kernels live in voxelmap.cu and factor.cu.
+// C ABI (include/vgicp_b200.h): contexts, handles, validation and launch orchestration (uploads,
+// builds, overlap sweeps, factor graphs incl. sharded ones, assembly, solver plans, replication).
+// Host code only; the kernels live in build.cu, voxelmap.cu, factor.cu, cloud.cu, covariance.cu,
+// solver.cu (and the native LM in lm.cu).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>

@@ -1,8 +1,11 @@
 // Batched VGICP matching-cost factor kernels (sm_100a): linearize (factors.cpp:90-148) and
 // evaluate (factors.cpp:150-181) for every factor of a graph in ONE launch.
 //
-// Grid: one CTA per work item (factor, chunk of source points). Per source point:
-//   fp64  q = T_ts·mu (reference op order), exact voxel key, hash probe of the target map
+// Grid: one CTA per work item (factor, chunk of source points); every warp streams its own 64-point
+// Morton tiles with TMA bulk copies. Per source point:
+//   fp64  q = T_ts·mu (reference op order), exact voxel key, brick-record lookup of the target map's
+//         occupancy bitmap (rank = the voxel's statistics index; cuckoo-hash probes for maps without)
+//   hits  are queued per warp; the math below runs on full batches of 32 queued hits
 //   fp32  e = voxel-local mean - (q - corner), M = C_t + R C_s Rᵀ, Omega = M⁻¹ (cofactor),
 //         H_tt = AᵀΩA with A = [-[q]x | I] as Q = -[q]xΩ[q]x (6), P = [q]xΩ (9), Ω (6),
 //         b_t = [-q×Ωe; -Ωe] (6), error eᵀΩe  -> 28 fp32 accumulators + int inliers
