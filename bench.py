@@ -852,6 +852,7 @@ def run_ours(args):
         "strong_c5": strong_c5,
         "clocks": clk,
         "inlier_fraction": inliers / P,
+        "native_libraries": loaded_native_libraries(),  # product .so + oracle/ (input generator, cpu_baseline)
         "build_seconds": {k: round(v, 3) for k, v in wl.build_seconds.items()} | {"total": round(t_build, 3)},
     }
     print(json.dumps(line), flush=True)
