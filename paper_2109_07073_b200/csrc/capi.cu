@@ -2022,6 +2022,7 @@ static void decompose(vgicp_ctx ctx, const vgicp_factor_desc* factors, int num_f
           !split ? chunk : (num_factors < slots ? few_chunk : (f >= num_factors - slots ? small_chunk : chunk));
       x.blk = d.source->sblk;  // Morton order: neighbouring lanes probe neighbouring voxels
       x.blk64 = d.source->blk64;
+      x.c64 = d.source->c64;
       x.map = g.rank ? d.target->dev_rank() : d.target->dev();
       x.n = static_cast<int>(d.source->n);
       x.tgt = d.target_index;
@@ -2216,6 +2217,7 @@ int vgicp_graph_create_sharded(const vgicp_ctx* ctxs, int num_shards, const vgic
         const vgicp_factor_desc& x = factors[r][f];
         dr.fd[f].blk = x.source->sblk;
         dr.fd[f].blk64 = x.source->blk64;
+        dr.fd[f].c64 = x.source->c64;
         dr.fd[f].map = d.rank ? x.target->dev_rank() : x.target->dev();
       }
       use = &dr;

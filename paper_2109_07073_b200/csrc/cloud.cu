@@ -133,6 +133,7 @@ __global__ void fill_cloud_kernel(Src src, size_t n, const unsigned* __restrict_
           if (blk64) {  // the exact float64 means, same Morton position
             PointBlock64& B64 = blk64[d / kPointBlock];
             src.get64(j, B64.x[d % kPointBlock], B64.y[d % kPointBlock], B64.z[d % kPointBlock]);
+            B64.idx[d % kPointBlock] = static_cast<unsigned>(j);
           }
         }
       }

@@ -55,6 +55,22 @@ __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, f
   return true;
 }
 
+// The same decision for a float64 source cloud: its exact float64 covariance (all 9 entries, as the
+// oracle / reference hold it) instead of the float32 tile copy, so a near-singular M is skipped or
+// kept exactly as the reference's double LDLT decides.
+__device__ __noinline__ bool omega_fp64_c9(const double* T, const double* Cs, const double* Ct, float* om) {
+  double M[9], O[9];
+  combined_cov_rn(T, Cs, Ct, M);
+  if (!invert_covariance_rn(M, O)) return false;
+  om[0] = (float)O[0];
+  om[1] = (float)O[1];
+  om[2] = (float)O[2];
+  om[3] = (float)O[4];
+  om[4] = (float)O[5];
+  om[5] = (float)O[8];
+  return true;
+}
+
 #ifndef VG_ILP
 #define VG_ILP 2
 #endif
@@ -99,11 +115,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 
 // Per-hit math of the linearization (factors.cpp:99-134) in fp32, accumulated into the 28 sums
 // (or the error only): l = (q - voxel corner, q.x), qy/qz the rest of q, C_s = (cxx, cs = (xy xz yy
-// yz), szz), v0/v1/v2 the voxel's slot statistics. Near-singular M -> the fp64 LDLT decision.
-template <bool kLinearize>
+// yz), szz), v0/v1/v2 the voxel's slot statistics. Near-singular M -> the fp64 LDLT decision
+// (kF64: on the float64 covariance of source point `pos`, Morton position in the cloud).
+template <bool kLinearize, bool kF64>
 __device__ __forceinline__ void hit_math(const float* Rf, const double* T, const MapDev& map, float4 l, float qy,
                                          float qz, float cxx, float4 cs, float szz, float4 v0, float4 v1, float2 v2,
-                                         float* acc, int& inl) {
+                                         float* acc, int& inl, const FactorDev* fp, int pos) {
   const float sxx = cxx, sxy = cs.x, sxz = cs.y, syy = cs.z, syz = cs.w;
 
   // residual e = mu' - q in voxel-local coordinates
@@ -153,7 +170,13 @@ __device__ __forceinline__ void hit_math(const float* Rf, const double* T, const
     o22 = a22 * inv;
   } else {
     float om[6];
-    if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64 + 9 * __float_as_int(v2.y), om)) return;
+    const double* Ct = map.cov64 + 9 * __float_as_int(v2.y);
+    if constexpr (kF64) {
+      const unsigned src_i = fp->blk64[pos / kPointBlock].idx[pos % kPointBlock];
+      if (!omega_fp64_c9(T, fp->c64 + 9 * static_cast<size_t>(src_i), Ct, om)) return;
+    } else {
+      if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, Ct, om)) return;
+    }
     o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
   }
   const float w0 = o00 * e0 + o01 * e1 + o02 * e2;
@@ -346,6 +369,7 @@ struct HitQueue {
   float4 b[kQueue];  // q.y q.z slot c_xx
   float4 c[kQueue];  // c_xy c_xz c_yy c_yz
   float d[kQueue];   // c_zz
+  int e[kQueue];     // float64 source clouds only: the point's Morton position in the cloud
 };
 #ifndef VG_MAP_SMEM
 #define VG_MAP_SMEM 1  // the linearize kernel reads the work item's map descriptor from shared memory
@@ -447,7 +471,8 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
            reinterpret_cast<unsigned&>(v0.z), reinterpret_cast<unsigned&>(v0.w), reinterpret_cast<unsigned&>(v1.x),
            reinterpret_cast<unsigned&>(v1.y), reinterpret_cast<unsigned&>(v1.z), reinterpret_cast<unsigned&>(v1.w));
     const float2 v2 = __ldg(reinterpret_cast<const float2*>(map.sb + sl));  // czz vid
-    hit_math<kLinearize>(sm.Rf, T, map, qa, qb.x, qb.y, qb.w, qc, hq.d[idx], v0, v1, v2, acc, inl);
+    hit_math<kLinearize, kF64>(sm.Rf, T, map, qa, qb.x, qb.y, qb.w, qc, hq.d[idx], v0, v1, v2, acc, inl, fp,
+                               kF64 ? hq.e[idx] : 0);
   };
 
   for (int k = 0; k < my_tiles; ++k) {
@@ -530,6 +555,7 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
           hq.b[idx] = make_float4(q1[u], q2[u], __int_as_float(s), kLinearize ? tb.pa[p].w : cxx[u]);
           hq.c[idx] = B;
           hq.d[idx] = tb.pc[p];
+        if constexpr (kF64) hq.e[idx] = w.begin + (warp + k * kWarps) * kPointBlock + p;
         }
         tail += __popc(ball);
       }
@@ -588,6 +614,7 @@ __global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
         hq.b[idx] = make_float4(q1[u], q2[u], __int_as_float(s), kLinearize ? tb.pa[p].w : cxx[u]);
         hq.c[idx] = B;
         hq.d[idx] = tb.pc[p];
+        if constexpr (kF64) hq.e[idx] = w.begin + (warp + k * kWarps) * kPointBlock + p;
       }
       tail += __popc(ball);
     }

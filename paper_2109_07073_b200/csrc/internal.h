@@ -58,17 +58,22 @@ struct PointBlock {
 static_assert(sizeof(PointBlock) % 128 == 0, "blocks must stay 128-B aligned");
 // Clouds whose means are not float32-exact (submap clouds: transform_cloud + voxel_downsample output,
 // pipeline.cpp:100-111; any float64 upload) also keep their float64 means in the same Morton blocks,
-// SoA per block: x[64] | y[64] | z[64] (1,536 B). The probe kernels transform THESE values, so keys,
+// SoA per block: x[64] | y[64] | z[64] | idx[64] (1,792 B). The probe kernels transform THESE values, so keys,
 // correspondences and overlap hits stay bit-exact against the reference's double arithmetic.
+// idx: each point's input index (its float64 covariance is c64[9 * idx]; read only by the factor
+// kernels' near-singular path, which must decide on the exact float64 source covariance).
 struct PointBlock64 {
   double x[kPointBlock];
   double y[kPointBlock];
   double z[kPointBlock];
+  unsigned idx[kPointBlock];
 };
+static_assert(sizeof(PointBlock64) % 128 == 0, "blocks must stay 128-B aligned");
 
 struct FactorDev {
   const PointBlock* blk;
   const PointBlock64* blk64;  // float64 means of the same blocks, or nullptr (float32-exact cloud)
+  const double* c64;          // float64 covariances (n×9, input order) of a float64 cloud, else nullptr
   MapDev map;
   int n;
   int tgt;
