@@ -398,7 +398,12 @@ static_assert(sizeof(WarpTile) * kStages >= sizeof(double) * 180, "epilogue scra
 // instead of the float32 tile copies); such items follow the float32 ones and run in their own
 // launch, so the float32 kernel keeps its register budget. item_base: first item of this launch.
 template <bool kLinearize, bool kRank, bool kF64>
-__global__ void __launch_bounds__(kFactorThreads, VG_MINB) factor_kernel(
+#ifdef VG_MAXNREG  // experiment switch: explicit register cap instead of the occupancy-derived one
+#define VG_FACTOR_BOUNDS __maxnreg__(VG_MAXNREG)
+#else
+#define VG_FACTOR_BOUNDS __launch_bounds__(kFactorThreads, VG_MINB)
+#endif
+__global__ void VG_FACTOR_BOUNDS factor_kernel(
     const FactorDev* __restrict__ factors, const WorkItem* __restrict__ items, int item_base,
     const double* __restrict__ poses, double* __restrict__ partials, int* __restrict__ part_inl,
     unsigned* __restrict__ counters, double* __restrict__ out, int* __restrict__ out_inl) {
