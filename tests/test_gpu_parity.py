@@ -171,6 +171,36 @@ def test_range_and_invalid(ctx):  # test_voxelmap.cpp:185-188, voxelmap.cpp:67-7
         V.overlap_rate(empty, O.IDENTITY, g)
 
 
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_map_points_are_out_of_range(ctx, monkeypatch, bad):
+    """A NaN / Inf point in a map's cloud fails the reference's range test (voxelmap.cpp:45-55:
+    !(c >= -2^20 && c < 2^20) holds for NaN) -> out_of_range, no map — for the hand-written build,
+    the sort-based build, a batch (the whole batch fails, as the oracle fails on that cloud), and
+    float64 clouds."""
+    rng = np.random.default_rng(5)
+    pts = rng.uniform(-5, 5, size=(500, 3))
+    pts[137, 1] = bad
+    cov = O.unit_covariances(len(pts))
+    with pytest.raises(O.OracleOutOfRange):
+        O.OracleMap(np.asarray(pts, np.float32).astype(np.float64), cov, 1.0)
+    cloud, _, _ = gpu_cloud(ctx, pts, cov)
+    good, _, _ = gpu_cloud(ctx, rng.uniform(-5, 5, size=(300, 3)), O.unit_covariances(300))
+    with pytest.raises(IndexError):
+        V.GaussianVoxelMap(cloud, 1.0)
+    with pytest.raises(IndexError):
+        V.GaussianVoxelMap.build_batch([good, cloud], [1.0, 0.5])
+    monkeypatch.setenv("VGICP_SORTED_BUILD", "1")
+    with pytest.raises(IndexError):
+        V.GaussianVoxelMap(cloud, 1.0)
+    monkeypatch.delenv("VGICP_SORTED_BUILD")
+    p64 = pts + 1e-9
+    c64 = V.PointCloud(p64, cov.reshape(-1, 3, 3), ctx)
+    assert c64.is_f64()
+    with pytest.raises(IndexError):
+        V.GaussianVoxelMap(c64, 1.0)
+    assert V.GaussianVoxelMap(good, 1.0).size() > 0  # the context stays usable
+
+
 # ------------------------------------------------------------------------------ overlap
 def test_overlap_self_and_far(ctx):  # test_voxelmap.cpp:138-149
     rng = O.Rng(14)
