@@ -722,3 +722,36 @@ def test_upload_batch_equals_single_uploads(ctx):
     rel = O.compose(O.inverse(poses[0]), poses[1])
     maps = V.GaussianVoxelMap.build_batch(batch[:1], [1.0])
     assert V.overlap_hits([batch[5]], [rel], maps)[0] == V.overlap_hits([V.PointCloud(raw, None, ctx)], [rel], maps)[0]
+
+
+def test_sprawling_map_in_a_batch_and_graph(ctx):
+    """A cloud whose occupied box is too large for an occupancy bitmap (two clusters ~4e5 voxels
+    apart) takes the sort-based build inside a batch of hand-built maps; every map still exports the
+    oracle's statistics, and a graph over both kinds falls back to hash probes for all its factors
+    (rank lookups need every target to carry bricks) with oracle-exact inliers."""
+    rng = O.Rng(77)
+    clouds, frames = [], []
+    for k in range(4):
+        means, covs = rng.gaussian_cloud(2500, 8.0)
+        means = np.asarray(means)
+        if k == 1:  # second cluster far away on every axis
+            means[1250:] += np.array([2.0e5, -1.9e5, 1.8e5])
+        c, m, c9 = gpu_cloud(ctx, means, covs)
+        clouds.append(c)
+        frames.append((m, c9))
+    maps = V.GaussianVoxelMap.build_batch(clouds, [0.5, 0.5, 1.0, 1.0])
+    omaps = [O.OracleMap(m, c9, r) for (m, c9), r in zip(frames, [0.5, 0.5, 1.0, 1.0])]
+    for g, o in zip(maps, omaps):
+        assert_map_parity(g, o)
+    poses = [rng.random_pose(0.03, 0.3) for _ in range(4)]
+    factors = [V.MatchingCostFactor(i, j, clouds[j], maps[i]) for i, j in ((0, 1), (1, 2), (1, 3), (2, 3), (0, 3))]
+    graph = V.FactorGraph(factors, 4)
+    raw, inl = graph.linearize_raw(np.stack(poses))
+    for k, f in enumerate(factors):
+        m, c9 = frames[f.source_index]
+        ref = O.linearize(m, c9, omaps[f.target_index], poses[f.target_index], poses[f.source_index])
+        assert int(inl[k]) == ref["inliers"]
+        d = rel_block_error(O.unpack121(raw[k]), ref)
+        assert max(d.values()) <= H_TOL, d
+    rel = O.compose(O.inverse(poses[1]), poses[2])
+    assert V.overlap_hits(clouds[2], [rel], [maps[1]])[0] == O.overlap_hits(frames[2][0], rel, omaps[1])
