@@ -755,3 +755,24 @@ def test_sprawling_map_in_a_batch_and_graph(ctx):
         assert max(d.values()) <= H_TOL, d
     rel = O.compose(O.inverse(poses[1]), poses[2])
     assert V.overlap_hits(clouds[2], [rel], [maps[1]])[0] == O.overlap_hits(frames[2][0], rel, omaps[1])
+
+
+@pytest.mark.parametrize("n,res", [(70000, 1000.0), (30000, 0.5)])
+def test_extreme_voxel_occupancy(ctx, n, res):
+    """One voxel holding every point (70k points, 1 km voxels: one lane folds them all in input order),
+    and 30k identical points: exports equal the oracle's Kahan merge bit for bit; a factor over the
+    one-voxel map matches the oracle."""
+    rng = np.random.default_rng(11)
+    if res > 1.0:
+        pts = rng.uniform(1.0, 900.0, size=(n, 3))
+    else:
+        pts = np.repeat(np.array([[3.3, -7.1, 0.26]]), n, axis=0)
+    covs = np.repeat(np.diag([0.3, 0.2, 1e-3])[None], n, axis=0)
+    cloud, m, c9 = gpu_cloud(ctx, pts, covs)
+    gmap = V.GaussianVoxelMap(cloud, res)
+    omap = O.OracleMap(m, c9, res)
+    assert gmap.size() == 1
+    assert_map_parity(gmap, omap)
+    src, sm, sc9 = gpu_cloud(ctx, pts[:5000] + 0.01, covs[:5000])
+    fac = V.MatchingCostFactor(0, 1, src, gmap)
+    check_factor(fac, sm, sc9, omap, O.IDENTITY, O.IDENTITY)
