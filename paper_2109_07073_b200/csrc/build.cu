@@ -485,7 +485,10 @@ constexpr int kAccWarps = kAccThreads / 32;
 constexpr int kStage = 64;  // staged points per warp and round
 
 template <bool kExport>
-__global__ void __launch_bounds__(kAccThreads, 3) fast_accumulate_kernel(const FastBuildJob* __restrict__ jobs,
+#ifndef VG_ACC_MINB
+#define VG_ACC_MINB 3
+#endif
+__global__ void __launch_bounds__(kAccThreads, VG_ACC_MINB) fast_accumulate_kernel(const FastBuildJob* __restrict__ jobs,
                                                                          const unsigned* __restrict__ list,
                                                                          const unsigned* __restrict__ offs,
                                                                          const unsigned* __restrict__ code) {
