@@ -164,6 +164,10 @@ int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* 
  * two launches and the hit download. Results equal vgicp_overlap_batch's. The set holds references
  * to its maps. */
 int vgicp_mapset_create(vgicp_ctx ctx, const vgicp_map* maps, int m, vgicp_mapset* out);
+/* Adds maps at the end of the set (a new keyframe's map): amortised O(1) device work per map (the
+ * device block grows geometrically); earlier maps keep their positions in hits[]. */
+int vgicp_mapset_append(vgicp_mapset set, const vgicp_map* maps, int m);
+int vgicp_mapset_size(vgicp_mapset set, int* size);
 int vgicp_mapset_destroy(vgicp_mapset set);
 int vgicp_overlap_mapset(vgicp_ctx ctx, vgicp_cloud cloud, const double* rel12, vgicp_mapset set, uint64_t* hits);
 

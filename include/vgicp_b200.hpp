@@ -330,6 +330,12 @@ class KeyframeSet {
     for (std::size_t k = 0; k < size_; ++k) out[k] = static_cast<double>(hits[k]) / static_cast<double>(cloud.size());
     return out;
   }
+  // a new keyframe's map joins the set (amortised O(1) device work)
+  void append(const GaussianVoxelMap& map) {
+    vgicp_map mh = map.get();
+    check(vgicp_mapset_append(h_.get(), &mh, 1));
+    ++size_;
+  }
   std::size_t size() const { return size_; }
 
  private:

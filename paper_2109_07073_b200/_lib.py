@@ -123,6 +123,8 @@ SIGNATURES = {
     "vgicp_graph_optimize": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
     "vgicp_mapset_create": (_i, [_vp, _vp, C.c_int, _vp]),
     "vgicp_mapset_destroy": (_i, [_vp]),
+    "vgicp_mapset_append": (_i, [_vp, _vp, C.c_int]),
+    "vgicp_mapset_size": (_i, [_vp, _vp]),
     "vgicp_overlap_mapset": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "vgicp_transform_cloud": (_i, [_vp, _vp, _vp, _sz, _vp, _vp, _vp]),
     "vgicp_submap_build": (_i, [_vp, _vp, _vp, _i, _d, _d, _vp, _vp, _vp]),

@@ -1838,41 +1838,100 @@ int vgicp_overlap_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* 
 }
 
 // ------------------------------------------------------------------------------- map sets
+// Device block of a map set laid out for `cap` maps (templates | items | chunks | hits | poses + box);
+// the first `keep` templates move over from the previous block.
+static int mapset_reserve(vgicp_mapset set, int cap, int keep) {
+  if (cap <= set->capacity) return VGICP_OK;
+  vgicp_ctx ctx = set->ctx;
+  const int nch = (cap + kOverlapMapsPerChunk - 1) / kOverlapMapsPerChunk;
+  const size_t bt = align_up(sizeof(OverlapItem) * cap, 256), bc = align_up(sizeof(int2) * nch, 256);
+  const size_t bh = align_up(sizeof(unsigned long long) * cap, 256), bp = align_up(sizeof(double) * 12 * cap + 64, 256);
+  void* block = nullptr;
+  if (const cudaError_t e = dmalloc(ctx, &block, 2 * bt + bc + bh + bp); e != cudaSuccess)
+    return cuda_fail(e, ("mapset block of " + std::to_string(cap) + " maps, " + std::to_string(2 * bt + bc + bh + bp) +
+                         " B").c_str());
+  char* b = static_cast<char*>(block);
+  auto* templates = reinterpret_cast<OverlapItem*>(b);
+  if (keep > 0) {
+    if (const cudaError_t e = cudaMemcpyAsync(templates, set->d_templates, sizeof(OverlapItem) * keep,
+                                              cudaMemcpyDeviceToDevice, ctx->stream);
+        e != cudaSuccess) {
+      dfree(ctx, block);
+      return cuda_fail(e, "cudaMemcpyAsync");
+    }
+  }
+  if (set->block) {
+    cudaStreamSynchronize(ctx->stream);  // the old block may still be read by a queued sweep / the copy
+    dfree(ctx, set->block);
+  }
+  set->block = block;
+  set->d_templates = templates;
+  set->d_items = reinterpret_cast<OverlapItem*>(b + bt);
+  set->d_chunks = reinterpret_cast<int2*>(b + 2 * bt);
+  set->d_hits = reinterpret_cast<unsigned long long*>(b + 2 * bt + bc);
+  set->d_poses = reinterpret_cast<double*>(b + 2 * bt + bc + bh);
+  set->capacity = cap;
+  return VGICP_OK;
+}
+
+// Appends maps[0..m) to the set: validation, then (device path) their templates after the existing
+// ones — the block grows geometrically, so a keyframe database that gains one map per keyframe
+// pays an amortised O(1) upload per map.
+static int mapset_add(vgicp_mapset set, const vgicp_map* maps, int m) {
+  vgicp_ctx ctx = set->ctx;
+  bool occ = set->all_occ;
+  for (int k = 0; k < m; ++k) {
+    if (!maps[k]) return fail(VGICP_E_INVALID_ARGUMENT, "null map");
+    if (maps[k]->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "handle of another context");
+    occ = occ && maps[k]->occ.occ != nullptr;
+  }
+  const int size = static_cast<int>(set->maps.size());
+  if (occ && m > 0) {
+    DeviceGuard g(ctx->device);
+    if (size + m > set->capacity)
+      if (int rc = mapset_reserve(set, std::max(size + m, 2 * set->capacity), size)) return rc;
+    static const double kIdentity[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+    vgicp_cloud_s dummy;  // the template carries no cloud; fill_overlap_item needs one for blk / n
+    std::vector<OverlapItem> templ(m);
+    for (int k = 0; k < m; ++k) fill_overlap_item(templ[k], &dummy, kIdentity, maps[k]);
+    VG_CUDA(cudaMemcpyAsync(set->d_templates + size, templ.data(), sizeof(OverlapItem) * m, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  set->all_occ = occ;  // a map without a bitmap moves the whole set to the generic path
+  for (int k = 0; k < m; ++k) {
+    maps[k]->refs.fetch_add(1);
+    set->maps.push_back(maps[k]);
+  }
+  return VGICP_OK;
+}
+
 int vgicp_mapset_create(vgicp_ctx ctx, const vgicp_map* maps, int m, vgicp_mapset* out) try {
   if (!ctx || !out || (m > 0 && !maps) || m < 0) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   auto set = std::make_unique<vgicp_mapset_s>();
   set->ctx = ctx;
-  std::vector<OverlapItem> templ(m);
-  for (int k = 0; k < m; ++k) {
-    if (!maps[k]) return fail(VGICP_E_INVALID_ARGUMENT, "null map");
-    if (maps[k]->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "handle of another context");
-    set->all_occ = set->all_occ && maps[k]->occ.occ != nullptr;
-  }
-  DeviceGuard g(ctx->device);
-  if (set->all_occ && m > 0) {
-    static const double kIdentity[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
-    vgicp_cloud_s dummy;  // the template carries no cloud; fill_overlap_item needs one for blk / n
-    for (int k = 0; k < m; ++k) fill_overlap_item(templ[k], &dummy, kIdentity, maps[k]);
-    const int nch = (m + kOverlapMapsPerChunk - 1) / kOverlapMapsPerChunk;
-    const size_t bt = align_up(sizeof(OverlapItem) * m, 256), bc = align_up(sizeof(int2) * nch, 256);
-    const size_t bh = align_up(sizeof(unsigned long long) * m, 256), bp = align_up(sizeof(double) * 12 * m + 64, 256);
-    VG_CUDA(dmalloc(ctx, &set->block, 2 * bt + bc + bh + bp));
-    char* b = static_cast<char*>(set->block);
-    set->d_templates = reinterpret_cast<OverlapItem*>(b);
-    set->d_items = reinterpret_cast<OverlapItem*>(b + bt);
-    set->d_chunks = reinterpret_cast<int2*>(b + 2 * bt);
-    set->d_hits = reinterpret_cast<unsigned long long*>(b + 2 * bt + bc);
-    set->d_poses = reinterpret_cast<double*>(b + 2 * bt + bc + bh);
-    VG_CUDA(cudaMemcpyAsync(set->d_templates, templ.data(), sizeof(OverlapItem) * m, cudaMemcpyHostToDevice,
-                            ctx->stream));
-    VG_CUDA(cudaStreamSynchronize(ctx->stream));
-  }
-  for (int k = 0; k < m; ++k) {
-    maps[k]->refs.fetch_add(1);
-    set->maps.push_back(maps[k]);
+  if (int rc = mapset_add(set.get(), maps, m)) {
+    vgicp_mapset_destroy(set.release());
+    return rc;
   }
   *out = set.release();
+  return VGICP_OK;
+} catch (...) {
+  return api_exception();
+}
+
+int vgicp_mapset_append(vgicp_mapset set, const vgicp_map* maps, int m) try {
+  NvtxRange nvtx_("vgicp_mapset_append");
+  if (!set || m < 0 || (m > 0 && !maps)) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  return mapset_add(set, maps, m);
+} catch (...) {
+  return api_exception();
+}
+
+int vgicp_mapset_size(vgicp_mapset set, int* size) try {
+  if (!set || !size) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
+  *size = static_cast<int>(set->maps.size());
   return VGICP_OK;
 } catch (...) {
   return api_exception();

@@ -429,6 +429,7 @@ struct vgicp_mapset_s {
   vgicp_ctx ctx = nullptr;
   std::vector<vgicp_map> maps;
   bool all_occ = true;            // every map carries an occupancy bitmap (device path)
+  int capacity = 0;               // maps the device block is laid out for (vgicp_mapset_append grows it)
   void* block = nullptr;          // templates | items | chunks | hits | poses
   vgicp::OverlapItem* d_templates = nullptr;
   vgicp::OverlapItem* d_items = nullptr;

@@ -500,15 +500,31 @@ class MapSet:
     frame is swept against, pipeline.cpp:135-150): overlap_hits(cloud, poses, map_set) then skips
     the per-call marshalling of thousands of handles."""
 
-    def __init__(self, maps):
+    def __init__(self, maps, ctx: Context | None = None):
         self.maps = list(maps)
         self.handles = np.fromiter((x.handle.value for x in self.maps), dtype=np.uint64, count=len(self.maps))
-        self.ctx = self.maps[0].ctx if self.maps else None
+        self.ctx = self.maps[0].ctx if self.maps else ctx
         self._h = None
-        if self.maps:  # device-resident copy (vgicp_mapset): single-cloud sweeps build their items on the GPU
+        if self.ctx is not None:  # device-resident copy (vgicp_mapset): single-cloud sweeps build their items on the GPU
             h = C.c_void_p()
             check(_lib.load().vgicp_mapset_create(self.ctx.handle, _ptr(self.handles), len(self.maps), C.byref(h)))
             self._h = h
+
+    def append(self, maps) -> "MapSet":
+        """Add maps at the end (a new keyframe's map): vgicp_mapset_append, amortised O(1) per map."""
+        new = [maps] if isinstance(maps, GaussianVoxelMap) else list(maps)
+        if not new:
+            return self
+        if self._h is None:  # an empty set made without a context: adopt the first map's
+            self.ctx = new[0].ctx
+            h = C.c_void_p()
+            check(_lib.load().vgicp_mapset_create(self.ctx.handle, None, 0, C.byref(h)))
+            self._h = h
+        handles = np.fromiter((x.handle.value for x in new), dtype=np.uint64, count=len(new))
+        check(_lib.load().vgicp_mapset_append(self._h, _ptr(handles), len(new)))
+        self.maps.extend(new)
+        self.handles = np.concatenate([self.handles, handles])
+        return self
 
     def close(self):
         if getattr(self, "_h", None):

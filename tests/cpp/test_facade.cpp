@@ -131,6 +131,9 @@ int main() {
     const auto r = set.overlap_rates(*cloud, {Pose::Identity(), T});
     REQUIRE(r.size() == 2 && r[0] == overlap_rate(*cloud, Pose::Identity(), *map) &&
             r[1] == overlap_rate(*cloud, T, *map));
+    set.append(*map);  // a new keyframe joins the set
+    const auto r3 = set.overlap_rates(*cloud, {Pose::Identity(), T, T});
+    REQUIRE(set.size() == 3 && r3[0] == r[0] && r3[1] == r[1] && r3[2] == r[1]);
   }
 
   // native LM (optimizer.cpp:88-194): the error never increases along the trace, the fixed pose

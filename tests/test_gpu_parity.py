@@ -776,3 +776,36 @@ def test_extreme_voxel_occupancy(ctx, n, res):
     src, sm, sc9 = gpu_cloud(ctx, pts[:5000] + 0.01, covs[:5000])
     fac = V.MatchingCostFactor(0, 1, src, gmap)
     check_factor(fac, sm, sc9, omap, O.IDENTITY, O.IDENTITY)
+
+
+def test_mapset_append_matches_batch(ctx):
+    """A keyframe database grown one map at a time (vgicp_mapset_append, geometric growth of the
+    device block) sweeps exactly like vgicp_overlap_batch and like a set created in one call; a map
+    without an occupancy bitmap (sprawling box) moves the set to the generic path, still exact."""
+    rng = O.Rng(91)
+    clouds, frames, maps = [], [], []
+    for k in range(40):
+        means, covs = rng.gaussian_cloud(800, 6.0)
+        c, m, c9 = gpu_cloud(ctx, means, covs)
+        clouds.append(c)
+        frames.append((m, c9))
+    maps = V.GaussianVoxelMap.build_batch(clouds, [0.5 + 0.05 * (k % 7) for k in range(40)])
+    probe = clouds[0]
+    grown = V.MapSet([], ctx=ctx)
+    for k, mp in enumerate(maps):
+        grown.append(mp)
+        if k in (0, 1, 4, 17, 39):
+            rels = [rng.random_pose(0.05, 0.4) for _ in range(k + 1)]
+            a = V.overlap_hits(probe, rels, grown)
+            b = V.overlap_hits([probe] * (k + 1), rels, maps[:k + 1])
+            c = V.overlap_hits(probe, rels, V.MapSet(maps[:k + 1]))
+            assert np.array_equal(a, b) and np.array_equal(a, c)
+    far = np.asarray(rng.gaussian_cloud(800, 6.0)[0])
+    far[400:] += np.array([2.0e5, 1.5e5, -2.5e5])
+    fc, fm, fc9 = gpu_cloud(ctx, far, O.unit_covariances(len(far)))
+    sprawl = V.GaussianVoxelMap(fc, 0.5)
+    grown.append([sprawl])
+    rels = [rng.random_pose(0.05, 0.4) for _ in range(41)]
+    a = V.overlap_hits(probe, rels, grown)
+    assert np.array_equal(a, V.overlap_hits([probe] * 41, rels, maps + [sprawl]))
+    assert a[40] == O.overlap_hits(frames[0][0], rels[40], O.OracleMap(fm, fc9, 0.5))
