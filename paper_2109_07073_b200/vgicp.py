@@ -178,7 +178,7 @@ class PointCloud(_Handle):
         m64 = np.asarray(means)
         m64 = m64.reshape(-1, 3) if m64.size else m64.reshape(0, 3)
         c64 = None if covariances is None else np.asarray(covariances)
-        if c64 is not None and len(c64.reshape(len(c64), -1)) != len(m64):
+        if c64 is not None and (c64.ndim == 0 or c64.shape[0] != len(m64)):
             raise ValueError("covariance count does not match point count")
         h = C.c_void_p()
         if self._needs_f64(m64, c64):

@@ -169,6 +169,13 @@ def test_range_and_invalid(ctx):  # test_voxelmap.cpp:185-188, voxelmap.cpp:67-7
     g = V.GaussianVoxelMap(ok, 1.0)
     with pytest.raises(ValueError):
         V.overlap_rate(empty, O.IDENTITY, g)
+    # an empty cloud has no covariances (point_cloud.hpp:28): no map (voxelmap.cpp:69-71), no factor
+    # source (factors.cpp:58-63)
+    empty_cov = V.PointCloud(np.zeros((0, 3), np.float32), np.zeros((0, 6), np.float32), ctx)
+    with pytest.raises(ValueError):
+        V.GaussianVoxelMap(empty_cov, 1.0)
+    with pytest.raises(ValueError):
+        V.MatchingCostFactor(0, 1, empty_cov, g)
 
 
 @pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
