@@ -290,6 +290,13 @@ __device__ __forceinline__ void finish_factor(const float* acc, int inl, int lan
   } else {
     const int f = w.factor;
     double* o = out + (size_t)f * VGICP_LINEARIZED_DOUBLES;
+    if (__shfl_sync(0xffffffffu, tinl, 0) == 0) {
+      // no hit: the reference's accumulators stay zero (factors.cpp:97-146) — also when T_ts is not
+      // finite, where the Ad(T_ts) expansion below would turn 0 into NaN
+      for (int t = lane; t < VGICP_LINEARIZED_DOUBLES - 1; t += 32) o[t] = 0.0;
+      if (lane == 0) o[VGICP_LINEARIZED_DOUBLES - 1] = 0.0, out_inl[f] = 0;
+      return;
+    }
     for (int t = lane; t < 36; t += 32) {
       const int i = t / 6, j = t % 6;
       // H_tt = [[Q, P], [Pᵀ, Ω]]

@@ -816,3 +816,24 @@ def test_mapset_append_matches_batch(ctx):
     a = V.overlap_hits(probe, rels, grown)
     assert np.array_equal(a, V.overlap_hits([probe] * 41, rels, maps + [sprawl]))
     assert a[40] == O.overlap_hits(frames[0][0], rels[40], O.OracleMap(fm, fc9, 0.5))
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_nonfinite_pose_gives_zero_factor(ctx, bad):
+    """A non-finite pose transforms every point to NaN / Inf: no lookup hits (voxelmap.cpp:110-112), so
+    the reference's accumulators stay zero (factors.cpp:97-146) — an all-zero block with 0 inliers,
+    not the NaN an Ad(T) expansion of zeros would give; the graph's other factors are unaffected."""
+    factors, frames, omaps, poses = build_graph_case(ctx, nframes=4, n=2000, seed=63)
+    P = np.stack(poses)
+    P[2, 9] = bad
+    raw, inl = V.FactorGraph(factors, 4).linearize_raw(P)
+    err, inl2 = V.FactorGraph(factors, 4).evaluate(P)
+    for k, f in enumerate(factors):
+        m, c9 = frames[f.source_index]
+        ref = O.linearize(m, c9, omaps[f.target_index], P[f.target_index], P[f.source_index])
+        if 2 in (f.target_index, f.source_index):
+            assert inl[k] == 0 == ref["inliers"] and inl2[k] == 0
+            assert not np.any(raw[k]) and not np.any(ref["raw"]) and err[k] == 0.0
+        else:
+            assert inl[k] == ref["inliers"] > 0
+            assert max(rel_block_error(O.unpack121(raw[k]), ref).values()) <= H_TOL

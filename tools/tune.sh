@@ -5,4 +5,4 @@ run() {  # $1 = label, rest = env/args
     python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$label', 'lin %.3f ms' % d['ms_linearize_kernel'], 'eval %.3f ms' % d['ms_evaluate_kernel'], 'value %.0f' % d['value'])"
 }
 run default VGICP_LIB=$PWD/paper_2109_07073_b200/lib/libvgicp_b200.so
-for v in paper_2109_07073_b200/lib_variants/*; do run "$(basename $v)" VGICP_LIB=$PWD/$v/libvgicp_b200.so; done
+for v in paper_2109_07073_b200/lib_variants/*/; do [ -d "$v" ] || continue; v=${v%/}; run "$(basename $v)" VGICP_LIB=$PWD/$v/libvgicp_b200.so; done
