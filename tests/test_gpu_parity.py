@@ -837,3 +837,30 @@ def test_nonfinite_pose_gives_zero_factor(ctx, bad):
         else:
             assert inl[k] == ref["inliers"] > 0
             assert max(rel_block_error(O.unpack121(raw[k]), ref).values()) <= H_TOL
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_overlap_nonfinite_pose_and_points(ctx, monkeypatch, bad):
+    """overlap_rate (voxelmap.cpp:119-135) with a non-finite pose counts no hit; non-finite probe points
+    never hit — on the occupancy path (batch and map set) and on the hash-probe path, equal to the
+    oracle."""
+    rng = O.Rng(95)
+    tm, tc = rng.gaussian_cloud(3000, 6.0)
+    sm, sc = rng.gaussian_cloud(3000, 6.0)
+    sm = np.asarray(sm)
+    sm[::37] = bad
+    tgt, tmm, tc9 = gpu_cloud(ctx, tm, tc)
+    src, smm, _ = gpu_cloud(ctx, sm, sc)
+    gmap = V.GaussianVoxelMap(tgt, 0.5)
+    omap = O.OracleMap(tmm, tc9, 0.5)
+    good = rng.random_pose(0.05, 0.3)
+    badpose = np.array(good)
+    badpose[4] = bad
+    poses = [good, badpose]
+    want = [O.overlap_hits(smm, p, omap) for p in poses]
+    assert want[1] == 0 and want[0] > 0
+    assert list(V.overlap_hits([src, src], poses, [gmap, gmap])) == want
+    assert list(V.overlap_hits(src, poses, V.MapSet([gmap, gmap]))) == want
+    monkeypatch.setenv("VGICP_OVERLAP_PERITEM", "1")  # the generic per-item kernel
+    assert list(V.overlap_hits([src, src], poses, [gmap, gmap])) == want
+    monkeypatch.delenv("VGICP_OVERLAP_PERITEM")
