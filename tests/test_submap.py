@@ -204,3 +204,19 @@ def test_gpu_submap_validation(V):
     raw = V.PointCloud(frames64[0][0])
     with pytest.raises(ValueError):
         V.build_submap([raw], poses[:1], 0.5, 1.0)
+
+
+@gpu
+def test_gpu_submap_nonfinite_pose_is_out_of_range(V):
+    """A non-finite frame pose makes NaN submap points; voxel_downsample / the map build then raise
+    out_of_range (voxelmap.cpp:45-55) in the oracle and on the GPU alike (with and without downsampling);
+    the context stays usable."""
+    frames64, poses, clouds = submap_case(V, nframes=2, n=200)
+    bad = np.array(poses, dtype=np.float64)
+    bad[1, 9] = np.nan
+    with pytest.raises(O.OracleOutOfRange):
+        O.submap(frames64, bad, 0.5, 1.0)
+    for ds in (0.5, 0.0):
+        with pytest.raises(IndexError):
+            V.build_submap(clouds, bad, ds, 1.0)
+    assert V.build_submap(clouds, poses, 0.5, 1.0) is not None
