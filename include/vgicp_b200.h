@@ -110,8 +110,9 @@ int vgicp_cloud_replicate(vgicp_cloud cloud, vgicp_ctx ctx, vgicp_cloud* out);
 
 /* ---------------------------------------------------------------- Gaussian voxel maps */
 /* GaussianVoxelMap(cloud, resolution) — voxelmap.cpp:65-104. Errors: resolution <= 0 or a
- * cloud without covariances -> INVALID_ARGUMENT; a coordinate beyond ±2^20 voxels ->
- * OUT_OF_RANGE (and no map). */
+ * cloud without covariances -> INVALID_ARGUMENT; a coordinate beyond ±2^20 voxels, a NaN / Inf
+ * point or a NaN resolution -> OUT_OF_RANGE (and no map), in the reference's check order. One
+ * deviation: resolution = +inf (the reference maps every point to voxel 0) -> INVALID_ARGUMENT. */
 int vgicp_voxelmap_build(vgicp_ctx ctx, vgicp_cloud cloud, double resolution, vgicp_map* out);
 /* m maps in one batched build (all-or-nothing: on error no map is returned). */
 int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* resolutions, int m,

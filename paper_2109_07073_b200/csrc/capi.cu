@@ -1003,6 +1003,16 @@ static int ensure_table(vgicp_map mp) {
   }
 }
 
+// GaussianVoxelMap ctor's resolution check (voxelmap.cpp:66-68: `resolution <= 0` -> invalid_argument).
+// A NaN resolution passes it there and fails the first voxel_coord as out_of_range — the callers map
+// it after their covariance check, in the reference's order. +inf, which the reference accepts (every
+// point in voxel 0), is rejected: voxel corners c·r would be 0·inf here.
+static int check_resolution(double r) {
+  if (r <= 0.0) return fail(VGICP_E_INVALID_ARGUMENT, "voxel resolution must be positive");
+  if (std::isinf(r)) return fail(VGICP_E_INVALID_ARGUMENT, "voxel resolution must be finite");
+  return VGICP_OK;
+}
+
 int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const double* resolutions, int m,
                                vgicp_map* out) try {
   NvtxRange nvtx_("vgicp_voxelmap_build_batch");
@@ -1011,11 +1021,13 @@ int vgicp_voxelmap_build_batch(vgicp_ctx ctx, const vgicp_cloud* clouds, const d
   for (int k = 0; k < m; ++k) out[k] = nullptr;
   // GaussianVoxelMap ctor validation order (voxelmap.cpp:67-72)
   for (int k = 0; k < m; ++k) {
-    if (!(resolutions[k] > 0.0)) return fail(VGICP_E_INVALID_ARGUMENT, "voxel resolution must be positive");
+    if (int rc = check_resolution(resolutions[k])) return rc;
     if (!clouds[k] || clouds[k]->ctx != ctx) return fail(VGICP_E_INVALID_ARGUMENT, "cloud of another context");
     if (!clouds[k]->has_cov)
       return fail(VGICP_E_INVALID_ARGUMENT, "voxel map construction requires per-point covariances");
   }
+  for (int k = 0; k < m; ++k)  // NaN: the reference's voxel_coord range check fails (voxelmap.cpp:48-51)
+    if (std::isnan(resolutions[k])) return fail(VGICP_E_OUT_OF_RANGE, "point beyond the +-2^20 voxel-per-axis range limit");
   DeviceGuard g(ctx->device);
   // float32 clouds whose occupied box has a bitmap of <= kOccMaxWords records take the hand-written
   // build (build.cu); float64 clouds and sprawling boxes the sort-based one below
@@ -1292,8 +1304,9 @@ int vgicp_voxelmap_build_f64(vgicp_ctx ctx, const double* xyz, const double* cov
   if (!ctx || !out) return fail(VGICP_E_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   // GaussianVoxelMap ctor validation order (voxelmap.cpp:67-72)
-  if (!(resolution > 0.0)) return fail(VGICP_E_INVALID_ARGUMENT, "voxel resolution must be positive");
+  if (int rc = check_resolution(resolution)) return rc;
   if (!cov9 || n == 0) return fail(VGICP_E_INVALID_ARGUMENT, "voxel map construction requires per-point covariances");
+  if (std::isnan(resolution)) return fail(VGICP_E_OUT_OF_RANGE, "point beyond the +-2^20 voxel-per-axis range limit");
   if (!xyz) return fail(VGICP_E_INVALID_ARGUMENT, "null point array");
   if (n >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "cloud too large (>= 2^31 points)");
   DeviceGuard g(ctx->device);
@@ -1417,7 +1430,8 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
   if (out_downsampled) *out_downsampled = nullptr;
   if (out_cloud) *out_cloud = nullptr;
   if (m <= 0) return fail(VGICP_E_INVALID_ARGUMENT, "submap requires at least one frame");
-  if (!(map_resolution > 0.0)) return fail(VGICP_E_INVALID_ARGUMENT, "voxel resolution must be positive");
+  if (int rc = check_resolution(map_resolution)) return rc;
+  if (std::isinf(downsample_resolution)) return fail(VGICP_E_INVALID_ARGUMENT, "voxel resolution must be finite");
   size_t total = 0;
   unsigned max_n = 0;
   for (int k = 0; k < m; ++k) {
@@ -1428,6 +1442,8 @@ int vgicp_submap_build(vgicp_ctx ctx, const vgicp_cloud* frames, const double* p
     max_n = std::max<unsigned>(max_n, static_cast<unsigned>(frames[k]->n));
   }
   if (total == 0) return fail(VGICP_E_INVALID_ARGUMENT, "voxel map construction requires per-point covariances");
+  if (std::isnan(downsample_resolution) || std::isnan(map_resolution))  // voxel_downsample / map voxel_coord
+    return fail(VGICP_E_OUT_OF_RANGE, "point beyond the +-2^20 voxel-per-axis range limit");
   if (total >= (1ull << 31)) return fail(VGICP_E_INVALID_ARGUMENT, "submap too large (>= 2^31 points)");
   DeviceGuard g(ctx->device);
   cudaStream_t s = ctx->stream;

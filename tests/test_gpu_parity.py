@@ -162,6 +162,17 @@ def test_range_and_invalid(ctx):  # test_voxelmap.cpp:185-188, voxelmap.cpp:67-7
     ok, _, _ = gpu_cloud(ctx, [[0.0, 0, 0]], O.unit_covariances(1))
     with pytest.raises(ValueError):
         V.GaussianVoxelMap(ok, 0.0)
+    with pytest.raises(ValueError):
+        V.GaussianVoxelMap(ok, -1.0)
+    # NaN passes the reference's `resolution <= 0` check and fails voxel_coord's range test
+    with pytest.raises(O.OracleOutOfRange):
+        O.OracleMap([[0.0, 0, 0]], O.unit_covariances(1), float("nan"))
+    with pytest.raises(IndexError):
+        V.GaussianVoxelMap(ok, float("nan"))
+    with pytest.raises(IndexError):
+        V.GaussianVoxelMap.build_batch([ok, ok], [1.0, float("nan")])
+    with pytest.raises(ValueError):  # documented deviation: +inf (every point in voxel 0) is rejected
+        V.GaussianVoxelMap(ok, float("inf"))
     raw = V.PointCloud(np.zeros((3, 3), np.float32), None, ctx)
     with pytest.raises(ValueError):
         V.GaussianVoxelMap(raw, 1.0)
