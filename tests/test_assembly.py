@@ -416,3 +416,29 @@ def test_gpu_native_lm_cuda_graph_identical(V, monkeypatch):
     assert [(t.accepted, t.lam, t.error) for t in r1.trace] == [(t.accepted, t.lam, t.error) for t in r2.trace]
     assert r1.linearizations == r2.linearizations and r1.linearizations >= 3
     assert np.array_equal(p1, p2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("native", [True, False])
+def test_zero_factor_graph_terminates_by_step_norm(native):
+    """test_optimizer.cpp:301-320 with a matching-only graph: the only factor is a zero factor (disjoint
+    clouds, 0 inliers), so the damped system solves to a zero step (damping floor) — the LM ends by
+    step norm, not abort, and the free pose is left bit-for-bit unchanged."""
+    import paper_2109_07073_b200 as V
+    from paper_2109_07073_b200 import optimizer as LM
+
+    ctx = V.default_context(0)
+    rng = np.random.default_rng(5)
+    tm = rng.normal(size=(500, 3)).astype(np.float32)
+    sm = (rng.normal(size=(500, 3)) + [1000.0, 0, 0]).astype(np.float32)
+    cov = np.tile(np.array([1, 0, 0, 1, 0, 1], np.float32), (500, 1))
+    tgt, src = V.PointCloud(tm, cov, ctx), V.PointCloud(sm, cov, ctx)
+    g = V.FactorGraph([V.MatchingCostFactor(0, 1, src, V.GaussianVoxelMap(tgt, 1.0))], 2)
+    b = np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, 1.0, 0, 0])
+    P = np.stack([np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0.0]), b])
+    fixed = np.array([1, 0], np.uint8)
+    run = LM.optimize_native if native else LM.optimize
+    poses, rep = run(g, P, fixed=fixed)
+    assert not rep.aborted
+    assert rep.reason == "converged_step_norm"
+    assert np.array_equal(np.asarray(poses)[1], b)
