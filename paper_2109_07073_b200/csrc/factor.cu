@@ -172,7 +172,9 @@ __device__ __forceinline__ void hit_math(const float* Rf, const double* T, const
     float om[6];
     const double* Ct = map.cov64 + 9 * __float_as_int(v2.y);
     if constexpr (kF64) {
+      VG_CHECK(pos >= 0 && pos < fp->n);
       const unsigned src_i = fp->blk64[pos / kPointBlock].idx[pos % kPointBlock];
+      VG_CHECK(src_i < static_cast<unsigned>(fp->n));
       if (!omega_fp64_c9(T, fp->c64 + 9 * static_cast<size_t>(src_i), Ct, om)) return;
     } else {
       if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, Ct, om)) return;
