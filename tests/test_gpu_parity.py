@@ -875,3 +875,22 @@ def test_overlap_nonfinite_pose_and_points(ctx, monkeypatch, bad):
     monkeypatch.setenv("VGICP_OVERLAP_PERITEM", "1")  # the generic per-item kernel
     assert list(V.overlap_hits([src, src], poses, [gmap, gmap])) == want
     monkeypatch.delenv("VGICP_OVERLAP_PERITEM")
+
+
+def test_signed_zero_subnormal_and_face_coordinates(ctx):
+    """Coordinates -0.0, float32 subnormals and exact voxel faces (x = k·r) take the reference's floor
+    (voxelmap.cpp:48: floor(x / r)); the same cloud twice in one batch at two resolutions gives two
+    independent maps — exports, lookups and overlap hits equal the oracle's."""
+    tiny = np.float32(1e-40)  # subnormal in float32, exact in float64
+    pts = np.array([[-0.0, 0.0, -0.0], [tiny, -tiny, 0.0], [1.0, -1.0, 2.0], [0.5, 0.25, -0.75],
+                    [-0.5, 3.0, -2.0], [2.0, 2.0, 2.0], [-tiny, 1.0, -1.0]], np.float32)
+    pts = np.concatenate([pts, np.random.default_rng(8).uniform(-3, 3, size=(200, 3)).astype(np.float32)])
+    cloud, m, c9 = gpu_cloud(ctx, pts, O.unit_covariances(len(pts)))
+    maps = V.GaussianVoxelMap.build_batch([cloud, cloud], [1.0, 0.25])
+    for g, r in zip(maps, [1.0, 0.25]):
+        omap = O.OracleMap(m, c9, r)
+        assert_map_parity(g, omap)
+        probe = np.concatenate([m, -m, m + 0.5 * r])
+        assert np.array_equal(g.lookup(probe), omap.lookup(probe))
+        rel = np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, 0.25 * r, 0, 0.0])
+        assert V.overlap_hits(cloud, [rel], [g])[0] == O.overlap_hits(m, rel, omap)
