@@ -894,3 +894,33 @@ def test_signed_zero_subnormal_and_face_coordinates(ctx):
         assert np.array_equal(g.lookup(probe), omap.lookup(probe))
         rel = np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, 0.25 * r, 0, 0.0])
         assert V.overlap_hits(cloud, [rel], [g])[0] == O.overlap_hits(m, rel, omap)
+
+
+def test_tile_boundary_source_sizes(ctx):
+    """Source clouds of 1 .. 4,097 points around the 32-lane / 64-point tile / 512-point item
+    boundaries, together in one graph with one 20k-point factor: inliers exact, blocks within
+    tolerance, errors equal to linearize's."""
+    rng = O.Rng(97)
+    tm, tc = rng.gaussian_cloud(20000, 8.0)
+    tgt, tmm, tc9 = gpu_cloud(ctx, tm, tc)
+    gmap = V.GaussianVoxelMap(tgt, 1.0)
+    omap = O.OracleMap(tmm, tc9, 1.0)
+    sizes = [1, 2, 31, 32, 33, 63, 64, 65, 127, 129, 511, 512, 513, 4097, 20000]
+    srcs, frames = [], []
+    for n in sizes:
+        sm, sc = rng.gaussian_cloud(n, 8.0)
+        c, m, c9 = gpu_cloud(ctx, sm, sc)
+        srcs.append(c)
+        frames.append((m, c9))
+    factors = [V.MatchingCostFactor(0, k + 1, s, gmap) for k, s in enumerate(srcs)]
+    poses = np.stack([O.IDENTITY] + [rng.random_pose(0.01, 0.1) for _ in sizes])
+    for chunk in (0, 512):
+        g = V.FactorGraph(factors, len(poses), chunk=chunk)
+        raw, inl = g.linearize_raw(poses)
+        err, inl2 = g.evaluate(poses)
+        assert np.array_equal(inl, inl2) and np.array_equal(err, raw[:, 120])
+        for k, (m, c9) in enumerate(frames):
+            ref = O.linearize(m, c9, omap, poses[0], poses[k + 1])
+            assert int(inl[k]) == ref["inliers"], (sizes[k], chunk)
+            d = rel_block_error(O.unpack121(raw[k]), ref)
+            assert max(d.values()) <= H_TOL, (sizes[k], d)
