@@ -924,3 +924,26 @@ def test_tile_boundary_source_sizes(ctx):
             assert int(inl[k]) == ref["inliers"], (sizes[k], chunk)
             d = rel_block_error(O.unpack121(raw[k]), ref)
             assert max(d.values()) <= H_TOL, (sizes[k], d)
+
+
+def test_overlap_probe_sizes(ctx, monkeypatch):
+    """Overlap probes of 1 .. 4,097 points (4 points per lane, 32 maps per chunk boundaries) against
+    33 maps: exact hits on the batched, map-set and per-item paths."""
+    rng = O.Rng(98)
+    maps, omaps = [], []
+    for k in range(33):
+        tm, tc = rng.gaussian_cloud(1500, 5.0)
+        c, m, c9 = gpu_cloud(ctx, tm, tc)
+        maps.append(V.GaussianVoxelMap(c, 0.5 + 0.1 * (k % 4)))
+        omaps.append(O.OracleMap(m, c9, 0.5 + 0.1 * (k % 4)))
+    mset = V.MapSet(maps)
+    for n in (1, 3, 4, 5, 127, 128, 129, 4097):
+        sm, sc = rng.gaussian_cloud(n, 5.0)
+        probe, smm, _ = gpu_cloud(ctx, sm, sc)
+        rels = [rng.random_pose(0.05, 0.5) for _ in maps]
+        want = [O.overlap_hits(smm, r, o) for r, o in zip(rels, omaps)]
+        assert list(V.overlap_hits([probe] * len(maps), rels, maps)) == want, n
+        assert list(V.overlap_hits(probe, rels, mset)) == want, n
+        monkeypatch.setenv("VGICP_OVERLAP_PERITEM", "1")
+        assert list(V.overlap_hits([probe] * len(maps), rels, maps)) == want, n
+        monkeypatch.delenv("VGICP_OVERLAP_PERITEM")
