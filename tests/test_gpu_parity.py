@@ -947,3 +947,40 @@ def test_overlap_probe_sizes(ctx, monkeypatch):
         monkeypatch.setenv("VGICP_OVERLAP_PERITEM", "1")
         assert list(V.overlap_hits([probe] * len(maps), rels, maps)) == want, n
         monkeypatch.delenv("VGICP_OVERLAP_PERITEM")
+
+
+def test_build_path_thresholds(ctx):
+    """Clouds straddling every switch of the hand-written build on this device (B200: 227 KB of
+    opt-in shared memory): the shared-memory radix sort's point limit (24,896 / 24,897 points), the
+    shared-memory bitmap's brick limit (28,928 / 28,929 bricks: a one-brick-wide box 4·28,928 voxels
+    long) and the counting kernel's shared-memory cursor limit (57,855 / 57,856 voxels in a
+    60,000-point cloud) — one batch and singly, exports equal to the oracle."""
+    import torch
+
+    optin = torch.cuda.get_device_properties(0).shared_memory_per_block_optin
+    sort_max = (optin - 32768 - 512) // 8
+    bricks = (optin - 1024) // 8
+    cursors = (optin - 1024) // 4 - 1
+    rng = np.random.default_rng(21)
+    clouds = []
+    for n in (sort_max, sort_max + 1):
+        clouds.append(rng.uniform(-40, 40, size=(n, 3)))
+    for w in (bricks, bricks + 1):  # a line of voxels x in [0, 4w), y = z = 0, both ends occupied
+        x = np.concatenate([[0.5, 4 * w - 0.5], rng.uniform(0, 4 * w, size=3000)])
+        clouds.append(np.stack([x, np.full_like(x, 0.5), np.full_like(x, 0.5)], 1))
+    for v in (cursors, cursors + 1):  # v distinct voxel centres, then repeats up to 60,000 points
+        cells = rng.permutation(80 * 80 * 80)[:v]
+        centres = np.stack([cells % 80, (cells // 80) % 80, cells // 6400], 1) + 0.5
+        pts = np.concatenate([centres, centres[rng.integers(0, v, size=60000 - v)] + 0.1])
+        clouds.append(pts)
+    gclouds, frames = [], []
+    for pts in clouds:
+        c, m, c9 = gpu_cloud(ctx, pts, O.unit_covariances(len(pts)))
+        gclouds.append(c)
+        frames.append((m, c9))
+    batch = V.GaussianVoxelMap.build_batch(gclouds, 1.0)
+    for k, (m, c9) in enumerate(frames):
+        omap = O.OracleMap(m, c9, 1.0)
+        assert_map_parity(batch[k], omap)
+        assert_map_parity(V.GaussianVoxelMap(gclouds[k], 1.0), omap)
+    assert batch[4].size() == cursors and batch[5].size() == cursors + 1
