@@ -442,3 +442,38 @@ def test_zero_factor_graph_terminates_by_step_norm(native):
     assert not rep.aborted
     assert rep.reason == "converged_step_norm"
     assert np.array_equal(np.asarray(poses)[1], b)
+
+
+@pytest.mark.gpu
+def test_native_lm_isolated_and_disconnected_components():
+    """effective_fixed_mask (optimizer.cpp:24-43) on the native LM: a pose no factor touches and a
+    second chain without a fixed pose are anchored at their first pose; anchored poses stay bit-for-
+    bit, the rest move, and the native and Python LM agree (same trace; poses to 1e-9)."""
+    import paper_2109_07073_b200 as V
+    from paper_2109_07073_b200 import optimizer as LM
+
+    ctx = V.default_context(0)
+    rng = O.Rng(71)
+    clouds = []
+    for _ in range(5):
+        m, c = rng.gaussian_cloud(3000, 6.0)
+        m32 = np.asarray(m, np.float32)
+        c6 = np.asarray(c).reshape(-1, 9)[:, [0, 1, 2, 4, 5, 8]].astype(np.float32)
+        clouds.append(V.PointCloud(m32, c6, ctx))
+    maps = V.GaussianVoxelMap.build_batch(clouds, 1.0)
+    # chain A: 0-1 (0 fixed by the caller); chain B: 3-4 (no fixed pose); pose 2 isolated
+    factors = [V.MatchingCostFactor(0, 1, clouds[1], maps[0]), V.MatchingCostFactor(3, 4, clouds[4], maps[3])]
+    g = V.FactorGraph(factors, 5)
+    P = np.stack([rng.random_pose(0.02, 0.1) for _ in range(5)])
+    fixed = np.array([1, 0, 0, 0, 0], np.uint8)
+    pn, rn = LM.optimize_native(g, P, fixed=fixed, settings=LM.LmSettings(max_iterations=5))
+    pp, rp = LM.optimize(g, P, fixed=fixed, settings=LM.LmSettings(max_iterations=5))
+    pn, pp = np.asarray(pn), np.asarray(pp)
+    for v in (0, 2, 3):
+        assert np.array_equal(pn[v], P[v]) and np.array_equal(pp[v], P[v])
+    assert not np.array_equal(pn[1], P[1]) and not np.array_equal(pn[4], P[4])
+    # same accept / reject sequence; poses and errors equal to the solvers' rounding (1e-9, as the
+    # native-vs-Python test above)
+    assert [(t.accepted, t.lam) for t in rn.trace] == [(t.accepted, t.lam) for t in rp.trace]
+    assert np.abs(pn - pp).max() < 1e-9
+    assert abs(rn.final_error - rp.final_error) <= 1e-9 * max(1.0, rp.final_error)
