@@ -248,3 +248,33 @@ def test_replicated_clouds_maps_and_sharded_graph(ctxs):
     fb = V.FactorGraph([V.MatchingCostFactor(0, 1, c64.replicate(ctxs[1]), r1)], 2).linearize_raw(poses[:2])
     assert np.array_equal(fa[0], fb[0]) and np.array_equal(fa[1], fb[1])
     assert src is not None
+
+
+def test_sharded_replicas_float64_rare_path(ctxs):
+    """float64 clouds with rank-deficient covariances (every hit's M near singular: the fp64 LDLT
+    decides on the source's float64 covariance, read through the cloud's point index / covariance
+    arrays) replicated onto the other contexts: the sharded graph's blocks, inliers and errors are
+    bit-identical to the single graph's, whose inliers equal the oracle's."""
+    rng = np.random.default_rng(77)
+    frames, clouds = [], []
+    for _ in range(4):
+        m = rng.normal(size=(3000, 3)) * 6.0 + 1e-9  # not float32-exact
+        v = rng.normal(size=(3000, 3))
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+        c = 0.05 * v[:, :, None] * v[:, None, :]  # rank 1
+        frames.append((m, c.reshape(-1, 9)))
+        clouds.append(V.PointCloud(m, c, ctxs[0]))
+    assert all(c.is_f64() for c in clouds)
+    maps = V.GaussianVoxelMap.build_batch(clouds, [1.0] * 4)
+    links = [(0, 1), (1, 2), (2, 3), (0, 2), (1, 3)]
+    factors = [V.MatchingCostFactor(i, j, clouds[j], maps[i]) for i, j in links]
+    poses = np.stack([np.concatenate([np.eye(3).reshape(9), rng.normal(size=3) * 0.05]) for _ in range(4)])
+    full = V.FactorGraph(factors, 4)
+    ref_raw, ref_inl = full.linearize_raw(poses)
+    for k, (i, j) in enumerate(links):
+        om = O.OracleMap(*frames[i], 1.0)
+        assert int(ref_inl[k]) == O.linearize(*frames[j], om, poses[i], poses[j])["inliers"]
+    sh = V.FactorGraph.sharded_replicas(factors, 4, ctxs[:3])
+    raw, inl = sh.linearize_raw(poses)
+    assert np.array_equal(raw, ref_raw) and np.array_equal(inl, ref_inl)
+    assert np.array_equal(sh.evaluate(poses)[0], full.evaluate(poses)[0])
