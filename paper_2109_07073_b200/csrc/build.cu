@@ -495,7 +495,8 @@ __global__ void __launch_bounds__(kAccThreads, VG_ACC_MINB) fast_accumulate_kern
   __shared__ float4 sA[kAccWarps][kStage];
   __shared__ float4 sB[kAccWarps][kStage];
   __shared__ float sZ[kAccWarps][kStage];
-  __shared__ __align__(16) double stage[kAccWarps][32 * 9];  // the warp's fp64 covariances, written out coalesced
+  constexpr int kCovW = kExport ? 9 : 6;  // row-major 3×3 for export, else the 6 unique entries
+  __shared__ __align__(16) double stage[kAccWarps][32 * kCovW];  // the warp's fp64 covariances, written out coalesced
   const FastBuildJob& j = jobs[blockIdx.y];
   const unsigned V = j.V;
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -593,10 +594,13 @@ __global__ void __launch_bounds__(kAccThreads, VG_ACC_MINB) fast_accumulate_kern
     a.cyz = static_cast<float>(cov[4]);
     j.ra[v] = a;
     j.rb[v] = SlotStatsB{static_cast<float>(cov[5]), static_cast<int>(v)};
-    {
+    if constexpr (kExport) {
       const int full[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};  // row-major 3×3 from the unique entries
 #pragma unroll
       for (int q = 0; q < 9; ++q) stage[warp][9 * lane + q] = cov[full[q]];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) stage[warp][6 * lane + q] = cov[q];
     }
     if constexpr (kExport) {
       unsigned hi, lo;
@@ -609,12 +613,13 @@ __global__ void __launch_bounds__(kAccThreads, VG_ACC_MINB) fast_accumulate_kern
     }
   }
   __syncwarp();
-  // the warp's covariances leave as one contiguous, coalesced run of 9·nv doubles, 16 B per store
+  // the warp's covariances leave as one contiguous, coalesced run of kCovW·nv doubles, 16 B per store
   // (v0 is a multiple of 32, so the run starts 16-B aligned)
-  double2* __restrict__ dst = reinterpret_cast<double2*>(j.cov9 + 9 * static_cast<size_t>(v0));
+  double2* __restrict__ dst = reinterpret_cast<double2*>(j.cov9 + kCovW * static_cast<size_t>(v0));
   const double2* src2 = reinterpret_cast<const double2*>(stage[warp]);
-  for (unsigned t = lane; t < (9 * nv) / 2; t += 32) dst[t] = src2[t];
-  if ((9 * nv) % 2 && lane == 0) j.cov9[9 * static_cast<size_t>(v0) + 9 * nv - 1] = stage[warp][9 * nv - 1];
+  for (unsigned t = lane; t < (kCovW * nv) / 2; t += 32) dst[t] = src2[t];
+  if ((kCovW * nv) % 2 && lane == 0)
+    j.cov9[kCovW * static_cast<size_t>(v0) + kCovW * nv - 1] = stage[warp][kCovW * nv - 1];
 }
 
 // Hash table of a rank-numbered map (on demand): slot <- the statistics of its key's rank.

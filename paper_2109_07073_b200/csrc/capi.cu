@@ -845,7 +845,9 @@ static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const do
       cleanup();
       return fail(VGICP_E_OUT_OF_RANGE, "point beyond the +-2^20 voxel-per-axis range limit");
     }
-  // per-map voxel arrays: ra | rb | cov64 (rank order)
+  // per-map voxel arrays: ra | rb | cov64 (rank order; the 6 unique entries — float32 clouds have
+  // symmetric covariances, so the sums are symmetric bit for bit — except in export mode, whose
+  // rebuilt map hands its full 9-entry rows to the caller)
   unsigned max_v = 0, smem_v = fast_order_smem_voxels(ctx->device);
   const unsigned sort_n = std::getenv("VGICP_BUILD_SCATTER") ? 0u : fast_sort_max_points(ctx->device);
   std::vector<int> in_sort, in_smem, in_global;
@@ -854,7 +856,8 @@ static int build_fast_ordered(vgicp_ctx ctx, const vgicp_cloud* clouds, const do
     const size_t V = hv[k];
     mp->voxels = V;
     const size_t b_ra = align_up(sizeof(SlotStatsA) * V, 256), b_rb = align_up(sizeof(SlotStatsB) * V, 256);
-    mp->cold_bytes = std::max<size_t>(b_ra + b_rb + sizeof(double) * 9 * V, 256);
+    mp->cov6 = exp == nullptr;
+    mp->cold_bytes = std::max<size_t>(b_ra + b_rb + sizeof(double) * (mp->cov6 ? 6 : 9) * V, 256);
     if (const cudaError_t e = dmalloc(ctx, &mp->cold, mp->cold_bytes);
         e != cudaSuccess) {
       cleanup();
@@ -1577,7 +1580,7 @@ int vgicp_voxelmap_replicate(vgicp_map map, vgicp_ctx ctx, vgicp_map* out) try {
   m->ctx = ctx;
   m->res = map->res, m->inv_res = map->inv_res, m->voxels = map->voxels, m->total_points = map->total_points;
   for (int a = 0; a < 3; ++a) m->cmin[a] = map->cmin[a], m->cmax[a] = map->cmax[a];
-  m->num_buckets = map->num_buckets, m->shift = map->shift, m->fast = map->fast;
+  m->num_buckets = map->num_buckets, m->shift = map->shift, m->fast = map->fast, m->cov6 = map->cov6;
   auto guard = on_failure([&]() {
     dfree(ctx, m->cold);
     dfree(ctx, m->table);

@@ -41,9 +41,10 @@ __device__ __forceinline__ double relative_pose_entry(const double* Tt, const do
 // Rare path: M near singular in fp32 -> recompute M and the LDLT decision in fp64 exactly as
 // the oracle (factors.cpp:38-46, :107) and return Omega as fp32.
 __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, float sxz, float syy, float syz,
-                                        float szz, const double* Ct, float* om) {
+                                        float szz, const double* cov_tagged, int vid, float* om) {
   const double Cs[9] = {sxx, sxy, sxz, sxy, syy, syz, sxz, syz, szz};
-  double M[9], O[9];
+  double Ct[9], M[9], O[9];
+  cov_row(cov_tagged, vid, Ct);
   combined_cov_rn(T, Cs, Ct, M);
   if (!invert_covariance_rn(M, O)) return false;
   om[0] = (float)O[0];
@@ -58,8 +59,10 @@ __device__ __noinline__ bool omega_fp64(const double* T, float sxx, float sxy, f
 // The same decision for a float64 source cloud: its exact float64 covariance (all 9 entries, as the
 // oracle / reference hold it) instead of the float32 tile copy, so a near-singular M is skipped or
 // kept exactly as the reference's double LDLT decides.
-__device__ __noinline__ bool omega_fp64_c9(const double* T, const double* Cs, const double* Ct, float* om) {
-  double M[9], O[9];
+__device__ __noinline__ bool omega_fp64_c9(const double* T, const double* Cs, const double* cov_tagged, int vid,
+                                           float* om) {
+  double Ct[9], M[9], O[9];
+  cov_row(cov_tagged, vid, Ct);
   combined_cov_rn(T, Cs, Ct, M);
   if (!invert_covariance_rn(M, O)) return false;
   om[0] = (float)O[0];
@@ -170,14 +173,14 @@ __device__ __forceinline__ void hit_math(const float* Rf, const double* T, const
     o22 = a22 * inv;
   } else {
     float om[6];
-    const double* Ct = map.cov64 + 9 * __float_as_int(v2.y);
+    const int vid = __float_as_int(v2.y);
     if constexpr (kF64) {
       VG_CHECK(pos >= 0 && pos < fp->n);
       const unsigned src_i = fp->blk64[pos / kPointBlock].idx[pos % kPointBlock];
       VG_CHECK(src_i < static_cast<unsigned>(fp->n));
-      if (!omega_fp64_c9(T, fp->c64 + 9 * static_cast<size_t>(src_i), Ct, om)) return;
+      if (!omega_fp64_c9(T, fp->c64 + 9 * static_cast<size_t>(src_i), map.cov64, vid, om)) return;
     } else {
-      if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, Ct, om)) return;
+      if (!omega_fp64(T, sxx, sxy, sxz, syy, syz, szz, map.cov64, vid, om)) return;
     }
     o00 = om[0], o01 = om[1], o02 = om[2], o11 = om[3], o12 = om[4], o22 = om[5];
   }

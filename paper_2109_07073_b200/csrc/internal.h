@@ -153,7 +153,7 @@ struct FastBuildJob {
   OccWord* occ;            // the map's bitmap (words records)
   SlotStatsA* ra;          // outputs by rank: voxel-local fp32 statistics ...
   SlotStatsB* rb;          //   ... (c_zz, rank)
-  double* cov9;            //   ... and the fp64 covariance (9 entries, row-major; the near-singular path)
+  double* cov9;            //   ... and the fp64 covariance (the near-singular path: 6 unique entries; 9 row-major in export mode)
   unsigned long long* keys;  // export mode (else nullptr): packed key, count and fp64 mean by rank
   int* counts;
   double* mean64;
@@ -419,10 +419,15 @@ struct vgicp_map_s {
   // table until one is needed (ensure_table); export recomputes the key-ordered statistics from `src`
   // with the same kernels.
   bool fast = false;
+  bool cov6 = false;          // cov64 holds the 6 unique entries per voxel (hand-built: symmetric inputs)
   vgicp_cloud src = nullptr;  // the source cloud (kept alive: export / on-demand hash table)
-  vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov64, res, inv_res, shift, 0u, occ}; }
+  // device descriptors carry cov64 tagged in bit 0 when it is 6-wide (vgicp::cov_row decodes it)
+  const double* cov_dev() const {
+    return cov6 ? reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(cov64) | 1u) : cov64;
+  }
+  vgicp::MapDev dev() const { return vgicp::MapDev{tkeys, sa, sb, cov_dev(), res, inv_res, shift, 0u, occ}; }
   // rank lookups: slot statistics replaced by the rank-ordered copies (requires occ)
-  vgicp::MapDev dev_rank() const { return vgicp::MapDev{tkeys, ra, rb, cov64, res, inv_res, shift, 0u, occ}; }
+  vgicp::MapDev dev_rank() const { return vgicp::MapDev{tkeys, ra, rb, cov_dev(), res, inv_res, shift, 0u, occ}; }
 };
 
 struct vgicp_mapset_s {

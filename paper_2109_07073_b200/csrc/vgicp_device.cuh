@@ -92,13 +92,27 @@ struct MapDev {
   const unsigned long long* keys;  // capacity = kBucket * num_buckets, kEmptyKey when free
   const SlotStatsA* sa;            // per slot
   const SlotStatsB* sb;            // per slot
-  const double* cov64;             // V×9 row-major fp64 covariances by voxel id (cold)
+  const double* cov64;             // fp64 covariances by voxel id (cold): V×9 row-major, or V×6 unique
+                                   // entries (xx xy xz yy yz zz) when bit 0 is set — see cov_row
   double res;
   double inv_res;
   unsigned shift;                  // 32 - log2(num_buckets)
   unsigned pad;
   OccDev occ;                      // occupancy bitmap; factor graphs in rank mode index sa / sb by rank
 };
+
+// The fp64 covariance of voxel `vid` as 9 row-major entries from a (possibly 6-wide, tagged) array.
+__device__ __forceinline__ void cov_row(const double* tagged, int vid, double* C) {
+  const uintptr_t b = reinterpret_cast<uintptr_t>(tagged);
+  if (b & 1u) {
+    const double* c = reinterpret_cast<const double*>(b & ~uintptr_t(1)) + 6 * static_cast<size_t>(vid);
+    C[0] = c[0], C[1] = c[1], C[2] = c[2], C[3] = c[1], C[4] = c[3], C[5] = c[4], C[6] = c[2], C[7] = c[4], C[8] = c[5];
+  } else {
+    const double* c = tagged + 9 * static_cast<size_t>(vid);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) C[e] = c[e];
+  }
+}
 
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256).
 __device__ __forceinline__ void ldg256(const void* p, unsigned& r0, unsigned& r1, unsigned& r2, unsigned& r3,
